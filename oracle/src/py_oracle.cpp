@@ -1,0 +1,251 @@
+// TEST INFRASTRUCTURE ONLY: Python binding of the CPU oracle for tests/ and
+// bench.py's CPU legs. Not part of the product.
+#include <pybind11/functional.h>
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <chrono>
+
+#include "slra_oracle.hpp"
+
+namespace py = pybind11;
+using namespace slra_oracle;
+
+using FArray = py::array_t<double, py::array::f_style | py::array::forcecast>;
+
+static Matrix from_np(const FArray& a) {
+  if (a.ndim() == 1) {
+    Matrix M(a.shape(0), 1);
+    std::copy(a.data(), a.data() + a.shape(0), M.v.begin());
+    return M;
+  }
+  if (a.ndim() != 2) throw std::invalid_argument("expected a 1-D or 2-D array");
+  Matrix M(a.shape(0), a.shape(1));
+  std::copy(a.data(), a.data() + M.size(), M.v.begin());
+  return M;
+}
+static FArray to_np(const Matrix& M) {
+  FArray a({M.rows(), M.cols()});
+  std::copy(M.v.begin(), M.v.end(), a.mutable_data());
+  return a;
+}
+static py::array_t<double> vec_np(const Vector& v) {
+  py::array_t<double> a(static_cast<py::ssize_t>(v.size()));
+  std::copy(v.begin(), v.end(), a.mutable_data());
+  return a;
+}
+static Vector np_vec(const FArray& a) { return Vector(a.data(), a.data() + a.size()); }
+struct PyOp { OpPtr p; };
+static IndexSet mkset(const std::vector<Index>& v, Index bound) { return IndexSet(v, bound); }
+
+static py::dict cur_dict(const CurDecomposition& c) {
+  py::dict d;
+  d["I"] = c.row_set.indices();
+  d["J"] = c.col_set.indices();
+  d["nucleus"] = to_np(c.nucleus);
+  d["r"] = c.r;
+  return d;
+}
+
+PYBIND11_MODULE(_oracle, m) {
+  m.doc() = "CPU oracle (restatement of the reference slra hot path) -- test infrastructure only";
+  auto base = py::register_exception<std::runtime_error>(m, "OracleRuntimeError");
+  py::register_exception<RangeFailure>(m, "RangeFailure", base.ptr());
+  py::register_exception<SketchRankFailure>(m, "SketchRankFailure", base.ptr());
+  py::register_exception<PremultRankFailure>(m, "PremultRankFailure", base.ptr());
+  py::register_exception<SelectionFailure>(m, "SelectionFailure", base.ptr());
+  py::register_exception<GeneratorRankFailure>(m, "GeneratorRankFailure", base.ptr());
+  py::register_exception<EmptySample>(m, "EmptySample", base.ptr());
+
+  py::class_<Rng>(m, "Rng")
+      .def(py::init<std::uint64_t>())
+      .def("next_u64", &Rng::next_u64)
+      .def("uniform", &Rng::uniform)
+      .def("gaussian", &Rng::gaussian)
+      .def("uniform_index", &Rng::uniform_index)
+      .def("sign", &Rng::sign)
+      .def("permutation", &Rng::permutation)
+      .def("distinct_indices", &Rng::distinct_indices)
+      .def("gaussian_matrix", [](Rng& r, Index a, Index b) { return to_np(r.gaussian_matrix(a, b)); })
+      .def("gaussian_vector", [](Rng& r, Index n) { return vec_np(r.gaussian_vector(n)); })
+      .def("child", &Rng::child)
+      .def_static("derive_seed", &Rng::derive_seed);
+
+  // ---- linalg
+  m.def("matmul", [](const FArray& A, const FArray& B) { return to_np(matmul(from_np(A), from_np(B))); });
+  m.def("thin_qr", [](const FArray& A) {
+    auto [Q, R] = thin_qr(from_np(A));
+    return py::make_tuple(to_np(Q), to_np(R));
+  });
+  m.def("svd", [](const FArray& A) {
+    Svd f = svd(from_np(A));
+    return py::make_tuple(to_np(f.S), vec_np(f.sigma), to_np(f.T));
+  });
+  m.def("pseudo_inverse", [](const FArray& A, double tol) { return to_np(pseudo_inverse(from_np(A), tol)); },
+        py::arg("A"), py::arg("rank_tol") = 1e-10);
+  m.def("numerical_rank", [](const FArray& A, double tol, bool relative) {
+    return numerical_rank(from_np(A), tol, relative ? RankMode::Relative : RankMode::Absolute);
+  }, py::arg("A"), py::arg("tol"), py::arg("relative") = false);
+  m.def("frobenius_norm", [](const FArray& A) { return frobenius_norm(from_np(A)); });
+  m.def("spectral_norm", [](const FArray& A) { return spectral_norm(from_np(A)); });
+  m.def("determinant_abs", [](const FArray& A) { return determinant_abs(from_np(A)); });
+  m.def("colpiv_qr", [](const FArray& A, double threshold) {
+    ColPivQR q(from_np(A));
+    q.threshold = threshold;
+    py::dict d;
+    d["perm"] = q.perm;
+    d["rank"] = q.rank();
+    d["nonzero_pivots"] = q.nonzero_pivots;
+    d["qr"] = to_np(q.qr);
+    return d;
+  }, py::arg("A"), py::arg("threshold") = -1.0);
+  m.def("colpiv_solve", [](const FArray& A, const FArray& B, double threshold) {
+    ColPivQR q(from_np(A));
+    q.threshold = threshold;
+    return to_np(q.solve(from_np(B)));
+  }, py::arg("A"), py::arg("B"), py::arg("threshold") = -1.0);
+
+  // ---- cur
+  m.def("t_factor", &t_factor);
+  m.def("maxvol_rows", [](const FArray& A, double h, Index max_swaps) {
+    return maxvol_rows(from_np(A), h, max_swaps).indices();
+  }, py::arg("A"), py::arg("h") = 1.1, py::arg("max_swaps") = 0);
+  m.def("select_rows_spanning", [](const FArray& A, Index count, double h) {
+    return select_rows_spanning(from_np(A), count, h).indices();
+  }, py::arg("A"), py::arg("count"), py::arg("h") = 1.1);
+  m.def("primitive_cur", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J, Index r) {
+    Matrix M = from_np(A);
+    DenseOracle o(M);
+    py::dict d = cur_dict(primitive_cur(o, mkset(I, M.rows()), mkset(J, M.cols()), r));
+    d["accesses"] = o.accesses();
+    return d;
+  });
+  m.def("cross_approx", [](const FArray& A, Index r, Index k, Index l, const std::vector<Index>& init_rows,
+                           int loops, double h, std::optional<double> stop_tol, Rng& rng) {
+    Matrix M = from_np(A);
+    DenseOracle o(M);
+    IndexSet init = init_rows.empty() ? IndexSet() : mkset(init_rows, M.rows());
+    auto [c, trace] = cross_approx(o, r, k, l, std::move(init), loops, h, stop_tol, rng);
+    py::dict d = cur_dict(c);
+    py::list steps;
+    for (auto& s : trace.steps) {
+      py::dict sd;
+      sd["horizontal"] = s.horizontal;
+      sd["rows"] = s.rows;
+      sd["cols"] = s.cols;
+      sd["volume_proxy"] = s.volume_proxy;
+      sd["error_estimate"] = s.error_estimate;
+      steps.append(sd);
+    }
+    d["trace"] = steps;
+    d["accesses"] = o.accesses();
+    return d;
+  }, py::arg("A"), py::arg("r"), py::arg("k"), py::arg("l"), py::arg("init_rows"), py::arg("loops"),
+     py::arg("h"), py::arg("stop_tol"), py::arg("rng"));
+  m.def("cur_reconstruct", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
+                              const FArray& U) {
+    Matrix M = from_np(A);
+    CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), from_np(U), 0};
+    return to_np(cur_reconstruct(M, c));
+  });
+  m.def("cur_evaluate", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
+                           const FArray& U, const std::string& norm) {
+    Matrix M = from_np(A);
+    CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), from_np(U), 0};
+    NormKind k = norm == "spectral" ? NormKind::Spectral : norm == "chebyshev" ? NormKind::Chebyshev : NormKind::Frobenius;
+    return cur_evaluate(M, c, k);
+  }, py::arg("A"), py::arg("I"), py::arg("J"), py::arg("U"), py::arg("norm") = "frobenius");
+
+  // ---- sketch operators
+  py::class_<PyOp>(m, "SketchOperator")
+      .def("rows", [](const PyOp& o) { return o.p->rows(); })
+      .def("cols", [](const PyOp& o) { return o.p->cols(); })
+      .def("kind", [](const PyOp& o) { return o.p->kind(); })
+      .def("apply", [](const PyOp& o, const FArray& M) { return to_np(o.p->apply(from_np(M))); })
+      .def("apply_transpose", [](const PyOp& o, const FArray& M) { return to_np(o.p->apply_transpose(from_np(M))); });
+  m.def("make_permutation", [](std::vector<Index> s) { return PyOp{make_permutation(std::move(s))}; });
+  m.def("make_sign_diagonal", [](const FArray& d) { return PyOp{make_sign_diagonal(np_vec(d))}; });
+  m.def("make_abridged_hadamard", [](Index n, int d) { return PyOp{make_abridged_hadamard(n, d)}; });
+  m.def("make_sparse_circulant", [](Index n, double f, std::vector<std::pair<Index, double>> nz) {
+    return PyOp{make_sparse_circulant(n, f, std::move(nz))};
+  });
+  m.def("make_gaussian", [](const FArray& G) { return PyOp{make_gaussian(from_np(G))}; });
+  m.def("make_sub_identity", [](const std::vector<Index>& sel, Index total) {
+    return PyOp{make_sub_identity(mkset(sel, total), total)};
+  });
+  m.def("make_product", [](const std::vector<PyOp>& ops) {
+    std::vector<OpPtr> v;
+    for (auto& o : ops) v.push_back(o.p);
+    return PyOp{make_product(std::move(v))};
+  });
+  m.def("take_columns", [](const PyOp& op, const std::vector<Index>& cols) {
+    return PyOp{take_columns(op.p, mkset(cols, op.p->cols()))};
+  });
+  m.def("take_columns_random", [](const PyOp& op, Index l, Rng& rng) {
+    return PyOp{take_columns(op.p, l, ColumnMode::Random, rng)};
+  });
+  m.def("gen_permutation", [](Index n, Rng& r) { return PyOp{gen_permutation(n, r)}; });
+  m.def("gen_sign_diagonal", [](Index n, Rng& r) { return PyOp{gen_sign_diagonal(n, r)}; });
+  m.def("gen_sparse_circulant", [](Index n, Index s, Rng& r) { return PyOp{gen_sparse_circulant(n, s, r)}; });
+  m.def("gen_gaussian", [](Index a, Index b, Rng& r) { return PyOp{gen_gaussian(a, b, r)}; });
+  m.def("gen_aph", [](Index n, int d, Rng& r) { return PyOp{gen_aph(n, d, r)}; });
+  m.def("gen_asph", [](Index n, int d, Rng& r) { return PyOp{gen_asph(n, d, r)}; });
+  m.def("apply", [](const PyOp& op, const FArray& M, const std::string& side) {
+    return to_np(apply(*op.p, from_np(M), side == "right" ? Side::Right : Side::Left));
+  });
+  m.def("materialize", [](const PyOp& op) { return to_np(materialize(*op.p)); });
+  m.def("reset_op_counter", &reset_op_counter);
+  m.def("op_counter", []() { return py::make_tuple(op_counter().adds, op_counter().muls); });
+
+  // ---- lra
+  m.def("range_finder", [](const FArray& M, const PyOp& H, Index r, bool truncated) {
+    LowRankFactors f = range_finder(from_np(M), *H.p, r, truncated ? RangeVariant::TruncatedRankR : RangeVariant::BasisQr);
+    return py::make_tuple(to_np(f.U), to_np(f.V));
+  }, py::arg("M"), py::arg("H"), py::arg("r"), py::arg("truncated") = false);
+  m.def("two_stage_truncate", [](const FArray& U, const FArray& V, Index r) {
+    LowRankFactors f{from_np(U), from_np(V), 0};
+    LowRankFactors g = two_stage_truncate(f, r);
+    return py::make_tuple(to_np(g.U), to_np(g.V));
+  });
+  m.def("posterior_error_estimate", [](const FArray& M, const FArray& U, const FArray& V, Index q, Index s, Rng& rng) {
+    Matrix A = from_np(M);
+    DenseOracle o(A);
+    LowRankFactors f{from_np(U), from_np(V), 0};
+    LraErrorEstimate e = posterior_error_estimate(o, f, q, s, rng);
+    return py::make_tuple(e.estimate_frobenius, e.ci_lo, e.ci_hi, e.has_interval);
+  });
+
+  // ---- lsr
+  m.def("sketch_solve", [](const FArray& A, const FArray& b, const PyOp& F, bool with_true) {
+    LsrProblem p{from_np(A), np_vec(b)};
+    LsrReport r = sketch_solve(p, *F.p, with_true);
+    py::dict d;
+    d["x_hat"] = vec_np(r.x_hat);
+    d["sketched_residual"] = r.sketched_residual;
+    d["true_residual"] = r.true_residual;
+    d["ratio"] = r.ratio;
+    d["k"] = r.k;
+    return d;
+  }, py::arg("A"), py::arg("b"), py::arg("F"), py::arg("with_true_residual") = false);
+  m.def("solve_exact", [](const FArray& A, const FArray& b) {
+    return vec_np(solve_exact(LsrProblem{from_np(A), np_vec(b)}));
+  });
+  m.def("residual_norm", [](const FArray& A, const FArray& b, const FArray& x) {
+    return residual_norm(LsrProblem{from_np(A), np_vec(b)}, np_vec(x));
+  });
+  m.def("residual_ratio", [](const FArray& A, const FArray& b, const FArray& x) {
+    return residual_ratio(LsrProblem{from_np(A), np_vec(b)}, np_vec(x));
+  });
+
+  // ---- testgen
+  m.def("random_orthonormal", [](Index r, Index c, Rng& rng) { return to_np(random_orthonormal(r, c, rng)); });
+  m.def("gen_svd_profile", [](Index n, Index r, Rng& rng) { return to_np(gen_svd_profile(n, r, rng)); });
+  m.def("gen_factor_gaussian", [](Index mm, Index n, Index r, double noise, Rng& rng) {
+    return to_np(gen_factor_gaussian(mm, n, r, noise, rng));
+  });
+  m.def("gen_lsr_gaussian", [](Index mm, Index n, double noise, Rng& rng) {
+    LsrProblem p = gen_lsr_gaussian(mm, n, noise, rng);
+    return py::make_tuple(to_np(p.A), vec_np(p.b));
+  });
+}

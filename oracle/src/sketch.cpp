@@ -1,0 +1,341 @@
+// TEST INFRASTRUCTURE ONLY (see slra_oracle.hpp). Restates the in-scope
+// structured operators of /root/reference/proj/src/sketch.cpp, literally:
+// composites transform every row and only then keep the requested ones
+// (sketch.cpp:520-529, 558-567), which is what the CPU baseline times.
+#include <algorithm>
+#include <cmath>
+
+#include "slra_oracle.hpp"
+
+namespace slra_oracle {
+
+OpCount& op_counter() {  // sketch.cpp:11-14
+  thread_local OpCount counter;
+  return counter;
+}
+
+namespace {
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+// sketch.cpp:43-69
+class PermutationOp final : public SketchOperator {
+ public:
+  explicit PermutationOp(std::vector<Index> sigma) : sigma_(std::move(sigma)) {
+    IndexSet check(sigma_, static_cast<Index>(sigma_.size()));
+  }
+  Index rows() const override { return static_cast<Index>(sigma_.size()); }
+  Index cols() const override { return rows(); }
+  std::string kind() const override { return "permutation"; }
+  Matrix apply(const Matrix& M) const override {
+    require(M.rows() == cols(), "permutation apply: dims");
+    Matrix out(rows(), M.cols());
+    for (Index j = 0; j < M.cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) out(i, j) = M(sigma_[static_cast<size_t>(i)], j);
+    return out;
+  }
+  Matrix apply_transpose(const Matrix& M) const override {
+    require(M.rows() == rows(), "permutation apply: dims");
+    Matrix out(cols(), M.cols());
+    for (Index j = 0; j < M.cols(); ++j)
+      for (Index i = 0; i < rows(); ++i) out(sigma_[static_cast<size_t>(i)], j) = M(i, j);
+    return out;
+  }
+
+ private:
+  std::vector<Index> sigma_;
+};
+
+// sketch.cpp:73-94
+class SignDiagonalOp final : public SketchOperator {
+ public:
+  explicit SignDiagonalOp(Vector d) : d_(std::move(d)) {
+    for (double x : d_) require(std::abs(x) > 1e-12, "sign diagonal: entry too close to 0");
+  }
+  Index rows() const override { return static_cast<Index>(d_.size()); }
+  Index cols() const override { return rows(); }
+  std::string kind() const override { return "sign_diagonal"; }
+  Matrix apply(const Matrix& M) const override {
+    require(M.rows() == rows(), "diagonal apply: dims");
+    op_counter().muls += static_cast<unsigned long long>(M.size());
+    Matrix out(M.rows(), M.cols());
+    for (Index j = 0; j < M.cols(); ++j)
+      for (Index i = 0; i < M.rows(); ++i) out(i, j) = d_[static_cast<size_t>(i)] * M(i, j);
+    return out;
+  }
+  Matrix apply_transpose(const Matrix& M) const override { return apply(M); }
+
+ private:
+  Vector d_;
+};
+
+// sketch.cpp:98-107: rows [r0, r0+len) of X, recursion depth `depth`.
+void ah_recurse(Matrix& X, Index r0, Index len, int depth) {
+  if (depth == 0) return;
+  op_counter().adds += static_cast<unsigned long long>(len * X.cols());
+  const Index s = len / 2;
+  for (Index j = 0; j < X.cols(); ++j) {
+    double* x = X.col(j) + r0;
+    for (Index i = 0; i < s; ++i) {
+      const double a = x[i];
+      x[i] = a + x[i + s];      // X.topRows(s) += X.bottomRows(s)
+      x[i + s] = a - x[i + s];  // X.bottomRows(s) = a - X.bottomRows(s)
+    }
+  }
+  ah_recurse(X, r0, s, depth - 1);
+  ah_recurse(X, r0 + s, s, depth - 1);
+}
+
+// sketch.cpp:109-133
+class AbridgedHadamardOp final : public SketchOperator {
+ public:
+  AbridgedHadamardOp(Index n, int d) : n_(n), d_(d) {
+    require(d >= 1, "abridged hadamard: depth >= 1");
+    require(n % (Index(1) << d) == 0, "abridged hadamard: 2^d must divide n");
+  }
+  Index rows() const override { return n_; }
+  Index cols() const override { return n_; }
+  std::string kind() const override { return "abridged_hadamard"; }
+  Matrix apply(const Matrix& M) const override {
+    require(M.rows() == n_, "AH apply: dims");
+    Matrix X = M;
+    ah_recurse(X, 0, n_, d_);
+    return X;
+  }
+  Matrix apply_transpose(const Matrix& M) const override { return apply(M); }
+
+ private:
+  Index n_;
+  int d_;
+};
+
+// sketch.cpp:215-282
+class SparseCirculantOp final : public SketchOperator {
+ public:
+  SparseCirculantOp(Index n, double f, std::vector<std::pair<Index, double>> nz)
+      : n_(n), f_(f), nz_(std::move(nz)) {
+    require(!nz_.empty() && static_cast<Index>(nz_.size()) <= n, "sparse circulant: 1 <= s <= n");
+    for (auto& [k, v] : nz_) {
+      require(k >= 0 && k < n, "sparse circulant: position out of range");
+      require(v != 0.0, "sparse circulant: zero value");
+    }
+    all_unit_ = std::abs(std::abs(f_) - 1.0) < 1e-15 &&
+                std::all_of(nz_.begin(), nz_.end(), [](const auto& p) { return std::abs(p.second) == 1.0; });
+  }
+  Index rows() const override { return n_; }
+  Index cols() const override { return n_; }
+  std::string kind() const override { return "sparse_circulant"; }
+  void count(const Matrix& M) const {
+    const auto s = static_cast<unsigned long long>(nz_.size());
+    const auto sz = static_cast<unsigned long long>(M.size());
+    if (all_unit_) {
+      op_counter().adds += s * sz;
+    } else {
+      op_counter().muls += s * sz;
+      op_counter().adds += (s - 1) * sz;
+    }
+  }
+  Matrix apply(const Matrix& M) const override {
+    require(M.rows() == n_, "sparse circulant apply: dims");
+    count(M);
+    Matrix out(n_, M.cols());
+    for (const auto& [k, v] : nz_) {
+      const double vf = v * f_;
+      for (Index j = 0; j < M.cols(); ++j) {
+        double* o = out.col(j);
+        const double* x = M.col(j);
+        if (k > 0)
+          for (Index i = 0; i < n_ - k; ++i) o[k + i] += v * x[i];   // bottomRows(n-k) += v*topRows
+        for (Index i = 0; i < k; ++i) o[i] += vf * x[n_ - k + i];  // topRows(k) += (v f) bottomRows(k)
+        if (k == 0)
+          for (Index i = 0; i < n_; ++i) o[i] += v * x[i];
+      }
+    }
+    return out;
+  }
+  Matrix apply_transpose(const Matrix& M) const override {
+    require(M.rows() == n_, "sparse circulant apply: dims");
+    count(M);
+    Matrix out(n_, M.cols());
+    for (const auto& [k, v] : nz_) {
+      const double vf = v * f_;
+      for (Index j = 0; j < M.cols(); ++j) {
+        double* o = out.col(j);
+        const double* x = M.col(j);
+        if (k > 0)
+          for (Index i = 0; i < n_ - k; ++i) o[i] += v * x[k + i];  // topRows(n-k) += v*bottomRows
+        for (Index i = 0; i < k; ++i) o[n_ - k + i] += vf * x[i];  // bottomRows(k) += (v f) topRows(k)
+        if (k == 0)
+          for (Index i = 0; i < n_; ++i) o[i] += v * x[i];
+      }
+    }
+    return out;
+  }
+
+ private:
+  Index n_;
+  double f_;
+  std::vector<std::pair<Index, double>> nz_;
+  bool all_unit_ = false;
+};
+
+// sketch.cpp:387-413
+class GaussianOp final : public SketchOperator {
+ public:
+  explicit GaussianOp(Matrix G) : G_(std::move(G)) {}
+  Index rows() const override { return G_.rows(); }
+  Index cols() const override { return G_.cols(); }
+  std::string kind() const override { return "gaussian"; }
+  Matrix apply(const Matrix& M) const override {
+    require(M.rows() == G_.cols(), "gaussian apply: dims");
+    return matmul(G_, M);
+  }
+  Matrix apply_transpose(const Matrix& M) const override {
+    require(M.rows() == G_.rows(), "gaussian apply: dims");
+    return matmul_tn(G_, M);
+  }
+
+ private:
+  Matrix G_;
+};
+
+// sketch.cpp:417-442
+class SubIdentityOp final : public SketchOperator {
+ public:
+  SubIdentityOp(IndexSet sel, Index total) : sel_(std::move(sel)), total_(total) {
+    require(sel_.bound() == total, "sub-identity: index bound mismatch");
+  }
+  Index rows() const override { return sel_.size(); }
+  Index cols() const override { return total_; }
+  std::string kind() const override { return "sub_identity"; }
+  Matrix apply(const Matrix& M) const override {
+    require(M.rows() == total_, "sub-identity apply: dims");
+    return select_rows(M, sel_);
+  }
+  Matrix apply_transpose(const Matrix& M) const override {
+    require(M.rows() == sel_.size(), "sub-identity apply: dims");
+    Matrix out(total_, M.cols());
+    for (Index j = 0; j < M.cols(); ++j)
+      for (Index t = 0; t < sel_.size(); ++t) out(sel_[t], j) = M(t, j);
+    return out;
+  }
+
+ private:
+  IndexSet sel_;
+  Index total_;
+};
+
+// sketch.cpp:502-543
+class ProductOp final : public SketchOperator {
+ public:
+  explicit ProductOp(std::vector<OpPtr> ops) : ops_(std::move(ops)) {
+    require(!ops_.empty(), "product: empty");
+    for (size_t i = 0; i + 1 < ops_.size(); ++i)
+      require(ops_[i]->cols() == ops_[i + 1]->rows(), "product: dimension mismatch");
+  }
+  Index rows() const override { return ops_.front()->rows(); }
+  Index cols() const override { return ops_.back()->cols(); }
+  std::string kind() const override { return "product"; }
+  Matrix apply(const Matrix& M) const override {
+    Matrix out = M;
+    for (size_t i = ops_.size(); i-- > 0;) out = ops_[i]->apply(out);
+    return out;
+  }
+  Matrix apply_transpose(const Matrix& M) const override {
+    Matrix out = M;
+    for (auto& op : ops_) out = op->apply_transpose(out);
+    return out;
+  }
+
+ private:
+  std::vector<OpPtr> ops_;
+};
+
+// sketch.cpp:545-583
+class ColumnSliceOp final : public SketchOperator {
+ public:
+  ColumnSliceOp(OpPtr inner, IndexSet columns) : inner_(std::move(inner)), cols_(std::move(columns)) {
+    require(cols_.bound() == inner_->cols(), "column slice: bound mismatch");
+  }
+  Index rows() const override { return inner_->rows(); }
+  Index cols() const override { return cols_.size(); }
+  std::string kind() const override { return "column_slice"; }
+  Matrix apply(const Matrix& M) const override {
+    require(M.rows() == cols_.size(), "column slice apply: dims");
+    Matrix full(inner_->cols(), M.cols());
+    for (Index j = 0; j < M.cols(); ++j)
+      for (Index t = 0; t < cols_.size(); ++t) full(cols_[t], j) = M(t, j);
+    return inner_->apply(full);
+  }
+  Matrix apply_transpose(const Matrix& M) const override {
+    Matrix full = inner_->apply_transpose(M);
+    return select_rows(full, cols_);
+  }
+
+ private:
+  OpPtr inner_;
+  IndexSet cols_;
+};
+
+}  // namespace
+
+// sketch.cpp:589-675
+OpPtr make_permutation(std::vector<Index> sigma) { return std::make_shared<PermutationOp>(std::move(sigma)); }
+OpPtr make_sign_diagonal(Vector d) { return std::make_shared<SignDiagonalOp>(std::move(d)); }
+OpPtr make_abridged_hadamard(Index n, int d) { return std::make_shared<AbridgedHadamardOp>(n, d); }
+OpPtr make_sparse_circulant(Index n, double f, std::vector<std::pair<Index, double>> nz) {
+  return std::make_shared<SparseCirculantOp>(n, f, std::move(nz));
+}
+OpPtr make_gaussian(Matrix G) { return std::make_shared<GaussianOp>(std::move(G)); }
+OpPtr make_sub_identity(IndexSet selected, Index total) {
+  return std::make_shared<SubIdentityOp>(std::move(selected), total);
+}
+OpPtr make_product(std::vector<OpPtr> ops) { return std::make_shared<ProductOp>(std::move(ops)); }
+OpPtr take_columns(OpPtr op, IndexSet columns) {
+  return std::make_shared<ColumnSliceOp>(std::move(op), std::move(columns));
+}
+OpPtr take_columns(OpPtr op, Index l, ColumnMode mode, Rng& rng) {
+  require(l >= 1 && l <= op->cols(), "take_columns: l out of range");
+  std::vector<Index> cols;
+  if (mode == ColumnMode::Leftmost) {
+    for (Index i = 0; i < l; ++i) cols.push_back(i);
+  } else {
+    cols = rng.distinct_indices(l, op->cols());
+  }
+  const Index bound = op->cols();
+  return take_columns(std::move(op), IndexSet(std::move(cols), bound));
+}
+OpPtr gen_permutation(Index n, Rng& rng) { return make_permutation(rng.permutation(n)); }
+OpPtr gen_sign_diagonal(Index n, Rng& rng) {
+  Vector d(static_cast<size_t>(n));
+  for (Index i = 0; i < n; ++i) d[static_cast<size_t>(i)] = rng.sign();
+  return make_sign_diagonal(std::move(d));
+}
+OpPtr gen_sparse_circulant(Index n, Index s, Rng& rng) {
+  std::vector<std::pair<Index, double>> nz;
+  for (Index k : rng.distinct_indices(s, n)) nz.emplace_back(k, static_cast<double>(rng.sign()));
+  const double f = static_cast<double>(rng.sign());
+  return make_sparse_circulant(n, f, std::move(nz));
+}
+OpPtr gen_gaussian(Index rows, Index cols, Rng& rng) { return make_gaussian(rng.gaussian_matrix(rows, cols)); }
+OpPtr gen_aph(Index n, int d, Rng& rng) {
+  return make_product({gen_permutation(n, rng), make_abridged_hadamard(n, d)});
+}
+OpPtr gen_asph(Index n, int d, Rng& rng) {
+  OpPtr diag = gen_sign_diagonal(n, rng);
+  return make_product({gen_permutation(n, rng), std::move(diag), make_abridged_hadamard(n, d)});
+}
+
+// sketch.cpp:679-688
+Matrix apply(const SketchOperator& op, const Matrix& M, Side side) {
+  if (side == Side::Left) return op.apply(M);
+  return op.apply_transpose(M.transpose()).transpose();
+}
+Matrix materialize(const SketchOperator& op, Index cap) {
+  require(op.rows() <= cap && op.cols() <= cap, "materialize: cap exceeded");
+  return op.apply(Matrix::identity(op.cols(), op.cols()));
+}
+
+}  // namespace slra_oracle

@@ -1,0 +1,453 @@
+"""Pin the CPU oracle (oracle/, test infrastructure) before trusting it.
+
+Every known-answer test the reference holds for the hot path
+is restated here against the oracle, plus the C++ standard's mt19937_64 value
+and LAPACK (scipy) cross-checks. Reference citations are
+/root/reference/proj/tests/<file>:<line>.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+
+# ---------------------------------------------------------------- Rng
+def test_mt19937_64_standard_value(oracle):
+    # [rand.predef]: the 10000th draw of a default-seeded mt19937_64.
+    r = oracle.Rng(5489)
+    for _ in range(9999):
+        r.next_u64()
+    assert r.next_u64() == 9981545732273789042
+
+
+def test_rng_determinism(oracle):  # test_linalg.cpp:243-251
+    a, b = oracle.Rng(42), oracle.Rng(42)
+    assert [a.gaussian() for _ in range(100)] == [b.gaussian() for _ in range(100)]
+    assert np.array_equal(oracle.Rng(7).gaussian_matrix(4, 4), oracle.Rng(7).gaussian_matrix(4, 4))
+    assert oracle.Rng(9).permutation(10) == oracle.Rng(9).permutation(10)
+
+
+def test_rng_formulas(oracle):
+    # rng.hpp:21-23: uniform = (u64 >> 11) * 2^-53; rng.cpp:60-66 splitmix.
+    r1, r2 = oracle.Rng(3), oracle.Rng(3)
+    u = r1.uniform()
+    assert u == (r2.next_u64() >> 11) * 2.0**-53
+    z = (0 + 0x9E3779B97F4A7C15 * 1) % 2**64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) % 2**64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) % 2**64
+    assert oracle.Rng.derive_seed(0, 0) == z ^ (z >> 31)
+    # gaussian: Box-Muller cos branch (rng.cpp:8-14)
+    r1, r2 = oracle.Rng(11), oracle.Rng(11)
+    g = r1.gaussian()
+    u1 = r2.uniform()
+    u2 = r2.uniform()
+    assert g == math.sqrt(-2.0 * math.log(u1)) * math.cos(2.0 * math.pi * u2)
+    # distinct_indices: partial Fisher-Yates, distinct and in range
+    d = oracle.Rng(5).distinct_indices(64, 100)
+    assert len(set(d)) == 64 and min(d) >= 0 and max(d) < 100
+    p = oracle.Rng(5).permutation(50)
+    assert sorted(p) == list(range(50))
+
+
+# ---------------------------------------------------------------- QR / SVD
+def test_thin_qr_known_answer(oracle):  # test_linalg.cpp:45-52
+    Q, R = oracle.thin_qr(np.array([[3.0], [4.0]]))
+    assert Q[0, 0] == pytest.approx(0.6) and Q[1, 0] == pytest.approx(0.8)
+    assert R[0, 0] == pytest.approx(5.0)
+
+
+def test_thin_qr_invariants(oracle):  # test_linalg.cpp:53-68
+    B = oracle.Rng(7).gaussian_matrix(8, 3)
+    Q, R = oracle.thin_qr(B)
+    assert np.linalg.norm(Q.T @ Q - np.eye(3)) <= 1e-13
+    assert np.linalg.norm(Q @ R - B) <= 1e-12 * np.linalg.norm(B)
+    assert (np.diag(R) >= 0).all()
+    with pytest.raises(ValueError):
+        oracle.thin_qr(np.zeros((2, 3)))
+    # agrees with LAPACK up to the sign convention
+    Qs, Rs = np.linalg.qr(B)
+    s = np.sign(np.diag(Rs))
+    assert np.allclose(Q, Qs * s, atol=1e-13)
+
+
+def test_svd_examples(oracle):  # test_linalg.cpp:70-98
+    S, sig, T = oracle.svd(np.diag([3.0, 1.0]))
+    assert sig[0] == pytest.approx(3) and sig[1] == pytest.approx(1)
+    assert np.linalg.norm(np.abs(S) - np.eye(2)) < 1e-12
+    rng = oracle.Rng(3)
+    u, v = rng.gaussian_vector(6), rng.gaussian_vector(4)
+    S, sig, T = oracle.svd(np.outer(u, v))
+    assert sig[0] == pytest.approx(np.linalg.norm(u) * np.linalg.norm(v))
+    assert (sig[1:] <= 1e-13 * sig[0]).all()
+    A = rng.gaussian_matrix(6, 4)
+    S, sig, T = oracle.svd(A)
+    lam = np.linalg.eigvalsh(A.T @ A)[::-1]
+    assert np.allclose(sig, np.sqrt(lam), rtol=1e-10)
+    assert np.linalg.norm(S @ np.diag(sig) @ T.T - A) <= 1e-12 * np.linalg.norm(A) * 4
+    assert np.linalg.norm(S.T @ S - np.eye(4)) <= 4e-12
+    assert np.linalg.norm(T.T @ T - np.eye(4)) <= 4e-12
+
+
+def test_svd_sign_convention(oracle):  # test_linalg.cpp:100-109
+    S, sig, T = oracle.svd(oracle.Rng(19).gaussian_matrix(7, 5))
+    for j in range(S.shape[1]):
+        assert S[np.argmax(np.abs(S[:, j])), j] >= 0
+
+
+@pytest.mark.parametrize("shape", [(50, 7), (7, 50), (64, 64), (300, 48)])
+def test_svd_vs_lapack(oracle, shape):
+    A = oracle.Rng(sum(shape)).gaussian_matrix(*shape)
+    S, sig, T = oracle.svd(A)
+    assert np.allclose(sig, np.linalg.svd(A, compute_uv=False), rtol=1e-12, atol=1e-13 * sig[0])
+    assert np.linalg.norm(S @ np.diag(sig) @ T.T - A) <= 1e-12 * np.linalg.norm(A) * 8
+
+
+def test_pseudo_inverse(oracle):  # test_linalg.cpp:150-169
+    rng = oracle.Rng(9)
+    Q, _ = oracle.thin_qr(rng.gaussian_matrix(4, 4))
+    assert np.linalg.norm(oracle.pseudo_inverse(Q) - Q.T) < 1e-12
+    Dp = oracle.pseudo_inverse(np.diag([2.0, 0.0]), 1e-8)
+    assert Dp[0, 0] == pytest.approx(0.5) and Dp[1, 1] == 0.0
+    A = rng.gaussian_matrix(5, 3)
+    Ap = oracle.pseudo_inverse(A)
+    assert np.linalg.norm(A @ Ap @ A - A) <= 1e-11 * np.linalg.norm(A)
+    assert np.linalg.norm(Ap @ A @ Ap - Ap) <= 1e-11 * np.linalg.norm(Ap)
+    assert np.linalg.norm(A @ Ap - (A @ Ap).T) <= 1e-11
+    assert np.linalg.norm(oracle.pseudo_inverse(np.zeros((3, 2)))) == 0.0
+
+
+def test_numerical_rank(oracle):  # test_linalg.cpp:171-179
+    D = np.diag([1.0, 1e-10])
+    assert oracle.numerical_rank(D, 1e-6) == 1
+    assert oracle.numerical_rank(np.zeros((3, 3)), 1e-6) == 0
+    assert oracle.numerical_rank(D, 1e-6, True) == 1
+    assert oracle.numerical_rank(D, 1e-11, True) == 2
+    with pytest.raises(ValueError):
+        oracle.numerical_rank(D, 0.0)
+
+
+@pytest.mark.parametrize("shape", [(6, 40), (16, 256), (32, 256), (48, 300)])
+def test_colpiv_pivots_match_lapack_geqp3(oracle, shape):
+    # Eigen ColPivHouseholderQR follows LAPACK xGEQP3's pivot rule and norm
+    # downdate; on generic inputs the pivot order must agree with dgeqp3.
+    A = oracle.Rng(100 + shape[1]).gaussian_matrix(*shape)
+    d = oracle.colpiv_qr(A)
+    _, _, piv = sla.qr(A, pivoting=True, mode="economic")
+    k = min(shape)
+    assert list(d["perm"][:k]) == list(piv[:k])
+    assert d["rank"] == k
+
+
+def test_colpiv_solve(oracle):
+    rng = oracle.Rng(77)
+    A = rng.gaussian_matrix(20, 6)
+    B = rng.gaussian_matrix(20, 3)
+    X = oracle.colpiv_solve(A, B, 1e-10)
+    Xs = np.linalg.lstsq(A, B, rcond=None)[0]
+    assert np.allclose(X, Xs, atol=1e-12)
+    G = rng.gaussian_matrix(5, 5)
+    assert np.allclose(oracle.colpiv_solve(G, np.eye(5)), np.linalg.inv(G), atol=1e-11)
+
+
+def test_index_set_validation(oracle):  # test_linalg.cpp:226-241 (through primitive_cur)
+    M = np.arange(9.0).reshape(3, 3)
+    with pytest.raises(ValueError):
+        oracle.primitive_cur(M, [0, 0], [1, 2], 1)
+    with pytest.raises(ValueError):
+        oracle.primitive_cur(M, [3], [1], 1)
+
+
+# ---------------------------------------------------------------- maxvol / CUR
+def test_t_factor(oracle):  # test_cur.cpp:11-14
+    assert oracle.t_factor(5, 5, 1.1) == pytest.approx(1.0)
+    assert oracle.t_factor(10, 2, 1.0) == pytest.approx(math.sqrt(17.0))
+
+
+def test_maxvol_known_answers(oracle):  # test_cur.cpp:16-33
+    A = np.zeros((9, 3))
+    A[0, 0] = A[1, 1] = A[2, 2] = 1.0
+    assert set(oracle.maxvol_rows(A)) >= {0, 1, 2}
+    assert oracle.maxvol_rows(np.array([[1.0], [2.0], [-3.0]]), 1.0) == [2]
+    with pytest.raises(oracle.SelectionFailure):
+        oracle.maxvol_rows(np.zeros((5, 2)))
+
+
+def test_maxvol_dominance_and_volume(oracle):  # test_cur.cpp:35-60
+    rng = oracle.Rng(31)
+    m, r, h = 64, 4, 1.1
+    A, _ = oracle.thin_qr(rng.gaussian_matrix(m, r))
+    I = oracle.maxvol_rows(A, h)
+    G = A[I, :]
+    B = A @ np.linalg.inv(G)
+    assert np.abs(B).max() <= h * (1 + 1e-12)
+    assert np.linalg.norm(np.linalg.inv(G), 2) <= oracle.t_factor(m, r, h) * (1 + 1e-6)
+    vol = abs(np.linalg.det(G))
+    beaten = sum(vol >= abs(np.linalg.det(A[rng.distinct_indices(r, m), :])) for _ in range(1000))
+    assert beaten >= 990
+
+
+def test_primitive_cur_exact_rank(oracle):  # test_cur.cpp:62-78
+    ok = failures = 0
+    for t in range(100):
+        rng = oracle.Rng(1300 + t)
+        n, r = 48, 4
+        M = oracle.gen_factor_gaussian(n, n, r, 0.0, rng)
+        try:
+            c = oracle.primitive_cur(M, rng.distinct_indices(r, n), rng.distinct_indices(r, n), r)
+            err = np.linalg.norm(M - oracle.cur_reconstruct(M, c["I"], c["J"], c["nucleus"]), 2)
+            ok += err <= 1e-8 * np.linalg.norm(M, 2)
+        except oracle.GeneratorRankFailure:
+            failures += 1
+    assert ok >= 95 and ok + failures == 100
+
+
+def test_primitive_cur_leading_block(oracle):  # test_cur.cpp:80-87
+    M = np.diag([5.0, 4, 3, 2, 1, 0.5])
+    c = oracle.primitive_cur(M, [0, 1, 2], [0, 1, 2], 3)
+    R = oracle.cur_reconstruct(M, c["I"], c["J"], c["nucleus"])
+    assert np.linalg.norm(R[:3, :3] - M[:3, :3]) <= 1e-12
+
+
+def test_primitive_cur_missed_delta(oracle):  # test_cur.cpp:89-100
+    D = np.zeros((8, 8))
+    D[5, 5] = 1.0
+    with pytest.raises(oracle.GeneratorRankFailure):
+        oracle.primitive_cur(D, [0, 1], [0, 1], 1)
+    Dp = D + 1e-8
+    c = oracle.primitive_cur(Dp, [0, 1], [0, 1], 1)
+    assert oracle.cur_evaluate(Dp, c["I"], c["J"], c["nucleus"], "chebyshev") >= 0.5
+
+
+def test_primitive_cur_reads_only_generator(oracle):  # test_cur.cpp:101-108
+    rng = oracle.Rng(32)
+    M = oracle.gen_factor_gaussian(40, 30, 3, 0.0, rng)
+    c = oracle.primitive_cur(M, rng.distinct_indices(5, 40), rng.distinct_indices(4, 30), 3)
+    assert c["accesses"] == 20
+
+
+def test_cross_approx_exactness_and_accounting(oracle):  # test_cur.cpp:145-155
+    rng = oracle.Rng(35)
+    m, n, r = 64, 48, 5
+    M = oracle.gen_factor_gaussian(m, n, r, 0.0, rng)
+    c = oracle.cross_approx(M, r, r, r, [], 1, 1.1, None, rng)
+    err = np.linalg.norm(M - oracle.cur_reconstruct(M, c["I"], c["J"], c["nucleus"]), 2)
+    assert err <= 1e-9 * np.linalg.norm(M, 2)
+    assert len(c["trace"]) == 2
+    assert c["accesses"] <= r * n + m * r + 2 * r * r
+
+
+def test_cross_approx_extra_loops(oracle):  # test_cur.cpp:169-183 (reduced to 30 trials)
+    ok = 0
+    for t in range(30):
+        M = oracle.gen_factor_gaussian(96, 96, 6, 1e-6, oracle.Rng(1600 + t))
+        c1 = oracle.cross_approx(M, 6, 6, 6, [], 1, 1.1, None, oracle.Rng(1700 + t))
+        c5 = oracle.cross_approx(M, 6, 6, 6, [], 5, 1.1, None, oracle.Rng(1700 + t))
+        e1 = oracle.cur_evaluate(M, c1["I"], c1["J"], c1["nucleus"])
+        e5 = oracle.cur_evaluate(M, c5["I"], c5["J"], c5["nucleus"])
+        ok += e5 <= e1 * (1 + 1e-6)
+    assert ok >= 27
+
+
+def test_cross_approx_early_stop(oracle):  # test_cur.cpp:185-192
+    rng = oracle.Rng(36)
+    M = oracle.gen_factor_gaussian(64, 64, 4, 0.0, rng)
+    c = oracle.cross_approx(M, 4, 4, 4, [], 8, 1.1, 1e-8, rng)
+    assert len(c["trace"]) < 16
+    assert c["trace"][-1]["error_estimate"] is not None
+
+
+def test_cur_evaluate_norm_ordering(oracle):  # test_cur.cpp:194-205
+    rng = oracle.Rng(37)
+    M = oracle.gen_factor_gaussian(24, 24, 3, 1e-3, rng)
+    c = oracle.primitive_cur(M, rng.distinct_indices(3, 24), rng.distinct_indices(3, 24), 3)
+    sp = oracle.cur_evaluate(M, c["I"], c["J"], c["nucleus"], "spectral")
+    fr = oracle.cur_evaluate(M, c["I"], c["J"], c["nucleus"], "frobenius")
+    ch = oracle.cur_evaluate(M, c["I"], c["J"], c["nucleus"], "chebyshev")
+    assert ch <= fr * (1 + 1e-12) and sp <= fr * (1 + 1e-12) and fr > 0
+
+
+# ---------------------------------------------------------------- sketch operators
+H4 = np.array([[1, 1, 1, 1], [1, -1, 1, -1], [1, 1, -1, -1], [1, -1, -1, 1]], float)
+
+
+def test_abridged_hadamard_displays(oracle):  # test_sketch.cpp:29-48
+    E1 = np.array([[1, 0, 1, 0], [0, 1, 0, 1], [1, 0, -1, 0], [0, 1, 0, -1]], float)
+    assert np.array_equal(oracle.materialize(oracle.make_abridged_hadamard(4, 1)), E1)
+    assert np.array_equal(oracle.materialize(oracle.make_abridged_hadamard(4, 2)), H4)
+    H8 = np.block([[H4, H4], [H4, -H4]])
+    assert np.array_equal(oracle.materialize(oracle.make_abridged_hadamard(8, 3)), H8)
+    with pytest.raises(ValueError):
+        oracle.make_abridged_hadamard(6, 2)
+
+
+def test_permutation_and_sign(oracle):  # test_sketch.cpp:79-96
+    P = oracle.materialize(oracle.make_permutation([3, 2, 1, 0]))
+    assert all(P[i, 3 - i] == 1.0 for i in range(4)) and P.sum() == 4.0
+    rng = oracle.Rng(1)
+    op = oracle.gen_permutation(8, rng)
+    X = rng.gaussian_matrix(8, 3)
+    assert np.array_equal(op.apply_transpose(op.apply(X)), X)
+    D = oracle.materialize(oracle.gen_sign_diagonal(8, rng))
+    assert np.array_equal(D @ D, np.eye(8))
+    with pytest.raises(ValueError):
+        oracle.make_sign_diagonal(np.zeros(3))
+
+
+def test_sparse_circulant_dense_oracle(oracle):  # test_sketch.cpp:101-117
+    rng = oracle.Rng(2)
+    n, s = 16, 3
+    op = oracle.gen_sparse_circulant(n, s, rng)
+    Z = oracle.materialize(op)
+    v = Z[:, 0]
+    f = 0.0
+    for i in range(1, n):
+        if Z[0, i] != 0:
+            f = Z[0, i] / v[n - i]
+    Zo = np.array([[v[i - j] if i >= j else f * v[n + i - j] for j in range(n)] for i in range(n)])
+    assert np.array_equal(Z, Zo)
+    assert all((Z[:, j] != 0).sum() == s for j in range(n))
+    X = rng.gaussian_matrix(n, 5)
+    assert np.linalg.norm(op.apply(X) - Z @ X) < 1e-13 * np.linalg.norm(Z) * np.linalg.norm(X)
+    assert np.linalg.norm(op.apply_transpose(X) - Z.T @ X) < 1e-13 * np.linalg.norm(Z) * np.linalg.norm(X)
+
+
+def test_sub_identity_and_product(oracle):  # test_sketch.cpp:159-182
+    op = oracle.make_sub_identity([1, 3], 4)
+    M = np.array([[1, 2], [3, 4], [5, 6], [7, 8]], float)
+    S = op.apply(M)
+    assert S[0, 0] == 3.0 and S[1, 1] == 8.0
+    assert (op.apply_transpose(S)[0] == 0).all()
+    rng = oracle.Rng(7)
+    prod = oracle.make_product([oracle.gen_permutation(8, rng), oracle.gen_sign_diagonal(8, rng),
+                                oracle.make_abridged_hadamard(8, 2)])
+    Pm = oracle.materialize(prod)
+    X = rng.gaussian_matrix(8, 3)
+    sc = 1e-13 * np.linalg.norm(Pm) * np.linalg.norm(X)
+    assert np.linalg.norm(prod.apply(X) - Pm @ X) < sc
+    assert np.linalg.norm(prod.apply_transpose(X) - Pm.T @ X) < sc
+
+
+def test_asph_orthogonal_up_to_2d(oracle):  # test_sketch.cpp:185-190
+    A = oracle.materialize(oracle.gen_asph(16, 2, oracle.Rng(8)))
+    assert np.linalg.norm(A.T @ A - 4.0 * np.eye(16)) < 1e-11
+
+
+def test_take_columns(oracle):  # test_sketch.cpp:192-203
+    S = oracle.materialize(oracle.take_columns(oracle.make_abridged_hadamard(4, 2), [0, 1]))
+    assert np.array_equal(S, H4[:, :2])
+
+
+@pytest.mark.parametrize("n", [4, 8, 16, 64])
+def test_apply_materialize_both_sides(oracle, n):  # test_sketch.cpp:223-240
+    rng = oracle.Rng(40 + n)
+    ops = [oracle.gen_permutation(n, rng), oracle.gen_sign_diagonal(n, rng),
+           oracle.make_abridged_hadamard(n, 2), oracle.gen_sparse_circulant(n, 3, rng),
+           oracle.gen_gaussian(n, n, rng), oracle.gen_asph(n, 2, rng)]
+    M = rng.gaussian_matrix(n, 3)
+    W = rng.gaussian_matrix(3, n)
+    for op in ops:
+        D = oracle.materialize(op)
+        scale = 1e-12 * np.linalg.norm(D) * np.linalg.norm(M) + 1e-13
+        assert np.linalg.norm(oracle.apply(op, M, "left") - D @ M) <= scale
+        assert np.linalg.norm(oracle.apply(op, W, "right") - W @ D) <= scale
+
+
+def test_flop_budgets(oracle):  # test_sketch.cpp:258-279
+    rng = oracle.Rng(60)
+    n, c = 64, 8
+    M = rng.gaussian_matrix(n, c)
+    oracle.reset_op_counter()
+    oracle.make_abridged_hadamard(n, 3).apply(M)
+    adds, muls = oracle.op_counter()
+    assert adds <= 3 * n * c and muls == 0
+    oracle.reset_op_counter()
+    oracle.gen_sparse_circulant(n, 4, rng).apply(M)
+    assert sum(oracle.op_counter()) <= (2 * 4 - 1) * n * c
+    oracle.reset_op_counter()
+    oracle.make_sub_identity([0, 5, 9], n).apply(M)
+    assert sum(oracle.op_counter()) == 0
+
+
+# ---------------------------------------------------------------- range finder / LSR
+def test_range_finder_exact_rank(oracle):  # test_lra.cpp:10-22
+    for t in range(10):
+        rng = oracle.Rng(700 + t)
+        m, n, r, l = 48, 40, 6, 10
+        M = oracle.gen_factor_gaussian(m, n, r, 0.0, rng)
+        H = oracle.gen_gaussian(n, l, rng)
+        for trunc in (False, True):
+            U, V = oracle.range_finder(M, H, r, trunc)
+            assert np.linalg.norm(M - U @ V, 2) <= 1e-10 * np.linalg.norm(M, 2)
+            if trunc:
+                assert U.shape[1] == r
+
+
+def test_range_finder_rank_failure(oracle):  # test_lra.cpp:24-30
+    rng = oracle.Rng(20)
+    H = oracle.gen_gaussian(16, 4, rng)
+    with pytest.raises(oracle.RangeFailure):
+        oracle.range_finder(np.zeros((16, 16)), H, 1)
+    M1 = rng.gaussian_matrix(16, 1) @ rng.gaussian_matrix(1, 16)
+    with pytest.raises(oracle.RangeFailure):
+        oracle.range_finder(M1, H, 2)
+
+
+def test_range_finder_graded_spectrum_asph(oracle):  # test_lra.cpp:32-44 (5 trials)
+    tot = 0.0
+    for t in range(5):
+        rng = oracle.Rng(800 + t)
+        M = oracle.gen_svd_profile(256, 8, rng)
+        H = oracle.take_columns_random(oracle.gen_asph(256, 3, rng), 8, rng)
+        U, V = oracle.range_finder(M, H, 8)
+        tot += np.linalg.norm(M - U @ V, 2)
+    assert tot / 5 <= 1e-6
+
+
+def test_lsr_full_permutation_exact(oracle):  # test_lsr.cpp:59-69
+    rng = oracle.Rng(13)
+    A = rng.gaussian_matrix(30, 3)
+    b = rng.gaussian_vector(30)
+    F = oracle.gen_permutation(30, rng)
+    rep = oracle.sketch_solve(A, b, F, True)
+    assert rep["k"] == 30
+    assert rep["ratio"] == pytest.approx(1.0, rel=1e-10)
+    assert rep["sketched_residual"] == pytest.approx(rep["true_residual"], rel=1e-10)
+
+
+def test_lsr_consistent_system(oracle):  # test_lsr.cpp:71-81
+    rng = oracle.Rng(14)
+    A = rng.gaussian_matrix(64, 6)
+    x0 = rng.gaussian_vector(6)
+    b = A @ x0
+    F = oracle.gen_gaussian(8, 64, rng)
+    rep = oracle.sketch_solve(A, b, F)
+    assert np.linalg.norm(rep["x_hat"] - x0) < 1e-8
+    assert rep["sketched_residual"] < 1e-10
+
+
+def test_lsr_rank_failure(oracle):  # test_lsr.cpp:83-90
+    rng = oracle.Rng(15)
+    A = rng.gaussian_matrix(32, 4)
+    b = rng.gaussian_vector(32)
+    with pytest.raises(oracle.SketchRankFailure):
+        oracle.sketch_solve(A, b, oracle.make_gaussian(np.zeros((6, 32))))
+
+
+def test_lsr_gaussian_ratio(oracle):  # test_lsr.cpp:92-105
+    m, d = 256, 10
+    tot = 0.0
+    for t in range(20):
+        rng = oracle.Rng(300 + t)
+        A, b = oracle.gen_lsr_gaussian(m, d, 0.01, rng)
+        rep = oracle.sketch_solve(A, b, oracle.gen_gaussian(6 * d, m, rng), True)
+        assert 1.0 - 1e-12 <= rep["ratio"] < 2.0
+        tot += rep["ratio"]
+    assert tot / 20 < 1.3
+
+
+def test_solve_exact_vs_lapack(oracle):
+    rng = oracle.Rng(16)
+    A, b = oracle.gen_lsr_gaussian(200, 12, 0.01, rng)
+    x = oracle.solve_exact(A, b)
+    assert np.allclose(x, np.linalg.lstsq(A, b, rcond=None)[0], atol=1e-12)
