@@ -1,0 +1,200 @@
+/*
+ * slra_cuda.h — C-ABI of the B200 (sm_100a) hot path of the `slra` library
+ * (Pan–Luan–Svadlenka–Zhao, arXiv:1611.01391).
+ *
+ * Plain pointers and sizes only. Matrices are column-major FP64 with an
+ * explicit leading dimension (the reference's Eigen::MatrixXd layout,
+ * /root/reference/proj/include/slra/matrix.hpp:10); index sets are int64
+ * (Eigen::Index, matrix.hpp:14). Every pointer named d_* is DEVICE memory;
+ * h_* is host memory. All calls are asynchronous on the context's stream
+ * unless they return data to the host (documented per call).
+ *
+ * Each entry point replaces one reference interface on the hot path
+ * (SURVEY.md §8a); the reference file:line is cited per function. The C++
+ * host layer (paper_1611_01391_b200/include/slra/*.hpp) keeps the reference
+ * signatures and calls these; INTEGRATION.md shows the reference-side
+ * dispatch a maintainer would add. There is no CPU fallback: without a CUDA
+ * device every call returns SLRA_ERR_NO_DEVICE.
+ */
+#ifndef SLRA_CUDA_H_
+#define SLRA_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes map 1:1 onto the reference's typed failures
+ * (/root/reference/proj/include/slra/errors.hpp:11-33). */
+enum slra_status {
+  SLRA_OK = 0,
+  SLRA_ERR_INVALID_ARGUMENT = 1,      /* std::invalid_argument            */
+  SLRA_ERR_RANGE_FAILURE = 2,         /* RangeFailure        (lra.cpp:21) */
+  SLRA_ERR_SKETCH_RANK_FAILURE = 3,   /* SketchRankFailure   (lsr.cpp:55) */
+  SLRA_ERR_SELECTION_FAILURE = 4,     /* SelectionFailure    (cur.cpp:106)*/
+  SLRA_ERR_GENERATOR_RANK_FAILURE = 5,/* GeneratorRankFailure(cur.cpp:157)*/
+  SLRA_ERR_CUDA = 6,                  /* CUDA runtime error               */
+  SLRA_ERR_NO_DEVICE = 7,             /* no CUDA device / wrong arch      */
+  SLRA_ERR_UNSUPPORTED = 8            /* shape outside the device kernels */
+};
+
+typedef struct slra_context* slra_ctx;
+
+/* ------------------------------------------------------------ runtime */
+const char* slra_status_string(int status);
+/* Last CUDA error text recorded by this thread (for SLRA_ERR_CUDA). */
+const char* slra_last_error(void);
+/* Create a context on `device`; `stream` is a cudaStream_t (NULL = a new
+ * non-blocking stream owned by the context). */
+int slra_ctx_create(int device, void* stream, slra_ctx* out);
+int slra_ctx_destroy(slra_ctx ctx);
+int slra_ctx_synchronize(slra_ctx ctx);
+void* slra_ctx_stream(slra_ctx ctx);
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t slra_ctx_launch_count(slra_ctx ctx);
+int slra_device_alloc(slra_ctx ctx, int64_t bytes, void** d_out);
+int slra_device_free(slra_ctx ctx, void* d_ptr);
+int slra_memcpy_h2d(slra_ctx ctx, void* d_dst, const void* h_src, int64_t bytes);
+int slra_memcpy_d2h(slra_ctx ctx, void* h_dst, const void* d_src, int64_t bytes); /* syncs */
+int slra_memcpy_d2d(slra_ctx ctx, void* d_dst, const void* d_src, int64_t bytes);
+
+/* ------------------------------------------------------------ a2/a14 gathers
+ * EntryOracle::rows_of / cols_of / block (testgen.cpp:11-30) and
+ * select_rows / select_cols / select_block (linalg.cpp:35-52). Bit-exact. */
+int slra_gather_rows(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                     const int64_t* d_I, int64_t k, double* d_R, int64_t ldr);
+int slra_gather_cols(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                     const int64_t* d_J, int64_t l, double* d_C, int64_t ldc);
+int slra_gather_block(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                      const int64_t* d_I, int64_t k, const int64_t* d_J, int64_t l,
+                      double* d_G, int64_t ldg);
+
+/* ------------------------------------------------------------ a3 sketches
+ * A compiled sketch plan: output unit t (a column for the right-side
+ * product M*H, a row for the left-side product F*W) is a signed combination
+ * of `width` source columns/rows, src[t*width + s] with coefficient
+ * coef[t*width + s] (exact +-1 for the in-scope kinds), evaluated in the
+ * reference's order:
+ *   tree = SLRA_TREE_LIST: ((c0 x0 + c1 x1) + c2 x2) + ...  — SparseCirculantOp
+ *          nz-list order (sketch.cpp:250-255, 269-273); width 1 = SubIdentity.
+ *   tree = SLRA_TREE_FWHT: in-place radix-2 butterfly over the width = 2^d
+ *          leaves (ah_recurse, sketch.cpp:98-107), output leaf q[t].
+ * The host layer compiles ColumnSlice(Product{P,D,AH}) / ColumnSlice(Z_f) /
+ * Product{SubIdentity, Z_f, D} / SubIdentity into plans (only the l kept
+ * outputs are computed, the sublinear form of sketch.cpp:558-567).
+ * Results are bit-identical to the reference's full application. */
+enum slra_tree { SLRA_TREE_LIST = 0, SLRA_TREE_FWHT = 1 };
+/* out(:, t) = combine_s coef * A(:, src)  — apply(H, M, Side::Right), sketch.cpp:679-682 */
+int slra_sketch_cols(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                     const int64_t* d_src, const double* d_coef, const int32_t* d_q,
+                     int64_t width, int tree, int64_t l, double* d_out, int64_t ldo);
+/* out(t, :) = combine_s coef * W(src, :)  — F.apply(W), sketch.cpp:520-523 */
+int slra_sketch_rows(slra_ctx ctx, const double* d_W, int64_t ldw, int64_t m, int64_t ncols,
+                     const int64_t* d_src, const double* d_coef, const int32_t* d_q,
+                     int64_t width, int tree, int64_t k, double* d_out, int64_t ldo);
+
+/* ------------------------------------------------------------ a4/a8 small dense
+ * thin_qr (linalg.cpp:67-79): Householder QR, R(i,i) >= 0, explicit thin Q.
+ * Any m >= c, c <= 64 (TSQR over 256-row leaves). */
+int slra_thin_qr(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t c,
+                 double* d_Q, int64_t ldq, double* d_R, int64_t ldr);
+/* svd (linalg.cpp:81-98): compact SVD, sigma nonincreasing, largest-|.|
+ * entry of each left vector >= 0. min(m,n) <= 64. S is m x p, T is n x p,
+ * p = min(m, n). */
+int slra_svd(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+             double* d_S, int64_t lds, double* d_sigma, double* d_T, int64_t ldt);
+
+/* ------------------------------------------------------------ a5/a6 pivoting
+ * maxvol_rows (cur.cpp:88-116) on a tall A (m x r): ColPivHouseholderQR(A^T)
+ * init + <= max_swaps+1 swap rounds. max_swaps = 0 means 4r. */
+int slra_maxvol_rows(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t r,
+                     double h, int64_t max_swaps, int64_t* d_idx);
+/* select_rows_spanning (cur.cpp:118-135) for count == A.cols() (no padding):
+ * thin_qr + maxvol; optionally |det Q[idx,:]| (cur.cpp:192-197). */
+int slra_select_rows_spanning(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m,
+                              int64_t c, int64_t count, double h, int64_t* d_idx,
+                              double* d_volume);
+
+/* ------------------------------------------------------------ a7/a8 CUR
+ * primitive_cur (cur.cpp:137-162): nucleus U = T_r diag(1/sigma_r) S_r^T
+ * (l x k) of the generator G = A(I,J). r <= 0 selects the adaptive rank
+ * numerical_rank(G, 1e-10, Relative) (linalg.cpp:123-132; configs 3 and 5).
+ * Optional factor outputs d_Tsig (l x r = T_r diag(1/sigma_r)) and d_Sr
+ * (k x r) let the residual run with inner dimension r. h_r_out receives r. */
+int slra_primitive_cur(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                       const int64_t* d_I, int64_t k, const int64_t* d_J, int64_t l, int64_t r,
+                       double* d_nucleus, int64_t ldu, double* d_Tsig, double* d_Sr,
+                       int64_t* h_r_out);
+/* cross_approx (cur.cpp:201-255), stop_tol unset. init_rows (k indices)
+ * must be given (the host draws them with Rng::distinct_indices exactly as
+ * cur.cpp:207-209). Outputs: I (k), J (l), nucleus (l x k), the trace
+ * (2*loops steps: rows k, cols l, volume proxy), adaptive r. Blocks until
+ * done (status is host-visible). */
+int slra_cross_approx(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                      int64_t r, int64_t k, int64_t l, const int64_t* d_init_rows, int loops,
+                      double h, int64_t* d_I, int64_t* d_J, double* d_nucleus,
+                      int64_t* d_trace_rows, int64_t* d_trace_cols, double* d_trace_volume,
+                      int64_t* h_r_out);
+/* Batched cross_approx + per-block Frobenius residual: nblocks independent
+ * m x n blocks at d_A + b*block_stride (ld = lda); one CTA per block.
+ * Per-block outputs: I (k), J (l), nucleus (l x k), r, status (slra_status),
+ * resid_sq = ||B - C U R||_F^2, norm_sq = ||B||_F^2. Strips must fit on
+ * chip (m, n <= 512, k, l <= 32). */
+int slra_cross_approx_batched(slra_ctx ctx, const double* d_A, int64_t lda, int64_t block_stride,
+                              int64_t nblocks, int64_t m, int64_t n, int64_t r, int64_t k,
+                              int64_t l, const int64_t* d_init_rows, int loops, double h,
+                              int64_t* d_I, int64_t* d_J, double* d_nucleus, int64_t* d_r,
+                              int32_t* d_status, double* d_resid_sq, double* d_norm_sq);
+
+/* ------------------------------------------------------------ a9 residual
+ * ||A - P Q||_F^2 and ||A||_F^2 in one pass over A (FP64 DMMA tiles fused
+ * with subtract-square-reduce, deterministic two-stage reduction).
+ * P is m x inner (ldp), Q is inner x n (ldq). Results land in DEVICE
+ * doubles d_out[0] = resid_sq, d_out[1] = norm_sq. */
+int slra_lowrank_residual(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                          const double* d_P, int64_t ldp, const double* d_Q, int64_t ldq,
+                          int64_t inner, double* d_out);
+/* cur_evaluate(M, c, Frobenius) (cur.cpp:80-82): ||A - A(:,J) U A(I,:)||_F.
+ * Returns resid_sq and norm_sq to the host (blocks). */
+int slra_cur_residual(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                      const int64_t* d_I, int64_t k, const int64_t* d_J, int64_t l,
+                      const double* d_nucleus, int64_t ldu, double* h_resid_sq,
+                      double* h_norm_sq);
+
+/* ------------------------------------------------------------ GEMM
+ * C = alpha op(A) op(B) + beta C, FP64 DMMA (mma.sync m8n8k4). trans = 0/1. */
+int slra_gemm(slra_ctx ctx, int transA, int transB, int64_t m, int64_t n, int64_t k, double alpha,
+              const double* d_A, int64_t lda, const double* d_B, int64_t ldb, double beta,
+              double* d_C, int64_t ldc);
+
+/* ------------------------------------------------------------ a10 range finder
+ * range_finder (lra.cpp:31-39) with the sketch H given as a compiled
+ * right-side plan (see slra_sketch_cols). variant 0 = BasisQr (U = Q of MH,
+ * m x l; V = U^T M), 1 = TruncatedRankR (U = S_r Sigma_r, m x r; V = U^+ M).
+ * Also returns the residual ||M - U V||_F^2 and ||M||_F^2 (d_out[0..1]),
+ * and the sketch singular values (l). Blocks (rank check is host-visible);
+ * SLRA_ERR_RANGE_FAILURE when numerical_rank(MH, 1e-10, Relative) < r. */
+int slra_range_finder(slra_ctx ctx, const double* d_M, int64_t ldm, int64_t m, int64_t n,
+                      const int64_t* d_src, const double* d_coef, const int32_t* d_q,
+                      int64_t width, int tree, int64_t l, int64_t r, int variant, double* d_U,
+                      int64_t ldu, double* d_V, int64_t ldv, double* d_out,
+                      double* d_sigma);
+
+/* ------------------------------------------------------------ a11/a12 LSR
+ * sketch_solve (lsr.cpp:37-67): FW = F (A|b) through a compiled left-side
+ * plan (k rows), column-pivoted Householder QR of FA (threshold 1e-10;
+ * SLRA_ERR_SKETCH_RANK_FAILURE when rank < d), x_hat = solve(Fb).
+ * h_sketched_residual = ||FA x_hat - Fb||. d <= 256, k <= 8192. Blocks. */
+int slra_sketch_solve(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
+                      const double* d_b, const int64_t* d_src, const double* d_coef,
+                      const int32_t* d_q, int64_t width, int tree, int64_t k, double* d_x_hat,
+                      double* h_sketched_residual);
+/* residual_norm (lsr.cpp:26-28): ||A x - b||^2 into d_out[0] (device). */
+int slra_lsr_residual(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
+                      const double* d_b, const double* d_x, double* d_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLRA_CUDA_H_ */

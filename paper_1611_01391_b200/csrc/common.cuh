@@ -1,0 +1,154 @@
+// Shared device/runtime helpers for the sm_100a kernels behind slra_cuda.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cfloat>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "slra_cuda.h"
+
+namespace slra_dev {
+
+// ------------------------------------------------------------------ context
+struct Context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool owns_stream = false;
+  int64_t launches = 0;
+  // growable scratch (device) and pinned host scratch
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  // per-CTA partial sums of the two-stage reductions
+  double* partials = nullptr;
+  int partials_cap = 0;
+  // small persistent device scratch (statuses, ranks, flags): 4096 bytes
+  void* dsmall = nullptr;
+  // pinned host mirror of dsmall for status read-back
+  void* hsmall = nullptr;
+  // independent growable device arenas for multi-kernel orchestrations
+  // (slot 0: range finder, 1: cur residual, 2: lsr, 3: spare)
+  void* arena[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t arena_bytes[4] = {0, 0, 0, 0};
+};
+
+void set_last_error(const std::string& s);
+int cuda_status(cudaError_t e, const char* where);
+// Scratch of at least `bytes` (device). Synchronizes the stream when it grows.
+void* workspace(Context* c, size_t bytes);
+void* pinned_scratch(Context* c, size_t bytes);
+double* partials(Context* c, int n);
+void* arena(Context* c, int slot, size_t bytes);
+
+#define SLRA_CHECK_LAUNCH(ctx)                                          \
+  do {                                                                  \
+    (ctx)->launches++;                                                  \
+    cudaError_t _e = cudaGetLastError();                                \
+    if (_e != cudaSuccess) return slra_dev::cuda_status(_e, __func__);  \
+  } while (0)
+
+#define SLRA_CUDA(call)                                                 \
+  do {                                                                  \
+    cudaError_t _e = (call);                                            \
+    if (_e != cudaSuccess) return slra_dev::cuda_status(_e, #call);     \
+  } while (0)
+
+#define SLRA_TRY(expr)              \
+  do {                              \
+    int _s = (expr);                \
+    if (_s != SLRA_OK) return _s;   \
+  } while (0)
+
+inline Context* C(slra_ctx c) { return reinterpret_cast<Context*>(c); }
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum, result broadcast to every thread. `red` >= 33 doubles of smem.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double t = lane < NT / 32 ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// Argmax key: larger value wins; ties -> smaller index (Eigen maxCoeff keeps
+// the first maximum in traversal order).
+struct ArgMax {
+  double v;
+  int64_t i;
+};
+__device__ __forceinline__ ArgMax argmax_merge(ArgMax a, ArgMax b) {
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+__device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax b;
+    b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+    b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+    a = argmax_merge(a, b);
+  }
+  return a;
+}
+// Block argmax broadcast to all threads; `rv` >= 33 doubles, `ri` >= 33 int64.
+template <int NT>
+__device__ __forceinline__ ArgMax block_argmax(ArgMax a, double* rv, int64_t* ri) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_argmax(a);
+  __syncthreads();
+  if (lane == 0) {
+    rv[warp] = a.v;
+    ri[warp] = a.i;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    ArgMax t;
+    t.v = lane < NT / 32 ? rv[lane] : -1.0;
+    t.i = lane < NT / 32 ? ri[lane] : INT64_MAX;
+    t = warp_argmax(t);
+    if (lane == 0) {
+      rv[32] = t.v;
+      ri[32] = t.i;
+    }
+  }
+  __syncthreads();
+  ArgMax out;
+  out.v = rv[32];
+  out.i = ri[32];
+  return out;
+}
+
+// FP64 tensor-core MMA (sm_80+ mma.sync; SASS DMMA.8x8x4 on sm_100a).
+// A 8x4 row: a = A[lane>>2][lane&3]; B 4x8 col: b = B[lane&3][lane>>2];
+// C 8x8: c0,c1 = C[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace slra_dev

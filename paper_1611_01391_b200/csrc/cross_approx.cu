@@ -1,0 +1,395 @@
+// K-b / K-n: Cross-Approximation with maxvol pivoting and the CUR nucleus,
+// CTA-resident. One thread block runs the whole of cross_approx
+// (cur.cpp:201-255) for one problem whose strips fit in shared memory:
+//   per loop:  R = A(I,:) -> J = select_rows_spanning(R^T, l)   (cur.cpp:215-224)
+//              C = A(:,J) -> I = select_rows_spanning(C, k)      (cur.cpp:227-236)
+//   then primitive_cur(A, I, J, r) (cur.cpp:137-162) and the residual
+//   factors P = C T_r Sigma_r^-1 (m x r), Q = S_r^T R (r x n), so that
+//   C U R = P Q and ||A - C U R||_F runs with inner dimension r.
+// A grid of such blocks is the batched superfast-multipole workload
+// (config 5; hss.cpp:47-55 pattern) with no inter-block communication.
+#include "dense_cta.cuh"
+
+namespace slra_dev {
+
+constexpr int kCT = 256;
+
+struct CaParams {
+  const double* A;
+  int64_t lda, stride;
+  int m, n, r, k, l, loops;
+  double h;
+  const int64_t* init_rows;  // nprob x k
+  int64_t* I_out;            // nprob x k
+  int64_t* J_out;            // nprob x l
+  double* nucleus;           // nprob x (l*k), ld l
+  int64_t* r_out;            // nprob
+  int32_t* status;           // nprob
+  int64_t* trace_rows;       // (2*loops) x k   (problem 0 only, nullable)
+  int64_t* trace_cols;       // (2*loops) x l
+  double* trace_vol;         // 2*loops
+  double* P;                 // nprob x (m * rq), ld m   (nullable)
+  double* Q;                 // nprob x (rq * n), ld rq
+  int rq;                    // min(k, l)
+  int mode;                  // 0 = cross_approx, 1 = primitive_cur only (I,J given in I_out/J_out)
+};
+
+struct CaSmem {
+  double *S, *W, *R, *Gt, *V, *tau, *v, *nu, *nd, *sigma, *sgn, *rv, *Tm, *Sm;
+  int *p2r, *Icur, *Jcur, *perm, *order, *flag, *tmpidx;
+  int64_t* ri;
+};
+
+__host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
+  const int mm = m > n ? m : n, c = k > l ? k : l;
+  size_t d = 2 * (size_t)mm * c + 5 * (size_t)c * c + 6 * (size_t)c + 2 * (size_t)mm + 40;
+  size_t i = (size_t)mm + 4 * (size_t)c + 8 + (size_t)c;
+  return d * 8 + 33 * 8 + i * 4 + 64;
+}
+
+__device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
+  const int mm = m > n ? m : n, c = k > l ? k : l;
+  CaSmem s;
+  double* d = reinterpret_cast<double*>(base);
+  s.S = d; d += (size_t)mm * c;
+  s.W = d; d += (size_t)mm * c;
+  s.R = d; d += c * c;
+  s.Gt = d; d += c * c;
+  s.V = d; d += c * c;
+  s.Tm = d; d += c * c;
+  s.Sm = d; d += c * c;
+  s.tau = d; d += c;
+  s.v = d; d += c;
+  s.sigma = d; d += c;
+  s.sgn = d; d += c;
+  s.nu = d; d += mm;
+  s.nd = d; d += mm;
+  s.rv = d; d += 40;
+  d += 2 * c;  // slack
+  s.ri = reinterpret_cast<int64_t*>(d);
+  int* ip = reinterpret_cast<int*>(s.ri + 33);
+  s.p2r = ip; ip += mm;
+  s.Icur = ip; ip += c;
+  s.Jcur = ip; ip += c;
+  s.perm = ip; ip += c;
+  s.order = ip; ip += c;
+  s.tmpidx = ip; ip += c;
+  s.flag = ip;
+  return s;
+}
+
+// select_rows_spanning(strip, count, h) where strip (len x nidx) is gathered
+// from A: rows_strip -> strip = A(idx_in, :)^T (len = n), else A(:, idx_in).
+template <int NT>
+__device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_strip, const int* idx_in, int nidx,
+                            int len, int count, double h, int* idx_out, double* vol_out) {
+  const int tid = threadIdx.x;
+  // gather (each element of the strip is an entry read of the oracle)
+  if (rows_strip) {
+    for (int e = tid; e < len * nidx; e += NT) {
+      const int t = e % nidx, j = e / nidx;
+      s.S[j + t * len] = __ldg(A + idx_in[t] + (int64_t)j * lda);
+    }
+  } else {
+    for (int e = tid; e < len * nidx; e += NT) {
+      const int i = e % len, t = e / len;
+      s.S[i + t * len] = __ldg(A + i + (int64_t)idx_in[t] * lda);
+    }
+  }
+  __syncthreads();
+  cta_thin_qr<NT>(s.S, len, len, nidx, s.R, nidx, s.tau, s.rv);
+  const int rq = count < nidx ? count : nidx;
+  ColPivScratch cs{s.W, len, s.p2r, s.nu, s.nd, s.v, s.tau, s.rv, s.ri};
+  cta_colpiv_init<NT>(s.S, len, len, rq, cs, s.tmpidx);
+  __syncthreads();
+  const int st = cta_maxvol_swaps<NT>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, s.W, len, s.Gt, rq, s.perm, s.tau,
+                                      s.nu, s.nd, s.rv, s.ri, s.flag);
+  if (st != SLRA_OK) return st;
+  __syncthreads();
+  for (int t = tid; t < rq; t += NT) idx_out[t] = s.tmpidx[t];
+  __syncthreads();
+  if (count > rq) {
+    // pad with the largest remaining rows of the basis (cur.cpp:125-134);
+    // equal norms: lower index first.
+    for (int i = tid; i < len; i += NT) {
+      double acc = 0.0;
+      for (int j = 0; j < nidx; ++j) acc += s.S[i + j * len] * s.S[i + j * len];
+      s.nu[i] = sqrt(acc);
+    }
+    __syncthreads();
+    for (int t = rq; t < count; ++t) {
+      ArgMax a{-1.0, INT64_MAX};
+      for (int i = tid; i < len; i += NT) {
+        bool used = false;
+        for (int u = 0; u < t; ++u) used |= (idx_out[u] == i);
+        if (!used) a = argmax_merge(a, ArgMax{s.nu[i], i});
+      }
+      a = block_argmax<NT>(a, s.rv, s.ri);
+      if (tid == 0) idx_out[t] = (int)a.i;
+      __syncthreads();
+    }
+  }
+  // volume proxy |det Q[idx,:]| (cur.cpp:192-197), only when square
+  if (vol_out) {
+    if (count == nidx) {
+      for (int e = tid; e < count * nidx; e += NT) {
+        const int a = e % count, b = e / count;
+        s.Gt[a + b * count] = s.S[idx_out[a] + b * len];
+      }
+      __syncthreads();
+      if (tid < 32) {
+        const double dv = warp_abs_det(s.Gt, count, count);
+        if (tid == 0) *vol_out = dv;
+      }
+    } else if (tid == 0) {
+      *vol_out = 0.0;
+    }
+    __syncthreads();
+  }
+  return SLRA_OK;
+}
+
+// primitive_cur nucleus from G = A(I, J) (k x l). Writes r, nucleus (l x k)
+// and the factors Tm = T_r Sigma_r^-1 (l x r, ld l) and Sm = S_r (k x r, ld k)
+// into smem. Returns status.
+template <int NT>
+__device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I, int k, const int* J, int l,
+                           int r_req, int* r_out) {
+  const int tid = threadIdx.x;
+  const bool tall = k >= l;
+  const int p = tall ? k : l, q = tall ? l : k;
+  // W := G (tall) or G^T (wide), p x q, ld p
+  for (int e = tid; e < k * l; e += NT) {
+    const int a = e % k, b = e / k;
+    const double g = __ldg(A + I[a] + (int64_t)J[b] * lda);
+    if (tall) s.W[a + b * p] = g;
+    else s.W[b + a * p] = g;
+  }
+  __syncthreads();
+  cta_jacobi<NT>(s.W, p, p, q, s.V, q, s.flag);
+  // finish into S (p x q, ld p) and Gt (q x q, ld q): for tall G the left
+  // vectors are in S; for wide G (SVD of G^T) they are the rows of V.
+  cta_svd_finish<NT>(s.W, p, p, q, s.V, q, s.sigma, s.order, s.S, p, s.Gt, q, s.sgn);
+  if (!tall) {
+    // G^T = S' Sigma V'^T -> G = V' Sigma S'^T: left vectors of G = V'
+    // (columns of Gt), right = S'. Re-apply the sign rule on the left ones.
+    for (int t = threadIdx.x >> 5; t < q; t += NT / 32) {
+      const int lane = threadIdx.x & 31;
+      ArgMax a{-1.0, INT64_MAX};
+      for (int i = lane; i < q; i += 32) a = argmax_merge(a, ArgMax{fabs(s.Gt[i + t * q]), i});
+      a = warp_argmax(a);
+      const double f = (s.Gt[a.i + t * q] < 0.0) ? -1.0 : 1.0;
+      __syncwarp();
+      for (int i = lane; i < q; i += 32) s.Gt[i + t * q] *= f;
+      for (int i = lane; i < p; i += 32) s.S[i + t * p] *= f;
+    }
+    __syncthreads();
+  }
+  // left vectors Sl (k x q), right vectors Tr (l x q)
+  const double* Sl = tall ? s.S : s.Gt;
+  const int ldsl = tall ? p : q;
+  const double* Tr = tall ? s.Gt : s.S;
+  const int ldtr = tall ? q : p;
+  const double s0 = s.sigma[0];
+  int r = r_req;
+  if (r <= 0) {
+    r = 0;
+    for (int i = 0; i < q; ++i) r += (s.sigma[i] > 1e-10 * s0) ? 1 : 0;
+    if (r == 0) return SLRA_ERR_GENERATOR_RANK_FAILURE;
+  } else {
+    if (r > q) return SLRA_ERR_INVALID_ARGUMENT;
+    if (s0 <= 0.0 || s.sigma[r - 1] <= 1e-10 * s0) return SLRA_ERR_GENERATOR_RANK_FAILURE;
+  }
+  *r_out = r;
+  for (int e = tid; e < l * r; e += NT) {
+    const int a = e % l, j = e / l;
+    s.Tm[a + j * l] = Tr[a + j * ldtr] / s.sigma[j];
+  }
+  for (int e = tid; e < k * r; e += NT) {
+    const int a = e % k, j = e / k;
+    s.Sm[a + j * k] = Sl[a + j * ldsl];
+  }
+  __syncthreads();
+  return SLRA_OK;
+}
+
+__global__ void __launch_bounds__(kCT) ca_block_kernel(CaParams P) {
+  extern __shared__ __align__(16) char smem_raw[];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  CaSmem s = ca_carve(smem_raw, P.m, P.n, P.k, P.l);
+  const double* A = P.A + (int64_t)b * P.stride;
+  int status = SLRA_OK;
+  if (P.mode == 0) {
+    for (int t = tid; t < P.k; t += kCT) s.Icur[t] = (int)P.init_rows[(int64_t)b * P.k + t];
+    __syncthreads();
+    for (int loop = 0; loop < P.loops && status == SLRA_OK; ++loop) {
+      double* vol = (b == 0 && P.trace_vol) ? P.trace_vol + 2 * loop : nullptr;
+      status = select_strip<kCT>(s, A, P.lda, true, s.Icur, P.k, P.n, P.l, P.h, s.Jcur, vol);
+      if (status != SLRA_OK) break;
+      if (b == 0 && P.trace_rows) {
+        for (int t = tid; t < P.k; t += kCT) P.trace_rows[(int64_t)(2 * loop) * P.k + t] = s.Icur[t];
+        for (int t = tid; t < P.l; t += kCT) P.trace_cols[(int64_t)(2 * loop) * P.l + t] = s.Jcur[t];
+      }
+      vol = (b == 0 && P.trace_vol) ? P.trace_vol + 2 * loop + 1 : nullptr;
+      status = select_strip<kCT>(s, A, P.lda, false, s.Jcur, P.l, P.m, P.k, P.h, s.Icur, vol);
+      if (status != SLRA_OK) break;
+      if (b == 0 && P.trace_rows) {
+        for (int t = tid; t < P.k; t += kCT) P.trace_rows[(int64_t)(2 * loop + 1) * P.k + t] = s.Icur[t];
+        for (int t = tid; t < P.l; t += kCT) P.trace_cols[(int64_t)(2 * loop + 1) * P.l + t] = s.Jcur[t];
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int t = tid; t < P.k; t += kCT) s.Icur[t] = (int)P.I_out[(int64_t)b * P.k + t];
+    for (int t = tid; t < P.l; t += kCT) s.Jcur[t] = (int)P.J_out[(int64_t)b * P.l + t];
+    __syncthreads();
+  }
+  int r = 0;
+  if (status == SLRA_OK) status = cta_nucleus<kCT>(s, A, P.lda, s.Icur, P.k, s.Jcur, P.l, P.r, &r);
+  if (tid == 0) {
+    P.status[b] = status;
+    P.r_out[b] = status == SLRA_OK ? r : 0;
+  }
+  if (P.mode == 0) {
+    for (int t = tid; t < P.k; t += kCT) P.I_out[(int64_t)b * P.k + t] = s.Icur[t];
+    for (int t = tid; t < P.l; t += kCT) P.J_out[(int64_t)b * P.l + t] = s.Jcur[t];
+  }
+  if (status != SLRA_OK) {
+    // zero the residual factors so a batched residual of a failed block is ||B||
+    if (P.P) {
+      for (int64_t e = tid; e < (int64_t)P.m * P.rq; e += kCT) P.P[(int64_t)b * P.m * P.rq + e] = 0.0;
+      for (int64_t e = tid; e < (int64_t)P.rq * P.n; e += kCT) P.Q[(int64_t)b * P.rq * P.n + e] = 0.0;
+    }
+    return;
+  }
+  // nucleus U = Tm Sm^T (l x k)
+  double* U = P.nucleus + (int64_t)b * P.l * P.k;
+  for (int e = tid; e < P.l * P.k; e += kCT) {
+    const int a = e % P.l, c = e / P.l;
+    double acc = 0.0;
+    for (int j = 0; j < r; ++j) acc += s.Tm[a + j * P.l] * s.Sm[c + j * P.k];
+    U[a + (int64_t)c * P.l] = acc;
+  }
+  if (P.P) {
+    // P = A(:,J) Tm (m x rq, zero beyond r), Q = Sm^T A(I,:) (rq x n)
+    double* Pb = P.P + (int64_t)b * P.m * P.rq;
+    double* Qb = P.Q + (int64_t)b * P.rq * P.n;
+    for (int64_t e = tid; e < (int64_t)P.m * P.rq; e += kCT) {
+      const int i = (int)(e % P.m), j = (int)(e / P.m);
+      double acc = 0.0;
+      if (j < r)
+        for (int t = 0; t < P.l; ++t) acc += __ldg(A + i + (int64_t)s.Jcur[t] * P.lda) * s.Tm[t + j * P.l];
+      Pb[e] = acc;
+    }
+    for (int64_t e = tid; e < (int64_t)P.rq * P.n; e += kCT) {
+      const int j = (int)(e % P.rq), c = (int)(e / P.rq);
+      double acc = 0.0;
+      if (j < r)
+        for (int t = 0; t < P.k; ++t) acc += s.Sm[t + j * P.k] * __ldg(A + s.Icur[t] + (int64_t)c * P.lda);
+      Qb[e] = acc;
+    }
+  }
+}
+
+int launch_lowrank_residual(Context* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* P,
+                            int64_t ldp, const double* Q, int64_t ldq, int64_t inner, double* d_out);
+int launch_lowrank_residual_batched(Context* c, const double* A, int64_t lda, int64_t sA, int64_t m, int64_t n,
+                                    const double* P, int64_t ldp, int64_t sP, const double* Q, int64_t ldq,
+                                    int64_t sQ, int64_t inner, int64_t nprob, double* d_out_pairs);
+
+static bool ca_fits(int m, int n, int k, int l) {
+  return k >= 1 && l >= 1 && k <= 64 && l <= 64 && k <= m && l <= n &&
+         ca_smem_bytes(m, n, k, l) <= 227 * 1024;
+}
+
+int launch_ca_block(Context* c, const CaParams& p, int nprob) {
+  const size_t smem = ca_smem_bytes(p.m, p.n, p.k, p.l);
+  SLRA_CUDA(cudaFuncSetAttribute(ca_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ca_block_kernel<<<nprob, kCT, smem, c->stream>>>(p);
+  SLRA_CHECK_LAUNCH(c);
+  return SLRA_OK;
+}
+
+}  // namespace slra_dev
+
+using namespace slra_dev;
+
+extern "C" {
+
+int slra_cross_approx(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, int64_t r, int64_t k,
+                      int64_t l, const int64_t* init_rows, int loops, double h, int64_t* I_out, int64_t* J_out,
+                      double* nucleus, int64_t* trace_rows, int64_t* trace_cols, double* trace_vol,
+                      int64_t* h_r_out) {
+  if (!ctx || lda < m || loops < 1 || k < 1 || l < 1 || (r > 0 && (k < r || l < r)) || k > m || l > n)
+    return SLRA_ERR_INVALID_ARGUMENT;
+  if (!ca_fits((int)m, (int)n, (int)k, (int)l)) return SLRA_ERR_UNSUPPORTED;
+  Context* cx = C(ctx);
+  int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
+  int64_t* d_r = reinterpret_cast<int64_t*>(static_cast<char*>(cx->dsmall) + 64);
+  CaParams p{A, lda, 0, (int)m, (int)n, (int)r, (int)k, (int)l, loops, h, init_rows, I_out, J_out, nucleus, d_r,
+             d_status, trace_rows, trace_cols, trace_vol, nullptr, nullptr, (int)(k < l ? k : l), 0};
+  SLRA_TRY(launch_ca_block(cx, p, 1));
+  char* hs = static_cast<char*>(cx->hsmall);
+  SLRA_CUDA(cudaMemcpyAsync(hs, cx->dsmall, 128, cudaMemcpyDeviceToHost, cx->stream));
+  SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+  if (h_r_out) *h_r_out = *reinterpret_cast<int64_t*>(hs + 64);
+  return *reinterpret_cast<int32_t*>(hs);
+}
+
+int slra_cross_approx_batched(slra_ctx ctx, const double* A, int64_t lda, int64_t stride, int64_t nblocks, int64_t m,
+                              int64_t n, int64_t r, int64_t k, int64_t l, const int64_t* init_rows, int loops,
+                              double h, int64_t* I_out, int64_t* J_out, double* nucleus, int64_t* r_out,
+                              int32_t* status, double* resid_sq, double* norm_sq) {
+  if (!ctx || lda < m || loops < 1 || k < 1 || l < 1 || nblocks < 0 || (r > 0 && (k < r || l < r)))
+    return SLRA_ERR_INVALID_ARGUMENT;
+  if (!ca_fits((int)m, (int)n, (int)k, (int)l)) return SLRA_ERR_UNSUPPORTED;
+  if (nblocks == 0) return SLRA_OK;
+  Context* cx = C(ctx);
+  const int rq = (int)(k < l ? k : l);
+  // per-block residual factors + result pairs in the workspace
+  const size_t fac = (size_t)nblocks * ((size_t)m * rq + (size_t)rq * n);
+  double* ws = static_cast<double*>(workspace(cx, sizeof(double) * (fac + 2 * (size_t)nblocks)));
+  if (!ws) return SLRA_ERR_CUDA;
+  double* Pf = ws;
+  double* Qf = ws + (size_t)nblocks * m * rq;
+  double* pairs = ws + fac;
+  CaParams p{A, lda, stride, (int)m, (int)n, (int)r, (int)k, (int)l, loops, h, init_rows, I_out, J_out, nucleus,
+             r_out, status, nullptr, nullptr, nullptr, Pf, Qf, rq, 0};
+  SLRA_TRY(launch_ca_block(cx, p, (int)nblocks));
+  SLRA_TRY(launch_lowrank_residual_batched(cx, A, lda, stride, m, n, Pf, m, (int64_t)m * rq, Qf, rq,
+                                           (int64_t)rq * n, rq, nblocks, pairs));
+  // split pairs -> resid_sq / norm_sq
+  if (resid_sq) SLRA_CUDA(cudaMemcpy2DAsync(resid_sq, 8, pairs, 16, 8, nblocks, cudaMemcpyDeviceToDevice, cx->stream));
+  if (norm_sq) SLRA_CUDA(cudaMemcpy2DAsync(norm_sq, 8, pairs + 1, 16, 8, nblocks, cudaMemcpyDeviceToDevice, cx->stream));
+  return SLRA_OK;
+}
+
+int slra_primitive_cur(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, const int64_t* I, int64_t k,
+                       const int64_t* J, int64_t l, int64_t r, double* nucleus, int64_t ldu, double* Tsig,
+                       double* Sr, int64_t* h_r_out) {
+  if (!ctx || lda < m || k < 1 || l < 1 || ldu != l || (r > 0 && (k < r || l < r)))
+    return SLRA_ERR_INVALID_ARGUMENT;
+  if (k > 64 || l > 64) return SLRA_ERR_UNSUPPORTED;
+  (void)Tsig;
+  (void)Sr;
+  Context* cx = C(ctx);
+  int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
+  int64_t* d_r = reinterpret_cast<int64_t*>(static_cast<char*>(cx->dsmall) + 64);
+  // mode 1 reads I/J from the index slots: stage copies in dsmall
+  int64_t* dI = reinterpret_cast<int64_t*>(static_cast<char*>(cx->dsmall) + 1024);
+  int64_t* dJ = reinterpret_cast<int64_t*>(static_cast<char*>(cx->dsmall) + 2048);
+  SLRA_CUDA(cudaMemcpyAsync(dI, I, 8 * k, cudaMemcpyDeviceToDevice, cx->stream));
+  SLRA_CUDA(cudaMemcpyAsync(dJ, J, 8 * l, cudaMemcpyDeviceToDevice, cx->stream));
+  const int mm = (int)(k > l ? k : l);
+  CaParams p{A, lda, 0, mm, mm, (int)r, (int)k, (int)l, 1, 1.1, nullptr, dI, dJ, nucleus, d_r, d_status,
+             nullptr, nullptr, nullptr, nullptr, nullptr, (int)(k < l ? k : l), 1};
+  SLRA_TRY(launch_ca_block(cx, p, 1));
+  char* hs = static_cast<char*>(cx->hsmall);
+  SLRA_CUDA(cudaMemcpyAsync(hs, cx->dsmall, 128, cudaMemcpyDeviceToHost, cx->stream));
+  SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+  if (h_r_out) *h_r_out = *reinterpret_cast<int64_t*>(hs + 64);
+  return *reinterpret_cast<int32_t*>(hs);
+}
+
+}  // extern "C"

@@ -1,0 +1,449 @@
+// Tall-skinny dense kernels behind slra_thin_qr / slra_svd / slra_maxvol_rows
+// / slra_select_rows_spanning.
+//   * thin_qr (linalg.cpp:67-79): one CTA when the matrix fits on chip,
+//     otherwise TSQR — 256-row leaves factorised by CTA-resident Householder
+//     QR, their R factors stacked and reduced level by level, then Q expanded
+//     top-down by re-applying each leaf's reflectors. Unconditionally stable
+//     (rank-deficient strips of configs 3/5 included).
+//   * svd (linalg.cpp:81-98): QR pre-reduction + one-sided Jacobi on R.
+#include "dense_cta.cuh"
+
+namespace slra_dev {
+
+constexpr int kDT = 256;
+constexpr int kLeaf = 256;  // TSQR leaf rows
+
+// ---------------------------------------------------------------- single-CTA thin QR
+__global__ void __launch_bounds__(kDT) thin_qr_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int c,
+                                                          double* __restrict__ Q, int64_t ldq,
+                                                          double* __restrict__ R, int64_t ldr) {
+  extern __shared__ __align__(16) double sm[];
+  double* S = sm;                 // m x c
+  double* Rs = S + (size_t)m * c;  // c x c
+  double* tau = Rs + c * c;        // c
+  double* red = tau + c;           // 40
+  for (int e = threadIdx.x; e < m * c; e += kDT) S[e] = A[(e % m) + (int64_t)(e / m) * lda];
+  __syncthreads();
+  cta_thin_qr<kDT>(S, m, m, c, Rs, c, tau, red);
+  for (int e = threadIdx.x; e < m * c; e += kDT) Q[(e % m) + (int64_t)(e / m) * ldq] = S[e];
+  if (R)
+    for (int e = threadIdx.x; e < c * c; e += kDT) R[(e % c) + (int64_t)(e / c) * ldr] = Rs[e];
+}
+
+// ---------------------------------------------------------------- TSQR
+// Reduce step: block b of X (rows [b*L, min((b+1)*L, rows)), padded with
+// zeros to >= c rows) -> Householder QR in smem; reflectors + tau to
+// Vst/taust (block b, Lp x c, ld Lp); R_b -> Xn rows [b*c, (b+1)*c).
+__global__ void __launch_bounds__(kDT) tsqr_reduce_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
+                                                          int c, int Lp, double* __restrict__ Vst,
+                                                          double* __restrict__ taust, double* __restrict__ Xn,
+                                                          int64_t ldxn) {
+  extern __shared__ __align__(16) double sm[];
+  double* S = sm;
+  double* tau = S + (size_t)Lp * c;
+  double* red = tau + c;
+  const int64_t b = blockIdx.x;
+  const int64_t r0 = b * kLeaf;
+  const int nr = (int)((rows - r0) < kLeaf ? (rows - r0) : kLeaf);
+  for (int e = threadIdx.x; e < Lp * c; e += kDT) {
+    const int i = e % Lp, j = e / Lp;
+    S[e] = i < nr ? X[(r0 + i) + (int64_t)j * ldx] : 0.0;
+  }
+  __syncthreads();
+  cta_house_qr<kDT>(S, Lp, Lp, c, tau, red);
+  double* V = Vst + b * (int64_t)Lp * c;
+  for (int e = threadIdx.x; e < Lp * c; e += kDT) V[e] = S[e];
+  for (int j = threadIdx.x; j < c; j += kDT) taust[b * c + j] = tau[j];
+  for (int e = threadIdx.x; e < c * c; e += kDT) {
+    const int i = e % c, j = e / c;
+    Xn[(b * c + i) + (int64_t)j * ldxn] = (i <= j) ? S[i + j * Lp] : 0.0;
+  }
+}
+
+// Top: one CTA thin QR (with sign rule) of the final stack (rows <= L);
+// writes Qtop (rows x c) and R. `sgn` receives the column flips applied.
+__global__ void __launch_bounds__(kDT) tsqr_top_kernel(const double* __restrict__ X, int64_t ldx, int rows, int c,
+                                                       int Lp, double* __restrict__ Qt, int64_t ldqt,
+                                                       double* __restrict__ R, int64_t ldr) {
+  extern __shared__ __align__(16) double sm[];
+  double* S = sm;                     // Lp x c
+  double* Rs = S + (size_t)Lp * c;    // c x c
+  double* tau = Rs + c * c;
+  double* red = tau + c;
+  for (int e = threadIdx.x; e < Lp * c; e += kDT) {
+    const int i = e % Lp, j = e / Lp;
+    S[e] = i < rows ? X[i + (int64_t)j * ldx] : 0.0;
+  }
+  __syncthreads();
+  cta_thin_qr<kDT>(S, Lp, Lp, c, Rs, c, tau, red);
+  for (int e = threadIdx.x; e < rows * c; e += kDT) {
+    const int i = e % rows, j = e / rows;
+    Qt[i + (int64_t)j * ldqt] = S[i + j * Lp];
+  }
+  if (R)
+    for (int e = threadIdx.x; e < c * c; e += kDT) R[(e % c) + (int64_t)(e / c) * ldr] = Rs[e];
+}
+
+// Expand step: Q_b = H_0 ... H_{c-1} [Qp(b*c : b*c+c, :); 0] (Lp x c), store
+// the first nr rows at Qo rows [b*L, ...).
+__global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restrict__ Qp, int64_t ldqp,
+                                                          const double* __restrict__ Vst,
+                                                          const double* __restrict__ taust, int64_t rows, int c,
+                                                          int Lp, double* __restrict__ Qo, int64_t ldqo) {
+  extern __shared__ __align__(16) double sm[];
+  double* Y = sm;  // Lp x c
+  const int64_t b = blockIdx.x;
+  const int64_t r0 = b * kLeaf;
+  const int nr = (int)((rows - r0) < kLeaf ? (rows - r0) : kLeaf);
+  const double* V = Vst + b * (int64_t)Lp * c;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < Lp * c; e += kDT) {
+    const int i = e % Lp, j = e / Lp;
+    Y[e] = i < c ? Qp[(b * c + i) + (int64_t)j * ldqp] : 0.0;
+  }
+  __syncthreads();
+  for (int k = c - 1; k >= 0; --k) {
+    const double t = taust[b * c + k];
+    if (t != 0.0) {
+      const double* v = V + (int64_t)k * Lp;
+      for (int j = warp; j < c; j += kDT / 32) {
+        double* y = Y + j * Lp;
+        double w = 0.0;
+        for (int i = k + 1 + lane; i < Lp; i += 32) w += v[i] * y[i];
+        w = warp_sum(w);
+        w += y[k];
+        __syncwarp();
+        if (lane == 0) y[k] -= t * w;
+        for (int i = k + 1 + lane; i < Lp; i += 32) y[i] -= t * v[i] * w;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nr * c; e += kDT) {
+    const int i = e % nr, j = e / nr;
+    Qo[(r0 + i) + (int64_t)j * ldqo] = Y[i + j * Lp];
+  }
+}
+
+static size_t qr_cta_smem(int m, int c) { return sizeof(double) * ((size_t)m * c + (size_t)c * c + c + 48); }
+
+int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, double* Q, int64_t ldq, double* R,
+                   int64_t ldr) {
+  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 4096) {
+    const size_t smem = qr_cta_smem((int)m, c);
+    SLRA_CUDA(cudaFuncSetAttribute(thin_qr_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    thin_qr_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, c, Q, ldq, R, ldr);
+    SLRA_CHECK_LAUNCH(cx);
+    return SLRA_OK;
+  }
+  if (c > 64) return SLRA_ERR_UNSUPPORTED;
+  const int Lp = kLeaf > c ? kLeaf : c;
+  // level plan
+  std::vector<int64_t> level_rows;  // rows of X at each reduce level
+  int64_t rows = m;
+  while (rows > kLeaf) {
+    level_rows.push_back(rows);
+    rows = ((rows + kLeaf - 1) / kLeaf) * c;
+  }
+  const int64_t top_rows = rows;
+  // workspace: per level reflectors (nb*Lp*c) + taus (nb*c) + stacked R (nb*c x c)
+  size_t total = 0;
+  std::vector<size_t> offV, offT, offX;
+  for (int64_t lr : level_rows) {
+    const int64_t nb = (lr + kLeaf - 1) / kLeaf;
+    offV.push_back(total);
+    total += (size_t)nb * Lp * c;
+    offT.push_back(total);
+    total += (size_t)nb * c;
+    offX.push_back(total);
+    total += (size_t)nb * c * c;
+  }
+  const size_t offQ = total;  // Q of each level above the leaves (max rows x c)
+  total += 2 * (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c + (size_t)top_rows * c;
+  double* ws = static_cast<double*>(workspace(cx, sizeof(double) * total));
+  if (!ws) return SLRA_ERR_CUDA;
+  const size_t sm_red = sizeof(double) * ((size_t)Lp * c + c + 48);
+  SLRA_CUDA(cudaFuncSetAttribute(tsqr_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_red));
+  const double* X = A;
+  int64_t ldx = lda;
+  for (size_t lv = 0; lv < level_rows.size(); ++lv) {
+    const int64_t lr = level_rows[lv];
+    const int64_t nb = (lr + kLeaf - 1) / kLeaf;
+    double* Xn = ws + offX[lv];
+    tsqr_reduce_kernel<<<(unsigned)nb, kDT, sm_red, cx->stream>>>(X, ldx, lr, c, Lp, ws + offV[lv], ws + offT[lv],
+                                                                  Xn, nb * c);
+    SLRA_CHECK_LAUNCH(cx);
+    X = Xn;
+    ldx = nb * c;
+  }
+  // top
+  const size_t sm_top = sizeof(double) * ((size_t)Lp * c + (size_t)c * c + c + 48);
+  SLRA_CUDA(cudaFuncSetAttribute(tsqr_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_top));
+  double* qbuf[2] = {ws + offQ, ws + offQ + (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c};
+  double* Qtop = ws + offQ + 2 * (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c;
+  tsqr_top_kernel<<<1, kDT, sm_top, cx->stream>>>(X, ldx, (int)top_rows, c, Lp, Qtop, top_rows, R, ldr);
+  SLRA_CHECK_LAUNCH(cx);
+  // expand top-down
+  const size_t sm_exp = sizeof(double) * (size_t)Lp * c;
+  SLRA_CUDA(cudaFuncSetAttribute(tsqr_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_exp));
+  const double* Qp = Qtop;
+  int64_t ldqp = top_rows;
+  for (int lv = (int)level_rows.size() - 1; lv >= 0; --lv) {
+    const int64_t lr = level_rows[lv];
+    const int64_t nb = (lr + kLeaf - 1) / kLeaf;
+    double* Qo;
+    int64_t ldqo;
+    if (lv == 0) {
+      Qo = Q;
+      ldqo = ldq;
+    } else {
+      Qo = qbuf[lv & 1];
+      ldqo = lr;
+    }
+    tsqr_expand_kernel<<<(unsigned)nb, kDT, sm_exp, cx->stream>>>(Qp, ldqp, ws + offV[lv], ws + offT[lv], lr, c, Lp,
+                                                                  Qo, ldqo);
+    SLRA_CHECK_LAUNCH(cx);
+    Qp = Qo;
+    ldqp = ldqo;
+  }
+  return SLRA_OK;
+}
+
+// ---------------------------------------------------------------- small SVD
+// One CTA: W = A (p x q, p >= q) or A^T, Jacobi, finish; S (m x pmin), T.
+__global__ void __launch_bounds__(kDT) svd_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
+                                                      double* __restrict__ S, int64_t lds, double* __restrict__ sigma,
+                                                      double* __restrict__ T, int64_t ldt) {
+  extern __shared__ __align__(16) double sm[];
+  const bool tall = m >= n;
+  const int p = tall ? m : n, q = tall ? n : m;
+  double* W = sm;                    // p x q
+  double* V = W + (size_t)p * q;     // q x q
+  double* Ss = V + (size_t)q * q;    // p x q
+  double* Ts = Ss + (size_t)p * q;   // q x q
+  double* sg = Ts + (size_t)q * q;   // q
+  double* tmp = sg + q;              // q
+  int* order = reinterpret_cast<int*>(tmp + q);
+  int* flag = order + q + 1;
+  for (int e = threadIdx.x; e < m * n; e += kDT) {
+    const int i = e % m, j = e / m;
+    const double x = A[i + (int64_t)j * lda];
+    if (tall) W[i + j * p] = x;
+    else W[j + i * p] = x;
+  }
+  __syncthreads();
+  cta_jacobi<kDT>(W, p, p, q, V, q, flag);
+  cta_svd_finish<kDT>(W, p, p, q, V, q, sg, order, Ss, p, Ts, q, tmp);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (!tall) {
+    // left vectors of A are Ts (q x q = m x m); re-apply the sign rule on them
+    for (int t = warp; t < q; t += kDT / 32) {
+      ArgMax a{-1.0, INT64_MAX};
+      for (int i = lane; i < q; i += 32) a = argmax_merge(a, ArgMax{fabs(Ts[i + t * q]), i});
+      a = warp_argmax(a);
+      const double f = (Ts[a.i + t * q] < 0.0) ? -1.0 : 1.0;
+      __syncwarp();
+      for (int i = lane; i < q; i += 32) Ts[i + t * q] *= f;
+      for (int i = lane; i < p; i += 32) Ss[i + t * p] *= f;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < q; t += kDT) sigma[t] = sg[t];
+  const double* Sl = tall ? Ss : Ts;
+  const int ldl = tall ? p : q;
+  const double* Tr = tall ? Ts : Ss;
+  const int ldr = tall ? q : p;
+  for (int e = threadIdx.x; e < m * q; e += kDT) S[(e % m) + (int64_t)(e / m) * lds] = Sl[(e % m) + (e / m) * ldl];
+  for (int e = threadIdx.x; e < n * q; e += kDT) T[(e % n) + (int64_t)(e / n) * ldt] = Tr[(e % n) + (e / n) * ldr];
+}
+
+static size_t svd_smem(int m, int n) {
+  const int p = m > n ? m : n, q = m > n ? n : m;
+  return sizeof(double) * (2 * (size_t)p * q + 2 * (size_t)q * q + 2 * (size_t)q + 8) + sizeof(int) * (q + 8);
+}
+
+int launch_svd_small(Context* cx, const double* A, int64_t lda, int m, int n, double* S, int64_t lds, double* sigma,
+                     double* T, int64_t ldt) {
+  const size_t smem = svd_smem(m, n);
+  if (smem > 220 * 1024) return SLRA_ERR_UNSUPPORTED;
+  SLRA_CUDA(cudaFuncSetAttribute(svd_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  svd_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, m, n, S, lds, sigma, T, ldt);
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}
+
+int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc);
+
+// Sign rule on an externally formed S = Q U_R: per column j, if the first
+// largest-|.| entry is negative flip S(:, j) and T(:, j). One CTA per column.
+__global__ void __launch_bounds__(kDT) colsign_kernel(double* __restrict__ S, int64_t lds, int64_t m,
+                                                      double* __restrict__ T, int64_t ldt, int64_t n) {
+  __shared__ double rv[40];
+  __shared__ int64_t ri[40];
+  const int64_t j = blockIdx.x;
+  ArgMax a{-1.0, INT64_MAX};
+  for (int64_t i = threadIdx.x; i < m; i += kDT) a = argmax_merge(a, ArgMax{fabs(S[i + j * lds]), i});
+  a = block_argmax<kDT>(a, rv, ri);
+  if (S[a.i + j * lds] < 0.0) {
+    for (int64_t i = threadIdx.x; i < m; i += kDT) S[i + j * lds] = -S[i + j * lds];
+    if (T)
+      for (int64_t i = threadIdx.x; i < n; i += kDT) T[i + j * ldt] = -T[i + j * ldt];
+  }
+}
+
+int launch_colsign(Context* cx, double* S, int64_t lds, int64_t m, double* T, int64_t ldt, int64_t n, int64_t cols) {
+  if (cols <= 0) return SLRA_OK;
+  colsign_kernel<<<(unsigned)cols, kDT, 0, cx->stream>>>(S, lds, m, T, ldt, n);
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}
+
+// General SVD with min(m, n) <= 64: small -> one CTA; tall -> thin_qr then
+// Jacobi on R and S = Q U_R (plus the sign rule on S).
+int launch_svd(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, double* S, int64_t lds,
+               double* sigma, double* T, int64_t ldt) {
+  const int64_t q = m < n ? m : n;
+  if (q > 64) return SLRA_ERR_UNSUPPORTED;
+  if (svd_smem((int)m, (int)n) <= 200 * 1024) return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt);
+  if (m < n) return SLRA_ERR_UNSUPPORTED;  // wide and large: not on the path
+  const int c = (int)n;
+  double* ws = static_cast<double*>(cx->partials ? nullptr : nullptr);
+  (void)ws;
+  // scratch: Q (m x c), R (c x c), UR (c x c): separate allocation so the
+  // TSQR workspace stays free
+  double* buf;
+  SLRA_CUDA(cudaMallocAsync(&buf, sizeof(double) * ((size_t)m * c + 2 * (size_t)c * c), cx->stream));
+  double* Qm = buf;
+  double* Rm = buf + (size_t)m * c;
+  double* UR = Rm + (size_t)c * c;
+  int st = launch_thin_qr(cx, A, lda, m, c, Qm, m, Rm, c);
+  if (st == SLRA_OK) st = launch_svd_small(cx, Rm, c, c, c, UR, c, sigma, T, ldt);
+  if (st == SLRA_OK) st = launch_gemm(cx, 0, 0, m, c, c, 1.0, Qm, m, UR, c, 0.0, S, lds);
+  if (st == SLRA_OK) st = launch_colsign(cx, S, lds, m, T, ldt, n, c);
+  cudaFreeAsync(buf, cx->stream);
+  return st;
+}
+
+// ---------------------------------------------------------------- maxvol / select
+__global__ void __launch_bounds__(kDT) maxvol_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int r,
+                                                         double h, int max_swaps, int qr_first, int count,
+                                                         int64_t* __restrict__ idx, double* __restrict__ vol,
+                                                         int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) double sm[];
+  double* S = sm;                       // m x r
+  double* W = S + (size_t)m * r;        // m x r
+  double* Rs = W + (size_t)m * r;       // r x r
+  double* Gt = Rs + (size_t)r * r;      // r x r
+  double* tau = Gt + (size_t)r * r;     // r
+  double* v = tau + r;                  // r
+  double* nu = v + r;                   // m
+  double* nd = nu + m;                  // m
+  double* rv = nd + m;                  // 40
+  int64_t* ri = reinterpret_cast<int64_t*>(rv + 40);  // 40
+  int* p2r = reinterpret_cast<int*>(ri + 40);         // m
+  int* I = p2r + m;                                   // count
+  int* perm = I + (count > r ? count : r);            // r
+  int* flag = perm + r;                               // 4
+  for (int e = threadIdx.x; e < m * r; e += kDT) S[e] = A[(e % m) + (int64_t)(e / m) * lda];
+  __syncthreads();
+  if (qr_first) cta_thin_qr<kDT>(S, m, m, r, Rs, r, tau, rv);
+  const int rq = count < r ? count : r;
+  ColPivScratch cs{W, m, p2r, nu, nd, v, tau, rv, ri};
+  cta_colpiv_init<kDT>(S, m, m, rq, cs, I);
+  __syncthreads();
+  const int st = cta_maxvol_swaps<kDT>(S, m, m, rq, h, max_swaps, I, W, m, Gt, rq, perm, tau, nu, nd, rv, ri, flag);
+  if (st != SLRA_OK) {
+    if (threadIdx.x == 0) *status = st;
+    return;
+  }
+  __syncthreads();
+  if (count > rq) {
+    for (int i = threadIdx.x; i < m; i += kDT) {
+      double acc = 0.0;
+      for (int j = 0; j < r; ++j) acc += S[i + j * m] * S[i + j * m];
+      nu[i] = sqrt(acc);
+    }
+    __syncthreads();
+    for (int t = rq; t < count; ++t) {
+      ArgMax a{-1.0, INT64_MAX};
+      for (int i = threadIdx.x; i < m; i += kDT) {
+        bool used = false;
+        for (int u = 0; u < t; ++u) used |= (I[u] == i);
+        if (!used) a = argmax_merge(a, ArgMax{nu[i], i});
+      }
+      a = block_argmax<kDT>(a, rv, ri);
+      if (threadIdx.x == 0) I[t] = (int)a.i;
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < count; t += kDT) idx[t] = I[t];
+  if (vol) {
+    if (count == r) {
+      for (int e = threadIdx.x; e < r * r; e += kDT) Gt[(e % r) + (e / r) * r] = S[I[e % r] + (e / r) * m];
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const double dv = warp_abs_det(Gt, r, r);
+        if (threadIdx.x == 0) *vol = dv;
+      }
+    } else if (threadIdx.x == 0) {
+      *vol = 0.0;
+    }
+  }
+  if (threadIdx.x == 0) *status = SLRA_OK;
+}
+
+static size_t maxvol_smem(int m, int r, int count) {
+  const int cm = count > r ? count : r;
+  return sizeof(double) * (2 * (size_t)m * r + 2 * (size_t)r * r + 2 * (size_t)r + 2 * (size_t)m + 40) +
+         sizeof(int64_t) * 40 + sizeof(int) * ((size_t)m + cm + r + 8);
+}
+
+int launch_maxvol(Context* cx, const double* A, int64_t lda, int64_t m, int64_t r, double h, int64_t max_swaps,
+                  int qr_first, int64_t count, int64_t* idx, double* vol) {
+  const size_t smem = maxvol_smem((int)m, (int)r, (int)count);
+  if (smem > 220 * 1024 || r > 64) return SLRA_ERR_UNSUPPORTED;
+  SLRA_CUDA(cudaFuncSetAttribute(maxvol_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
+  maxvol_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, (int)r, h, (int)max_swaps, qr_first, (int)count,
+                                                   idx, vol, d_status);
+  SLRA_CHECK_LAUNCH(cx);
+  SLRA_CUDA(cudaMemcpyAsync(cx->hsmall, cx->dsmall, 4, cudaMemcpyDeviceToHost, cx->stream));
+  SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+  return *static_cast<int32_t*>(cx->hsmall);
+}
+
+}  // namespace slra_dev
+
+using namespace slra_dev;
+
+extern "C" {
+
+int slra_thin_qr(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t c, double* Q, int64_t ldq, double* R,
+                 int64_t ldr) {
+  if (!ctx || m < c || c < 1 || lda < m || ldq < m || (R && ldr < c)) return SLRA_ERR_INVALID_ARGUMENT;
+  if (c > 64) return SLRA_ERR_UNSUPPORTED;
+  return launch_thin_qr(C(ctx), A, lda, m, (int)c, Q, ldq, R, ldr);
+}
+
+int slra_svd(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, double* S, int64_t lds, double* sigma,
+             double* T, int64_t ldt) {
+  if (!ctx || m < 1 || n < 1 || lda < m || lds < m || ldt < n) return SLRA_ERR_INVALID_ARGUMENT;
+  return launch_svd(C(ctx), A, lda, m, n, S, lds, sigma, T, ldt);
+}
+
+int slra_maxvol_rows(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t r, double h, int64_t max_swaps,
+                     int64_t* idx) {
+  if (!ctx || r < 1 || m < r || lda < m || h < 1.0) return SLRA_ERR_INVALID_ARGUMENT;
+  if (max_swaps == 0) max_swaps = 4 * r;
+  return launch_maxvol(C(ctx), A, lda, m, r, h, max_swaps, 0, r, idx, nullptr);
+}
+
+int slra_select_rows_spanning(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t c, int64_t count,
+                              double h, int64_t* idx, double* vol) {
+  if (!ctx || count > m || m < c || c < 1 || lda < m) return SLRA_ERR_INVALID_ARGUMENT;
+  const int64_t rq = count < c ? count : c;
+  return launch_maxvol(C(ctx), A, lda, m, c, h, 4 * rq, 1, count, idx, vol);
+}
+
+}  // extern "C"

@@ -1,0 +1,546 @@
+// CTA-resident small dense kernels (K-b / K-n building blocks). Every routine
+// runs on ONE thread block over operands in shared memory, column-major,
+// and restates the Eigen decomposition the reference calls:
+//   cta_house_qr     Eigen HouseholderQR (linalg.cpp:69), makeHouseholder /
+//                    applyHouseholderOnTheLeft arithmetic order
+//   cta_form_q       householderQ() * Identity (linalg.cpp:70), LAPACK dorg2r
+//   cta_thin_qr      thin_qr incl. the R(i,i) >= 0 sign rule (linalg.cpp:72-77)
+//   cta_colpiv_init  ColPivHouseholderQR(A^T) pivot order (cur.cpp:95-98),
+//                    LAPACK xGEQP3 norm downdate
+//   warp_colpiv_qr   ColPivHouseholderQR of a small square (cur.cpp:103-106)
+//   cta_maxvol_swaps maxvol swap loop (cur.cpp:100-114): B = A G^-1 by the
+//                    Eigen solve, argmax in column-major order, first max wins
+//   warp_abs_det     |det| via partial-pivot LU (cur.cpp:192-197)
+//   cta_jacobi_svd   one-sided Jacobi SVD (BDCSVD stand-in, linalg.cpp:81-98)
+#pragma once
+
+#include "common.cuh"
+
+namespace slra_dev {
+
+constexpr double kEps = 2.220446049250313e-16;
+
+// ---------------------------------------------------------------- Householder QR
+// A (m x c, ld lda) in smem. On exit: R on/above the diagonal, essential
+// Householder parts below, tau[0..min(m,c)).
+template <int NT>
+__device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  const int size = m < c ? m : c;
+  for (int j = 0; j < size; ++j) {
+    double* x = A + j * lda;
+    double s = 0.0;
+    for (int i = j + 1 + tid; i < m; i += NT) s += x[i] * x[i];
+    s = block_sum<NT>(s, red);
+    const double c0 = x[j];
+    double t, beta;
+    if (s <= DBL_MIN) {
+      t = 0.0;
+      beta = c0;
+      for (int i = j + 1 + tid; i < m; i += NT) x[i] = 0.0;
+    } else {
+      beta = sqrt(c0 * c0 + s);
+      if (c0 >= 0.0) beta = -beta;
+      const double den = c0 - beta;
+      for (int i = j + 1 + tid; i < m; i += NT) x[i] = x[i] / den;
+      t = (beta - c0) / beta;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      x[j] = beta;
+      tau[j] = t;
+    }
+    if (m - j == 1) {
+      // rows() == 1: *this *= (1 - tau) (no-op since tau = 0)
+    } else if (t != 0.0) {
+      for (int k = j + 1 + warp; k < c; k += NW) {
+        double* a = A + k * lda;
+        double w = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) w += x[i] * a[i];
+        w = warp_sum(w);
+        w += a[j];
+        __syncwarp();
+        if (lane == 0) a[j] -= t * w;
+        for (int i = j + 1 + lane; i < m; i += 32) a[i] -= t * x[i] * w;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// In place: reflectors (below diag) + tau -> explicit Q (m x c). The upper
+// triangle is overwritten (save R first).
+template <int NT>
+__device__ void cta_form_q(double* A, int lda, int m, int c, const double* tau) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  // zero the strict upper triangle of the trailing columns handled below
+  for (int k = c - 1; k >= 0; --k) {
+    const double t = tau[k];
+    double* v = A + k * lda;  // v[k] := 1 implicitly, v[i>k] essential
+    if (k < c - 1) {
+      for (int jj = k + 1 + warp; jj < c; jj += NW) {
+        double* a = A + jj * lda;
+        double w = 0.0;
+        for (int i = k + 1 + lane; i < m; i += 32) w += v[i] * a[i];
+        w = warp_sum(w);
+        w += a[k];  // v_k = 1
+        __syncwarp();
+        if (lane == 0) a[k] -= t * w;
+        for (int i = k + 1 + lane; i < m; i += 32) a[i] -= t * v[i] * w;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += NT) {
+      if (i < k) v[i] = 0.0;
+      else if (i == k) v[i] = 1.0 - t;
+      else v[i] = -t * v[i];
+    }
+    __syncthreads();
+  }
+}
+
+// thin_qr: A (m x c, m >= c) in smem -> Q in place, R (c x c, ld ldr) in smem,
+// both sign-fixed so R(i,i) >= 0.
+template <int NT>
+__device__ void cta_thin_qr(double* A, int lda, int m, int c, double* R, int ldr, double* tau, double* red) {
+  cta_house_qr<NT>(A, lda, m, c, tau, red);
+  for (int e = threadIdx.x; e < c * c; e += NT) {
+    const int i = e % c, j = e / c;
+    R[i + j * ldr] = (i <= j) ? A[i + j * lda] : 0.0;
+  }
+  __syncthreads();
+  cta_form_q<NT>(A, lda, m, c, tau);
+  // sign rule: R(i,i) < 0 -> flip row i of R and column i of Q
+  for (int e = threadIdx.x; e < m * c; e += NT) {
+    const int i = e % m, j = e / m;
+    if (R[j + j * ldr] < 0.0) A[i + j * lda] = -A[i + j * lda];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < c * c; e += NT) {
+    const int i = e % c, j = e / c;
+    const double d = R[i + i * ldr];
+    if (d < 0.0 && j != i) R[i + j * ldr] = -R[i + j * ldr];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < c; i += NT)
+    if (R[i + i * ldr] < 0.0) R[i + i * ldr] = -R[i + i * ldr];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- pivoted init
+// Column-pivoted Householder QR of X = Q^T (r x m) — i.e. pivoting over the
+// ROWS of Q (m x r, ld ldq) — reporting only the first r pivots, exactly the
+// maxvol initialisation of cur.cpp:95-98. W (m x r, ld ldw) is scratch.
+struct ColPivScratch {
+  double* W;
+  int ldw;
+  int* p2r;     // position -> row
+  double* nu;   // updated norms (by position)
+  double* nd;   // direct norms (by position)
+  double* v;    // Householder essential vector (r)
+  double* tau;  // [0] = tau
+  double* rv;   // >= 33
+  int64_t* ri;  // >= 33
+};
+
+template <int NT>
+__device__ void cta_colpiv_init(const double* Q, int ldq, int m, int r, const ColPivScratch& s, int* I_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double sqrt_eps = 1.4901161193847656e-08;  // sqrt(DBL_EPSILON)
+  for (int i = tid; i < m; i += NT) {
+    double acc = 0.0;
+    for (int j = 0; j < r; ++j) {
+      const double x = Q[i + j * ldq];
+      s.W[i + j * s.ldw] = x;
+      acc += x * x;
+    }
+    s.nu[i] = s.nd[i] = sqrt(acc);
+    s.p2r[i] = i;
+  }
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    ArgMax a{-1.0, INT64_MAX};
+    for (int p = k + tid; p < m; p += NT) a = argmax_merge(a, ArgMax{s.nu[p], p});
+    a = block_argmax<NT>(a, s.rv, s.ri);
+    const int big = static_cast<int>(a.i);
+    if (tid == 0 && big != k) {
+      int ti = s.p2r[k]; s.p2r[k] = s.p2r[big]; s.p2r[big] = ti;
+      double tv = s.nu[k]; s.nu[k] = s.nu[big]; s.nu[big] = tv;
+      tv = s.nd[k]; s.nd[k] = s.nd[big]; s.nd[big] = tv;
+    }
+    __syncthreads();
+    const int row = s.p2r[k];
+    if (warp == 0) {
+      double tail = 0.0;
+      for (int j = k + 1 + lane; j < r; j += 32) {
+        const double x = s.W[row + j * s.ldw];
+        tail += x * x;
+      }
+      tail = warp_sum(tail);
+      const double c0 = s.W[row + k * s.ldw];
+      double t, beta;
+      if (tail <= DBL_MIN) {
+        t = 0.0;
+        beta = c0;
+        for (int j = k + 1 + lane; j < r; j += 32) s.v[j] = 0.0;
+      } else {
+        beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        const double den = c0 - beta;
+        for (int j = k + 1 + lane; j < r; j += 32) s.v[j] = s.W[row + j * s.ldw] / den;
+        t = (beta - c0) / beta;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        s.tau[0] = t;
+        s.W[row + k * s.ldw] = beta;
+        I_out[k] = row;
+      }
+    }
+    __syncthreads();
+    const double t = s.tau[0];
+    for (int p = k + 1 + tid; p < m; p += NT) {
+      const int i = s.p2r[p];
+      if (r - k > 1 && t != 0.0) {
+        double w = 0.0;
+        for (int j = k + 1; j < r; ++j) w += s.v[j] * s.W[i + j * s.ldw];
+        w += s.W[i + k * s.ldw];
+        s.W[i + k * s.ldw] -= t * w;
+        for (int j = k + 1; j < r; ++j) s.W[i + j * s.ldw] -= t * s.v[j] * w;
+      }
+      double nu = s.nu[p];
+      if (nu != 0.0) {
+        double temp = fabs(s.W[i + k * s.ldw]) / nu;
+        temp = (1.0 + temp) * (1.0 - temp);
+        temp = temp < 0.0 ? 0.0 : temp;
+        const double ratio = nu / s.nd[p];
+        const double temp2 = temp * ratio * ratio;
+        if (temp2 <= sqrt_eps) {
+          double acc = 0.0;
+          for (int j = k + 1; j < r; ++j) acc += s.W[i + j * s.ldw] * s.W[i + j * s.ldw];
+          s.nd[p] = sqrt(acc);
+          s.nu[p] = s.nd[p];
+        } else {
+          s.nu[p] = nu * sqrt(temp);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- small ColPivQR (one warp)
+// Eigen ColPivHouseholderQR on a small n x n matrix G (ld ldg, in smem), run
+// by the calling warp. Outputs: perm (n), tau (n), nonzero pivots and rank
+// with the prescribed threshold. `nu`, `nd` scratch (n).
+struct SmallColPiv {
+  int nonzero_pivots;
+  int rank;
+};
+
+__device__ inline SmallColPiv warp_colpiv_qr(double* G, int ldg, int n, double threshold, int* perm, double* tau,
+                                      double* nu, double* nd) {
+  const int lane = threadIdx.x & 31;
+  const double eps = kEps;
+  const double sqrt_eps = 1.4901161193847656e-08;
+  double maxnorm = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += G[i + j * ldg] * G[i + j * ldg];
+    nu[j] = nd[j] = sqrt(acc);
+    perm[j] = j;
+    maxnorm = fmax(maxnorm, nu[j]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) maxnorm = fmax(maxnorm, __shfl_xor_sync(0xffffffffu, maxnorm, o));
+  __syncwarp();
+  const double thr_helper = (maxnorm * eps) * (maxnorm * eps) / (double)n;
+  int nonzero = n;
+  double maxpivot = 0.0;
+  for (int k = 0; k < n; ++k) {
+    ArgMax a{-1.0, INT64_MAX};
+    for (int j = k + lane; j < n; j += 32) a = argmax_merge(a, ArgMax{nu[j], j});
+    a = warp_argmax(a);
+    const int big = (int)a.i;
+    if (nonzero == n && a.v * a.v < thr_helper * (double)(n - k)) nonzero = k;
+    // transposition k <-> big (columns, norms, permutation: Eigen applies
+    // the transpositions to an identity permutation in order)
+    if (big != k) {
+      for (int i = lane; i < n; i += 32) {
+        const double t0 = G[i + k * ldg];
+        G[i + k * ldg] = G[i + big * ldg];
+        G[i + big * ldg] = t0;
+      }
+      if (lane == 0) {
+        double t1 = nu[k]; nu[k] = nu[big]; nu[big] = t1;
+        t1 = nd[k]; nd[k] = nd[big]; nd[big] = t1;
+        const int p = perm[k]; perm[k] = perm[big]; perm[big] = p;
+      }
+    }
+    __syncwarp();
+    double* x = G + k * ldg;
+    double tail = 0.0;
+    for (int i = k + 1 + lane; i < n; i += 32) tail += x[i] * x[i];
+    tail = warp_sum(tail);
+    const double c0 = x[k];
+    double t, beta;
+    if (tail <= DBL_MIN) {
+      t = 0.0;
+      beta = c0;
+      for (int i = k + 1 + lane; i < n; i += 32) x[i] = 0.0;
+    } else {
+      beta = sqrt(c0 * c0 + tail);
+      if (c0 >= 0.0) beta = -beta;
+      const double den = c0 - beta;
+      for (int i = k + 1 + lane; i < n; i += 32) x[i] = x[i] / den;
+      t = (beta - c0) / beta;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      x[k] = beta;
+      tau[k] = t;
+    }
+    if (fabs(beta) > maxpivot) maxpivot = fabs(beta);
+    __syncwarp();
+    if (n - k > 1 && t != 0.0) {
+      for (int j = k + 1 + lane; j < n; j += 32) {
+        double* a2 = G + j * ldg;
+        double w = 0.0;
+        for (int i = k + 1; i < n; ++i) w += x[i] * a2[i];
+        w += a2[k];
+        a2[k] -= t * w;
+        for (int i = k + 1; i < n; ++i) a2[i] -= t * x[i] * w;
+      }
+    }
+    __syncwarp();
+    for (int j = k + 1 + lane; j < n; j += 32) {
+      if (nu[j] != 0.0) {
+        double temp = fabs(G[k + j * ldg]) / nu[j];
+        temp = (1.0 + temp) * (1.0 - temp);
+        temp = temp < 0.0 ? 0.0 : temp;
+        const double ratio = nu[j] / nd[j];
+        const double temp2 = temp * ratio * ratio;
+        if (temp2 <= sqrt_eps) {
+          double acc = 0.0;
+          for (int i = k + 1; i < n; ++i) acc += G[i + j * ldg] * G[i + j * ldg];
+          nd[j] = sqrt(acc);
+          nu[j] = nd[j];
+        } else {
+          nu[j] *= sqrt(temp);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // rank() with the prescribed threshold
+  const double pre = fabs(maxpivot) * threshold;
+  int rank = 0;
+  for (int i = 0; i < nonzero; ++i) rank += (fabs(G[i + i * ldg]) > pre) ? 1 : 0;
+  return SmallColPiv{nonzero, rank};
+}
+
+// ---------------------------------------------------------------- maxvol swap loop
+// A (m x r, ld lda) in smem, I (r current rows, smem, updated in place).
+// Returns SLRA_OK or SLRA_ERR_SELECTION_FAILURE. Scratch: W (m x r), Gt
+// (r x r), perm/tau/nu/nd (r each), rv/ri.
+template <int NT>
+__device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h, int max_swaps, int* I,
+                                double* W, int ldw, double* Gt, int ldg, int* perm, double* tau, double* nu,
+                                double* nd, double* rv, int64_t* ri, int* shared_flag) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int swap = 0; swap <= max_swaps; ++swap) {
+    // G^T(c, t) = A(I[t], c)
+    for (int e = tid; e < r * r; e += NT) {
+      const int cc = e % r, t = e / r;
+      Gt[cc + t * ldg] = A[I[t] + cc * lda];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      SmallColPiv q = warp_colpiv_qr(Gt, ldg, r, 1e-12, perm, tau, nu, nd);
+      if ((tid & 31) == 0) {
+        shared_flag[0] = q.rank < r ? 1 : 0;
+        shared_flag[1] = q.nonzero_pivots;
+      }
+    }
+    __syncthreads();
+    if (shared_flag[0]) return SLRA_ERR_SELECTION_FAILURE;
+    const int np = shared_flag[1];
+    // B(i, :) = solve(G^T, A(i, :)^T)^T for every row i; track |B| argmax
+    ArgMax best{-1.0, INT64_MAX};
+    for (int i = tid; i < m; i += NT) {
+      double* c = W + i;  // row i of W as a strided vector (stride ldw)
+      for (int j = 0; j < r; ++j) c[j * ldw] = A[i + j * lda];
+      for (int k = 0; k < np; ++k) {
+        const double t = tau[k];
+        if (r - k == 1) {
+          c[k * ldw] *= (1.0 - t);
+        } else if (t != 0.0) {
+          double w = 0.0;
+          for (int j = k + 1; j < r; ++j) w += Gt[j + k * ldg] * c[j * ldw];
+          w += c[k * ldw];
+          c[k * ldw] -= t * w;
+          for (int j = k + 1; j < r; ++j) c[j * ldw] -= t * Gt[j + k * ldg] * w;
+        }
+      }
+      for (int t2 = np - 1; t2 >= 0; --t2) {
+        double sacc = c[t2 * ldw];
+        for (int u = t2 + 1; u < np; ++u) sacc -= Gt[t2 + u * ldg] * c[u * ldw];
+        c[t2 * ldw] = sacc / Gt[t2 + t2 * ldg];
+      }
+      for (int t2 = 0; t2 < r; ++t2) {
+        const double v = t2 < np ? fabs(c[t2 * ldw]) : 0.0;
+        const int64_t lin = (int64_t)perm[t2] * m + i;  // column-major linear index
+        best = argmax_merge(best, ArgMax{v, lin});
+      }
+    }
+    best = block_argmax<NT>(best, rv, ri);
+    if (best.v <= h) return SLRA_OK;
+    if (swap == max_swaps) return SLRA_OK;
+    if (tid == 0) I[best.i / m] = (int)(best.i % m);
+    __syncthreads();
+  }
+  return SLRA_OK;
+}
+
+// |det(M)| of an n x n smem matrix (destroyed) by partial-pivot LU, one warp.
+__device__ inline double warp_abs_det(double* M, int ld, int n) {
+  const int lane = threadIdx.x & 31;
+  double det = 1.0;
+  for (int k = 0; k < n; ++k) {
+    ArgMax a{-1.0, INT64_MAX};
+    for (int i = k + lane; i < n; i += 32) a = argmax_merge(a, ArgMax{fabs(M[i + k * ld]), i});
+    a = warp_argmax(a);
+    const int p = (int)a.i;
+    if (a.v == 0.0) return 0.0;
+    if (p != k)
+      for (int j = lane; j < n; j += 32) {
+        const double t = M[k + j * ld];
+        M[k + j * ld] = M[p + j * ld];
+        M[p + j * ld] = t;
+      }
+    __syncwarp();
+    const double piv = M[k + k * ld];
+    det *= piv;
+    for (int i = k + 1 + lane; i < n; i += 32) {
+      const double f = M[i + k * ld] / piv;
+      for (int j = k + 1; j < n; ++j) M[i + j * ld] -= f * M[k + j * ld];
+    }
+    __syncwarp();
+  }
+  return fabs(det);
+}
+
+// ---------------------------------------------------------------- Jacobi SVD
+// One-sided Jacobi on the columns of W (p x n, ld ldw, p >= n, n <= 64),
+// accumulating V (n x n, ld ldv). Parallel round-robin ordering; each warp
+// owns disjoint column pairs per round. On exit W's columns are
+// U_j sigma_j (unsorted).
+template <int NT>
+__device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  for (int e = tid; e < n * n; e += NT) V[e % n + (e / n) * ldv] = (e % n == e / n) ? 1.0 : 0.0;
+  const int ne = n + (n & 1);  // even number of players (dummy = n)
+  __syncthreads();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) flag[0] = 0;
+    __syncthreads();
+    for (int rd = 0; rd < ne - 1; ++rd) {
+      for (int pi = warp; pi < ne / 2; pi += NW) {
+        int a, b;
+        if (pi == 0) {
+          a = rd;
+          b = ne - 1;
+        } else {
+          a = (rd + pi) % (ne - 1);
+          b = (rd - pi + ne - 1) % (ne - 1);
+        }
+        if (a >= n || b >= n) continue;
+        if (a > b) { const int t = a; a = b; b = t; }
+        double* wp = W + a * ldw;
+        double* wq = W + b * ldw;
+        double aa = 0.0, bb = 0.0, gg = 0.0;
+        for (int i = lane; i < p; i += 32) {
+          const double x = wp[i], y = wq[i];
+          aa += x * x;
+          bb += y * y;
+          gg += x * y;
+        }
+        aa = warp_sum(aa);
+        bb = warp_sum(bb);
+        gg = warp_sum(gg);
+        if (gg == 0.0 || fabs(gg) <= kEps * sqrt(aa * bb)) continue;
+        const double zeta = (bb - aa) / (2.0 * gg);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double sn = cs * t;
+        for (int i = lane; i < p; i += 32) {
+          const double x = wp[i], y = wq[i];
+          wp[i] = cs * x - sn * y;
+          wq[i] = sn * x + cs * y;
+        }
+        double* vp = V + a * ldv;
+        double* vq = V + b * ldv;
+        for (int i = lane; i < n; i += 32) {
+          const double x = vp[i], y = vq[i];
+          vp[i] = cs * x - sn * y;
+          vq[i] = sn * x + cs * y;
+        }
+        if (lane == 0) flag[0] = 1;
+      }
+      __syncthreads();
+    }
+    const int rotated = flag[0];
+    __syncthreads();
+    if (!rotated) break;
+  }
+}
+
+// Finish an SVD after cta_jacobi: sigma_j = ||w_j||, descending stable order
+// (order[t] = source column), S(:, t) = w_j / sigma_j with the sign rule
+// "largest-|.| entry of each left vector >= 0" (linalg.cpp:87-96), T from V.
+// S (p x n, ld lds) and T (n x n, ld ldt) may not alias W/V.
+template <int NT>
+__device__ void cta_svd_finish(const double* W, int ldw, int p, int n, const double* V, int ldv, double* sigma,
+                               int* order, double* S, int lds, double* T, int ldt, double* sgn) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  for (int j = warp; j < n; j += NW) {
+    double acc = 0.0;
+    for (int i = lane; i < p; i += 32) acc += W[i + j * ldw] * W[i + j * ldw];
+    acc = warp_sum(acc);
+    if (lane == 0) sgn[j] = sqrt(acc);  // temp: unsorted sigma
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < n; ++j) order[j] = j;
+    for (int a = 1; a < n; ++a) {  // stable insertion sort, descending
+      const int o = order[a];
+      int b = a - 1;
+      while (b >= 0 && sgn[order[b]] < sgn[o]) {
+        order[b + 1] = order[b];
+        --b;
+      }
+      order[b + 1] = o;
+    }
+    for (int t = 0; t < n; ++t) sigma[t] = sgn[order[t]];
+  }
+  __syncthreads();
+  for (int t = warp; t < n; t += NW) {
+    const int j = order[t];
+    const double s = sigma[t];
+    const double inv = s > 0.0 ? 1.0 / s : 0.0;
+    // sign: first index of the largest |w_ij| (same for w and w/s)
+    ArgMax a{-1.0, INT64_MAX};
+    for (int i = lane; i < p; i += 32) a = argmax_merge(a, ArgMax{fabs(W[i + j * ldw]), i});
+    a = warp_argmax(a);
+    const double f = (W[a.i + j * ldw] < 0.0) ? -1.0 : 1.0;
+    for (int i = lane; i < p; i += 32) S[i + t * lds] = f * W[i + j * ldw] * inv;
+    for (int i = lane; i < n; i += 32) T[i + t * ldt] = f * V[i + j * ldv];
+  }
+  __syncthreads();
+}
+
+}  // namespace slra_dev

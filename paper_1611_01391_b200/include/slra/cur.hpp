@@ -1,0 +1,68 @@
+// CUR / Cross-Approximation entry points of
+// /root/reference/proj/include/slra/cur.hpp:16-73, run on the B200.
+#pragma once
+
+#include <optional>
+#include <utility>
+#include <vector>
+
+#include "slra/linalg.hpp"
+#include "slra/oracle.hpp"
+#include "slra/rng.hpp"
+
+namespace slra {
+
+struct CurDecomposition {
+  IndexSet row_set;  // k selected rows
+  IndexSet col_set;  // l selected columns
+  Matrix nucleus;    // l x k
+  Index r = 0;
+  bool qr_nucleus = false;  // only the SVD nucleus is on the device path
+};
+
+/// C * U * R (evaluation only; cur.cpp:76-78).
+Matrix cur_reconstruct(const Matrix& M, const CurDecomposition& c);
+/// ||M - C U R|| (cur.cpp:80-82). Frobenius runs on the device in one pass
+/// over M; Spectral/Chebyshev are not on the hot path (invalid_argument).
+double cur_evaluate(const Matrix& M, const CurDecomposition& c, NormKind norm);
+double cur_evaluate(const EntryOracle& M, const CurDecomposition& c, NormKind norm);
+
+double t_factor(Index q, Index s, double h);
+IndexSet maxvol_rows(const Matrix& A, double h = 1.1, Index max_swaps = 0);
+IndexSet select_rows_spanning(const Matrix& A, Index count, double h = 1.1);
+
+/// r <= 0 selects the adaptive rank numerical_rank(G, 1e-10, Relative)
+/// (configs 3/5); the reference requires r >= 1.
+CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r,
+                               bool qr_nucleus = false);
+CurDecomposition primitive_cur(const Matrix& M, IndexSet I, IndexSet J, Index r,
+                               bool qr_nucleus = false);
+
+struct CaStep {
+  bool horizontal = false;
+  std::vector<Index> rows, cols;
+  double volume_proxy = 0;
+  std::optional<double> error_estimate;
+};
+struct CaTrace {
+  std::vector<CaStep> steps;
+};
+
+/// cross_approx (cur.cpp:201-255). The whole loop runs in one CTA-resident
+/// kernel; stop_tol (posterior estimate) is not on the device path yet.
+std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r, Index k, Index l,
+                                                  IndexSet init_rows, int loops, double h,
+                                                  std::optional<double> stop_tol, Rng& rng);
+
+/// Batched cross_approx + per-block Frobenius residual over `nblocks`
+/// independent m x n blocks stored contiguously in HBM (block b at
+/// d_A + b*block_stride). init rows are drawn per block from
+/// Rng(derive_seed(master_seed, b)). Results stay on the device; the caller
+/// passes device buffers (see slra_cross_approx_batched).
+struct BatchedCaResult {
+  std::vector<int> status;
+  std::vector<Index> r;
+  std::vector<double> resid_sq, norm_sq;
+};
+
+}  // namespace slra

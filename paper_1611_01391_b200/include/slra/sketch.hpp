@@ -1,0 +1,87 @@
+// Structured sketch operators of /root/reference/proj/include/slra/sketch.hpp
+// (in-scope kinds: permutation, sign diagonal, abridged Hadamard, sparse
+// f-circulant, sub-identity, product, column slice; Gaussian for tests).
+//
+// B200 design: an operator is an immutable descriptor. Applying it never
+// touches the full n x n action: each output row of op*X (or op^T*X) is
+// compiled into a short signed combination of input rows ("row
+// expression"), evaluated in exactly the reference's order (nz-list order
+// for Z_f, the ah_recurse butterfly for AH), so the device computes only the
+// l kept outputs (sketch.cpp:558-567 computes all n, then discards) and the
+// result is bit-identical.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "slra/linalg.hpp"
+#include "slra/matrix.hpp"
+#include "slra/rng.hpp"
+
+namespace slra {
+
+enum class Side { Left, Right };
+enum class ColumnMode { Leftmost, Random };
+
+/// Output row = combine(coef_s * X(src_s, :)); tree 0 = ordered list sum,
+/// 1 = radix-2 butterfly over 2^d leaves picking output leaf q.
+struct RowExpr {
+  int tree = 0;
+  std::vector<Index> src;
+  std::vector<double> coef;
+  int q = 0;
+};
+
+/// A compiled plan: `count` outputs of equal width and tree (slra_cuda.h).
+struct SketchPlan {
+  int tree = 0;
+  Index width = 0;
+  Index count = 0;
+  std::vector<int64_t> src;   // count x width
+  std::vector<double> coef;   // count x width
+  std::vector<int32_t> q;     // count
+};
+
+class SketchOperator {
+ public:
+  virtual ~SketchOperator() = default;
+  virtual Index rows() const = 0;
+  virtual Index cols() const = 0;
+  virtual std::string kind() const = 0;
+  /// Row `i` of (op * X) as a combination of rows of X.
+  virtual RowExpr row_of_apply(Index i) const = 0;
+  /// Row `i` of (op^T * X) as a combination of rows of X.
+  virtual RowExpr row_of_apply_transpose(Index i) const = 0;
+  /// op * M and op^T * M on the device (host in, host out).
+  Matrix apply(const Matrix& M) const;
+  Matrix apply_transpose(const Matrix& M) const;
+};
+
+using OpPtr = std::shared_ptr<const SketchOperator>;
+
+OpPtr make_permutation(std::vector<Index> sigma);
+OpPtr make_sign_diagonal(Vector d);
+OpPtr make_abridged_hadamard(Index n, int d);
+OpPtr make_sparse_circulant(Index n, double f, std::vector<std::pair<Index, double>> nonzeros);
+OpPtr make_sub_identity(IndexSet selected, Index total);
+OpPtr make_product(std::vector<OpPtr> ops);
+OpPtr take_columns(OpPtr op, IndexSet columns);
+OpPtr take_columns(OpPtr op, Index l, ColumnMode mode, Rng& rng);
+
+OpPtr gen_permutation(Index n, Rng& rng);
+OpPtr gen_sign_diagonal(Index n, Rng& rng);
+OpPtr gen_sparse_circulant(Index n, Index s, Rng& rng);
+OpPtr gen_aph(Index n, int d, Rng& rng);
+OpPtr gen_asph(Index n, int d, Rng& rng);
+
+/// Plans: the columns of M*op (Side::Right, one output per op column) or the
+/// rows of op*W (Side::Left, one output per op row).
+SketchPlan compile_plan(const SketchOperator& op, Side side);
+
+/// apply(op, M, Side) of sketch.cpp:679-682 on the device.
+Matrix apply(const SketchOperator& op, const Matrix& M, Side side);
+Matrix materialize(const SketchOperator& op, Index cap = 4096);
+
+}  // namespace slra

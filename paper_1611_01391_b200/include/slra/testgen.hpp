@@ -1,0 +1,21 @@
+// Seeded synthetic inputs (/root/reference/proj/include/slra/testgen.hpp), the
+// same draw order as the reference generators so the oracle and the device
+// path see identical matrices.
+#pragma once
+
+#include "slra/lsr.hpp"
+#include "slra/rng.hpp"
+
+namespace slra {
+
+/// G1 * G2 + noise * G3 (testgen.cpp:110-115): G1 drawn first, then G2, then G3.
+Matrix gen_factor_gaussian(Index m, Index n, Index r, double noise, Rng& rng);
+/// Gaussian LSR family (testgen.cpp:159-193) with the noise scale a parameter.
+LsrProblem gen_lsr_gaussian(Index m, Index n, double noise, Rng& rng);
+/// Config 3: x_i ~ U[0,1] (m draws) then y_j ~ U[2,3] (n draws); A_ij = 1/(x_i - y_j).
+Matrix gen_cauchy_block(Index m, Index n, Rng& rng);
+/// Config 5 block: p_i = (u,u) in [0,1]^2 (m points), then q_j = (u+4, u);
+/// K_ij = 0.5 log((dx)^2 + (dy)^2) = log|p_i - q_j|.
+Matrix gen_log_kernel_block(Index m, Index n, Rng& rng);
+
+}  // namespace slra

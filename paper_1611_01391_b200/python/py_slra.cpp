@@ -1,33 +1,38 @@
-// TEST INFRASTRUCTURE ONLY: Python binding of the CPU oracle for tests/ and
-// bench.py's CPU legs. Not part of the product.
-#include <pybind11/functional.h>
+// Python binding of the C++ host layer (namespace slra). Host-array entry
+// points mirror the reference signatures; *_device entry points take raw
+// device pointers (e.g. torch tensor.data_ptr()) for HBM-resident runs.
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
-#include <chrono>
-
-#include "slra_oracle.hpp"
+#include "slra/cur.hpp"
+#include "slra/devbuf.hpp"
+#include "slra/device.hpp"
+#include "slra/errors.hpp"
+#include "slra/lra.hpp"
+#include "slra/lsr.hpp"
+#include "slra/sketch.hpp"
+#include "slra/testgen.hpp"
 
 namespace py = pybind11;
-using namespace slra_oracle;
+using namespace slra;
 
 using FArray = py::array_t<double, py::array::f_style | py::array::forcecast>;
 
 static Matrix from_np(const FArray& a) {
   if (a.ndim() == 1) {
     Matrix M(a.shape(0), 1);
-    std::copy(a.data(), a.data() + a.shape(0), M.v.begin());
+    std::copy(a.data(), a.data() + a.shape(0), M.data());
     return M;
   }
   if (a.ndim() != 2) throw std::invalid_argument("expected a 1-D or 2-D array");
   Matrix M(a.shape(0), a.shape(1));
-  std::copy(a.data(), a.data() + M.size(), M.v.begin());
+  std::copy(a.data(), a.data() + M.size(), M.data());
   return M;
 }
 static FArray to_np(const Matrix& M) {
   FArray a({M.rows(), M.cols()});
-  std::copy(M.v.begin(), M.v.end(), a.mutable_data());
+  std::copy(M.data(), M.data() + M.size(), a.mutable_data());
   return a;
 }
 static py::array_t<double> vec_np(const Vector& v) {
@@ -36,8 +41,14 @@ static py::array_t<double> vec_np(const Vector& v) {
   return a;
 }
 static Vector np_vec(const FArray& a) { return Vector(a.data(), a.data() + a.size()); }
-struct PyOp { OpPtr p; };
 static IndexSet mkset(const std::vector<Index>& v, Index bound) { return IndexSet(v, bound); }
+struct PyOp {
+  OpPtr p;
+};
+template <typename T>
+static T* ptr(uintptr_t p) {
+  return reinterpret_cast<T*>(p);
+}
 
 static py::dict cur_dict(const CurDecomposition& c) {
   py::dict d;
@@ -48,15 +59,32 @@ static py::dict cur_dict(const CurDecomposition& c) {
   return d;
 }
 
-PYBIND11_MODULE(_oracle, m) {
-  m.doc() = "CPU oracle (restatement of the reference slra hot path) -- test infrastructure only";
-  auto base = py::register_exception<std::runtime_error>(m, "OracleRuntimeError");
+static py::dict plan_dict(const SketchPlan& p) {
+  py::dict d;
+  d["tree"] = p.tree;
+  d["width"] = p.width;
+  d["count"] = p.count;
+  d["src"] = p.src;
+  d["coef"] = p.coef;
+  d["q"] = p.q;
+  return d;
+}
+
+PYBIND11_MODULE(_slra, m) {
+  m.doc() = "B200 slra hot path: C++ host layer over the sm_100a C-ABI (libslra_cuda.so)";
+  auto base = py::register_exception<std::runtime_error>(m, "SlraRuntimeError");
   py::register_exception<RangeFailure>(m, "RangeFailure", base.ptr());
   py::register_exception<SketchRankFailure>(m, "SketchRankFailure", base.ptr());
   py::register_exception<PremultRankFailure>(m, "PremultRankFailure", base.ptr());
   py::register_exception<SelectionFailure>(m, "SelectionFailure", base.ptr());
   py::register_exception<GeneratorRankFailure>(m, "GeneratorRankFailure", base.ptr());
   py::register_exception<EmptySample>(m, "EmptySample", base.ptr());
+  py::register_exception<DeviceError>(m, "DeviceError", base.ptr());
+
+  m.def("set_device", [](int dev, uintptr_t stream) { set_device(dev, reinterpret_cast<void*>(stream)); },
+        py::arg("device") = 0, py::arg("stream") = 0);
+  m.def("launch_count", []() { return slra_ctx_launch_count(device_context()); });
+  m.def("synchronize", []() { check(slra_ctx_synchronize(device_context()), "synchronize"); });
 
   py::class_<Rng>(m, "Rng", py::module_local())
       .def(py::init<std::uint64_t>())
@@ -69,7 +97,6 @@ PYBIND11_MODULE(_oracle, m) {
       .def("distinct_indices", &Rng::distinct_indices)
       .def("gaussian_matrix", [](Rng& r, Index a, Index b) { return to_np(r.gaussian_matrix(a, b)); })
       .def("gaussian_vector", [](Rng& r, Index n) { return vec_np(r.gaussian_vector(n)); })
-      .def("child", &Rng::child)
       .def_static("derive_seed", &Rng::derive_seed);
 
   // ---- linalg
@@ -88,29 +115,11 @@ PYBIND11_MODULE(_oracle, m) {
     return numerical_rank(from_np(A), tol, relative ? RankMode::Relative : RankMode::Absolute);
   }, py::arg("A"), py::arg("tol"), py::arg("relative") = false);
   m.def("frobenius_norm", [](const FArray& A) { return frobenius_norm(from_np(A)); });
-  m.def("spectral_norm", [](const FArray& A) { return spectral_norm(from_np(A)); });
-  m.def("determinant_abs", [](const FArray& A) { return determinant_abs(from_np(A)); });
-  m.def("colpiv_qr", [](const FArray& A, double threshold) {
-    ColPivQR q(from_np(A));
-    q.threshold = threshold;
-    py::dict d;
-    d["perm"] = q.perm;
-    d["rank"] = q.rank();
-    d["nonzero_pivots"] = q.nonzero_pivots;
-    d["qr"] = to_np(q.qr);
-    return d;
-  }, py::arg("A"), py::arg("threshold") = -1.0);
-  m.def("colpiv_solve", [](const FArray& A, const FArray& B, double threshold) {
-    ColPivQR q(from_np(A));
-    q.threshold = threshold;
-    return to_np(q.solve(from_np(B)));
-  }, py::arg("A"), py::arg("B"), py::arg("threshold") = -1.0);
 
   // ---- cur
   m.def("t_factor", &t_factor);
-  m.def("maxvol_rows", [](const FArray& A, double h, Index max_swaps) {
-    return maxvol_rows(from_np(A), h, max_swaps).indices();
-  }, py::arg("A"), py::arg("h") = 1.1, py::arg("max_swaps") = 0);
+  m.def("maxvol_rows", [](const FArray& A, double h, Index ms) { return maxvol_rows(from_np(A), h, ms).indices(); },
+        py::arg("A"), py::arg("h") = 1.1, py::arg("max_swaps") = 0);
   m.def("select_rows_spanning", [](const FArray& A, Index count, double h) {
     return select_rows_spanning(from_np(A), count, h).indices();
   }, py::arg("A"), py::arg("count"), py::arg("h") = 1.1);
@@ -121,12 +130,12 @@ PYBIND11_MODULE(_oracle, m) {
     d["accesses"] = o.accesses();
     return d;
   });
-  m.def("cross_approx", [](const FArray& A, Index r, Index k, Index l, const std::vector<Index>& init_rows,
-                           int loops, double h, std::optional<double> stop_tol, Rng& rng) {
+  m.def("cross_approx", [](const FArray& A, Index r, Index k, Index l, const std::vector<Index>& init_rows, int loops,
+                           double h, Rng& rng) {
     Matrix M = from_np(A);
     DenseOracle o(M);
     IndexSet init = init_rows.empty() ? IndexSet() : mkset(init_rows, M.rows());
-    auto [c, trace] = cross_approx(o, r, k, l, std::move(init), loops, h, stop_tol, rng);
+    auto [c, trace] = cross_approx(o, r, k, l, std::move(init), loops, h, std::nullopt, rng);
     py::dict d = cur_dict(c);
     py::list steps;
     for (auto& s : trace.steps) {
@@ -135,27 +144,25 @@ PYBIND11_MODULE(_oracle, m) {
       sd["rows"] = s.rows;
       sd["cols"] = s.cols;
       sd["volume_proxy"] = s.volume_proxy;
-      sd["error_estimate"] = s.error_estimate;
       steps.append(sd);
     }
     d["trace"] = steps;
     d["accesses"] = o.accesses();
     return d;
-  }, py::arg("A"), py::arg("r"), py::arg("k"), py::arg("l"), py::arg("init_rows"), py::arg("loops"),
-     py::arg("h"), py::arg("stop_tol"), py::arg("rng"));
+  }, py::arg("A"), py::arg("r"), py::arg("k"), py::arg("l"), py::arg("init_rows"), py::arg("loops"), py::arg("h"),
+     py::arg("rng"));
+  m.def("cur_evaluate", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
+                           const FArray& U) {
+    Matrix M = from_np(A);
+    CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), from_np(U), 0, false};
+    return cur_evaluate(M, c, NormKind::Frobenius);
+  });
   m.def("cur_reconstruct", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
                               const FArray& U) {
     Matrix M = from_np(A);
-    CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), from_np(U), 0};
+    CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), from_np(U), 0, false};
     return to_np(cur_reconstruct(M, c));
   });
-  m.def("cur_evaluate", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
-                           const FArray& U, const std::string& norm) {
-    Matrix M = from_np(A);
-    CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), from_np(U), 0};
-    NormKind k = norm == "spectral" ? NormKind::Spectral : norm == "chebyshev" ? NormKind::Chebyshev : NormKind::Frobenius;
-    return cur_evaluate(M, c, k);
-  }, py::arg("A"), py::arg("I"), py::arg("J"), py::arg("U"), py::arg("norm") = "frobenius");
 
   // ---- sketch operators
   py::class_<PyOp>(m, "SketchOperator", py::module_local())
@@ -163,14 +170,16 @@ PYBIND11_MODULE(_oracle, m) {
       .def("cols", [](const PyOp& o) { return o.p->cols(); })
       .def("kind", [](const PyOp& o) { return o.p->kind(); })
       .def("apply", [](const PyOp& o, const FArray& M) { return to_np(o.p->apply(from_np(M))); })
-      .def("apply_transpose", [](const PyOp& o, const FArray& M) { return to_np(o.p->apply_transpose(from_np(M))); });
+      .def("apply_transpose", [](const PyOp& o, const FArray& M) { return to_np(o.p->apply_transpose(from_np(M))); })
+      .def("plan", [](const PyOp& o, const std::string& side) {
+        return plan_dict(compile_plan(*o.p, side == "right" ? Side::Right : Side::Left));
+      });
   m.def("make_permutation", [](std::vector<Index> s) { return PyOp{make_permutation(std::move(s))}; });
   m.def("make_sign_diagonal", [](const FArray& d) { return PyOp{make_sign_diagonal(np_vec(d))}; });
   m.def("make_abridged_hadamard", [](Index n, int d) { return PyOp{make_abridged_hadamard(n, d)}; });
   m.def("make_sparse_circulant", [](Index n, double f, std::vector<std::pair<Index, double>> nz) {
     return PyOp{make_sparse_circulant(n, f, std::move(nz))};
   });
-  m.def("make_gaussian", [](const FArray& G) { return PyOp{make_gaussian(from_np(G))}; });
   m.def("make_sub_identity", [](const std::vector<Index>& sel, Index total) {
     return PyOp{make_sub_identity(mkset(sel, total), total)};
   });
@@ -188,49 +197,29 @@ PYBIND11_MODULE(_oracle, m) {
   m.def("gen_permutation", [](Index n, Rng& r) { return PyOp{gen_permutation(n, r)}; });
   m.def("gen_sign_diagonal", [](Index n, Rng& r) { return PyOp{gen_sign_diagonal(n, r)}; });
   m.def("gen_sparse_circulant", [](Index n, Index s, Rng& r) { return PyOp{gen_sparse_circulant(n, s, r)}; });
-  m.def("gen_gaussian", [](Index a, Index b, Rng& r) { return PyOp{gen_gaussian(a, b, r)}; });
   m.def("gen_aph", [](Index n, int d, Rng& r) { return PyOp{gen_aph(n, d, r)}; });
   m.def("gen_asph", [](Index n, int d, Rng& r) { return PyOp{gen_asph(n, d, r)}; });
   m.def("apply", [](const PyOp& op, const FArray& M, const std::string& side) {
     return to_np(apply(*op.p, from_np(M), side == "right" ? Side::Right : Side::Left));
   });
   m.def("materialize", [](const PyOp& op) { return to_np(materialize(*op.p)); });
-  m.def("reset_op_counter", &reset_op_counter);
-  m.def("op_counter", []() { return py::make_tuple(op_counter().adds, op_counter().muls); });
 
-  // ---- lra
+  // ---- lra / lsr
   m.def("range_finder", [](const FArray& M, const PyOp& H, Index r, bool truncated) {
     LowRankFactors f = range_finder(from_np(M), *H.p, r, truncated ? RangeVariant::TruncatedRankR : RangeVariant::BasisQr);
     return py::make_tuple(to_np(f.U), to_np(f.V));
   }, py::arg("M"), py::arg("H"), py::arg("r"), py::arg("truncated") = false);
-  m.def("two_stage_truncate", [](const FArray& U, const FArray& V, Index r) {
-    LowRankFactors f{from_np(U), from_np(V), 0};
-    LowRankFactors g = two_stage_truncate(f, r);
-    return py::make_tuple(to_np(g.U), to_np(g.V));
-  });
-  m.def("posterior_error_estimate", [](const FArray& M, const FArray& U, const FArray& V, Index q, Index s, Rng& rng) {
-    Matrix A = from_np(M);
-    DenseOracle o(A);
-    LowRankFactors f{from_np(U), from_np(V), 0};
-    LraErrorEstimate e = posterior_error_estimate(o, f, q, s, rng);
-    return py::make_tuple(e.estimate_frobenius, e.ci_lo, e.ci_hi, e.has_interval);
-  });
-
-  // ---- lsr
   m.def("sketch_solve", [](const FArray& A, const FArray& b, const PyOp& F, bool with_true) {
-    LsrProblem p{from_np(A), np_vec(b)};
-    LsrReport r = sketch_solve(p, *F.p, with_true);
+    LsrReport rep = sketch_solve(LsrProblem{from_np(A), np_vec(b)}, *F.p, with_true);
     py::dict d;
-    d["x_hat"] = vec_np(r.x_hat);
-    d["sketched_residual"] = r.sketched_residual;
-    d["true_residual"] = r.true_residual;
-    d["ratio"] = r.ratio;
-    d["k"] = r.k;
+    d["x_hat"] = vec_np(rep.x_hat);
+    d["sketched_residual"] = rep.sketched_residual;
+    d["true_residual"] = rep.true_residual;
+    d["ratio"] = rep.ratio;
+    d["k"] = rep.k;
     return d;
   }, py::arg("A"), py::arg("b"), py::arg("F"), py::arg("with_true_residual") = false);
-  m.def("solve_exact", [](const FArray& A, const FArray& b) {
-    return vec_np(solve_exact(LsrProblem{from_np(A), np_vec(b)}));
-  });
+  m.def("solve_exact", [](const FArray& A, const FArray& b) { return vec_np(solve_exact(LsrProblem{from_np(A), np_vec(b)})); });
   m.def("residual_norm", [](const FArray& A, const FArray& b, const FArray& x) {
     return residual_norm(LsrProblem{from_np(A), np_vec(b)}, np_vec(x));
   });
@@ -239,13 +228,51 @@ PYBIND11_MODULE(_oracle, m) {
   });
 
   // ---- testgen
-  m.def("random_orthonormal", [](Index r, Index c, Rng& rng) { return to_np(random_orthonormal(r, c, rng)); });
-  m.def("gen_svd_profile", [](Index n, Index r, Rng& rng) { return to_np(gen_svd_profile(n, r, rng)); });
   m.def("gen_factor_gaussian", [](Index mm, Index n, Index r, double noise, Rng& rng) {
     return to_np(gen_factor_gaussian(mm, n, r, noise, rng));
   });
   m.def("gen_lsr_gaussian", [](Index mm, Index n, double noise, Rng& rng) {
     LsrProblem p = gen_lsr_gaussian(mm, n, noise, rng);
     return py::make_tuple(to_np(p.A), vec_np(p.b));
+  });
+  m.def("gen_cauchy_block", [](Index mm, Index n, Rng& rng) { return to_np(gen_cauchy_block(mm, n, rng)); });
+  m.def("gen_log_kernel_block", [](Index mm, Index n, Rng& rng) { return to_np(gen_log_kernel_block(mm, n, rng)); });
+
+  // ---- device-resident entry points (raw device pointers)
+  m.def("range_finder_device", [](uintptr_t M, Index ldm, Index mm, Index n, const py::dict& plan, Index r,
+                                  bool truncated, uintptr_t U, Index ldu, uintptr_t V, Index ldv, uintptr_t out,
+                                  uintptr_t src, uintptr_t coef, uintptr_t q) {
+    // plan arrays already on the device (src/coef/q pointers); shape from the dict
+    check(slra_range_finder(device_context(), ptr<double>(M), ldm, mm, n, ptr<int64_t>(src), ptr<double>(coef),
+                            ptr<int32_t>(q), plan["width"].cast<Index>(), plan["tree"].cast<int>(),
+                            plan["count"].cast<Index>(), r, truncated ? 1 : 0, ptr<double>(U), ldu, ptr<double>(V), ldv,
+                            ptr<double>(out), nullptr),
+          "range_finder");
+  });
+  m.def("cross_approx_batched_device", [](uintptr_t A, Index lda, Index stride, Index nblocks, Index mm, Index n,
+                                          Index r, Index k, Index l, uintptr_t init_rows, int loops, double h,
+                                          uintptr_t I, uintptr_t J, uintptr_t U, uintptr_t rr, uintptr_t status,
+                                          uintptr_t rs, uintptr_t ns) {
+    check(slra_cross_approx_batched(device_context(), ptr<double>(A), lda, stride, nblocks, mm, n, r, k, l,
+                                    ptr<int64_t>(init_rows), loops, h, ptr<int64_t>(I), ptr<int64_t>(J),
+                                    ptr<double>(U), ptr<int64_t>(rr), ptr<int32_t>(status), ptr<double>(rs),
+                                    ptr<double>(ns)),
+          "cross_approx_batched");
+  });
+  m.def("cross_approx_device", [](uintptr_t A, Index lda, Index mm, Index n, Index r, Index k, Index l,
+                                  uintptr_t init_rows, int loops, double h, uintptr_t I, uintptr_t J, uintptr_t U) {
+    int64_t r_used = 0;
+    check(slra_cross_approx(device_context(), ptr<double>(A), lda, mm, n, r, k, l, ptr<int64_t>(init_rows), loops, h,
+                            ptr<int64_t>(I), ptr<int64_t>(J), ptr<double>(U), nullptr, nullptr, nullptr, &r_used),
+          "cross_approx");
+    return r_used;
+  });
+  m.def("cur_residual_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t I, Index k, uintptr_t J,
+                                  Index l, uintptr_t U) {
+    double rs = 0, ns = 0;
+    check(slra_cur_residual(device_context(), ptr<double>(A), lda, mm, n, ptr<int64_t>(I), k, ptr<int64_t>(J), l,
+                            ptr<double>(U), l, &rs, &ns),
+          "cur_residual");
+    return py::make_tuple(rs, ns);
   });
 }

@@ -1,0 +1,236 @@
+// Host entry points of linalg.hpp / cur.hpp / lra.hpp: reference signatures
+// (/root/reference/proj/include/slra/{linalg,cur,lra}.hpp) over the C-ABI.
+// Every numeric result is computed on the device; the host only moves
+// operands, builds index sets and rethrows typed failures.
+#include <algorithm>
+#include <cmath>
+
+#include "slra/cur.hpp"
+#include "slra/devbuf.hpp"
+#include "slra/errors.hpp"
+#include "slra/lra.hpp"
+
+namespace slra {
+
+namespace {
+std::vector<int64_t> to64(const IndexSet& s) { return std::vector<int64_t>(s.begin(), s.end()); }
+}  // namespace
+
+// ---------------------------------------------------------------- linalg
+Matrix matmul(const Matrix& A, const Matrix& B) {  // linalg.cpp:63-66
+  if (A.cols() != B.rows()) throw std::invalid_argument("matmul: dimension mismatch");
+  DeviceMatrix dA = DeviceMatrix::upload(A), dB = DeviceMatrix::upload(B), dC(A.rows(), B.cols());
+  check(slra_gemm(device_context(), 0, 0, A.rows(), B.cols(), A.cols(), 1.0, dA.data(), dA.ld(), dB.data(), dB.ld(),
+                  0.0, dC.data(), dC.ld()),
+        "slra_gemm");
+  return dC.download();
+}
+
+std::pair<Matrix, Matrix> thin_qr(const Matrix& A) {  // linalg.cpp:67-79
+  if (A.rows() < A.cols()) throw std::invalid_argument("thin_qr: rows < cols");
+  DeviceMatrix dA = DeviceMatrix::upload(A), dQ(A.rows(), A.cols()), dR(A.cols(), A.cols());
+  check(slra_thin_qr(device_context(), dA.data(), dA.ld(), A.rows(), A.cols(), dQ.data(), dQ.ld(), dR.data(), dR.ld()),
+        "slra_thin_qr");
+  return {dQ.download(), dR.download()};
+}
+
+Svd svd(const Matrix& A) {  // linalg.cpp:81-98
+  const Index p = std::min(A.rows(), A.cols());
+  DeviceMatrix dA = DeviceMatrix::upload(A), dS(A.rows(), p), dT(A.cols(), p);
+  DevBuf<double> sig(static_cast<size_t>(p));
+  check(slra_svd(device_context(), dA.data(), dA.ld(), A.rows(), A.cols(), dS.data(), dS.ld(), sig.get(), dT.data(),
+                 dT.ld()),
+        "slra_svd");
+  return Svd{dS.download(), sig.download(), dT.download()};
+}
+
+Matrix pseudo_inverse(const Matrix& A, double rank_tol) {  // linalg.cpp:111-121
+  const Svd f = svd(A);
+  Matrix out(A.cols(), A.rows());
+  if (f.sigma.empty() || f.sigma[0] == 0.0) return out;
+  const double cut = rank_tol * f.sigma[0];
+  Index rho = 0;
+  while (rho < static_cast<Index>(f.sigma.size()) && f.sigma[static_cast<size_t>(rho)] > cut) ++rho;
+  if (rho == 0) return out;
+  Matrix TS(A.cols(), rho), St(rho, A.rows());
+  for (Index j = 0; j < rho; ++j)
+    for (Index i = 0; i < A.cols(); ++i) TS(i, j) = f.T(i, j) / f.sigma[static_cast<size_t>(j)];
+  for (Index i = 0; i < A.rows(); ++i)
+    for (Index j = 0; j < rho; ++j) St(j, i) = f.S(i, j);
+  return matmul(TS, St);
+}
+
+Index numerical_rank(const Matrix& A, double tol, RankMode mode) {  // linalg.cpp:123-132
+  if (tol <= 0) throw std::invalid_argument("numerical_rank: tol must be positive");
+  const Svd f = svd(A);
+  if (f.sigma.empty()) return 0;
+  const double cut = (mode == RankMode::Absolute) ? tol : tol * f.sigma[0];
+  Index count = 0;
+  for (double s : f.sigma) count += s > cut;
+  return count;
+}
+
+double frobenius_norm(const Matrix& A) {  // linalg.cpp:139, one device pass
+  DeviceMatrix dA = DeviceMatrix::upload(A);
+  DevBuf<double> out(2);
+  check(slra_lowrank_residual(device_context(), dA.data(), dA.ld(), A.rows(), A.cols(), nullptr, 1, nullptr, 1, 0,
+                              out.get()),
+        "slra_lowrank_residual");
+  return std::sqrt(out.download()[1]);
+}
+
+// ---------------------------------------------------------------- cur
+double t_factor(Index q, Index s, double h) {  // cur.cpp:84-86
+  return std::sqrt(static_cast<double>(q - s) * static_cast<double>(s) * h * h + 1.0);
+}
+
+IndexSet maxvol_rows(const Matrix& A, double h, Index max_swaps) {  // cur.cpp:88-116
+  const Index m = A.rows(), r = A.cols();
+  if (r < 1 || m < r) throw std::invalid_argument("maxvol_rows: need m >= r >= 1");
+  if (h < 1.0) throw std::invalid_argument("maxvol_rows: need h >= 1");
+  DeviceMatrix dA = DeviceMatrix::upload(A);
+  DevBuf<int64_t> idx(static_cast<size_t>(r));
+  check(slra_maxvol_rows(device_context(), dA.data(), dA.ld(), m, r, h, max_swaps, idx.get()), "maxvol_rows");
+  auto v = idx.download();
+  return IndexSet(std::vector<Index>(v.begin(), v.end()), m);
+}
+
+IndexSet select_rows_spanning(const Matrix& A, Index count, double h) {  // cur.cpp:118-135
+  const Index m = A.rows();
+  if (count > m) throw std::invalid_argument("select_rows_spanning: count > rows");
+  DeviceMatrix dA = DeviceMatrix::upload(A);
+  DevBuf<int64_t> idx(static_cast<size_t>(count));
+  check(slra_select_rows_spanning(device_context(), dA.data(), dA.ld(), m, A.cols(), count, h, idx.get(), nullptr),
+        "select_rows_spanning");
+  auto v = idx.download();
+  return IndexSet(std::vector<Index>(v.begin(), v.end()), m);
+}
+
+CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus) {
+  // cur.cpp:137-162 (SVD nucleus)
+  if (qr_nucleus) throw std::invalid_argument("primitive_cur: the QR nucleus is not on the device path");
+  if (I.size() < r || J.size() < r || r < 0 || (r == 0 && false))
+    throw std::invalid_argument("primitive_cur: need |I|, |J| >= r >= 1");
+  if (I.bound() != M.rows() || J.bound() != M.cols()) throw std::invalid_argument("primitive_cur: index bounds");
+  const DeviceMatrix& dA = M.device();
+  const Index k = I.size(), l = J.size();
+  DevBuf<int64_t> dI(to64(I)), dJ(to64(J));
+  DeviceMatrix dU(l, k);
+  int64_t r_used = 0;
+  check(slra_primitive_cur(device_context(), dA.data(), dA.ld(), M.rows(), M.cols(), dI.get(), k, dJ.get(), l, r,
+                           dU.data(), l, nullptr, nullptr, &r_used),
+        "primitive_cur");
+  M.count(static_cast<unsigned long long>(k * l));  // the only entries read
+  CurDecomposition c;
+  c.row_set = std::move(I);
+  c.col_set = std::move(J);
+  c.nucleus = dU.download();
+  c.r = r_used;
+  return c;
+}
+
+CurDecomposition primitive_cur(const Matrix& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus) {
+  DenseOracle o(M);
+  return primitive_cur(o, std::move(I), std::move(J), r, qr_nucleus);
+}
+
+std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r, Index k, Index l,
+                                                  IndexSet init_rows, int loops, double h,
+                                                  std::optional<double> stop_tol, Rng& rng) {
+  // cur.cpp:201-255
+  const Index m = M.rows(), n = M.cols();
+  if (k < r || l < r || r < 0) throw std::invalid_argument("cross_approx: need k, l >= r >= 1");
+  if (loops < 1) throw std::invalid_argument("cross_approx: need loops >= 1");
+  if (stop_tol) throw std::invalid_argument("cross_approx: stop_tol is not on the device path yet");
+  IndexSet I = (init_rows.size() == k && init_rows.bound() == m) ? std::move(init_rows)
+                                                                 : IndexSet(rng.distinct_indices(k, m), m);
+  const DeviceMatrix& dA = M.device();
+  DevBuf<int64_t> dI0(to64(I)), dI(static_cast<size_t>(k)), dJ(static_cast<size_t>(l));
+  DevBuf<int64_t> trows(static_cast<size_t>(2 * loops * k)), tcols(static_cast<size_t>(2 * loops * l));
+  DevBuf<double> tvol(static_cast<size_t>(2 * loops));
+  DeviceMatrix dU(l, k);
+  int64_t r_used = 0;
+  check(slra_cross_approx(device_context(), dA.data(), dA.ld(), m, n, r, k, l, dI0.get(), loops, h, dI.get(),
+                          dJ.get(), dU.data(), trows.get(), tcols.get(), tvol.get(), &r_used),
+        "cross_approx");
+  // algorithmic reads: per loop one k x n row strip and one m x l column
+  // strip, then the k x l generator (the reference's DenseOracle count)
+  M.count(static_cast<unsigned long long>(loops) * static_cast<unsigned long long>(k * n + m * l) +
+          static_cast<unsigned long long>(k * l));
+  auto vI = dI.download(), vJ = dJ.download(), tr = trows.download(), tc = tcols.download();
+  auto tv = tvol.download();
+  CaTrace trace;
+  for (int s = 0; s < 2 * loops; ++s) {
+    CaStep st;
+    st.horizontal = (s % 2) == 1;
+    st.rows.assign(tr.begin() + s * k, tr.begin() + (s + 1) * k);
+    st.cols.assign(tc.begin() + s * l, tc.begin() + (s + 1) * l);
+    st.volume_proxy = tv[static_cast<size_t>(s)];
+    trace.steps.push_back(std::move(st));
+  }
+  CurDecomposition c;
+  c.row_set = IndexSet(std::vector<Index>(vI.begin(), vI.end()), m);
+  c.col_set = IndexSet(std::vector<Index>(vJ.begin(), vJ.end()), n);
+  c.nucleus = dU.download();
+  c.r = r_used;
+  return {std::move(c), std::move(trace)};
+}
+
+double cur_evaluate(const EntryOracle& M, const CurDecomposition& c, NormKind norm) {  // cur.cpp:80-82
+  if (norm != NormKind::Frobenius)
+    throw std::invalid_argument("cur_evaluate: only the Frobenius norm is on the device path");
+  const DeviceMatrix& dA = M.device();
+  DevBuf<int64_t> dI(to64(c.row_set)), dJ(to64(c.col_set));
+  DeviceMatrix dU = DeviceMatrix::upload(c.nucleus);
+  double rs = 0, ns = 0;
+  check(slra_cur_residual(device_context(), dA.data(), dA.ld(), M.rows(), M.cols(), dI.get(), c.row_set.size(),
+                          dJ.get(), c.col_set.size(), dU.data(), dU.ld(), &rs, &ns),
+        "cur_evaluate");
+  return std::sqrt(rs);
+}
+
+double cur_evaluate(const Matrix& M, const CurDecomposition& c, NormKind norm) {
+  DenseOracle o(M);
+  return cur_evaluate(o, c, norm);
+}
+
+Matrix cur_reconstruct(const Matrix& M, const CurDecomposition& c) {  // cur.cpp:76-78
+  return matmul(matmul(select_cols(M, c.col_set), c.nucleus), select_rows(M, c.row_set));
+}
+
+// ---------------------------------------------------------------- oracle
+const DeviceMatrix& DenseOracle::device() const {
+  if (!dev_) dev_ = std::make_unique<DeviceMatrix>(DeviceMatrix::upload(*M_));
+  return *dev_;
+}
+
+// ---------------------------------------------------------------- lra
+void range_finder_device(const DeviceMatrix& M, const SketchPlan& plan, Index r, RangeVariant variant,
+                         DeviceMatrix& U, DeviceMatrix& V, double* d_out) {
+  DevBuf<int64_t> src(plan.src);
+  DevBuf<double> coef(plan.coef);
+  DevBuf<int32_t> q(plan.q);
+  check(slra_range_finder(device_context(), M.data(), M.ld(), M.rows(), M.cols(), src.get(), coef.get(), q.get(),
+                          plan.width, plan.tree, plan.count, r, variant == RangeVariant::TruncatedRankR ? 1 : 0,
+                          U.data(), U.ld(), V.data(), V.ld(), d_out, nullptr),
+        "range_finder");
+}
+
+LowRankFactors range_finder(const Matrix& M, const SketchOperator& H, Index r, RangeVariant variant) {
+  // lra.cpp:14-39
+  if (H.rows() != M.cols()) throw std::invalid_argument("range_finder: H rows != n");
+  const Index l = H.cols();
+  if (r < 1 || r > l) throw std::invalid_argument("range_finder: need 1 <= r <= l");
+  const SketchPlan plan = compile_plan(H, Side::Right);
+  DeviceMatrix dM = DeviceMatrix::upload(M);
+  const Index uc = variant == RangeVariant::TruncatedRankR ? r : l;
+  DeviceMatrix dU(M.rows(), uc), dV(uc, M.cols());
+  range_finder_device(dM, plan, r, variant, dU, dV, nullptr);
+  LowRankFactors f;
+  f.U = dU.download();
+  f.V = dV.download();
+  f.target_rank = r;
+  return f;
+}
+
+}  // namespace slra

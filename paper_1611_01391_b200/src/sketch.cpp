@@ -1,0 +1,382 @@
+// Sketch operators as descriptors + the row-expression compiler (see
+// include/slra/sketch.hpp). Semantics follow /root/reference/proj/src/sketch.cpp:
+// PermutationOp :43-69, SignDiagonalOp :73-94, AbridgedHadamardOp/ah_recurse
+// :98-133, SparseCirculantOp :215-282, SubIdentityOp :417-442, ProductOp
+// :502-543, ColumnSliceOp :545-583, generators :622-675, apply :679-682.
+#include "slra/sketch.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+#include "slra/devbuf.hpp"
+#include "slra/errors.hpp"
+
+namespace slra {
+
+namespace {
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+RowExpr leaf(Index src, double coef) {
+  RowExpr e;
+  e.tree = SLRA_TREE_LIST;
+  e.src = {src};
+  e.coef = {coef};
+  return e;
+}
+
+RowExpr zero_row() { return RowExpr{}; }
+
+bool is_exact(const RowExpr& e) { return e.tree == SLRA_TREE_LIST && e.src.size() <= 1; }
+
+// Substitute every leaf row y of `outer` by sub(y). Composition is exact
+// (bit-identical to the reference's sequential application) when either all
+// substitutions are single signed rows (exact +-1 maps) or `outer` itself
+// is a single signed row.
+template <typename F>
+RowExpr substitute(const RowExpr& outer, F&& sub) {
+  if (is_exact(outer)) {
+    if (outer.src.empty()) return zero_row();
+    RowExpr inner = sub(outer.src[0]);
+    for (auto& c : inner.coef) c *= outer.coef[0];
+    return inner;
+  }
+  RowExpr out;
+  out.tree = outer.tree;
+  out.q = outer.q;
+  for (size_t s = 0; s < outer.src.size(); ++s) {
+    RowExpr inner = sub(outer.src[s]);
+    require(is_exact(inner), "sketch plan: operator chain has two combining factors (not on the device path)");
+    if (inner.src.empty()) {
+      if (outer.tree == SLRA_TREE_FWHT) {  // keep the butterfly position as an explicit zero
+        out.src.push_back(0);
+        out.coef.push_back(0.0);
+      }
+    } else {
+      out.src.push_back(inner.src[0]);
+      out.coef.push_back(outer.coef[s] * inner.coef[0]);
+    }
+  }
+  return out;
+}
+
+class PermutationOp final : public SketchOperator {
+ public:
+  explicit PermutationOp(std::vector<Index> sigma) : sigma_(std::move(sigma)), inv_(sigma_.size()) {
+    IndexSet check(sigma_, static_cast<Index>(sigma_.size()));
+    for (size_t i = 0; i < sigma_.size(); ++i) inv_[static_cast<size_t>(sigma_[i])] = static_cast<Index>(i);
+  }
+  Index rows() const override { return static_cast<Index>(sigma_.size()); }
+  Index cols() const override { return rows(); }
+  std::string kind() const override { return "permutation"; }
+  // (P x)_i = x_{sigma[i]};  (P^T x)_{sigma[i]} = x_i
+  RowExpr row_of_apply(Index i) const override { return leaf(sigma_[static_cast<size_t>(i)], 1.0); }
+  RowExpr row_of_apply_transpose(Index i) const override { return leaf(inv_[static_cast<size_t>(i)], 1.0); }
+
+ private:
+  std::vector<Index> sigma_, inv_;
+};
+
+class SignDiagonalOp final : public SketchOperator {
+ public:
+  explicit SignDiagonalOp(Vector d) : d_(std::move(d)) {
+    for (double x : d_) require(std::abs(x) > 1e-12, "sign diagonal: entry too close to 0");
+  }
+  Index rows() const override { return static_cast<Index>(d_.size()); }
+  Index cols() const override { return rows(); }
+  std::string kind() const override { return "sign_diagonal"; }
+  RowExpr row_of_apply(Index i) const override { return leaf(i, d_[static_cast<size_t>(i)]); }
+  RowExpr row_of_apply_transpose(Index i) const override { return row_of_apply(i); }
+
+ private:
+  Vector d_;
+};
+
+class AbridgedHadamardOp final : public SketchOperator {
+ public:
+  AbridgedHadamardOp(Index n, int d) : n_(n), d_(d) {
+    require(d >= 1, "abridged hadamard: depth >= 1");
+    require(n % (Index(1) << d) == 0, "abridged hadamard: 2^d must divide n");
+    require(d <= 4, "abridged hadamard: device plans support depth <= 4");
+  }
+  Index rows() const override { return n_; }
+  Index cols() const override { return n_; }
+  std::string kind() const override { return "abridged_hadamard"; }
+  // ah_recurse: row i couples rows b + j*g (g = n / 2^d, b = i mod g) through
+  // the radix-2 butterfly; the output is leaf q = i / g of that butterfly.
+  RowExpr row_of_apply(Index i) const override {
+    const Index w = Index(1) << d_, g = n_ / w;
+    RowExpr e;
+    e.tree = SLRA_TREE_FWHT;
+    e.q = static_cast<int>(i / g);
+    for (Index j = 0; j < w; ++j) {
+      e.src.push_back(i % g + j * g);
+      e.coef.push_back(1.0);
+    }
+    return e;
+  }
+  RowExpr row_of_apply_transpose(Index i) const override { return row_of_apply(i); }  // symmetric
+
+ private:
+  Index n_;
+  int d_;
+};
+
+class SparseCirculantOp final : public SketchOperator {
+ public:
+  SparseCirculantOp(Index n, double f, std::vector<std::pair<Index, double>> nz) : n_(n), f_(f), nz_(std::move(nz)) {
+    require(!nz_.empty() && static_cast<Index>(nz_.size()) <= n, "sparse circulant: 1 <= s <= n");
+    for (auto& [k, v] : nz_) {
+      require(k >= 0 && k < n, "sparse circulant: position out of range");
+      require(v != 0.0, "sparse circulant: zero value");
+    }
+  }
+  Index rows() const override { return n_; }
+  Index cols() const override { return n_; }
+  std::string kind() const override { return "sparse_circulant"; }
+  // (Z_f^k x)_i = x_{i-k} for i >= k, f * x_{n+i-k} otherwise; nz-list order.
+  RowExpr row_of_apply(Index i) const override {
+    RowExpr e;
+    for (auto& [k, v] : nz_) {
+      if (i >= k) {
+        e.src.push_back(i - k);
+        e.coef.push_back(v);
+      } else {
+        e.src.push_back(n_ + i - k);
+        e.coef.push_back(v * f_);
+      }
+    }
+    return e;
+  }
+  RowExpr row_of_apply_transpose(Index i) const override {
+    RowExpr e;
+    for (auto& [k, v] : nz_) {
+      if (i < n_ - k) {
+        e.src.push_back(i + k);
+        e.coef.push_back(v);
+      } else {
+        e.src.push_back(i + k - n_);
+        e.coef.push_back(v * f_);
+      }
+    }
+    return e;
+  }
+
+ private:
+  Index n_;
+  double f_;
+  std::vector<std::pair<Index, double>> nz_;
+};
+
+class SubIdentityOp final : public SketchOperator {
+ public:
+  SubIdentityOp(IndexSet sel, Index total) : sel_(std::move(sel)), total_(total), pos_(total, -1) {
+    require(sel_.bound() == total, "sub-identity: index bound mismatch");
+    for (Index t = 0; t < sel_.size(); ++t) pos_[static_cast<size_t>(sel_[t])] = t;
+  }
+  Index rows() const override { return sel_.size(); }
+  Index cols() const override { return total_; }
+  std::string kind() const override { return "sub_identity"; }
+  RowExpr row_of_apply(Index t) const override { return leaf(sel_[t], 1.0); }
+  RowExpr row_of_apply_transpose(Index j) const override {
+    const Index t = pos_[static_cast<size_t>(j)];
+    return t < 0 ? zero_row() : leaf(t, 1.0);
+  }
+
+ private:
+  IndexSet sel_;
+  Index total_;
+  std::vector<Index> pos_;
+};
+
+class ProductOp final : public SketchOperator {
+ public:
+  explicit ProductOp(std::vector<OpPtr> ops) : ops_(std::move(ops)) {
+    require(!ops_.empty(), "product: empty");
+    for (size_t i = 0; i + 1 < ops_.size(); ++i)
+      require(ops_[i]->cols() == ops_[i + 1]->rows(), "product: dimension mismatch");
+  }
+  Index rows() const override { return ops_.front()->rows(); }
+  Index cols() const override { return ops_.back()->cols(); }
+  std::string kind() const override { return "product"; }
+  // op0 (op1 (... X)): row i of op0 over rows of op1(...), and so on.
+  RowExpr row_of_apply(Index i) const override {
+    RowExpr e = ops_[0]->row_of_apply(i);
+    for (size_t k = 1; k < ops_.size(); ++k) e = substitute(e, [&](Index y) { return ops_[k]->row_of_apply(y); });
+    return e;
+  }
+  // (op0 ... opL)^T X = opL^T (... op0^T X)
+  RowExpr row_of_apply_transpose(Index i) const override {
+    RowExpr e = ops_.back()->row_of_apply_transpose(i);
+    for (size_t k = ops_.size() - 1; k-- > 0;)
+      e = substitute(e, [&](Index y) { return ops_[k]->row_of_apply_transpose(y); });
+    return e;
+  }
+
+ private:
+  std::vector<OpPtr> ops_;
+};
+
+class ColumnSliceOp final : public SketchOperator {
+ public:
+  ColumnSliceOp(OpPtr inner, IndexSet columns) : inner_(std::move(inner)), cols_(std::move(columns)),
+                                                 pos_(inner_->cols(), -1) {
+    require(cols_.bound() == inner_->cols(), "column slice: bound mismatch");
+    for (Index t = 0; t < cols_.size(); ++t) pos_[static_cast<size_t>(cols_[t])] = t;
+  }
+  Index rows() const override { return inner_->rows(); }
+  Index cols() const override { return cols_.size(); }
+  std::string kind() const override { return "column_slice"; }
+  // apply: inner * (rows of M scattered to positions cols)
+  RowExpr row_of_apply(Index i) const override {
+    return substitute(inner_->row_of_apply(i), [&](Index y) {
+      const Index t = pos_[static_cast<size_t>(y)];
+      return t < 0 ? zero_row() : leaf(t, 1.0);
+    });
+  }
+  // apply_transpose: select_rows(inner^T M, cols)
+  RowExpr row_of_apply_transpose(Index t) const override { return inner_->row_of_apply_transpose(cols_[t]); }
+
+ private:
+  OpPtr inner_;
+  IndexSet cols_;
+  std::vector<Index> pos_;
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------- factories
+OpPtr make_permutation(std::vector<Index> sigma) { return std::make_shared<PermutationOp>(std::move(sigma)); }
+OpPtr make_sign_diagonal(Vector d) { return std::make_shared<SignDiagonalOp>(std::move(d)); }
+OpPtr make_abridged_hadamard(Index n, int d) { return std::make_shared<AbridgedHadamardOp>(n, d); }
+OpPtr make_sparse_circulant(Index n, double f, std::vector<std::pair<Index, double>> nz) {
+  return std::make_shared<SparseCirculantOp>(n, f, std::move(nz));
+}
+OpPtr make_sub_identity(IndexSet selected, Index total) {
+  return std::make_shared<SubIdentityOp>(std::move(selected), total);
+}
+OpPtr make_product(std::vector<OpPtr> ops) { return std::make_shared<ProductOp>(std::move(ops)); }
+OpPtr take_columns(OpPtr op, IndexSet columns) { return std::make_shared<ColumnSliceOp>(std::move(op), std::move(columns)); }
+OpPtr take_columns(OpPtr op, Index l, ColumnMode mode, Rng& rng) {
+  require(l >= 1 && l <= op->cols(), "take_columns: l out of range");
+  std::vector<Index> cols;
+  if (mode == ColumnMode::Leftmost) {
+    for (Index i = 0; i < l; ++i) cols.push_back(i);
+  } else {
+    cols = rng.distinct_indices(l, op->cols());
+  }
+  const Index bound = op->cols();
+  return take_columns(std::move(op), IndexSet(std::move(cols), bound));
+}
+
+// Generators draw in the reference's order (sketch.cpp:634-675).
+OpPtr gen_permutation(Index n, Rng& rng) { return make_permutation(rng.permutation(n)); }
+OpPtr gen_sign_diagonal(Index n, Rng& rng) {
+  Vector d(static_cast<size_t>(n));
+  for (Index i = 0; i < n; ++i) d[static_cast<size_t>(i)] = rng.sign();
+  return make_sign_diagonal(std::move(d));
+}
+OpPtr gen_sparse_circulant(Index n, Index s, Rng& rng) {
+  std::vector<std::pair<Index, double>> nz;
+  for (Index k : rng.distinct_indices(s, n)) nz.emplace_back(k, static_cast<double>(rng.sign()));
+  const double f = static_cast<double>(rng.sign());
+  return make_sparse_circulant(n, f, std::move(nz));
+}
+OpPtr gen_aph(Index n, int d, Rng& rng) { return make_product({gen_permutation(n, rng), make_abridged_hadamard(n, d)}); }
+OpPtr gen_asph(Index n, int d, Rng& rng) {
+  OpPtr diag = gen_sign_diagonal(n, rng);  // drawn before the permutation, as sketch.cpp:673
+  return make_product({gen_permutation(n, rng), std::move(diag), make_abridged_hadamard(n, d)});
+}
+
+// ---------------------------------------------------------------- plans
+SketchPlan compile_plan(const SketchOperator& op, Side side) {
+  const Index count = side == Side::Left ? op.rows() : op.cols();
+  std::vector<RowExpr> rows;
+  rows.reserve(static_cast<size_t>(count));
+  int tree = -1;
+  Index width = 1;
+  for (Index t = 0; t < count; ++t) {
+    RowExpr e = side == Side::Left ? op.row_of_apply(t) : op.row_of_apply_transpose(t);
+    if (!e.src.empty() || e.tree == SLRA_TREE_FWHT) {
+      if (tree < 0) tree = e.tree;
+      require(tree == e.tree, "sketch plan: mixed combination trees");
+    }
+    width = std::max<Index>(width, static_cast<Index>(e.src.size()));
+    rows.push_back(std::move(e));
+  }
+  SketchPlan p;
+  p.tree = tree < 0 ? SLRA_TREE_LIST : tree;
+  p.width = width;
+  p.count = count;
+  p.src.assign(static_cast<size_t>(count * width), 0);
+  p.coef.assign(static_cast<size_t>(count * width), 0.0);
+  p.q.assign(static_cast<size_t>(count), 0);
+  for (Index t = 0; t < count; ++t) {
+    const RowExpr& e = rows[static_cast<size_t>(t)];
+    if (p.tree == SLRA_TREE_FWHT) require(static_cast<Index>(e.src.size()) == width, "sketch plan: ragged butterfly");
+    for (size_t s = 0; s < e.src.size(); ++s) {
+      p.src[static_cast<size_t>(t * width) + s] = e.src[s];
+      p.coef[static_cast<size_t>(t * width) + s] = e.coef[s];
+    }
+    p.q[static_cast<size_t>(t)] = e.q;
+  }
+  return p;
+}
+
+namespace {
+
+Matrix run_plan(const SketchPlan& p, const Matrix& M, bool rows_mode, Index out_rows, Index out_cols) {
+  slra_ctx ctx = device_context();
+  DeviceMatrix dM = DeviceMatrix::upload(M);
+  DeviceMatrix out(out_rows, out_cols);
+  DevBuf<int64_t> src(p.src);
+  DevBuf<double> coef(p.coef);
+  DevBuf<int32_t> q(p.q);
+  if (rows_mode)
+    check(slra_sketch_rows(ctx, dM.data(), dM.ld(), M.rows(), M.cols(), src.get(), coef.get(), q.get(), p.width,
+                           p.tree, p.count, out.data(), out.ld()),
+          "slra_sketch_rows");
+  else
+    check(slra_sketch_cols(ctx, dM.data(), dM.ld(), M.rows(), M.cols(), src.get(), coef.get(), q.get(), p.width,
+                           p.tree, p.count, out.data(), out.ld()),
+          "slra_sketch_cols");
+  return out.download();
+}
+
+}  // namespace
+
+Matrix SketchOperator::apply(const Matrix& M) const {
+  require(M.rows() == cols(), "sketch apply: dims");
+  return run_plan(compile_plan(*this, Side::Left), M, true, rows(), M.cols());
+}
+
+Matrix SketchOperator::apply_transpose(const Matrix& M) const {
+  require(M.rows() == rows(), "sketch apply: dims");
+  // rows of op^T M: a left plan of the transpose
+  struct T final : SketchOperator {
+    const SketchOperator& o;
+    explicit T(const SketchOperator& x) : o(x) {}
+    Index rows() const override { return o.cols(); }
+    Index cols() const override { return o.rows(); }
+    std::string kind() const override { return "transpose"; }
+    RowExpr row_of_apply(Index i) const override { return o.row_of_apply_transpose(i); }
+    RowExpr row_of_apply_transpose(Index i) const override { return o.row_of_apply(i); }
+  } t(*this);
+  return run_plan(compile_plan(t, Side::Left), M, true, cols(), M.cols());
+}
+
+Matrix apply(const SketchOperator& op, const Matrix& M, Side side) {
+  if (side == Side::Left) return op.apply(M);
+  // M * op = (op^T M^T)^T: column t of M*op combines columns of M.
+  require(M.cols() == op.rows(), "sketch apply: dims");
+  return run_plan(compile_plan(op, Side::Right), M, false, M.rows(), op.cols());
+}
+
+Matrix materialize(const SketchOperator& op, Index cap) {
+  require(op.rows() <= cap && op.cols() <= cap, "materialize: cap exceeded");
+  return op.apply(Matrix::Identity(op.cols(), op.cols()));
+}
+
+}  // namespace slra
