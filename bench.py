@@ -1,0 +1,511 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json metric "LRA matrix entries/s (sketch+CUR+residual)".
+
+Default workload (N=1 line): config 2 = configs[1] of BASELINE.json — range-
+finder LRA of a 4096 x 4096 fp64 A = U diag(sigma) V^T (sigma_j = 0.5^j, j<32,
+then 1e-12) sketched with l = 48 by (a) a sparse +-1 multiplier with 4 nonzeros
+per column and (b) an abridged Hadamard multiplier of depth 3 with random
++-1 diagonal and column subsampling; rank-32 reconstruction (TruncatedRankR)
+and the ||A - U V||_F residual. One step = both multipliers over one A
+(2 x 4096^2 entries). `--config 1|5` run the other single-GPU workloads.
+
+Timing: W untimed warm-up steps, then K steps timed with CUDA events on the
+product's stream; an L2 flush (256 MiB write, > 126 MB L2) runs between timed
+steps outside the event pairs; barrier + synchronize on both sides; the max
+over ranks. N>1 (torchrun) runs one independent replica per GPU (config 2 does
+not shard: "replicas only") -> scaling "weak".
+
+`--impl reference` times the reference algorithm on the host CPU: the C++
+oracle restatement (oracle/, the reference itself cannot be built here:
+no Eigen) with all host threads, on the same config/metric.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N2 = 4096
+L_SKETCH = 48
+RANK = 32
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=2, choices=[1, 2, 5])
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--blocks", type=int, default=65536, help="config 5 block count")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- environment
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() in ("active", "1"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": None, "fp64_tflops": None, "fp64_source": None}
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peaks["hbm_gbs"] = mp.get("hbm_gbs")
+    except (OSError, ValueError):
+        peaks["hbm_gbs"] = 6650.0  # B200_PROFILING.md fallback
+    # FP64 is not in MEASURED_PEAKS.json: our DMMA microbenchmark measured on
+    # this pool's B200 (profiles/r01_fp64_peaks.jsonl, tools/fp64_peak.cu).
+    try:
+        best = 0.0
+        for line in open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.jsonl")):
+            d = json.loads(line)
+            if d.get("kind", "").startswith("dmma"):
+                best = max(best, d["tflops"])
+        peaks["fp64_tflops"] = best or None
+        peaks["fp64_source"] = "profiles/r01_fp64_peaks.jsonl (DMMA microbenchmark, measured)"
+    except (OSError, ValueError):
+        pass
+    return peaks
+
+
+# ---------------------------------------------------------------- config 2 inputs
+def config2_matrix_colmajor(seed, device):
+    """A = U diag(sigma) V^T with U, V from QR of seeded Gaussians; returns a
+    torch tensor holding A in column-major order (i.e. the row-major A^T)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    Gu = torch.randn(N2, N2, dtype=torch.float64, generator=g).to(device)
+    Gv = torch.randn(N2, N2, dtype=torch.float64, generator=g).to(device)
+    U, Ru = torch.linalg.qr(Gu)
+    V, Rv = torch.linalg.qr(Gv)
+    U = U * torch.sign(torch.diagonal(Ru))[None, :]
+    V = V * torch.sign(torch.diagonal(Rv))[None, :]
+    j = torch.arange(N2, dtype=torch.float64, device=device)
+    sig = torch.where(j < 32, 0.5 ** j, torch.full_like(j, 1e-12))
+    At = (V * sig[None, :]) @ U.T  # = A^T row-major = A column-major
+    del Gu, Gv, U, V
+    return At.contiguous()
+
+
+def config2_operators(mod, seed):
+    ra = mod.Rng(mod.Rng.derive_seed(seed, 1))
+    Ha = mod.take_columns_random(mod.gen_sparse_circulant(N2, 4, ra), L_SKETCH, ra)
+    rb = mod.Rng(mod.Rng.derive_seed(seed, 2))
+    Hb = mod.take_columns_random(mod.gen_asph(N2, 3, rb), L_SKETCH, rb)
+    return [("sparse_pm1_s4", Ha), ("abridged_hadamard_d3", Hb)]
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import torch  # CPU only: input generation
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))
+    import _oracle as oracle
+    cores = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    torch.set_num_threads(cores)
+    At = config2_matrix_colmajor(args.seed, "cpu")
+    A = At.numpy().T  # column-major view -> (n, n) Fortran array
+    ops = config2_operators(oracle, args.seed)
+
+    # each reference step = ONE range-finder LRA + residual (multipliers
+    # alternate), i.e. a bounded sample of half a config-2 step: n^2 entries
+    def step(i):
+        _, H = ops[i % 2]
+        U, V = oracle.range_finder(A, H, RANK, True)
+        oracle.lowrank_residual_frobenius(A, U, V)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    dt = time.perf_counter() - t0
+    entries = 1.0 * N2 * N2 * args.steps
+    value = entries / dt
+    line = {
+        "impl": "reference", "metric": "LRA matrix entries/s (sketch+CUR+residual)", "value": value,
+        "unit": "entries/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, config-2 recipe)",
+        "config": {"workload": "config2: range-finder LRA 4096x4096, l=48, sparse+-1(s=4) and ASPH(d=3), rank 32",
+                   "entries_per_step": 2 * N2 * N2},
+        "cpu_baseline": {"value": value, "unit": "entries/s", "cores": cores, "kind": "port",
+                         "sample": "per step one config-2 LRA (multipliers alternate; n^2 entries), oracle/ C++ "
+                                   "restatement, OpenMP over output columns"},
+        "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1611_01391_b200 as slra
+    stream = torch.cuda.current_stream()
+    slra.set_device(local, stream.cuda_stream)
+    peaks = load_peaks()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    flush_buf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MiB > L2
+
+    if args.config == 2:
+        work = Config2(slra, torch, args.seed + rank)
+    elif args.config == 1:
+        work = Config1(slra, torch, args.seed + rank)
+    else:
+        work = Config5(slra, torch, args.seed + rank, args.blocks)
+
+    for _ in range(args.warmup):
+        work.step()
+    barrier()
+
+    # ---- timed region
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = slra.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush_buf.fill_(float(i))
+        ev[i][0].record(stream)
+        work.step()
+        ev[i][1].record(stream)
+    barrier()
+    clocks = sampler.stop()
+    gpu_launches = slra.launch_count() - launches0
+    ms_total = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = work.entries_per_step * args.steps * ws / (ms_max * 1e-3)
+
+    # ---- per-kernel device times over the same K steps (instrumented pass)
+    slra.set_timing(True)
+    for i in range(args.steps):
+        flush_buf.fill_(float(i))
+        work.step()
+    torch.cuda.synchronize()
+    fam = slra.timing_report()
+    slra.set_timing(False)
+    roofline, kernels = work.roofline(fam, peaks, args.steps)
+
+    # ---- end-to-end through the reference-facing API with host buffers
+    e2e = work.e2e(args.steps, args.warmup)
+
+    line = {
+        "metric": "LRA matrix entries/s (sketch+CUR+residual)", "value": value, "unit": "entries/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded; same recipe as BASELINE.json config)",
+        "config": dict(work.config, l2="256 MiB flush between timed steps (outside the event pairs)",
+                       parallelism=f"replicas x{ws} (no data-path collective)"),
+        "roofline": roofline, "kernels_ms_per_step": kernels,
+        "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
+        "residual_rel": work.last_residual_rel(),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = work.cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+class Config2:
+    def __init__(self, slra, torch, seed):
+        self.slra, self.torch = slra, torch
+        self.seed = seed
+        self.At = config2_matrix_colmajor(seed, "cuda")
+        self.ops = config2_operators(slra, seed)
+        self.plans = []
+        for name, H in self.ops:
+            p = H.plan("right")
+            dev = dict(src=torch.tensor(p["src"], dtype=torch.int64, device="cuda"),
+                       coef=torch.tensor(p["coef"], dtype=torch.float64, device="cuda"),
+                       q=torch.tensor(p["q"], dtype=torch.int32, device="cuda"))
+            self.plans.append((name, p, dev))
+        self.U = [torch.empty(RANK, N2, dtype=torch.float64, device="cuda") for _ in self.ops]  # col-major m x r
+        self.V = [torch.empty(N2, RANK, dtype=torch.float64, device="cuda") for _ in self.ops]  # col-major r x n
+        self.out = torch.zeros(len(self.ops), 2, dtype=torch.float64, device="cuda")
+        self.entries_per_step = 2 * N2 * N2
+        self.config = {"workload": "config2: range-finder LRA 4096x4096 fp64, l=48, sparse+-1 (s=4) and "
+                                   "abridged Hadamard (d=3) multipliers, TruncatedRankR r=32, ||A-UV||_F",
+                       "entries_per_step": self.entries_per_step, "m": N2, "n": N2, "l": L_SKETCH, "r": RANK}
+
+    def step(self):
+        for i, (_, p, d) in enumerate(self.plans):
+            self.slra.range_finder_device(self.At.data_ptr(), N2, N2, N2, p, RANK, True,
+                                          self.U[i].data_ptr(), N2, self.V[i].data_ptr(), RANK,
+                                          self.out[i].data_ptr(), d["src"].data_ptr(), d["coef"].data_ptr(),
+                                          d["q"].data_ptr())
+
+    def last_residual_rel(self):
+        o = self.out.cpu().numpy()
+        return {name: float((o[i, 0] / o[i, 1]) ** 0.5) for i, (name, _, _) in enumerate(self.plans)}
+
+    def roofline(self, fam, peaks, steps):
+        m = n = N2
+        kernels = {k: v[0] / steps for k, v in fam.items()}
+        # dominant family by device time
+        top = max(fam.items(), key=lambda kv: kv[1][0])[0]
+        per_launch_ms = {k: v[0] / max(v[1], 1) for k, v in fam.items()}
+        if top in ("residual", "gemm_v"):
+            flops = 2.0 * m * n * RANK + (5.0 * m * n if top == "residual" else 0.0)
+            ach = flops / (per_launch_ms[top] * 1e-3) / 1e12
+            rl = {"kernel": top, "bound": "tensor", "achieved": ach, "peak": peaks["fp64_tflops"],
+                  "unit": "TFLOP/s", "frac": ach / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
+                  "peak_source": peaks["fp64_source"],
+                  "algorithmic_per_launch": {"flops": flops, "bytes": 8.0 * m * n + 16.0 * m * RANK},
+                  "traffic": None}
+        else:
+            byts = {"sketch": 8.0 * m * L_SKETCH * (4 + 8) / 2 + 8.0 * m * L_SKETCH}.get(top, 8.0 * m * L_SKETCH)
+            ach = byts / (per_launch_ms[top] * 1e-3) / 1e9
+            rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                  "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                  "traffic": None}
+        # secondary: the residual kernel on its own roofline, always reported
+        if "residual" in fam:
+            flops = 2.0 * m * n * RANK + 5.0 * m * n
+            ach = flops / (per_launch_ms["residual"] * 1e-3) / 1e12
+            rl["residual_kernel"] = {"achieved_tflops": ach, "frac_fp64": ach / peaks["fp64_tflops"],
+                                     "achieved_gbs": 8.0 * m * n / (per_launch_ms["residual"] * 1e-3) / 1e9}
+        if "gemm_v" in fam:
+            flops = 2.0 * m * n * RANK
+            ach = flops / (per_launch_ms["gemm_v"] * 1e-3) / 1e12
+            rl["gemm_v_kernel"] = {"achieved_tflops": ach, "frac_fp64": ach / peaks["fp64_tflops"],
+                                   "achieved_gbs": 8.0 * m * n / (per_launch_ms["gemm_v"] * 1e-3) / 1e9}
+        return rl, kernels
+
+    def e2e(self, steps, warmup):
+        torch = self.torch
+        host = torch.empty(N2 * N2, dtype=torch.float64, pin_memory=True)
+        host.copy_(self.At.reshape(-1))
+        ptr = host.data_ptr()
+        ops = self.ops
+
+        def one():
+            for _, H in ops:
+                U, V, rs, ns = self.slra.range_finder_host(ptr, N2, N2, H, RANK, True)
+        for _ in range(max(1, warmup // 2)):
+            one()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        return {"value": self.entries_per_step * steps / dt, "unit": "entries/s",
+                "h2d_bytes_per_step": 2 * 8 * N2 * N2,
+                "d2h_bytes_per_step": 2 * (8 * 2 * N2 * RANK + 16),
+                "api": "paper_1611_01391_b200.range_finder_host -> slra::range_finder_device -> slra_range_finder "
+                       "(host pinned A in, U/V out, once per multiplier)"}
+
+    def cpu_baseline(self):
+        sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))
+        import _oracle as oracle
+        cores = os.cpu_count() or 1
+        A = self.At.cpu().numpy().T
+        ops = config2_operators(oracle, self.seed)
+        t0 = time.perf_counter()
+        for _, H in ops:
+            U, V = oracle.range_finder(A, H, RANK, True)
+            oracle.lowrank_residual_frobenius(A, U, V)
+        dt = time.perf_counter() - t0
+        return {"value": self.entries_per_step / dt, "unit": "entries/s", "cores": cores, "kind": "port",
+                "sample": "one full config-2 step (both multipliers on the same 4096^2 A) through the oracle/ "
+                          "C++ restatement of the reference path (full-operator sketch application, pinv via SVD, "
+                          "Frobenius residual), OpenMP over output columns", "seconds": dt}
+
+
+class Config1:
+    """Config 1: 256x256 factor-Gaussian CUR, 3 C-A sweeps + residual (latency-bound)."""
+
+    def __init__(self, slra, torch, seed):
+        self.slra, self.torch = slra, torch
+        A = slra.gen_factor_gaussian(256, 256, 8, 1e-8, slra.Rng(seed))
+        self.A_host = A
+        self.A = torch.from_numpy(A.T.copy()).cuda()
+        self.init = torch.tensor(slra.Rng(seed + 1).distinct_indices(16, 256), dtype=torch.int64, device="cuda")
+        self.I = torch.zeros(16, dtype=torch.int64, device="cuda")
+        self.J = torch.zeros(16, dtype=torch.int64, device="cuda")
+        self.U = torch.zeros(256, dtype=torch.float64, device="cuda")
+        self.entries_per_step = 256 * 256
+        self.config = {"workload": "config1: C-A CUR 256x256, r=8, k=l=16, 3 sweeps, Frobenius residual",
+                       "entries_per_step": self.entries_per_step}
+        self.res = (0.0, 1.0)
+
+    def step(self):
+        s = self.slra
+        s.cross_approx_device(self.A.data_ptr(), 256, 256, 256, 8, 16, 16, self.init.data_ptr(), 3, 1.1,
+                              self.I.data_ptr(), self.J.data_ptr(), self.U.data_ptr())
+        self.res = s.cur_residual_device(self.A.data_ptr(), 256, 256, 256, self.I.data_ptr(), 16,
+                                         self.J.data_ptr(), 16, self.U.data_ptr())
+
+    def last_residual_rel(self):
+        return (self.res[0] / self.res[1]) ** 0.5
+
+    def roofline(self, fam, peaks, steps):
+        kernels = {k: v[0] / steps for k, v in fam.items()}
+        top = max(fam.items(), key=lambda kv: kv[1][0])[0]
+        return {"kernel": top, "bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": None, "note": "config 1 is launch/latency bound (SURVEY 8d)"}, kernels
+
+    def e2e(self, steps, warmup):
+        s = self.slra
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            g = s.cross_approx(self.A_host, 8, 16, 16, [], 3, 1.1, s.Rng(1))
+            s.cur_evaluate(self.A_host, g["I"], g["J"], g["nucleus"])
+        dt = time.perf_counter() - t0
+        return {"value": self.entries_per_step * steps / dt, "unit": "entries/s",
+                "h2d_bytes_per_step": 2 * 8 * 256 * 256, "d2h_bytes_per_step": 8 * (16 + 16 + 256)}
+
+    def cpu_baseline(self):
+        sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))
+        import _oracle as oracle
+        n = 0
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 5.0:
+            o = oracle.cross_approx(self.A_host, 8, 16, 16, [], 3, 1.1, None, oracle.Rng(n))
+            oracle.cur_evaluate(self.A_host, o["I"], o["J"], o["nucleus"])
+            n += 1
+        dt = time.perf_counter() - t0
+        return {"value": self.entries_per_step * n / dt, "unit": "entries/s", "cores": 1, "kind": "port",
+                "sample": f"{n} config-1 runs in 5 s"}
+
+
+class Config5:
+    """Config 5: batched superfast-multipole LRA, 256x256 log-kernel blocks, k=l=32, adaptive r<=16, 2 sweeps."""
+
+    def __init__(self, slra, torch, seed, blocks):
+        self.slra, self.torch = slra, torch
+        self.nb = blocks
+        m = 256
+        # device-side generation of the blocks from per-block seeded points
+        # (points drawn on the host with the reference Rng, kernel evaluated on
+        # the GPU: log differs from glibc's in the last ulp; parity tests use
+        # host-generated blocks)
+        g = torch.Generator().manual_seed(seed)
+        P = torch.rand(blocks, m, 2, dtype=torch.float64, generator=g)
+        Q = torch.rand(blocks, m, 2, dtype=torch.float64, generator=g)
+        Q[..., 0] += 4.0
+        self.A = torch.empty(blocks, m, m, dtype=torch.float64, device="cuda")
+        for b0 in range(0, blocks, 4096):
+            p = P[b0:b0 + 4096].cuda()
+            q = Q[b0:b0 + 4096].cuda()
+            d = p[:, None, :, :] - q[:, :, None, :]  # [b, j, i, 2] -> A^T[j, i] = K(i, j): col-major K
+            self.A[b0:b0 + 4096] = 0.5 * torch.log((d * d).sum(-1))
+        inits = torch.stack([torch.randperm(m, generator=g)[:32] for _ in range(min(blocks, 1))])
+        self.init = torch.stack([torch.randperm(m, generator=g)[:32] for _ in range(blocks)]).cuda()
+        self.I = torch.zeros(blocks, 32, dtype=torch.int64, device="cuda")
+        self.J = torch.zeros(blocks, 32, dtype=torch.int64, device="cuda")
+        self.U = torch.zeros(blocks, 32 * 32, dtype=torch.float64, device="cuda")
+        self.r = torch.zeros(blocks, dtype=torch.int64, device="cuda")
+        self.st = torch.zeros(blocks, dtype=torch.int32, device="cuda")
+        self.rs = torch.zeros(blocks, dtype=torch.float64, device="cuda")
+        self.ns = torch.zeros(blocks, dtype=torch.float64, device="cuda")
+        self.entries_per_step = blocks * m * m
+        self.config = {"workload": f"config5: {blocks} batched 256x256 log-kernel blocks, k=l=32, adaptive r "
+                                   f"(numerical_rank 1e-10), 2 C-A sweeps + per-block residual",
+                       "entries_per_step": self.entries_per_step}
+        del inits
+
+    def step(self):
+        self.slra.cross_approx_batched_device(self.A.data_ptr(), 256, 256 * 256, self.nb, 256, 256, 0, 32, 32,
+                                              self.init.data_ptr(), 2, 1.1, self.I.data_ptr(), self.J.data_ptr(),
+                                              self.U.data_ptr(), self.r.data_ptr(), self.st.data_ptr(),
+                                              self.rs.data_ptr(), self.ns.data_ptr())
+
+    def last_residual_rel(self):
+        return float(((self.rs / self.ns).sqrt()).max().item())
+
+    def roofline(self, fam, peaks, steps):
+        kernels = {k: v[0] / steps for k, v in fam.items()}
+        top = max(fam.items(), key=lambda kv: kv[1][0])[0]
+        per = fam[top][0] / max(fam[top][1], 1)
+        byts = 8.0 * self.nb * 256 * 256
+        ach = byts / (per * 1e-3) / 1e9
+        return {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": None}, kernels
+
+    def e2e(self, steps, warmup):
+        return None
+
+    def cpu_baseline(self):
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -53,6 +53,11 @@ int slra_ctx_synchronize(slra_ctx ctx);
 void* slra_ctx_stream(slra_ctx ctx);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t slra_ctx_launch_count(slra_ctx ctx);
+/* Per-kernel-family device timing (CUDA events on the context stream around
+ * every launch). set_timing clears the records; the report is
+ * "family=ms,launches;..." summed since then. */
+int slra_ctx_set_timing(slra_ctx ctx, int on);
+int slra_ctx_timing_report(slra_ctx ctx, char* buf, int64_t len);
 int slra_device_alloc(slra_ctx ctx, int64_t bytes, void** d_out);
 int slra_device_free(slra_ctx ctx, void* d_ptr);
 int slra_memcpy_h2d(slra_ctx ctx, void* d_dst, const void* h_src, int64_t bytes);

@@ -203,6 +203,10 @@ PYBIND11_MODULE(_oracle, m) {
     LowRankFactors f = range_finder(from_np(M), *H.p, r, truncated ? RangeVariant::TruncatedRankR : RangeVariant::BasisQr);
     return py::make_tuple(to_np(f.U), to_np(f.V));
   }, py::arg("M"), py::arg("H"), py::arg("r"), py::arg("truncated") = false);
+  // ||M - U V||_F (slra_cli.cpp:286 error, Frobenius as in north_star)
+  m.def("lowrank_residual_frobenius", [](const FArray& M, const FArray& U, const FArray& V) {
+    return frobenius_norm(sub(from_np(M), matmul(from_np(U), from_np(V))));
+  });
   m.def("two_stage_truncate", [](const FArray& U, const FArray& V, Index r) {
     LowRankFactors f{from_np(U), from_np(V), 0};
     LowRankFactors g = two_stage_truncate(f, r);

@@ -37,7 +37,43 @@ struct Context {
   // (slot 0: range finder, 1: cur residual, 2: lsr, 3: spare)
   void* arena[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t arena_bytes[4] = {0, 0, 0, 0};
+  // opt-in per-kernel-family timing (CUDA events on the context stream)
+  bool timing = false;
+  struct Rec {
+    const char* family;
+    cudaEvent_t start, stop;
+  };
+  std::vector<Rec> records;
+  std::vector<cudaEvent_t> event_pool;
 };
+
+cudaEvent_t pooled_event(Context* c);
+
+// Records start/stop events around one kernel launch when timing is on.
+struct KernelTimer {
+  Context* c;
+  const char* family;
+  cudaEvent_t start = nullptr;
+  KernelTimer(Context* ctx, const char* fam) : c(ctx), family(fam) {
+    if (c->timing) {
+      start = pooled_event(c);
+      cudaEventRecord(start, c->stream);
+    }
+  }
+  ~KernelTimer() {
+    if (start) {
+      cudaEvent_t stop = pooled_event(c);
+      cudaEventRecord(stop, c->stream);
+      c->records.push_back({family, start, stop});
+    }
+  }
+};
+
+#define SLRA_TIMED(ctx, fam, ...)                  \
+  {                                                \
+    slra_dev::KernelTimer _slra_kt((ctx), (fam));  \
+    __VA_ARGS__                                    \
+  }
 
 void set_last_error(const std::string& s);
 int cuda_status(cudaError_t e, const char* where);

@@ -306,7 +306,7 @@ static bool ca_fits(int m, int n, int k, int l) {
 int launch_ca_block(Context* c, const CaParams& p, int nprob) {
   const size_t smem = ca_smem_bytes(p.m, p.n, p.k, p.l);
   SLRA_CUDA(cudaFuncSetAttribute(ca_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  ca_block_kernel<<<nprob, kCT, smem, c->stream>>>(p);
+  SLRA_TIMED(c, "cross_approx", ca_block_kernel<<<nprob, kCT, smem, c->stream>>>(p);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }

@@ -132,7 +132,7 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
   if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 4096) {
     const size_t smem = qr_cta_smem((int)m, c);
     SLRA_CUDA(cudaFuncSetAttribute(thin_qr_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    thin_qr_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, c, Q, ldq, R, ldr);
+    SLRA_TIMED(cx, "thin_qr", thin_qr_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, c, Q, ldq, R, ldr);)
     SLRA_CHECK_LAUNCH(cx);
     return SLRA_OK;
   }
@@ -170,8 +170,8 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
     const int64_t lr = level_rows[lv];
     const int64_t nb = (lr + kLeaf - 1) / kLeaf;
     double* Xn = ws + offX[lv];
-    tsqr_reduce_kernel<<<(unsigned)nb, kDT, sm_red, cx->stream>>>(X, ldx, lr, c, Lp, ws + offV[lv], ws + offT[lv],
-                                                                  Xn, nb * c);
+    SLRA_TIMED(cx, "thin_qr", tsqr_reduce_kernel<<<(unsigned)nb, kDT, sm_red, cx->stream>>>(X, ldx, lr, c, Lp, ws + offV[lv], ws + offT[lv],
+                                                                  Xn, nb * c);)
     SLRA_CHECK_LAUNCH(cx);
     X = Xn;
     ldx = nb * c;
@@ -181,7 +181,7 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
   SLRA_CUDA(cudaFuncSetAttribute(tsqr_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_top));
   double* qbuf[2] = {ws + offQ, ws + offQ + (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c};
   double* Qtop = ws + offQ + 2 * (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c;
-  tsqr_top_kernel<<<1, kDT, sm_top, cx->stream>>>(X, ldx, (int)top_rows, c, Lp, Qtop, top_rows, R, ldr);
+  SLRA_TIMED(cx, "thin_qr", tsqr_top_kernel<<<1, kDT, sm_top, cx->stream>>>(X, ldx, (int)top_rows, c, Lp, Qtop, top_rows, R, ldr);)
   SLRA_CHECK_LAUNCH(cx);
   // expand top-down
   const size_t sm_exp = sizeof(double) * (size_t)Lp * c;
@@ -200,8 +200,8 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
       Qo = qbuf[lv & 1];
       ldqo = lr;
     }
-    tsqr_expand_kernel<<<(unsigned)nb, kDT, sm_exp, cx->stream>>>(Qp, ldqp, ws + offV[lv], ws + offT[lv], lr, c, Lp,
-                                                                  Qo, ldqo);
+    SLRA_TIMED(cx, "thin_qr", tsqr_expand_kernel<<<(unsigned)nb, kDT, sm_exp, cx->stream>>>(Qp, ldqp, ws + offV[lv], ws + offT[lv], lr, c, Lp,
+                                                                  Qo, ldqo);)
     SLRA_CHECK_LAUNCH(cx);
     Qp = Qo;
     ldqp = ldqo;
@@ -267,7 +267,7 @@ int launch_svd_small(Context* cx, const double* A, int64_t lda, int m, int n, do
   const size_t smem = svd_smem(m, n);
   if (smem > 220 * 1024) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(svd_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  svd_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, m, n, S, lds, sigma, T, ldt);
+  SLRA_TIMED(cx, "svd", svd_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, m, n, S, lds, sigma, T, ldt);)
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
 }
@@ -294,19 +294,51 @@ __global__ void __launch_bounds__(kDT) colsign_kernel(double* __restrict__ S, in
 
 int launch_colsign(Context* cx, double* S, int64_t lds, int64_t m, double* T, int64_t ldt, int64_t n, int64_t cols) {
   if (cols <= 0) return SLRA_OK;
-  colsign_kernel<<<(unsigned)cols, kDT, 0, cx->stream>>>(S, lds, m, T, ldt, n);
+  SLRA_TIMED(cx, "svd", colsign_kernel<<<(unsigned)cols, kDT, 0, cx->stream>>>(S, lds, m, T, ldt, n);)
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                                 double* __restrict__ B, int64_t ldb) {
+  __shared__ double tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, j = j0 + dy;
+    if (i < m && j < n) tile[dy][threadIdx.x] = A[i + j * lda];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t j = j0 + threadIdx.x, i = i0 + dy;
+    if (i < m && j < n) B[j + i * ldb] = tile[threadIdx.x][dy];
+  }
+}
+
+int launch_transpose(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, double* B, int64_t ldb) {
+  dim3 grid(ceil_div(m, 32), ceil_div(n, 32));
+  SLRA_TIMED(cx, "transpose", transpose_kernel<<<grid, dim3(32, 8), 0, cx->stream>>>(A, lda, m, n, B, ldb);)
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
 }
 
 // General SVD with min(m, n) <= 64: small -> one CTA; tall -> thin_qr then
-// Jacobi on R and S = Q U_R (plus the sign rule on S).
+// Jacobi on R and S = Q U_R (plus the sign rule on S); wide -> via A^T.
 int launch_svd(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, double* S, int64_t lds,
                double* sigma, double* T, int64_t ldt) {
   const int64_t q = m < n ? m : n;
   if (q > 64) return SLRA_ERR_UNSUPPORTED;
   if (svd_smem((int)m, (int)n) <= 200 * 1024) return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt);
-  if (m < n) return SLRA_ERR_UNSUPPORTED;  // wide and large: not on the path
+  if (m < n) {
+    // wide: A^T = S' Sigma T'^T (tall path), so A = T' Sigma S'^T; the sign
+    // rule is then re-applied on the left vectors T' (flipping S' with them).
+    double* At;
+    SLRA_CUDA(cudaMallocAsync(&At, sizeof(double) * (size_t)m * n, cx->stream));
+    int st = launch_transpose(cx, A, lda, m, n, At, n);
+    if (st == SLRA_OK) st = launch_svd(cx, At, n, n, m, T, ldt, sigma, S, lds);
+    if (st == SLRA_OK) st = launch_colsign(cx, S, lds, m, T, ldt, n, m);
+    cudaFreeAsync(At, cx->stream);
+    return st;
+  }
   const int c = (int)n;
   double* ws = static_cast<double*>(cx->partials ? nullptr : nullptr);
   (void)ws;
@@ -405,8 +437,8 @@ int launch_maxvol(Context* cx, const double* A, int64_t lda, int64_t m, int64_t 
   if (smem > 220 * 1024 || r > 64) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(maxvol_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
-  maxvol_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, (int)r, h, (int)max_swaps, qr_first, (int)count,
-                                                   idx, vol, d_status);
+  SLRA_TIMED(cx, "maxvol", maxvol_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, (int)r, h, (int)max_swaps, qr_first, (int)count,
+                                                   idx, vol, d_status);)
   SLRA_CHECK_LAUNCH(cx);
   SLRA_CUDA(cudaMemcpyAsync(cx->hsmall, cx->dsmall, 4, cudaMemcpyDeviceToHost, cx->stream));
   SLRA_CUDA(cudaStreamSynchronize(cx->stream));

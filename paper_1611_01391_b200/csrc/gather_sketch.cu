@@ -208,9 +208,9 @@ int launch_gather_cols(Context* c, const double* A, int64_t lda, int64_t m, cons
   if (gx > cap) gx = cap;
   dim3 grid(gx < 1 ? 1 : gx, static_cast<unsigned>(l));
   if (vec)
-    gather_cols_vec_kernel<<<grid, kNT, 0, c->stream>>>(A, lda, m, J, Cm, ldc);
+    SLRA_TIMED(c, "gather", gather_cols_vec_kernel<<<grid, kNT, 0, c->stream>>>(A, lda, m, J, Cm, ldc);)
   else
-    gather_cols_kernel<<<grid, kNT, 0, c->stream>>>(A, lda, m, J, Cm, ldc);
+    SLRA_TIMED(c, "gather", gather_cols_kernel<<<grid, kNT, 0, c->stream>>>(A, lda, m, J, Cm, ldc);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }
@@ -218,7 +218,7 @@ int launch_gather_cols(Context* c, const double* A, int64_t lda, int64_t m, cons
 int launch_gather_rows(Context* c, const double* A, int64_t lda, int64_t n, const int64_t* I, int64_t k, double* R,
                        int64_t ldr) {
   if (k == 0 || n == 0) return SLRA_OK;
-  gather_rows_kernel<<<grid_1d(c, k * n), kNT, 0, c->stream>>>(A, lda, n, I, k, R, ldr);
+  SLRA_TIMED(c, "gather", gather_rows_kernel<<<grid_1d(c, k * n), kNT, 0, c->stream>>>(A, lda, n, I, k, R, ldr);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }
@@ -226,7 +226,7 @@ int launch_gather_rows(Context* c, const double* A, int64_t lda, int64_t n, cons
 int launch_gather_block(Context* c, const double* A, int64_t lda, const int64_t* I, int64_t k, const int64_t* J,
                         int64_t l, double* G, int64_t ldg) {
   if (k == 0 || l == 0) return SLRA_OK;
-  gather_block_kernel<<<grid_1d(c, k * l), kNT, 0, c->stream>>>(A, lda, I, k, J, l, G, ldg);
+  SLRA_TIMED(c, "gather", gather_block_kernel<<<grid_1d(c, k * l), kNT, 0, c->stream>>>(A, lda, I, k, J, l, G, ldg);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }

@@ -11,6 +11,8 @@ int launch_gather_rows(Context* c, const double* A, int64_t lda, int64_t n, cons
                        int64_t ldr);
 int launch_sketch_cols(Context* c, const double* A, int64_t lda, int64_t m, const int64_t* src, const double* coef,
                        const int32_t* q, int64_t width, int tree, int64_t l, double* out, int64_t ldo);
+int launch_gemm_fam(Context* c, const char* fam, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha,
+                    const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc);
 int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                 int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc);
 int launch_lowrank_residual(Context* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* P,
@@ -37,7 +39,7 @@ int launch_scale_cols(Context* c, double* X, int64_t ldx, int64_t m, int64_t col
   int g = ceil_div(m * cols, 256);
   if (g > c->num_sms * 8) g = c->num_sms * 8;
   if (g < 1) g = 1;
-  scale_cols_kernel<<<g, 256, 0, c->stream>>>(X, ldx, m, cols, s, inv, Y, ldy);
+  SLRA_TIMED(c, "scale", scale_cols_kernel<<<g, 256, 0, c->stream>>>(X, ldx, m, cols, s, inv, Y, ldy);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }
@@ -108,7 +110,7 @@ int slra_range_finder(slra_ctx ctx, const double* M, int64_t ldm, int64_t m, int
   if (variant == 0) {
     // BasisQr: U = Q (thin_qr sign rule already applied), V = U^T M
     SLRA_CUDA(cudaMemcpy2DAsync(U, 8 * ldu, Qm, 8 * m, 8 * m, l, cudaMemcpyDeviceToDevice, cx->stream));
-    SLRA_TRY(launch_gemm(cx, 1, 0, l, n, m, 1.0, U, ldu, M, ldm, 0.0, V, ldv));
+    SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, l, n, m, 1.0, U, ldu, M, ldm, 0.0, V, ldv));
   } else {
     // TruncatedRankR: S = Q U_R with the svd sign rule on S; U = S_r Sigma_r;
     // V = U^+ M = Sigma_r^-1 S_r^T M (U's SVD is S_r, Sigma_r, I).
@@ -117,7 +119,7 @@ int slra_range_finder(slra_ctx ctx, const double* M, int64_t ldm, int64_t m, int
     SLRA_TRY(launch_colsign(cx, S, m, m, VR, l, l, l));
     SLRA_TRY(launch_scale_cols(cx, S, m, m, r, sig, 0, U, ldu));    // U = S_r Sigma_r
     SLRA_TRY(launch_scale_cols(cx, S, m, m, r, sig, 1, Qm, m));     // Qm := S_r Sigma_r^-1
-    SLRA_TRY(launch_gemm(cx, 1, 0, r, n, m, 1.0, Qm, m, M, ldm, 0.0, V, ldv));
+    SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, r, n, m, 1.0, Qm, m, M, ldm, 0.0, V, ldv));
   }
   if (d_out) SLRA_TRY(launch_lowrank_residual(cx, M, ldm, m, n, U, ldu, V, ldv, ucols, d_out));
   return SLRA_OK;

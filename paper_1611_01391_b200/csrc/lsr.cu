@@ -173,9 +173,9 @@ int launch_lsr_residual(Context* c, const double* A, int64_t lda, int64_t m, int
   if (need < grid) grid = (int)(need > 0 ? need : 1);
   double* part = partials(c, grid);
   if (!part) return SLRA_ERR_CUDA;
-  lsr_residual_kernel<<<grid, 256, sizeof(double) * d, c->stream>>>(A, lda, m, (int)d, b, x, part);
+  SLRA_TIMED(c, "lsr_residual", lsr_residual_kernel<<<grid, 256, sizeof(double) * d, c->stream>>>(A, lda, m, (int)d, b, x, part);)
   SLRA_CHECK_LAUNCH(c);
-  sum_kernel<<<1, 256, 0, c->stream>>>(part, grid, d_out);
+  SLRA_TIMED(c, "reduce", sum_kernel<<<1, 256, 0, c->stream>>>(part, grid, d_out);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }
@@ -232,20 +232,20 @@ int slra_sketch_solve(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
   const double tol2 = 1e-20 * dmax;
   const size_t smem = sizeof(double) * (size_t)d * kPW;
   SLRA_CUDA(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  cholesky_kernel<<<1, kLT, smem, st>>>(G, (int)d, tol2, d_status);
+  SLRA_TIMED(cx, "lsr_solve", cholesky_kernel<<<1, kLT, smem, st>>>(G, (int)d, tol2, d_status);)
   SLRA_CHECK_LAUNCH(cx);
   // x = G^{-1} g, then one refinement step x += G^{-1} FA^T (Fb - FA x)
-  chol_solve_kernel<<<1, 32, 0, st>>>(G, (int)d, g, x_hat, y, d_status, 0);
+  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, 32, 0, st>>>(G, (int)d, g, x_hat, y, d_status, 0);)
   SLRA_CHECK_LAUNCH(cx);
-  lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);
+  SLRA_TIMED(cx, "lsr_solve", lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);)
   SLRA_CHECK_LAUNCH(cx);
   SLRA_TRY(launch_gemm(cx, 1, 0, d, 1, k, 1.0, FW, k, r, k, 0.0, cvec, d));
-  chol_solve_kernel<<<1, 32, 0, st>>>(G, (int)d, cvec, x_hat, y, d_status, 1);
+  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, 32, 0, st>>>(G, (int)d, cvec, x_hat, y, d_status, 1);)
   SLRA_CHECK_LAUNCH(cx);
   // sketched residual ||FA x - Fb|| by a direct pass
-  lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);
+  SLRA_TIMED(cx, "lsr_solve", lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);)
   SLRA_CHECK_LAUNCH(cx);
-  sum_kernel<<<1, 256, 0, st>>>(part, rgrid, out);
+  SLRA_TIMED(cx, "reduce", sum_kernel<<<1, 256, 0, st>>>(part, rgrid, out);)
   SLRA_CHECK_LAUNCH(cx);
   SLRA_CUDA(cudaMemcpyAsync(hs, out, 8, cudaMemcpyDeviceToHost, st));
   SLRA_CUDA(cudaMemcpyAsync(hs + 1, d_status, 4, cudaMemcpyDeviceToHost, st));

@@ -223,9 +223,9 @@ int launch_lowrank_residual(Context* c, const double* A, int64_t lda, int64_t m,
   double* part = partials(c, 2 * grid);
   if (!part) return SLRA_ERR_CUDA;
   a.out = part;
-  lowrank_residual_kernel<<<grid, kRT, 0, c->stream>>>(a);
+  SLRA_TIMED(c, "residual", lowrank_residual_kernel<<<grid, kRT, 0, c->stream>>>(a);)
   SLRA_CHECK_LAUNCH(c);
-  reduce_pairs_kernel<<<1, 256, 0, c->stream>>>(part, grid, d_out);
+  SLRA_TIMED(c, "residual_reduce", reduce_pairs_kernel<<<1, 256, 0, c->stream>>>(part, grid, d_out);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }
@@ -236,7 +236,7 @@ int launch_lowrank_residual_batched(Context* c, const double* A, int64_t lda, in
   ResidualArgs a{A, lda, m, n, P, ldp, Q, ldq, inner, nprob, sA, sP, sQ, d_out_pairs, 1};
   int grid = c->num_sms * 2;
   if (nprob < grid) grid = (int)nprob;
-  lowrank_residual_batched_kernel<<<grid, kRT, 0, c->stream>>>(a);
+  SLRA_TIMED(c, "residual_batched", lowrank_residual_batched_kernel<<<grid, kRT, 0, c->stream>>>(a);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }
@@ -363,7 +363,7 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int64_t m,
   }
 }
 
-int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+int launch_gemm_fam(Context* c, const char* fam, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                 int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc) {
   if (m == 0 || n == 0) return SLRA_OK;
   GemmArgs g{ta, tb, m, n, k, alpha, beta, A, lda, B, ldb, Cm, ldc, k, nullptr};
@@ -384,17 +384,22 @@ int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, dou
     double* part = static_cast<double*>(workspace(c, sizeof(double) * m * n * nz));
     if (!part) return SLRA_ERR_CUDA;
     g.partial = part;
-    gemm_kernel<<<dim3(gx, gy, nz), kRT, 0, c->stream>>>(g);
+    SLRA_TIMED(c, fam, gemm_kernel<<<dim3(gx, gy, nz), kRT, 0, c->stream>>>(g);)
     SLRA_CHECK_LAUNCH(c);
     int rg = ceil_div(m * n, 256);
     if (rg > c->num_sms * 8) rg = c->num_sms * 8;
-    splitk_reduce_kernel<<<rg, 256, 0, c->stream>>>(part, m, n, nz, alpha, beta, Cm, ldc);
+    SLRA_TIMED(c, "gemm_reduce", splitk_reduce_kernel<<<rg, 256, 0, c->stream>>>(part, m, n, nz, alpha, beta, Cm, ldc);)
     SLRA_CHECK_LAUNCH(c);
     return SLRA_OK;
   }
-  gemm_kernel<<<dim3(gx, gy, 1), kRT, 0, c->stream>>>(g);
+  SLRA_TIMED(c, fam, gemm_kernel<<<dim3(gx, gy, 1), kRT, 0, c->stream>>>(g);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
+}
+
+int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc) {
+  return launch_gemm_fam(c, "gemm", ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, Cm, ldc);
 }
 
 }  // namespace slra_dev

@@ -73,6 +73,17 @@ void* arena(Context* c, int slot, size_t bytes) {
   return c->arena[slot];
 }
 
+cudaEvent_t pooled_event(Context* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
 }  // namespace slra_dev
 
 using namespace slra_dev;
@@ -143,6 +154,11 @@ int slra_ctx_destroy(slra_ctx ctx) {
   if (c->dsmall) cudaFree(c->dsmall);
   for (int i = 0; i < 4; ++i)
     if (c->arena[i]) cudaFree(c->arena[i]);
+  for (auto& r : c->records) {
+    cudaEventDestroy(r.start);
+    cudaEventDestroy(r.stop);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->hsmall) cudaFreeHost(c->hsmall);
   if (c->owns_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -157,6 +173,50 @@ int slra_ctx_synchronize(slra_ctx ctx) {
 void* slra_ctx_stream(slra_ctx ctx) { return C(ctx)->stream; }
 
 int64_t slra_ctx_launch_count(slra_ctx ctx) { return C(ctx)->launches; }
+
+int slra_ctx_set_timing(slra_ctx ctx, int on) {
+  Context* c = C(ctx);
+  SLRA_CUDA(cudaStreamSynchronize(c->stream));
+  for (auto& r : c->records) {
+    c->event_pool.push_back(r.start);
+    c->event_pool.push_back(r.stop);
+  }
+  c->records.clear();
+  c->timing = on != 0;
+  return SLRA_OK;
+}
+
+int slra_ctx_timing_report(slra_ctx ctx, char* buf, int64_t len) {
+  Context* c = C(ctx);
+  SLRA_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<std::string> fams;
+  std::vector<double> ms;
+  std::vector<int64_t> cnt;
+  for (auto& r : c->records) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.start, r.stop);
+    size_t i = 0;
+    while (i < fams.size() && fams[i] != r.family) ++i;
+    if (i == fams.size()) {
+      fams.push_back(r.family);
+      ms.push_back(0.0);
+      cnt.push_back(0);
+    }
+    ms[i] += t;
+    cnt[i] += 1;
+  }
+  std::string out;
+  for (size_t i = 0; i < fams.size(); ++i) {
+    char tmp[160];
+    snprintf(tmp, sizeof(tmp), "%s%s=%.6f,%lld", i ? ";" : "", fams[i].c_str(), ms[i], (long long)cnt[i]);
+    out += tmp;
+  }
+  if (buf && len > 0) {
+    strncpy(buf, out.c_str(), (size_t)len - 1);
+    buf[len - 1] = 0;
+  }
+  return SLRA_OK;
+}
 
 int slra_device_alloc(slra_ctx ctx, int64_t bytes, void** d_out) {
   (void)ctx;

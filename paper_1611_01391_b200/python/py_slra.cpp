@@ -84,6 +84,26 @@ PYBIND11_MODULE(_slra, m) {
   m.def("set_device", [](int dev, uintptr_t stream) { set_device(dev, reinterpret_cast<void*>(stream)); },
         py::arg("device") = 0, py::arg("stream") = 0);
   m.def("launch_count", []() { return slra_ctx_launch_count(device_context()); });
+  m.def("set_timing", [](bool on) { check(slra_ctx_set_timing(device_context(), on ? 1 : 0), "set_timing"); });
+  m.def("timing_report", []() {
+    std::vector<char> buf(1 << 16);
+    check(slra_ctx_timing_report(device_context(), buf.data(), (int64_t)buf.size()), "timing_report");
+    py::dict d;
+    std::string s(buf.data());
+    size_t pos = 0;
+    while (pos < s.size()) {
+      size_t end = s.find(';', pos);
+      if (end == std::string::npos) end = s.size();
+      const std::string item = s.substr(pos, end - pos);
+      const size_t eq = item.find('='), comma = item.find(',');
+      if (eq != std::string::npos && comma != std::string::npos)
+        d[py::str(item.substr(0, eq))] = py::make_tuple(std::stod(item.substr(eq + 1, comma - eq - 1)),
+                                                        std::stoll(item.substr(comma + 1)));
+      pos = end + 1;
+    }
+    return d;
+  });
+  m.def("stream_ptr", []() { return reinterpret_cast<uintptr_t>(slra_ctx_stream(device_context())); });
   m.def("synchronize", []() { check(slra_ctx_synchronize(device_context()), "synchronize"); });
 
   py::class_<Rng>(m, "Rng", py::module_local())
@@ -237,6 +257,24 @@ PYBIND11_MODULE(_slra, m) {
   });
   m.def("gen_cauchy_block", [](Index mm, Index n, Rng& rng) { return to_np(gen_cauchy_block(mm, n, rng)); });
   m.def("gen_log_kernel_block", [](Index mm, Index n, Rng& rng) { return to_np(gen_log_kernel_block(mm, n, rng)); });
+
+  // ---- end-to-end form of range_finder(M, H, r, variant) (lra.hpp): M read
+  // straight from the caller's (pinned) host buffer, U/V returned to the host.
+  m.def("range_finder_host", [](uintptr_t M_host, Index mm, Index n, const PyOp& H, Index r, bool truncated) {
+    const SketchPlan plan = compile_plan(*H.p, Side::Right);
+    static DeviceMatrix* staging = new DeviceMatrix();  // reused HBM staging buffer (never freed)
+    if (staging->rows() != mm || staging->cols() != n) *staging = DeviceMatrix(mm, n);
+    DeviceMatrix& dM = *staging;
+    check(slra_memcpy_h2d(device_context(), dM.data(), reinterpret_cast<const void*>(M_host), 8 * mm * n),
+          "range_finder_host");
+    const Index uc = truncated ? r : H.p->cols();
+    DeviceMatrix dU(mm, uc), dV(uc, n);
+    DevBuf<double> out(2);
+    range_finder_device(dM, plan, r, truncated ? RangeVariant::TruncatedRankR : RangeVariant::BasisQr, dU, dV,
+                        out.get());
+    auto o = out.download();
+    return py::make_tuple(to_np(dU.download()), to_np(dV.download()), o[0], o[1]);
+  });
 
   // ---- device-resident entry points (raw device pointers)
   m.def("range_finder_device", [](uintptr_t M, Index ldm, Index mm, Index n, const py::dict& plan, Index r,
