@@ -113,6 +113,8 @@ def load_peaks():
     try:
         best = 0.0
         for line in open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.jsonl")):
+            if not line.strip():
+                continue
             d = json.loads(line)
             if d.get("kind", "").startswith("dmma"):
                 best = max(best, d["tflops"])
