@@ -97,12 +97,12 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
     }
   }
   __syncthreads();
-  cta_thin_qr<NT>(s.S, len, len, nidx, s.R, nidx, s.tau, s.rv);
+  cta_thin_qr<NT>(s.S, len, len, nidx, s.W, len, s.R, nidx, s.tau, s.rv);  // Q -> W
   const int rq = count < nidx ? count : nidx;
-  ColPivScratch cs{s.W, len, s.p2r, s.nu, s.nd, s.v, s.tau, s.rv, s.ri};
-  cta_colpiv_init<NT>(s.S, len, len, rq, cs, s.tmpidx);
+  ColPivScratch cs{s.S, len, s.p2r, s.nu, s.nd, s.v, s.tau, s.rv, s.ri};
+  cta_colpiv_init<NT>(s.W, len, len, rq, cs, s.tmpidx);
   __syncthreads();
-  const int st = cta_maxvol_swaps<NT>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, s.W, len, s.Gt, rq, s.perm, s.tau,
+  const int st = cta_maxvol_swaps<NT>(s.W, len, len, rq, h, 4 * rq, s.tmpidx, s.S, len, s.Gt, rq, s.perm, s.tau,
                                       s.nu, s.nd, s.rv, s.ri, s.flag);
   if (st != SLRA_OK) return st;
   __syncthreads();
@@ -113,7 +113,7 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
     // equal norms: lower index first.
     for (int i = tid; i < len; i += NT) {
       double acc = 0.0;
-      for (int j = 0; j < nidx; ++j) acc += s.S[i + j * len] * s.S[i + j * len];
+      for (int j = 0; j < nidx; ++j) acc += s.W[i + j * len] * s.W[i + j * len];
       s.nu[i] = sqrt(acc);
     }
     __syncthreads();
@@ -134,7 +134,7 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
     if (count == nidx) {
       for (int e = tid; e < count * nidx; e += NT) {
         const int a = e % count, b = e / count;
-        s.Gt[a + b * count] = s.S[idx_out[a] + b * len];
+        s.Gt[a + b * count] = s.W[idx_out[a] + b * len];
       }
       __syncthreads();
       if (tid < 32) {

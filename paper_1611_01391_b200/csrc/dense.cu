@@ -24,8 +24,7 @@ __global__ void __launch_bounds__(kDT) thin_qr_cta_kernel(const double* __restri
   double* red = tau + c;           // 40
   for (int e = threadIdx.x; e < m * c; e += kDT) S[e] = A[(e % m) + (int64_t)(e / m) * lda];
   __syncthreads();
-  cta_thin_qr<kDT>(S, m, m, c, Rs, c, tau, red);
-  for (int e = threadIdx.x; e < m * c; e += kDT) Q[(e % m) + (int64_t)(e / m) * ldq] = S[e];
+  cta_thin_qr<kDT>(S, m, m, c, Q, (int)ldq, Rs, c, tau, red);
   if (R)
     for (int e = threadIdx.x; e < c * c; e += kDT) R[(e % c) + (int64_t)(e / c) * ldr] = Rs[e];
 }
@@ -66,70 +65,76 @@ __global__ void __launch_bounds__(kDT) tsqr_top_kernel(const double* __restrict_
                                                        int Lp, double* __restrict__ Qt, int64_t ldqt,
                                                        double* __restrict__ R, int64_t ldr) {
   extern __shared__ __align__(16) double sm[];
-  double* S = sm;                     // Lp x c
+  double* S = sm;                     // rows x c (rows <= Lp, rows >= c)
   double* Rs = S + (size_t)Lp * c;    // c x c
   double* tau = Rs + c * c;
   double* red = tau + c;
-  for (int e = threadIdx.x; e < Lp * c; e += kDT) {
-    const int i = e % Lp, j = e / Lp;
-    S[e] = i < rows ? X[i + (int64_t)j * ldx] : 0.0;
-  }
+  for (int e = threadIdx.x; e < rows * c; e += kDT) S[e] = X[(e % rows) + (int64_t)(e / rows) * ldx];
   __syncthreads();
-  cta_thin_qr<kDT>(S, Lp, Lp, c, Rs, c, tau, red);
-  for (int e = threadIdx.x; e < rows * c; e += kDT) {
-    const int i = e % rows, j = e / rows;
-    Qt[i + (int64_t)j * ldqt] = S[i + j * Lp];
-  }
+  cta_thin_qr<kDT>(S, rows, rows, c, Qt, (int)ldqt, Rs, c, tau, red);
   if (R)
     for (int e = threadIdx.x; e < c * c; e += kDT) R[(e % c) + (int64_t)(e / c) * ldr] = Rs[e];
 }
 
 // Expand step: Q_b = H_0 ... H_{c-1} [Qp(b*c : b*c+c, :); 0] (Lp x c), store
-// the first nr rows at Qo rows [b*L, ...).
+// the first nr rows at Qo rows [b*L, ...). Reflectors staged in smem; each
+// warp carries its output columns in registers (no block barriers).
+template <int RPL>
 __global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restrict__ Qp, int64_t ldqp,
                                                           const double* __restrict__ Vst,
                                                           const double* __restrict__ taust, int64_t rows, int c,
                                                           int Lp, double* __restrict__ Qo, int64_t ldqo) {
   extern __shared__ __align__(16) double sm[];
-  double* Y = sm;  // Lp x c
+  double* V = sm;            // Lp x c reflectors
+  double* tau = V + (size_t)Lp * c;
   const int64_t b = blockIdx.x;
   const int64_t r0 = b * kLeaf;
   const int nr = (int)((rows - r0) < kLeaf ? (rows - r0) : kLeaf);
-  const double* V = Vst + b * (int64_t)Lp * c;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < Lp * c; e += kDT) {
-    const int i = e % Lp, j = e / Lp;
-    Y[e] = i < c ? Qp[(b * c + i) + (int64_t)j * ldqp] : 0.0;
-  }
+  const double* Vg = Vst + b * (int64_t)Lp * c;
+  for (int e = threadIdx.x; e < Lp * c; e += kDT) V[e] = Vg[e];
+  for (int j = threadIdx.x; j < c; j += kDT) tau[j] = taust[b * c + j];
   __syncthreads();
-  for (int k = c - 1; k >= 0; --k) {
-    const double t = taust[b * c + k];
-    if (t != 0.0) {
-      const double* v = V + (int64_t)k * Lp;
-      for (int j = warp; j < c; j += kDT / 32) {
-        double* y = Y + j * Lp;
-        double w = 0.0;
-        for (int i = k + 1 + lane; i < Lp; i += 32) w += v[i] * y[i];
-        w = warp_sum(w);
-        w += y[k];
-        __syncwarp();
-        if (lane == 0) y[k] -= t * w;
-        for (int i = k + 1 + lane; i < Lp; i += 32) y[i] -= t * v[i] * w;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < c; j += kDT / 32) {
+    double y[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      y[r] = i < c ? Qp[(b * c + i) + (int64_t)j * ldqp] : 0.0;
+    }
+    for (int k = c - 1; k >= 0; --k) {
+      const double t = tau[k];
+      if (t == 0.0) continue;
+      const double* v = V + (size_t)k * Lp;
+      double w = 0.0, yk = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i > k && i < Lp) w += v[i] * y[r];
+        if (i == k) yk = y[r];
+      }
+      w = warp_sum(w);
+      w += __shfl_sync(0xffffffffu, yk, k & 31);
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i > k && i < Lp) y[r] -= t * v[i] * w;
+        if (i == k) y[r] -= t * w;
       }
     }
-    __syncthreads();
-  }
-  for (int e = threadIdx.x; e < nr * c; e += kDT) {
-    const int i = e % nr, j = e / nr;
-    Qo[(r0 + i) + (int64_t)j * ldqo] = Y[i + j * Lp];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i < nr) Qo[(r0 + i) + (int64_t)j * ldqo] = y[r];
+    }
   }
 }
 
-static size_t qr_cta_smem(int m, int c) { return sizeof(double) * ((size_t)m * c + (size_t)c * c + c + 48); }
+static size_t qr_cta_smem(int m, int c) { return sizeof(double) * ((size_t)m * c + (size_t)c * c + c + 112); }
 
 int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, double* Q, int64_t ldq, double* R,
                    int64_t ldr) {
-  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 4096) {
+  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 1024) {
     const size_t smem = qr_cta_smem((int)m, c);
     SLRA_CUDA(cudaFuncSetAttribute(thin_qr_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SLRA_TIMED(cx, "thin_qr", thin_qr_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, c, Q, ldq, R, ldr);)
@@ -162,7 +167,7 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
   total += 2 * (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c + (size_t)top_rows * c;
   double* ws = static_cast<double*>(workspace(cx, sizeof(double) * total));
   if (!ws) return SLRA_ERR_CUDA;
-  const size_t sm_red = sizeof(double) * ((size_t)Lp * c + c + 48);
+  const size_t sm_red = sizeof(double) * ((size_t)Lp * c + c + 112);
   SLRA_CUDA(cudaFuncSetAttribute(tsqr_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_red));
   const double* X = A;
   int64_t ldx = lda;
@@ -177,15 +182,16 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
     ldx = nb * c;
   }
   // top
-  const size_t sm_top = sizeof(double) * ((size_t)Lp * c + (size_t)c * c + c + 48);
+  const size_t sm_top = sizeof(double) * ((size_t)Lp * c + (size_t)c * c + c + 112);
   SLRA_CUDA(cudaFuncSetAttribute(tsqr_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_top));
   double* qbuf[2] = {ws + offQ, ws + offQ + (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c};
   double* Qtop = ws + offQ + 2 * (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c;
   SLRA_TIMED(cx, "thin_qr", tsqr_top_kernel<<<1, kDT, sm_top, cx->stream>>>(X, ldx, (int)top_rows, c, Lp, Qtop, top_rows, R, ldr);)
   SLRA_CHECK_LAUNCH(cx);
   // expand top-down
-  const size_t sm_exp = sizeof(double) * (size_t)Lp * c;
-  SLRA_CUDA(cudaFuncSetAttribute(tsqr_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_exp));
+  const size_t sm_exp = sizeof(double) * ((size_t)Lp * c + c);
+  SLRA_CUDA(cudaFuncSetAttribute(tsqr_expand_kernel<kLeaf / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm_exp));
   const double* Qp = Qtop;
   int64_t ldqp = top_rows;
   for (int lv = (int)level_rows.size() - 1; lv >= 0; --lv) {
@@ -200,7 +206,7 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
       Qo = qbuf[lv & 1];
       ldqo = lr;
     }
-    SLRA_TIMED(cx, "thin_qr", tsqr_expand_kernel<<<(unsigned)nb, kDT, sm_exp, cx->stream>>>(Qp, ldqp, ws + offV[lv], ws + offT[lv], lr, c, Lp,
+    SLRA_TIMED(cx, "thin_qr", tsqr_expand_kernel<kLeaf / 32><<<(unsigned)nb, kDT, sm_exp, cx->stream>>>(Qp, ldqp, ws + offV[lv], ws + offT[lv], lr, c, Lp,
                                                                   Qo, ldqo);)
     SLRA_CHECK_LAUNCH(cx);
     Qp = Qo;
@@ -371,15 +377,20 @@ __global__ void __launch_bounds__(kDT) maxvol_cta_kernel(const double* __restric
   double* v = tau + r;                  // r
   double* nu = v + r;                   // m
   double* nd = nu + m;                  // m
-  double* rv = nd + m;                  // 40
-  int64_t* ri = reinterpret_cast<int64_t*>(rv + 40);  // 40
+  double* rv = nd + m;                  // 112 (reduction scratch, >= r + 8)
+  int64_t* ri = reinterpret_cast<int64_t*>(rv + 112);  // 40
   int* p2r = reinterpret_cast<int*>(ri + 40);         // m
   int* I = p2r + m;                                   // count
   int* perm = I + (count > r ? count : r);            // r
   int* flag = perm + r;                               // 4
   for (int e = threadIdx.x; e < m * r; e += kDT) S[e] = A[(e % m) + (int64_t)(e / m) * lda];
   __syncthreads();
-  if (qr_first) cta_thin_qr<kDT>(S, m, m, r, Rs, r, tau, rv);
+  if (qr_first) {
+    cta_thin_qr<kDT>(S, m, m, r, W, m, Rs, r, tau, rv);  // Q -> W, then swap roles
+    double* t = S;
+    S = W;
+    W = t;
+  }
   const int rq = count < r ? count : r;
   ColPivScratch cs{W, m, p2r, nu, nd, v, tau, rv, ri};
   cta_colpiv_init<kDT>(S, m, m, rq, cs, I);
@@ -427,14 +438,14 @@ __global__ void __launch_bounds__(kDT) maxvol_cta_kernel(const double* __restric
 
 static size_t maxvol_smem(int m, int r, int count) {
   const int cm = count > r ? count : r;
-  return sizeof(double) * (2 * (size_t)m * r + 2 * (size_t)r * r + 2 * (size_t)r + 2 * (size_t)m + 40) +
+  return sizeof(double) * (2 * (size_t)m * r + 2 * (size_t)r * r + 2 * (size_t)r + 2 * (size_t)m + 112) +
          sizeof(int64_t) * 40 + sizeof(int) * ((size_t)m + cm + r + 8);
 }
 
 int launch_maxvol(Context* cx, const double* A, int64_t lda, int64_t m, int64_t r, double h, int64_t max_swaps,
                   int qr_first, int64_t count, int64_t* idx, double* vol) {
   const size_t smem = maxvol_smem((int)m, (int)r, (int)count);
-  if (smem > 220 * 1024 || r > 64) return SLRA_ERR_UNSUPPORTED;
+  if (smem > 220 * 1024 || r > 64 || (qr_first && m > 1024)) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(maxvol_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
   SLRA_TIMED(cx, "maxvol", maxvol_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, (int)r, h, (int)max_swaps, qr_first, (int)count,

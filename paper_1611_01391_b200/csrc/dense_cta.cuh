@@ -22,40 +22,51 @@ constexpr double kEps = 2.220446049250313e-16;
 
 // ---------------------------------------------------------------- Householder QR
 // A (m x c, ld lda) in smem. On exit: R on/above the diagonal, essential
-// Householder parts below, tau[0..min(m,c)).
+// Householder parts below, tau[0..min(m,c)). Warp w owns columns j = w mod
+// NW; the owner of column j+1 accumulates its next tail norm while applying
+// reflector j, so each column costs two block barriers. `red` >= c + 8.
 template <int NT>
 __device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   const int size = m < c ? m : c;
+  double* tn = red;  // tn[j] = sum_{i>j} A(i,j)^2 when step j starts
+  if (size > 0 && warp == 0) {
+    double s = 0.0;
+    for (int i = 1 + lane; i < m; i += 32) s += A[i] * A[i];
+    s = warp_sum(s);
+    if (lane == 0) tn[0] = s;
+  }
+  __syncthreads();
   for (int j = 0; j < size; ++j) {
     double* x = A + j * lda;
-    double s = 0.0;
-    for (int i = j + 1 + tid; i < m; i += NT) s += x[i] * x[i];
-    s = block_sum<NT>(s, red);
-    const double c0 = x[j];
-    double t, beta;
-    if (s <= DBL_MIN) {
-      t = 0.0;
-      beta = c0;
-      for (int i = j + 1 + tid; i < m; i += NT) x[i] = 0.0;
-    } else {
-      beta = sqrt(c0 * c0 + s);
-      if (c0 >= 0.0) beta = -beta;
-      const double den = c0 - beta;
-      for (int i = j + 1 + tid; i < m; i += NT) x[i] = x[i] / den;
-      t = (beta - c0) / beta;
+    if (warp == j % NW) {
+      const double s = tn[j];
+      const double c0 = x[j];
+      double t, beta;
+      if (s <= DBL_MIN) {  // Eigen makeHouseholder: tau = 0, beta = c0
+        t = 0.0;
+        beta = c0;
+        for (int i = j + 1 + lane; i < m; i += 32) x[i] = 0.0;
+      } else {
+        beta = sqrt(c0 * c0 + s);
+        if (c0 >= 0.0) beta = -beta;
+        const double den = c0 - beta;
+        for (int i = j + 1 + lane; i < m; i += 32) x[i] = x[i] / den;
+        t = (beta - c0) / beta;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        x[j] = beta;
+        tau[j] = t;
+      }
     }
     __syncthreads();
-    if (tid == 0) {
-      x[j] = beta;
-      tau[j] = t;
-    }
-    if (m - j == 1) {
-      // rows() == 1: *this *= (1 - tau) (no-op since tau = 0)
-    } else if (t != 0.0) {
-      for (int k = j + 1 + warp; k < c; k += NW) {
-        double* a = A + k * lda;
+    const double t = tau[j];
+    const bool apply = (m - j > 1) && t != 0.0;  // rows()==1 or tau==0: identity
+    for (int k = j + 1 + ((warp - (j + 1) % NW + NW) % NW); k < c; k += NW) {
+      double* a = A + k * lda;
+      if (apply) {
         double w = 0.0;
         for (int i = j + 1 + lane; i < m; i += 32) w += x[i] * a[i];
         w = warp_sum(w);
@@ -64,68 +75,85 @@ __device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, doub
         if (lane == 0) a[j] -= t * w;
         for (int i = j + 1 + lane; i < m; i += 32) a[i] -= t * x[i] * w;
       }
-    }
-    __syncthreads();
-  }
-}
-
-// In place: reflectors (below diag) + tau -> explicit Q (m x c). The upper
-// triangle is overwritten (save R first).
-template <int NT>
-__device__ void cta_form_q(double* A, int lda, int m, int c, const double* tau) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = NT / 32;
-  // zero the strict upper triangle of the trailing columns handled below
-  for (int k = c - 1; k >= 0; --k) {
-    const double t = tau[k];
-    double* v = A + k * lda;  // v[k] := 1 implicitly, v[i>k] essential
-    if (k < c - 1) {
-      for (int jj = k + 1 + warp; jj < c; jj += NW) {
-        double* a = A + jj * lda;
-        double w = 0.0;
-        for (int i = k + 1 + lane; i < m; i += 32) w += v[i] * a[i];
-        w = warp_sum(w);
-        w += a[k];  // v_k = 1
+      if (k == j + 1) {
         __syncwarp();
-        if (lane == 0) a[k] -= t * w;
-        for (int i = k + 1 + lane; i < m; i += 32) a[i] -= t * v[i] * w;
+        double s = 0.0;
+        for (int i = k + 1 + lane; i < m; i += 32) s += a[i] * a[i];
+        s = warp_sum(s);
+        if (lane == 0) tn[k] = s;
       }
     }
     __syncthreads();
-    for (int i = tid; i < m; i += NT) {
-      if (i < k) v[i] = 0.0;
-      else if (i == k) v[i] = 1.0 - t;
-      else v[i] = -t * v[i];
-    }
-    __syncthreads();
   }
 }
 
-// thin_qr: A (m x c, m >= c) in smem -> Q in place, R (c x c, ld ldr) in smem,
-// both sign-fixed so R(i,i) >= 0.
+// Explicit thin Q = H_0 H_1 ... H_{c-1} [I_c; 0] (m x c) from the reflectors
+// stored below the diagonal of V (ld ldv) and tau, written to Q (ld ldq, smem
+// or global, must not alias V). Column j = H_0 ... H_j e_j is built in the
+// registers of the warp that owns it (RPL rows per lane): no block barriers.
+template <int NT, int RPL>
+__device__ void cta_form_q_regs(const double* V, int ldv, int m, int c, const double* tau, double* Q, int ldq) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  for (int j = warp; j < c; j += NW) {
+    double y[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) y[r] = (lane + 32 * r == j) ? 1.0 : 0.0;
+    for (int k = j; k >= 0; --k) {
+      const double t = tau[k];
+      if (t == 0.0) continue;
+      const double* v = V + k * ldv;
+      double w = 0.0, yk = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i > k && i < m) w += v[i] * y[r];
+        if (i == k) yk = y[r];
+      }
+      w = warp_sum(w);
+      w += __shfl_sync(0xffffffffu, yk, k & 31);
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i > k && i < m) y[r] -= t * v[i] * w;
+        if (i == k) y[r] -= t * w;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i < m) Q[i + (int64_t)j * ldq] = y[r];
+    }
+  }
+}
+
 template <int NT>
-__device__ void cta_thin_qr(double* A, int lda, int m, int c, double* R, int ldr, double* tau, double* red) {
+__device__ void cta_form_q(const double* V, int ldv, int m, int c, const double* tau, double* Q, int ldq) {
+  if (m <= 256) cta_form_q_regs<NT, 8>(V, ldv, m, c, tau, Q, ldq);
+  else if (m <= 512) cta_form_q_regs<NT, 16>(V, ldv, m, c, tau, Q, ldq);
+  else cta_form_q_regs<NT, 32>(V, ldv, m, c, tau, Q, ldq);  // m <= 1024
+}
+
+// thin_qr (linalg.cpp:67-79): A (m x c, m >= c, m <= 1024) in smem is
+// factorised in place; Q (m x c, ld ldq, smem or global, distinct from A)
+// and R (c x c, ld ldr, smem) are sign-fixed so R(i,i) >= 0.
+template <int NT>
+__device__ void cta_thin_qr(double* A, int lda, int m, int c, double* Q, int ldq, double* R, int ldr, double* tau,
+                            double* red) {
   cta_house_qr<NT>(A, lda, m, c, tau, red);
+  cta_form_q<NT>(A, lda, m, c, tau, Q, ldq);
   for (int e = threadIdx.x; e < c * c; e += NT) {
     const int i = e % c, j = e / c;
-    R[i + j * ldr] = (i <= j) ? A[i + j * lda] : 0.0;
+    const double rii = A[i + i * lda];
+    double v = (i <= j) ? A[i + j * lda] : 0.0;
+    if (rii < 0.0) v = -v;  // flip row i of R
+    R[i + j * ldr] = v;
   }
   __syncthreads();
-  cta_form_q<NT>(A, lda, m, c, tau);
-  // sign rule: R(i,i) < 0 -> flip row i of R and column i of Q
   for (int e = threadIdx.x; e < m * c; e += NT) {
     const int i = e % m, j = e / m;
-    if (R[j + j * ldr] < 0.0) A[i + j * lda] = -A[i + j * lda];
+    if (A[j + j * lda] < 0.0) Q[i + (int64_t)j * ldq] = -Q[i + (int64_t)j * ldq];  // and column i of Q
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < c * c; e += NT) {
-    const int i = e % c, j = e / c;
-    const double d = R[i + i * ldr];
-    if (d < 0.0 && j != i) R[i + j * ldr] = -R[i + j * ldr];
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < c; i += NT)
-    if (R[i + i * ldr] < 0.0) R[i + i * ldr] = -R[i + i * ldr];
   __syncthreads();
 }
 
@@ -443,6 +471,7 @@ __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv,
   constexpr int NW = NT / 32;
   for (int e = tid; e < n * n; e += NT) V[e % n + (e / n) * ldv] = (e % n == e / n) ? 1.0 : 0.0;
   const int ne = n + (n & 1);  // even number of players (dummy = n)
+  const double tol = sqrt((double)p) * kEps;
   __syncthreads();
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) flag[0] = 0;
@@ -471,7 +500,10 @@ __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv,
         aa = warp_sum(aa);
         bb = warp_sum(bb);
         gg = warp_sum(gg);
-        if (gg == 0.0 || fabs(gg) <= kEps * sqrt(aa * bb)) continue;
+        // convergence test of LAPACK dgesvj: |<w_p, w_q>| <= sqrt(p) eps ||w_p|| ||w_q||
+        // (a bare eps threshold never settles once the dot products are
+        // evaluated in a different order than the rotation was computed)
+        if (gg == 0.0 || fabs(gg) <= tol * sqrt(aa * bb)) continue;
         const double zeta = (bb - aa) / (2.0 * gg);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double cs = 1.0 / sqrt(1.0 + t * t);
