@@ -210,7 +210,11 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1611_01391_b200 as slra
-    stream = torch.cuda.current_stream()
+    # one dedicated stream for the product, the L2 flush and the CUDA events
+    # (the legacy default stream has handle 0, which the C-ABI would replace
+    # by a private stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     slra.set_device(local, stream.cuda_stream)
     peaks = load_peaks()
 

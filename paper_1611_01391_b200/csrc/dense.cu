@@ -10,7 +10,7 @@
 
 namespace slra_dev {
 
-constexpr int kDT = 256;
+constexpr int kDT = 512;
 constexpr int kLeaf = 256;  // TSQR leaf rows
 
 // ---------------------------------------------------------------- single-CTA thin QR
@@ -134,7 +134,7 @@ static size_t qr_cta_smem(int m, int c) { return sizeof(double) * ((size_t)m * c
 
 int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, double* Q, int64_t ldq, double* R,
                    int64_t ldr) {
-  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 1024) {
+  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 512) {
     const size_t smem = qr_cta_smem((int)m, c);
     SLRA_CUDA(cudaFuncSetAttribute(thin_qr_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SLRA_TIMED(cx, "thin_qr", thin_qr_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, c, Q, ldq, R, ldr);)
@@ -445,7 +445,7 @@ static size_t maxvol_smem(int m, int r, int count) {
 int launch_maxvol(Context* cx, const double* A, int64_t lda, int64_t m, int64_t r, double h, int64_t max_swaps,
                   int qr_first, int64_t count, int64_t* idx, double* vol) {
   const size_t smem = maxvol_smem((int)m, (int)r, (int)count);
-  if (smem > 220 * 1024 || r > 64 || (qr_first && m > 1024)) return SLRA_ERR_UNSUPPORTED;
+  if (smem > 220 * 1024 || r > 64 || (qr_first && m > 512)) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(maxvol_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
   SLRA_TIMED(cx, "maxvol", maxvol_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, (int)r, h, (int)max_swaps, qr_first, (int)count,

@@ -25,15 +25,19 @@ constexpr double kEps = 2.220446049250313e-16;
 // Householder parts below, tau[0..min(m,c)). Warp w owns columns j = w mod
 // NW; the owner of column j+1 accumulates its next tail norm while applying
 // reflector j, so each column costs two block barriers. `red` >= c + 8.
-template <int NT>
-__device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, double* red) {
+template <int NT, int RPL>
+__device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   const int size = m < c ? m : c;
   double* tn = red;  // tn[j] = sum_{i>j} A(i,j)^2 when step j starts
   if (size > 0 && warp == 0) {
     double s = 0.0;
-    for (int i = 1 + lane; i < m; i += 32) s += A[i] * A[i];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i >= 1 && i < m) s += A[i] * A[i];
+    }
     s = warp_sum(s);
     if (lane == 0) tn[0] = s;
   }
@@ -47,12 +51,20 @@ __device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, doub
       if (s <= DBL_MIN) {  // Eigen makeHouseholder: tau = 0, beta = c0
         t = 0.0;
         beta = c0;
-        for (int i = j + 1 + lane; i < m; i += 32) x[i] = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          if (i > j && i < m) x[i] = 0.0;
+        }
       } else {
         beta = sqrt(c0 * c0 + s);
         if (c0 >= 0.0) beta = -beta;
-        const double den = c0 - beta;
-        for (int i = j + 1 + lane; i < m; i += 32) x[i] = x[i] / den;
+        const double rden = 1.0 / (c0 - beta);  // essential = tail / (c0 - beta)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          if (i > j && i < m) x[i] *= rden;
+        }
         t = (beta - c0) / beta;
       }
       __syncwarp();
@@ -64,27 +76,58 @@ __device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, doub
     __syncthreads();
     const double t = tau[j];
     const bool apply = (m - j > 1) && t != 0.0;  // rows()==1 or tau==0: identity
-    for (int k = j + 1 + ((warp - (j + 1) % NW + NW) % NW); k < c; k += NW) {
+    int k = j + 1 + ((warp - (j + 1) % NW + NW) % NW);
+    for (; k < c; k += NW) {
       double* a = A + k * lda;
       if (apply) {
         double w = 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) w += x[i] * a[i];
+        double xr[RPL], ar[RPL];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          const bool in = i > j && i < m;
+          xr[r] = in ? x[i] : 0.0;
+          ar[r] = in ? a[i] : 0.0;
+          w += xr[r] * ar[r];
+        }
         w = warp_sum(w);
         w += a[j];
         __syncwarp();
         if (lane == 0) a[j] -= t * w;
-        for (int i = j + 1 + lane; i < m; i += 32) a[i] -= t * x[i] * w;
-      }
-      if (k == j + 1) {
-        __syncwarp();
         double s = 0.0;
-        for (int i = k + 1 + lane; i < m; i += 32) s += a[i] * a[i];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          if (i > j && i < m) {
+            const double v = ar[r] - t * xr[r] * w;
+            a[i] = v;
+            if (i > j + 1) s += v * v;
+          }
+        }
+        if (k == j + 1) {
+          s = warp_sum(s);
+          if (lane == 0) tn[k] = s;
+        }
+      } else if (k == j + 1) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          if (i > k && i < m) s += a[i] * a[i];
+        }
         s = warp_sum(s);
         if (lane == 0) tn[k] = s;
       }
     }
     __syncthreads();
   }
+}
+
+template <int NT>
+__device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, double* red) {
+  if (m <= 64) cta_house_qr_t<NT, 2>(A, lda, m, c, tau, red);
+  else if (m <= 256) cta_house_qr_t<NT, 8>(A, lda, m, c, tau, red);
+  else cta_house_qr_t<NT, 16>(A, lda, m, c, tau, red);  // m <= 512 (callers enforce)
 }
 
 // Explicit thin Q = H_0 H_1 ... H_{c-1} [I_c; 0] (m x c) from the reflectors
@@ -129,9 +172,10 @@ __device__ void cta_form_q_regs(const double* V, int ldv, int m, int c, const do
 
 template <int NT>
 __device__ void cta_form_q(const double* V, int ldv, int m, int c, const double* tau, double* Q, int ldq) {
-  if (m <= 256) cta_form_q_regs<NT, 8>(V, ldv, m, c, tau, Q, ldq);
+  if (m <= 64) cta_form_q_regs<NT, 2>(V, ldv, m, c, tau, Q, ldq);
+  else if (m <= 256) cta_form_q_regs<NT, 8>(V, ldv, m, c, tau, Q, ldq);
   else if (m <= 512) cta_form_q_regs<NT, 16>(V, ldv, m, c, tau, Q, ldq);
-  else cta_form_q_regs<NT, 32>(V, ldv, m, c, tau, Q, ldq);  // m <= 1024
+  else cta_form_q_regs<NT, 16>(V, ldv, m, c, tau, Q, ldq);  // m <= 512 (callers enforce)
 }
 
 // thin_qr (linalg.cpp:67-79): A (m x c, m >= c, m <= 1024) in smem is
@@ -504,9 +548,9 @@ __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv,
         // (a bare eps threshold never settles once the dot products are
         // evaluated in a different order than the rotation was computed)
         if (gg == 0.0 || fabs(gg) <= tol * sqrt(aa * bb)) continue;
-        const double zeta = (bb - aa) / (2.0 * gg);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double zeta = (bb - aa) * __drcp_rn(2.0 * gg);
+        const double t = copysign(__drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+        const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
         for (int i = lane; i < p; i += 32) {
           const double x = wp[i], y = wq[i];
