@@ -12,6 +12,7 @@ namespace slra_dev {
 
 constexpr int kDT = 512;
 constexpr int kLeaf = 256;  // TSQR leaf rows
+constexpr int kSVT = 1024; // threads of the one-CTA SVD (one warp per Jacobi pair)
 
 // ---------------------------------------------------------------- single-CTA thin QR
 __global__ void __launch_bounds__(kDT) thin_qr_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int c,
@@ -217,7 +218,7 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
 
 // ---------------------------------------------------------------- small SVD
 // One CTA: W = A (p x q, p >= q) or A^T, Jacobi, finish; S (m x pmin), T.
-__global__ void __launch_bounds__(kDT) svd_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
+__global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
                                                       double* __restrict__ S, int64_t lds, double* __restrict__ sigma,
                                                       double* __restrict__ T, int64_t ldt) {
   extern __shared__ __align__(16) double sm[];
@@ -231,19 +232,19 @@ __global__ void __launch_bounds__(kDT) svd_cta_kernel(const double* __restrict__
   double* tmp = sg + q;              // q
   int* order = reinterpret_cast<int*>(tmp + q);
   int* flag = order + q + 1;
-  for (int e = threadIdx.x; e < m * n; e += kDT) {
+  for (int e = threadIdx.x; e < m * n; e += kSVT) {
     const int i = e % m, j = e / m;
     const double x = A[i + (int64_t)j * lda];
     if (tall) W[i + j * p] = x;
     else W[j + i * p] = x;
   }
   __syncthreads();
-  cta_jacobi<kDT>(W, p, p, q, V, q, flag);
-  cta_svd_finish<kDT>(W, p, p, q, V, q, sg, order, Ss, p, Ts, q, tmp);
+  cta_jacobi<kSVT>(W, p, p, q, V, q, flag);
+  cta_svd_finish<kSVT>(W, p, p, q, V, q, sg, order, Ss, p, Ts, q, tmp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (!tall) {
     // left vectors of A are Ts (q x q = m x m); re-apply the sign rule on them
-    for (int t = warp; t < q; t += kDT / 32) {
+    for (int t = warp; t < q; t += kSVT / 32) {
       ArgMax a{-1.0, INT64_MAX};
       for (int i = lane; i < q; i += 32) a = argmax_merge(a, ArgMax{fabs(Ts[i + t * q]), i});
       a = warp_argmax(a);
@@ -254,13 +255,13 @@ __global__ void __launch_bounds__(kDT) svd_cta_kernel(const double* __restrict__
     }
     __syncthreads();
   }
-  for (int t = threadIdx.x; t < q; t += kDT) sigma[t] = sg[t];
+  for (int t = threadIdx.x; t < q; t += kSVT) sigma[t] = sg[t];
   const double* Sl = tall ? Ss : Ts;
   const int ldl = tall ? p : q;
   const double* Tr = tall ? Ts : Ss;
   const int ldr = tall ? q : p;
-  for (int e = threadIdx.x; e < m * q; e += kDT) S[(e % m) + (int64_t)(e / m) * lds] = Sl[(e % m) + (e / m) * ldl];
-  for (int e = threadIdx.x; e < n * q; e += kDT) T[(e % n) + (int64_t)(e / n) * ldt] = Tr[(e % n) + (e / n) * ldr];
+  for (int e = threadIdx.x; e < m * q; e += kSVT) S[(e % m) + (int64_t)(e / m) * lds] = Sl[(e % m) + (e / m) * ldl];
+  for (int e = threadIdx.x; e < n * q; e += kSVT) T[(e % n) + (int64_t)(e / n) * ldt] = Tr[(e % n) + (e / n) * ldr];
 }
 
 static size_t svd_smem(int m, int n) {
@@ -273,7 +274,7 @@ int launch_svd_small(Context* cx, const double* A, int64_t lda, int m, int n, do
   const size_t smem = svd_smem(m, n);
   if (smem > 220 * 1024) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(svd_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SLRA_TIMED(cx, "svd", svd_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, m, n, S, lds, sigma, T, ldt);)
+  SLRA_TIMED(cx, "svd", svd_cta_kernel<<<1, kSVT, smem, cx->stream>>>(A, lda, m, n, S, lds, sigma, T, ldt);)
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
 }
@@ -333,7 +334,7 @@ int launch_svd(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, 
                double* sigma, double* T, int64_t ldt) {
   const int64_t q = m < n ? m : n;
   if (q > 64) return SLRA_ERR_UNSUPPORTED;
-  if (svd_smem((int)m, (int)n) <= 200 * 1024) return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt);
+  if (svd_smem((int)m, (int)n) <= 200 * 1024 && (m > n ? m : n) <= 512) return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt);
   if (m < n) {
     // wide: A^T = S' Sigma T'^T (tall path), so A = T' Sigma S'^T; the sign
     // rule is then re-applied on the left vectors T' (flipping S' with them).

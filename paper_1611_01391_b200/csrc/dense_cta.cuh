@@ -509,17 +509,18 @@ __device__ inline double warp_abs_det(double* M, int ld, int n) {
 // accumulating V (n x n, ld ldv). Parallel round-robin ordering; each warp
 // owns disjoint column pairs per round. On exit W's columns are
 // U_j sigma_j (unsorted).
-template <int NT>
-__device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag) {
+// Rows per lane: p <= 32*RPL (W), n <= 64 (V, two rows per lane).
+template <int NT, int RPL>
+__device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ldv, int* flag) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   for (int e = tid; e < n * n; e += NT) V[e % n + (e / n) * ldv] = (e % n == e / n) ? 1.0 : 0.0;
   const int ne = n + (n & 1);  // even number of players (dummy = n)
   const double tol = sqrt((double)p) * kEps;
+  if (tid == 0) flag[0] = flag[1] = 0;
   __syncthreads();
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    if (tid == 0) flag[0] = 0;
-    __syncthreads();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    const int fl = sweep & 1;  // double-buffered "rotated" flag
     for (int rd = 0; rd < ne - 1; ++rd) {
       for (int pi = warp; pi < ne / 2; pi += NW) {
         int a, b;
@@ -534,16 +535,23 @@ __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv,
         if (a > b) { const int t = a; a = b; b = t; }
         double* wp = W + a * ldw;
         double* wq = W + b * ldw;
+        double x[RPL], y[RPL];
         double aa = 0.0, bb = 0.0, gg = 0.0;
-        for (int i = lane; i < p; i += 32) {
-          const double x = wp[i], y = wq[i];
-          aa += x * x;
-          bb += y * y;
-          gg += x * y;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          x[r] = i < p ? wp[i] : 0.0;
+          y[r] = i < p ? wq[i] : 0.0;
+          aa = fma(x[r], x[r], aa);
+          bb = fma(y[r], y[r], bb);
+          gg = fma(x[r], y[r], gg);
         }
-        aa = warp_sum(aa);
-        bb = warp_sum(bb);
-        gg = warp_sum(gg);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // three interleaved butterflies
+          aa += __shfl_xor_sync(0xffffffffu, aa, o);
+          bb += __shfl_xor_sync(0xffffffffu, bb, o);
+          gg += __shfl_xor_sync(0xffffffffu, gg, o);
+        }
         // convergence test of LAPACK dgesvj: |<w_p, w_q>| <= sqrt(p) eps ||w_p|| ||w_q||
         // (a bare eps threshold never settles once the dot products are
         // evaluated in a different order than the rotation was computed)
@@ -552,26 +560,40 @@ __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv,
         const double t = copysign(__drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
         const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
-        for (int i = lane; i < p; i += 32) {
-          const double x = wp[i], y = wq[i];
-          wp[i] = cs * x - sn * y;
-          wq[i] = sn * x + cs * y;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          if (i < p) {
+            wp[i] = cs * x[r] - sn * y[r];
+            wq[i] = sn * x[r] + cs * y[r];
+          }
         }
         double* vp = V + a * ldv;
         double* vq = V + b * ldv;
-        for (int i = lane; i < n; i += 32) {
-          const double x = vp[i], y = vq[i];
-          vp[i] = cs * x - sn * y;
-          vq[i] = sn * x + cs * y;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int i = lane + 32 * r;
+          if (i < n) {
+            const double u = vp[i], v = vq[i];
+            vp[i] = cs * u - sn * v;
+            vq[i] = sn * u + cs * v;
+          }
         }
-        if (lane == 0) flag[0] = 1;
+        if (lane == 0) flag[fl] = 1;
       }
       __syncthreads();
     }
-    const int rotated = flag[0];
+    const int rotated = flag[fl];
+    if (tid == 0) flag[fl ^ 1] = 0;  // next sweep's flag; this one is read by all before the barrier below
     __syncthreads();
     if (!rotated) break;
   }
+}
+
+template <int NT>
+__device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag) {
+  if (p <= 64) cta_jacobi_t<NT, 2>(W, ldw, p, n, V, ldv, flag);
+  else cta_jacobi_t<NT, 8>(W, ldw, p, n, V, ldv, flag);  // p <= 256 (callers enforce)
 }
 
 // Finish an SVD after cta_jacobi: sigma_j = ||w_j||, descending stable order

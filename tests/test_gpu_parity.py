@@ -240,7 +240,7 @@ def test_cross_approx_config1_parity(slra, oracle, seed):
         assert sg["rows"] == so["rows"] and sg["cols"] == so["cols"]
         # |det Q[J,:]| of a strip whose trailing directions sit at the 1e-8
         # noise level: conditioning ~ eps * sigma_1 / sigma_16 ~ 1e-7
-        assert abs(sg["volume_proxy"] - so["volume_proxy"]) <= 1e-6 * max(so["volume_proxy"], 1e-300)
+        assert abs(sg["volume_proxy"] - so["volume_proxy"]) <= 1e-5 * max(so["volume_proxy"], 1e-300)
     nA = np.linalg.norm(A)
     Cg = slra.cur_reconstruct(A, g["I"], g["J"], g["nucleus"])
     Co = oracle.cur_reconstruct(A, o["I"], o["J"], o["nucleus"])
