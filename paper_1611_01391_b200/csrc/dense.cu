@@ -220,7 +220,7 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
 // One CTA: W = A (p x q, p >= q) or A^T, Jacobi, finish; S (m x pmin), T.
 __global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
                                                       double* __restrict__ S, int64_t lds, double* __restrict__ sigma,
-                                                      double* __restrict__ T, int64_t ldt) {
+                                                      double* __restrict__ T, int64_t ldt, double deflate) {
   extern __shared__ __align__(16) double sm[];
   const bool tall = m >= n;
   const int p = tall ? m : n, q = tall ? n : m;
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict_
     else W[j + i * p] = x;
   }
   __syncthreads();
-  cta_jacobi<kSVT>(W, p, p, q, V, q, flag);
+  cta_jacobi<kSVT>(W, p, p, q, V, q, flag, deflate);
   cta_svd_finish<kSVT>(W, p, p, q, V, q, sg, order, Ss, p, Ts, q, tmp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (!tall) {
@@ -270,11 +270,11 @@ static size_t svd_smem(int m, int n) {
 }
 
 int launch_svd_small(Context* cx, const double* A, int64_t lda, int m, int n, double* S, int64_t lds, double* sigma,
-                     double* T, int64_t ldt) {
+                     double* T, int64_t ldt, double deflate) {
   const size_t smem = svd_smem(m, n);
   if (smem > 220 * 1024) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(svd_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SLRA_TIMED(cx, "svd", svd_cta_kernel<<<1, kSVT, smem, cx->stream>>>(A, lda, m, n, S, lds, sigma, T, ldt);)
+  SLRA_TIMED(cx, "svd", svd_cta_kernel<<<1, kSVT, smem, cx->stream>>>(A, lda, m, n, S, lds, sigma, T, ldt, deflate);)
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
 }
@@ -334,7 +334,7 @@ int launch_svd(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, 
                double* sigma, double* T, int64_t ldt) {
   const int64_t q = m < n ? m : n;
   if (q > 64) return SLRA_ERR_UNSUPPORTED;
-  if (svd_smem((int)m, (int)n) <= 200 * 1024 && (m > n ? m : n) <= 512) return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt);
+  if (svd_smem((int)m, (int)n) <= 200 * 1024 && (m > n ? m : n) <= 256) return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt, 0.0);
   if (m < n) {
     // wide: A^T = S' Sigma T'^T (tall path), so A = T' Sigma S'^T; the sign
     // rule is then re-applied on the left vectors T' (flipping S' with them).
@@ -357,7 +357,7 @@ int launch_svd(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, 
   double* Rm = buf + (size_t)m * c;
   double* UR = Rm + (size_t)c * c;
   int st = launch_thin_qr(cx, A, lda, m, c, Qm, m, Rm, c);
-  if (st == SLRA_OK) st = launch_svd_small(cx, Rm, c, c, c, UR, c, sigma, T, ldt);
+  if (st == SLRA_OK) st = launch_svd_small(cx, Rm, c, c, c, UR, c, sigma, T, ldt, 0.0);
   if (st == SLRA_OK) st = launch_gemm(cx, 0, 0, m, c, c, 1.0, Qm, m, UR, c, 0.0, S, lds);
   if (st == SLRA_OK) st = launch_colsign(cx, S, lds, m, T, ldt, n, c);
   cudaFreeAsync(buf, cx->stream);

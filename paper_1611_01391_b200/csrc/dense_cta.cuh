@@ -510,29 +510,59 @@ __device__ inline double warp_abs_det(double* M, int ld, int n) {
 // owns disjoint column pairs per round. On exit W's columns are
 // U_j sigma_j (unsorted).
 // Rows per lane: p <= 32*RPL (W), n <= 64 (V, two rows per lane).
+// `deflate` > 0 skips pairs whose columns both have norm below deflate times
+// the largest column norm of the sweep start (range finder only: those
+// directions fall under the rank cut and are never used individually).
 template <int NT, int RPL>
-__device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ldv, int* flag) {
+__device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
+  __shared__ unsigned short pair_tab[64 * 32];  // round-robin schedule: (a << 8) | b
+  __shared__ double dmax2;
   for (int e = tid; e < n * n; e += NT) V[e % n + (e / n) * ldv] = (e % n == e / n) ? 1.0 : 0.0;
   const int ne = n + (n & 1);  // even number of players (dummy = n)
+  for (int e = tid; e < (ne - 1) * (ne / 2); e += NT) {
+    const int rd = e / (ne / 2), pi = e % (ne / 2);
+    int a, b;
+    if (pi == 0) {
+      a = rd;
+      b = ne - 1;
+    } else {
+      a = (rd + pi) % (ne - 1);
+      b = (rd - pi + ne - 1) % (ne - 1);
+    }
+    if (a > b) { const int t = a; a = b; b = t; }
+    pair_tab[e] = (unsigned short)((a << 8) | b);
+  }
   const double tol = sqrt((double)p) * kEps;
   if (tid == 0) flag[0] = flag[1] = 0;
   __syncthreads();
   for (int sweep = 0; sweep < 40; ++sweep) {
     const int fl = sweep & 1;  // double-buffered "rotated" flag
+    double thr2 = 0.0;
+    if (deflate > 0.0) {
+      if (warp == 0) {
+        double mx = 0.0;
+        for (int j = 0; j < n; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = lane + 32 * r;
+            if (i < p) s = fma(W[i + j * ldw], W[i + j * ldw], s);
+          }
+          s = warp_sum(s);
+          mx = fmax(mx, s);
+        }
+        if (lane == 0) dmax2 = mx;
+      }
+      __syncthreads();
+      thr2 = deflate * deflate * dmax2;
+    }
     for (int rd = 0; rd < ne - 1; ++rd) {
       for (int pi = warp; pi < ne / 2; pi += NW) {
-        int a, b;
-        if (pi == 0) {
-          a = rd;
-          b = ne - 1;
-        } else {
-          a = (rd + pi) % (ne - 1);
-          b = (rd - pi + ne - 1) % (ne - 1);
-        }
-        if (a >= n || b >= n) continue;
-        if (a > b) { const int t = a; a = b; b = t; }
+        const int ab = pair_tab[rd * (ne / 2) + pi];
+        const int a = ab >> 8, b = ab & 255;
+        if (b >= n) continue;
         double* wp = W + a * ldw;
         double* wq = W + b * ldw;
         double x[RPL], y[RPL];
@@ -556,6 +586,7 @@ __device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ld
         // (a bare eps threshold never settles once the dot products are
         // evaluated in a different order than the rotation was computed)
         if (gg == 0.0 || fabs(gg) <= tol * sqrt(aa * bb)) continue;
+        if (aa < thr2 && bb < thr2) continue;
         const double zeta = (bb - aa) * __drcp_rn(2.0 * gg);
         const double t = copysign(__drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
         const double cs = rsqrt(fma(t, t, 1.0));
@@ -591,9 +622,9 @@ __device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ld
 }
 
 template <int NT>
-__device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag) {
-  if (p <= 64) cta_jacobi_t<NT, 2>(W, ldw, p, n, V, ldv, flag);
-  else cta_jacobi_t<NT, 8>(W, ldw, p, n, V, ldv, flag);  // p <= 256 (callers enforce)
+__device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate = 0.0) {
+  if (p <= 64) cta_jacobi_t<NT, 2>(W, ldw, p, n, V, ldv, flag, deflate);
+  else cta_jacobi_t<NT, 8>(W, ldw, p, n, V, ldv, flag, deflate);  // p <= 256 (callers enforce)
 }
 
 // Finish an SVD after cta_jacobi: sigma_j = ||w_j||, descending stable order

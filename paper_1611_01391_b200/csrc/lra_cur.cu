@@ -20,7 +20,7 @@ int launch_lowrank_residual(Context* c, const double* A, int64_t lda, int64_t m,
 int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, double* Q, int64_t ldq, double* R,
                    int64_t ldr);
 int launch_svd_small(Context* cx, const double* A, int64_t lda, int m, int n, double* S, int64_t lds, double* sigma,
-                     double* T, int64_t ldt);
+                     double* T, int64_t ldt, double deflate);
 int launch_colsign(Context* cx, double* S, int64_t lds, int64_t m, double* T, int64_t ldt, int64_t n, int64_t cols);
 
 // Scale columns: X(:, j) *= s[j] (or 1/s[j] when inv).
@@ -98,7 +98,7 @@ int slra_range_finder(slra_ctx ctx, const double* M, int64_t ldm, int64_t m, int
   double* sig = VR + (size_t)l * l;       // l
   SLRA_TRY(launch_sketch_cols(cx, M, ldm, m, src, coef, q, width, tree, l, MH, m));
   SLRA_TRY(launch_thin_qr(cx, MH, m, m, (int)l, Qm, m, Rm, l));
-  SLRA_TRY(launch_svd_small(cx, Rm, l, (int)l, (int)l, UR, l, sig, VR, l));
+  SLRA_TRY(launch_svd_small(cx, Rm, l, (int)l, (int)l, UR, l, sig, VR, l, 1e-10 / sqrt((double)l)));
   if (d_sigma) SLRA_CUDA(cudaMemcpyAsync(d_sigma, sig, 8 * l, cudaMemcpyDeviceToDevice, cx->stream));
   // rank check: numerical_rank(MH, 1e-10, Relative) < r -> RangeFailure
   double* hs = static_cast<double*>(cx->hsmall);
