@@ -311,11 +311,12 @@ class Config2:
                        "entries_per_step": self.entries_per_step, "m": N2, "n": N2, "l": L_SKETCH, "r": RANK}
 
     def step(self):
-        for i, (_, p, d) in enumerate(self.plans):
-            self.slra.range_finder_device(self.At.data_ptr(), N2, N2, N2, p, RANK, True,
-                                          self.U[i].data_ptr(), N2, self.V[i].data_ptr(), RANK,
-                                          self.out[i].data_ptr(), d["src"].data_ptr(), d["coef"].data_ptr(),
-                                          d["q"].data_ptr())
+        # both multipliers in one call: their TSQR/SVD stages run concurrently
+        plans = [(p["width"], p["tree"], d["src"].data_ptr(), d["coef"].data_ptr(), d["q"].data_ptr())
+                 for _, p, d in self.plans]
+        self.slra.range_finder_batched_device(self.At.data_ptr(), N2, N2, N2, plans, L_SKETCH, RANK, True,
+                                              [u.data_ptr() for u in self.U], N2,
+                                              [v.data_ptr() for v in self.V], RANK, self.out.data_ptr())
 
     def last_residual_rel(self):
         o = self.out.cpu().numpy()

@@ -185,6 +185,18 @@ int slra_range_finder(slra_ctx ctx, const double* d_M, int64_t ldm, int64_t m, i
                       int64_t width, int tree, int64_t l, int64_t r, int variant, double* d_U,
                       int64_t ldu, double* d_V, int64_t ldv, double* d_out,
                       double* d_sigma);
+/* The same for nsk sketches of one M in one call (their factorisations run
+ * concurrently, one CTA per sketch). h_* are HOST arrays of nsk entries
+ * (device pointers / sizes); d_out holds 2*nsk doubles, d_sigma nsk*l. With
+ * h_status non-null a rank failure is reported per sketch (SLRA_OK or
+ * SLRA_ERR_RANGE_FAILURE) and the call returns SLRA_OK. For variant 1 the
+ * singular values below the rank cut are upper bounds (Jacobi deflation). */
+int slra_range_finder_batched(slra_ctx ctx, const double* d_M, int64_t ldm, int64_t m, int64_t n,
+                              int nsk, const int64_t* const* h_src, const double* const* h_coef,
+                              const int32_t* const* h_q, const int64_t* h_width, const int* h_tree,
+                              int64_t l, int64_t r, int variant, double* const* h_U, int64_t ldu,
+                              double* const* h_V, int64_t ldv, double* d_out, double* d_sigma,
+                              int32_t* h_status);
 
 /* ------------------------------------------------------------ a11/a12 LSR
  * sketch_solve (lsr.cpp:37-67): FW = F (A|b) through a compiled left-side

@@ -156,7 +156,7 @@ template <int NT>
 __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I, int k, const int* J, int l,
                            int r_req, int* r_out) {
   const int tid = threadIdx.x;
-  const bool tall = k >= l;
+  const bool tall = k > l;  // square generators take the transposed (faster) path
   const int p = tall ? k : l, q = tall ? l : k;
   // W := G (tall) or G^T (wide), p x q, ld p
   for (int e = tid; e < k * l; e += NT) {

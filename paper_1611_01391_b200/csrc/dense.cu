@@ -1,99 +1,116 @@
 // Tall-skinny dense kernels behind slra_thin_qr / slra_svd / slra_maxvol_rows
-// / slra_select_rows_spanning.
+// / slra_select_rows_spanning, all batched over independent problems (the
+// problem index rides on a grid dimension; operands are strided) so that the
+// latency-bound factorisations of several sketches overlap on separate SMs.
 //   * thin_qr (linalg.cpp:67-79): one CTA when the matrix fits on chip,
 //     otherwise TSQR — 256-row leaves factorised by CTA-resident Householder
 //     QR, their R factors stacked and reduced level by level, then Q expanded
 //     top-down by re-applying each leaf's reflectors. Unconditionally stable
 //     (rank-deficient strips of configs 3/5 included).
-//   * svd (linalg.cpp:81-98): QR pre-reduction + one-sided Jacobi on R.
+//   * svd (linalg.cpp:81-98): one-sided Jacobi (on A^T for square inputs,
+//     which converges in far fewer sweeps on the graded triangles the QR
+//     pre-reduction produces), QR pre-reduction for tall inputs.
 #include "dense_cta.cuh"
 
 namespace slra_dev {
 
 constexpr int kDT = 512;
 constexpr int kLeaf = 256;  // TSQR leaf rows
-constexpr int kSVT = 1024; // threads of the one-CTA SVD (one warp per Jacobi pair)
+constexpr int kSVT = 1024;  // threads of the one-CTA SVD (one warp per Jacobi pair)
 
 // ---------------------------------------------------------------- single-CTA thin QR
-__global__ void __launch_bounds__(kDT) thin_qr_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int c,
-                                                          double* __restrict__ Q, int64_t ldq,
-                                                          double* __restrict__ R, int64_t ldr) {
+__global__ void __launch_bounds__(kDT) thin_qr_cta_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                                                          int m, int c, double* __restrict__ Q, int64_t ldq,
+                                                          int64_t sQ, double* __restrict__ R, int64_t ldr,
+                                                          int64_t sR) {
   extern __shared__ __align__(16) double sm[];
-  double* S = sm;                 // m x c
+  double* S = sm;                  // m x c
   double* Rs = S + (size_t)m * c;  // c x c
   double* tau = Rs + c * c;        // c
-  double* red = tau + c;           // 40
-  for (int e = threadIdx.x; e < m * c; e += kDT) S[e] = A[(e % m) + (int64_t)(e / m) * lda];
+  double* red = tau + c;           // >= c + 8
+  const int64_t b = blockIdx.x;
+  A += b * sA;
+  Q += b * sQ;
+  for (int j = 0; j < c; ++j)
+    for (int i = threadIdx.x; i < m; i += kDT) S[i + j * m] = A[i + (int64_t)j * lda];
   __syncthreads();
   cta_thin_qr<kDT>(S, m, m, c, Q, (int)ldq, Rs, c, tau, red);
   if (R)
-    for (int e = threadIdx.x; e < c * c; e += kDT) R[(e % c) + (int64_t)(e / c) * ldr] = Rs[e];
+    for (int j = 0; j < c; ++j)
+      for (int i = threadIdx.x; i < c; i += kDT) R[b * sR + i + (int64_t)j * ldr] = Rs[i + j * c];
 }
 
 // ---------------------------------------------------------------- TSQR
-// Reduce step: block b of X (rows [b*L, min((b+1)*L, rows)), padded with
-// zeros to >= c rows) -> Householder QR in smem; reflectors + tau to
-// Vst/taust (block b, Lp x c, ld Lp); R_b -> Xn rows [b*c, (b+1)*c).
-__global__ void __launch_bounds__(kDT) tsqr_reduce_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
-                                                          int c, int Lp, double* __restrict__ Vst,
-                                                          double* __restrict__ taust, double* __restrict__ Xn,
-                                                          int64_t ldxn) {
+// Reduce step: block x of problem y — rows [x*L, min((x+1)*L, rows)) of X,
+// padded with zeros to >= c rows — is factorised in smem; reflectors + tau go
+// to Vst/taust (block x: Lp x c, ld Lp), R_x to Xn rows [x*c, (x+1)*c).
+__global__ void __launch_bounds__(kDT) tsqr_reduce_kernel(const double* __restrict__ X, int64_t ldx, int64_t sX,
+                                                          int64_t rows, int c, int Lp, double* __restrict__ Vst,
+                                                          double* __restrict__ taust, int64_t sV,
+                                                          double* __restrict__ Xn, int64_t ldxn, int64_t sXn) {
   extern __shared__ __align__(16) double sm[];
   double* S = sm;
   double* tau = S + (size_t)Lp * c;
   double* red = tau + c;
-  const int64_t b = blockIdx.x;
+  const int64_t b = blockIdx.x, pb = blockIdx.y;
+  X += pb * sX;
+  Xn += pb * sXn;
   const int64_t r0 = b * kLeaf;
   const int nr = (int)((rows - r0) < kLeaf ? (rows - r0) : kLeaf);
-  for (int e = threadIdx.x; e < Lp * c; e += kDT) {
-    const int i = e % Lp, j = e / Lp;
-    S[e] = i < nr ? X[(r0 + i) + (int64_t)j * ldx] : 0.0;
-  }
+  for (int j = 0; j < c; ++j)
+    for (int i = threadIdx.x; i < Lp; i += kDT) S[i + j * Lp] = i < nr ? X[(r0 + i) + (int64_t)j * ldx] : 0.0;
   __syncthreads();
   cta_house_qr<kDT>(S, Lp, Lp, c, tau, red);
-  double* V = Vst + b * (int64_t)Lp * c;
+  const int64_t nblk = gridDim.x;
+  double* V = Vst + pb * sV + b * (int64_t)Lp * c;
+  double* T = taust + pb * (nblk * c) + b * c;
   for (int e = threadIdx.x; e < Lp * c; e += kDT) V[e] = S[e];
-  for (int j = threadIdx.x; j < c; j += kDT) taust[b * c + j] = tau[j];
-  for (int e = threadIdx.x; e < c * c; e += kDT) {
-    const int i = e % c, j = e / c;
-    Xn[(b * c + i) + (int64_t)j * ldxn] = (i <= j) ? S[i + j * Lp] : 0.0;
-  }
+  for (int j = threadIdx.x; j < c; j += kDT) T[j] = tau[j];
+  for (int j = 0; j < c; ++j)
+    for (int i = threadIdx.x; i < c; i += kDT) Xn[(b * c + i) + (int64_t)j * ldxn] = (i <= j) ? S[i + j * Lp] : 0.0;
 }
 
-// Top: one CTA thin QR (with sign rule) of the final stack (rows <= L);
-// writes Qtop (rows x c) and R. `sgn` receives the column flips applied.
-__global__ void __launch_bounds__(kDT) tsqr_top_kernel(const double* __restrict__ X, int64_t ldx, int rows, int c,
-                                                       int Lp, double* __restrict__ Qt, int64_t ldqt,
-                                                       double* __restrict__ R, int64_t ldr) {
+// Top: one CTA per problem, thin QR (with sign rule) of the final stack
+// (c <= rows <= L); writes Qtop (rows x c) and R.
+__global__ void __launch_bounds__(kDT) tsqr_top_kernel(const double* __restrict__ X, int64_t ldx, int64_t sX, int rows,
+                                                       int c, int Lp, double* __restrict__ Qt, int64_t ldqt,
+                                                       int64_t sQt, double* __restrict__ R, int64_t ldr, int64_t sR) {
   extern __shared__ __align__(16) double sm[];
-  double* S = sm;                     // rows x c (rows <= Lp, rows >= c)
-  double* Rs = S + (size_t)Lp * c;    // c x c
+  double* S = sm;                   // rows x c
+  double* Rs = S + (size_t)Lp * c;  // c x c
   double* tau = Rs + c * c;
   double* red = tau + c;
-  for (int e = threadIdx.x; e < rows * c; e += kDT) S[e] = X[(e % rows) + (int64_t)(e / rows) * ldx];
+  const int64_t pb = blockIdx.x;
+  X += pb * sX;
+  for (int j = 0; j < c; ++j)
+    for (int i = threadIdx.x; i < rows; i += kDT) S[i + j * rows] = X[i + (int64_t)j * ldx];
   __syncthreads();
-  cta_thin_qr<kDT>(S, rows, rows, c, Qt, (int)ldqt, Rs, c, tau, red);
+  cta_thin_qr<kDT>(S, rows, rows, c, Qt + pb * sQt, (int)ldqt, Rs, c, tau, red);
   if (R)
-    for (int e = threadIdx.x; e < c * c; e += kDT) R[(e % c) + (int64_t)(e / c) * ldr] = Rs[e];
+    for (int j = 0; j < c; ++j)
+      for (int i = threadIdx.x; i < c; i += kDT) R[pb * sR + i + (int64_t)j * ldr] = Rs[i + j * c];
 }
 
-// Expand step: Q_b = H_0 ... H_{c-1} [Qp(b*c : b*c+c, :); 0] (Lp x c), store
-// the first nr rows at Qo rows [b*L, ...). Reflectors staged in smem; each
+// Expand step: Q_x = H_0 ... H_{c-1} [Qp(x*c : x*c+c, :); 0] (Lp x c), the
+// first nr rows stored at Qo rows [x*L, ...). Reflectors staged in smem; each
 // warp carries its output columns in registers (no block barriers).
 template <int RPL>
-__global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restrict__ Qp, int64_t ldqp,
+__global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restrict__ Qp, int64_t ldqp, int64_t sQp,
                                                           const double* __restrict__ Vst,
-                                                          const double* __restrict__ taust, int64_t rows, int c,
-                                                          int Lp, double* __restrict__ Qo, int64_t ldqo) {
+                                                          const double* __restrict__ taust, int64_t sV, int64_t rows,
+                                                          int c, int Lp, double* __restrict__ Qo, int64_t ldqo,
+                                                          int64_t sQo) {
   extern __shared__ __align__(16) double sm[];
-  double* V = sm;            // Lp x c reflectors
+  double* V = sm;  // Lp x c reflectors
   double* tau = V + (size_t)Lp * c;
-  const int64_t b = blockIdx.x;
+  const int64_t b = blockIdx.x, pb = blockIdx.y, nblk = gridDim.x;
+  Qp += pb * sQp;
+  Qo += pb * sQo;
   const int64_t r0 = b * kLeaf;
   const int nr = (int)((rows - r0) < kLeaf ? (rows - r0) : kLeaf);
-  const double* Vg = Vst + b * (int64_t)Lp * c;
+  const double* Vg = Vst + pb * sV + b * (int64_t)Lp * c;
   for (int e = threadIdx.x; e < Lp * c; e += kDT) V[e] = Vg[e];
-  for (int j = threadIdx.x; j < c; j += kDT) tau[j] = taust[b * c + j];
+  for (int j = threadIdx.x; j < c; j += kDT) tau[j] = taust[pb * (nblk * c) + b * c + j];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int j = warp; j < c; j += kDT / 32) {
@@ -111,7 +128,7 @@ __global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restri
 #pragma unroll
       for (int r = 0; r < RPL; ++r) {
         const int i = lane + 32 * r;
-        if (i > k && i < Lp) w += v[i] * y[r];
+        if (i > k && i < Lp) w = fma(v[i], y[r], w);
         if (i == k) yk = y[r];
       }
       w = warp_sum(w);
@@ -133,18 +150,36 @@ __global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restri
 
 static size_t qr_cta_smem(int m, int c) { return sizeof(double) * ((size_t)m * c + (size_t)c * c + c + 112); }
 
-int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, double* Q, int64_t ldq, double* R,
-                   int64_t ldr) {
+// Workspace doubles needed by launch_thin_qr_batched for one problem.
+size_t tsqr_workspace_doubles(int64_t m, int c) {
+  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 512) return 0;
+  const int Lp = kLeaf > c ? kLeaf : c;
+  size_t total = 0;
+  int64_t rows = m, first_upper = -1;
+  while (rows > kLeaf) {
+    const int64_t nb = (rows + kLeaf - 1) / kLeaf;
+    total += (size_t)nb * Lp * c + (size_t)nb * c + (size_t)nb * c * c;
+    rows = nb * c;
+    if (first_upper < 0) first_upper = rows;
+  }
+  total += 2 * (size_t)(first_upper > 0 ? first_upper : rows) * c + (size_t)rows * c;
+  return total;
+}
+
+// Batched thin QR of nb problems (A + b*sA, Q + b*sQ, R + b*sR). `ws` (may
+// be null -> context workspace) holds nb * tsqr_workspace_doubles(m, c).
+int launch_thin_qr_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int64_t m, int c, double* Q,
+                           int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws) {
   if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 512) {
     const size_t smem = qr_cta_smem((int)m, c);
     SLRA_CUDA(cudaFuncSetAttribute(thin_qr_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SLRA_TIMED(cx, "thin_qr", thin_qr_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, c, Q, ldq, R, ldr);)
+    SLRA_TIMED(cx, "thin_qr", thin_qr_cta_kernel<<<nb, kDT, smem, cx->stream>>>(A, lda, sA, (int)m, c, Q, ldq, sQ, R,
+                                                                               ldr, sR);)
     SLRA_CHECK_LAUNCH(cx);
     return SLRA_OK;
   }
   if (c > 64) return SLRA_ERR_UNSUPPORTED;
   const int Lp = kLeaf > c ? kLeaf : c;
-  // level plan
   std::vector<int64_t> level_rows;  // rows of X at each reduce level
   int64_t rows = m;
   while (rows > kLeaf) {
@@ -152,92 +187,113 @@ int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, 
     rows = ((rows + kLeaf - 1) / kLeaf) * c;
   }
   const int64_t top_rows = rows;
-  // workspace: per level reflectors (nb*Lp*c) + taus (nb*c) + stacked R (nb*c x c)
-  size_t total = 0;
-  std::vector<size_t> offV, offT, offX;
-  for (int64_t lr : level_rows) {
-    const int64_t nb = (lr + kLeaf - 1) / kLeaf;
-    offV.push_back(total);
-    total += (size_t)nb * Lp * c;
-    offT.push_back(total);
-    total += (size_t)nb * c;
-    offX.push_back(total);
-    total += (size_t)nb * c * c;
-  }
-  const size_t offQ = total;  // Q of each level above the leaves (max rows x c)
-  total += 2 * (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c + (size_t)top_rows * c;
-  double* ws = static_cast<double*>(workspace(cx, sizeof(double) * total));
+  const size_t per = tsqr_workspace_doubles(m, c);
+  if (!ws) ws = static_cast<double*>(workspace(cx, sizeof(double) * per * nb));
   if (!ws) return SLRA_ERR_CUDA;
+  // per-level arrays laid out problem-major inside each level region
+  std::vector<double*> V(level_rows.size()), T(level_rows.size()), X(level_rows.size());
+  std::vector<int64_t> sVl(level_rows.size()), sXl(level_rows.size());
+  double* cur = ws;
+  for (size_t lv = 0; lv < level_rows.size(); ++lv) {
+    const int64_t nblk = (level_rows[lv] + kLeaf - 1) / kLeaf;
+    sVl[lv] = nblk * (int64_t)Lp * c;
+    V[lv] = cur;
+    cur += (size_t)sVl[lv] * nb;
+    T[lv] = cur;
+    cur += (size_t)nblk * c * nb;
+    sXl[lv] = nblk * (int64_t)c * c;
+    X[lv] = cur;
+    cur += (size_t)sXl[lv] * nb;
+  }
+  const int64_t qup = level_rows.size() > 1 ? level_rows[1] : top_rows;
+  double* qbuf[2] = {cur, cur + (size_t)qup * c * nb};
+  double* Qtop = cur + 2 * (size_t)qup * c * nb;
   const size_t sm_red = sizeof(double) * ((size_t)Lp * c + c + 112);
   SLRA_CUDA(cudaFuncSetAttribute(tsqr_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_red));
-  const double* X = A;
-  int64_t ldx = lda;
+  const double* Xc = A;
+  int64_t ldx = lda, sX = sA;
   for (size_t lv = 0; lv < level_rows.size(); ++lv) {
     const int64_t lr = level_rows[lv];
-    const int64_t nb = (lr + kLeaf - 1) / kLeaf;
-    double* Xn = ws + offX[lv];
-    SLRA_TIMED(cx, "thin_qr", tsqr_reduce_kernel<<<(unsigned)nb, kDT, sm_red, cx->stream>>>(X, ldx, lr, c, Lp, ws + offV[lv], ws + offT[lv],
-                                                                  Xn, nb * c);)
+    const int64_t nblk = (lr + kLeaf - 1) / kLeaf;
+    SLRA_TIMED(cx, "thin_qr",
+               tsqr_reduce_kernel<<<dim3((unsigned)nblk, nb), kDT, sm_red, cx->stream>>>(
+                   Xc, ldx, sX, lr, c, Lp, V[lv], T[lv], sVl[lv], X[lv], nblk * c, sXl[lv]);)
     SLRA_CHECK_LAUNCH(cx);
-    X = Xn;
-    ldx = nb * c;
+    Xc = X[lv];
+    ldx = nblk * c;
+    sX = sXl[lv];
   }
-  // top
   const size_t sm_top = sizeof(double) * ((size_t)Lp * c + (size_t)c * c + c + 112);
   SLRA_CUDA(cudaFuncSetAttribute(tsqr_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_top));
-  double* qbuf[2] = {ws + offQ, ws + offQ + (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c};
-  double* Qtop = ws + offQ + 2 * (size_t)(level_rows.size() > 1 ? level_rows[1] : top_rows) * c;
-  SLRA_TIMED(cx, "thin_qr", tsqr_top_kernel<<<1, kDT, sm_top, cx->stream>>>(X, ldx, (int)top_rows, c, Lp, Qtop, top_rows, R, ldr);)
+  SLRA_TIMED(cx, "thin_qr",
+             tsqr_top_kernel<<<nb, kDT, sm_top, cx->stream>>>(Xc, ldx, sX, (int)top_rows, c, Lp, Qtop, top_rows,
+                                                              top_rows * c, R, ldr, sR);)
   SLRA_CHECK_LAUNCH(cx);
-  // expand top-down
   const size_t sm_exp = sizeof(double) * ((size_t)Lp * c + c);
   SLRA_CUDA(cudaFuncSetAttribute(tsqr_expand_kernel<kLeaf / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm_exp));
   const double* Qp = Qtop;
-  int64_t ldqp = top_rows;
+  int64_t ldqp = top_rows, sQp = top_rows * c;
   for (int lv = (int)level_rows.size() - 1; lv >= 0; --lv) {
     const int64_t lr = level_rows[lv];
-    const int64_t nb = (lr + kLeaf - 1) / kLeaf;
+    const int64_t nblk = (lr + kLeaf - 1) / kLeaf;
     double* Qo;
-    int64_t ldqo;
+    int64_t ldqo, sQo;
     if (lv == 0) {
       Qo = Q;
       ldqo = ldq;
+      sQo = sQ;
     } else {
       Qo = qbuf[lv & 1];
       ldqo = lr;
+      sQo = lr * c;
     }
-    SLRA_TIMED(cx, "thin_qr", tsqr_expand_kernel<kLeaf / 32><<<(unsigned)nb, kDT, sm_exp, cx->stream>>>(Qp, ldqp, ws + offV[lv], ws + offT[lv], lr, c, Lp,
-                                                                  Qo, ldqo);)
+    SLRA_TIMED(cx, "thin_qr",
+               tsqr_expand_kernel<kLeaf / 32><<<dim3((unsigned)nblk, nb), kDT, sm_exp, cx->stream>>>(
+                   Qp, ldqp, sQp, V[lv], T[lv], sVl[lv], lr, c, Lp, Qo, ldqo, sQo);)
     SLRA_CHECK_LAUNCH(cx);
     Qp = Qo;
     ldqp = ldqo;
+    sQp = sQo;
   }
   return SLRA_OK;
 }
 
+int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, double* Q, int64_t ldq, double* R,
+                   int64_t ldr) {
+  return launch_thin_qr_batched(cx, A, lda, 0, m, c, Q, ldq, 0, R, ldr, 0, 1, nullptr);
+}
+
 // ---------------------------------------------------------------- small SVD
-// One CTA: W = A (p x q, p >= q) or A^T, Jacobi, finish; S (m x pmin), T.
-__global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
-                                                      double* __restrict__ S, int64_t lds, double* __restrict__ sigma,
-                                                      double* __restrict__ T, int64_t ldt, double deflate) {
+// One CTA per problem: W = A (p x q, m > n) or A^T (m <= n: square inputs
+// take this path too), Jacobi, finish; S (m x min), sigma, T (n x min).
+__global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict__ A, int64_t lda, int64_t sA, int m,
+                                                       int n, double* __restrict__ S, int64_t lds, int64_t sS,
+                                                       double* __restrict__ sigma, int64_t sSig,
+                                                       double* __restrict__ T, int64_t ldt, int64_t sT,
+                                                       double deflate) {
   extern __shared__ __align__(16) double sm[];
-  const bool tall = m >= n;
+  const int64_t pb = blockIdx.x;
+  A += pb * sA;
+  S += pb * sS;
+  sigma += pb * sSig;
+  T += pb * sT;
+  const bool tall = m > n;
   const int p = tall ? m : n, q = tall ? n : m;
-  double* W = sm;                    // p x q
-  double* V = W + (size_t)p * q;     // q x q
-  double* Ss = V + (size_t)q * q;    // p x q
-  double* Ts = Ss + (size_t)p * q;   // q x q
-  double* sg = Ts + (size_t)q * q;   // q
-  double* tmp = sg + q;              // q
+  double* W = sm;                   // p x q
+  double* V = W + (size_t)p * q;    // q x q
+  double* Ss = V + (size_t)q * q;   // p x q
+  double* Ts = Ss + (size_t)p * q;  // q x q
+  double* sg = Ts + (size_t)q * q;  // q
+  double* tmp = sg + q;             // q
   int* order = reinterpret_cast<int*>(tmp + q);
   int* flag = order + q + 1;
-  for (int e = threadIdx.x; e < m * n; e += kSVT) {
-    const int i = e % m, j = e / m;
-    const double x = A[i + (int64_t)j * lda];
-    if (tall) W[i + j * p] = x;
-    else W[j + i * p] = x;
-  }
+  for (int j = 0; j < n; ++j)
+    for (int i = threadIdx.x; i < m; i += kSVT) {
+      const double x = A[i + (int64_t)j * lda];
+      if (tall) W[i + j * p] = x;
+      else W[j + i * p] = x;
+    }
   __syncthreads();
   cta_jacobi<kSVT>(W, p, p, q, V, q, flag, deflate);
   cta_svd_finish<kSVT>(W, p, p, q, V, q, sg, order, Ss, p, Ts, q, tmp);
@@ -260,8 +316,10 @@ __global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict_
   const int ldl = tall ? p : q;
   const double* Tr = tall ? Ts : Ss;
   const int ldr = tall ? q : p;
-  for (int e = threadIdx.x; e < m * q; e += kSVT) S[(e % m) + (int64_t)(e / m) * lds] = Sl[(e % m) + (e / m) * ldl];
-  for (int e = threadIdx.x; e < n * q; e += kSVT) T[(e % n) + (int64_t)(e / n) * ldt] = Tr[(e % n) + (e / n) * ldr];
+  for (int j = 0; j < q; ++j) {
+    for (int i = threadIdx.x; i < m; i += kSVT) S[i + (int64_t)j * lds] = Sl[i + j * ldl];
+    for (int i = threadIdx.x; i < n; i += kSVT) T[i + (int64_t)j * ldt] = Tr[i + j * ldr];
+  }
 }
 
 static size_t svd_smem(int m, int n) {
@@ -269,26 +327,35 @@ static size_t svd_smem(int m, int n) {
   return sizeof(double) * (2 * (size_t)p * q + 2 * (size_t)q * q + 2 * (size_t)q + 8) + sizeof(int) * (q + 8);
 }
 
-int launch_svd_small(Context* cx, const double* A, int64_t lda, int m, int n, double* S, int64_t lds, double* sigma,
-                     double* T, int64_t ldt, double deflate) {
+int launch_svd_small_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int m, int n, double* S,
+                             int64_t lds, int64_t sS, double* sigma, int64_t sSig, double* T, int64_t ldt, int64_t sT,
+                             int nb, double deflate) {
   const size_t smem = svd_smem(m, n);
-  if (smem > 220 * 1024) return SLRA_ERR_UNSUPPORTED;
+  if (smem > 220 * 1024 || (m > n ? m : n) > 256) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(svd_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SLRA_TIMED(cx, "svd", svd_cta_kernel<<<1, kSVT, smem, cx->stream>>>(A, lda, m, n, S, lds, sigma, T, ldt, deflate);)
+  SLRA_TIMED(cx, "svd", svd_cta_kernel<<<nb, kSVT, smem, cx->stream>>>(A, lda, sA, m, n, S, lds, sS, sigma, sSig, T,
+                                                                      ldt, sT, deflate);)
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
+}
+
+int launch_svd_small(Context* cx, const double* A, int64_t lda, int m, int n, double* S, int64_t lds, double* sigma,
+                     double* T, int64_t ldt, double deflate) {
+  return launch_svd_small_batched(cx, A, lda, 0, m, n, S, lds, 0, sigma, 0, T, ldt, 0, 1, deflate);
 }
 
 int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                 int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc);
 
-// Sign rule on an externally formed S = Q U_R: per column j, if the first
-// largest-|.| entry is negative flip S(:, j) and T(:, j). One CTA per column.
-__global__ void __launch_bounds__(kDT) colsign_kernel(double* __restrict__ S, int64_t lds, int64_t m,
-                                                      double* __restrict__ T, int64_t ldt, int64_t n) {
+// Sign rule on an externally formed S = Q U_R: per column j of problem y, if
+// the first largest-|.| entry is negative flip S(:, j) and T(:, j).
+__global__ void __launch_bounds__(kDT) colsign_kernel(double* __restrict__ S, int64_t lds, int64_t sS, int64_t m,
+                                                      double* __restrict__ T, int64_t ldt, int64_t sT, int64_t n) {
   __shared__ double rv[40];
   __shared__ int64_t ri[40];
   const int64_t j = blockIdx.x;
+  S += blockIdx.y * sS;
+  if (T) T += blockIdx.y * sT;
   ArgMax a{-1.0, INT64_MAX};
   for (int64_t i = threadIdx.x; i < m; i += kDT) a = argmax_merge(a, ArgMax{fabs(S[i + j * lds]), i});
   a = block_argmax<kDT>(a, rv, ri);
@@ -299,11 +366,17 @@ __global__ void __launch_bounds__(kDT) colsign_kernel(double* __restrict__ S, in
   }
 }
 
-int launch_colsign(Context* cx, double* S, int64_t lds, int64_t m, double* T, int64_t ldt, int64_t n, int64_t cols) {
+int launch_colsign_batched(Context* cx, double* S, int64_t lds, int64_t sS, int64_t m, double* T, int64_t ldt,
+                           int64_t sT, int64_t n, int64_t cols, int nb) {
   if (cols <= 0) return SLRA_OK;
-  SLRA_TIMED(cx, "svd", colsign_kernel<<<(unsigned)cols, kDT, 0, cx->stream>>>(S, lds, m, T, ldt, n);)
+  SLRA_TIMED(cx, "svd", colsign_kernel<<<dim3((unsigned)cols, nb), kDT, 0, cx->stream>>>(S, lds, sS, m, T, ldt, sT,
+                                                                                        n);)
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
+}
+
+int launch_colsign(Context* cx, double* S, int64_t lds, int64_t m, double* T, int64_t ldt, int64_t n, int64_t cols) {
+  return launch_colsign_batched(cx, S, lds, 0, m, T, ldt, 0, n, cols, 1);
 }
 
 __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
@@ -334,34 +407,30 @@ int launch_svd(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, 
                double* sigma, double* T, int64_t ldt) {
   const int64_t q = m < n ? m : n;
   if (q > 64) return SLRA_ERR_UNSUPPORTED;
-  if (svd_smem((int)m, (int)n) <= 200 * 1024 && (m > n ? m : n) <= 256) return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt, 0.0);
+  if (svd_smem((int)m, (int)n) <= 200 * 1024 && (m > n ? m : n) <= 256)
+    return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt, 0.0);
   if (m < n) {
     // wide: A^T = S' Sigma T'^T (tall path), so A = T' Sigma S'^T; the sign
     // rule is then re-applied on the left vectors T' (flipping S' with them).
-    double* At;
-    SLRA_CUDA(cudaMallocAsync(&At, sizeof(double) * (size_t)m * n, cx->stream));
-    int st = launch_transpose(cx, A, lda, m, n, At, n);
-    if (st == SLRA_OK) st = launch_svd(cx, At, n, n, m, T, ldt, sigma, S, lds);
-    if (st == SLRA_OK) st = launch_colsign(cx, S, lds, m, T, ldt, n, m);
-    cudaFreeAsync(At, cx->stream);
-    return st;
+    double* At = static_cast<double*>(arena(cx, 3, sizeof(double) * (size_t)m * n));
+    if (!At) return SLRA_ERR_CUDA;
+    SLRA_TRY(launch_transpose(cx, A, lda, m, n, At, n));
+    SLRA_TRY(launch_svd(cx, At, n, n, m, T, ldt, sigma, S, lds));
+    return launch_colsign(cx, S, lds, m, T, ldt, n, m);
   }
   const int c = (int)n;
-  double* ws = static_cast<double*>(cx->partials ? nullptr : nullptr);
-  (void)ws;
-  // scratch: Q (m x c), R (c x c), UR (c x c): separate allocation so the
-  // TSQR workspace stays free
-  double* buf;
-  SLRA_CUDA(cudaMallocAsync(&buf, sizeof(double) * ((size_t)m * c + 2 * (size_t)c * c), cx->stream));
+  // scratch: Q (m x c), R (c x c), UR (c x c) + the TSQR workspace
+  const size_t tw = tsqr_workspace_doubles(m, c);
+  double* buf = static_cast<double*>(arena(cx, 3, sizeof(double) * ((size_t)m * c + 2 * (size_t)c * c + tw)));
+  if (!buf) return SLRA_ERR_CUDA;
   double* Qm = buf;
   double* Rm = buf + (size_t)m * c;
   double* UR = Rm + (size_t)c * c;
-  int st = launch_thin_qr(cx, A, lda, m, c, Qm, m, Rm, c);
-  if (st == SLRA_OK) st = launch_svd_small(cx, Rm, c, c, c, UR, c, sigma, T, ldt, 0.0);
-  if (st == SLRA_OK) st = launch_gemm(cx, 0, 0, m, c, c, 1.0, Qm, m, UR, c, 0.0, S, lds);
-  if (st == SLRA_OK) st = launch_colsign(cx, S, lds, m, T, ldt, n, c);
-  cudaFreeAsync(buf, cx->stream);
-  return st;
+  double* tws = UR + (size_t)c * c;
+  SLRA_TRY(launch_thin_qr_batched(cx, A, lda, 0, m, c, Qm, m, 0, Rm, c, 0, 1, tw ? tws : nullptr));
+  SLRA_TRY(launch_svd_small(cx, Rm, c, c, c, UR, c, sigma, T, ldt, 0.0));
+  SLRA_TRY(launch_gemm(cx, 0, 0, m, c, c, 1.0, Qm, m, UR, c, 0.0, S, lds));
+  return launch_colsign(cx, S, lds, m, T, ldt, n, c);
 }
 
 // ---------------------------------------------------------------- maxvol / select
@@ -370,21 +439,22 @@ __global__ void __launch_bounds__(kDT) maxvol_cta_kernel(const double* __restric
                                                          int64_t* __restrict__ idx, double* __restrict__ vol,
                                                          int32_t* __restrict__ status) {
   extern __shared__ __align__(16) double sm[];
-  double* S = sm;                       // m x r
-  double* W = S + (size_t)m * r;        // m x r
-  double* Rs = W + (size_t)m * r;       // r x r
-  double* Gt = Rs + (size_t)r * r;      // r x r
-  double* tau = Gt + (size_t)r * r;     // r
-  double* v = tau + r;                  // r
-  double* nu = v + r;                   // m
-  double* nd = nu + m;                  // m
-  double* rv = nd + m;                  // 112 (reduction scratch, >= r + 8)
+  double* S = sm;                    // m x r
+  double* W = S + (size_t)m * r;     // m x r
+  double* Rs = W + (size_t)m * r;    // r x r
+  double* Gt = Rs + (size_t)r * r;   // r x r
+  double* tau = Gt + (size_t)r * r;  // r
+  double* v = tau + r;               // r
+  double* nu = v + r;                // m
+  double* nd = nu + m;               // m
+  double* rv = nd + m;               // 112 (reduction scratch, >= r + 8)
   int64_t* ri = reinterpret_cast<int64_t*>(rv + 112);  // 40
-  int* p2r = reinterpret_cast<int*>(ri + 40);         // m
-  int* I = p2r + m;                                   // count
-  int* perm = I + (count > r ? count : r);            // r
-  int* flag = perm + r;                               // 4
-  for (int e = threadIdx.x; e < m * r; e += kDT) S[e] = A[(e % m) + (int64_t)(e / m) * lda];
+  int* p2r = reinterpret_cast<int*>(ri + 40);          // m
+  int* I = p2r + m;                                    // count
+  int* perm = I + (count > r ? count : r);             // r
+  int* flag = perm + r;                                // 4
+  for (int j = 0; j < r; ++j)
+    for (int i = threadIdx.x; i < m; i += kDT) S[i + j * m] = A[i + (int64_t)j * lda];
   __syncthreads();
   if (qr_first) {
     cta_thin_qr<kDT>(S, m, m, r, W, m, Rs, r, tau, rv);  // Q -> W, then swap roles
@@ -449,8 +519,9 @@ int launch_maxvol(Context* cx, const double* A, int64_t lda, int64_t m, int64_t 
   if (smem > 220 * 1024 || r > 64 || (qr_first && m > 512)) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(maxvol_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
-  SLRA_TIMED(cx, "maxvol", maxvol_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, (int)r, h, (int)max_swaps, qr_first, (int)count,
-                                                   idx, vol, d_status);)
+  SLRA_TIMED(cx, "maxvol",
+             maxvol_cta_kernel<<<1, kDT, smem, cx->stream>>>(A, lda, (int)m, (int)r, h, (int)max_swaps, qr_first,
+                                                             (int)count, idx, vol, d_status);)
   SLRA_CHECK_LAUNCH(cx);
   SLRA_CUDA(cudaMemcpyAsync(cx->hsmall, cx->dsmall, 4, cudaMemcpyDeviceToHost, cx->stream));
   SLRA_CUDA(cudaStreamSynchronize(cx->stream));

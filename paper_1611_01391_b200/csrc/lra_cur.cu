@@ -1,6 +1,8 @@
 // Orchestration of the multi-kernel entry points: cur_evaluate(Frobenius)
-// (cur.cpp:76-82) and range_finder (lra.cpp:14-39). Everything stays on the
-// device; only rank/status decisions are read back.
+// (cur.cpp:76-82) and range_finder (lra.cpp:14-39), the latter batched over
+// several sketches of the same matrix so their latency-bound factorisations
+// overlap (one kernel launch covers all sketches, one CTA per sketch).
+// Everything stays on the device; only rank/status decisions are read back.
 #include "common.cuh"
 
 namespace slra_dev {
@@ -17,31 +19,29 @@ int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, dou
                 int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc);
 int launch_lowrank_residual(Context* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* P,
                             int64_t ldp, const double* Q, int64_t ldq, int64_t inner, double* d_out);
-int launch_thin_qr(Context* cx, const double* A, int64_t lda, int64_t m, int c, double* Q, int64_t ldq, double* R,
-                   int64_t ldr);
-int launch_svd_small(Context* cx, const double* A, int64_t lda, int m, int n, double* S, int64_t lds, double* sigma,
-                     double* T, int64_t ldt, double deflate);
-int launch_colsign(Context* cx, double* S, int64_t lds, int64_t m, double* T, int64_t ldt, int64_t n, int64_t cols);
+size_t tsqr_workspace_doubles(int64_t m, int c);
+int launch_thin_qr_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int64_t m, int c, double* Q,
+                           int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws);
+int launch_svd_small_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int m, int n, double* S,
+                             int64_t lds, int64_t sS, double* sigma, int64_t sSig, double* T, int64_t ldt, int64_t sT,
+                             int nb, double deflate);
+int launch_colsign_batched(Context* cx, double* S, int64_t lds, int64_t sS, int64_t m, double* T, int64_t ldt,
+                           int64_t sT, int64_t n, int64_t cols, int nb);
 
-// Scale columns: X(:, j) *= s[j] (or 1/s[j] when inv).
-__global__ void scale_cols_kernel(double* __restrict__ X, int64_t ldx, int64_t m, int64_t cols,
-                                  const double* __restrict__ s, int inv, double* __restrict__ Y, int64_t ldy) {
+// Y_b(:, j) = X_b(:, j) * s_b[j] (or / s_b[j] when inv), batched over problems.
+__global__ void scale_cols_kernel(const double* __restrict__ X, int64_t ldx, int64_t sX, int64_t m, int64_t cols,
+                                  const double* __restrict__ s, int64_t sS, int inv, double* const* __restrict__ Yp,
+                                  int64_t ldy) {
   const int64_t total = m * cols;
+  const int pb = blockIdx.y;
+  X += pb * sX;
+  s += pb * sS;
+  double* Y = Yp[pb];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e % m, j = e / m;
     const double f = inv ? 1.0 / s[j] : s[j];
     Y[i + j * ldy] = X[i + j * ldx] * f;
   }
-}
-
-int launch_scale_cols(Context* c, double* X, int64_t ldx, int64_t m, int64_t cols, const double* s, int inv,
-                      double* Y, int64_t ldy) {
-  int g = ceil_div(m * cols, 256);
-  if (g > c->num_sms * 8) g = c->num_sms * 8;
-  if (g < 1) g = 1;
-  SLRA_TIMED(c, "scale", scale_cols_kernel<<<g, 256, 0, c->stream>>>(X, ldx, m, cols, s, inv, Y, ldy);)
-  SLRA_CHECK_LAUNCH(c);
-  return SLRA_OK;
 }
 
 }  // namespace slra_dev
@@ -63,66 +63,114 @@ int slra_cur_residual(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
   double* Rm = Cm + (size_t)m * l;
   double* CU = Rm + (size_t)k * n;
   double* out = CU + (size_t)m * k;
-  int st = launch_gather_cols(cx, A, lda, m, J, l, Cm, m);
-  if (st == SLRA_OK) st = launch_gather_rows(cx, A, lda, n, I, k, Rm, k);
+  SLRA_TRY(launch_gather_cols(cx, A, lda, m, J, l, Cm, m));
+  SLRA_TRY(launch_gather_rows(cx, A, lda, n, I, k, Rm, k));
   // (C U) R, Eigen's left-to-right evaluation (cur.cpp:76-78)
-  if (st == SLRA_OK) st = launch_gemm(cx, 0, 0, m, k, l, 1.0, Cm, m, U, ldu, 0.0, CU, m);
-  if (st == SLRA_OK) st = launch_lowrank_residual(cx, A, lda, m, n, CU, m, Rm, k, k, out);
+  SLRA_TRY(launch_gemm(cx, 0, 0, m, k, l, 1.0, Cm, m, U, ldu, 0.0, CU, m));
+  SLRA_TRY(launch_lowrank_residual(cx, A, lda, m, n, CU, m, Rm, k, k, out));
   double* hs = static_cast<double*>(cx->hsmall);
-  if (st == SLRA_OK) cudaMemcpyAsync(hs, out, 16, cudaMemcpyDeviceToHost, cx->stream);
+  SLRA_CUDA(cudaMemcpyAsync(hs, out, 16, cudaMemcpyDeviceToHost, cx->stream));
   SLRA_CUDA(cudaStreamSynchronize(cx->stream));
-  if (st != SLRA_OK) return st;
   if (h_resid_sq) *h_resid_sq = hs[0];
   if (h_norm_sq) *h_norm_sq = hs[1];
   return SLRA_OK;
 }
 
-// range_finder: MH (sketch plan) -> Q R (thin QR / TSQR) -> SVD(R) -> rank
-// check -> U, V -> residual. Workspace is allocated once per shape.
+// range_finder over nsk sketches H_s of one M: MH_s (plans) -> Q_s R_s (batched
+// thin QR / TSQR) -> SVD(R_s) (batched, one CTA each) -> one rank check for
+// all -> U_s, V_s -> residuals. Host-array arguments (h_*) hold per-sketch
+// device pointers / sizes.
+int slra_range_finder_batched(slra_ctx ctx, const double* M, int64_t ldm, int64_t m, int64_t n, int nsk,
+                              const int64_t* const* h_src, const double* const* h_coef, const int32_t* const* h_q,
+                              const int64_t* h_width, const int* h_tree, int64_t l, int64_t r, int variant,
+                              double* const* h_U, int64_t ldu, double* const* h_V, int64_t ldv, double* d_out,
+                              double* d_sigma, int32_t* h_status) {
+  if (!ctx || ldm < m || l < 1 || r < 1 || r > l || l > m || l > 64 || nsk < 1 || nsk > 64)
+    return SLRA_ERR_INVALID_ARGUMENT;
+  Context* cx = C(ctx);
+  const int64_t ucols = variant == 1 ? r : l;
+  if (ldu < m || ldv < ucols) return SLRA_ERR_INVALID_ARGUMENT;
+  const size_t tw = tsqr_workspace_doubles(m, (int)l);
+  const size_t per = 2 * (size_t)m * l + 3 * (size_t)l * l + (size_t)l + tw;
+  double* buf = static_cast<double*>(arena(cx, 0, sizeof(double) * (per * nsk + 64)));
+  if (!buf) return SLRA_ERR_CUDA;
+  const int64_t sMH = m * l, sLL = l * l;
+  double* MH = buf;                     // nsk x (m x l)
+  double* Qm = MH + (size_t)nsk * sMH;  // nsk x (m x l)
+  double* Rm = Qm + (size_t)nsk * sMH;  // nsk x (l x l)
+  double* UR = Rm + (size_t)nsk * sLL;
+  double* VR = UR + (size_t)nsk * sLL;
+  double* sig = VR + (size_t)nsk * sLL;  // nsk x l
+  double* tws = sig + (size_t)nsk * l;   // TSQR workspace (nsk problems)
+  double** dptr = reinterpret_cast<double**>(static_cast<char*>(cx->dsmall) + 2048);  // 2*nsk pointers
+  for (int s = 0; s < nsk; ++s)
+    SLRA_TRY(launch_sketch_cols(cx, M, ldm, m, h_src[s], h_coef[s], h_q[s], h_width[s], h_tree[s], l,
+                                MH + s * sMH, m));
+  SLRA_TRY(launch_thin_qr_batched(cx, MH, m, sMH, m, (int)l, Qm, m, sMH, Rm, l, sLL, nsk, tw ? tws : nullptr));
+  // TruncatedRankR only needs the top r triplets and the count of sigma above
+  // the cut: Jacobi skips pairs of columns below cut / sqrt(l) (dense_cta.cuh)
+  const double deflate = variant == 1 ? 1e-10 / sqrt((double)l) : 0.0;
+  SLRA_TRY(launch_svd_small_batched(cx, Rm, l, sLL, (int)l, (int)l, UR, l, sLL, sig, l, VR, l, sLL, nsk, deflate));
+  if (d_sigma) SLRA_CUDA(cudaMemcpyAsync(d_sigma, sig, 8 * l * nsk, cudaMemcpyDeviceToDevice, cx->stream));
+  // rank check: numerical_rank(MH, 1e-10, Relative) < r -> RangeFailure
+  double* hs = static_cast<double*>(cx->hsmall);
+  SLRA_CUDA(cudaMemcpyAsync(hs, sig, 8 * l * nsk, cudaMemcpyDeviceToHost, cx->stream));
+  SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+  int first_fail = -1;
+  std::vector<int> ok(nsk, 1);
+  for (int s = 0; s < nsk; ++s) {
+    int64_t rank = 0;
+    for (int64_t i = 0; i < l; ++i) rank += (hs[s * l + i] > 1e-10 * hs[s * l]) ? 1 : 0;
+    const int st = rank < r ? SLRA_ERR_RANGE_FAILURE : SLRA_OK;
+    ok[s] = st == SLRA_OK;
+    if (h_status) h_status[s] = st;
+    if (st != SLRA_OK && first_fail < 0) first_fail = s;
+  }
+  if (first_fail >= 0 && !h_status) return SLRA_ERR_RANGE_FAILURE;
+  if (variant == 1) {
+    // TruncatedRankR: S = Q U_R with the svd sign rule on S; U = S_r Sigma_r;
+    // V = U^+ M = Sigma_r^-1 S_r^T M (U's SVD is S_r, Sigma_r, I).
+    double* S = MH;  // reuse: nsk x (m x l)
+    for (int s = 0; s < nsk; ++s)
+      SLRA_TRY(launch_gemm(cx, 0, 0, m, l, l, 1.0, Qm + s * sMH, m, UR + s * sLL, l, 0.0, S + s * sMH, m));
+    SLRA_TRY(launch_colsign_batched(cx, S, m, sMH, m, VR, l, sLL, l, l, nsk));
+    std::vector<double*> hp(2 * nsk);
+    for (int s = 0; s < nsk; ++s) {
+      hp[s] = h_U[s];
+      hp[nsk + s] = Qm + s * sMH;
+    }
+    SLRA_CUDA(cudaMemcpyAsync(dptr, hp.data(), sizeof(double*) * 2 * nsk, cudaMemcpyHostToDevice, cx->stream));
+    int g = ceil_div(m * r, 256);
+    if (g > cx->num_sms * 4) g = cx->num_sms * 4;
+    // U = S_r Sigma_r ; Qm := S_r Sigma_r^-1
+    SLRA_TIMED(cx, "scale", scale_cols_kernel<<<dim3(g, nsk), 256, 0, cx->stream>>>(S, m, sMH, m, r, sig, l, 0, dptr,
+                                                                                    ldu);)
+    SLRA_CHECK_LAUNCH(cx);
+    SLRA_TIMED(cx, "scale", scale_cols_kernel<<<dim3(g, nsk), 256, 0, cx->stream>>>(S, m, sMH, m, r, sig, l, 1,
+                                                                                    dptr + nsk, m);)
+    SLRA_CHECK_LAUNCH(cx);
+    for (int s = 0; s < nsk; ++s)
+      if (ok[s]) SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, r, n, m, 1.0, Qm + s * sMH, m, M, ldm, 0.0, h_V[s], ldv));
+  } else {
+    // BasisQr: U = Q (thin_qr sign rule already applied), V = U^T M
+    for (int s = 0; s < nsk; ++s) {
+      SLRA_CUDA(cudaMemcpy2DAsync(h_U[s], 8 * ldu, Qm + s * sMH, 8 * m, 8 * m, l, cudaMemcpyDeviceToDevice,
+                                  cx->stream));
+      if (ok[s]) SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, l, n, m, 1.0, h_U[s], ldu, M, ldm, 0.0, h_V[s], ldv));
+    }
+  }
+  if (d_out)
+    for (int s = 0; s < nsk; ++s)
+      if (ok[s]) SLRA_TRY(launch_lowrank_residual(cx, M, ldm, m, n, h_U[s], ldu, h_V[s], ldv, ucols, d_out + 2 * s));
+  return SLRA_OK;
+}
+
 int slra_range_finder(slra_ctx ctx, const double* M, int64_t ldm, int64_t m, int64_t n, const int64_t* src,
                       const double* coef, const int32_t* q, int64_t width, int tree, int64_t l, int64_t r,
                       int variant, double* U, int64_t ldu, double* V, int64_t ldv, double* d_out,
                       double* d_sigma) {
-  if (!ctx || ldm < m || l < 1 || r < 1 || r > l || l > m || l > 64) return SLRA_ERR_INVALID_ARGUMENT;
-  Context* cx = C(ctx);
-  const int64_t ucols = variant == 1 ? r : l;
-  if (ldu < m || ldv < ucols) return SLRA_ERR_INVALID_ARGUMENT;
-  const size_t need = 2 * (size_t)m * l + 3 * (size_t)l * l + 2 * (size_t)l + 64;
-  double* buf = static_cast<double*>(arena(cx, 0, sizeof(double) * need));
-  if (!buf) return SLRA_ERR_CUDA;
-  double* MH = buf;                       // m x l
-  double* Qm = MH + (size_t)m * l;        // m x l
-  double* Rm = Qm + (size_t)m * l;        // l x l
-  double* UR = Rm + (size_t)l * l;        // l x l
-  double* VR = UR + (size_t)l * l;        // l x l
-  double* sig = VR + (size_t)l * l;       // l
-  SLRA_TRY(launch_sketch_cols(cx, M, ldm, m, src, coef, q, width, tree, l, MH, m));
-  SLRA_TRY(launch_thin_qr(cx, MH, m, m, (int)l, Qm, m, Rm, l));
-  SLRA_TRY(launch_svd_small(cx, Rm, l, (int)l, (int)l, UR, l, sig, VR, l, 1e-10 / sqrt((double)l)));
-  if (d_sigma) SLRA_CUDA(cudaMemcpyAsync(d_sigma, sig, 8 * l, cudaMemcpyDeviceToDevice, cx->stream));
-  // rank check: numerical_rank(MH, 1e-10, Relative) < r -> RangeFailure
-  double* hs = static_cast<double*>(cx->hsmall);
-  SLRA_CUDA(cudaMemcpyAsync(hs, sig, 8 * l, cudaMemcpyDeviceToHost, cx->stream));
-  SLRA_CUDA(cudaStreamSynchronize(cx->stream));
-  int64_t rank = 0;
-  for (int64_t i = 0; i < l; ++i) rank += (hs[i] > 1e-10 * hs[0]) ? 1 : 0;
-  if (rank < r) return SLRA_ERR_RANGE_FAILURE;
-  if (variant == 0) {
-    // BasisQr: U = Q (thin_qr sign rule already applied), V = U^T M
-    SLRA_CUDA(cudaMemcpy2DAsync(U, 8 * ldu, Qm, 8 * m, 8 * m, l, cudaMemcpyDeviceToDevice, cx->stream));
-    SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, l, n, m, 1.0, U, ldu, M, ldm, 0.0, V, ldv));
-  } else {
-    // TruncatedRankR: S = Q U_R with the svd sign rule on S; U = S_r Sigma_r;
-    // V = U^+ M = Sigma_r^-1 S_r^T M (U's SVD is S_r, Sigma_r, I).
-    double* S = MH;  // reuse: m x l
-    SLRA_TRY(launch_gemm(cx, 0, 0, m, l, l, 1.0, Qm, m, UR, l, 0.0, S, m));
-    SLRA_TRY(launch_colsign(cx, S, m, m, VR, l, l, l));
-    SLRA_TRY(launch_scale_cols(cx, S, m, m, r, sig, 0, U, ldu));    // U = S_r Sigma_r
-    SLRA_TRY(launch_scale_cols(cx, S, m, m, r, sig, 1, Qm, m));     // Qm := S_r Sigma_r^-1
-    SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, r, n, m, 1.0, Qm, m, M, ldm, 0.0, V, ldv));
-  }
-  if (d_out) SLRA_TRY(launch_lowrank_residual(cx, M, ldm, m, n, U, ldu, V, ldv, ucols, d_out));
-  return SLRA_OK;
+  return slra_range_finder_batched(ctx, M, ldm, m, n, 1, &src, &coef, &q, &width, &tree, l, r, variant, &U, ldu, &V,
+                                   ldv, d_out, d_sigma, nullptr);
 }
 
 }  // extern "C"

@@ -287,6 +287,34 @@ PYBIND11_MODULE(_slra, m) {
                             ptr<double>(out), nullptr),
           "range_finder");
   });
+  // nsk sketches of one HBM-resident M in one call: plans = [(width, tree, src_ptr, coef_ptr, q_ptr), ...]
+  m.def("range_finder_batched_device", [](uintptr_t M, Index ldm, Index mm, Index n,
+                                          const std::vector<std::tuple<Index, int, uintptr_t, uintptr_t, uintptr_t>>& plans,
+                                          Index l, Index r, bool truncated, const std::vector<uintptr_t>& U, Index ldu,
+                                          const std::vector<uintptr_t>& V, Index ldv, uintptr_t out) {
+    const int nsk = static_cast<int>(plans.size());
+    std::vector<const int64_t*> src(nsk);
+    std::vector<const double*> coef(nsk);
+    std::vector<const int32_t*> q(nsk);
+    std::vector<int64_t> width(nsk);
+    std::vector<int> tree(nsk);
+    std::vector<double*> Up(nsk), Vp(nsk);
+    for (int s = 0; s < nsk; ++s) {
+      width[s] = std::get<0>(plans[s]);
+      tree[s] = std::get<1>(plans[s]);
+      src[s] = ptr<const int64_t>(std::get<2>(plans[s]));
+      coef[s] = ptr<const double>(std::get<3>(plans[s]));
+      q[s] = ptr<const int32_t>(std::get<4>(plans[s]));
+      Up[s] = ptr<double>(U[s]);
+      Vp[s] = ptr<double>(V[s]);
+    }
+    std::vector<int32_t> status(nsk, 0);
+    check(slra_range_finder_batched(device_context(), ptr<double>(M), ldm, mm, n, nsk, src.data(), coef.data(),
+                                    q.data(), width.data(), tree.data(), l, r, truncated ? 1 : 0, Up.data(), ldu,
+                                    Vp.data(), ldv, ptr<double>(out), nullptr, status.data()),
+          "range_finder_batched");
+    for (int s = 0; s < nsk; ++s) check(status[s], "range_finder_batched");
+  });
   m.def("cross_approx_batched_device", [](uintptr_t A, Index lda, Index stride, Index nblocks, Index mm, Index n,
                                           Index r, Index k, Index l, uintptr_t init_rows, int loops, double h,
                                           uintptr_t I, uintptr_t J, uintptr_t U, uintptr_t rr, uintptr_t status,
