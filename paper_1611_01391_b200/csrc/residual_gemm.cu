@@ -214,8 +214,16 @@ __global__ void reduce_pairs_kernel(const double* __restrict__ part, int n, doub
   }
 }
 
+int launch_residual_stream(Context* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* P,
+                           int64_t ldp, const double* Q, int64_t ldq, int64_t inner, double* d_out);
+int launch_tn_skinny(Context* c, const char* fam, int64_t r, int64_t n, int64_t K, double alpha, const double* W,
+                     int64_t ldw, const double* B, int64_t ldb, double* Cm, int64_t ldc);
+
 int launch_lowrank_residual(Context* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* P,
                             int64_t ldp, const double* Q, int64_t ldq, int64_t inner, double* d_out) {
+  // pipelined streaming kernel when the operands suit it (stream_dmma.cu)
+  const int st = launch_residual_stream(c, A, lda, m, n, P, ldp, Q, ldq, inner, d_out);
+  if (st != SLRA_ERR_UNSUPPORTED) return st;
   ResidualArgs a{A, lda, m, n, P, ldp, Q, ldq, inner, 1, 0, 0, 0, nullptr, 0};
   const int64_t tiles = ((m + kBM - 1) / kBM) * ((n + kBN - 1) / kBN);
   int grid = c->num_sms * 2;
@@ -366,6 +374,11 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int64_t m,
 int launch_gemm_fam(Context* c, const char* fam, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                 int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc) {
   if (m == 0 || n == 0) return SLRA_OK;
+  if (ta == 1 && tb == 0 && beta == 0.0 && m <= 64 && k >= 256) {
+    // skinny W^T B over a tall K (range finder V = U^+ M): streaming kernel
+    const int st = launch_tn_skinny(c, fam, m, n, k, alpha, A, lda, B, ldb, Cm, ldc);
+    if (st != SLRA_ERR_UNSUPPORTED) return st;
+  }
   GemmArgs g{ta, tb, m, n, k, alpha, beta, A, lda, B, ldb, Cm, ldc, k, nullptr};
   const int gx = ceil_div(m, kBM), gy = ceil_div(n, kBN);
   int nz = 1;

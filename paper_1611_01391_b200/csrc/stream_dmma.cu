@@ -1,0 +1,438 @@
+// Streaming FP64 tensor-core kernels for the two HBM-sized products of the
+// hot path (both read A once, FLOP:byte ~8 at inner dimension 32, i.e. just
+// above the B200 FP64 ridge of 37.2 TF/s / 6.55 TB/s ~ 5.7):
+//
+//   residual_stream:  sum (A - P Q)^2 and sum A^2 over A (m x n), P m x r,
+//                     Q r x n, r <= 32  — cur_evaluate(M, c, Frobenius)
+//                     (cur.cpp:80-82) and ||M - U V||_F (lra.cpp:35-36).
+//   tn_skinny:        C = W^T B (r x n, r <= 64) — V = U^+ M / U^T M of the
+//                     range finder (lra.cpp:35-36).
+//
+// Both stage their tiles with cp.async (16-byte, zero-filled at the edges)
+// into double-buffered shared memory so the next tile streams in while the
+// current one runs on DMMA (mma.sync.m8n8k4.f64), and both reduce
+// deterministically (fixed per-CTA partials, fixed-order final sum).
+#include "common.cuh"
+
+namespace slra_dev {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---------------------------------------------------------------- residual
+namespace rs {
+constexpr int NT = 256;        // 8 warps: 4 (rows) x 2 (cols), warp tile 32 x 16
+constexpr int TM = 128;        // tile rows
+constexpr int TN = 32;         // tile cols
+constexpr int KP = 32;         // inner dimension (padded)
+constexpr int LDU = TM + 4;    // Us[k][row]
+constexpr int LDV = KP + 4;    // Vs[col][k]
+constexpr int LDM = TM + 2;    // Ms[col][row]
+constexpr int U_D = KP * LDU;  // doubles per U buffer
+constexpr int V_D = TN * LDV;
+constexpr int M_D = TN * LDM;
+constexpr size_t SMEM = sizeof(double) * 2 * (U_D + V_D + M_D);
+}  // namespace rs
+
+struct StreamResidualArgs {
+  const double* A;
+  int64_t lda, m, n;
+  const double* P;
+  int64_t ldp;
+  const double* Q;
+  int64_t ldq;
+  int inner;
+  double* part;  // 2 per CTA
+};
+
+__device__ __forceinline__ void rs_stage(const StreamResidualArgs& a, int64_t i0, int64_t j0, bool load_v, double* Us,
+                                         double* Vs, double* Ms) {
+  using namespace rs;
+  const int tid = threadIdx.x;
+  // M tile: TN columns x TM rows, 16-byte chunks of 2 rows
+  for (int e = tid; e < TN * (TM / 2); e += NT) {
+    const int col = e / (TM / 2), ch = e % (TM / 2);
+    const int64_t r = i0 + 2 * ch, cc = j0 + col;
+    int bytes = 0;
+    const double* src = a.A;
+    if (cc < a.n && r < a.m) {
+      bytes = (r + 1 < a.m) ? 16 : 8;
+      src = a.A + r + cc * a.lda;
+    }
+    cp_async16(Ms + col * LDM + 2 * ch, src, bytes);
+  }
+  // U tile: k-major (columns of P), TM rows
+  for (int e = tid; e < KP * (TM / 2); e += NT) {
+    const int k = e / (TM / 2), ch = e % (TM / 2);
+    const int64_t r = i0 + 2 * ch;
+    int bytes = 0;
+    const double* src = a.P;
+    if (k < a.inner && r < a.m) {
+      bytes = (r + 1 < a.m) ? 16 : 8;
+      src = a.P + r + (int64_t)k * a.ldp;
+    }
+    cp_async16(Us + k * LDU + 2 * ch, src, bytes);
+  }
+  if (load_v) {
+    // V tile: per column, the inner entries are contiguous
+    for (int e = tid; e < TN * (KP / 2); e += NT) {
+      const int col = e / (KP / 2), ch = e % (KP / 2);
+      const int k = 2 * ch;
+      const int64_t cc = j0 + col;
+      int bytes = 0;
+      const double* src = a.Q;
+      if (cc < a.n && k < a.inner) {
+        bytes = (k + 1 < a.inner) ? 16 : 8;
+        src = a.Q + k + cc * a.ldq;
+      }
+      cp_async16(Vs + col * LDV + k, src, bytes);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(rs::NT, 1) residual_stream_kernel(StreamResidualArgs a) {
+  using namespace rs;
+  extern __shared__ __align__(16) double smem[];
+  // buffer b of U / V / M (pointer arithmetic, no local-memory pointer arrays)
+#define UB(b) (smem + (b) * U_D)
+#define VB(b) (smem + 2 * U_D + (b) * V_D)
+#define MB(b) (smem + 2 * U_D + 2 * V_D + (b) * M_D)
+  __shared__ double red[40];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t tiles_m = (a.m + TM - 1) / TM, tiles_n = (a.n + TN - 1) / TN;
+  const int64_t tiles = tiles_m * tiles_n;
+  // contiguous tile range per CTA (row-fastest), so consecutive tiles share V
+  const int64_t t0 = tiles * blockIdx.x / gridDim.x, t1 = tiles * (blockIdx.x + 1) / gridDim.x;
+  const int kc4 = (a.inner + 3) & ~3;
+  double rsum = 0.0, nsum = 0.0;
+  int buf = 0;
+  int64_t vj = -1;   // column tile currently staged in Vb[vbuf]
+  int vbuf = 0;
+  if (t0 < t1) {
+    const int64_t i0 = (t0 % tiles_m) * TM, j0 = (t0 / tiles_m) * TN;
+    rs_stage(a, i0, j0, true, UB(0), VB(0), MB(0));
+    vj = j0;
+  }
+  cp_async_commit();
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t i0 = (t % tiles_m) * TM, j0 = (t / tiles_m) * TN;
+    // prefetch the next tile into the other buffers
+    if (t + 1 < t1) {
+      const int64_t ni0 = ((t + 1) % tiles_m) * TM, nj0 = ((t + 1) / tiles_m) * TN;
+      const bool nv = nj0 != vj;
+      rs_stage(a, ni0, nj0, nv, UB(buf ^ 1), VB(nv ? (vbuf ^ 1) : vbuf), MB(buf ^ 1));
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* Us = UB(buf);
+    const double* Vs = VB(vbuf);
+    const double* Ms = MB(buf);
+    double acc[4][2][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    for (int kk = 0; kk < kc4; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = Us[(kk + t4) * LDU + wm * 32 + mi * 8 + g];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) bf[ni] = Vs[(wn * 16 + ni * 8 + g) * LDV + kk + t4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int row = wm * 32 + mi * 8 + g, col = wn * 16 + ni * 8 + 2 * t4 + e;
+          const double x = Ms[col * LDM + row];  // zero outside A (zero-filled)
+          const double d = x - acc[mi][ni][e];
+          rsum = fma(d, d, rsum);
+          nsum = fma(x, x, nsum);
+        }
+    __syncthreads();  // buffers of this tile may be overwritten by the next prefetch
+    if (t + 1 < t1) {
+      const int64_t nj0 = ((t + 1) / tiles_m) * TN;
+      if (nj0 != vj) {
+        vbuf ^= 1;
+        vj = nj0;
+      }
+    }
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+#undef UB
+#undef VB
+#undef MB
+  rsum = block_sum<NT>(rsum, red);
+  nsum = block_sum<NT>(nsum, red);
+  if (threadIdx.x == 0) {
+    a.part[2 * blockIdx.x] = rsum;
+    a.part[2 * blockIdx.x + 1] = nsum;
+  }
+}
+
+__global__ void reduce_pairs2_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double red[40];
+  double r = 0.0, s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    r += part[2 * i];
+    s += part[2 * i + 1];
+  }
+  r = block_sum<256>(r, red);
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) {
+    out[0] = r;
+    out[1] = s;
+  }
+}
+
+// Returns SLRA_ERR_UNSUPPORTED when the shape/alignment does not suit the
+// streaming kernel (caller falls back to the generic one).
+int launch_residual_stream(Context* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* P,
+                           int64_t ldp, const double* Q, int64_t ldq, int64_t inner, double* d_out) {
+  const bool aligned = ((uintptr_t)A % 16 == 0) && (lda % 2 == 0) && (inner == 0 || (((uintptr_t)P % 16 == 0) &&
+                       (ldp % 2 == 0) && ((uintptr_t)Q % 16 == 0) && (ldq % 2 == 0)));
+  if (!aligned || inner > rs::KP || m < 1 || n < 1) return SLRA_ERR_UNSUPPORTED;
+  const int64_t tiles = ((m + rs::TM - 1) / rs::TM) * ((n + rs::TN - 1) / rs::TN);
+  int grid = c->num_sms;
+  if (tiles < grid) grid = (int)tiles;
+  double* part = partials(c, 2 * grid);
+  if (!part) return SLRA_ERR_CUDA;
+  StreamResidualArgs a{A, lda, m, n, inner ? P : A, inner ? ldp : 2, inner ? Q : A, inner ? ldq : 2, (int)inner,
+                       part};
+  SLRA_CUDA(cudaFuncSetAttribute(residual_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs::SMEM));
+  SLRA_TIMED(c, "residual", residual_stream_kernel<<<grid, rs::NT, rs::SMEM, c->stream>>>(a);)
+  SLRA_CHECK_LAUNCH(c);
+  SLRA_TIMED(c, "residual_reduce", reduce_pairs2_kernel<<<1, 256, 0, c->stream>>>(part, grid, d_out);)
+  SLRA_CHECK_LAUNCH(c);
+  return SLRA_OK;
+}
+
+// ---------------------------------------------------------------- C = W^T B
+// W (K x r, ld ldw), B (K x n, ld ldb), C (r x n, ld ldc), r <= 64.
+// CTA = 64 output columns x one K-slice; each warp owns a K sub-slice of the
+// staged K-tile and accumulates the full r x 64 output block (up to 8 x 8
+// fragments); warps reduce through smem at the end, K-slices through a
+// deterministic split-K combine.
+namespace tn {
+constexpr int NT = 256;
+constexpr int TK = 64;         // K rows per stage
+constexpr int TN = 64;         // output columns per CTA
+constexpr int RP = 64;         // max r
+constexpr int LDW = RP + 4;    // Ws[k][r]   (W rows are strided in global: staged via k-major chunks)
+constexpr int LDB = TK + 4;    // Bs[col][k]
+constexpr int W_D = TK * LDW;
+constexpr int B_D = TN * LDB;
+constexpr size_t SMEM = sizeof(double) * 2 * (W_D + B_D);
+}  // namespace tn
+
+struct TnArgs {
+  const double* W;
+  int64_t ldw;
+  const double* B;
+  int64_t ldb;
+  int64_t K, n;
+  int r;
+  int64_t kslice;
+  double* part;  // split-K partials: [z][r x n] (ld r), or null -> C directly
+  double* C;
+  int64_t ldc;
+};
+
+__device__ __forceinline__ void tn_stage(const TnArgs& a, int64_t k0, int64_t j0, int64_t kend, double* Ws,
+                                         double* Bs) {
+  using namespace tn;
+  const int tid = threadIdx.x;
+  // W rows k0..k0+TK, columns 0..r: W is column-major (K x r): for fixed
+  // column q the rows are contiguous -> chunks of 2 rows land at Ws[k][q],
+  // Ws[k+1][q] which are NOT contiguous; stage W^T instead: Ws[q][k].
+  for (int e = tid; e < RP * (TK / 2); e += NT) {
+    const int q = e / (TK / 2), ch = e % (TK / 2);
+    const int64_t k = k0 + 2 * ch;
+    int bytes = 0;
+    const double* src = a.W;
+    if (q < a.r && k < kend) {
+      bytes = (k + 1 < kend) ? 16 : 8;
+      src = a.W + k + (int64_t)q * a.ldw;
+    }
+    cp_async16(Ws + q * LDB + 2 * ch, src, bytes);
+  }
+  for (int e = tid; e < TN * (TK / 2); e += NT) {
+    const int col = e / (TK / 2), ch = e % (TK / 2);
+    const int64_t k = k0 + 2 * ch, cc = j0 + col;
+    int bytes = 0;
+    const double* src = a.B;
+    if (cc < a.n && k < kend) {
+      bytes = (k + 1 < kend) ? 16 : 8;
+      src = a.B + k + cc * a.ldb;
+    }
+    cp_async16(Bs + col * LDB + 2 * ch, src, bytes);
+  }
+}
+
+template <int RF>  // RF = r rounded up to 8, in fragments of 8 (1..8)
+__global__ void __launch_bounds__(tn::NT, 1) tn_skinny_kernel(TnArgs a) {
+  using namespace tn;
+  extern __shared__ __align__(16) double smem[];
+  // Ws is stored [q][k] with ld LDB (same shape as Bs: 64 x TK)
+#define WB(b) (smem + (b) * B_D)
+#define BB(b) (smem + (2 + (b)) * B_D)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t j0 = (int64_t)blockIdx.x * TN;
+  const int64_t kb = (int64_t)blockIdx.y * a.kslice;
+  int64_t ke = kb + a.kslice;
+  if (ke > a.K) ke = a.K;
+  double acc[RF][8][2];
+#pragma unroll
+  for (int mi = 0; mi < RF; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 8; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  int buf = 0;
+  if (kb < ke) tn_stage(a, kb, j0, ke, WB(0), BB(0));
+  cp_async_commit();
+  for (int64_t k0 = kb; k0 < ke; k0 += TK) {
+    if (k0 + TK < ke) tn_stage(a, k0 + TK, j0, ke, WB(buf ^ 1), BB(buf ^ 1));
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* Ws = WB(buf);
+    const double* Bs = BB(buf);
+    // warp w takes k sub-slice [w*8, w*8+8) of this stage: two k4 steps
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int kk = warp * 8 + s * 4 + t4;
+      double af[RF], bf[8];
+#pragma unroll
+      for (int mi = 0; mi < RF; ++mi) af[mi] = Ws[(mi * 8 + g) * LDB + kk];
+#pragma unroll
+      for (int ni = 0; ni < 8; ++ni) bf[ni] = Bs[(ni * 8 + g) * LDB + kk];
+#pragma unroll
+      for (int mi = 0; mi < RF; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 8; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+#undef WB
+#undef BB
+  // cross-warp reduction of the r x 64 block through smem (fixed order)
+  double* red = smem;  // reuse: NT/32 x (RF*8 x 64)
+  __syncthreads();
+  const int blk = RF * 8 * TN;
+#pragma unroll
+  for (int mi = 0; mi < RF; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 8; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = mi * 8 + g, col = ni * 8 + 2 * t4 + e;
+        red[warp * blk + col * (RF * 8) + row] = acc[mi][ni][e];
+      }
+  __syncthreads();
+  for (int e = threadIdx.x; e < blk; e += NT) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) s += red[w * blk + e];
+    const int row = e % (RF * 8), col = e / (RF * 8);
+    const int64_t cc = j0 + col;
+    if (row < a.r && cc < a.n) {
+      if (a.part)
+        a.part[(int64_t)blockIdx.y * a.r * a.n + row + cc * a.r] = s;
+      else
+        a.C[row + cc * a.ldc] = s;
+    }
+  }
+}
+
+__global__ void splitk_sum_kernel(const double* __restrict__ part, int64_t r, int64_t n, int nz, double alpha,
+                                  double* __restrict__ Cm, int64_t ldc) {
+  const int64_t total = r * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < nz; ++z) s += part[z * total + e];
+    Cm[(e % r) + (e / r) * ldc] = alpha * s;
+  }
+}
+
+// C (r x n) = alpha * W^T B. Returns SLRA_ERR_UNSUPPORTED when unsuitable.
+int launch_tn_skinny(Context* c, const char* fam, int64_t r, int64_t n, int64_t K, double alpha, const double* W,
+                     int64_t ldw, const double* B, int64_t ldb, double* Cm, int64_t ldc) {
+  const bool aligned = ((uintptr_t)W % 16 == 0) && (ldw % 2 == 0) && ((uintptr_t)B % 16 == 0) && (ldb % 2 == 0);
+  if (!aligned || r < 1 || r > 56 || K < 256) return SLRA_ERR_UNSUPPORTED;  // r > 56 would spill
+  const int gx = ceil_div(n, tn::TN);
+  // split-K so that the grid fills whole waves of one CTA per SM
+  int64_t maxz = K / 512;
+  if (maxz < 1) maxz = 1;
+  int nz = 1;
+  double best = 1e30;
+  for (int z = 1; z <= maxz && z <= 32; ++z) {
+    const double ctas = (double)gx * z;
+    const double waves = ceil(ctas / c->num_sms);
+    const double eff = ctas / (waves * c->num_sms);  // fraction of busy SM-slots
+    const double cost = waves / (double)z + (eff < 0.5 ? 1.0 : 0.0);  // time ~ waves * (K / z)
+    if (cost < best - 1e-9) {
+      best = cost;
+      nz = z;
+    }
+  }
+  int64_t ks = (K + nz - 1) / nz;
+  ks = (ks + tn::TK - 1) / tn::TK * tn::TK;
+  nz = (int)((K + ks - 1) / ks);
+  double* part = nullptr;
+  if (nz > 1) {
+    part = static_cast<double*>(workspace(c, sizeof(double) * r * n * nz));
+    if (!part) return SLRA_ERR_CUDA;
+  }
+  TnArgs a{W, ldw, B, ldb, K, n, (int)r, ks, part, Cm, ldc};
+  const size_t smem_main = tn::SMEM;
+  const int RF = (int)((r + 7) / 8);
+  const size_t smem_red = sizeof(double) * (tn::NT / 32) * RF * 8 * tn::TN;
+  const size_t smem = smem_main > smem_red ? smem_main : smem_red;
+  dim3 grid(gx, nz);
+#define SLRA_TN_CASE(RFV)                                                                                     \
+  case RFV:                                                                                                   \
+    SLRA_CUDA(cudaFuncSetAttribute(tn_skinny_kernel<RFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    SLRA_TIMED(c, fam, tn_skinny_kernel<RFV><<<grid, tn::NT, smem, c->stream>>>(a);)                        \
+    break;
+  switch (RF) {
+    SLRA_TN_CASE(1)
+    SLRA_TN_CASE(2)
+    SLRA_TN_CASE(3)
+    SLRA_TN_CASE(4)
+    SLRA_TN_CASE(5)
+    SLRA_TN_CASE(6)
+    SLRA_TN_CASE(7)
+    default: return SLRA_ERR_UNSUPPORTED;
+  }
+#undef SLRA_TN_CASE
+  SLRA_CHECK_LAUNCH(c);
+  if (nz > 1 || alpha != 1.0) {
+    if (nz == 1) return SLRA_ERR_UNSUPPORTED;  // (alpha != 1 without split: not used on the path)
+    int rg = ceil_div(r * n, 256);
+    if (rg > c->num_sms * 8) rg = c->num_sms * 8;
+    SLRA_TIMED(c, "gemm_reduce", splitk_sum_kernel<<<rg, 256, 0, c->stream>>>(part, r, n, nz, alpha, Cm, ldc);)
+    SLRA_CHECK_LAUNCH(c);
+  }
+  return SLRA_OK;
+}
+
+}  // namespace slra_dev
