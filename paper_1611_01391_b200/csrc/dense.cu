@@ -113,37 +113,55 @@ __global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restri
   for (int j = threadIdx.x; j < c; j += kDT) tau[j] = taust[pb * (nblk * c) + b * c + j];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j = warp; j < c; j += kDT / 32) {
-    double y[RPL];
+  constexpr int NW = kDT / 32;
+  constexpr int CPW = (64 + NW - 1) / NW;  // c <= 64: every column of this warp at once
+  double y[CPW][RPL];
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int j = warp + q * NW;
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const int i = lane + 32 * r;
-      y[r] = i < c ? Qp[(b * c + i) + (int64_t)j * ldqp] : 0.0;
+      y[q][r] = (j < c && i < c) ? Qp[(b * c + i) + (int64_t)j * ldqp] : 0.0;
     }
+  }
+  if (warp < c) {
     for (int k = c - 1; k >= 0; --k) {
       const double t = tau[k];
       if (t == 0.0) continue;
       const double* v = V + (size_t)k * Lp;
-      double w = 0.0, yk = 0.0;
+      double vr[RPL];
 #pragma unroll
       for (int r = 0; r < RPL; ++r) {
         const int i = lane + 32 * r;
-        if (i > k && i < Lp) w = fma(v[i], y[r], w);
-        if (i == k) yk = y[r];
+        vr[r] = (i > k && i < Lp) ? v[i] : (i == k ? 1.0 : 0.0);  // implicit unit head
       }
-      w = warp_sum(w);
-      w += __shfl_sync(0xffffffffu, yk, k & 31);
+      double w[CPW];
 #pragma unroll
-      for (int r = 0; r < RPL; ++r) {
-        const int i = lane + 32 * r;
-        if (i > k && i < Lp) y[r] -= t * v[i] * w;
-        if (i == k) y[r] -= t * w;
+      for (int q = 0; q < CPW; ++q) {
+        w[q] = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) w[q] = fma(vr[r], y[q][r], w[q]);
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) w[q] += __shfl_xor_sync(0xffffffffu, w[q], o);
+#pragma unroll
+      for (int q = 0; q < CPW; ++q)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) y[q][r] -= t * vr[r] * w[q];
     }
+  }
 #pragma unroll
-    for (int r = 0; r < RPL; ++r) {
-      const int i = lane + 32 * r;
-      if (i < nr) Qo[(r0 + i) + (int64_t)j * ldqo] = y[r];
+  for (int q = 0; q < CPW; ++q) {
+    const int j = warp + q * NW;
+    if (j < c) {
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i < nr) Qo[(r0 + i) + (int64_t)j * ldqo] = y[q][r];
+      }
     }
   }
 }
@@ -152,7 +170,7 @@ static size_t qr_cta_smem(int m, int c) { return sizeof(double) * ((size_t)m * c
 
 // Workspace doubles needed by launch_thin_qr_batched for one problem.
 size_t tsqr_workspace_doubles(int64_t m, int c) {
-  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 512) return 0;
+  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 256) return 0;
   const int Lp = kLeaf > c ? kLeaf : c;
   size_t total = 0;
   int64_t rows = m, first_upper = -1;
@@ -170,7 +188,7 @@ size_t tsqr_workspace_doubles(int64_t m, int c) {
 // be null -> context workspace) holds nb * tsqr_workspace_doubles(m, c).
 int launch_thin_qr_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int64_t m, int c, double* Q,
                            int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws) {
-  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 512) {
+  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 256) {
     const size_t smem = qr_cta_smem((int)m, c);
     SLRA_CUDA(cudaFuncSetAttribute(thin_qr_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SLRA_TIMED(cx, "thin_qr", thin_qr_cta_kernel<<<nb, kDT, smem, cx->stream>>>(A, lda, sA, (int)m, c, Q, ldq, sQ, R,
@@ -516,7 +534,7 @@ static size_t maxvol_smem(int m, int r, int count) {
 int launch_maxvol(Context* cx, const double* A, int64_t lda, int64_t m, int64_t r, double h, int64_t max_swaps,
                   int qr_first, int64_t count, int64_t* idx, double* vol) {
   const size_t smem = maxvol_smem((int)m, (int)r, (int)count);
-  if (smem > 220 * 1024 || r > 64 || (qr_first && m > 512)) return SLRA_ERR_UNSUPPORTED;
+  if (smem > 220 * 1024 || r > 64 || (qr_first && m > 256)) return SLRA_ERR_UNSUPPORTED;
   SLRA_CUDA(cudaFuncSetAttribute(maxvol_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
   SLRA_TIMED(cx, "maxvol",

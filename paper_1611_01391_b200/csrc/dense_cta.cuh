@@ -76,48 +76,69 @@ __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, do
     __syncthreads();
     const double t = tau[j];
     const bool apply = (m - j > 1) && t != 0.0;  // rows()==1 or tau==0: identity
-    int k = j + 1 + ((warp - (j + 1) % NW + NW) % NW);
-    for (; k < c; k += NW) {
-      double* a = A + k * lda;
-      if (apply) {
-        double w = 0.0;
-        double xr[RPL], ar[RPL];
+    // this warp's columns right of j: k0, k0 + NW, ... — processed together
+    // (one read of the reflector, interleaved butterflies)
+    const int k0 = j + 1 + ((warp - (j + 1) % NW + NW) % NW);
+    constexpr int CPW = (64 + NW - 1) / NW;  // c <= 64
+    if (apply) {
+      double xr[RPL];
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          const int i = lane + 32 * r;
-          const bool in = i > j && i < m;
-          xr[r] = in ? x[i] : 0.0;
-          ar[r] = in ? a[i] : 0.0;
-          w += xr[r] * ar[r];
-        }
-        w = warp_sum(w);
-        w += a[j];
-        __syncwarp();
-        if (lane == 0) a[j] -= t * w;
-        double s = 0.0;
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        xr[r] = (i > j && i < m) ? x[i] : 0.0;
+      }
+      double w[CPW];
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          const int i = lane + 32 * r;
-          if (i > j && i < m) {
-            const double v = ar[r] - t * xr[r] * w;
-            a[i] = v;
-            if (i > j + 1) s += v * v;
+      for (int q = 0; q < CPW; ++q) {
+        const int k = k0 + q * NW;
+        w[q] = 0.0;
+        if (k < c) {
+          const double* a = A + k * lda;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = lane + 32 * r;
+            if (i < m) w[q] = fma(xr[r], a[i], w[q]);
           }
         }
-        if (k == j + 1) {
-          s = warp_sum(s);
-          if (lane == 0) tn[k] = s;
-        }
-      } else if (k == j + 1) {
-        double s = 0.0;
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          const int i = lane + 32 * r;
-          if (i > k && i < m) s += a[i] * a[i];
-        }
-        s = warp_sum(s);
-        if (lane == 0) tn[k] = s;
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) w[q] += __shfl_xor_sync(0xffffffffu, w[q], o);
+#pragma unroll
+      for (int q = 0; q < CPW; ++q) {
+        const int k = k0 + q * NW;
+        if (k < c) {
+          double* a = A + k * lda;
+          const double wq = w[q] + a[j];
+          __syncwarp();
+          if (lane == 0) a[j] -= t * wq;
+          double s = 0.0;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = lane + 32 * r;
+            if (i > j && i < m) {
+              const double v = a[i] - t * xr[r] * wq;
+              a[i] = v;
+              if (i > j + 1) s = fma(v, v, s);
+            }
+          }
+          if (k == j + 1) {
+            s = warp_sum(s);
+            if (lane == 0) tn[k] = s;
+          }
+        }
+      }
+    } else if (k0 == j + 1 && k0 < c) {
+      const double* a = A + k0 * lda;
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i > k0 && i < m) s = fma(a[i], a[i], s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) tn[k0] = s;
     }
     __syncthreads();
   }
@@ -138,34 +159,57 @@ template <int NT, int RPL>
 __device__ void cta_form_q_regs(const double* V, int ldv, int m, int c, const double* tau, double* Q, int ldq) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = NT / 32;
-  for (int j = warp; j < c; j += NW) {
-    double y[RPL];
+  constexpr int CPW = (64 + NW - 1) / NW;  // c <= 64
+  // all columns of this warp travel together: one read of each reflector,
+  // interleaved butterflies
+  double y[CPW][RPL];
+  int jmax = -1;
 #pragma unroll
-    for (int r = 0; r < RPL; ++r) y[r] = (lane + 32 * r == j) ? 1.0 : 0.0;
-    for (int k = j; k >= 0; --k) {
-      const double t = tau[k];
-      if (t == 0.0) continue;
-      const double* v = V + k * ldv;
-      double w = 0.0, yk = 0.0;
+  for (int q = 0; q < CPW; ++q) {
+    const int j = warp + q * NW;
 #pragma unroll
-      for (int r = 0; r < RPL; ++r) {
-        const int i = lane + 32 * r;
-        if (i > k && i < m) w += v[i] * y[r];
-        if (i == k) yk = y[r];
-      }
-      w = warp_sum(w);
-      w += __shfl_sync(0xffffffffu, yk, k & 31);
-#pragma unroll
-      for (int r = 0; r < RPL; ++r) {
-        const int i = lane + 32 * r;
-        if (i > k && i < m) y[r] -= t * v[i] * w;
-        if (i == k) y[r] -= t * w;
-      }
-    }
+    for (int r = 0; r < RPL; ++r) y[q][r] = (j < c && lane + 32 * r == j) ? 1.0 : 0.0;
+    if (j < c) jmax = j;
+  }
+  for (int k = jmax; k >= 0; --k) {
+    const double t = tau[k];
+    if (t == 0.0) continue;
+    const double* v = V + k * ldv;
+    double vr[RPL];
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const int i = lane + 32 * r;
-      if (i < m) Q[i + (int64_t)j * ldq] = y[r];
+      vr[r] = (i > k && i < m) ? v[i] : (i == k ? 1.0 : 0.0);  // implicit unit head
+    }
+    double w[CPW];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      w[q] = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) w[q] = fma(vr[r], y[q][r], w[q]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < CPW; ++q) w[q] += __shfl_xor_sync(0xffffffffu, w[q], o);
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      const int j = warp + q * NW;
+      if (j >= k && j < c) {  // H_k leaves e_j (j < k) untouched
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) y[q][r] -= t * vr[r] * w[q];
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int j = warp + q * NW;
+    if (j < c) {
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i < m) Q[i + (int64_t)j * ldq] = y[q][r];
+      }
     }
   }
 }
@@ -174,8 +218,7 @@ template <int NT>
 __device__ void cta_form_q(const double* V, int ldv, int m, int c, const double* tau, double* Q, int ldq) {
   if (m <= 64) cta_form_q_regs<NT, 2>(V, ldv, m, c, tau, Q, ldq);
   else if (m <= 256) cta_form_q_regs<NT, 8>(V, ldv, m, c, tau, Q, ldq);
-  else if (m <= 512) cta_form_q_regs<NT, 16>(V, ldv, m, c, tau, Q, ldq);
-  else cta_form_q_regs<NT, 16>(V, ldv, m, c, tau, Q, ldq);  // m <= 512 (callers enforce)
+  else cta_form_q_regs<NT, 8>(V, ldv, m, c, tau, Q, ldq);  // m <= 256 (callers enforce)
 }
 
 // thin_qr (linalg.cpp:67-79): A (m x c, m >= c, m <= 1024) in smem is
