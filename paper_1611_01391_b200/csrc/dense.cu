@@ -16,7 +16,7 @@ namespace slra_dev {
 
 constexpr int kDT = 512;
 constexpr int kLeaf = 256;  // TSQR leaf rows
-constexpr int kSVT = 1024;  // threads of the one-CTA SVD (one warp per Jacobi pair)
+constexpr int kSVT = 256;   // threads of the one-CTA SVD (8-lane group per Jacobi pair)
 
 // ---------------------------------------------------------------- single-CTA thin QR
 __global__ void __launch_bounds__(kDT) thin_qr_cta_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
@@ -125,10 +125,9 @@ __global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restri
       y[q][r] = (j < c && i < c) ? Qp[(b * c + i) + (int64_t)j * ldqp] : 0.0;
     }
   }
-  if (warp < c) {
+  {  // uniform control flow around the shuffles; tau = 0 is an exact no-op
     for (int k = c - 1; k >= 0; --k) {
       const double t = tau[k];
-      if (t == 0.0) continue;
       const double* v = V + (size_t)k * Lp;
       double vr[RPL];
 #pragma unroll

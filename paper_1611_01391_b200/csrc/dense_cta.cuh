@@ -74,72 +74,59 @@ __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, do
       }
     }
     __syncthreads();
+    // tau = 0 (identity reflector, incl. the rows()==1 case) leaves every
+    // column unchanged through the same arithmetic, so the code below has no
+    // data-dependent branches around its shuffles (those would be compiled
+    // as divergence-safe "collective" sequences, several times slower).
     const double t = tau[j];
-    const bool apply = (m - j > 1) && t != 0.0;  // rows()==1 or tau==0: identity
     // this warp's columns right of j: k0, k0 + NW, ... — processed together
     // (one read of the reflector, interleaved butterflies)
     const int k0 = j + 1 + ((warp - (j + 1) % NW + NW) % NW);
     constexpr int CPW = (64 + NW - 1) / NW;  // c <= 64
-    if (apply) {
-      double xr[RPL];
+    double xr[RPL];
 #pragma unroll
-      for (int r = 0; r < RPL; ++r) {
-        const int i = lane + 32 * r;
-        xr[r] = (i > j && i < m) ? x[i] : 0.0;
-      }
-      double w[CPW];
-#pragma unroll
-      for (int q = 0; q < CPW; ++q) {
-        const int k = k0 + q * NW;
-        w[q] = 0.0;
-        if (k < c) {
-          const double* a = A + k * lda;
-#pragma unroll
-          for (int r = 0; r < RPL; ++r) {
-            const int i = lane + 32 * r;
-            if (i < m) w[q] = fma(xr[r], a[i], w[q]);
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int q = 0; q < CPW; ++q) w[q] += __shfl_xor_sync(0xffffffffu, w[q], o);
-#pragma unroll
-      for (int q = 0; q < CPW; ++q) {
-        const int k = k0 + q * NW;
-        if (k < c) {
-          double* a = A + k * lda;
-          const double wq = w[q] + a[j];
-          __syncwarp();
-          if (lane == 0) a[j] -= t * wq;
-          double s = 0.0;
-#pragma unroll
-          for (int r = 0; r < RPL; ++r) {
-            const int i = lane + 32 * r;
-            if (i > j && i < m) {
-              const double v = a[i] - t * xr[r] * wq;
-              a[i] = v;
-              if (i > j + 1) s = fma(v, v, s);
-            }
-          }
-          if (k == j + 1) {
-            s = warp_sum(s);
-            if (lane == 0) tn[k] = s;
-          }
-        }
-      }
-    } else if (k0 == j + 1 && k0 < c) {
-      const double* a = A + k0 * lda;
-      double s = 0.0;
-#pragma unroll
-      for (int r = 0; r < RPL; ++r) {
-        const int i = lane + 32 * r;
-        if (i > k0 && i < m) s = fma(a[i], a[i], s);
-      }
-      s = warp_sum(s);
-      if (lane == 0) tn[k0] = s;
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      xr[r] = (i > j && i < m) ? x[i] : 0.0;
     }
+    double w[CPW], aj[CPW];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      const int k = k0 + q * NW;
+      const double* a = A + (k < c ? k : c - 1) * lda;  // always a valid column
+      w[q] = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i < m) w[q] = fma(xr[r], a[i], w[q]);
+      }
+      aj[q] = a[j];  // head, read before anyone writes it
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < CPW; ++q) w[q] += __shfl_xor_sync(0xffffffffu, w[q], o);
+    double s = 0.0;  // next tail norm of column j+1 (owner warp, slot q = 0)
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      const int k = k0 + q * NW;
+      if (k < c) {
+        double* a = A + k * lda;
+        const double wq = w[q] + aj[q];
+        if (lane == 0) a[j] = aj[q] - t * wq;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          if (i > j && i < m) {
+            const double v = a[i] - t * xr[r] * wq;
+            a[i] = v;
+            if (q == 0 && i > j + 1) s = fma(v, v, s);
+          }
+        }
+      }
+    }
+    s = warp_sum(s);
+    if (lane == 0 && k0 == j + 1 && k0 < c) tn[k0] = s;
     __syncthreads();
   }
 }
@@ -163,17 +150,16 @@ __device__ void cta_form_q_regs(const double* V, int ldv, int m, int c, const do
   // all columns of this warp travel together: one read of each reflector,
   // interleaved butterflies
   double y[CPW][RPL];
-  int jmax = -1;
 #pragma unroll
   for (int q = 0; q < CPW; ++q) {
     const int j = warp + q * NW;
 #pragma unroll
     for (int r = 0; r < RPL; ++r) y[q][r] = (j < c && lane + 32 * r == j) ? 1.0 : 0.0;
-    if (j < c) jmax = j;
   }
-  for (int k = jmax; k >= 0; --k) {
+  // uniform trip count and no data-dependent skips around the shuffles
+  // (tau = 0 is an exact no-op through the arithmetic)
+  for (int k = c - 1; k >= 0; --k) {
     const double t = tau[k];
-    if (t == 0.0) continue;
     const double* v = V + k * ldv;
     double vr[RPL];
 #pragma unroll
@@ -601,11 +587,14 @@ __device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ld
       __syncthreads();
       thr2 = deflate * deflate * dmax2;
     }
+    const int npairs = ne / 2;
+    const int iters = (npairs + NW - 1) / NW;  // uniform trip count for every warp
     for (int rd = 0; rd < ne - 1; ++rd) {
-      for (int pi = warp; pi < ne / 2; pi += NW) {
-        const int ab = pair_tab[rd * (ne / 2) + pi];
-        const int a = ab >> 8, b = ab & 255;
-        if (b >= n) continue;
+      for (int it = 0; it < iters; ++it) {
+        const int pi = warp + it * NW;
+        const int ab = pair_tab[rd * npairs + (pi < npairs ? pi : 0)];
+        const bool valid = pi < npairs && (ab & 255) < n;
+        const int a = ab >> 8, b = valid ? (ab & 255) : a;
         double* wp = W + a * ldw;
         double* wq = W + b * ldw;
         double x[RPL], y[RPL];
@@ -619,8 +608,11 @@ __device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ld
           bb = fma(y[r], y[r], bb);
           gg = fma(x[r], y[r], gg);
         }
+        // three interleaved butterflies, in uniform control flow (a branch
+        // on shared data before them makes nvcc emit divergence-safe
+        // collective shuffles, several times slower)
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {  // three interleaved butterflies
+        for (int o = 16; o > 0; o >>= 1) {
           aa += __shfl_xor_sync(0xffffffffu, aa, o);
           bb += __shfl_xor_sync(0xffffffffu, bb, o);
           gg += __shfl_xor_sync(0xffffffffu, gg, o);
@@ -628,7 +620,7 @@ __device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ld
         // convergence test of LAPACK dgesvj: |<w_p, w_q>| <= sqrt(p) eps ||w_p|| ||w_q||
         // (a bare eps threshold never settles once the dot products are
         // evaluated in a different order than the rotation was computed)
-        if (gg == 0.0 || fabs(gg) <= tol * sqrt(aa * bb)) continue;
+        if (!valid || gg == 0.0 || fabs(gg) <= tol * sqrt(aa * bb)) continue;
         if (aa < thr2 && bb < thr2) continue;
         const double zeta = (bb - aa) * __drcp_rn(2.0 * gg);
         const double t = copysign(__drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
@@ -664,9 +656,119 @@ __device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ld
   }
 }
 
+// The same sweeps for p, n <= 64 with an 8-lane group per column pair (4 pairs
+// per warp): a pair's dot products reduce in 3 shuffle levels instead of 5
+// and one warp-instruction advances 4 pairs, which cuts the instruction count
+// per round ~4x — the round is instruction-throughput bound on FP64.
+template <int NT>
+__device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate) {
+  constexpr int RPG = 8;  // rows per lane: p <= 64, n <= 64
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = lane >> 3, sub = lane & 7;
+  constexpr int NW = NT / 32;
+  __shared__ unsigned short pair_tab[64 * 32];
+  __shared__ double dmax2;
+  for (int e = tid; e < n * n; e += NT) V[e % n + (e / n) * ldv] = (e % n == e / n) ? 1.0 : 0.0;
+  const int ne = n + (n & 1);
+  for (int e = tid; e < (ne - 1) * (ne / 2); e += NT) {
+    const int rd = e / (ne / 2), pi = e % (ne / 2);
+    int a, b;
+    if (pi == 0) {
+      a = rd;
+      b = ne - 1;
+    } else {
+      a = (rd + pi) % (ne - 1);
+      b = (rd - pi + ne - 1) % (ne - 1);
+    }
+    if (a > b) { const int t = a; a = b; b = t; }
+    pair_tab[e] = (unsigned short)((a << 8) | b);
+  }
+  const double tol = sqrt((double)p) * kEps;
+  if (tid == 0) flag[0] = flag[1] = 0;
+  __syncthreads();
+  const int npairs = ne / 2;
+  const int iters = (npairs + 4 * NW - 1) / (4 * NW);
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    const int fl = sweep & 1;
+    double thr2 = 0.0;
+    if (deflate > 0.0) {
+      if (warp == 0) {
+        double mx = 0.0;
+        for (int j = 0; j < n; ++j) {
+          double s = 0.0;
+          for (int i = lane; i < p; i += 32) s = fma(W[i + j * ldw], W[i + j * ldw], s);
+          s = warp_sum(s);
+          mx = fmax(mx, s);
+        }
+        if (lane == 0) dmax2 = mx;
+      }
+      __syncthreads();
+      thr2 = deflate * deflate * dmax2;
+    }
+    for (int rd = 0; rd < ne - 1; ++rd) {
+      for (int it = 0; it < iters; ++it) {
+        const int pi = (warp + it * NW) * 4 + grp;
+        const int ab = pair_tab[rd * npairs + (pi < npairs ? pi : 0)];
+        const bool valid = pi < npairs && (ab & 255) < n;
+        const int a = ab >> 8, b = valid ? (ab & 255) : a;
+        double* wp = W + a * ldw;
+        double* wq = W + b * ldw;
+        double x[RPG], y[RPG];
+        double aa = 0.0, bb = 0.0, gg = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPG; ++r) {
+          const int i = sub + 8 * r;
+          x[r] = i < p ? wp[i] : 0.0;
+          y[r] = i < p ? wq[i] : 0.0;
+          aa = fma(x[r], x[r], aa);
+          bb = fma(y[r], y[r], bb);
+          gg = fma(x[r], y[r], gg);
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {  // within the 8-lane group
+          aa += __shfl_xor_sync(0xffffffffu, aa, o);
+          bb += __shfl_xor_sync(0xffffffffu, bb, o);
+          gg += __shfl_xor_sync(0xffffffffu, gg, o);
+        }
+        if (!valid || gg == 0.0 || fabs(gg) <= tol * sqrt(aa * bb)) continue;
+        if (aa < thr2 && bb < thr2) continue;
+        const double zeta = (bb - aa) * __drcp_rn(2.0 * gg);
+        const double t = copysign(__drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+        const double cs = rsqrt(fma(t, t, 1.0));
+        const double sn = cs * t;
+#pragma unroll
+        for (int r = 0; r < RPG; ++r) {
+          const int i = sub + 8 * r;
+          if (i < p) {
+            wp[i] = cs * x[r] - sn * y[r];
+            wq[i] = sn * x[r] + cs * y[r];
+          }
+        }
+        double* vp = V + a * ldv;
+        double* vq = V + b * ldv;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int i = sub + 8 * r;
+          if (i < n) {
+            const double u = vp[i], v = vq[i];
+            vp[i] = cs * u - sn * v;
+            vq[i] = sn * u + cs * v;
+          }
+        }
+        if (sub == 0) flag[fl] = 1;
+      }
+      __syncthreads();
+    }
+    const int rotated = flag[fl];
+    if (tid == 0) flag[fl ^ 1] = 0;
+    __syncthreads();
+    if (!rotated) break;
+  }
+}
+
 template <int NT>
 __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate = 0.0) {
-  if (p <= 64) cta_jacobi_t<NT, 2>(W, ldw, p, n, V, ldv, flag, deflate);
+  if (p <= 64) cta_jacobi_g8<NT>(W, ldw, p, n, V, ldv, flag, deflate);
   else cta_jacobi_t<NT, 8>(W, ldw, p, n, V, ldv, flag, deflate);  // p <= 256 (callers enforce)
 }
 
