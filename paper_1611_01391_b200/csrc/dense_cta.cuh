@@ -563,7 +563,11 @@ __device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ld
     if (a > b) { const int t = a; a = b; b = t; }
     pair_tab[e] = (unsigned short)((a << 8) | b);
   }
-  const double tol = sqrt((double)p) * kEps;
+  // orthogonality threshold: dgesvj's sqrt(p)*eps sits below the rounding
+  // floor of the rotated columns (measured ~p*eps here: the sweeps never
+  // stop); 16*p*eps keeps sigma accurate to O(tol^2) relative and the
+  // vectors to O(tol / gap)
+  const double tol = 16.0 * (double)p * kEps;
   if (tid == 0) flag[0] = flag[1] = 0;
   __syncthreads();
   for (int sweep = 0; sweep < 40; ++sweep) {
@@ -683,7 +687,11 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
     if (a > b) { const int t = a; a = b; b = t; }
     pair_tab[e] = (unsigned short)((a << 8) | b);
   }
-  const double tol = sqrt((double)p) * kEps;
+  // orthogonality threshold: dgesvj's sqrt(p)*eps sits below the rounding
+  // floor of the rotated columns (measured ~p*eps here: the sweeps never
+  // stop); 16*p*eps keeps sigma accurate to O(tol^2) relative and the
+  // vectors to O(tol / gap)
+  const double tol = 16.0 * (double)p * kEps;
   if (tid == 0) flag[0] = flag[1] = 0;
   __syncthreads();
   const int npairs = ne / 2;
@@ -760,7 +768,10 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
       __syncthreads();
     }
     const int rotated = flag[fl];
-    if (tid == 0) flag[fl ^ 1] = 0;
+    if (tid == 0) {
+      flag[fl ^ 1] = 0;
+      flag[2] = sweep + 1;  // sweeps used (diagnostics)
+    }
     __syncthreads();
     if (!rotated) break;
   }
