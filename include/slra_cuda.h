@@ -11,7 +11,7 @@
  *
  * Each entry point replaces one reference interface on the hot path
  * (SURVEY.md §8a); the reference file:line is cited per function. The C++
- * host layer (paper_1611_01391_b200/include/slra/*.hpp) keeps the reference
+ * host layer (the headers under paper_1611_01391_b200/include/slra) keeps the reference
  * signatures and calls these; INTEGRATION.md shows the reference-side
  * dispatch a maintainer would add. There is no CPU fallback: without a CUDA
  * device every call returns SLRA_ERR_NO_DEVICE.
@@ -134,8 +134,10 @@ int slra_primitive_cur(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, 
 /* cross_approx (cur.cpp:201-255), stop_tol unset. init_rows (k indices)
  * must be given (the host draws them with Rng::distinct_indices exactly as
  * cur.cpp:207-209). Outputs: I (k), J (l), nucleus (l x k), the trace
- * (2*loops steps: rows k, cols l, volume proxy), adaptive r. Blocks until
- * done (status is host-visible). */
+ * (2*loops steps: rows k, cols l, volume proxy), adaptive r. k, l <= 64.
+ * Strips that fit one SM run the whole loop in one CTA-resident kernel;
+ * taller ones (config 3) use TSQR + the grid-wide cooperative maxvol per
+ * half-sweep (k == l there). Blocks until done (status is host-visible). */
 int slra_cross_approx(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
                       int64_t r, int64_t k, int64_t l, const int64_t* d_init_rows, int loops,
                       double h, int64_t* d_I, int64_t* d_J, double* d_nucleus,
@@ -166,6 +168,13 @@ int slra_cur_residual(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, i
                       const int64_t* d_I, int64_t k, const int64_t* d_J, int64_t l,
                       const double* d_nucleus, int64_t ldu, double* h_resid_sq,
                       double* h_norm_sq);
+/* The same residual with the nucleus in its factored form U = Tsig Sr^T
+ * (Tsig l x r, Sr k x r, as returned by slra_primitive_cur): the pass over A
+ * runs at inner dimension r instead of k. d_out[0..1] = resid_sq, norm_sq. */
+int slra_cur_residual_factored(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                               const int64_t* d_I, int64_t k, const int64_t* d_J, int64_t l,
+                               const double* d_Tsig, const double* d_Sr, int64_t r,
+                               double* d_out);
 
 /* ------------------------------------------------------------ GEMM
  * C = alpha op(A) op(B) + beta C, FP64 DMMA (mma.sync m8n8k4). trans = 0/1. */

@@ -34,9 +34,9 @@ struct Context {
   // pinned host mirror of dsmall for status read-back
   void* hsmall = nullptr;
   // independent growable device arenas for multi-kernel orchestrations
-  // (slot 0: range finder, 1: cur residual, 2: lsr, 3: spare)
-  void* arena[4] = {nullptr, nullptr, nullptr, nullptr};
-  size_t arena_bytes[4] = {0, 0, 0, 0};
+  // (0: range finder, 1: cur residual, 2: lsr, 3: svd/transpose, 4: large C-A, 5: factored residual)
+  void* arena[8] = {};
+  size_t arena_bytes[8] = {};
   // opt-in per-kernel-family timing (CUDA events on the context stream)
   bool timing = false;
   struct Rec {

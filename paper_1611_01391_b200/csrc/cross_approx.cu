@@ -32,6 +32,8 @@ struct CaParams {
   double* Q;                 // nprob x (rq * n), ld rq
   int rq;                    // min(k, l)
   int mode;                  // 0 = cross_approx, 1 = primitive_cur only (I,J given in I_out/J_out)
+  double* Tsig_out = nullptr;  // problem 0: T_r Sigma_r^-1 (l x r, ld l), nullable
+  double* Sr_out = nullptr;    // problem 0: S_r (k x r, ld k), nullable
 };
 
 struct CaSmem {
@@ -263,6 +265,10 @@ __global__ void __launch_bounds__(kCT) ca_block_kernel(CaParams P) {
     }
     return;
   }
+  if (b == 0 && P.Tsig_out) {
+    for (int e = tid; e < P.l * r; e += kCT) P.Tsig_out[e] = s.Tm[e];
+    for (int e = tid; e < P.k * r; e += kCT) P.Sr_out[e] = s.Sm[e];
+  }
   // nucleus U = Tm Sm^T (l x k)
   double* U = P.nucleus + (int64_t)b * P.l * P.k;
   for (int e = tid; e < P.l * P.k; e += kCT) {
@@ -298,6 +304,17 @@ int launch_lowrank_residual_batched(Context* c, const double* A, int64_t lda, in
                                     const double* P, int64_t ldp, int64_t sP, const double* Q, int64_t ldq,
                                     int64_t sQ, int64_t inner, int64_t nprob, double* d_out_pairs);
 
+int launch_gather_rows_t(Context* c, const double* A, int64_t lda, int64_t n, const int64_t* I, int64_t k,
+                         double* RT, int64_t ldrt);
+int launch_gather_cols(Context* c, const double* A, int64_t lda, int64_t m, const int64_t* J, int64_t l, double* Cm,
+                       int64_t ldc);
+size_t tsqr_workspace_doubles(int64_t m, int c);
+int launch_thin_qr_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int64_t m, int c, double* Q,
+                           int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws);
+size_t maxvol_large_scratch_doubles(int num_sms, int64_t m);
+int launch_maxvol_large(Context* cx, const double* Q, int64_t ldq, int64_t m, int r, double h, int max_swaps,
+                        int64_t* d_idx, double* d_vol, double* scratch);
+
 static bool ca_fits(int m, int n, int k, int l) {
   return k >= 1 && l >= 1 && k <= 64 && l <= 64 && k <= m && l <= n &&
          ca_smem_bytes(m, n, k, l) <= 227 * 1024;
@@ -317,13 +334,73 @@ using namespace slra_dev;
 
 extern "C" {
 
+int slra_primitive_cur(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, const int64_t* I, int64_t k,
+                       const int64_t* J, int64_t l, int64_t r, double* nucleus, int64_t ldu, double* Tsig,
+                       double* Sr, int64_t* h_r_out);
+
 int slra_cross_approx(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, int64_t r, int64_t k,
                       int64_t l, const int64_t* init_rows, int loops, double h, int64_t* I_out, int64_t* J_out,
                       double* nucleus, int64_t* trace_rows, int64_t* trace_cols, double* trace_vol,
                       int64_t* h_r_out) {
   if (!ctx || lda < m || loops < 1 || k < 1 || l < 1 || (r > 0 && (k < r || l < r)) || k > m || l > n)
     return SLRA_ERR_INVALID_ARGUMENT;
-  if (!ca_fits((int)m, (int)n, (int)k, (int)l)) return SLRA_ERR_UNSUPPORTED;
+  if (!ca_fits((int)m, (int)n, (int)k, (int)l)) {
+    if (k > 64 || l > 64) return SLRA_ERR_UNSUPPORTED;
+    // strips too tall for one SM (config 3): per half-sweep a gather, a
+    // batched TSQR and the grid-wide maxvol, orchestrated from the host with
+    // every index set kept on the device.
+    Context* cx = C(ctx);
+    const int64_t c = k > l ? k : l, mm = m > n ? m : n;
+    const size_t tw = tsqr_workspace_doubles(mm, (int)c);
+    const size_t mvs = maxvol_large_scratch_doubles(cx->num_sms, mm);
+    const size_t need = 2 * (size_t)mm * c + (size_t)c * c + tw + mvs + 2 * (size_t)c + 64;
+    double* buf = static_cast<double*>(arena(cx, 4, sizeof(double) * need));
+    if (!buf) return SLRA_ERR_CUDA;
+    double* S = buf;                      // strip (len x nidx)
+    double* Q = S + (size_t)mm * c;       // its orthonormal basis
+    double* R = Q + (size_t)mm * c;       // c x c
+    double* tws = R + (size_t)c * c;
+    double* mvw = tws + tw;
+    int64_t* dI = reinterpret_cast<int64_t*>(mvw + mvs);  // k
+    int64_t* dJ = dI + c;                                  // l
+    SLRA_CUDA(cudaMemcpyAsync(dI, init_rows, 8 * k, cudaMemcpyDeviceToDevice, cx->stream));
+    for (int loop = 0; loop < loops; ++loop) {
+      // vertical: J = select_rows_spanning(A(I,:)^T, l)
+      SLRA_TRY(launch_gather_rows_t(cx, A, lda, n, dI, k, S, n));
+      SLRA_TRY(launch_thin_qr_batched(cx, S, n, 0, n, (int)k, Q, n, 0, R, k, 0, 1, tw ? tws : nullptr));
+      if (l > k) return SLRA_ERR_UNSUPPORTED;  // padding (cur.cpp:125-134) not on the large path
+      SLRA_TRY(launch_maxvol_large(cx, Q, n, n, (int)l, h, 4 * (int)l, dJ,
+                                   trace_vol ? trace_vol + 2 * loop : nullptr, mvw));
+      {
+        int32_t st = 0;  // SelectionFailure is reported through dsmall
+        SLRA_CUDA(cudaMemcpyAsync(&st, cx->dsmall, 4, cudaMemcpyDeviceToHost, cx->stream));
+        SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+        if (st != SLRA_OK) return st;
+      }
+      if (trace_rows) {
+        SLRA_CUDA(cudaMemcpyAsync(trace_rows + (2 * loop) * k, dI, 8 * k, cudaMemcpyDeviceToDevice, cx->stream));
+        SLRA_CUDA(cudaMemcpyAsync(trace_cols + (2 * loop) * l, dJ, 8 * l, cudaMemcpyDeviceToDevice, cx->stream));
+      }
+      // horizontal: I = select_rows_spanning(A(:,J), k)
+      SLRA_TRY(launch_gather_cols(cx, A, lda, m, dJ, l, S, m));
+      SLRA_TRY(launch_thin_qr_batched(cx, S, m, 0, m, (int)l, Q, m, 0, R, l, 0, 1, tw ? tws : nullptr));
+      if (k > l) return SLRA_ERR_UNSUPPORTED;
+      SLRA_TRY(launch_maxvol_large(cx, Q, m, m, (int)k, h, 4 * (int)k, dI,
+                                   trace_vol ? trace_vol + 2 * loop + 1 : nullptr, mvw));
+      if (trace_rows) {
+        SLRA_CUDA(cudaMemcpyAsync(trace_rows + (2 * loop + 1) * k, dI, 8 * k, cudaMemcpyDeviceToDevice, cx->stream));
+        SLRA_CUDA(cudaMemcpyAsync(trace_cols + (2 * loop + 1) * l, dJ, 8 * l, cudaMemcpyDeviceToDevice, cx->stream));
+      }
+      // the grid-wide maxvol reports SelectionFailure through dsmall
+      int32_t st = 0;
+      SLRA_CUDA(cudaMemcpyAsync(&st, cx->dsmall, 4, cudaMemcpyDeviceToHost, cx->stream));
+      SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+      if (st != SLRA_OK) return st;
+    }
+    SLRA_CUDA(cudaMemcpyAsync(I_out, dI, 8 * k, cudaMemcpyDeviceToDevice, cx->stream));
+    SLRA_CUDA(cudaMemcpyAsync(J_out, dJ, 8 * l, cudaMemcpyDeviceToDevice, cx->stream));
+    return slra_primitive_cur(ctx, A, lda, m, n, I_out, k, J_out, l, r, nucleus, l, nullptr, nullptr, h_r_out);
+  }
   Context* cx = C(ctx);
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
   int64_t* d_r = reinterpret_cast<int64_t*>(static_cast<char*>(cx->dsmall) + 64);
@@ -371,8 +448,6 @@ int slra_primitive_cur(slra_ctx ctx, const double* A, int64_t lda, int64_t m, in
   if (!ctx || lda < m || k < 1 || l < 1 || ldu != l || (r > 0 && (k < r || l < r)))
     return SLRA_ERR_INVALID_ARGUMENT;
   if (k > 64 || l > 64) return SLRA_ERR_UNSUPPORTED;
-  (void)Tsig;
-  (void)Sr;
   Context* cx = C(ctx);
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
   int64_t* d_r = reinterpret_cast<int64_t*>(static_cast<char*>(cx->dsmall) + 64);
@@ -383,7 +458,7 @@ int slra_primitive_cur(slra_ctx ctx, const double* A, int64_t lda, int64_t m, in
   SLRA_CUDA(cudaMemcpyAsync(dJ, J, 8 * l, cudaMemcpyDeviceToDevice, cx->stream));
   const int mm = (int)(k > l ? k : l);
   CaParams p{A, lda, 0, mm, mm, (int)r, (int)k, (int)l, 1, 1.1, nullptr, dI, dJ, nucleus, d_r, d_status,
-             nullptr, nullptr, nullptr, nullptr, nullptr, (int)(k < l ? k : l), 1};
+             nullptr, nullptr, nullptr, nullptr, nullptr, (int)(k < l ? k : l), 1, Tsig, Sr};
   SLRA_TRY(launch_ca_block(cx, p, 1));
   char* hs = static_cast<char*>(cx->hsmall);
   SLRA_CUDA(cudaMemcpyAsync(hs, cx->dsmall, 128, cudaMemcpyDeviceToHost, cx->stream));

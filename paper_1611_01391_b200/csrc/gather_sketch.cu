@@ -46,6 +46,19 @@ __global__ void __launch_bounds__(kNT) gather_rows_kernel(const double* __restri
   }
 }
 
+// RT(j, t) = A(I[t], j): the row strip of the C-A sweep (cur.cpp:215-217)
+// written straight as the n x k tall matrix R^T that select_rows_spanning
+// factorises; consecutive threads walk j so the stores coalesce.
+__global__ void __launch_bounds__(kNT) gather_rows_t_kernel(const double* __restrict__ A, int64_t lda, int64_t n,
+                                                            const int64_t* __restrict__ I, int64_t k,
+                                                            double* __restrict__ RT, int64_t ldrt) {
+  const int64_t total = k * n;
+  for (int64_t e = blockIdx.x * (int64_t)kNT + threadIdx.x; e < total; e += (int64_t)gridDim.x * kNT) {
+    const int64_t j = e % n, t = e / n;
+    RT[j + t * ldrt] = __ldg(A + I[t] + j * lda);
+  }
+}
+
 __global__ void __launch_bounds__(kNT) gather_block_kernel(const double* __restrict__ A, int64_t lda,
                                                            const int64_t* __restrict__ I, int64_t k,
                                                            const int64_t* __restrict__ J, int64_t l,
@@ -219,6 +232,14 @@ int launch_gather_rows(Context* c, const double* A, int64_t lda, int64_t n, cons
                        int64_t ldr) {
   if (k == 0 || n == 0) return SLRA_OK;
   SLRA_TIMED(c, "gather", gather_rows_kernel<<<grid_1d(c, k * n), kNT, 0, c->stream>>>(A, lda, n, I, k, R, ldr);)
+  SLRA_CHECK_LAUNCH(c);
+  return SLRA_OK;
+}
+
+int launch_gather_rows_t(Context* c, const double* A, int64_t lda, int64_t n, const int64_t* I, int64_t k,
+                         double* RT, int64_t ldrt) {
+  if (k == 0 || n == 0) return SLRA_OK;
+  SLRA_TIMED(c, "gather", gather_rows_t_kernel<<<grid_1d(c, k * n), kNT, 0, c->stream>>>(A, lda, n, I, k, RT, ldrt);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }

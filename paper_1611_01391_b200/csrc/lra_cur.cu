@@ -76,6 +76,28 @@ int slra_cur_residual(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
   return SLRA_OK;
 }
 
+// ||A - C U R||_F with the nucleus in factored form U = Tsig Sr^T (rank r):
+// P = C Tsig (m x r), Q = Sr^T R (r x n), one pass over A at inner dimension r.
+int slra_cur_residual_factored(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, const int64_t* I,
+                               int64_t k, const int64_t* J, int64_t l, const double* Tsig, const double* Sr, int64_t r,
+                               double* d_out) {
+  if (!ctx || lda < m || k < 1 || l < 1 || r < 1 || r > k || r > l) return SLRA_ERR_INVALID_ARGUMENT;
+  Context* cx = C(ctx);
+  const int64_t ldq = (r + 1) & ~1;  // even ld keeps the streaming kernel's 16-byte staging
+  const size_t need = (size_t)m * l + (size_t)k * n + (size_t)m * r + (size_t)ldq * n + 16;
+  double* ws = static_cast<double*>(arena(cx, 5, sizeof(double) * need));
+  if (!ws) return SLRA_ERR_CUDA;
+  double* Cm = ws;
+  double* Rm = Cm + (size_t)m * l;
+  double* P = Rm + (size_t)k * n;
+  double* Q = P + (size_t)m * r;
+  SLRA_TRY(launch_gather_cols(cx, A, lda, m, J, l, Cm, m));
+  SLRA_TRY(launch_gather_rows(cx, A, lda, n, I, k, Rm, k));
+  SLRA_TRY(launch_gemm(cx, 0, 0, m, r, l, 1.0, Cm, m, Tsig, l, 0.0, P, m));
+  SLRA_TRY(launch_gemm(cx, 1, 0, r, n, k, 1.0, Sr, k, Rm, k, 0.0, Q, ldq));
+  return launch_lowrank_residual(cx, A, lda, m, n, P, m, Q, ldq, r, d_out);
+}
+
 // range_finder over nsk sketches H_s of one M: MH_s (plans) -> Q_s R_s (batched
 // thin QR / TSQR) -> SVD(R_s) (batched, one CTA each) -> one rank check for
 // all -> U_s, V_s -> residuals. Host-array arguments (h_*) hold per-sketch

@@ -152,7 +152,7 @@ int slra_ctx_destroy(slra_ctx ctx) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->partials) cudaFree(c->partials);
   if (c->dsmall) cudaFree(c->dsmall);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
     if (c->arena[i]) cudaFree(c->arena[i]);
   for (auto& r : c->records) {
     cudaEventDestroy(r.start);

@@ -18,6 +18,9 @@ struct CurDecomposition {
   Matrix nucleus;    // l x k
   Index r = 0;
   bool qr_nucleus = false;  // only the SVD nucleus is on the device path
+  // Factored nucleus U = tsig * sr^T (l x r, k x r), filled by primitive_cur /
+  // cross_approx: cur_evaluate then runs its pass over M at inner dimension r.
+  Matrix tsig, sr;
 };
 
 /// C * U * R (evaluation only; cur.cpp:76-78).

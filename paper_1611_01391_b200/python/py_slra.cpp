@@ -56,6 +56,10 @@ static py::dict cur_dict(const CurDecomposition& c) {
   d["J"] = c.col_set.indices();
   d["nucleus"] = to_np(c.nucleus);
   d["r"] = c.r;
+  if (c.tsig.cols() > 0) {
+    d["tsig"] = to_np(c.tsig);
+    d["sr"] = to_np(c.sr);
+  }
   return d;
 }
 
@@ -175,6 +179,15 @@ PYBIND11_MODULE(_slra, m) {
                            const FArray& U) {
     Matrix M = from_np(A);
     CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), from_np(U), 0, false};
+    return cur_evaluate(M, c, NormKind::Frobenius);
+  });
+  m.def("cur_evaluate_factored", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
+                                    const FArray& T, const FArray& S) {
+    Matrix M = from_np(A);
+    CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), Matrix(), 0, false};
+    c.tsig = from_np(T);
+    c.sr = from_np(S);
+    c.r = c.tsig.cols();
     return cur_evaluate(M, c, NormKind::Frobenius);
   });
   m.def("cur_reconstruct", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
@@ -332,6 +345,31 @@ PYBIND11_MODULE(_slra, m) {
                             ptr<int64_t>(I), ptr<int64_t>(J), ptr<double>(U), nullptr, nullptr, nullptr, &r_used),
           "cross_approx");
     return r_used;
+  });
+  m.def("cross_approx_traced_device", [](uintptr_t A, Index lda, Index mm, Index n, Index r, Index k, Index l,
+                                         uintptr_t init_rows, int loops, double h, uintptr_t I, uintptr_t J,
+                                         uintptr_t U, uintptr_t trows, uintptr_t tcols, uintptr_t tvol) {
+    int64_t r_used = 0;
+    check(slra_cross_approx(device_context(), ptr<double>(A), lda, mm, n, r, k, l, ptr<int64_t>(init_rows), loops, h,
+                            ptr<int64_t>(I), ptr<int64_t>(J), ptr<double>(U), ptr<int64_t>(trows),
+                            ptr<int64_t>(tcols), ptr<double>(tvol), &r_used),
+          "cross_approx");
+    return r_used;
+  });
+  m.def("primitive_cur_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t I, Index k, uintptr_t J,
+                                   Index l, Index r, uintptr_t U, uintptr_t Tsig, uintptr_t Sr) {
+    int64_t r_used = 0;
+    check(slra_primitive_cur(device_context(), ptr<double>(A), lda, mm, n, ptr<int64_t>(I), k, ptr<int64_t>(J), l, r,
+                             ptr<double>(U), l, ptr<double>(Tsig), ptr<double>(Sr), &r_used),
+          "primitive_cur");
+    return r_used;
+  });
+  m.def("cur_residual_factored_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t I, Index k,
+                                           uintptr_t J, Index l, uintptr_t Tsig, uintptr_t Sr, Index r,
+                                           uintptr_t out) {
+    check(slra_cur_residual_factored(device_context(), ptr<double>(A), lda, mm, n, ptr<int64_t>(I), k,
+                                     ptr<int64_t>(J), l, ptr<double>(Tsig), ptr<double>(Sr), r, ptr<double>(out)),
+          "cur_residual_factored");
   });
   m.def("cur_residual_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t I, Index k, uintptr_t J,
                                   Index l, uintptr_t U) {

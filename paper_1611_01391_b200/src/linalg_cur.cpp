@@ -116,9 +116,11 @@ CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Ind
   const Index k = I.size(), l = J.size();
   DevBuf<int64_t> dI(to64(I)), dJ(to64(J));
   DeviceMatrix dU(l, k);
+  const Index kl = std::min(k, l);
+  DevBuf<double> dT(static_cast<size_t>(l * kl)), dS(static_cast<size_t>(k * kl));
   int64_t r_used = 0;
   check(slra_primitive_cur(device_context(), dA.data(), dA.ld(), M.rows(), M.cols(), dI.get(), k, dJ.get(), l, r,
-                           dU.data(), l, nullptr, nullptr, &r_used),
+                           dU.data(), l, dT.get(), dS.get(), &r_used),
         "primitive_cur");
   M.count(static_cast<unsigned long long>(k * l));  // the only entries read
   CurDecomposition c;
@@ -126,6 +128,11 @@ CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Ind
   c.col_set = std::move(J);
   c.nucleus = dU.download();
   c.r = r_used;
+  const auto t = dT.download(), s = dS.download();
+  c.tsig = Matrix(l, r_used);
+  c.sr = Matrix(k, r_used);
+  std::copy(t.begin(), t.begin() + l * r_used, c.tsig.data());
+  std::copy(s.begin(), s.begin() + k * r_used, c.sr.data());
   return c;
 }
 
@@ -181,6 +188,16 @@ double cur_evaluate(const EntryOracle& M, const CurDecomposition& c, NormKind no
     throw std::invalid_argument("cur_evaluate: only the Frobenius norm is on the device path");
   const DeviceMatrix& dA = M.device();
   DevBuf<int64_t> dI(to64(c.row_set)), dJ(to64(c.col_set));
+  if (c.r > 0 && c.tsig.cols() == c.r && c.sr.cols() == c.r) {
+    // factored nucleus: the pass over M runs at inner dimension r
+    DeviceMatrix dT = DeviceMatrix::upload(c.tsig), dS = DeviceMatrix::upload(c.sr);
+    DevBuf<double> out(2);
+    check(slra_cur_residual_factored(device_context(), dA.data(), dA.ld(), M.rows(), M.cols(), dI.get(),
+                                     c.row_set.size(), dJ.get(), c.col_set.size(), dT.data(), dS.data(), c.r,
+                                     out.get()),
+          "cur_evaluate");
+    return std::sqrt(out.download()[0]);
+  }
   DeviceMatrix dU = DeviceMatrix::upload(c.nucleus);
   double rs = 0, ns = 0;
   check(slra_cur_residual(device_context(), dA.data(), dA.ld(), M.rows(), M.cols(), dI.get(), c.row_set.size(),
