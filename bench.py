@@ -28,6 +28,8 @@ import sys
 import tempfile
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -42,7 +44,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", type=int, default=2, choices=[1, 2, 5])
+    p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--blocks", type=int, default=65536, help="config 5 block count")
@@ -227,6 +229,8 @@ def main():
 
     if args.config == 2:
         work = Config2(slra, torch, args.seed + rank)
+    elif args.config == 3:
+        work = Config3(slra, torch, args.seed + rank)
     elif args.config == 1:
         work = Config1(slra, torch, args.seed + rank)
     else:
@@ -451,6 +455,117 @@ class Config1:
         dt = time.perf_counter() - t0
         return {"value": self.entries_per_step * n / dt, "unit": "entries/s", "cores": 1, "kind": "port",
                 "sample": f"{n} config-1 runs in 5 s"}
+
+
+N3, K3, LOOPS3 = 16384, 64, 5
+
+
+def config3_points(mod, seed, n=N3):
+    """x_i ~ U[0,1], y_j ~ U[2,3] drawn with the reference Rng (testgen order)."""
+    r = mod.Rng(seed)
+    x = [r.uniform() for _ in range(n)]
+    y = [2.0 + r.uniform() for _ in range(n)]
+    return x, y
+
+
+class Config3:
+    """Config 3: C-A on the 16384^2 Cauchy block 1/(x_i - y_j), k=l=64, 5 sweeps,
+    adaptive r (numerical_rank 1e-10), full ||A - CUR||_F."""
+
+    def __init__(self, slra, torch, seed):
+        self.slra, self.torch = slra, torch
+        self.seed = seed
+        x, y = config3_points(slra, seed)
+        xd = torch.tensor(x, dtype=torch.float64, device="cuda")
+        yd = torch.tensor(y, dtype=torch.float64, device="cuda")
+        # column-major A: At[j, i] = 1/(x_i - y_j) (one IEEE division: bit-identical to the host generator)
+        self.At = (1.0 / (xd[None, :] - yd[:, None])).contiguous()
+        self.init = slra.Rng(seed + 1).distinct_indices(K3, N3)
+        self.init_d = torch.tensor(self.init, dtype=torch.int64, device="cuda")
+        self.I = torch.zeros(K3, dtype=torch.int64, device="cuda")
+        self.J = torch.zeros(K3, dtype=torch.int64, device="cuda")
+        self.U = torch.zeros(K3 * K3, dtype=torch.float64, device="cuda")
+        self.T = torch.zeros(K3 * K3, dtype=torch.float64, device="cuda")
+        self.S = torch.zeros(K3 * K3, dtype=torch.float64, device="cuda")
+        self.out = torch.zeros(2, dtype=torch.float64, device="cuda")
+        self.r = 0
+        self.entries_per_step = N3 * N3
+        self.config = {"workload": "config3: C-A CUR of the 16384x16384 fp64 Cauchy block 1/(x-y), k=l=64, "
+                                   "5 sweeps, adaptive r (numerical_rank 1e-10), full ||A-CUR||_F",
+                       "entries_per_step": self.entries_per_step, "m": N3, "n": N3, "k": K3, "l": K3,
+                       "loops": LOOPS3}
+
+    def step(self):
+        s = self.slra
+        a = self.At.data_ptr()
+        self.r = s.cross_approx_device(a, N3, N3, N3, 0, K3, K3, self.init_d.data_ptr(), LOOPS3, 1.1,
+                                       self.I.data_ptr(), self.J.data_ptr(), self.U.data_ptr(),
+                                       self.T.data_ptr(), self.S.data_ptr())
+        s.cur_residual_factored_device(a, N3, N3, N3, self.I.data_ptr(), K3, self.J.data_ptr(), K3,
+                                       self.T.data_ptr(), self.S.data_ptr(), self.r, self.out.data_ptr())
+
+    def last_residual_rel(self):
+        o = self.out.cpu().numpy()
+        return {"rel": float((o[0] / o[1]) ** 0.5), "r": int(self.r)}
+
+    def roofline(self, fam, peaks, steps):
+        kernels = {k: v[0] / steps for k, v in fam.items()}
+        per = {k: v[0] / max(v[1], 1) for k, v in fam.items()}
+        top = max(fam.items(), key=lambda kv: kv[1][0])[0]
+        n, r = N3, max(self.r, 1)
+        # algorithmic bytes per launch of each family (DESIGN.md roofline table)
+        strip = 8.0 * n * K3
+        byts = {"residual": 8.0 * n * n + 16.0 * n * r, "gather": strip * 2, "thin_qr": strip * 2,
+                "maxvol": strip}
+        b = byts.get(top, strip)
+        ach = b / (per[top] * 1e-3) / 1e9
+        rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+              "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+              "algorithmic_bytes_per_launch": b, "traffic": None}
+        if "residual" in per:
+            rb = 8.0 * n * n + 16.0 * n * r
+            rl["residual_kernel"] = {"achieved_gbs": rb / (per["residual"] * 1e-3) / 1e9,
+                                     "frac_hbm": rb / (per["residual"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                     "inner_dim_r": r}
+        return rl, kernels
+
+    def e2e(self, steps, warmup):
+        torch = self.torch
+        host = torch.empty(N3 * N3, dtype=torch.float64, pin_memory=True)
+        host.copy_(self.At.reshape(-1))
+        ptr = host.data_ptr()
+
+        def one():
+            return self.slra.cross_approx_host(ptr, N3, N3, 0, K3, K3, self.init, LOOPS3, 1.1)
+        for _ in range(max(1, warmup // 2)):
+            one()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            d = one()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        return {"value": self.entries_per_step * steps / dt, "unit": "entries/s",
+                "h2d_bytes_per_step": 8 * N3 * N3 + 8 * K3,
+                "d2h_bytes_per_step": 8 * (2 * K3 + K3 * K3 + 2 * K3 * d["r"] + 2),
+                "api": "paper_1611_01391_b200.cross_approx_host -> slra::cross_approx + slra::cur_evaluate "
+                       "(host pinned A in; I, J, nucleus, residual out)"}
+
+    def cpu_baseline(self):
+        sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))
+        import _oracle as oracle
+        cores = os.cpu_count() or 1
+        A = self.At.cpu().numpy().T
+        t0 = time.perf_counter()
+        o = oracle.cross_approx(A, 1, K3, K3, self.init, LOOPS3, 1.1, None, oracle.Rng(0))
+        G = A[np.ix_(o["I"], o["J"])]
+        rk = oracle.numerical_rank(G, 1e-10, True)
+        c = oracle.primitive_cur(A, o["I"], o["J"], rk)
+        oracle.cur_evaluate(A, o["I"], o["J"], c["nucleus"])
+        dt = time.perf_counter() - t0
+        return {"value": self.entries_per_step / dt, "unit": "entries/s", "cores": cores, "kind": "port",
+                "sample": "one full config-3 step (5 C-A sweeps on 16384^2, adaptive-rank nucleus, "
+                          "cur_evaluate) through the oracle/ C++ restatement, OpenMP", "seconds": dt}
 
 
 class Config5:

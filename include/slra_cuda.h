@@ -137,12 +137,14 @@ int slra_primitive_cur(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, 
  * (2*loops steps: rows k, cols l, volume proxy), adaptive r. k, l <= 64.
  * Strips that fit one SM run the whole loop in one CTA-resident kernel;
  * taller ones (config 3) use TSQR + the grid-wide cooperative maxvol per
- * half-sweep (k == l there). Blocks until done (status is host-visible). */
+ * half-sweep (k == l there). d_Tsig / d_Sr (nullable) receive the factored
+ * nucleus as in slra_primitive_cur. Blocks until done (status is
+ * host-visible). */
 int slra_cross_approx(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
                       int64_t r, int64_t k, int64_t l, const int64_t* d_init_rows, int loops,
                       double h, int64_t* d_I, int64_t* d_J, double* d_nucleus,
                       int64_t* d_trace_rows, int64_t* d_trace_cols, double* d_trace_volume,
-                      int64_t* h_r_out);
+                      double* d_Tsig, double* d_Sr, int64_t* h_r_out);
 /* Batched cross_approx + per-block Frobenius residual: nblocks independent
  * m x n blocks at d_A + b*block_stride (ld = lda); one CTA per block.
  * Per-block outputs: I (k), J (l), nucleus (l x k), r, status (slra_status),

@@ -44,7 +44,7 @@ struct CaSmem {
 
 __host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
-  size_t d = 2 * (size_t)mm * c + 5 * (size_t)c * c + 6 * (size_t)c + 2 * (size_t)mm + 40;
+  size_t d = 2 * (size_t)mm * c + 4 * (size_t)c * c + 6 * (size_t)c + 2 * (size_t)mm + 40;
   size_t i = (size_t)mm + 4 * (size_t)c + 8 + (size_t)c;
   return d * 8 + 33 * 8 + i * 4 + 64;
 }
@@ -58,7 +58,7 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   s.R = d; d += c * c;
   s.Gt = d; d += c * c;
   s.V = d; d += c * c;
-  s.Tm = d; d += c * c;
+  s.Tm = s.R;  // R (the selection's QR factor) is dead once the nucleus starts
   s.Sm = d; d += c * c;
   s.tau = d; d += c;
   s.v = d; d += c;
@@ -341,7 +341,7 @@ int slra_primitive_cur(slra_ctx ctx, const double* A, int64_t lda, int64_t m, in
 int slra_cross_approx(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, int64_t r, int64_t k,
                       int64_t l, const int64_t* init_rows, int loops, double h, int64_t* I_out, int64_t* J_out,
                       double* nucleus, int64_t* trace_rows, int64_t* trace_cols, double* trace_vol,
-                      int64_t* h_r_out) {
+                      double* Tsig, double* Sr, int64_t* h_r_out) {
   if (!ctx || lda < m || loops < 1 || k < 1 || l < 1 || (r > 0 && (k < r || l < r)) || k > m || l > n)
     return SLRA_ERR_INVALID_ARGUMENT;
   if (!ca_fits((int)m, (int)n, (int)k, (int)l)) {
@@ -399,13 +399,13 @@ int slra_cross_approx(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
     }
     SLRA_CUDA(cudaMemcpyAsync(I_out, dI, 8 * k, cudaMemcpyDeviceToDevice, cx->stream));
     SLRA_CUDA(cudaMemcpyAsync(J_out, dJ, 8 * l, cudaMemcpyDeviceToDevice, cx->stream));
-    return slra_primitive_cur(ctx, A, lda, m, n, I_out, k, J_out, l, r, nucleus, l, nullptr, nullptr, h_r_out);
+    return slra_primitive_cur(ctx, A, lda, m, n, I_out, k, J_out, l, r, nucleus, l, Tsig, Sr, h_r_out);
   }
   Context* cx = C(ctx);
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
   int64_t* d_r = reinterpret_cast<int64_t*>(static_cast<char*>(cx->dsmall) + 64);
   CaParams p{A, lda, 0, (int)m, (int)n, (int)r, (int)k, (int)l, loops, h, init_rows, I_out, J_out, nucleus, d_r,
-             d_status, trace_rows, trace_cols, trace_vol, nullptr, nullptr, (int)(k < l ? k : l), 0};
+             d_status, trace_rows, trace_cols, trace_vol, nullptr, nullptr, (int)(k < l ? k : l), 0, Tsig, Sr};
   SLRA_TRY(launch_ca_block(cx, p, 1));
   char* hs = static_cast<char*>(cx->hsmall);
   SLRA_CUDA(cudaMemcpyAsync(hs, cx->dsmall, 128, cudaMemcpyDeviceToHost, cx->stream));

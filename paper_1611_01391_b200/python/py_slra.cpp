@@ -289,6 +289,24 @@ PYBIND11_MODULE(_slra, m) {
     return py::make_tuple(to_np(dU.download()), to_np(dV.download()), o[0], o[1]);
   });
 
+  // ---- end-to-end cross_approx(M, ...) + cur_evaluate(M, c, Frobenius)
+  // (cur.hpp) with M read from the caller's (pinned) host buffer; I, J, the
+  // nucleus and the residual come back to the host.
+  m.def("cross_approx_host", [](uintptr_t M_host, Index mm, Index n, Index r, Index k, Index l,
+                                const std::vector<Index>& init_rows, int loops, double h) {
+    static DeviceMatrix* staging = new DeviceMatrix();  // reused HBM staging buffer (never freed)
+    if (staging->rows() != mm || staging->cols() != n) *staging = DeviceMatrix(mm, n);
+    check(slra_memcpy_h2d(device_context(), staging->data(), reinterpret_cast<const void*>(M_host), 8 * mm * n),
+          "cross_approx_host");
+    DeviceOracle o(staging->data(), mm, n, mm);
+    Rng rng(0);
+    auto [c, trace] = cross_approx(o, r, k, l, mkset(init_rows, mm), loops, h, std::nullopt, rng);
+    const double res = cur_evaluate(o, c, NormKind::Frobenius);
+    py::dict d = cur_dict(c);
+    d["residual"] = res;
+    return d;
+  });
+
   // ---- device-resident entry points (raw device pointers)
   m.def("range_finder_device", [](uintptr_t M, Index ldm, Index mm, Index n, const py::dict& plan, Index r,
                                   bool truncated, uintptr_t U, Index ldu, uintptr_t V, Index ldv, uintptr_t out,
@@ -339,23 +357,17 @@ PYBIND11_MODULE(_slra, m) {
           "cross_approx_batched");
   });
   m.def("cross_approx_device", [](uintptr_t A, Index lda, Index mm, Index n, Index r, Index k, Index l,
-                                  uintptr_t init_rows, int loops, double h, uintptr_t I, uintptr_t J, uintptr_t U) {
+                                  uintptr_t init_rows, int loops, double h, uintptr_t I, uintptr_t J, uintptr_t U,
+                                  uintptr_t Tsig, uintptr_t Sr) {
     int64_t r_used = 0;
     check(slra_cross_approx(device_context(), ptr<double>(A), lda, mm, n, r, k, l, ptr<int64_t>(init_rows), loops, h,
-                            ptr<int64_t>(I), ptr<int64_t>(J), ptr<double>(U), nullptr, nullptr, nullptr, &r_used),
+                            ptr<int64_t>(I), ptr<int64_t>(J), ptr<double>(U), nullptr, nullptr, nullptr,
+                            ptr<double>(Tsig), ptr<double>(Sr), &r_used),
           "cross_approx");
     return r_used;
-  });
-  m.def("cross_approx_traced_device", [](uintptr_t A, Index lda, Index mm, Index n, Index r, Index k, Index l,
-                                         uintptr_t init_rows, int loops, double h, uintptr_t I, uintptr_t J,
-                                         uintptr_t U, uintptr_t trows, uintptr_t tcols, uintptr_t tvol) {
-    int64_t r_used = 0;
-    check(slra_cross_approx(device_context(), ptr<double>(A), lda, mm, n, r, k, l, ptr<int64_t>(init_rows), loops, h,
-                            ptr<int64_t>(I), ptr<int64_t>(J), ptr<double>(U), ptr<int64_t>(trows),
-                            ptr<int64_t>(tcols), ptr<double>(tvol), &r_used),
-          "cross_approx");
-    return r_used;
-  });
+  }, py::arg("A"), py::arg("lda"), py::arg("m"), py::arg("n"), py::arg("r"), py::arg("k"), py::arg("l"),
+     py::arg("init_rows"), py::arg("loops"), py::arg("h"), py::arg("I"), py::arg("J"), py::arg("U"),
+     py::arg("Tsig") = 0, py::arg("Sr") = 0);
   m.def("primitive_cur_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t I, Index k, uintptr_t J,
                                    Index l, Index r, uintptr_t U, uintptr_t Tsig, uintptr_t Sr) {
     int64_t r_used = 0;

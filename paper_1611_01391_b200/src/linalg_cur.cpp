@@ -106,6 +106,16 @@ IndexSet select_rows_spanning(const Matrix& A, Index count, double h) {  // cur.
   return IndexSet(std::vector<Index>(v.begin(), v.end()), m);
 }
 
+// factored nucleus U = tsig * sr^T from the device buffers (first r columns)
+static void set_factors(CurDecomposition& c, const DevBuf<double>& dT, const DevBuf<double>& dS, Index l, Index k,
+                        Index r) {
+  const auto t = dT.download(), s = dS.download();
+  c.tsig = Matrix(l, r);
+  c.sr = Matrix(k, r);
+  std::copy(t.begin(), t.begin() + l * r, c.tsig.data());
+  std::copy(s.begin(), s.begin() + k * r, c.sr.data());
+}
+
 CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus) {
   // cur.cpp:137-162 (SVD nucleus)
   if (qr_nucleus) throw std::invalid_argument("primitive_cur: the QR nucleus is not on the device path");
@@ -128,11 +138,7 @@ CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Ind
   c.col_set = std::move(J);
   c.nucleus = dU.download();
   c.r = r_used;
-  const auto t = dT.download(), s = dS.download();
-  c.tsig = Matrix(l, r_used);
-  c.sr = Matrix(k, r_used);
-  std::copy(t.begin(), t.begin() + l * r_used, c.tsig.data());
-  std::copy(s.begin(), s.begin() + k * r_used, c.sr.data());
+  set_factors(c, dT, dS, l, k, r_used);
   return c;
 }
 
@@ -156,9 +162,11 @@ std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r,
   DevBuf<int64_t> trows(static_cast<size_t>(2 * loops * k)), tcols(static_cast<size_t>(2 * loops * l));
   DevBuf<double> tvol(static_cast<size_t>(2 * loops));
   DeviceMatrix dU(l, k);
+  const Index kl = std::min(k, l);
+  DevBuf<double> dT(static_cast<size_t>(l * kl)), dS(static_cast<size_t>(k * kl));
   int64_t r_used = 0;
   check(slra_cross_approx(device_context(), dA.data(), dA.ld(), m, n, r, k, l, dI0.get(), loops, h, dI.get(),
-                          dJ.get(), dU.data(), trows.get(), tcols.get(), tvol.get(), &r_used),
+                          dJ.get(), dU.data(), trows.get(), tcols.get(), tvol.get(), dT.get(), dS.get(), &r_used),
         "cross_approx");
   // algorithmic reads: per loop one k x n row strip and one m x l column
   // strip, then the k x l generator (the reference's DenseOracle count)
@@ -180,6 +188,7 @@ std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r,
   c.col_set = IndexSet(std::vector<Index>(vJ.begin(), vJ.end()), n);
   c.nucleus = dU.download();
   c.r = r_used;
+  set_factors(c, dT, dS, l, k, r_used);
   return {std::move(c), std::move(trace)};
 }
 

@@ -316,7 +316,10 @@ def test_cross_approx_cauchy_reduced(slra, oracle, n, seed):
     """Config 3 at reduced size: 1/(x-y) block, k=l=64, 5 sweeps, adaptive r."""
     k = 64
     A = slra.gen_cauchy_block(n, n, slra.Rng(seed))
-    assert np.array_equal(A, oracle.gen_cauchy_block(n, n, oracle.Rng(seed)))
+    r = oracle.Rng(seed)
+    x = np.array([r.uniform() for _ in range(n)])
+    y = np.array([2.0 + r.uniform() for _ in range(n)])
+    assert np.array_equal(A, 1.0 / (x[:, None] - y[None, :]))
     init = slra.Rng(700 + seed).distinct_indices(k, n)
     g = slra.cross_approx(A, 0, k, k, init, 5, 1.1, slra.Rng(0))
     o = oracle.cross_approx(A, 1, k, k, init, 5, 1.1, None, oracle.Rng(0))
