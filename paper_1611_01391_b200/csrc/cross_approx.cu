@@ -168,7 +168,12 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
     else s.W[b + a * p] = g;
   }
   __syncthreads();
-  cta_jacobi<NT>(s.W, p, p, q, s.V, q, s.flag);
+  // Only sigma_i > 1e-10 sigma_1 enter the nucleus (pinv cut, linalg.cpp:111-121;
+  // rank checks cur.cpp:156-157): columns below 1e-10/sqrt(q) of the largest
+  // column norm jointly carry less than that, so pairs of two such columns
+  // are not rotated (the noise directions of rank-deficient generators, as in
+  // configs 3 and 5, otherwise keep the sweeps going to the cap).
+  cta_jacobi<NT>(s.W, p, p, q, s.V, q, s.flag, 1e-10 / sqrt((double)q));
   // finish into S (p x q, ld p) and Gt (q x q, ld q): for tall G the left
   // vectors are in S; for wide G (SVD of G^T) they are the rows of V.
   cta_svd_finish<NT>(s.W, p, p, q, s.V, q, s.sigma, s.order, s.S, p, s.Gt, q, s.sgn);

@@ -9,7 +9,8 @@
 //                    LAPACK xGEQP3 norm downdate
 //   warp_colpiv_qr   ColPivHouseholderQR of a small square (cur.cpp:103-106)
 //   cta_maxvol_swaps maxvol swap loop (cur.cpp:100-114): B = A G^-1 by the
-//                    Eigen solve, argmax in column-major order, first max wins
+//                    Eigen solve (round 0) then rank-1 updates, argmax in
+//                    column-major order, first max wins
 //   warp_abs_det     |det| via partial-pivot LU (cur.cpp:192-197)
 //   cta_jacobi_svd   one-sided Jacobi SVD (BDCSVD stand-in, linalg.cpp:81-98)
 #pragma once
@@ -451,55 +452,67 @@ __device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h
                                 double* W, int ldw, double* Gt, int ldg, int* perm, double* tau, double* nu,
                                 double* nd, double* rv, int64_t* ri, int* shared_flag) {
   const int tid = threadIdx.x, warp = tid >> 5;
+  // swap round 0 exactly as the reference: ColPivQR(G^T) and its solve for
+  // every row. G^T(c, t) = A(I[t], c)
+  for (int e = tid; e < r * r; e += NT) {
+    const int cc = e % r, t = e / r;
+    Gt[cc + t * ldg] = A[I[t] + cc * lda];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    SmallColPiv q = warp_colpiv_qr(Gt, ldg, r, 1e-12, perm, tau, nu, nd);
+    if ((tid & 31) == 0) shared_flag[0] = q.rank < r ? 1 : 0;  // rank == r implies r nonzero pivots
+  }
+  __syncthreads();
+  if (shared_flag[0]) return SLRA_ERR_SELECTION_FAILURE;
+  // W(i, t) holds B(i, perm[t]) (storage order of the solve)
+  for (int i = tid; i < m; i += NT) {
+    double* c = W + i;  // row i of W as a strided vector (stride ldw)
+    for (int j = 0; j < r; ++j) c[j * ldw] = A[i + j * lda];
+    for (int k = 0; k < r; ++k) {
+      const double t = tau[k];
+      if (r - k == 1) {
+        c[k * ldw] *= (1.0 - t);
+      } else if (t != 0.0) {
+        double w = 0.0;
+        for (int j = k + 1; j < r; ++j) w += Gt[j + k * ldg] * c[j * ldw];
+        w += c[k * ldw];
+        c[k * ldw] -= t * w;
+        for (int j = k + 1; j < r; ++j) c[j * ldw] -= t * Gt[j + k * ldg] * w;
+      }
+    }
+    for (int t2 = r - 1; t2 >= 0; --t2) {
+      double sacc = c[t2 * ldw];
+      for (int u = t2 + 1; u < r; ++u) sacc -= Gt[t2 + u * ldg] * c[u * ldw];
+      c[t2 * ldw] = sacc / Gt[t2 + t2 * ldg];
+    }
+  }
+  int* iperm = reinterpret_cast<int*>(nd);  // B column -> storage column
+  for (int t = tid; t < r; t += NT) iperm[perm[t]] = t;
+  __syncthreads();
+  // swap rounds: argmax |B| (column-major first maximum), then the rank-1
+  // update B <- B - B(:, j) (B(i, :) - e_j) / B(i, j) for row i placed at
+  // slot j: the same B = A G^-1 the reference re-solves each round, at
+  // O(m r) instead of O(m r^2 + r^3) per round.
+  double* g = tau;  // snapshot of the pivot row (r)
   for (int swap = 0; swap <= max_swaps; ++swap) {
-    // G^T(c, t) = A(I[t], c)
-    for (int e = tid; e < r * r; e += NT) {
-      const int cc = e % r, t = e / r;
-      Gt[cc + t * ldg] = A[I[t] + cc * lda];
-    }
-    __syncthreads();
-    if (warp == 0) {
-      SmallColPiv q = warp_colpiv_qr(Gt, ldg, r, 1e-12, perm, tau, nu, nd);
-      if ((tid & 31) == 0) {
-        shared_flag[0] = q.rank < r ? 1 : 0;
-        shared_flag[1] = q.nonzero_pivots;
-      }
-    }
-    __syncthreads();
-    if (shared_flag[0]) return SLRA_ERR_SELECTION_FAILURE;
-    const int np = shared_flag[1];
-    // B(i, :) = solve(G^T, A(i, :)^T)^T for every row i; track |B| argmax
     ArgMax best{-1.0, INT64_MAX};
-    for (int i = tid; i < m; i += NT) {
-      double* c = W + i;  // row i of W as a strided vector (stride ldw)
-      for (int j = 0; j < r; ++j) c[j * ldw] = A[i + j * lda];
-      for (int k = 0; k < np; ++k) {
-        const double t = tau[k];
-        if (r - k == 1) {
-          c[k * ldw] *= (1.0 - t);
-        } else if (t != 0.0) {
-          double w = 0.0;
-          for (int j = k + 1; j < r; ++j) w += Gt[j + k * ldg] * c[j * ldw];
-          w += c[k * ldw];
-          c[k * ldw] -= t * w;
-          for (int j = k + 1; j < r; ++j) c[j * ldw] -= t * Gt[j + k * ldg] * w;
-        }
-      }
-      for (int t2 = np - 1; t2 >= 0; --t2) {
-        double sacc = c[t2 * ldw];
-        for (int u = t2 + 1; u < np; ++u) sacc -= Gt[t2 + u * ldg] * c[u * ldw];
-        c[t2 * ldw] = sacc / Gt[t2 + t2 * ldg];
-      }
-      for (int t2 = 0; t2 < r; ++t2) {
-        const double v = t2 < np ? fabs(c[t2 * ldw]) : 0.0;
-        const int64_t lin = (int64_t)perm[t2] * m + i;  // column-major linear index
-        best = argmax_merge(best, ArgMax{v, lin});
-      }
-    }
+    for (int i = tid; i < m; i += NT)
+      for (int t2 = 0; t2 < r; ++t2)
+        best = argmax_merge(best, ArgMax{fabs(W[i + t2 * ldw]), (int64_t)perm[t2] * m + i});
     best = block_argmax<NT>(best, rv, ri);
     if (best.v <= h) return SLRA_OK;
     if (swap == max_swaps) return SLRA_OK;
-    if (tid == 0) I[best.i / m] = (int)(best.i % m);
+    const int j = (int)(best.i / m), piv = (int)(best.i % m);
+    const int ts = iperm[j];
+    for (int t2 = tid; t2 < r; t2 += NT) g[t2] = W[piv + t2 * ldw] - (t2 == ts ? 1.0 : 0.0);
+    __syncthreads();
+    const double p = W[piv + ts * ldw];
+    if (tid == 0) I[j] = piv;
+    for (int i = tid; i < m; i += NT) {
+      const double f = W[i + ts * ldw] / p;
+      for (int t2 = 0; t2 < r; ++t2) W[i + t2 * ldw] -= f * g[t2];
+    }
     __syncthreads();
   }
   return SLRA_OK;

@@ -28,97 +28,122 @@ struct MaxvolLargeArgs {
   int64_t* I_out;     // r
   double* vol_out;    // nullable
   int32_t* status;
-  // global scratch: 2 x grid candidate slots (value, pos, row) + vectors
+  // global scratch: 2 x grid candidate slots (value, key, row) + vectors
   double* cand_v;     // 2 x G
   int64_t* cand_pos;  // 2 x G
   int64_t* cand_row;  // 2 x G
   double* cand_vec;   // 2 x G x kMR
 };
 
+// Publish this CTA's candidate (value, key, global row, r-vector) into slot.
+__device__ __forceinline__ void publish(const MaxvolLargeArgs& a, int slot, int G, int b, double v, int64_t key,
+                                        int64_t row, const double* vec, int r) {
+  if (threadIdx.x == 0) {
+    a.cand_v[slot * G + b] = v;
+    a.cand_pos[slot * G + b] = key;
+    a.cand_row[slot * G + b] = row;
+  }
+  if (row >= 0)
+    for (int j = threadIdx.x; j < r; j += kMT) a.cand_vec[(size_t)(slot * G + b) * kMR + j] = vec[j];
+}
+
+// After grid.sync: every CTA reduces the G candidates identically (warp 0)
+// and returns the winning CTA (first slot holding the winning key).
+__device__ __forceinline__ int reduce_candidates(const MaxvolLargeArgs& a, int slot, int G, double* rv, int64_t* ri,
+                                                 int* sflag) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    ArgMax g{-1.0, INT64_MAX};
+    for (int c = lane; c < G; c += 32) {
+      if (__ldcg(a.cand_row + slot * G + c) < 0) continue;
+      g = argmax_merge(g, ArgMax{__ldcg(a.cand_v + slot * G + c), __ldcg(a.cand_pos + slot * G + c)});
+    }
+    g = warp_argmax(g);
+    int win = G;
+    for (int c = lane; c < G; c += 32)
+      if (__ldcg(a.cand_row + slot * G + c) >= 0 && __ldcg(a.cand_pos + slot * G + c) == g.i) win = min(win, c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) win = min(win, __shfl_xor_sync(0xffffffffu, win, o));
+    if (lane == 0) {
+      sflag[0] = win;
+      rv[0] = g.v;
+      ri[0] = g.i;
+    }
+  }
+  __syncthreads();
+  return sflag[0];
+}
+
 __global__ void __launch_bounds__(kMT) maxvol_large_kernel(MaxvolLargeArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   const int G = gridDim.x, b = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int r = a.r;
+  const int ldw = r | 1;  // odd row stride: conflict-free column access by row-threads
   const int64_t rows_per = (a.m + G - 1) / G;
   const int64_t row0 = b * rows_per;
   const int nr = (int)((a.m - row0) < rows_per ? ((a.m - row0) > 0 ? (a.m - row0) : 0) : rows_per);
-  double* W = sm;                       // nr x r, row-major (ld r): W[i*r + j]
-  double* Gt = W + kMRB * kMR;          // r x r (ld r)
-  double* vv = Gt + kMR * kMR;          // reflector (r)
+  double* W = sm;                       // nr x r, row-major (ld ldw): Q rows, then B rows
+  double* Rm = W + kMRB * (kMR + 1);    // r x r (ld r): R11 of ColPivQR(Q^T) restricted to I
+  double* vv = Rm + kMR * kMR;          // reflector (r)
   double* nu = vv + kMR;                // nr
   double* nd = nu + kMRB;               // nr
-  double* tau = nd + kMRB;              // r
-  double* nu2 = tau + kMR;              // r  (small colpiv scratch)
-  double* nd2 = nu2 + kMR;              // r
-  double* rv = nd2 + kMR;               // 40
+  double* fr = nd + kMRB;               // nr (swap factors)
+  double* bi = fr + kMRB;               // r (winning row of B)
+  double* rv = bi + kMR;                // 40
   int64_t* ri = reinterpret_cast<int64_t*>(rv + 40);  // 40
   int64_t* pos = ri + 40;                              // nr current positions
-  int* chosen = reinterpret_cast<int*>(pos + kMRB);     // nr
-  int* perm = chosen + kMRB;                            // r
-  int* Iloc = perm + kMR;                               // r
+  int* chosen = reinterpret_cast<int*>(pos + kMRB);     // nr: 0, or 1 + pivot step
+  int* Iloc = chosen + kMRB;                            // r
   __shared__ int sflag[4];
-  __shared__ double sbeta;
+  __shared__ double sbeta, stau, smaxpivot;
+  int sync_no = 0;
   // load my rows (first r columns of Q) and their norms
   for (int i = tid; i < nr; i += kMT) {
     double s = 0.0;
     for (int j = 0; j < r; ++j) {
       const double x = a.Q[(row0 + i) + (int64_t)j * a.ldq];
-      W[i * r + j] = x;
+      W[i * ldw + j] = x;
       s += x * x;
     }
     nu[i] = nd[i] = sqrt(s);
     pos[i] = row0 + i;
     chosen[i] = 0;
   }
+  if (tid == 0) smaxpivot = 0.0;
   __syncthreads();
   const double sqrt_eps = 1.4901161193847656e-08;
-  // ---------------- phase 1: ColPivHouseholderQR(Q^T) pivot order
+  // ---------------- phase 1: ColPivHouseholderQR(Q^T) pivot order. Its
+  // reflectors and R11 are exactly those of ColPivQR(G^T) for G = Q[I,:]
+  // (same columns, same greedy order), so the first solve B = Q G^-1 reuses
+  // them (cur.cpp:100-108).
   for (int k = 0; k < r; ++k) {
-    const int slot = k & 1;
+    const int slot = (sync_no++) & 1;
     ArgMax best{-1.0, INT64_MAX};  // key: value, then lowest current position
     for (int i = tid; i < nr; i += kMT)
       if (!chosen[i]) best = argmax_merge(best, ArgMax{nu[i], pos[i]});
     best = block_argmax<kMT>(best, rv, ri);
-    if (tid == 0) {
-      a.cand_v[slot * G + b] = best.v;
-      a.cand_pos[slot * G + b] = best.i;
-      int64_t row = -1;
-      for (int i = 0; i < nr; ++i)
-        if (!chosen[i] && pos[i] == best.i) row = row0 + i;
-      a.cand_row[slot * G + b] = row;
-      if (row >= 0)
-        for (int j = 0; j < r; ++j) a.cand_vec[(slot * G + b) * kMR + j] = W[(row - row0) * r + j];
-    }
-    grid.sync();
-    // every CTA reduces the G candidates identically
-    if (warp == 0) {
-      ArgMax g{-1.0, INT64_MAX};
-      for (int c = lane; c < G; c += 32) {
-        if (a.cand_row[slot * G + c] < 0) continue;
-        g = argmax_merge(g, ArgMax{a.cand_v[slot * G + c], a.cand_pos[slot * G + c]});
-      }
-      g = warp_argmax(g);
-      if (lane == 0) {
-        int win = -1;
-        for (int c = 0; c < G; ++c)
-          if (a.cand_row[slot * G + c] >= 0 && a.cand_pos[slot * G + c] == g.i) win = c;
-        sflag[0] = win;
-        ri[0] = g.i;  // winning position
-      }
-    }
+    if (tid == 0) sflag[1] = -1;
     __syncthreads();
-    const int win = sflag[0];
+    for (int i = tid; i < nr; i += kMT)
+      if (!chosen[i] && pos[i] == best.i) sflag[1] = i;
+    __syncthreads();
+    const int li = sflag[1];
+    publish(a, slot, G, b, best.v, best.i, li >= 0 ? row0 + li : -1, li >= 0 ? W + li * ldw : nullptr, r);
+    grid.sync();
+    const int win = reduce_candidates(a, slot, G, rv, ri, sflag);
     const int64_t big = ri[0];
-    const int64_t wrow = a.cand_row[slot * G + win];
-    const double* xv = a.cand_vec + (slot * G + win) * kMR;
+    const double pivnorm = rv[0];
+    const int64_t wrow = __ldcg(a.cand_row + slot * G + win);
+    const double* xv = a.cand_vec + (size_t)(slot * G + win) * kMR;
     // Householder of x = winner row components k..r-1 (warp 0), Eigen arithmetic
-    if (warp == 0) {
+    if (tid < 32) {
+      const int lane = tid;
       double tail = 0.0;
-      for (int j = k + 1 + lane; j < r; j += 32) tail += xv[j] * xv[j];
+      for (int j = k + 1 + lane; j < r; j += 32) tail += __ldcg(xv + j) * __ldcg(xv + j);
       tail = warp_sum(tail);
-      const double c0 = xv[k];
+      const double c0 = __ldcg(xv + k);
       double t, beta;
       if (tail <= DBL_MIN) {
         t = 0.0;
@@ -128,27 +153,33 @@ __global__ void __launch_bounds__(kMT) maxvol_large_kernel(MaxvolLargeArgs a) {
         beta = sqrt(c0 * c0 + tail);
         if (c0 >= 0.0) beta = -beta;
         const double den = c0 - beta;
-        for (int j = k + 1 + lane; j < r; j += 32) vv[j] = xv[j] / den;
+        for (int j = k + 1 + lane; j < r; j += 32) vv[j] = __ldcg(xv + j) / den;
         t = (beta - c0) / beta;
       }
       if (lane == 0) {
-        tau[0] = t;
+        stau = t;
         sbeta = beta;
+        if (fabs(beta) > smaxpivot) smaxpivot = fabs(beta);
       }
+    } else {
+      // R11 column k: entries above the diagonal are the winner's first k components
+      for (int t2 = tid - 32; t2 < k; t2 += kMT - 32) Rm[t2 + k * r] = __ldcg(xv + t2);
     }
     // position swap k <-> big, mark the winner chosen
     for (int i = tid; i < nr; i += kMT) {
-      if (row0 + i == wrow) chosen[i] = 1;
+      if (row0 + i == wrow) chosen[i] = 1 + k;
       if (pos[i] == k) pos[i] = big;
       else if (pos[i] == big) pos[i] = k;
     }
     if (tid == 0) Iloc[k] = (int)wrow;
     __syncthreads();
-    const double t = tau[0];
+    (void)pivnorm;
+    const double t = stau;
+    if (tid == 0) Rm[k + k * r] = sbeta;
     // update my remaining rows and downdate their norms
     for (int i = tid; i < nr; i += kMT) {
       if (chosen[i]) continue;
-      double* wi = W + i * r;
+      double* wi = W + i * ldw;
       if (r - k > 1 && t != 0.0) {
         double w = 0.0;
         for (int j = k + 1; j < r; ++j) w += vv[j] * wi[j];
@@ -175,83 +206,72 @@ __global__ void __launch_bounds__(kMT) maxvol_large_kernel(MaxvolLargeArgs a) {
     }
     __syncthreads();
   }
-  // ---------------- phase 2: swap rounds B = Q G^-1 (cur.cpp:100-114)
-  for (int swap = 0; swap <= a.max_swaps; ++swap) {
-    const int slot = (r + swap) & 1;
-    for (int e = tid; e < r * r; e += kMT) {
-      const int cc = e % r, t2 = e / r;
-      Gt[cc + t2 * r] = a.Q[Iloc[t2] + (int64_t)cc * a.ldq];
-    }
-    __syncthreads();
-    if (warp == 0) {
-      SmallColPiv q = warp_colpiv_qr(Gt, r, r, 1e-12, perm, tau, nu2, nd2);
-      if (lane == 0) {
-        sflag[1] = q.rank < r ? 1 : 0;
-        sflag[2] = q.nonzero_pivots;
-      }
-    }
-    __syncthreads();
-    if (sflag[1]) {
+  // rank() of ColPivQR(G^T) with threshold 1e-12 (cur.cpp:103-104): the R11
+  // diagonal is the same for every CTA, so the exit is grid-uniform.
+  {
+    const double pre = smaxpivot * 1e-12;
+    int rank = 0;
+    for (int k = 0; k < r; ++k) rank += fabs(Rm[k + k * r]) > pre ? 1 : 0;
+    if (rank < r) {
       if (b == 0 && tid == 0) *a.status = SLRA_ERR_SELECTION_FAILURE;
-      return;  // uniform across the grid: every CTA holds the same G
+      return;
     }
-    const int np = sflag[2];
+  }
+  // ---------------- phase 2: B = Q G^-1 for my rows (R11 back substitution
+  // of the reflected rows), then swap rounds with the rank-1 update
+  // B <- B - B[:,j] (B[i,:] - e_j) / B[i,j] after placing row i at slot j.
+  for (int i = tid; i < nr; i += kMT) {
+    double* c = W + i * ldw;
+    if (chosen[i]) {
+      const int pk = chosen[i] - 1;
+      for (int j = 0; j < r; ++j) c[j] = j == pk ? 1.0 : 0.0;
+      continue;
+    }
+    // (the last reflector has tau = 0: nothing left to apply)
+    for (int t2 = r - 1; t2 >= 0; --t2) {
+      double s = c[t2];
+      for (int u = t2 + 1; u < r; ++u) s -= Rm[t2 + u * r] * c[u];
+      c[t2] = s / Rm[t2 + t2 * r];
+    }
+  }
+  __syncthreads();
+  for (int swap = 0; swap <= a.max_swaps; ++swap) {
+    const int slot = (sync_no++) & 1;
+    // B.cwiseAbs().maxCoeff: column-major first maximum -> key j*m + row
     ArgMax best{-1.0, INT64_MAX};
-    for (int i = tid; i < nr; i += kMT) {
-      double c[kMR];
-      for (int j = 0; j < r; ++j) c[j] = a.Q[(row0 + i) + (int64_t)j * a.ldq];
-      for (int k = 0; k < np; ++k) {
-        const double t2 = tau[k];
-        if (r - k == 1) {
-          c[k] *= (1.0 - t2);
-        } else if (t2 != 0.0) {
-          double w = 0.0;
-          for (int j = k + 1; j < r; ++j) w += Gt[j + k * r] * c[j];
-          w += c[k];
-          c[k] -= t2 * w;
-          for (int j = k + 1; j < r; ++j) c[j] -= t2 * Gt[j + k * r] * w;
-        }
-      }
-      for (int t2 = np - 1; t2 >= 0; --t2) {
-        double s = c[t2];
-        for (int u = t2 + 1; u < np; ++u) s -= Gt[t2 + u * r] * c[u];
-        c[t2] = s / Gt[t2 + t2 * r];
-      }
-      for (int t2 = 0; t2 < r; ++t2) {
-        const double v = t2 < np ? fabs(c[t2]) : 0.0;
-        best = argmax_merge(best, ArgMax{v, (int64_t)perm[t2] * a.m + (row0 + i)});
-      }
+    for (int e = tid; e < nr * r; e += kMT) {
+      const int i = e / r, j = e - i * r;
+      best = argmax_merge(best, ArgMax{fabs(W[i * ldw + j]), (int64_t)j * a.m + (row0 + i)});
     }
     best = block_argmax<kMT>(best, rv, ri);
-    if (tid == 0) {
-      a.cand_v[slot * G + b] = best.v;
-      a.cand_pos[slot * G + b] = best.i;
-    }
+    const int64_t lrow = best.i == INT64_MAX ? -1 : (best.i % a.m);
+    publish(a, slot, G, b, best.v, best.i, lrow, lrow >= 0 ? W + (lrow - row0) * ldw : nullptr, r);
     grid.sync();
-    if (warp == 0) {
-      ArgMax g{-1.0, INT64_MAX};
-      for (int c = lane; c < G; c += 32) g = argmax_merge(g, ArgMax{a.cand_v[slot * G + c], a.cand_pos[slot * G + c]});
-      g = warp_argmax(g);
-      if (lane == 0) {
-        rv[0] = g.v;
-        ri[0] = g.i;
-      }
-    }
-    __syncthreads();
+    const int win = reduce_candidates(a, slot, G, rv, ri, sflag);
     const double mx = rv[0];
     const int64_t lin = ri[0];
-    __syncthreads();
     if (mx <= a.h || swap == a.max_swaps) break;
-    if (tid == 0) Iloc[lin / a.m] = (int)(lin % a.m);
+    const int j = (int)(lin / a.m);
+    const double* xv = a.cand_vec + (size_t)(slot * G + win) * kMR;
+    for (int c = tid; c < r; c += kMT) bi[c] = __ldcg(xv + c) - (c == j ? 1.0 : 0.0);
+    const double p = __ldcg(xv + j);
+    for (int i = tid; i < nr; i += kMT) fr[i] = W[i * ldw + j] / p;
+    if (tid == 0) Iloc[j] = (int)(lin % a.m);
+    __syncthreads();
+    for (int e = tid; e < nr * r; e += kMT) {
+      const int i = e / r, c = e - i * r;
+      W[i * ldw + c] -= fr[i] * bi[c];
+    }
     __syncthreads();
   }
   if (b == 0) {
     for (int t2 = tid; t2 < r; t2 += kMT) a.I_out[t2] = Iloc[t2];
     if (a.vol_out) {
-      for (int e = tid; e < r * r; e += kMT) Gt[(e % r) + (e / r) * r] = a.Q[Iloc[e % r] + (int64_t)(e / r) * a.ldq];
+      __syncthreads();
+      for (int e = tid; e < r * r; e += kMT) Rm[(e % r) + (e / r) * r] = a.Q[Iloc[e % r] + (int64_t)(e / r) * a.ldq];
       __syncthreads();
       if (tid < 32) {
-        const double dv = warp_abs_det(Gt, r, r);
+        const double dv = warp_abs_det(Rm, r, r);
         if (tid == 0) *a.vol_out = dv;
       }
     }
@@ -267,8 +287,8 @@ static int maxvol_large_grid(int num_sms, int64_t m) {
 }
 
 static size_t maxvol_large_smem() {
-  return sizeof(double) * ((size_t)kMRB * kMR + (size_t)kMR * kMR + kMR + 2 * kMRB + 3 * kMR + 40) +
-         sizeof(int64_t) * (40 + kMRB) + sizeof(int) * (kMRB + 2 * kMR) + 64;
+  return sizeof(double) * ((size_t)kMRB * (kMR + 1) + (size_t)kMR * kMR + kMR + 3 * kMRB + kMR + 40) +
+         sizeof(int64_t) * (40 + kMRB) + sizeof(int) * (kMRB + kMR) + 64;
 }
 
 // Grid-wide maxvol over an orthonormal m x r basis Q (device), r <= 64.
