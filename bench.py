@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--blocks", type=int, default=65536, help="config 5 block count")
@@ -227,14 +227,19 @@ def main():
 
     flush_buf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 256 MiB > L2
 
+    from paper_1611_01391_b200 import shard
+    comm = shard.Comm(dist)
     if args.config == 2:
         work = Config2(slra, torch, args.seed + rank)
     elif args.config == 3:
-        work = Config3(slra, torch, args.seed + rank)
+        work = Config3(slra, torch, args.seed) if ws == 1 else Config3Sharded(slra, torch, args.seed, comm)
+    elif args.config == 4:
+        work = Config4(slra, torch, args.seed, comm)
     elif args.config == 1:
         work = Config1(slra, torch, args.seed + rank)
     else:
-        work = Config5(slra, torch, args.seed + rank, args.blocks)
+        work = Config5(slra, torch, args.seed, args.blocks, comm)
+    scaling = getattr(work, "scaling", "weak")
 
     for _ in range(args.warmup):
         work.step()
@@ -259,7 +264,8 @@ def main():
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = work.entries_per_step * args.steps * ws / (ms_max * 1e-3)
+    # weak: every rank runs its own replica; strong: the ranks share one job
+    value = work.entries_per_step * args.steps * (ws if scaling == "weak" else 1) / (ms_max * 1e-3)
 
     # ---- per-kernel device times over the same K steps (instrumented pass)
     slra.set_timing(True)
@@ -272,15 +278,15 @@ def main():
     roofline, kernels = work.roofline(fam, peaks, args.steps)
 
     # ---- end-to-end through the reference-facing API with host buffers
-    e2e = work.e2e(args.steps, args.warmup)
+    e2e = work.e2e(args.steps, args.warmup) if ws == 1 or scaling == "weak" else None
 
     line = {
         "metric": "LRA matrix entries/s (sketch+CUR+residual)", "value": value, "unit": "entries/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded; same recipe as BASELINE.json config)",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": getattr(work, "data", "synthetic (seeded; same recipe as BASELINE.json config)"),
         "config": dict(work.config, l2="256 MiB flush between timed steps (outside the event pairs)",
-                       parallelism=f"replicas x{ws} (no data-path collective)"),
+                       parallelism=getattr(work, "parallelism", f"replicas x{ws} (no data-path collective)")),
         "roofline": roofline, "kernels_ms_per_step": kernels,
         "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
         "residual_rel": work.last_residual_rel(),
@@ -568,41 +574,247 @@ class Config3:
                           "cur_evaluate) through the oracle/ C++ restatement, OpenMP", "seconds": dt}
 
 
+class Config3Sharded:
+    """Config 3 row-sharded over the torchrun ranks (shard.cross_approx): total
+    work fixed (16384^2), each rank holds m/N rows -> scaling "strong"."""
+
+    scaling = "strong"
+
+    def __init__(self, slra, torch, seed, comm):
+        from paper_1611_01391_b200 import shard
+        self.slra, self.torch, self.shard, self.comm = slra, torch, shard, comm
+        x, y = config3_points(slra, seed)
+        self.row0, self.mloc = shard.split(N3, comm.world, comm.rank)
+        xd = torch.tensor(x[self.row0:self.row0 + self.mloc], dtype=torch.float64, device="cuda")
+        yd = torch.tensor(y, dtype=torch.float64, device="cuda")
+        self.At = (1.0 / (xd[None, :] - yd[:, None])).contiguous()  # (n, m_local): local rows, column-major
+        self.init = slra.Rng(seed + 1).distinct_indices(K3, N3)
+        self.ops = shard.DeviceOps(slra, torch)
+        self.res = None
+        self.entries_per_step = N3 * N3
+        self.parallelism = f"row-sharded x{comm.world}: allreduce(A(I,:)) + allgather(A(:,J)) per sweep, " \
+                           f"allreduce of the residual partials (NCCL)"
+        self.config = {"workload": "config3: C-A CUR of the 16384x16384 fp64 Cauchy block 1/(x-y), k=l=64, "
+                                   "5 sweeps, adaptive r, full ||A-CUR||_F, row-sharded",
+                       "entries_per_step": self.entries_per_step, "m": N3, "n": N3, "k": K3, "l": K3,
+                       "loops": LOOPS3, "rows_per_rank": self.mloc}
+
+    def step(self):
+        self.res = self.shard.cross_approx(self.ops, self.comm, self.At, self.row0, N3, 0, K3, K3, self.init,
+                                           LOOPS3, 1.1, self.torch)
+
+    def last_residual_rel(self):
+        return {"rel": (self.res.resid_sq / self.res.norm_sq) ** 0.5, "r": self.res.r}
+
+    def roofline(self, fam, peaks, steps):
+        return Config3.roofline(self, fam, peaks, steps)
+
+    @property
+    def r(self):
+        return self.res.r if self.res else 1
+
+    def e2e(self, steps, warmup):
+        return None
+
+    def cpu_baseline(self):
+        return None
+
+
+M4, D4, K4 = 1 << 20, 256, 4096
+
+
+class Config4:
+    """Config 4: sketched LSR, A 2^20 x 256 Gaussian, b = A x0 + 1e-6 e; 4096
+    rows sampled (a) uniformly, (b) by a sparse +-1 sketch with 2 nonzeros
+    per row; solve + ||A x_hat - b||. One step = both samplers (2 x m(d+1)
+    entries). N > 1: rows sharded, one allreduce of the sketch (shard.py)."""
+
+    CHUNK = 4096
+
+    def __init__(self, slra, torch, seed, comm):
+        from paper_1611_01391_b200 import shard
+        self.slra, self.torch, self.shard, self.comm = slra, torch, shard, comm
+        ws = comm.world
+        self.scaling = "weak" if ws == 1 else "strong"
+        self.row0, self.mloc = shard.split(M4, ws, comm.rank)
+        # device-side seeded Gaussians, generated per 4096-row chunk so every
+        # rank builds exactly its rows of the same global A, b
+        gx = torch.Generator(device="cuda").manual_seed(seed * 1000003 + 7)
+        self.x0 = torch.randn(D4, dtype=torch.float64, device="cuda", generator=gx)
+        self.At = torch.empty(D4, self.mloc, dtype=torch.float64, device="cuda")  # (d, m_local) column-major
+        self.b = torch.empty(self.mloc, dtype=torch.float64, device="cuda")
+        c0 = self.row0 // self.CHUNK
+        for c in range(c0, c0 + (self.mloc + self.CHUNK - 1) // self.CHUNK):
+            g = torch.Generator(device="cuda").manual_seed(seed * 1000003 + 11 + c)
+            blk = torch.randn(self.CHUNK, D4, dtype=torch.float64, device="cuda", generator=g)  # rows x d
+            e = torch.randn(self.CHUNK, dtype=torch.float64, device="cuda", generator=g)
+            lo = c * self.CHUNK - self.row0
+            self.At[:, lo:lo + self.CHUNK] = blk.T
+            self.b[lo:lo + self.CHUNK] = blk @ self.x0 + 1e-6 * e
+        ru = slra.Rng(slra.Rng.derive_seed(seed, 41))
+        Fu = slra.make_sub_identity(ru.distinct_indices(K4, M4), M4)
+        rs = slra.Rng(slra.Rng.derive_seed(seed, 42))
+        Fs = slra.make_product([slra.make_sub_identity(rs.distinct_indices(K4, M4), M4),
+                                slra.gen_sparse_circulant(M4, 2, rs), slra.gen_sign_diagonal(M4, rs)])
+        self.ops_host = [("uniform_rows", Fu), ("sparse_pm1_s2", Fs)]
+        self.plans = []
+        for name, F in self.ops_host:
+            p = F.plan("left")
+            self.plans.append((name, p, dict(src=torch.tensor(p["src"], dtype=torch.int64, device="cuda"),
+                                              coef=torch.tensor(p["coef"], dtype=torch.float64, device="cuda"),
+                                              q=torch.tensor(p["q"], dtype=torch.int32, device="cuda"))))
+        self.x = [torch.zeros(D4, dtype=torch.float64, device="cuda") for _ in self.plans]
+        self.out = torch.zeros(len(self.plans), 2, dtype=torch.float64, device="cuda")
+        self.sres = [0.0] * len(self.plans)
+        self.tres = [0.0] * len(self.plans)
+        self.dev_ops = shard.DeviceOps(slra, torch)
+        self.entries_per_step = 2 * M4 * (D4 + 1)
+        self.data = "synthetic (seeded torch Gaussians on the device, config-4 shapes and noise 1e-6)"
+        if ws > 1:
+            self.parallelism = f"row-sharded x{ws}: per-rank sketch contributions + one allreduce (NCCL)"
+        self.config = {"workload": "config4: sketched LSR, A 1048576x256 fp64 Gaussian, b = A x0 + 1e-6 e, "
+                                   "4096 rows: uniform sampling and sparse +-1 (s=2); solve + ||A x - b||",
+                       "entries_per_step": self.entries_per_step, "m": M4, "d": D4, "k": K4,
+                       "rows_per_rank": self.mloc}
+
+    def step(self):
+        s = self.slra
+        if self.comm.world == 1:
+            for i, (_, p, d) in enumerate(self.plans):
+                self.sres[i] = s.sketch_solve_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(),
+                                                     d["src"].data_ptr(), d["coef"].data_ptr(), d["q"].data_ptr(),
+                                                     p["width"], p["tree"], K4, self.x[i].data_ptr())
+                s.lsr_residual_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(), self.x[i].data_ptr(),
+                                      self.out[i].data_ptr())
+        else:
+            for i, (_, p, d) in enumerate(self.plans):
+                x, self.sres[i], self.tres[i] = self.shard.sketch_solve(
+                    self.dev_ops, self.comm, self.At, self.b, self.row0, D4, d["src"], d["coef"], p["width"], K4,
+                    self.torch)
+                self.x[i] = x
+
+    def last_residual_rel(self):
+        torch = self.torch
+        bn = self.b.norm().item()
+        out = {}
+        for i, (name, _, _) in enumerate(self.plans):
+            tres = self.out[i, 0].item() ** 0.5 if self.comm.world == 1 else self.tres[i]
+            out[name] = {"sketched_residual": self.sres[i], "true_residual": tres, "rel_to_b": tres / bn}
+        if self.comm.world == 1:
+            # residual ratio against the exact LS solution (certification, untimed)
+            src = torch.arange(M4, dtype=torch.int64, device="cuda")
+            coef = torch.ones(M4, dtype=torch.float64, device="cuda")
+            q = torch.zeros(M4, dtype=torch.int32, device="cuda")
+            xe = torch.zeros(D4, dtype=torch.float64, device="cuda")
+            self.slra.sketch_solve_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(), src.data_ptr(),
+                                          coef.data_ptr(), q.data_ptr(), 1, 0, M4, xe.data_ptr())
+            o = torch.zeros(2, dtype=torch.float64, device="cuda")
+            self.slra.lsr_residual_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(), xe.data_ptr(),
+                                          o.data_ptr())
+            opt = o[0].item() ** 0.5
+            for name in out:
+                out[name]["ratio_vs_exact"] = out[name]["true_residual"] / opt
+        return out
+
+    def roofline(self, fam, peaks, steps):
+        kernels = {k: v[0] / steps for k, v in fam.items()}
+        per = {k: v[0] / max(v[1], 1) for k, v in fam.items()}
+        top = max(fam.items(), key=lambda kv: kv[1][0])[0]
+        byts = {"lsr_residual": 8.0 * self.mloc * (D4 + 1), "sketch": 8.0 * K4 * 2 * (D4 + 1) * 1.5,
+                "gemm": 8.0 * K4 * (D4 + 1)}
+        b = byts.get(top, 8.0 * self.mloc * (D4 + 1))
+        ach = b / (per[top] * 1e-3) / 1e9
+        rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+              "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+              "algorithmic_bytes_per_launch": b, "traffic": None}
+        return rl, kernels
+
+    def e2e(self, steps, warmup):
+        torch = self.torch
+        Ah = torch.empty(M4 * D4, dtype=torch.float64, pin_memory=True)
+        Ah.copy_(self.At.reshape(-1))
+        bh = torch.empty(M4, dtype=torch.float64, pin_memory=True)
+        bh.copy_(self.b)
+
+        def one():
+            for _, F in self.ops_host:
+                self.slra.sketch_solve_host(Ah.data_ptr(), bh.data_ptr(), M4, D4, F)
+        one()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        return {"value": self.entries_per_step * steps / dt, "unit": "entries/s",
+                "h2d_bytes_per_step": 2 * 8 * M4 * (D4 + 1), "d2h_bytes_per_step": 2 * 8 * (D4 + 2),
+                "api": "paper_1611_01391_b200.sketch_solve_host -> slra_sketch_solve + slra_lsr_residual "
+                       "(host pinned A|b in, x_hat and residuals out, once per sampler)"}
+
+    def cpu_baseline(self):
+        sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))
+        import _oracle as oracle
+        cores = os.cpu_count() or 1
+        A = self.At.cpu().numpy().T  # (m, d) Fortran
+        b = self.b.cpu().numpy()
+        ru = oracle.Rng(oracle.Rng.derive_seed(0, 41))
+        F = oracle.make_sub_identity(ru.distinct_indices(K4, M4), M4)
+        t0 = time.perf_counter()
+        rep = oracle.sketch_solve(A, b, F, False)
+        oracle.residual_norm(A, b, rep["x_hat"])
+        dt = time.perf_counter() - t0
+        return {"value": M4 * (D4 + 1) / dt, "unit": "entries/s", "cores": cores, "kind": "port",
+                "sample": "one config-4 sampler (uniform rows): oracle sketch_solve (ColPivHouseholderQR of "
+                          "the 4096x256 sketch) + residual_norm over the full A", "seconds": dt}
+
+
 class Config5:
     """Config 5: batched superfast-multipole LRA, 256x256 log-kernel blocks, k=l=32, adaptive r<=16, 2 sweeps."""
 
-    def __init__(self, slra, torch, seed, blocks):
+    CHUNK = 4096
+
+    def __init__(self, slra, torch, seed, blocks, comm):
+        from paper_1611_01391_b200 import shard
         self.slra, self.torch = slra, torch
-        self.nb = blocks
+        ws = comm.world
+        self.b0, self.nb = shard.split(blocks, ws, comm.rank)
+        self.scaling = "weak" if ws == 1 else "strong"
+        if ws > 1:
+            self.parallelism = f"block-split x{ws}: {self.nb} blocks per rank, no communication"
         m = 256
-        # device-side generation of the blocks from per-block seeded points
-        # (points drawn on the host with the reference Rng, kernel evaluated on
-        # the GPU: log differs from glibc's in the last ulp; parity tests use
-        # host-generated blocks)
-        g = torch.Generator().manual_seed(seed)
-        P = torch.rand(blocks, m, 2, dtype=torch.float64, generator=g)
-        Q = torch.rand(blocks, m, 2, dtype=torch.float64, generator=g)
-        Q[..., 0] += 4.0
-        self.A = torch.empty(blocks, m, m, dtype=torch.float64, device="cuda")
-        for b0 in range(0, blocks, 4096):
-            p = P[b0:b0 + 4096].cuda()
-            q = Q[b0:b0 + 4096].cuda()
+        # device-side generation of the blocks from seeded points, per chunk
+        # of 4096 blocks so every rank builds exactly its blocks of the same
+        # global set (log on the GPU differs from glibc's in the last ulp;
+        # parity tests use host-generated blocks)
+        self.A = torch.empty(self.nb, m, m, dtype=torch.float64, device="cuda")
+        self.init = torch.empty(self.nb, 32, dtype=torch.int64, device="cuda")
+        c_lo, c_hi = self.b0 // self.CHUNK, (self.b0 + self.nb + self.CHUNK - 1) // self.CHUNK
+        for c in range(c_lo, c_hi):
+            g = torch.Generator().manual_seed(seed * 1000003 + c)
+            P = torch.rand(self.CHUNK, m, 2, dtype=torch.float64, generator=g)
+            Q = torch.rand(self.CHUNK, m, 2, dtype=torch.float64, generator=g)
+            Q[..., 0] += 4.0
+            init = torch.argsort(torch.rand(self.CHUNK, m, generator=g), dim=1)[:, :32]
+            lo, hi = max(self.b0, c * self.CHUNK), min(self.b0 + self.nb, (c + 1) * self.CHUNK)
+            if lo >= hi:
+                continue
+            p = P[lo - c * self.CHUNK:hi - c * self.CHUNK].cuda()
+            q = Q[lo - c * self.CHUNK:hi - c * self.CHUNK].cuda()
             d = p[:, None, :, :] - q[:, :, None, :]  # [b, j, i, 2] -> A^T[j, i] = K(i, j): col-major K
-            self.A[b0:b0 + 4096] = 0.5 * torch.log((d * d).sum(-1))
-        inits = torch.stack([torch.randperm(m, generator=g)[:32] for _ in range(min(blocks, 1))])
-        self.init = torch.stack([torch.randperm(m, generator=g)[:32] for _ in range(blocks)]).cuda()
-        self.I = torch.zeros(blocks, 32, dtype=torch.int64, device="cuda")
-        self.J = torch.zeros(blocks, 32, dtype=torch.int64, device="cuda")
-        self.U = torch.zeros(blocks, 32 * 32, dtype=torch.float64, device="cuda")
-        self.r = torch.zeros(blocks, dtype=torch.int64, device="cuda")
-        self.st = torch.zeros(blocks, dtype=torch.int32, device="cuda")
-        self.rs = torch.zeros(blocks, dtype=torch.float64, device="cuda")
-        self.ns = torch.zeros(blocks, dtype=torch.float64, device="cuda")
-        self.entries_per_step = blocks * m * m
+            self.A[lo - self.b0:hi - self.b0] = 0.5 * torch.log((d * d).sum(-1))
+            self.init[lo - self.b0:hi - self.b0] = init[lo - c * self.CHUNK:hi - c * self.CHUNK].cuda()
+        nb = self.nb
+        self.I = torch.zeros(nb, 32, dtype=torch.int64, device="cuda")
+        self.J = torch.zeros(nb, 32, dtype=torch.int64, device="cuda")
+        self.U = torch.zeros(nb, 32 * 32, dtype=torch.float64, device="cuda")
+        self.r = torch.zeros(nb, dtype=torch.int64, device="cuda")
+        self.st = torch.zeros(nb, dtype=torch.int32, device="cuda")
+        self.rs = torch.zeros(nb, dtype=torch.float64, device="cuda")
+        self.ns = torch.zeros(nb, dtype=torch.float64, device="cuda")
+        self.entries_per_step = blocks * m * m  # the whole job (all ranks)
         self.config = {"workload": f"config5: {blocks} batched 256x256 log-kernel blocks, k=l=32, adaptive r "
                                    f"(numerical_rank 1e-10), 2 C-A sweeps + per-block residual",
-                       "entries_per_step": self.entries_per_step}
-        del inits
+                       "entries_per_step": self.entries_per_step, "blocks_per_rank": nb}
 
     def step(self):
         self.slra.cross_approx_batched_device(self.A.data_ptr(), 256, 256 * 256, self.nb, 256, 256, 0, 32, 32,

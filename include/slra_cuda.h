@@ -98,6 +98,16 @@ int slra_sketch_cols(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, in
 int slra_sketch_rows(slra_ctx ctx, const double* d_W, int64_t ldw, int64_t m, int64_t ncols,
                      const int64_t* d_src, const double* d_coef, const int32_t* d_q,
                      int64_t width, int tree, int64_t k, double* d_out, int64_t ldo);
+/* Row-sharded LIST-order sketch / gather:
+ * d_W holds rows [row0, row0 + m_local) of the full W (ld ldw); src holds
+ * GLOBAL row indices. Terms from rows held elsewhere are skipped, so the sum
+ * over ranks (NCCL allreduce) equals slra_sketch_rows on the full W —
+ * bit-exactly for width <= 2. transpose = 1 writes the ncols x k transpose
+ * (the n x k strip A(I,:)^T that select_rows_spanning factorises). */
+int slra_sketch_rows_shard(slra_ctx ctx, const double* d_W, int64_t ldw, int64_t row0,
+                           int64_t m_local, int64_t ncols, const int64_t* d_src,
+                           const double* d_coef, int64_t width, int64_t k, double* d_out,
+                           int64_t ldo, int transpose);
 
 /* ------------------------------------------------------------ a4/a8 small dense
  * thin_qr (linalg.cpp:67-79): Householder QR, R(i,i) >= 0, explicit thin Q.
@@ -112,11 +122,14 @@ int slra_svd(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
 
 /* ------------------------------------------------------------ a5/a6 pivoting
  * maxvol_rows (cur.cpp:88-116) on a tall A (m x r): ColPivHouseholderQR(A^T)
- * init + <= max_swaps+1 swap rounds. max_swaps = 0 means 4r. */
+ * init + <= max_swaps+1 swap rounds. max_swaps = 0 means 4r. r <= 64; A that
+ * does not fit one SM runs the grid-wide cooperative kernel. */
 int slra_maxvol_rows(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t r,
                      double h, int64_t max_swaps, int64_t* d_idx);
-/* select_rows_spanning (cur.cpp:118-135) for count == A.cols() (no padding):
- * thin_qr + maxvol; optionally |det Q[idx,:]| (cur.cpp:192-197). */
+/* select_rows_spanning (cur.cpp:118-135): thin_qr + maxvol (+ the padding
+ * rows when count > c, strips up to 256 rows); optionally |det Q[idx,:]|
+ * (cur.cpp:192-197). Taller strips (count == c <= 64): TSQR + grid-wide
+ * maxvol. */
 int slra_select_rows_spanning(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m,
                               int64_t c, int64_t count, double h, int64_t* d_idx,
                               double* d_volume);
@@ -218,6 +231,11 @@ int slra_sketch_solve(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, i
                       const double* d_b, const int64_t* d_src, const double* d_coef,
                       const int32_t* d_q, int64_t width, int tree, int64_t k, double* d_x_hat,
                       double* h_sketched_residual);
+/* The solve half of sketch_solve (lsr.cpp:52-60) for an already sketched
+ * system FW = (FA | Fb), k x (d+1), ld k — the row-sharded path (config 4)
+ * all-reduces the per-rank sketch contributions and then calls this. */
+int slra_lsr_solve_sketched(slra_ctx ctx, const double* d_FW, int64_t ldfw, int64_t k, int64_t d,
+                            double* d_x_hat, double* h_sketched_residual);
 /* residual_norm (lsr.cpp:26-28): ||A x - b||^2 into d_out[0] (device). */
 int slra_lsr_residual(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
                       const double* d_b, const double* d_x, double* d_out);

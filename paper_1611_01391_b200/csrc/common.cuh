@@ -34,7 +34,8 @@ struct Context {
   // pinned host mirror of dsmall for status read-back
   void* hsmall = nullptr;
   // independent growable device arenas for multi-kernel orchestrations
-  // (0: range finder, 1: cur residual, 2: lsr, 3: svd/transpose, 4: large C-A, 5: factored residual)
+  // (0: range finder, 1: cur residual, 2: lsr, 3: svd, 4: large C-A, 5: factored residual,
+  //  6: wide-svd transpose, 7: tall maxvol/select)
   void* arena[8] = {};
   size_t arena_bytes[8] = {};
   // opt-in per-kernel-family timing (CUDA events on the context stream)

@@ -429,7 +429,7 @@ int launch_svd(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, 
   if (m < n) {
     // wide: A^T = S' Sigma T'^T (tall path), so A = T' Sigma S'^T; the sign
     // rule is then re-applied on the left vectors T' (flipping S' with them).
-    double* At = static_cast<double*>(arena(cx, 3, sizeof(double) * (size_t)m * n));
+    double* At = static_cast<double*>(arena(cx, 6, sizeof(double) * (size_t)m * n));  // slot 3 is the tall path's
     if (!At) return SLRA_ERR_CUDA;
     SLRA_TRY(launch_transpose(cx, A, lda, m, n, At, n));
     SLRA_TRY(launch_svd(cx, At, n, n, m, T, ldt, sigma, S, lds));
@@ -545,6 +545,34 @@ int launch_maxvol(Context* cx, const double* A, int64_t lda, int64_t m, int64_t 
   return *static_cast<int32_t*>(cx->hsmall);
 }
 
+size_t maxvol_large_scratch_doubles(int num_sms, int64_t m);
+int launch_maxvol_large(Context* cx, const double* Q, int64_t ldq, int64_t m, int r, double h, int max_swaps,
+                        int64_t* d_idx, double* d_vol, double* scratch);
+
+// maxvol / select_rows_spanning on strips taller than one SM: (TSQR when
+// qr_first) then the grid-wide maxvol; blocks until the status is known.
+int launch_maxvol_tall(Context* cx, const double* A, int64_t lda, int64_t m, int r, double h, int max_swaps,
+                       int64_t* idx, double* vol, bool qr_first) {
+  const size_t tw = qr_first ? tsqr_workspace_doubles(m, r) : 0;
+  const size_t mvs = maxvol_large_scratch_doubles(cx->num_sms, m);
+  const size_t qsz = qr_first ? (size_t)m * r + (size_t)r * r : 0;
+  double* buf = static_cast<double*>(arena(cx, 7, sizeof(double) * (qsz + tw + mvs + 64)));
+  if (!buf) return SLRA_ERR_CUDA;
+  const double* Q = A;
+  int64_t ldq = lda;
+  if (qr_first) {
+    double* Qm = buf;
+    SLRA_TRY(launch_thin_qr_batched(cx, A, lda, 0, m, r, Qm, m, 0, Qm + (size_t)m * r, r, 0, 1,
+                                    tw ? buf + qsz : nullptr));
+    Q = Qm;
+    ldq = m;
+  }
+  SLRA_TRY(launch_maxvol_large(cx, Q, ldq, m, r, h, max_swaps, idx, vol, buf + qsz + tw));
+  SLRA_CUDA(cudaMemcpyAsync(cx->hsmall, cx->dsmall, 4, cudaMemcpyDeviceToHost, cx->stream));
+  SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+  return *static_cast<int32_t*>(cx->hsmall);
+}
+
 }  // namespace slra_dev
 
 using namespace slra_dev;
@@ -568,14 +596,20 @@ int slra_maxvol_rows(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int6
                      int64_t* idx) {
   if (!ctx || r < 1 || m < r || lda < m || h < 1.0) return SLRA_ERR_INVALID_ARGUMENT;
   if (max_swaps == 0) max_swaps = 4 * r;
-  return launch_maxvol(C(ctx), A, lda, m, r, h, max_swaps, 0, r, idx, nullptr);
+  const int st = launch_maxvol(C(ctx), A, lda, m, r, h, max_swaps, 0, r, idx, nullptr);
+  if (st != SLRA_ERR_UNSUPPORTED || r > 64) return st;
+  return launch_maxvol_tall(C(ctx), A, lda, m, (int)r, h, (int)max_swaps, idx, nullptr, false);
 }
 
 int slra_select_rows_spanning(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t c, int64_t count,
                               double h, int64_t* idx, double* vol) {
   if (!ctx || count > m || m < c || c < 1 || lda < m) return SLRA_ERR_INVALID_ARGUMENT;
   const int64_t rq = count < c ? count : c;
-  return launch_maxvol(C(ctx), A, lda, m, c, h, 4 * rq, 1, count, idx, vol);
+  const int st = launch_maxvol(C(ctx), A, lda, m, c, h, 4 * rq, 1, count, idx, vol);
+  // tall strips (config 3 and the row-sharded path): TSQR + grid-wide maxvol;
+  // the padding branch (count > c, cur.cpp:125-134) is not needed there
+  if (st != SLRA_ERR_UNSUPPORTED || c > 64 || count != c) return st;
+  return launch_maxvol_tall(C(ctx), A, lda, m, (int)c, h, (int)(4 * c), idx, vol, true);
 }
 
 }  // extern "C"

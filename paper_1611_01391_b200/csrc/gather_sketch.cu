@@ -173,6 +173,34 @@ __global__ void __launch_bounds__(kNT) sketch_rows_list_kernel(const double* __r
   }
 }
 
+// Row-sharded form of the LIST-order sketch (width 1 = gather): this rank
+// holds rows [row0, row0 + mloc) of W; terms whose source row lives on
+// another rank are skipped, so summing the per-rank outputs (NCCL
+// allreduce) reproduces the full combination — bit-exactly for width <= 2,
+// where every output is one or two terms plus exact zeros. transpose = 1
+// writes out(j, t) (ncols x k) instead of out(t, j).
+__global__ void __launch_bounds__(kNT) sketch_rows_shard_kernel(const double* __restrict__ Wm, int64_t ldw,
+                                                                int64_t row0, int64_t mloc, int64_t ncols,
+                                                                const int64_t* __restrict__ src,
+                                                                const double* __restrict__ coef, int64_t w,
+                                                                int64_t k, double* __restrict__ out, int64_t ldo,
+                                                                int transpose) {
+  const int64_t total = k * ncols;
+  for (int64_t e = blockIdx.x * (int64_t)kNT + threadIdx.x; e < total; e += (int64_t)gridDim.x * kNT) {
+    const int64_t t = transpose ? e / ncols : e % k, j = transpose ? e % ncols : e / k;
+    double acc = 0.0;
+    bool first = true;
+    for (int64_t s = 0; s < w; ++s) {
+      const int64_t r = src[t * w + s] - row0;
+      if (r < 0 || r >= mloc) continue;
+      const double term = coef[t * w + s] * __ldg(Wm + r + j * ldw);
+      acc = first ? term : acc + term;
+      first = false;
+    }
+    out[transpose ? j + t * ldo : t + j * ldo] = acc;
+  }
+}
+
 static int grid_1d(const Context* c, int64_t work) {
   const int64_t per = kNT * 4;
   int64_t g = (work + per - 1) / per;
@@ -258,6 +286,7 @@ int launch_sketch_rows(Context* c, const double* Wm, int64_t ldw, int64_t ncols,
   const int g = grid_1d(c, k * ncols);
   cudaStream_t s = c->stream;
   if (tree == SLRA_TREE_FWHT) {
+    KernelTimer kt(c, "sketch");
     switch (width) {
       case 1: sketch_rows_kernel<1, SLRA_TREE_FWHT><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
       case 2: sketch_rows_kernel<2, SLRA_TREE_FWHT><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
@@ -267,6 +296,7 @@ int launch_sketch_rows(Context* c, const double* Wm, int64_t ldw, int64_t ncols,
       default: return SLRA_ERR_UNSUPPORTED;
     }
   } else {
+    KernelTimer kt(c, "sketch");
     switch (width) {
       case 1: sketch_rows_kernel<1, SLRA_TREE_LIST><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
       case 2: sketch_rows_kernel<2, SLRA_TREE_LIST><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
@@ -322,6 +352,19 @@ int slra_sketch_rows(slra_ctx ctx, const double* Wm, int64_t ldw, int64_t m, int
   if (tree == SLRA_TREE_FWHT && (width & (width - 1))) return SLRA_ERR_INVALID_ARGUMENT;
   if (k == 0 || ncols == 0) return SLRA_OK;
   return launch_sketch_rows(C(ctx), Wm, ldw, ncols, src, coef, q, width, tree, k, out, ldo);
+}
+
+int slra_sketch_rows_shard(slra_ctx ctx, const double* Wm, int64_t ldw, int64_t row0, int64_t mloc, int64_t ncols,
+                           const int64_t* src, const double* coef, int64_t width, int64_t k, double* out,
+                           int64_t ldo, int transpose) {
+  if (!ctx || ldw < mloc || mloc < 0 || row0 < 0 || width < 1 || k < 0 || ncols < 0) return SLRA_ERR_INVALID_ARGUMENT;
+  if (ldo < (transpose ? ncols : k)) return SLRA_ERR_INVALID_ARGUMENT;
+  if (k == 0 || ncols == 0) return SLRA_OK;
+  Context* c = C(ctx);
+  SLRA_TIMED(c, "sketch", sketch_rows_shard_kernel<<<grid_1d(c, k * ncols), kNT, 0, c->stream>>>(
+                              Wm, ldw, row0, mloc, ncols, src, coef, width, k, out, ldo, transpose);)
+  SLRA_CHECK_LAUNCH(c);
+  return SLRA_OK;
 }
 
 }  // extern "C"

@@ -4,7 +4,7 @@
 // Device formulation: FW = F (A|b) through a compiled left plan (one pass,
 // only the k sampled/sketched rows are touched), the Gram matrix
 // [FA Fb]^T [FA Fb] on the DMMA GEMM (split-K, deterministic), a blocked
-// Cholesky of FA^T FA in one CTA (left-looking, 32-column panels), two
+// Cholesky of FA^T FA in one CTA (right-looking, 32-column panels), two
 // triangular solves, one step of iterative refinement, and the sketched
 // residual ||FA x - Fb|| by a direct pass (never from the Gram identity).
 // Rank test: a Cholesky pivot that is non-positive or below
@@ -23,102 +23,169 @@ int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, dou
 constexpr int kLT = 512;
 constexpr int kPW = 32;  // Cholesky panel width
 
-// In-place lower Cholesky of G (d x d, ld d, global/L2), one CTA.
+// In-place lower Cholesky of G (d x d, ld d, global/L2), one CTA,
+// right-looking with 32-column panels. The panel is factorised in shared
+// memory with one thread per row (no index arithmetic in the inner loops),
+// written back, and the trailing lower triangle is updated
+// G22 -= L21 L21^T with L21 read from shared memory.
 // status[0] = 0 ok, 1 rank failure.
 __global__ void __launch_bounds__(kLT) cholesky_kernel(double* __restrict__ G, int d, double tol2,
                                                        int32_t* __restrict__ status) {
-  extern __shared__ __align__(16) double P[];  // d x kPW panel (ld d)
+  extern __shared__ __align__(16) double P[];  // rows x kPW panel, ld = d + 1 (odd: row-threads conflict-free)
   __shared__ int fail;
   const int tid = threadIdx.x;
+  const int ldp = d + 1;
   if (tid == 0) fail = 0;
   for (int p0 = 0; p0 < d; p0 += kPW) {
     const int pw = (d - p0) < kPW ? (d - p0) : kPW;
     const int rows = d - p0;
-    // load panel G[p0:d, p0:p0+pw] and subtract L[p0:d, 0:p0] L[p0:p0+pw, 0:p0]^T
-    for (int e = tid; e < rows * pw; e += kLT) {
-      const int i = e % rows, c = e / rows;
-      if (i < c) {
-        P[i + c * d] = 0.0;
-        continue;
-      }
-      const double* Li = G + (p0 + i);
-      const double* Lc = G + (p0 + c);
-      double acc = G[(p0 + i) + (int64_t)(p0 + c) * d];
-      for (int t = 0; t < p0; ++t) acc -= Li[(int64_t)t * d] * Lc[(int64_t)t * d];
-      P[i + c * d] = acc;
+    for (int i = tid; i < rows; i += kLT) {  // all 32 loads of a row in flight at once
+      double g[kPW];
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) g[c] = (c < pw && i >= c) ? G[(p0 + i) + (int64_t)(p0 + c) * d] : 0.0;
+#pragma unroll
+      for (int c = 0; c < kPW; ++c)
+        if (c < pw) P[i + c * ldp] = g[c];
     }
     __syncthreads();
-    // unblocked factorisation of the panel
     for (int j = 0; j < pw; ++j) {
-      const double piv = P[j + j * d];
-      if (!(piv > tol2)) {
+      const double piv = P[j + j * ldp];
+      if (!(piv > tol2)) {  // uniform: every thread read the same pivot
         if (tid == 0) fail = 1;
-        __syncthreads();
         break;
       }
       const double ljj = sqrt(piv);
+      __syncthreads();  // everyone has read the pivot before column j is scaled
+      for (int i = j + tid; i < rows; i += kLT) P[i + j * ldp] = (i == j) ? ljj : P[i + j * ldp] / ljj;
       __syncthreads();
-      for (int i = j + tid; i < rows; i += kLT) P[i + j * d] = (i == j) ? ljj : P[i + j * d] / ljj;
-      __syncthreads();
-      for (int e = tid; e < rows * (pw - j - 1); e += kLT) {
-        const int i = e % rows, c = j + 1 + e / rows;
-        if (i >= c) P[i + c * d] -= P[i + j * d] * P[c + j * d];
+      // update my row of the remaining panel columns
+      for (int i = j + 1 + tid; i < rows; i += kLT) {
+        const double lij = P[i + j * ldp];
+        const int cmax = i < pw - 1 ? i : pw - 1;
+        for (int c = j + 1; c <= cmax; ++c) P[i + c * ldp] -= lij * P[c + j * ldp];
       }
       __syncthreads();
     }
+    __syncthreads();
     if (fail) break;
-    for (int e = tid; e < rows * pw; e += kLT) {
-      const int i = e % rows, c = e / rows;
-      G[(p0 + i) + (int64_t)(p0 + c) * d] = P[i + c * d];
+    for (int c = 0; c < pw; ++c)
+      for (int i = c + tid; i < rows; i += kLT) G[(p0 + i) + (int64_t)(p0 + c) * d] = P[i + c * ldp];
+    // trailing lower triangle: thread pair (row i, column parity) walks columns
+    const int tr = rows - pw;
+    for (int e = tid; e < 2 * tr; e += kLT) {
+      const int i = pw + (e >> 1), par = e & 1;
+      double li[kPW];
+#pragma unroll
+      for (int t = 0; t < kPW; ++t) li[t] = t < pw ? P[i + t * ldp] : 0.0;
+      // four columns per batch: their G loads are issued before the FMAs
+      for (int c0 = pw + par; c0 <= i; c0 += 8) {
+        double gv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + 2 * u;
+          gv[u] = c <= i ? G[(p0 + i) + (int64_t)(p0 + c) * d] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + 2 * u;
+          if (c > i) break;
+          double acc = 0.0;
+#pragma unroll
+          for (int t = 0; t < kPW; ++t) acc = fma(li[t], P[c + t * ldp], acc);
+          G[(p0 + i) + (int64_t)(p0 + c) * d] = gv[u] - acc;
+        }
+      }
     }
     __syncthreads();
   }
   if (tid == 0) *status = fail;
 }
 
-// x = (L L^T)^{-1} rhs (lower L in G, ld d), one warp; rhs/x may alias.
-__device__ void warp_chol_solve(const double* G, int d, const double* rhs, double* x, double* y) {
-  const int lane = threadIdx.x & 31;
-  for (int i = 0; i < d; ++i) {  // L y = rhs
-    double s = 0.0;
-    for (int j = lane; j < i; j += 32) s += G[i + (int64_t)j * d] * y[j];
-    s = warp_sum(s);
-    if (lane == 0) y[i] = (rhs[i] - s) / G[i + (int64_t)i * d];
-    __syncwarp();
-  }
-  for (int i = d - 1; i >= 0; --i) {  // L^T x = y
-    double s = 0.0;
-    for (int j = i + 1 + lane; j < d; j += 32) s += G[j + (int64_t)i * d] * x[j];
-    s = warp_sum(s);
-    if (lane == 0) x[i] = (y[i] - s) / G[i + (int64_t)i * d];
-    __syncwarp();
-  }
-}
-
-__global__ void chol_solve_kernel(const double* __restrict__ L, int d, const double* __restrict__ rhs,
-                                  double* __restrict__ x, double* __restrict__ y, const int32_t* __restrict__ status,
-                                  int accumulate) {
+// x (+)= (L L^T)^{-1} rhs for the lower Cholesky factor L (ld d), one CTA.
+// Both sweeps stage 32-wide blocks of L in shared memory (coalesced loads),
+// then run the 32 column steps from there with one barrier per step.
+constexpr int kST = 256;
+constexpr int kSB = 32;
+__global__ void __launch_bounds__(kST) chol_solve_kernel(const double* __restrict__ L, int d,
+                                                         const double* __restrict__ rhs, double* __restrict__ x,
+                                                         const int32_t* __restrict__ status, int accumulate) {
+  extern __shared__ __align__(16) double sm[];
+  double* v = sm;            // d
+  double* B = sm + d;        // d x kSB block (ld d)
   if (*status) return;
-  if (threadIdx.x >= 32) return;
-  // solve into y2 = scratch at y + d, then x (+)= solution
-  double* sol = y + d;
-  warp_chol_solve(L, d, rhs, sol, y);
-  for (int i = threadIdx.x; i < d; i += 32) x[i] = accumulate ? x[i] + sol[i] : sol[i];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < d; i += kST) v[i] = rhs[i];
+  // forward: L y = rhs, column blocks [j0, j0 + kSB)
+  for (int j0 = 0; j0 < d; j0 += kSB) {
+    const int jw = (d - j0) < kSB ? (d - j0) : kSB;
+    for (int i = j0 + tid; i < d; i += kST) {  // row i of the block: 32 independent loads
+      double g[kSB];
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) g[c] = (c < jw && i >= j0 + c) ? L[i + (int64_t)(j0 + c) * d] : 0.0;
+#pragma unroll
+      for (int c = 0; c < kSB; ++c)
+        if (c < jw) B[i + c * d] = g[c];
+    }
+    __syncthreads();
+    for (int c = 0; c < jw; ++c) {
+      const int j = j0 + c;
+      const double yj = v[j] / B[j + c * d];
+      for (int i = j + 1 + tid; i < d; i += kST) v[i] -= B[i + c * d] * yj;
+      __syncthreads();
+      if (tid == 0) v[j] = yj;
+    }
+    __syncthreads();
+  }
+  // backward: L^T x = y, row blocks [i0, i0 + kSB) from the bottom; B holds
+  // rows i0..i0+iw-1 of L transposed: B[j + r * d] = L(i0 + r, j), j <= i0 + r
+  for (int i1 = d; i1 > 0; i1 -= kSB) {
+    const int i0 = i1 - kSB > 0 ? i1 - kSB : 0;
+    const int iw = i1 - i0;
+    for (int j = tid; j < i1; j += kST) {  // column j of L, rows i0..i1-1: iw independent loads
+      double g[kSB];
+#pragma unroll
+      for (int r = 0; r < kSB; ++r) g[r] = (r < iw && j <= i0 + r) ? L[(i0 + r) + (int64_t)j * d] : 0.0;
+#pragma unroll
+      for (int r = 0; r < kSB; ++r)
+        if (r < iw) B[j + r * d] = g[r];
+    }
+    __syncthreads();
+    for (int r = iw - 1; r >= 0; --r) {
+      const int i = i0 + r;
+      const double xi = v[i] / B[i + r * d];
+      for (int j = tid; j < i; j += kST) v[j] -= B[j + r * d] * xi;
+      __syncthreads();
+      if (tid == 0) v[i] = xi;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < d; i += kST) x[i] = accumulate ? x[i] + v[i] : v[i];
 }
 
-// r = Fb - FA x (k rows); also writes the squared norm partials.
-__global__ void lsq_residual_kernel(const double* __restrict__ FW, int64_t k, int d, const double* __restrict__ x,
-                                    double* __restrict__ r, double* __restrict__ part) {
-  __shared__ double red[40];
+// r = Fb - FA x (k rows) and the squared-norm partials: 32 rows x 8 column
+// groups per CTA, combined in shared memory.
+__global__ void __launch_bounds__(256) lsq_residual_kernel(const double* __restrict__ FW, int64_t k, int d,
+                                                           const double* __restrict__ x, double* __restrict__ r,
+                                                           double* __restrict__ part) {
+  __shared__ double red[8][33];
+  __shared__ double red2[40];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t i = blockIdx.x * 32LL + lane;
+  double acc = 0.0;
+  if (i < k)
+    for (int j = grp; j < d; j += 8) acc = fma(FW[i + (int64_t)j * k], x[j], acc);
+  red[grp][lane] = acc;
+  __syncthreads();
   double s = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int j = 0; j < d; ++j) acc += FW[i + j * k] * x[j];
-    const double e = FW[i + (int64_t)d * k] - acc;
+  if (grp == 0 && i < k) {
+    double a = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) a += red[g][lane];
+    const double e = FW[i + (int64_t)d * k] - a;
     r[i] = e;
-    s += e * e;
+    s = e * e;
   }
-  s = block_sum<256>(s, red);
+  s = block_sum<256>(s, red2);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
@@ -192,15 +259,17 @@ int slra_lsr_residual(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
   return launch_lsr_residual(C(ctx), A, lda, m, d, b, x, d_out);
 }
 
-int slra_sketch_solve(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t d, const double* b,
-                      const int64_t* src, const double* coef, const int32_t* q, int64_t width, int tree, int64_t k,
-                      double* x_hat, double* h_sketched_residual) {
-  if (!ctx || lda < m || m <= d || d < 1 || k <= d) return SLRA_ERR_INVALID_ARGUMENT;
-  if (d > 768) return SLRA_ERR_UNSUPPORTED;
-  Context* cx = C(ctx);
+}  // extern "C"
+
+namespace slra_dev {
+
+// Solve min ||FA x - Fb|| for a sketched system FW = (FA | Fb) (k x (d+1),
+// ld k). FW == nullptr: the caller has already written FW into the arena
+// (returned through *fw_slot when fw_slot != nullptr on a first call).
+static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, double* x_hat,
+                     double* h_sketched_residual, double** fw_slot) {
   const int64_t dc = d + 1;
-  int rgrid = cx->num_sms * 2;
-  if ((k + 255) / 256 < rgrid) rgrid = (int)((k + 255) / 256);
+  const int rgrid = (int)((k + 31) / 32);  // lsq_residual_kernel: 32 rows per CTA
   // arena 2: FW (k x dc) | Gw (dc x dc) | G (d x d) | g (d) | r (k) | c (d) | y (2d) | part | out
   const size_t need = (size_t)k * dc + (size_t)dc * dc + (size_t)d * d + 4 * (size_t)d + (size_t)k + rgrid + 16;
   double* ws = static_cast<double*>(arena(cx, 2, sizeof(double) * need));
@@ -216,9 +285,11 @@ int slra_sketch_solve(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
   double* out = part + rgrid;
   int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
   cudaStream_t st = cx->stream;
-  // FW = F (A | b): one pass over the k sketched rows
-  SLRA_TRY(launch_sketch_rows(cx, A, lda, d, src, coef, q, width, tree, k, FW, k));
-  SLRA_TRY(launch_sketch_rows(cx, b, m, 1, src, coef, q, width, tree, k, FW + (size_t)k * d, k));
+  if (fw_slot) {
+    *fw_slot = FW;
+    return SLRA_OK;
+  }
+  if (FWext) SLRA_CUDA(cudaMemcpyAsync(FW, FWext, 8 * (size_t)k * dc, cudaMemcpyDeviceToDevice, st));
   // Gram [FA Fb]^T [FA Fb] (dc x dc); G = leading d x d block, g = FA^T Fb
   SLRA_TRY(launch_gemm(cx, 1, 0, dc, dc, k, 1.0, FW, k, FW, k, 0.0, Gw, dc));
   SLRA_CUDA(cudaMemcpy2DAsync(G, 8 * d, Gw, 8 * dc, 8 * d, d, cudaMemcpyDeviceToDevice, st));
@@ -230,17 +301,19 @@ int slra_sketch_solve(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
   double dmax = 0.0;
   for (int64_t i = 0; i < (d < 500 ? d : 500); ++i) dmax = hs[i] > dmax ? hs[i] : dmax;
   const double tol2 = 1e-20 * dmax;
-  const size_t smem = sizeof(double) * (size_t)d * kPW;
+  const size_t smem = sizeof(double) * (size_t)(d + 1) * kPW;
+  SLRA_CUDA(cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(8 * d * (kSB + 1))));
   SLRA_CUDA(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SLRA_TIMED(cx, "lsr_solve", cholesky_kernel<<<1, kLT, smem, st>>>(G, (int)d, tol2, d_status);)
   SLRA_CHECK_LAUNCH(cx);
   // x = G^{-1} g, then one refinement step x += G^{-1} FA^T (Fb - FA x)
-  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, 32, 0, st>>>(G, (int)d, g, x_hat, y, d_status, 0);)
+  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, kST, 8 * d * (kSB + 1), st>>>(G, (int)d, g, x_hat, d_status, 0);)
   SLRA_CHECK_LAUNCH(cx);
   SLRA_TIMED(cx, "lsr_solve", lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);)
   SLRA_CHECK_LAUNCH(cx);
   SLRA_TRY(launch_gemm(cx, 1, 0, d, 1, k, 1.0, FW, k, r, k, 0.0, cvec, d));
-  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, 32, 0, st>>>(G, (int)d, cvec, x_hat, y, d_status, 1);)
+  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, kST, 8 * d * (kSB + 1), st>>>(G, (int)d, cvec, x_hat, d_status, 1);)
   SLRA_CHECK_LAUNCH(cx);
   // sketched residual ||FA x - Fb|| by a direct pass
   SLRA_TIMED(cx, "lsr_solve", lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);)
@@ -253,6 +326,31 @@ int slra_sketch_solve(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
   if (*reinterpret_cast<int32_t*>(hs + 1)) return SLRA_ERR_SKETCH_RANK_FAILURE;
   if (h_sketched_residual) *h_sketched_residual = sqrt(hs[0]);
   return SLRA_OK;
+}
+
+}  // namespace slra_dev
+
+extern "C" {
+
+int slra_sketch_solve(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t d, const double* b,
+                      const int64_t* src, const double* coef, const int32_t* q, int64_t width, int tree, int64_t k,
+                      double* x_hat, double* h_sketched_residual) {
+  if (!ctx || lda < m || m <= d || d < 1 || k <= d) return SLRA_ERR_INVALID_ARGUMENT;
+  if (d > 768) return SLRA_ERR_UNSUPPORTED;
+  Context* cx = C(ctx);
+  double* FW = nullptr;
+  SLRA_TRY(lsr_solve(cx, nullptr, k, d, nullptr, nullptr, &FW));
+  // FW = F (A | b): one pass over the k sketched rows
+  SLRA_TRY(launch_sketch_rows(cx, A, lda, d, src, coef, q, width, tree, k, FW, k));
+  SLRA_TRY(launch_sketch_rows(cx, b, m, 1, src, coef, q, width, tree, k, FW + (size_t)k * d, k));
+  return lsr_solve(cx, nullptr, k, d, x_hat, h_sketched_residual, nullptr);
+}
+
+int slra_lsr_solve_sketched(slra_ctx ctx, const double* FW, int64_t ldfw, int64_t k, int64_t d, double* x_hat,
+                            double* h_sketched_residual) {
+  if (!ctx || !FW || ldfw != k || k <= d || d < 1) return SLRA_ERR_INVALID_ARGUMENT;
+  if (d > 768) return SLRA_ERR_UNSUPPORTED;
+  return lsr_solve(C(ctx), FW, k, d, x_hat, h_sketched_residual, nullptr);
 }
 
 }  // extern "C"

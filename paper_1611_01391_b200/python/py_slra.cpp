@@ -289,6 +289,31 @@ PYBIND11_MODULE(_slra, m) {
     return py::make_tuple(to_np(dU.download()), to_np(dV.download()), o[0], o[1]);
   });
 
+  // ---- end-to-end sketch_solve(p, F, false) + residual_norm(p, x_hat)
+  // (lsr.hpp) with A (m x d, column-major) and b read from the caller's
+  // (pinned) host buffers; x_hat and both residuals come back to the host.
+  m.def("sketch_solve_host", [](uintptr_t A_host, uintptr_t b_host, Index mm, Index d, const PyOp& F) {
+    const SketchPlan plan = compile_plan(*F.p, Side::Left);
+    static DeviceMatrix* staging = new DeviceMatrix();  // reused HBM staging buffer (never freed)
+    if (staging->rows() != mm || staging->cols() != d + 1) *staging = DeviceMatrix(mm, d + 1);
+    slra_ctx cx = device_context();
+    double* dA = staging->data();
+    double* db = dA + mm * d;
+    check(slra_memcpy_h2d(cx, dA, reinterpret_cast<const void*>(A_host), 8 * mm * d), "sketch_solve_host");
+    check(slra_memcpy_h2d(cx, db, reinterpret_cast<const void*>(b_host), 8 * mm), "sketch_solve_host");
+    DevBuf<int64_t> src(plan.src);
+    DevBuf<double> coef(plan.coef);
+    DevBuf<int32_t> q(plan.q);
+    DevBuf<double> x(static_cast<size_t>(d)), out(2);
+    double sres = 0;
+    check(slra_sketch_solve(cx, dA, mm, mm, d, db, src.get(), coef.get(), q.get(), plan.width, plan.tree, plan.count,
+                            x.get(), &sres),
+          "sketch_solve");
+    check(slra_lsr_residual(cx, dA, mm, mm, d, db, x.get(), out.get()), "residual_norm");
+    Vector xv = x.download();
+    return py::make_tuple(vec_np(xv), sres, std::sqrt(out.download()[0]));
+  });
+
   // ---- end-to-end cross_approx(M, ...) + cur_evaluate(M, c, Frobenius)
   // (cur.hpp) with M read from the caller's (pinned) host buffer; I, J, the
   // nucleus and the residual come back to the host.
@@ -382,6 +407,68 @@ PYBIND11_MODULE(_slra, m) {
     check(slra_cur_residual_factored(device_context(), ptr<double>(A), lda, mm, n, ptr<int64_t>(I), k,
                                      ptr<int64_t>(J), l, ptr<double>(Tsig), ptr<double>(Sr), r, ptr<double>(out)),
           "cur_residual_factored");
+  });
+  // ---- building blocks of the row-sharded drivers (shard.py)
+  m.def("gather_rows_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t I, Index k, uintptr_t R,
+                                 Index ldr) {
+    check(slra_gather_rows(device_context(), ptr<double>(A), lda, mm, n, ptr<int64_t>(I), k, ptr<double>(R), ldr),
+          "gather_rows");
+  });
+  m.def("gather_cols_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t J, Index l, uintptr_t Cm,
+                                 Index ldc) {
+    check(slra_gather_cols(device_context(), ptr<double>(A), lda, mm, n, ptr<int64_t>(J), l, ptr<double>(Cm), ldc),
+          "gather_cols");
+  });
+  m.def("select_rows_spanning_device", [](uintptr_t A, Index lda, Index mm, Index c, Index count, double h,
+                                          uintptr_t idx, uintptr_t vol) {
+    check(slra_select_rows_spanning(device_context(), ptr<double>(A), lda, mm, c, count, h, ptr<int64_t>(idx),
+                                    ptr<double>(vol)),
+          "select_rows_spanning");
+  });
+  m.def("sketch_rows_device", [](uintptr_t W, Index ldw, Index mm, Index ncols, uintptr_t src, uintptr_t coef,
+                                 uintptr_t q, Index width, int tree, Index k, uintptr_t out, Index ldo) {
+    check(slra_sketch_rows(device_context(), ptr<double>(W), ldw, mm, ncols, ptr<int64_t>(src), ptr<double>(coef),
+                           ptr<int32_t>(q), width, tree, k, ptr<double>(out), ldo),
+          "sketch_rows");
+  });
+  m.def("sketch_rows_shard_device", [](uintptr_t W, Index ldw, Index row0, Index mloc, Index ncols, uintptr_t src,
+                                       uintptr_t coef, Index width, Index k, uintptr_t out, Index ldo,
+                                       bool transpose) {
+    check(slra_sketch_rows_shard(device_context(), ptr<double>(W), ldw, row0, mloc, ncols, ptr<int64_t>(src),
+                                 ptr<double>(coef), width, k, ptr<double>(out), ldo, transpose ? 1 : 0),
+          "sketch_rows_shard");
+  });
+  m.def("lsr_solve_sketched_device",[](uintptr_t FW, Index k, Index d, uintptr_t x) {
+    double res = 0;
+    check(slra_lsr_solve_sketched(device_context(), ptr<double>(FW), k, k, d, ptr<double>(x), &res),
+          "lsr_solve_sketched");
+    return res;
+  });
+  m.def("sketch_solve_device", [](uintptr_t A, Index lda, Index mm, Index d, uintptr_t b, uintptr_t src,
+                                  uintptr_t coef, uintptr_t q, Index width, int tree, Index k, uintptr_t x) {
+    double res = 0;
+    check(slra_sketch_solve(device_context(), ptr<double>(A), lda, mm, d, ptr<double>(b), ptr<int64_t>(src),
+                            ptr<double>(coef), ptr<int32_t>(q), width, tree, k, ptr<double>(x), &res),
+          "sketch_solve");
+    return res;
+  });
+  m.def("lsr_residual_device", [](uintptr_t A, Index lda, Index mm, Index d, uintptr_t b, uintptr_t x,
+                                  uintptr_t out) {
+    check(slra_lsr_residual(device_context(), ptr<double>(A), lda, mm, d, ptr<double>(b), ptr<double>(x),
+                            ptr<double>(out)),
+          "lsr_residual");
+  });
+  m.def("gemm_device", [](int ta, int tb, Index mm, Index n, Index k, double alpha, uintptr_t A, Index lda,
+                          uintptr_t B, Index ldb, double beta, uintptr_t Cm, Index ldc) {
+    check(slra_gemm(device_context(), ta, tb, mm, n, k, alpha, ptr<double>(A), lda, ptr<double>(B), ldb, beta,
+                    ptr<double>(Cm), ldc),
+          "gemm");
+  });
+  m.def("lowrank_residual_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t P, Index ldp, uintptr_t Q,
+                                      Index ldq, Index inner, uintptr_t out) {
+    check(slra_lowrank_residual(device_context(), ptr<double>(A), lda, mm, n, ptr<double>(P), ldp, ptr<double>(Q),
+                                ldq, inner, ptr<double>(out)),
+          "lowrank_residual");
   });
   m.def("cur_residual_device", [](uintptr_t A, Index lda, Index mm, Index n, uintptr_t I, Index k, uintptr_t J,
                                   Index l, uintptr_t U) {

@@ -1,0 +1,236 @@
+"""World-size-2 gloo tests of the multi-GPU drivers (paper_1611_01391_b200/shard.py).
+
+The drivers' host logic — row ownership, the allreduce/allgather exchanges,
+the order of the replicated selections — runs here on CPU with an
+oracle-backed stand-in for the device operations (test infrastructure; the
+product binds shard.DeviceOps to the sm_100a library). The sharded results
+must equal the single-process oracle on the full matrix:
+* config 3 shape (C-A, k == l): identical I, J and residual;
+* config 4 shape (sketched LSR, uniform rows and sparse +-1 s=2): the
+  all-reduced sketch is bit-identical to the oracle's F (A|b), and x_hat
+  matches.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from paper_1611_01391_b200 import shard  # noqa: E402
+
+
+def _oracle():
+    from conftest import load_oracle
+    return load_oracle()
+
+
+class OracleOps:
+    """CPU stand-in for shard.DeviceOps (same tensor conventions)."""
+
+    def __init__(self, oracle):
+        self.o = oracle
+
+    def rows_shard(self, W_t, row0, src, coef, width, k, transpose, out=None):
+        W = W_t.numpy()  # (ncols, mloc): W[j, i] = row (row0 + i), column j
+        ncols, mloc = W.shape
+        res = np.zeros((k, ncols))
+        s, c = src.numpy().reshape(k, width), coef.numpy().reshape(k, width)
+        for t in range(k):
+            acc, first = np.zeros(ncols), True
+            for q in range(width):
+                rr = int(s[t, q]) - row0
+                if 0 <= rr < mloc:
+                    term = c[t, q] * W[:, rr]
+                    acc = term if first else acc + term
+                    first = False
+            res[t] = acc
+        r = torch.from_numpy(res if transpose else np.ascontiguousarray(res.T))
+        if out is not None:
+            out.copy_(r)
+            return out
+        return r
+
+    def select(self, S_t, count, h):
+        S = np.asfortranarray(S_t.numpy().T)
+        return torch.tensor(self.o.select_rows_spanning(S, count, h), dtype=torch.int64)
+
+    def gather_cols(self, A_t, J):
+        return A_t[J, :].contiguous()
+
+    def primitive_cur(self, C_t, I, r):
+        C = np.asfortranarray(C_t.numpy().T)
+        l = C.shape[1]
+        Il = I.tolist()
+        G = C[Il, :]
+        rr = r if r > 0 else self.o.numerical_rank(G, 1e-10, True)
+        o = self.o.primitive_cur(C, Il, list(range(l)), rr)
+        S, sig, T = self.o.svd(G)
+        Tsig = T[:, :rr] / sig[:rr]
+        return (torch.from_numpy(np.ascontiguousarray(o["nucleus"].T)), torch.from_numpy(np.ascontiguousarray(Tsig.T)),
+                torch.from_numpy(np.ascontiguousarray(S[:, :rr].T)), rr)
+
+    def cur_residual_partial(self, A_t, C_loc, T, S, R_t, r):
+        A = A_t.numpy().T
+        E = A - C_loc.numpy().T @ T.numpy()[:r].T @ S.numpy()[:r] @ R_t.numpy().T
+        return torch.tensor([float((E * E).sum()), float((A * A).sum())], dtype=torch.float64)
+
+    def lsr_solve(self, FW_t, k, d):
+        FW = FW_t.numpy().T
+        x, *_ = np.linalg.lstsq(FW[:, :d], FW[:, d], rcond=None)
+        return torch.from_numpy(x), float(np.linalg.norm(FW[:, :d] @ x - FW[:, d]))
+
+    def lsr_residual_partial(self, A_t, b, x):
+        r = A_t.numpy().T @ x.numpy() - b.numpy()
+        return torch.tensor([float(r @ r), 0.0], dtype=torch.float64)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run(rank, world, port, fn, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(rank, world)))
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(60)
+    return out
+
+
+def _cauchy(m, n, seed, oracle):
+    r = oracle.Rng(seed)
+    x = np.array([r.uniform() for _ in range(m)])
+    y = np.array([2.0 + r.uniform() for _ in range(n)])
+    return 1.0 / (x[:, None] - y[None, :])
+
+
+M3, N3, K3 = 301, 260, 10
+
+
+def _ca_worker(rank, world):
+    oracle = _oracle()
+    A = oracle.gen_factor_gaussian(M3, N3, K3, 1e-9, oracle.Rng(4))
+    row0, mloc = shard.split(M3, world, rank)
+    A_t = torch.from_numpy(np.ascontiguousarray(A[row0:row0 + mloc, :].T))  # (n, mloc)
+    init = oracle.Rng(9).distinct_indices(K3, M3)
+    res = shard.cross_approx(OracleOps(oracle), shard.Comm(dist), A_t, row0, M3, 0, K3, K3, init, 3, 1.1, torch)
+    return {"I": res.I.tolist(), "J": res.J.tolist(), "r": res.r, "rs": res.resid_sq, "ns": res.norm_sq,
+            "mloc": mloc}
+
+
+def test_split_partitions():
+    for total in (0, 1, 7, 16384, 65536, 1 << 20):
+        for world in (1, 2, 3, 4, 8):
+            parts = [shard.split(total, world, r) for r in range(world)]
+            assert sum(c for _, c in parts) == total
+            assert all(parts[i][0] + parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
+
+
+def test_sharded_cross_approx_matches_oracle(oracle):
+    out = _spawn(_ca_worker)
+    assert all(isinstance(v, dict) for v in out.values()), out
+    a, b = out[0], out[1]
+    assert a["mloc"] + b["mloc"] == M3 and a["mloc"] != b["mloc"]  # ragged shards
+    assert a["I"] == b["I"] and a["J"] == b["J"] and a["rs"] == b["rs"]
+    A = oracle.gen_factor_gaussian(M3, N3, K3, 1e-9, oracle.Rng(4))
+    init = oracle.Rng(9).distinct_indices(K3, M3)
+    o = oracle.cross_approx(A, 1, K3, K3, init, 3, 1.1, None, oracle.Rng(0))
+    assert a["I"] == o["I"] and a["J"] == o["J"]
+    rk = oracle.numerical_rank(A[np.ix_(o["I"], o["J"])], 1e-10, True)
+    assert a["r"] == rk
+    c = oracle.primitive_cur(A, o["I"], o["J"], rk)
+    e = oracle.cur_evaluate(A, o["I"], o["J"], c["nucleus"])
+    nA = np.linalg.norm(A)
+    assert abs(np.sqrt(a["rs"]) - e) <= 1e-12 * nA
+    assert abs(np.sqrt(a["ns"]) - nA) <= 1e-13 * nA
+
+
+M4, D4, K4 = 1001, 12, 64
+
+
+def _lsr_problem(oracle):
+    A, b = oracle.gen_lsr_gaussian(M4, D4, 1e-6, oracle.Rng(21))
+    return A, b
+
+
+def _lsr_ops(oracle, kind):
+    rng = oracle.Rng(22)
+    if kind == "uniform":
+        rows = rng.distinct_indices(K4, M4)
+        return oracle.make_sub_identity(rows, M4)
+    return oracle.make_product([oracle.make_sub_identity(rng.distinct_indices(K4, M4), M4),
+                                oracle.gen_sparse_circulant(M4, 2, rng), oracle.gen_sign_diagonal(M4, rng)])
+
+
+def _lsr_worker_factory(kind):
+    def worker(rank, world):
+        import paper_1611_01391_b200 as slra
+        oracle = _oracle()
+        A, b = _lsr_problem(oracle)
+        F = _lsr_ops(oracle, kind)
+        # the plan is compiled by the product's host layer from the same operator recipe
+        Fp = _lsr_ops(slra, kind)
+        plan = Fp.plan("left")
+        row0, mloc = shard.split(M4, world, rank)
+        A_t = torch.from_numpy(np.ascontiguousarray(A[row0:row0 + mloc, :].T))
+        bl = torch.from_numpy(np.ascontiguousarray(b[row0:row0 + mloc]))
+        src = torch.tensor(plan["src"], dtype=torch.int64)
+        coef = torch.tensor(plan["coef"], dtype=torch.float64)
+        ops = OracleOps(oracle)
+        comm = shard.Comm(dist)
+        FW = torch.zeros(D4 + 1, K4, dtype=torch.float64)
+        ops.rows_shard(A_t, row0, src, coef, plan["width"], K4, False, out=FW[:D4])
+        ops.rows_shard(bl.reshape(1, -1), row0, src, coef, plan["width"], K4, False, out=FW[D4:])
+        comm.allreduce_(FW)
+        W = np.asfortranarray(np.column_stack([A, b]))
+        ref = oracle.apply(F, W, "left")
+        x, sres, tres = shard.sketch_solve(ops, comm, A_t, bl, row0, D4, src, coef, plan["width"], K4, torch)
+        return {"exact": bool(np.array_equal(FW.numpy().T, ref)), "x": x.tolist(), "tres": tres}
+    return worker
+
+
+def _lsr_uniform(rank, world):
+    return _lsr_worker_factory("uniform")(rank, world)
+
+
+def _lsr_sparse(rank, world):
+    return _lsr_worker_factory("sparse")(rank, world)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "sparse"])
+def test_sharded_sketch_solve_matches_oracle(oracle, kind):
+    out = _spawn(_lsr_uniform if kind == "uniform" else _lsr_sparse)
+    assert all(isinstance(v, dict) for v in out.values()), out
+    assert out[0]["exact"] and out[1]["exact"]  # all-reduced sketch == F (A|b), bit for bit
+    A, b = _lsr_problem(oracle)
+    rep = oracle.sketch_solve(A, b, _lsr_ops(oracle, kind), True)
+    x = np.array(out[0]["x"])
+    assert np.linalg.norm(x - rep["x_hat"]) <= 1e-10 * np.linalg.norm(rep["x_hat"])
+    assert abs(out[0]["tres"] - np.linalg.norm(A @ rep["x_hat"] - b)) <= 1e-10 * np.linalg.norm(b)
