@@ -50,13 +50,13 @@ static py::dict cur_dict(const CurDecomposition& c) {
 
 PYBIND11_MODULE(_oracle, m) {
   m.doc() = "CPU oracle (restatement of the reference slra hot path) -- test infrastructure only";
-  auto base = py::register_exception<std::runtime_error>(m, "OracleRuntimeError");
-  py::register_exception<RangeFailure>(m, "RangeFailure", base.ptr());
-  py::register_exception<SketchRankFailure>(m, "SketchRankFailure", base.ptr());
-  py::register_exception<PremultRankFailure>(m, "PremultRankFailure", base.ptr());
-  py::register_exception<SelectionFailure>(m, "SelectionFailure", base.ptr());
-  py::register_exception<GeneratorRankFailure>(m, "GeneratorRankFailure", base.ptr());
-  py::register_exception<EmptySample>(m, "EmptySample", base.ptr());
+  auto base = py::register_local_exception<std::runtime_error>(m, "OracleRuntimeError");
+  py::register_local_exception<RangeFailure>(m, "RangeFailure", base.ptr());
+  py::register_local_exception<SketchRankFailure>(m, "SketchRankFailure", base.ptr());
+  py::register_local_exception<PremultRankFailure>(m, "PremultRankFailure", base.ptr());
+  py::register_local_exception<SelectionFailure>(m, "SelectionFailure", base.ptr());
+  py::register_local_exception<GeneratorRankFailure>(m, "GeneratorRankFailure", base.ptr());
+  py::register_local_exception<EmptySample>(m, "EmptySample", base.ptr());
 
   py::class_<Rng>(m, "Rng", py::module_local())
       .def(py::init<std::uint64_t>())

@@ -1,0 +1,287 @@
+// Shifted CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa,
+// "Shifted Cholesky QR for computing the QR factorization of ill-conditioned
+// matrices", SISC 2020) for the tall-skinny sketch Y = M H of the range
+// finder (lra.cpp:14-39, thin_qr linalg.cpp:67-79).
+//
+// Why here: Householder QR of a 4096 x 48 strip is a chain of 48 dependent
+// column steps per tree level (latency-bound on one SM per leaf); CholeskyQR
+// is three rounds of {Gram, an n x n Cholesky, a row-parallel triangular
+// solve}. Pass 1 adds the shift s = 11 (m n + n (n + 1)) u ||Y||_F^2 so the
+// Cholesky succeeds for cond(Y) up to ~1/u; passes 2-3 restore orthogonality
+// to O(u). R = R3 R2 R1 has a positive diagonal — thin_qr's R(i,i) >= 0
+// convention. Q spans the same space as Householder's Q; the range finder
+// consumes only the top-r singular subspace of R, which is well conditioned
+// here, so the result matches the oracle within tolerance. A Cholesky
+// breakdown (cond(Y) beyond ~1/u, e.g. an exactly rank-deficient sketch) sets
+// status[b] = 1 and the caller falls back to the Householder TSQR.
+//
+// Kernels per pass: gram_partial_kernel (row chunks -> partial n x n Grams,
+// no atomics), chol_small_kernel (sums the partials in a fixed order, shift,
+// Cholesky, 1/R(i,i)), trsm_rows_kernel (Q = Y R^-1, a thread per row).
+#include "common.cuh"
+
+namespace slra_dev {
+
+constexpr int kCQ = 256;
+constexpr int kCQMax = 64;
+constexpr int kGR = 128;  // rows per Gram chunk
+
+// P_{b,k} = Y_b(chunk k, :)^T Y_b(chunk k, :) for chunk k = blockIdx.x
+// (upper triangle only).
+__global__ void __launch_bounds__(kCQ) gram_partial_kernel(const double* __restrict__ Y, int64_t ldy, int64_t sY,
+                                                           int64_t m, int n, double* __restrict__ P, int64_t sP,
+                                                           const int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) double T[];  // chunk rows, ld kGR + 1 per column (odd: conflict-free)
+  constexpr int ldt = kGR + 1;
+  const int b = blockIdx.y, k = blockIdx.x, tid = threadIdx.x;
+  if (status[b]) return;
+  Y += b * sY;
+  const int64_t r0 = (int64_t)k * kGR;
+  const int rows = (int)((m - r0) < kGR ? (m - r0) : kGR);
+#pragma unroll 4
+  for (int e = tid; e < kGR * n; e += kCQ) {
+    const int i = e % kGR, c = e / kGR;  // kGR is a power of two
+    T[i + c * ldt] = i < rows ? Y[(r0 + i) + (int64_t)c * ldy] : 0.0;
+  }
+  __syncthreads();
+  double* out = P + b * sP + (int64_t)k * n * n;
+  for (int e = tid; e < n * n; e += kCQ) {
+    const int i = e % n, c = e / n;
+    if (i > c) continue;
+    const double* a = T + i * ldt;
+    const double* d = T + c * ldt;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < kGR; t += 2) {
+      acc0 = fma(a[t], d[t], acc0);
+      acc1 = fma(a[t + 1], d[t + 1], acc1);
+    }
+    out[i + c * n] = acc0 + acc1;
+  }
+}
+
+// Upper Cholesky factor R of G + shift*I where G = sum of the nchunk partial
+// Grams (upper triangles, summed in chunk order); shift = shift_coef *
+// trace(G). One CTA per problem, a thread per row for the updates. Writes R
+// (ld n, zeros below) and 1/R(i,i). A breakdown sets status[b] = 1.
+__global__ void __launch_bounds__(kCQ) chol_small_kernel(const double* __restrict__ P, int64_t sP, int nchunk, int n,
+                                                         double shift_coef, double* __restrict__ R, int64_t sR,
+                                                         double* __restrict__ rinv, int64_t sRi,
+                                                         int32_t* __restrict__ status) {
+  __shared__ double L[kCQMax * (kCQMax + 1)];  // L(i, c) at i + c * ld, lower triangle
+  __shared__ double red[40];
+  __shared__ int fail;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (status[b]) return;
+  const int ld = n + 1;
+  P += b * sP;
+  R += b * sR;
+  rinv += b * sRi;
+  const int64_t nn = (int64_t)n * n;
+  for (int e = tid; e < n * n; e += kCQ) {
+    const int i = e % n, c = e / n;
+    if (i > c) continue;
+    double s = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < nchunk; ++k) s += P[k * nn + e];  // fixed order; loads issued ahead
+    L[c + i * ld] = s;  // lower: L(c, i) = G(i, c), c >= i
+  }
+  __syncthreads();
+  double tr = 0.0;
+  for (int i = tid; i < n; i += kCQ) tr += L[i + i * ld];
+  tr = block_sum<kCQ>(tr, red);
+  for (int i = tid; i < n; i += kCQ) L[i + i * ld] += shift_coef * tr;
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  {
+    // thread (row ti, phase tc) owns L(ti, c) for c = tc, tc + 4, ...: each
+    // step stages column j in registers, then writes (2 barriers per step,
+    // no load/store aliasing chains)
+    constexpr int kQ = kCQMax / 4;
+    const int ti = tid & 63, tc = tid >> 6;
+    for (int j = 0; j < n; ++j) {
+      const double piv = L[j + j * ld];
+      if (!(piv > 0.0)) {  // uniform: every thread read the same pivot
+        if (tid == 0) fail = 1;
+        break;
+      }
+      const double ljj = sqrt(piv);
+      const double inv = 1.0 / ljj;
+      const bool row = ti > j && ti < n;
+      const double lij = row ? L[ti + j * ld] * inv : 0.0;
+      double lcj[kQ], cur[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int c = tc + 4 * q;
+        const bool act = row && c > j && c <= ti;
+        lcj[q] = act ? L[c + j * ld] * inv : 0.0;
+        cur[q] = act ? L[ti + c * ld] : 0.0;
+      }
+      __syncthreads();
+      if (tc == 0 && ti >= j && ti < n) L[ti + j * ld] = (ti == j) ? ljj : lij;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int c = tc + 4 * q;
+        if (row && c > j && c <= ti) L[ti + c * ld] = cur[q] - lij * lcj[q];
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) status[b] = 1;
+    return;
+  }
+  for (int e = tid; e < n * n; e += kCQ) {
+    const int i = e % n, c = e / n;  // R(i, c) = L(c, i) for i <= c
+    R[e] = (i <= c) ? L[c + i * ld] : 0.0;
+  }
+  for (int i = tid; i < n; i += kCQ) rinv[i] = 1.0 / L[i + i * ld];
+}
+
+// Q(i, :) = Y(i, :) R^-1 for every row i (forward substitution along the
+// columns of the upper R), one thread per row; problem blockIdx.y. Dynamic
+// shared memory: R (n x n) | 1/R(i,i) (n) | z (n x 128, thread-major).
+__global__ void __launch_bounds__(128) trsm_rows_kernel(const double* __restrict__ Y, int64_t ldy, int64_t sY,
+                                                        int64_t m, int n, const double* __restrict__ R, int64_t sR,
+                                                        const double* __restrict__ rinv, int64_t sRi,
+                                                        double* __restrict__ Q, int64_t ldq, int64_t sQ,
+                                                        const int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) double tsm[];
+  double* Rs = tsm;
+  double* ri = Rs + n * n;
+  double* z = ri + n;  // z[c * 128 + tid]
+  const int b = blockIdx.y, tid = threadIdx.x;
+  if (status[b]) return;
+  Y += b * sY;
+  Q += b * sQ;
+  R += b * sR;
+  rinv += b * sRi;
+  for (int e = tid; e < n * n; e += 128) Rs[e] = R[e];
+  for (int c = tid; c < n; c += 128) ri[c] = rinv[c];
+  __syncthreads();
+  const int64_t i = blockIdx.x * 128LL + tid;
+  if (i >= m) return;
+  (void)z;
+  // the row lives in registers (fully unrolled for n <= 64); R is read as
+  // shared-memory broadcasts
+  double zr[kCQMax];
+#pragma unroll
+  for (int c = 0; c < kCQMax; ++c) zr[c] = c < n ? Y[i + (int64_t)c * ldy] : 0.0;
+#pragma unroll
+  for (int c = 0; c < kCQMax; ++c) {
+    if (c < n) {
+      double s = zr[c];
+      const double* rc = Rs + c * n;  // column c of R: R(t, c), t < c
+#pragma unroll
+      for (int t = 0; t < c; ++t) s = fma(-zr[t], rc[t], s);
+      zr[c] = s * ri[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kCQMax; ++c)
+    if (c < n) Q[i + (int64_t)c * ldq] = zr[c];
+}
+
+// R = (R3 R2) R1 for upper-triangular n x n factors (ld n), problem
+// blockIdx.x, operands staged in shared memory.
+__global__ void __launch_bounds__(kCQ) trmm3_upper_kernel(const double* __restrict__ R1, const double* __restrict__ R2,
+                                                          const double* __restrict__ R3, int64_t sIn, int n,
+                                                          double* __restrict__ Rout, int64_t sOut, int64_t ldo,
+                                                          const int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) double tm[];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (status[b]) return;
+  const int nn = n * n;
+  double* A = tm;
+  double* B = tm + nn;
+  for (int e = tid; e < nn; e += kCQ) {
+    A[e] = R3[b * sIn + e];
+    B[e] = R2[b * sIn + e];
+  }
+  __syncthreads();
+  constexpr int kPer = (kCQMax * kCQMax + kCQ - 1) / kCQ;
+  double t3[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {  // T = R3 R2 (upper)
+    const int e = tid + q * kCQ;
+    double acc = 0.0;
+    if (e < nn) {
+      const int i = e % n, c = e / n;
+      for (int t = i; t <= c; ++t) acc = fma(A[i + t * n], B[t + c * n], acc);
+    }
+    t3[q] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int e = tid + q * kCQ;
+    if (e < nn) {
+      A[e] = t3[q];
+      B[e] = R1[b * sIn + e];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nn; e += kCQ) {  // R = T R1
+    const int i = e % n, c = e / n;
+    double acc = 0.0;
+    for (int t = i; t <= c; ++t) acc = fma(A[i + t * n], B[t + c * n], acc);
+    Rout[b * sOut + i + (int64_t)c * ldo] = i <= c ? acc : 0.0;
+  }
+}
+
+static int64_t gram_chunks(int64_t m) { return (m + kGR - 1) / kGR; }
+
+size_t cholqr3_workspace_doubles(int64_t m, int n) {
+  return (size_t)m * n + (size_t)gram_chunks(m) * n * n + 3 * (size_t)n * n + kCQMax + 8;
+}
+
+// Batched shifted CholeskyQR3 of nb problems Y_b (m x n, n <= 64): Q_b
+// (ld ldq) and R_b (ld n) as thin_qr. ws: nb * cholqr3_workspace_doubles.
+// status (device, nb ints) is zeroed here; status[b] != 0 marks a breakdown.
+int launch_cholqr3_batched(Context* cx, const double* Y, int64_t ldy, int64_t sY, int64_t m, int n, double* Q,
+                           int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws,
+                           int32_t* status) {
+  if (n > kCQMax || ldr != n || m < n) return SLRA_ERR_UNSUPPORTED;
+  const int64_t per = (int64_t)cholqr3_workspace_doubles(m, n);
+  const int64_t nn = (int64_t)n * n, nch = gram_chunks(m);
+  // per problem: T (m x n) | partial Grams (nch x n x n) | R1 | R2 | R3 | rinv
+  double* T = ws;
+  double* P = ws + m * n;
+  double* R1 = P + nch * nn;
+  double* rinv = R1 + 3 * nn;
+  const double shift_coef = 11.0 * ((double)m * n + (double)n * (n + 1)) * (2.220446049250313e-16 / 2);  // u = eps/2
+  const size_t tsm_bytes = sizeof(double) * ((size_t)n * n + n);
+  const size_t gsm_bytes = sizeof(double) * (size_t)(kGR + 1) * n;
+  SLRA_CUDA(cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm_bytes));
+  SLRA_CUDA(cudaFuncSetAttribute(gram_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm_bytes));
+  SLRA_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * nb, cx->stream));
+  const double* src[3] = {Y, Q, T};
+  const int64_t lds[3] = {ldy, ldq, m}, ss[3] = {sY, sQ, per};
+  double* dst[3] = {Q, T, Q};
+  const int64_t ldd[3] = {ldq, m, ldq}, sd[3] = {sQ, per, sQ};
+  const dim3 gg((unsigned)nch, (unsigned)nb), tg((unsigned)((m + 127) / 128), (unsigned)nb);
+  for (int pass = 0; pass < 3; ++pass) {
+    double* Rk = R1 + pass * nn;
+    SLRA_TIMED(cx, "cholqr_gram", gram_partial_kernel<<<gg, kCQ, gsm_bytes, cx->stream>>>(src[pass], lds[pass], ss[pass], m,
+                                                                                       n, P, per, status);)
+    SLRA_CHECK_LAUNCH(cx);
+    SLRA_TIMED(cx, "cholqr_chol",
+               chol_small_kernel<<<nb, kCQ, 0, cx->stream>>>(P, per, (int)nch, n, pass == 0 ? shift_coef : 0.0, Rk,
+                                                             per, rinv, per, status);)
+    SLRA_CHECK_LAUNCH(cx);
+    SLRA_TIMED(cx, "cholqr_trsm",
+               trsm_rows_kernel<<<tg, 128, tsm_bytes, cx->stream>>>(src[pass], lds[pass], ss[pass], m, n, Rk, per,
+                                                                    rinv, per, dst[pass], ldd[pass], sd[pass],
+                                                                    status);)
+    SLRA_CHECK_LAUNCH(cx);
+  }
+  const size_t msm_bytes = sizeof(double) * 2 * (size_t)nn;
+  SLRA_CUDA(cudaFuncSetAttribute(trmm3_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm_bytes));
+  SLRA_TIMED(cx, "cholqr_trmm", trmm3_upper_kernel<<<nb, kCQ, msm_bytes, cx->stream>>>(R1, R1 + nn, R1 + 2 * nn, per, n, R, sR,
+                                                                            ldr, status);)
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}
+
+}  // namespace slra_dev

@@ -705,42 +705,57 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
   // stop); 16*p*eps keeps sigma accurate to O(tol^2) relative and the
   // vectors to O(tol / gap)
   const double tol = 16.0 * (double)p * kEps;
+  const double tol2 = tol * tol;
   if (tid == 0) flag[0] = flag[1] = 0;
+  __shared__ double cmax2[NW];
   __syncthreads();
   const int npairs = ne / 2;
   const int iters = (npairs + 4 * NW - 1) / (4 * NW);
   for (int sweep = 0; sweep < 40; ++sweep) {
     const int fl = sweep & 1;
     double thr2 = 0.0;
-    if (deflate > 0.0) {
-      if (warp == 0) {
-        double mx = 0.0;
-        for (int j = 0; j < n; ++j) {
-          double s = 0.0;
-          for (int i = lane; i < p; i += 32) s = fma(W[i + j * ldw], W[i + j * ldw], s);
-          s = warp_sum(s);
-          mx = fmax(mx, s);
-        }
-        if (lane == 0) dmax2 = mx;
+    if (deflate > 0.0) {  // largest squared column norm, columns spread over the warps
+      double mx = 0.0;
+      for (int j = warp; j < n; j += NW) {
+        double s = 0.0;
+        for (int i = lane; i < p; i += 32) s = fma(W[i + j * ldw], W[i + j * ldw], s);
+        mx = fmax(mx, warp_sum(s));
+      }
+      if (lane == 0) cmax2[warp] = mx;
+      __syncthreads();
+      if (tid == 0) {
+        double m2 = 0.0;
+        for (int w = 0; w < NW; ++w) m2 = fmax(m2, cmax2[w]);
+        dmax2 = m2;
       }
       __syncthreads();
       thr2 = deflate * deflate * dmax2;
     }
+    int ab_next = pair_tab[(warp * 4 + grp) < npairs ? (warp * 4 + grp) : 0];
     for (int rd = 0; rd < ne - 1; ++rd) {
       for (int it = 0; it < iters; ++it) {
         const int pi = (warp + it * NW) * 4 + grp;
-        const int ab = pair_tab[rd * npairs + (pi < npairs ? pi : 0)];
+        const int ab = (iters == 1) ? ab_next : pair_tab[rd * npairs + (pi < npairs ? pi : 0)];
         const bool valid = pi < npairs && (ab & 255) < n;
         const int a = ab >> 8, b = valid ? (ab & 255) : a;
         double* wp = W + a * ldw;
         double* wq = W + b * ldw;
-        double x[RPG], y[RPG];
+        double* vp = V + a * ldv;
+        double* vq = V + b * ldv;
+        // W and V rows of both columns up front: every load is in flight
+        // before the reduction and rotation chain starts
+        double x[RPG], y[RPG], u[RPG], v[RPG];
         double aa = 0.0, bb = 0.0, gg = 0.0;
 #pragma unroll
         for (int r = 0; r < RPG; ++r) {
           const int i = sub + 8 * r;
           x[r] = i < p ? wp[i] : 0.0;
           y[r] = i < p ? wq[i] : 0.0;
+          u[r] = i < n ? vp[i] : 0.0;
+          v[r] = i < n ? vq[i] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < RPG; ++r) {
           aa = fma(x[r], x[r], aa);
           bb = fma(y[r], y[r], bb);
           gg = fma(x[r], y[r], gg);
@@ -751,10 +766,17 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
           bb += __shfl_xor_sync(0xffffffffu, bb, o);
           gg += __shfl_xor_sync(0xffffffffu, gg, o);
         }
-        if (!valid || gg == 0.0 || fabs(gg) <= tol * sqrt(aa * bb)) continue;
+        // the next round's pair, read before this round's barrier
+        if (iters == 1 && rd + 1 < ne - 1) ab_next = pair_tab[(rd + 1) * npairs + (pi < npairs ? pi : 0)];
+        // |g| <= tol sqrt(a b), squared (no sqrt on the chain)
+        if (!valid || gg == 0.0 || gg * gg <= tol2 * (aa * bb)) continue;
         if (aa < thr2 && bb < thr2) continue;
-        const double zeta = (bb - aa) * __drcp_rn(2.0 * gg);
-        const double t = copysign(__drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+        // t = sign(z) / (|z| + sqrt(1 + z^2)), z = (b - a) / (2g), written as
+        // t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), d = b - a: one sqrt, one
+        // division, one rsqrt on the dependent chain
+        const double d = bb - aa, g2 = 2.0 * gg;
+        const double rr = sqrt(fma(d, d, g2 * g2));
+        const double t = copysign(1.0, d) * g2 / (fabs(d) + rr);
         const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
 #pragma unroll
@@ -764,16 +786,9 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
             wp[i] = cs * x[r] - sn * y[r];
             wq[i] = sn * x[r] + cs * y[r];
           }
-        }
-        double* vp = V + a * ldv;
-        double* vq = V + b * ldv;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int i = sub + 8 * r;
           if (i < n) {
-            const double u = vp[i], v = vq[i];
-            vp[i] = cs * u - sn * v;
-            vq[i] = sn * u + cs * v;
+            vp[i] = cs * u[r] - sn * v[r];
+            vq[i] = sn * u[r] + cs * v[r];
           }
         }
         if (sub == 0) flag[fl] = 1;

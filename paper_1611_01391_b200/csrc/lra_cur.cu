@@ -20,6 +20,10 @@ int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, dou
 int launch_lowrank_residual(Context* c, const double* A, int64_t lda, int64_t m, int64_t n, const double* P,
                             int64_t ldp, const double* Q, int64_t ldq, int64_t inner, double* d_out);
 size_t tsqr_workspace_doubles(int64_t m, int c);
+size_t cholqr3_workspace_doubles(int64_t m, int n);
+int launch_cholqr3_batched(Context* cx, const double* Y, int64_t ldy, int64_t sY, int64_t m, int n, double* Q,
+                           int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws,
+                           int32_t* status);
 int launch_thin_qr_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int64_t m, int c, double* Q,
                            int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws);
 int launch_svd_small_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int m, int n, double* S,
@@ -113,7 +117,8 @@ int slra_range_finder_batched(slra_ctx ctx, const double* M, int64_t ldm, int64_
   const int64_t ucols = variant == 1 ? r : l;
   if (ldu < m || ldv < ucols) return SLRA_ERR_INVALID_ARGUMENT;
   const size_t tw = tsqr_workspace_doubles(m, (int)l);
-  const size_t per = 2 * (size_t)m * l + 3 * (size_t)l * l + (size_t)l + tw;
+  const size_t cw = cholqr3_workspace_doubles(m, (int)l);
+  const size_t per = 2 * (size_t)m * l + 3 * (size_t)l * l + (size_t)l + tw + cw;
   double* buf = static_cast<double*>(arena(cx, 0, sizeof(double) * (per * nsk + 64)));
   if (!buf) return SLRA_ERR_CUDA;
   const int64_t sMH = m * l, sLL = l * l;
@@ -124,20 +129,40 @@ int slra_range_finder_batched(slra_ctx ctx, const double* M, int64_t ldm, int64_
   double* VR = UR + (size_t)nsk * sLL;
   double* sig = VR + (size_t)nsk * sLL;  // nsk x l
   double* tws = sig + (size_t)nsk * l;   // TSQR workspace (nsk problems)
+  double* cws = tws + (size_t)nsk * tw;  // CholeskyQR3 workspace (nsk problems)
   double** dptr = reinterpret_cast<double**>(static_cast<char*>(cx->dsmall) + 2048);  // 2*nsk pointers
+  int32_t* cq_status = reinterpret_cast<int32_t*>(static_cast<char*>(cx->dsmall) + 3584);  // nsk flags
   for (int s = 0; s < nsk; ++s)
     SLRA_TRY(launch_sketch_cols(cx, M, ldm, m, h_src[s], h_coef[s], h_q[s], h_width[s], h_tree[s], l,
                                 MH + s * sMH, m));
-  SLRA_TRY(launch_thin_qr_batched(cx, MH, m, sMH, m, (int)l, Qm, m, sMH, Rm, l, sLL, nsk, tw ? tws : nullptr));
+  // Q R of the sketch: shifted CholeskyQR3 (cholqr.cu); a breakdown falls
+  // back to the Householder TSQR below, after the one host sync
+  SLRA_TRY(launch_cholqr3_batched(cx, MH, m, sMH, m, (int)l, Qm, m, sMH, Rm, l, sLL, nsk, cws, cq_status));
   // TruncatedRankR only needs the top r triplets and the count of sigma above
   // the cut: Jacobi skips pairs of columns below cut / sqrt(l) (dense_cta.cuh)
   const double deflate = variant == 1 ? 1e-10 / sqrt((double)l) : 0.0;
   SLRA_TRY(launch_svd_small_batched(cx, Rm, l, sLL, (int)l, (int)l, UR, l, sLL, sig, l, VR, l, sLL, nsk, deflate));
-  if (d_sigma) SLRA_CUDA(cudaMemcpyAsync(d_sigma, sig, 8 * l * nsk, cudaMemcpyDeviceToDevice, cx->stream));
   // rank check: numerical_rank(MH, 1e-10, Relative) < r -> RangeFailure
-  double* hs = static_cast<double*>(cx->hsmall);
+  std::vector<double> hsv((size_t)nsk * l);
+  std::vector<int32_t> hq((size_t)nsk);
+  double* hs = hsv.data();
+  SLRA_CUDA(cudaMemcpyAsync(hq.data(), cq_status, 4 * nsk, cudaMemcpyDeviceToHost, cx->stream));
   SLRA_CUDA(cudaMemcpyAsync(hs, sig, 8 * l * nsk, cudaMemcpyDeviceToHost, cx->stream));
   SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+  bool redo = false;
+  for (int s = 0; s < nsk; ++s)
+    if (hq[s]) {
+      redo = true;
+      SLRA_TRY(launch_thin_qr_batched(cx, MH + s * sMH, m, sMH, m, (int)l, Qm + s * sMH, m, sMH, Rm + s * sLL, l, sLL,
+                                      1, tw ? tws : nullptr));
+      SLRA_TRY(launch_svd_small_batched(cx, Rm + s * sLL, l, sLL, (int)l, (int)l, UR + s * sLL, l, sLL, sig + s * l,
+                                        l, VR + s * sLL, l, sLL, 1, deflate));
+    }
+  if (redo) {
+    SLRA_CUDA(cudaMemcpyAsync(hs, sig, 8 * l * nsk, cudaMemcpyDeviceToHost, cx->stream));
+    SLRA_CUDA(cudaStreamSynchronize(cx->stream));
+  }
+  if (d_sigma) SLRA_CUDA(cudaMemcpyAsync(d_sigma, sig, 8 * l * nsk, cudaMemcpyDeviceToDevice, cx->stream));
   int first_fail = -1;
   std::vector<int> ok(nsk, 1);
   for (int s = 0; s < nsk; ++s) {

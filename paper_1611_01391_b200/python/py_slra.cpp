@@ -76,14 +76,14 @@ static py::dict plan_dict(const SketchPlan& p) {
 
 PYBIND11_MODULE(_slra, m) {
   m.doc() = "B200 slra hot path: C++ host layer over the sm_100a C-ABI (libslra_cuda.so)";
-  auto base = py::register_exception<std::runtime_error>(m, "SlraRuntimeError");
-  py::register_exception<RangeFailure>(m, "RangeFailure", base.ptr());
-  py::register_exception<SketchRankFailure>(m, "SketchRankFailure", base.ptr());
-  py::register_exception<PremultRankFailure>(m, "PremultRankFailure", base.ptr());
-  py::register_exception<SelectionFailure>(m, "SelectionFailure", base.ptr());
-  py::register_exception<GeneratorRankFailure>(m, "GeneratorRankFailure", base.ptr());
-  py::register_exception<EmptySample>(m, "EmptySample", base.ptr());
-  py::register_exception<DeviceError>(m, "DeviceError", base.ptr());
+  auto base = py::register_local_exception<std::runtime_error>(m, "SlraRuntimeError");
+  py::register_local_exception<RangeFailure>(m, "RangeFailure", base.ptr());
+  py::register_local_exception<SketchRankFailure>(m, "SketchRankFailure", base.ptr());
+  py::register_local_exception<PremultRankFailure>(m, "PremultRankFailure", base.ptr());
+  py::register_local_exception<SelectionFailure>(m, "SelectionFailure", base.ptr());
+  py::register_local_exception<GeneratorRankFailure>(m, "GeneratorRankFailure", base.ptr());
+  py::register_local_exception<EmptySample>(m, "EmptySample", base.ptr());
+  py::register_local_exception<DeviceError>(m, "DeviceError", base.ptr());
 
   m.def("set_device", [](int dev, uintptr_t stream) { set_device(dev, reinterpret_cast<void*>(stream)); },
         py::arg("device") = 0, py::arg("stream") = 0);
