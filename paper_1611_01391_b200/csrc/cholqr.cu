@@ -15,9 +15,13 @@
 // breakdown (cond(Y) beyond ~1/u, e.g. an exactly rank-deficient sketch) sets
 // status[b] = 1 and the caller falls back to the Householder TSQR.
 //
-// Kernels per pass: gram_partial_kernel (row chunks -> partial n x n Grams,
-// no atomics), chol_small_kernel (sums the partials in a fixed order, shift,
-// Cholesky, 1/R(i,i)), trsm_rows_kernel (Q = Y R^-1, a thread per row).
+// Kernels per pass (templated on NP = n rounded up to a multiple of 8, so
+// every loop bound is a compile-time constant — FP64 dependent latency is
+// ~24 cycles here and index/predicate arithmetic was most of the issue
+// slots): gram_partial_kernel (row chunks -> partial NP x NP Grams, no
+// atomics), chol_small_kernel (sums the partials in a fixed order, shift,
+// Cholesky padded with the identity beyond n, 1/R(i,i)), trsm_rows_kernel
+// (Q = Y R^-1, a thread per row, right-looking in registers).
 #include "common.cuh"
 
 namespace slra_dev {
@@ -27,7 +31,8 @@ constexpr int kCQMax = 64;
 constexpr int kGR = 128;  // rows per Gram chunk
 
 // P_{b,k} = Y_b(chunk k, :)^T Y_b(chunk k, :) for chunk k = blockIdx.x
-// (upper triangle only).
+// (upper triangle, NP x NP with zero columns beyond n).
+template <int NP>
 __global__ void __launch_bounds__(kCQ) gram_partial_kernel(const double* __restrict__ Y, int64_t ldy, int64_t sY,
                                                            int64_t m, int n, double* __restrict__ P, int64_t sP,
                                                            const int32_t* __restrict__ status) {
@@ -39,93 +44,106 @@ __global__ void __launch_bounds__(kCQ) gram_partial_kernel(const double* __restr
   const int64_t r0 = (int64_t)k * kGR;
   const int rows = (int)((m - r0) < kGR ? (m - r0) : kGR);
 #pragma unroll 4
-  for (int e = tid; e < kGR * n; e += kCQ) {
-    const int i = e % kGR, c = e / kGR;  // kGR is a power of two
-    T[i + c * ldt] = i < rows ? Y[(r0 + i) + (int64_t)c * ldy] : 0.0;
+  for (int e = tid; e < kGR * NP; e += kCQ) {
+    const int i = e % kGR, c = e / kGR;
+    T[i + c * ldt] = (i < rows && c < n) ? Y[(r0 + i) + (int64_t)c * ldy] : 0.0;
   }
   __syncthreads();
-  double* out = P + b * sP + (int64_t)k * n * n;
-  for (int e = tid; e < n * n; e += kCQ) {
-    const int i = e % n, c = e / n;
-    if (i > c) continue;
-    const double* a = T + i * ldt;
-    const double* d = T + c * ldt;
-    double acc0 = 0.0, acc1 = 0.0;
+  double* out = P + b * sP + (int64_t)k * NP * NP;
+  constexpr int NB = NP / 2;  // 2 x 2 output blocks: four independent FMA chains per thread
+  for (int e = tid; e < NB * NB; e += kCQ) {
+    const int bi = e % NB, bc = e / NB;
+    if (bi > bc) continue;
+    const int i0 = 2 * bi, c0 = 2 * bc;
+    const double* a0 = T + i0 * ldt;
+    const double* d0 = T + c0 * ldt;
+    double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
 #pragma unroll 8
-    for (int t = 0; t < kGR; t += 2) {
-      acc0 = fma(a[t], d[t], acc0);
-      acc1 = fma(a[t + 1], d[t + 1], acc1);
+    for (int t = 0; t < kGR; ++t) {
+      const double x0 = a0[t], x1 = a0[t + ldt], y0 = d0[t], y1 = d0[t + ldt];
+      s00 = fma(x0, y0, s00);
+      s01 = fma(x0, y1, s01);
+      s10 = fma(x1, y0, s10);
+      s11 = fma(x1, y1, s11);
     }
-    out[i + c * n] = acc0 + acc1;
+    out[i0 + c0 * NP] = s00;
+    out[i0 + (c0 + 1) * NP] = s01;
+    out[(i0 + 1) + c0 * NP] = s10;  // below the diagonal when bi == bc: unused
+    out[(i0 + 1) + (c0 + 1) * NP] = s11;
   }
 }
 
-// Upper Cholesky factor R of G + shift*I where G = sum of the nchunk partial
-// Grams (upper triangles, summed in chunk order); shift = shift_coef *
-// trace(G). One CTA per problem, a thread per row for the updates. Writes R
-// (ld n, zeros below) and 1/R(i,i). A breakdown sets status[b] = 1.
+// Upper Cholesky factor R of G + shift*I (first n entries) padded with the
+// identity beyond n, where G = the sum of the nchunk partial Grams (chunk
+// order fixed); shift = shift_coef * trace(G). Thread (row ti, phase tc)
+// owns L(ti, c) for c = tc, tc + 4, ...: each column step stages column j in
+// registers, then writes (two barriers per step). Writes R (n x n, ld n),
+// and 1/R(i,i) for all NP entries. A breakdown sets status[b] = 1.
+template <int NP>
 __global__ void __launch_bounds__(kCQ) chol_small_kernel(const double* __restrict__ P, int64_t sP, int nchunk, int n,
                                                          double shift_coef, double* __restrict__ R, int64_t sR,
                                                          double* __restrict__ rinv, int64_t sRi,
                                                          int32_t* __restrict__ status) {
-  __shared__ double L[kCQMax * (kCQMax + 1)];  // L(i, c) at i + c * ld, lower triangle
+  constexpr int ld = NP + 1;
+  __shared__ double L[NP * ld];  // L(i, c) at i + c * ld, lower triangle
   __shared__ double red[40];
   __shared__ int fail;
   const int b = blockIdx.x, tid = threadIdx.x;
   if (status[b]) return;
-  const int ld = n + 1;
   P += b * sP;
   R += b * sR;
   rinv += b * sRi;
-  const int64_t nn = (int64_t)n * n;
-  for (int e = tid; e < n * n; e += kCQ) {
-    const int i = e % n, c = e / n;
+  constexpr int NN = NP * NP;
+  for (int e = tid; e < NN; e += kCQ) {
+    const int i = e % NP, c = e / NP;
     if (i > c) continue;
-    double s = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < nchunk; ++k) s += P[k * nn + e];  // fixed order; loads issued ahead
+    double s = 0.0;  // chunk order fixed; each batch of 8 loads in flight before the adds
+    int k = 0;
+    for (; k + 8 <= nchunk; k += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = P[(k + u) * NN + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; k < nchunk; ++k) s += P[k * NN + e];
     L[c + i * ld] = s;  // lower: L(c, i) = G(i, c), c >= i
   }
   __syncthreads();
   double tr = 0.0;
   for (int i = tid; i < n; i += kCQ) tr += L[i + i * ld];
   tr = block_sum<kCQ>(tr, red);
-  for (int i = tid; i < n; i += kCQ) L[i + i * ld] += shift_coef * tr;
+  for (int i = tid; i < NP; i += kCQ) L[i + i * ld] = i < n ? L[i + i * ld] + shift_coef * tr : 1.0;
   if (tid == 0) fail = 0;
   __syncthreads();
-  {
-    // thread (row ti, phase tc) owns L(ti, c) for c = tc, tc + 4, ...: each
-    // step stages column j in registers, then writes (2 barriers per step,
-    // no load/store aliasing chains)
-    constexpr int kQ = kCQMax / 4;
-    const int ti = tid & 63, tc = tid >> 6;
-    for (int j = 0; j < n; ++j) {
-      const double piv = L[j + j * ld];
-      if (!(piv > 0.0)) {  // uniform: every thread read the same pivot
-        if (tid == 0) fail = 1;
-        break;
-      }
-      const double ljj = sqrt(piv);
-      const double inv = 1.0 / ljj;
-      const bool row = ti > j && ti < n;
-      const double lij = row ? L[ti + j * ld] * inv : 0.0;
-      double lcj[kQ], cur[kQ];
-#pragma unroll
-      for (int q = 0; q < kQ; ++q) {
-        const int c = tc + 4 * q;
-        const bool act = row && c > j && c <= ti;
-        lcj[q] = act ? L[c + j * ld] * inv : 0.0;
-        cur[q] = act ? L[ti + c * ld] : 0.0;
-      }
-      __syncthreads();
-      if (tc == 0 && ti >= j && ti < n) L[ti + j * ld] = (ti == j) ? ljj : lij;
-#pragma unroll
-      for (int q = 0; q < kQ; ++q) {
-        const int c = tc + 4 * q;
-        if (row && c > j && c <= ti) L[ti + c * ld] = cur[q] - lij * lcj[q];
-      }
-      __syncthreads();
+  constexpr int kQ = (NP + 3) / 4;
+  const int ti = tid & 63, tc = tid >> 6;
+  for (int j = 0; j < NP; ++j) {
+    const double piv = L[j + j * ld];
+    if (!(piv > 0.0)) {  // uniform: every thread read the same pivot
+      if (tid == 0) fail = 1;
+      break;
     }
+    const double ljj = sqrt(piv);
+    const double inv = 1.0 / ljj;
+    const bool row = ti > j && ti < NP;
+    const double lij = row ? L[ti + j * ld] * inv : 0.0;
+    double lcj[kQ], cur[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int c = tc + 4 * q;
+      const bool act = row && c > j && c <= ti;
+      lcj[q] = act ? L[c + j * ld] * inv : 0.0;
+      cur[q] = act ? L[ti + c * ld] : 0.0;
+    }
+    __syncthreads();
+    if (tc == 0 && ti >= j && ti < NP) L[ti + j * ld] = (ti == j) ? ljj : lij;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int c = tc + 4 * q;
+      if (row && c > j && c <= ti) L[ti + c * ld] = cur[q] - lij * lcj[q];
+    }
+    __syncthreads();
   }
   __syncthreads();
   if (fail) {
@@ -136,50 +154,48 @@ __global__ void __launch_bounds__(kCQ) chol_small_kernel(const double* __restric
     const int i = e % n, c = e / n;  // R(i, c) = L(c, i) for i <= c
     R[e] = (i <= c) ? L[c + i * ld] : 0.0;
   }
-  for (int i = tid; i < n; i += kCQ) rinv[i] = 1.0 / L[i + i * ld];
+  for (int i = tid; i < NP; i += kCQ) rinv[i] = 1.0 / L[i + i * ld];
 }
 
-// Q(i, :) = Y(i, :) R^-1 for every row i (forward substitution along the
-// columns of the upper R), one thread per row; problem blockIdx.y. Dynamic
-// shared memory: R (n x n) | 1/R(i,i) (n) | z (n x 128, thread-major).
+// Q(i, :) = Y(i, :) R^-1 for every row i, one thread per row; problem
+// blockIdx.y. R (n x n, ld n) is padded to NP x NP with the identity in
+// shared memory; the row lives in registers and the substitution is
+// right-looking (each final z(c) updates the later entries), so the
+// dependent chain is one multiply + one FMA per column.
+template <int NP>
 __global__ void __launch_bounds__(128) trsm_rows_kernel(const double* __restrict__ Y, int64_t ldy, int64_t sY,
                                                         int64_t m, int n, const double* __restrict__ R, int64_t sR,
                                                         const double* __restrict__ rinv, int64_t sRi,
                                                         double* __restrict__ Q, int64_t ldq, int64_t sQ,
                                                         const int32_t* __restrict__ status) {
-  extern __shared__ __align__(16) double tsm[];
-  double* Rs = tsm;
-  double* ri = Rs + n * n;
-  double* z = ri + n;  // z[c * 128 + tid]
+  __shared__ double Rs[NP * NP];
+  __shared__ double ri[NP];
   const int b = blockIdx.y, tid = threadIdx.x;
   if (status[b]) return;
   Y += b * sY;
   Q += b * sQ;
   R += b * sR;
   rinv += b * sRi;
-  for (int e = tid; e < n * n; e += 128) Rs[e] = R[e];
-  for (int c = tid; c < n; c += 128) ri[c] = rinv[c];
+  for (int e = tid; e < NP * NP; e += 128) {
+    const int r = e % NP, c = e / NP;
+    Rs[e] = (r < n && c < n) ? R[r + c * n] : (r == c ? 1.0 : 0.0);
+  }
+  for (int c = tid; c < NP; c += 128) ri[c] = rinv[c];
   __syncthreads();
   const int64_t i = blockIdx.x * 128LL + tid;
   if (i >= m) return;
-  (void)z;
-  // the row lives in registers (fully unrolled for n <= 64); R is read as
-  // shared-memory broadcasts
-  double zr[kCQMax];
+  double zr[NP];
 #pragma unroll
-  for (int c = 0; c < kCQMax; ++c) zr[c] = c < n ? Y[i + (int64_t)c * ldy] : 0.0;
+  for (int c = 0; c < NP; ++c) zr[c] = c < n ? Y[i + (int64_t)c * ldy] : 0.0;
 #pragma unroll
-  for (int c = 0; c < kCQMax; ++c) {
-    if (c < n) {
-      double s = zr[c];
-      const double* rc = Rs + c * n;  // column c of R: R(t, c), t < c
+  for (int c = 0; c < NP; ++c) {
+    const double z = zr[c] * ri[c];
+    zr[c] = z;
 #pragma unroll
-      for (int t = 0; t < c; ++t) s = fma(-zr[t], rc[t], s);
-      zr[c] = s * ri[c];
-    }
+    for (int c2 = c + 1; c2 < NP; ++c2) zr[c2] = fma(-z, Rs[c + c2 * NP], zr[c2]);
   }
 #pragma unroll
-  for (int c = 0; c < kCQMax; ++c)
+  for (int c = 0; c < NP; ++c)
     if (c < n) Q[i + (int64_t)c * ldq] = zr[c];
 }
 
@@ -233,28 +249,24 @@ __global__ void __launch_bounds__(kCQ) trmm3_upper_kernel(const double* __restri
 static int64_t gram_chunks(int64_t m) { return (m + kGR - 1) / kGR; }
 
 size_t cholqr3_workspace_doubles(int64_t m, int n) {
-  return (size_t)m * n + (size_t)gram_chunks(m) * n * n + 3 * (size_t)n * n + kCQMax + 8;
+  return (size_t)m * n + (size_t)gram_chunks(m) * kCQMax * kCQMax + 3 * (size_t)n * n + kCQMax + 8;
 }
 
-// Batched shifted CholeskyQR3 of nb problems Y_b (m x n, n <= 64): Q_b
-// (ld ldq) and R_b (ld n) as thin_qr. ws: nb * cholqr3_workspace_doubles.
-// status (device, nb ints) is zeroed here; status[b] != 0 marks a breakdown.
-int launch_cholqr3_batched(Context* cx, const double* Y, int64_t ldy, int64_t sY, int64_t m, int n, double* Q,
-                           int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws,
-                           int32_t* status) {
-  if (n > kCQMax || ldr != n || m < n) return SLRA_ERR_UNSUPPORTED;
+template <int NP>
+static int cholqr3_passes(Context* cx, const double* Y, int64_t ldy, int64_t sY, int64_t m, int n, double* Q,
+                          int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws,
+                          int32_t* status) {
   const int64_t per = (int64_t)cholqr3_workspace_doubles(m, n);
   const int64_t nn = (int64_t)n * n, nch = gram_chunks(m);
-  // per problem: T (m x n) | partial Grams (nch x n x n) | R1 | R2 | R3 | rinv
+  // per problem: T (m x n) | partial Grams (nch x NP x NP) | R1 | R2 | R3 | rinv (NP)
   double* T = ws;
   double* P = ws + m * n;
-  double* R1 = P + nch * nn;
+  double* R1 = P + nch * kCQMax * kCQMax;
   double* rinv = R1 + 3 * nn;
   const double shift_coef = 11.0 * ((double)m * n + (double)n * (n + 1)) * (2.220446049250313e-16 / 2);  // u = eps/2
-  const size_t tsm_bytes = sizeof(double) * ((size_t)n * n + n);
-  const size_t gsm_bytes = sizeof(double) * (size_t)(kGR + 1) * n;
-  SLRA_CUDA(cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm_bytes));
-  SLRA_CUDA(cudaFuncSetAttribute(gram_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm_bytes));
+  const size_t gsm_bytes = sizeof(double) * (size_t)(kGR + 1) * NP;
+  SLRA_CUDA(cudaFuncSetAttribute(gram_partial_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)gsm_bytes));
   SLRA_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * nb, cx->stream));
   const double* src[3] = {Y, Q, T};
   const int64_t lds[3] = {ldy, ldq, m}, ss[3] = {sY, sQ, per};
@@ -263,25 +275,43 @@ int launch_cholqr3_batched(Context* cx, const double* Y, int64_t ldy, int64_t sY
   const dim3 gg((unsigned)nch, (unsigned)nb), tg((unsigned)((m + 127) / 128), (unsigned)nb);
   for (int pass = 0; pass < 3; ++pass) {
     double* Rk = R1 + pass * nn;
-    SLRA_TIMED(cx, "cholqr_gram", gram_partial_kernel<<<gg, kCQ, gsm_bytes, cx->stream>>>(src[pass], lds[pass], ss[pass], m,
-                                                                                       n, P, per, status);)
+    SLRA_TIMED(cx, "cholqr_gram", gram_partial_kernel<NP><<<gg, kCQ, gsm_bytes, cx->stream>>>(
+                                      src[pass], lds[pass], ss[pass], m, n, P, per, status);)
     SLRA_CHECK_LAUNCH(cx);
     SLRA_TIMED(cx, "cholqr_chol",
-               chol_small_kernel<<<nb, kCQ, 0, cx->stream>>>(P, per, (int)nch, n, pass == 0 ? shift_coef : 0.0, Rk,
-                                                             per, rinv, per, status);)
+               chol_small_kernel<NP><<<nb, kCQ, 0, cx->stream>>>(P, per, (int)nch, n, pass == 0 ? shift_coef : 0.0,
+                                                                 Rk, per, rinv, per, status);)
     SLRA_CHECK_LAUNCH(cx);
     SLRA_TIMED(cx, "cholqr_trsm",
-               trsm_rows_kernel<<<tg, 128, tsm_bytes, cx->stream>>>(src[pass], lds[pass], ss[pass], m, n, Rk, per,
-                                                                    rinv, per, dst[pass], ldd[pass], sd[pass],
-                                                                    status);)
+               trsm_rows_kernel<NP><<<tg, 128, 0, cx->stream>>>(src[pass], lds[pass], ss[pass], m, n, Rk, per, rinv,
+                                                                per, dst[pass], ldd[pass], sd[pass], status);)
     SLRA_CHECK_LAUNCH(cx);
   }
   const size_t msm_bytes = sizeof(double) * 2 * (size_t)nn;
   SLRA_CUDA(cudaFuncSetAttribute(trmm3_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm_bytes));
-  SLRA_TIMED(cx, "cholqr_trmm", trmm3_upper_kernel<<<nb, kCQ, msm_bytes, cx->stream>>>(R1, R1 + nn, R1 + 2 * nn, per, n, R, sR,
-                                                                            ldr, status);)
+  SLRA_TIMED(cx, "cholqr_trmm", trmm3_upper_kernel<<<nb, kCQ, msm_bytes, cx->stream>>>(R1, R1 + nn, R1 + 2 * nn, per,
+                                                                                        n, R, sR, ldr, status);)
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
+}
+
+// Batched shifted CholeskyQR3 of nb problems Y_b (m x n, n <= 64): Q_b
+// (ld ldq) and R_b (ld n) as thin_qr. ws: nb * cholqr3_workspace_doubles.
+// status (device, nb ints) is zeroed here; status[b] != 0 marks a breakdown.
+int launch_cholqr3_batched(Context* cx, const double* Y, int64_t ldy, int64_t sY, int64_t m, int n, double* Q,
+                           int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws,
+                           int32_t* status) {
+  if (n < 1 || n > kCQMax || ldr != n || m < n) return SLRA_ERR_UNSUPPORTED;
+  switch ((n + 7) / 8) {
+    case 1: return cholqr3_passes<8>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, ldr, sR, nb, ws, status);
+    case 2: return cholqr3_passes<16>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, ldr, sR, nb, ws, status);
+    case 3: return cholqr3_passes<24>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, ldr, sR, nb, ws, status);
+    case 4: return cholqr3_passes<32>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, ldr, sR, nb, ws, status);
+    case 5: return cholqr3_passes<40>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, ldr, sR, nb, ws, status);
+    case 6: return cholqr3_passes<48>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, ldr, sR, nb, ws, status);
+    case 7: return cholqr3_passes<56>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, ldr, sR, nb, ws, status);
+    default: return cholqr3_passes<64>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, ldr, sR, nb, ws, status);
+  }
 }
 
 }  // namespace slra_dev

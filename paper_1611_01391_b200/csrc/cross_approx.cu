@@ -44,7 +44,7 @@ struct CaSmem {
 
 __host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
-  size_t d = 2 * (size_t)mm * c + 4 * (size_t)c * c + 6 * (size_t)c + 2 * (size_t)mm + 40;
+  size_t d = 2 * (size_t)mm * c + 4 * (size_t)c * c + 8 * (size_t)c + 2 * (size_t)mm + 40;  // + odd-ld padding of W, V
   size_t i = (size_t)mm + 4 * (size_t)c + 8 + (size_t)c;
   return d * 8 + 33 * 8 + i * 4 + 64;
 }
@@ -54,10 +54,10 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   CaSmem s;
   double* d = reinterpret_cast<double*>(base);
   s.S = d; d += (size_t)mm * c;
-  s.W = d; d += (size_t)mm * c;
+  s.W = d; d += (size_t)mm * c + c;  // room for ld = p | 1
   s.R = d; d += c * c;
   s.Gt = d; d += c * c;
-  s.V = d; d += c * c;
+  s.V = d; d += c * c + c;  // room for ld = q | 1
   s.Tm = s.R;  // R (the selection's QR factor) is dead once the nucleus starts
   s.Sm = d; d += c * c;
   s.tau = d; d += c;
@@ -164,8 +164,8 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
   for (int e = tid; e < k * l; e += NT) {
     const int a = e % k, b = e / k;
     const double g = __ldg(A + I[a] + (int64_t)J[b] * lda);
-    if (tall) s.W[a + b * p] = g;
-    else s.W[b + a * p] = g;
+    if (tall) s.W[a + b * (p | 1)] = g;
+    else s.W[b + a * (p | 1)] = g;
   }
   __syncthreads();
   // Only sigma_i > 1e-10 sigma_1 enter the nucleus (pinv cut, linalg.cpp:111-121;
@@ -173,10 +173,10 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
   // column norm jointly carry less than that, so pairs of two such columns
   // are not rotated (the noise directions of rank-deficient generators, as in
   // configs 3 and 5, otherwise keep the sweeps going to the cap).
-  cta_jacobi<NT>(s.W, p, p, q, s.V, q, s.flag, 1e-10 / sqrt((double)q));
+  cta_jacobi<NT>(s.W, p | 1, p, q, s.V, q | 1, s.flag, 1e-10 / sqrt((double)q));
   // finish into S (p x q, ld p) and Gt (q x q, ld q): for tall G the left
   // vectors are in S; for wide G (SVD of G^T) they are the rows of V.
-  cta_svd_finish<NT>(s.W, p, p, q, s.V, q, s.sigma, s.order, s.S, p, s.Gt, q, s.sgn);
+  cta_svd_finish<NT>(s.W, p | 1, p, q, s.V, q | 1, s.sigma, s.order, s.S, p, s.Gt, q, s.sgn);
   if (!tall) {
     // G^T = S' Sigma V'^T -> G = V' Sigma S'^T: left vectors of G = V'
     // (columns of Gt), right = S'. Re-apply the sign rule on the left ones.

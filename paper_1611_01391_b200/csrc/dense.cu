@@ -297,23 +297,27 @@ __global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict_
   T += pb * sT;
   const bool tall = m > n;
   const int p = tall ? m : n, q = tall ? n : m;
-  double* W = sm;                   // p x q
-  double* V = W + (size_t)p * q;    // q x q
-  double* Ss = V + (size_t)q * q;   // p x q
-  double* Ts = Ss + (size_t)p * q;  // q x q
-  double* sg = Ts + (size_t)q * q;  // q
-  double* tmp = sg + q;             // q
+  // odd leading dimensions for the Jacobi operands: the 8-lane groups of a
+  // warp read four different columns, which an even ld would put on the
+  // same banks
+  const int ldw = p | 1, ldv = q | 1;
+  double* W = sm;                     // p x q (ld ldw)
+  double* V = W + (size_t)ldw * q;    // q x q (ld ldv)
+  double* Ss = V + (size_t)ldv * q;   // p x q
+  double* Ts = Ss + (size_t)p * q;    // q x q
+  double* sg = Ts + (size_t)q * q;    // q
+  double* tmp = sg + q;               // q
   int* order = reinterpret_cast<int*>(tmp + q);
   int* flag = order + q + 1;
   for (int j = 0; j < n; ++j)
     for (int i = threadIdx.x; i < m; i += kSVT) {
       const double x = A[i + (int64_t)j * lda];
-      if (tall) W[i + j * p] = x;
-      else W[j + i * p] = x;
+      if (tall) W[i + j * ldw] = x;
+      else W[j + i * ldw] = x;
     }
   __syncthreads();
-  cta_jacobi<kSVT>(W, p, p, q, V, q, flag, deflate);
-  cta_svd_finish<kSVT>(W, p, p, q, V, q, sg, order, Ss, p, Ts, q, tmp);
+  cta_jacobi<kSVT>(W, ldw, p, q, V, ldv, flag, deflate);
+  cta_svd_finish<kSVT>(W, ldw, p, q, V, ldv, sg, order, Ss, p, Ts, q, tmp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (!tall) {
     // left vectors of A are Ts (q x q = m x m); re-apply the sign rule on them
@@ -341,7 +345,8 @@ __global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict_
 
 static size_t svd_smem(int m, int n) {
   const int p = m > n ? m : n, q = m > n ? n : m;
-  return sizeof(double) * (2 * (size_t)p * q + 2 * (size_t)q * q + 2 * (size_t)q + 8) + sizeof(int) * (q + 8);
+  return sizeof(double) * (2 * (size_t)(p + 1) * q + 2 * (size_t)(q + 1) * q + 2 * (size_t)q + 8) +
+         sizeof(int) * (q + 8);
 }
 
 int launch_svd_small_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int m, int n, double* S,

@@ -712,7 +712,7 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
   const int npairs = ne / 2;
   const int iters = (npairs + 4 * NW - 1) / (4 * NW);
   for (int sweep = 0; sweep < 40; ++sweep) {
-    const int fl = sweep & 1;
+    int rot_any = 0;  // this thread rotated a pair during the sweep
     double thr2 = 0.0;
     if (deflate > 0.0) {  // largest squared column norm, columns spread over the warps
       double mx = 0.0;
@@ -754,11 +754,20 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
           u[r] = i < n ? vp[i] : 0.0;
           v[r] = i < n ? vq[i] : 0.0;
         }
+        {  // two accumulators per product: FP64 FMA latency is ~24 cycles on sm_100
+          double a1 = 0.0, b1 = 0.0, g1 = 0.0;
 #pragma unroll
-        for (int r = 0; r < RPG; ++r) {
-          aa = fma(x[r], x[r], aa);
-          bb = fma(y[r], y[r], bb);
-          gg = fma(x[r], y[r], gg);
+          for (int r = 0; r < RPG; r += 2) {
+            aa = fma(x[r], x[r], aa);
+            bb = fma(y[r], y[r], bb);
+            gg = fma(x[r], y[r], gg);
+            a1 = fma(x[r + 1], x[r + 1], a1);
+            b1 = fma(y[r + 1], y[r + 1], b1);
+            g1 = fma(x[r + 1], y[r + 1], g1);
+          }
+          aa += a1;
+          bb += b1;
+          gg += g1;
         }
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) {  // within the 8-lane group
@@ -775,7 +784,9 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
         // t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), d = b - a: one sqrt, one
         // division, one rsqrt on the dependent chain
         const double d = bb - aa, g2 = 2.0 * gg;
-        const double rr = sqrt(fma(d, d, g2 * g2));
+        // late sweeps: (2g/d)^2 below eps makes sqrt(d^2 + 4g^2) == |d| in
+        // FP64, so t = g / d exactly as rounded — skip the sqrt
+        const double rr = (g2 * g2 < 1e-17 * (d * d)) ? fabs(d) : sqrt(fma(d, d, g2 * g2));
         const double t = copysign(1.0, d) * g2 / (fabs(d) + rr);
         const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
@@ -791,17 +802,12 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
             vq[i] = sn * u[r] + cs * v[r];
           }
         }
-        if (sub == 0) flag[fl] = 1;
+        rot_any = 1;
       }
       __syncthreads();
     }
-    const int rotated = flag[fl];
-    if (tid == 0) {
-      flag[fl ^ 1] = 0;
-      flag[2] = sweep + 1;  // sweeps used (diagnostics)
-    }
-    __syncthreads();
-    if (!rotated) break;
+    if (tid == 0) flag[2] = sweep + 1;  // sweeps used (diagnostics)
+    if (!__syncthreads_or(rot_any)) break;
   }
 }
 

@@ -45,13 +45,20 @@ __global__ void __launch_bounds__(NT) probe(const double* A, int n, long long* c
       const int a = ab >> 8, b = valid ? (ab & 255) : a;
       double* wp = W + a * ldw;
       double* wq = W + b * ldw;
-      double x[RPG], y[RPG];
+      double* vp = V + a * ldv;
+      double* vq = V + b * ldv;
+      double x[RPG], y[RPG], u[RPG], v[RPG];
       double aa = 0.0, bb = 0.0, gg = 0.0;
 #pragma unroll
       for (int r = 0; r < RPG; ++r) {
         const int i = sub + 8 * r;
         x[r] = i < p ? wp[i] : 0.0;
         y[r] = i < p ? wq[i] : 0.0;
+        u[r] = i < n ? vp[i] : 0.0;
+        v[r] = i < n ? vq[i] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < RPG; ++r) {
         aa = fma(x[r], x[r], aa);
         bb = fma(y[r], y[r], bb);
         gg = fma(x[r], y[r], gg);
@@ -64,10 +71,11 @@ __global__ void __launch_bounds__(NT) probe(const double* A, int n, long long* c
         gg += __shfl_xor_sync(0xffffffffu, gg, o);
       }
       long long t2 = clock64(), t3 = t2, t4 = t2, t5 = t2;
-      const bool rot = valid && gg != 0.0 && fabs(gg) > tol * sqrt(aa * bb);
+      const bool rot = valid && gg != 0.0 && gg * gg > tol * tol * (aa * bb);
       if (rot) {
-        const double zeta = (bb - aa) * __drcp_rn(2.0 * gg);
-        const double t = copysign(__drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+        const double d = bb - aa, g2 = 2.0 * gg;
+        const double rr = sqrt(fma(d, d, g2 * g2));
+        const double t = copysign(1.0, d) * g2 / (fabs(d) + rr);
         const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
         t3 = clock64();
@@ -75,16 +83,10 @@ __global__ void __launch_bounds__(NT) probe(const double* A, int n, long long* c
         for (int r = 0; r < RPG; ++r) {
           const int i = sub + 8 * r;
           if (i < p) { wp[i] = cs * x[r] - sn * y[r]; wq[i] = sn * x[r] + cs * y[r]; }
+          if (i < n) { vp[i] = cs * u[r] - sn * v[r]; vq[i] = sn * u[r] + cs * v[r]; }
         }
         t4 = clock64();
-        double* vp = V + a * ldv;
-        double* vq = V + b * ldv;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int i = sub + 8 * r;
-          if (i < n) { const double u = vp[i], v = vq[i]; vp[i] = cs * u - sn * v; vq[i] = sn * u + cs * v; }
-        }
-        t5 = clock64();
+        t5 = t4;
         if (sub == 0) flag[fl] = 1;
       }
       __syncthreads();
