@@ -180,6 +180,21 @@ __device__ __forceinline__ ArgMax block_argmax(ArgMax a, double* rv, int64_t* ri
 // FP64 tensor-core MMA (sm_80+ mma.sync; SASS DMMA.8x8x4 on sm_100a).
 // A 8x4 row: a = A[lane>>2][lane&3]; B 4x8 col: b = B[lane&3][lane>>2];
 // C 8x8: c0,c1 = C[lane>>2][2*(lane&3) + {0,1}].
+// m16n8k16 FP64 MMA (SASS DMMA.16816: 8x the work of 8x8x4 per instruction).
+// Fragments (g = lane >> 2, t = lane & 3), from the PTX f64 m16n8k16 layout
+// (as in CuTe's SM90_16x8x16_F64F64F64F64_TN traits):
+//   a[v] = A[g + 8 (v & 1)][t + 4 (v >> 1)]      v = 0..7  (A 16 x 16, row)
+//   b[v] = B[t + 4 v][g]                          v = 0..3  (B 16 x 8, col)
+//   c[v] = C[g + 8 (v >> 1)][2 t + (v & 1)]       v = 0..3  (C 16 x 8)
+__device__ __forceinline__ void dmma_16x8x16(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+      "{%12,%13,%14,%15}, {%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]),
+        "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)

@@ -32,13 +32,14 @@ constexpr int NT = 256;        // 8 warps: 4 (rows) x 2 (cols), warp tile 32 x 1
 constexpr int TM = 128;        // tile rows
 constexpr int TN = 32;         // tile cols
 constexpr int KP = 32;         // inner dimension (padded)
-constexpr int LDU = TM + 4;    // Us[k][row]
+constexpr int LDU = TM + 2;    // Us[k][row]
 constexpr int LDV = KP + 4;    // Vs[col][k]
 constexpr int LDM = TM + 2;    // Ms[col][row]
 constexpr int U_D = KP * LDU;  // doubles per U buffer
 constexpr int V_D = TN * LDV;
 constexpr int M_D = TN * LDM;
-constexpr size_t SMEM = sizeof(double) * 2 * (U_D + V_D + M_D);
+constexpr int NS = 3;          // cp.async pipeline depth (tiles in flight)
+constexpr size_t SMEM = sizeof(double) * NS * (U_D + V_D + M_D);
 }  // namespace rs
 
 struct StreamResidualArgs {
@@ -100,80 +101,84 @@ __device__ __forceinline__ void rs_stage(const StreamResidualArgs& a, int64_t i0
 __global__ void __launch_bounds__(rs::NT, 1) residual_stream_kernel(StreamResidualArgs a) {
   using namespace rs;
   extern __shared__ __align__(16) double smem[];
-  // buffer b of U / V / M (pointer arithmetic, no local-memory pointer arrays)
-#define UB(b) (smem + (b) * U_D)
-#define VB(b) (smem + 2 * U_D + (b) * V_D)
-#define MB(b) (smem + 2 * U_D + 2 * V_D + (b) * M_D)
+  // stage slot s of U / V / M (pointer arithmetic, no local-memory pointer arrays)
+#define UB(s) (smem + (s) * U_D)
+#define VB(s) (smem + NS * U_D + (s) * V_D)
+#define MB(s) (smem + NS * U_D + NS * V_D + (s) * M_D)
   __shared__ double red[40];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t tiles_m = (a.m + TM - 1) / TM, tiles_n = (a.n + TN - 1) / TN;
   const int64_t tiles = tiles_m * tiles_n;
-  // contiguous tile range per CTA (row-fastest), so consecutive tiles share V
+  // contiguous tile range per CTA; NS tiles in flight (cp.async groups),
+  // so the HBM latency of a tile hides behind NS - 1 tiles of DMMA work
   const int64_t t0 = tiles * blockIdx.x / gridDim.x, t1 = tiles * (blockIdx.x + 1) / gridDim.x;
-  const int kc4 = (a.inner + 3) & ~3;
+  const int kc16 = (a.inner + 15) & ~15;
   double rsum = 0.0, nsum = 0.0;
-  int buf = 0;
-  int64_t vj = -1;   // column tile currently staged in Vb[vbuf]
-  int vbuf = 0;
-  if (t0 < t1) {
-    const int64_t i0 = (t0 % tiles_m) * TM, j0 = (t0 / tiles_m) * TN;
-    rs_stage(a, i0, j0, true, UB(0), VB(0), MB(0));
-    vj = j0;
-  }
-  cp_async_commit();
-  for (int64_t t = t0; t < t1; ++t) {
-    const int64_t i0 = (t % tiles_m) * TM, j0 = (t / tiles_m) * TN;
-    // prefetch the next tile into the other buffers
-    if (t + 1 < t1) {
-      const int64_t ni0 = ((t + 1) % tiles_m) * TM, nj0 = ((t + 1) / tiles_m) * TN;
-      const bool nv = nj0 != vj;
-      rs_stage(a, ni0, nj0, nv, UB(buf ^ 1), VB(nv ? (vbuf ^ 1) : vbuf), MB(buf ^ 1));
-    }
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    const int64_t t = t0 + s;
+    if (t < t1) rs_stage(a, (t % tiles_m) * TM, (t / tiles_m) * TN, true, UB(s), VB(s), MB(s));
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const double* Us = UB(buf);
-    const double* Vs = VB(vbuf);
-    const double* Ms = MB(buf);
-    double acc[4][2][2];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-    for (int kk = 0; kk < kc4; kk += 4) {
-      double af[4], bf[2];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) af[mi] = Us[(kk + t4) * LDU + wm * 32 + mi * 8 + g];
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) bf[ni] = Vs[(wn * 16 + ni * 8 + g) * LDV + kk + t4];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+  }
+  int slot = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    {  // prefetch tile t + NS - 1 into the slot freed by tile t - 1
+      const int64_t tp = t + NS - 1;
+      const int sp = (slot + NS - 1) % NS;
+      if (tp < t1) rs_stage(a, (tp % tiles_m) * TM, (tp / tiles_m) * TN, true, UB(sp), VB(sp), MB(sp));
+      cp_async_commit();
     }
+    cp_async_wait<NS - 1>();
+    __syncthreads();
+    const double* Us = UB(slot);
+    const double* Vs = VB(slot);
+    const double* Ms = MB(slot);
+    // warp tile 32 x 16 = 2 (16-row) x 2 (8-col) m16n8k16 blocks; K padded
+    // to 16 (the staged U / V tiles are zero-filled up to KP)
+    double acc[2][2][4];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int row = wm * 32 + mi * 8 + g, col = wn * 16 + ni * 8 + 2 * t4 + e;
-          const double x = Ms[col * LDM + row];  // zero outside A (zero-filled)
-          const double d = x - acc[mi][ni][e];
-          rsum = fma(d, d, rsum);
-          nsum = fma(x, x, nsum);
-        }
-    __syncthreads();  // buffers of this tile may be overwritten by the next prefetch
-    if (t + 1 < t1) {
-      const int64_t nj0 = ((t + 1) / tiles_m) * TN;
-      if (nj0 != vj) {
-        vbuf ^= 1;
-        vj = nj0;
-      }
+        for (int v = 0; v < 4; ++v) acc[mi][ni][v] = 0.0;
+    for (int kk = 0; kk < kc16; kk += 16) {
+      double af[2][8], bf[2][4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          af[mi][v] = Us[(kk + t4 + 4 * (v >> 1)) * LDU + wm * 32 + mi * 16 + g + 8 * (v & 1)];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) bf[ni][v] = Vs[(wn * 16 + ni * 8 + g) * LDV + kk + t4 + 4 * v];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma_16x8x16(acc[mi][ni], af[mi], bf[ni]);
     }
-    buf ^= 1;
+    double r0 = 0.0, r1 = 0.0, n0 = 0.0, n1 = 0.0;  // short chains (FP64 FMA latency ~24)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int v = 0; v < 4; v += 2) {
+          const int row = wm * 32 + mi * 16 + g + 8 * (v >> 1), col = wn * 16 + ni * 8 + 2 * t4;
+          const double x0 = Ms[col * LDM + row], x1 = Ms[(col + 1) * LDM + row];  // zero outside A
+          const double d0 = x0 - acc[mi][ni][v], d1 = x1 - acc[mi][ni][v + 1];
+          r0 = fma(d0, d0, r0);
+          r1 = fma(d1, d1, r1);
+          n0 = fma(x0, x0, n0);
+          n1 = fma(x1, x1, n1);
+        }
+    rsum += r0 + r1;
+    nsum += n0 + n1;
+    __syncthreads();  // this slot is refilled by the prefetch of the next iteration
+    slot = (slot + 1) % NS;
   }
   cp_async_wait<0>();
 #undef UB
