@@ -127,6 +127,19 @@ def load_peaks():
     return peaks
 
 
+def profiled_traffic(config, kernel, tag="r01"):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture (profiles/<tag>_c<config>_traffic.json, written by
+    tools/summarize_profiles.py), or None when not captured."""
+    if kernel is None:
+        return None
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", f"{tag}_c{config}_traffic.json")))
+        return d[kernel]["dram_bytes"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 # ---------------------------------------------------------------- config 2 inputs
 def config2_matrix_colmajor(seed, device):
     """A = U diag(sigma) V^T with U, V from QR of seeded Gaussians; returns a
@@ -347,22 +360,31 @@ class Config2:
                   "algorithmic_per_launch": {"flops": flops, "bytes": 8.0 * m * n + 16.0 * m * RANK},
                   "traffic": None}
         else:
-            byts = {"sketch": 8.0 * m * L_SKETCH * (4 + 8) / 2 + 8.0 * m * L_SKETCH}.get(top, 8.0 * m * L_SKETCH)
+            # latency-bound small dense factorisations (the 48 x 48 Jacobi SVD,
+            # the CholeskyQR steps): algorithmic bytes = the operands they read
+            # and write once (l x l per sketch for svd; the sketch strip for QR)
+            byts = {"sketch": 8.0 * m * L_SKETCH * (4 + 8) / 2 + 8.0 * m * L_SKETCH,
+                    "svd": 2 * 4 * 8.0 * L_SKETCH * L_SKETCH}.get(top, 8.0 * m * L_SKETCH)
             ach = byts / (per_launch_ms[top] * 1e-3) / 1e9
             rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                   "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                  "traffic": None}
-        # secondary: the residual kernel on its own roofline, always reported
+                  "algorithmic_bytes_per_launch": byts,
+                  "traffic": profiled_traffic(2, {"svd": "svd_cta_kernel"}.get(top)),
+                  "note": "latency-bound: one CTA per sketch runs a serial chain (Jacobi rounds, FP64 FMA "
+                          "latency ~24 cycles); see kernels_ms_per_step and profiles/"}
+        # the HBM/FP64-tensor kernels on their own rooflines, always reported
         if "residual" in fam:
             flops = 2.0 * m * n * RANK + 5.0 * m * n
             ach = flops / (per_launch_ms["residual"] * 1e-3) / 1e12
             rl["residual_kernel"] = {"achieved_tflops": ach, "frac_fp64": ach / peaks["fp64_tflops"],
-                                     "achieved_gbs": 8.0 * m * n / (per_launch_ms["residual"] * 1e-3) / 1e9}
+                                     "achieved_gbs": 8.0 * m * n / (per_launch_ms["residual"] * 1e-3) / 1e9,
+                                     "traffic": profiled_traffic(2, "residual_stream_kernel")}
         if "gemm_v" in fam:
             flops = 2.0 * m * n * RANK
             ach = flops / (per_launch_ms["gemm_v"] * 1e-3) / 1e12
             rl["gemm_v_kernel"] = {"achieved_tflops": ach, "frac_fp64": ach / peaks["fp64_tflops"],
-                                   "achieved_gbs": 8.0 * m * n / (per_launch_ms["gemm_v"] * 1e-3) / 1e9}
+                                   "achieved_gbs": 8.0 * m * n / (per_launch_ms["gemm_v"] * 1e-3) / 1e9,
+                                   "traffic": profiled_traffic(2, "tn_skinny_kernel")}
         return rl, kernels
 
     def e2e(self, steps, warmup):
