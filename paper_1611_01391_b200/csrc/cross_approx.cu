@@ -283,22 +283,51 @@ __global__ void __launch_bounds__(kCT) ca_block_kernel(CaParams P) {
     U[a + (int64_t)c * P.l] = acc;
   }
   if (P.P) {
-    // P = A(:,J) Tm (m x rq, zero beyond r), Q = Sm^T A(I,:) (rq x n)
+    // P = A(:,J) Tm (m x rq, zero beyond r), Q = Sm^T A(I,:) (rq x n). The
+    // strips are staged once in shared memory (S and W are free after the
+    // nucleus): C = A(:,J) in S (m x l, coalesced columns), R^T = A(I,:)^T
+    // in W (n x k); then a thread per row of P / column of Q, with r
+    // independent FMA chains each.
     double* Pb = P.P + (int64_t)b * P.m * P.rq;
     double* Qb = P.Q + (int64_t)b * P.rq * P.n;
-    for (int64_t e = tid; e < (int64_t)P.m * P.rq; e += kCT) {
-      const int i = (int)(e % P.m), j = (int)(e / P.m);
-      double acc = 0.0;
-      if (j < r)
-        for (int t = 0; t < P.l; ++t) acc += __ldg(A + i + (int64_t)s.Jcur[t] * P.lda) * s.Tm[t + j * P.l];
-      Pb[e] = acc;
+    __syncthreads();
+    for (int e = tid; e < P.m * P.l; e += kCT) {
+      const int i = e % P.m, t = e / P.m;
+      s.S[i + t * P.m] = __ldg(A + i + (int64_t)s.Jcur[t] * P.lda);
     }
-    for (int64_t e = tid; e < (int64_t)P.rq * P.n; e += kCT) {
-      const int j = (int)(e % P.rq), c = (int)(e / P.rq);
-      double acc = 0.0;
-      if (j < r)
-        for (int t = 0; t < P.k; ++t) acc += s.Sm[t + j * P.k] * __ldg(A + s.Icur[t] + (int64_t)c * P.lda);
-      Qb[e] = acc;
+    for (int e = tid; e < P.n * P.k; e += kCT) {
+      const int t = e % P.k, c = e / P.k;
+      s.W[c + t * P.n] = __ldg(A + s.Icur[t] + (int64_t)c * P.lda);
+    }
+    __syncthreads();
+    constexpr int kRQ = 64;  // rq <= min(k, l) <= 64
+    for (int i = tid; i < P.m; i += kCT) {
+      double acc[kRQ];
+#pragma unroll
+      for (int j = 0; j < kRQ; ++j) acc[j] = 0.0;
+      for (int t = 0; t < P.l; ++t) {
+        const double cv = s.S[i + t * P.m];
+#pragma unroll
+        for (int j = 0; j < kRQ; ++j)
+          if (j < r) acc[j] = fma(cv, s.Tm[t + j * P.l], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kRQ; ++j)
+        if (j < P.rq) Pb[i + (int64_t)j * P.m] = acc[j];  // zero beyond r
+    }
+    for (int c = tid; c < P.n; c += kCT) {
+      double acc[kRQ];
+#pragma unroll
+      for (int j = 0; j < kRQ; ++j) acc[j] = 0.0;
+      for (int t = 0; t < P.k; ++t) {
+        const double rv = s.W[c + t * P.n];
+#pragma unroll
+        for (int j = 0; j < kRQ; ++j)
+          if (j < r) acc[j] = fma(s.Sm[t + j * P.k], rv, acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kRQ; ++j)
+        if (j < P.rq) Qb[j + (int64_t)c * P.rq] = acc[j];
     }
   }
 }
