@@ -394,9 +394,12 @@ class Config2:
         ptr = host.data_ptr()
         ops = self.ops
 
+        Hs = [H for _, H in ops]
+
         def one():
-            for _, H in ops:
-                U, V, rs, ns = self.slra.range_finder_host(ptr, N2, N2, H, RANK, True)
+            # both multipliers of the step on one upload of A (the batched
+            # form of range_finder(M, H, r, TruncatedRankR))
+            self.slra.range_finder_batched_host(ptr, N2, N2, Hs, RANK, True)
         for _ in range(max(1, warmup // 2)):
             one()
         torch.cuda.synchronize()
@@ -406,10 +409,10 @@ class Config2:
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         return {"value": self.entries_per_step * steps / dt, "unit": "entries/s",
-                "h2d_bytes_per_step": 2 * 8 * N2 * N2,
+                "h2d_bytes_per_step": 8 * N2 * N2 + sum(8 * 2 * L_SKETCH * 8 + 4 * L_SKETCH for _ in Hs),
                 "d2h_bytes_per_step": 2 * (8 * 2 * N2 * RANK + 16),
-                "api": "paper_1611_01391_b200.range_finder_host -> slra::range_finder_device -> slra_range_finder "
-                       "(host pinned A in, U/V out, once per multiplier)"}
+                "api": "paper_1611_01391_b200.range_finder_batched_host -> slra_range_finder_batched "
+                       "(host pinned A in once, both multipliers' plans, U/V and residuals out)"}
 
     def cpu_baseline(self):
         sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))

@@ -289,6 +289,62 @@ PYBIND11_MODULE(_slra, m) {
     return py::make_tuple(to_np(dU.download()), to_np(dV.download()), o[0], o[1]);
   });
 
+  // ---- end-to-end range_finder(M, H_s, r, variant) for several sketches of
+  // the same M: M crosses the bus once, the factorisations of all sketches
+  // run batched on the device, every (U_s, V_s, resid_s, norm_s) comes back.
+  m.def("range_finder_batched_host", [](uintptr_t M_host, Index mm, Index n, const std::vector<PyOp>& Hs, Index r,
+                                        bool truncated) {
+    const int nsk = static_cast<int>(Hs.size());
+    if (nsk < 1) throw std::invalid_argument("range_finder_batched_host: no sketches");
+    const Index l = Hs[0].p->cols();
+    static DeviceMatrix* staging = new DeviceMatrix();  // reused HBM staging buffer (never freed)
+    if (staging->rows() != mm || staging->cols() != n) *staging = DeviceMatrix(mm, n);
+    check(slra_memcpy_h2d(device_context(), staging->data(), reinterpret_cast<const void*>(M_host), 8 * mm * n),
+          "range_finder_batched_host");
+    std::vector<SketchPlan> plans;
+    std::vector<DevBuf<int64_t>> dsrc;
+    std::vector<DevBuf<double>> dcoef;
+    std::vector<DevBuf<int32_t>> dq;
+    std::vector<const int64_t*> src(nsk);
+    std::vector<const double*> coef(nsk);
+    std::vector<const int32_t*> q(nsk);
+    std::vector<int64_t> width(nsk);
+    std::vector<int> tree(nsk);
+    const Index uc = truncated ? r : l;
+    std::vector<DeviceMatrix> dU, dV;
+    std::vector<double*> Up(nsk), Vp(nsk);
+    for (int s = 0; s < nsk; ++s) {
+      if (Hs[s].p->rows() != n || Hs[s].p->cols() != l) throw std::invalid_argument("range_finder_batched_host: H");
+      plans.push_back(compile_plan(*Hs[s].p, Side::Right));
+      dsrc.emplace_back(plans.back().src);
+      dcoef.emplace_back(plans.back().coef);
+      dq.emplace_back(plans.back().q);
+      dU.emplace_back(mm, uc);
+      dV.emplace_back(uc, n);
+    }
+    for (int s = 0; s < nsk; ++s) {
+      src[s] = dsrc[s].get();
+      coef[s] = dcoef[s].get();
+      q[s] = dq[s].get();
+      width[s] = plans[s].width;
+      tree[s] = plans[s].tree;
+      Up[s] = dU[s].data();
+      Vp[s] = dV[s].data();
+    }
+    DevBuf<double> out(2 * static_cast<size_t>(nsk));
+    std::vector<int32_t> status(nsk, 0);
+    check(slra_range_finder_batched(device_context(), staging->data(), mm, mm, n, nsk, src.data(), coef.data(),
+                                    q.data(), width.data(), tree.data(), l, r, truncated ? 1 : 0, Up.data(), mm,
+                                    Vp.data(), uc, out.get(), nullptr, status.data()),
+          "range_finder_batched_host");
+    for (int s = 0; s < nsk; ++s) check(status[s], "range_finder_batched_host");
+    const auto o = out.download();
+    py::list res;
+    for (int s = 0; s < nsk; ++s)
+      res.append(py::make_tuple(to_np(dU[s].download()), to_np(dV[s].download()), o[2 * s], o[2 * s + 1]));
+    return res;
+  });
+
   // ---- end-to-end sketch_solve(p, F, false) + residual_norm(p, x_hat)
   // (lsr.hpp) with A (m x d, column-major) and b read from the caller's
   // (pinned) host buffers; x_hat and both residuals come back to the host.

@@ -452,6 +452,25 @@ def test_range_finder_config2_parity(slra, oracle, n, kind):
         assert err < 1e-9
 
 
+def test_range_finder_batched_host_matches_single(slra):
+    """The e2e entry (one upload of A, both config-2 multipliers batched)
+    returns what range_finder returns per multiplier."""
+    import torch
+    n = 1024
+    A = _config2_matrix(n, 5)
+    rp = slra.Rng(3)
+    Hs = [slra.take_columns_random(slra.gen_sparse_circulant(n, 4, rp), 48, rp),
+          slra.take_columns_random(slra.gen_asph(n, 3, rp), 48, rp)]
+    host = torch.from_numpy(np.asfortranarray(A).T.copy().reshape(-1)).pin_memory()  # column-major bytes
+    out = slra.range_finder_batched_host(host.data_ptr(), n, n, Hs, 32, True)
+    nA = np.linalg.norm(A)
+    for (U, V, rs, ns), H in zip(out, Hs):
+        U1, V1 = slra.range_finder(A, H, 32, True)
+        assert np.allclose(U, U1, atol=1e-13) and np.allclose(V, V1, atol=1e-13 * nA)
+        assert abs(np.sqrt(rs) - np.linalg.norm(A - U1 @ V1)) <= 1e-12 * nA
+        assert abs(np.sqrt(ns) - nA) <= 1e-13 * nA
+
+
 def test_range_finder_rank_failure(slra):  # test_lra.cpp:24-30
     rng = slra.Rng(20)
     H = slra.take_columns_random(slra.gen_sparse_circulant(64, 3, rng), 8, rng)
