@@ -677,14 +677,28 @@ __device__ void cta_jacobi_t(double* W, int ldw, int p, int n, double* V, int ld
 // per warp): a pair's dot products reduce in 3 shuffle levels instead of 5
 // and one warp-instruction advances 4 pairs, which cuts the instruction count
 // per round ~4x — the round is instruction-throughput bound on FP64.
-template <int NT>
+struct JacobiShared {
+  unsigned short pair_tab[64 * 32];  // round-robin schedule: (a << 8) | b
+  double dmax2;
+  double cmax2[32];
+};
+__device__ inline JacobiShared& jacobi_shared() {
+  __shared__ JacobiShared s;
+  return s;
+}
+
+template <int NT, int RPG, bool EXACT>
 __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate) {
-  constexpr int RPG = 8;  // rows per lane: p <= 64, n <= 64
+  // RPG rows per lane (p <= 8 RPG, n <= p); EXACT: p == n == 8 RPG (no row predicates)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = lane >> 3, sub = lane & 7;
   constexpr int NW = NT / 32;
-  __shared__ unsigned short pair_tab[64 * 32];
-  __shared__ double dmax2;
+  // one shared scratch for every instantiation (static __shared__ in a
+  // template would be allocated once per instantiation)
+  JacobiShared& js = jacobi_shared();
+  unsigned short* pair_tab = js.pair_tab;
+  double& dmax2 = js.dmax2;
+  double* cmax2 = js.cmax2;
   for (int e = tid; e < n * n; e += NT) V[e % n + (e / n) * ldv] = (e % n == e / n) ? 1.0 : 0.0;
   const int ne = n + (n & 1);
   for (int e = tid; e < (ne - 1) * (ne / 2); e += NT) {
@@ -707,7 +721,6 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
   const double tol = 16.0 * (double)p * kEps;
   const double tol2 = tol * tol;
   if (tid == 0) flag[0] = flag[1] = 0;
-  __shared__ double cmax2[NW];
   __syncthreads();
   const int npairs = ne / 2;
   const int iters = (npairs + 4 * NW - 1) / (4 * NW);
@@ -749,10 +762,10 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
 #pragma unroll
         for (int r = 0; r < RPG; ++r) {
           const int i = sub + 8 * r;
-          x[r] = i < p ? wp[i] : 0.0;
-          y[r] = i < p ? wq[i] : 0.0;
-          u[r] = i < n ? vp[i] : 0.0;
-          v[r] = i < n ? vq[i] : 0.0;
+          x[r] = (EXACT || i < p) ? wp[i] : 0.0;
+          y[r] = (EXACT || i < p) ? wq[i] : 0.0;
+          u[r] = (EXACT || i < n) ? vp[i] : 0.0;
+          v[r] = (EXACT || i < n) ? vq[i] : 0.0;
         }
         {  // two accumulators per product: FP64 FMA latency is ~24 cycles on sm_100
           double a1 = 0.0, b1 = 0.0, g1 = 0.0;
@@ -793,11 +806,11 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
 #pragma unroll
         for (int r = 0; r < RPG; ++r) {
           const int i = sub + 8 * r;
-          if (i < p) {
+          if (EXACT || i < p) {
             wp[i] = cs * x[r] - sn * y[r];
             wq[i] = sn * x[r] + cs * y[r];
           }
-          if (i < n) {
+          if (EXACT || i < n) {
             vp[i] = cs * u[r] - sn * v[r];
             vq[i] = sn * u[r] + cs * v[r];
           }
@@ -813,7 +826,18 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
 
 template <int NT>
 __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate = 0.0) {
-  if (p <= 64) cta_jacobi_g8<NT>(W, ldw, p, n, V, ldv, flag, deflate);
+  if (p <= 64) {
+    const int rpg = (p + 7) / 8;
+    const bool exact = p == 8 * rpg && n == p;
+#define SLRA_G8(R)                                                                   \
+  if (rpg == R) {                                                                    \
+    if (exact) cta_jacobi_g8<NT, R, true>(W, ldw, p, n, V, ldv, flag, deflate);      \
+    else cta_jacobi_g8<NT, R, false>(W, ldw, p, n, V, ldv, flag, deflate);           \
+    return;                                                                          \
+  }
+    SLRA_G8(1) SLRA_G8(2) SLRA_G8(3) SLRA_G8(4) SLRA_G8(5) SLRA_G8(6) SLRA_G8(7) SLRA_G8(8)
+#undef SLRA_G8
+  }
   else cta_jacobi_t<NT, 8>(W, ldw, p, n, V, ldv, flag, deflate);  // p <= 256 (callers enforce)
 }
 

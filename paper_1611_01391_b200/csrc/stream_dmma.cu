@@ -29,7 +29,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // ---------------------------------------------------------------- residual
 namespace rs {
 constexpr int NT = 256;        // 8 warps: 4 (rows) x 2 (cols), warp tile 32 x 16
-constexpr int TM = 128;        // tile rows
+constexpr int TM = 64;         // tile rows (4 row-warps x MI m16 blocks)
 constexpr int TN = 32;         // tile cols
 constexpr int KP = 32;         // inner dimension (padded)
 constexpr int LDU = TM + 2;    // Us[k][row]
@@ -38,7 +38,8 @@ constexpr int LDM = TM + 2;    // Ms[col][row]
 constexpr int U_D = KP * LDU;  // doubles per U buffer
 constexpr int V_D = TN * LDV;
 constexpr int M_D = TN * LDM;
-constexpr int NS = 3;          // cp.async pipeline depth (tiles in flight)
+constexpr int NS = 2;          // cp.async pipeline depth (tiles in flight); 2 CTAs per SM
+constexpr int MI = TM / 64;    // m16 row blocks per warp
 constexpr size_t SMEM = sizeof(double) * NS * (U_D + V_D + M_D);
 }  // namespace rs
 
@@ -98,7 +99,7 @@ __device__ __forceinline__ void rs_stage(const StreamResidualArgs& a, int64_t i0
   }
 }
 
-__global__ void __launch_bounds__(rs::NT, 1) residual_stream_kernel(StreamResidualArgs a) {
+__global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidualArgs a) {
   using namespace rs;
   extern __shared__ __align__(16) double smem[];
   // stage slot s of U / V / M (pointer arithmetic, no local-memory pointer arrays)
@@ -137,37 +138,37 @@ __global__ void __launch_bounds__(rs::NT, 1) residual_stream_kernel(StreamResidu
     const double* Ms = MB(slot);
     // warp tile 32 x 16 = 2 (16-row) x 2 (8-col) m16n8k16 blocks; K padded
     // to 16 (the staged U / V tiles are zero-filled up to KP)
-    double acc[2][2][4];
+    double acc[MI][2][4];
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[mi][ni][v] = 0.0;
     for (int kk = 0; kk < kc16; kk += 16) {
-      double af[2][8], bf[2][4];
+      double af[MI][8], bf[2][4];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
         for (int v = 0; v < 8; ++v)
-          af[mi][v] = Us[(kk + t4 + 4 * (v >> 1)) * LDU + wm * 32 + mi * 16 + g + 8 * (v & 1)];
+          af[mi][v] = Us[(kk + t4 + 4 * (v >> 1)) * LDU + wm * (TM / 4) + mi * 16 + g + 8 * (v & 1)];
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
         for (int v = 0; v < 4; ++v) bf[ni][v] = Vs[(wn * 16 + ni * 8 + g) * LDV + kk + t4 + 4 * v];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) dmma_16x8x16(acc[mi][ni], af[mi], bf[ni]);
     }
     double r0 = 0.0, r1 = 0.0, n0 = 0.0, n1 = 0.0;  // short chains (FP64 FMA latency ~24)
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
         for (int v = 0; v < 4; v += 2) {
-          const int row = wm * 32 + mi * 16 + g + 8 * (v >> 1), col = wn * 16 + ni * 8 + 2 * t4;
+          const int row = wm * (TM / 4) + mi * 16 + g + 8 * (v >> 1), col = wn * 16 + ni * 8 + 2 * t4;
           const double x0 = Ms[col * LDM + row], x1 = Ms[(col + 1) * LDM + row];  // zero outside A
           const double d0 = x0 - acc[mi][ni][v], d1 = x1 - acc[mi][ni][v + 1];
           r0 = fma(d0, d0, r0);
@@ -215,7 +216,7 @@ int launch_residual_stream(Context* c, const double* A, int64_t lda, int64_t m, 
                        (ldp % 2 == 0) && ((uintptr_t)Q % 16 == 0) && (ldq % 2 == 0)));
   if (!aligned || inner > rs::KP || m < 1 || n < 1) return SLRA_ERR_UNSUPPORTED;
   const int64_t tiles = ((m + rs::TM - 1) / rs::TM) * ((n + rs::TN - 1) / rs::TN);
-  int grid = c->num_sms;
+  int grid = 2 * c->num_sms;  // two co-resident CTAs per SM: their sync phases interleave
   if (tiles < grid) grid = (int)tiles;
   double* part = partials(c, 2 * grid);
   if (!part) return SLRA_ERR_CUDA;
