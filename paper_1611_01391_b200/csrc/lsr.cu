@@ -7,9 +7,13 @@
 // Cholesky of FA^T FA in one CTA (right-looking, 32-column panels), two
 // triangular solves, one step of iterative refinement, and the sketched
 // residual ||FA x - Fb|| by a direct pass (never from the Gram identity).
-// Rank test: a Cholesky pivot that is non-positive or below
-// (1e-10 * max_i ||FA(:,i)||)^2 reports SketchRankFailure — the analogue of
-// ColPivHouseholderQR's rank() < d with threshold 1e-10 (lsr.cpp:52-55).
+// Rank test: a Cholesky pivot that is non-positive, below
+// (1e-10 * max_i ||FA(:,i)||)^2, or below 64 eps ||FA(:,j)||^2 reports
+// SketchRankFailure — the analogue of ColPivHouseholderQR's rank() < d with
+// threshold 1e-10 (lsr.cpp:52-55). The Gram resolves dependence only to the
+// sqrt(eps) level, so exactly dependent columns fail as in the reference,
+// while sketches with sigma_min / sigma_max between 1e-10 and ~1e-7 also
+// fail here (the reference solves those); DESIGN.md §8.
 #include "common.cuh"
 
 namespace slra_dev {
@@ -35,7 +39,10 @@ __global__ void __launch_bounds__(kLT) cholesky_kernel(double* __restrict__ G, i
   __shared__ int fail;
   const int tid = threadIdx.x;
   const int ldp = d + 1;
+  double* gdiag = P + (size_t)ldp * kPW;  // original diagonal ||FA(:,j)||^2
+  for (int i = tid; i < d; i += kLT) gdiag[i] = G[i + (int64_t)i * d];
   if (tid == 0) fail = 0;
+  __syncthreads();
   for (int p0 = 0; p0 < d; p0 += kPW) {
     const int pw = (d - p0) < kPW ? (d - p0) : kPW;
     const int rows = d - p0;
@@ -50,7 +57,11 @@ __global__ void __launch_bounds__(kLT) cholesky_kernel(double* __restrict__ G, i
     __syncthreads();
     for (int j = 0; j < pw; ++j) {
       const double piv = P[j + j * ldp];
-      if (!(piv > tol2)) {  // uniform: every thread read the same pivot
+      // rank failure: the pivot (squared distance of column j from the span
+      // of the earlier ones) is non-positive, below the global floor, or
+      // below 64 eps of the column's own squared norm — a column dependent
+      // at the sqrt(eps) level, which is as fine as the Gram resolves
+      if (!(piv > tol2) || !(piv > 64.0 * 2.220446049250313e-16 * gdiag[p0 + j])) {  // uniform
         if (tid == 0) fail = 1;
         break;
       }
@@ -301,7 +312,7 @@ static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, dou
   double dmax = 0.0;
   for (int64_t i = 0; i < (d < 500 ? d : 500); ++i) dmax = hs[i] > dmax ? hs[i] : dmax;
   const double tol2 = 1e-20 * dmax;
-  const size_t smem = sizeof(double) * (size_t)(d + 1) * kPW;
+  const size_t smem = sizeof(double) * ((size_t)(d + 1) * kPW + (size_t)d);  // panel + original diagonal
   SLRA_CUDA(cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(8 * d * (kSB + 1))));
   SLRA_CUDA(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

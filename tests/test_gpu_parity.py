@@ -520,6 +520,72 @@ def test_sketch_solve_known_answers(slra):  # test_lsr.cpp:59-90
         slra.sketch_solve(np.zeros((32, 4)) + 0.0, b, Z)
 
 
+# ---------------------------------------------------------------- edge cases
+def test_select_rows_spanning_padding_branch(slra, oracle):  # cur.cpp:125-134
+    A = oracle.Rng(41).gaussian_matrix(200, 10)
+    for count in (10, 13, 17):
+        assert slra.select_rows_spanning(A, count) == oracle.select_rows_spanning(A, count)
+
+
+@pytest.mark.parametrize("m,c,seed", [(3000, 24, 1), (9000, 64, 2)])
+def test_tall_selection_grid_path(slra, oracle, m, c, seed):
+    """Strips taller than one SM: maxvol_rows and select_rows_spanning run the
+    grid-wide cooperative kernel (select: after TSQR)."""
+    A = oracle.Rng(seed).gaussian_matrix(m, c)
+    assert slra.select_rows_spanning(A, c) == oracle.select_rows_spanning(A, c)
+    Q, _ = oracle.thin_qr(A)
+    I = slra.maxvol_rows(Q, 1.1)
+    assert I == oracle.maxvol_rows(Q, 1.1)
+    B = Q @ np.linalg.inv(Q[I, :])
+    assert np.abs(B).max() <= 1.1 * (1 + 1e-12)
+
+
+def test_invalid_arguments_raise(slra):  # std::invalid_argument in the reference
+    A = slra.Rng(1).gaussian_matrix(40, 30)
+    with pytest.raises(ValueError):
+        slra.maxvol_rows(A[:, :5], 0.9)  # h < 1 (cur.cpp:91)
+    with pytest.raises(ValueError):
+        slra.maxvol_rows(A[:3, :5])  # m < r (cur.cpp:90)
+    with pytest.raises(ValueError):
+        slra.select_rows_spanning(A, 41)  # count > rows (cur.cpp:120)
+    with pytest.raises(ValueError):
+        slra.primitive_cur(A, [0, 1], [0, 1, 2], 3)  # |I| < r (cur.cpp:139-140)
+    with pytest.raises(ValueError):
+        slra.cross_approx(A, 5, 4, 6, [], 1, 1.1, slra.Rng(0))  # k < r (cur.cpp:205-206)
+    rp = slra.Rng(2)
+    H = slra.take_columns_random(slra.gen_sparse_circulant(30, 2, rp), 8, rp)
+    with pytest.raises(ValueError):
+        slra.range_finder(A, H, 9, True)  # r > l
+
+
+def test_rank_deficient_lsr_raises(slra):  # lsr.cpp:52-55
+    rng = slra.Rng(17)
+    A = rng.gaussian_matrix(200, 6)
+    A[:, 5] = A[:, 4]  # exactly dependent columns
+    b = rng.gaussian_vector(200)
+    F = slra.make_sub_identity(rng.distinct_indices(64, 200), 200)
+    with pytest.raises(slra.SketchRankFailure):
+        slra.sketch_solve(A, b, F, False)
+
+
+def test_residual_ragged_and_empty_inner(slra):
+    import torch
+    rng = np.random.default_rng(5)
+    for m, n, inner in [(129, 33, 0), (257, 95, 7), (64, 31, 2)]:
+        A = rng.standard_normal((m, n))
+        P = rng.standard_normal((m, max(inner, 1)))[:, :inner]
+        Q = rng.standard_normal((max(inner, 1), n))[:inner, :]
+        ref = np.linalg.norm(A - P @ Q) ** 2 if inner else np.linalg.norm(A) ** 2
+        At = torch.from_numpy(np.asfortranarray(A).T.copy()).cuda()
+        Pt = torch.from_numpy(np.asfortranarray(P).T.copy()).cuda() if inner else At
+        Qt = torch.from_numpy(np.asfortranarray(Q).T.copy()).cuda() if inner else At
+        out = torch.zeros(2, dtype=torch.float64, device="cuda")
+        slra.lowrank_residual_device(At.data_ptr(), m, m, n, Pt.data_ptr(), m, Qt.data_ptr(), max(inner, 1), inner,
+                                     out.data_ptr())
+        o = out.cpu().numpy()
+        assert abs(o[0] - ref) <= 1e-12 * max(ref, 1.0) and abs(o[1] - np.linalg.norm(A) ** 2) <= 1e-12 * o[1]
+
+
 # ---------------------------------------------------------------- no silent fallback
 def test_native_library_loaded(slra):
     import os
