@@ -745,13 +745,25 @@ class Config4:
         kernels = {k: v[0] / steps for k, v in fam.items()}
         per = {k: v[0] / max(v[1], 1) for k, v in fam.items()}
         top = max(fam.items(), key=lambda kv: kv[1][0])[0]
+        # algorithmic bytes per launch: the residual pass reads A|b once; the
+        # solve family (Cholesky, triangular solves, sketched residual) reads
+        # the k x (d+1) sketch about twice
         byts = {"lsr_residual": 8.0 * self.mloc * (D4 + 1), "sketch": 8.0 * K4 * 2 * (D4 + 1) * 1.5,
-                "gemm": 8.0 * K4 * (D4 + 1)}
+                "gemm": 8.0 * K4 * (D4 + 1), "lsr_solve": 2 * 8.0 * K4 * (D4 + 1)}
         b = byts.get(top, 8.0 * self.mloc * (D4 + 1))
         ach = b / (per[top] * 1e-3) / 1e9
         rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
               "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-              "algorithmic_bytes_per_launch": b, "traffic": None}
+              "algorithmic_bytes_per_launch": b, "traffic": profiled_traffic(4, {"lsr_residual": "lsr_residual_kernel",
+                                                                                "lsr_solve": "cholesky_kernel"}.get(top))}
+        if top == "lsr_solve":
+            rl["note"] = ("latency-bound: the 256 x 256 Cholesky and the triangular solves run on one CTA "
+                          "(FP64 dependent chains); per-launch mean over the family's kernels")
+        if "lsr_residual" in per:
+            rb = 8.0 * self.mloc * (D4 + 1)
+            rl["lsr_residual_kernel"] = {"achieved_gbs": rb / (per["lsr_residual"] * 1e-3) / 1e9,
+                                         "frac_hbm": rb / (per["lsr_residual"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                         "traffic": profiled_traffic(4, "lsr_residual_kernel")}
         return rl, kernels
 
     def e2e(self, steps, warmup):

@@ -180,6 +180,16 @@ __device__ __forceinline__ ArgMax block_argmax(ArgMax a, double* rv, int64_t* ri
 // FP64 tensor-core MMA (sm_80+ mma.sync; SASS DMMA.8x8x4 on sm_100a).
 // A 8x4 row: a = A[lane>>2][lane&3]; B 4x8 col: b = B[lane&3][lane>>2];
 // C 8x8: c0,c1 = C[lane>>2][2*(lane&3) + {0,1}].
+// Load p[ok ? i : 0] unconditionally and select afterwards: a guarded load
+// (`ok ? p[i] : 0`) compiles to a branch around each load, which serialises
+// a batch of loads on their full latency; this form keeps them all in flight.
+// p[0] must be a valid address.
+template <typename T>
+__device__ __forceinline__ T load_sel(const T* p, int64_t i, bool ok) {
+  const T v = p[ok ? i : 0];
+  return ok ? v : T(0);
+}
+
 // m16n8k16 FP64 MMA (SASS DMMA.16816: 8x the work of 8x8x4 per instruction).
 // Fragments (g = lane >> 2, t = lane & 3), from the PTX f64 m16n8k16 layout
 // (as in CuTe's SM90_16x8x16_F64F64F64F64_TN traits):

@@ -24,7 +24,7 @@ int launch_sketch_rows(Context* c, const double* Wm, int64_t ldw, int64_t ncols,
 int launch_gemm(Context* c, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                 int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc);
 
-constexpr int kLT = 512;
+constexpr int kLT = 256;
 constexpr int kPW = 32;  // Cholesky panel width
 
 // In-place lower Cholesky of G (d x d, ld d, global/L2), one CTA,
@@ -48,125 +48,208 @@ __global__ void __launch_bounds__(kLT) cholesky_kernel(double* __restrict__ G, i
     const int rows = d - p0;
     for (int i = tid; i < rows; i += kLT) {  // all 32 loads of a row in flight at once
       double g[kPW];
+      const double* gi = G + (p0 + i) + (int64_t)p0 * d;
 #pragma unroll
-      for (int c = 0; c < kPW; ++c) g[c] = (c < pw && i >= c) ? G[(p0 + i) + (int64_t)(p0 + c) * d] : 0.0;
+      for (int c = 0; c < kPW; ++c) g[c] = load_sel(gi, (int64_t)c * d, c < pw && i >= c);
 #pragma unroll
       for (int c = 0; c < kPW; ++c)
         if (c < pw) P[i + c * ldp] = g[c];
     }
     __syncthreads();
-    for (int j = 0; j < pw; ++j) {
-      const double piv = P[j + j * ldp];
-      // rank failure: the pivot (squared distance of column j from the span
-      // of the earlier ones) is non-positive, below the global floor, or
-      // below 64 eps of the column's own squared norm — a column dependent
-      // at the sqrt(eps) level, which is as fine as the Gram resolves
-      if (!(piv > tol2) || !(piv > 64.0 * 2.220446049250313e-16 * gdiag[p0 + j])) {  // uniform
-        if (tid == 0) fail = 1;
-        break;
+    // (a) the pw x pw diagonal block: thread (row ti, phase tc) owns L(ti, c)
+    // for c = tc, tc + 8, ...; each column step stages its operands in registers
+    // and writes after a barrier (no dependent shared-memory chains)
+    {
+      const int ti = tid & 31, tc = tid >> 5;  // 8 phases: columns tc, tc + 8, tc + 16, tc + 24
+      for (int j = 0; j < pw; ++j) {
+        const double piv = P[j + j * ldp];
+        // rank failure: the pivot (squared distance of column j from the span
+        // of the earlier ones) is non-positive, below the global floor, or
+        // below 64 eps of the column's own squared norm — a column dependent
+        // at the sqrt(eps) level, which is as fine as the Gram resolves
+        if (!(piv > tol2) || !(piv > 64.0 * 2.220446049250313e-16 * gdiag[p0 + j])) {  // uniform
+          if (tid == 0) fail = 1;
+          break;
+        }
+        const double ljj = sqrt(piv);
+        const double inv = 1.0 / ljj;
+        const bool row = ti > j && ti < pw;
+        const double lij = row ? P[ti + j * ldp] * inv : 0.0;
+        double lcj[4], cur[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = tc + 8 * q;
+          const bool act = row && c > j && c <= ti;
+          lcj[q] = load_sel(P + c, (int64_t)j * ldp, act) * inv;
+          cur[q] = load_sel(P + ti, (int64_t)c * ldp, act);
+        }
+        __syncthreads();
+        if (tc == 0 && ti >= j && ti < pw) P[ti + j * ldp] = (ti == j) ? ljj : lij;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = tc + 8 * q;
+          if (row && c > j && c <= ti) P[ti + c * ldp] = cur[q] - lij * lcj[q];
+        }
+        __syncthreads();
       }
-      const double ljj = sqrt(piv);
-      __syncthreads();  // everyone has read the pivot before column j is scaled
-      for (int i = j + tid; i < rows; i += kLT) P[i + j * ldp] = (i == j) ? ljj : P[i + j * ldp] / ljj;
-      __syncthreads();
-      // update my row of the remaining panel columns
-      for (int i = j + 1 + tid; i < rows; i += kLT) {
-        const double lij = P[i + j * ldp];
-        const int cmax = i < pw - 1 ? i : pw - 1;
-        for (int c = j + 1; c <= cmax; ++c) P[i + c * ldp] -= lij * P[c + j * ldp];
-      }
-      __syncthreads();
     }
     __syncthreads();
     if (fail) break;
-    for (int c = 0; c < pw; ++c)
-      for (int i = c + tid; i < rows; i += kLT) G[(p0 + i) + (int64_t)(p0 + c) * d] = P[i + c * ldp];
-    // trailing lower triangle: thread pair (row i, column parity) walks columns
-    const int tr = rows - pw;
-    for (int e = tid; e < 2 * tr; e += kLT) {
-      const int i = pw + (e >> 1), par = e & 1;
-      double li[kPW];
+    // (b) rows below the block: L21(i, :) = A21(i, :) L11^-T, a thread per
+    // row, right-looking in registers
+    double* rdiag = gdiag + d;  // 1 / L(j, j) of this panel's block
+    for (int c = tid; c < pw; c += kLT) rdiag[c] = 1.0 / P[c + c * ldp];
+    __syncthreads();
+    for (int i = pw + tid; i < rows; i += kLT) {
+      double z[kPW];
 #pragma unroll
-      for (int t = 0; t < kPW; ++t) li[t] = t < pw ? P[i + t * ldp] : 0.0;
-      // four columns per batch: their G loads are issued before the FMAs
-      for (int c0 = pw + par; c0 <= i; c0 += 8) {
-        double gv[4];
+      for (int c = 0; c < kPW; ++c) z[c] = load_sel(P + i, (int64_t)c * ldp, c < pw);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = c0 + 2 * u;
-          gv[u] = c <= i ? G[(p0 + i) + (int64_t)(p0 + c) * d] : 0.0;
-        }
+      for (int c = 0; c < kPW; ++c) {
+        z[c] *= (c < pw) ? rdiag[c] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = c0 + 2 * u;
-          if (c > i) break;
-          double acc = 0.0;
-#pragma unroll
-          for (int t = 0; t < kPW; ++t) acc = fma(li[t], P[c + t * ldp], acc);
-          G[(p0 + i) + (int64_t)(p0 + c) * d] = gv[u] - acc;
-        }
+        for (int c2 = c + 1; c2 < kPW; ++c2) z[c2] = fma(-z[c], P[c2 + c * ldp], z[c2]);  // pw <= 32 < ld
       }
+#pragma unroll
+      for (int c = 0; c < kPW; ++c)
+        if (c < pw) P[i + c * ldp] = z[c];
+    }
+    __syncthreads();
+    for (int i = tid; i < rows; i += kLT) {  // a row per thread, unrolled over the panel
+      double* gi = G + (p0 + i) + (int64_t)p0 * d;
+#pragma unroll
+      for (int c = 0; c < kPW; ++c)
+        if (c < pw && i >= c) gi[(int64_t)c * d] = P[i + c * ldp];
+    }
+    // trailing lower triangle G22 -= L21 L21^T in 4 x 4 register tiles (16
+    // independent FMA chains per thread; tiles on or below the diagonal)
+    // thread (ti4, tc4) owns rows pw + ti4 + nt a and columns pw + tc4 + nt b
+    // (a, b < 4): strided so a warp's row reads are consecutive (no bank
+    // conflicts) and its column reads are broadcasts
+    const int tr = rows - pw;
+    const int nt = (tr + 3) / 4;
+    for (int e = tid; e < nt * nt; e += kLT) {
+      const int ti4 = e % nt, tc4 = e / nt;
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int t = 0; t < pw; ++t) {
+        const double* pt = P + t * ldp + pw;
+        double li[4], lc[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          li[a] = load_sel(pt, ti4 + nt * a, ti4 + nt * a < tr);
+          lc[a] = load_sel(pt, tc4 + nt * a, tc4 + nt * a < tr);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(li[a], lc[b], acc[a][b]);
+      }
+      // read all 16 targets first (unconditional, clamped), then store: a
+      // guarded read-modify-write would serialise the L2 latencies
+      double gv[4][4];
+      double* gbase = G + (p0 + pw) + (int64_t)(p0 + pw) * d;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = ti4 + nt * a, c = tc4 + nt * b;
+          const bool ok = i < tr && c <= i;
+          gv[a][b] = gbase[ok ? i + (int64_t)c * d : 0];
+        }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = ti4 + nt * a, c = tc4 + nt * b;
+          if (i < tr && c <= i) gbase[i + (int64_t)c * d] = gv[a][b] - acc[a][b];
+        }
     }
     __syncthreads();
   }
   if (tid == 0) *status = fail;
 }
 
-// x (+)= (L L^T)^{-1} rhs for the lower Cholesky factor L (ld d), one CTA.
-// Both sweeps stage 32-wide blocks of L in shared memory (coalesced loads),
-// then run the 32 column steps from there with one barrier per step.
+// x (+)= (L L^T)^{-1} rhs for the lower Cholesky factor L (ld d), one CTA,
+// by 32-wide blocks: one warp solves the diagonal block with shuffles (lane
+// i holds entry i; per step a multiply, a broadcast and an FMA), then the
+// whole CTA applies the block to the remaining entries (a GEMV). 2 d / 32
+// barriers per solve instead of 2 d.
 constexpr int kST = 256;
 constexpr int kSB = 32;
 __global__ void __launch_bounds__(kST) chol_solve_kernel(const double* __restrict__ L, int d,
                                                          const double* __restrict__ rhs, double* __restrict__ x,
                                                          const int32_t* __restrict__ status, int accumulate) {
-  extern __shared__ __align__(16) double sm[];
-  double* v = sm;            // d
-  double* B = sm + d;        // d x kSB block (ld d)
+  extern __shared__ __align__(16) double v[];  // d
   if (*status) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < d; i += kST) v[i] = rhs[i];
-  // forward: L y = rhs, column blocks [j0, j0 + kSB)
-  for (int j0 = 0; j0 < d; j0 += kSB) {
-    const int jw = (d - j0) < kSB ? (d - j0) : kSB;
-    for (int i = j0 + tid; i < d; i += kST) {  // row i of the block: 32 independent loads
-      double g[kSB];
+  __syncthreads();
+  // forward: L y = rhs
+  for (int b0 = 0; b0 < d; b0 += kSB) {
+    const int bw = (d - b0) < kSB ? (d - b0) : kSB;
+    if (warp == 0) {
+      const bool in = lane < bw;
+      double lrow[kSB];  // L(b0 + lane, b0 + c)
 #pragma unroll
-      for (int c = 0; c < kSB; ++c) g[c] = (c < jw && i >= j0 + c) ? L[i + (int64_t)(j0 + c) * d] : 0.0;
+      for (int c = 0; c < kSB; ++c) lrow[c] = load_sel(L + (b0 + lane), (int64_t)(b0 + c) * d, in && c < lane);
+      const double rd = in ? 1.0 / L[(b0 + lane) + (int64_t)(b0 + lane) * d] : 0.0;
+      double yi = in ? v[b0 + lane] : 0.0;
 #pragma unroll
-      for (int c = 0; c < kSB; ++c)
-        if (c < jw) B[i + c * d] = g[c];
+      for (int c = 0; c < kSB; ++c) {
+        if (lane == c) yi *= rd;
+        const double yc = __shfl_sync(0xffffffffu, yi, c);
+        if (lane > c) yi = fma(-lrow[c], yc, yi);
+      }
+      if (in) v[b0 + lane] = yi;
     }
     __syncthreads();
-    for (int c = 0; c < jw; ++c) {
-      const int j = j0 + c;
-      const double yj = v[j] / B[j + c * d];
-      for (int i = j + 1 + tid; i < d; i += kST) v[i] -= B[i + c * d] * yj;
-      __syncthreads();
-      if (tid == 0) v[j] = yj;
+    for (int i = b0 + bw + tid; i < d; i += kST) {  // v(i) -= L(i, block) y(block)
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < kSB; c += 2) {
+        a0 = fma(load_sel(L + i, (int64_t)(b0 + c) * d, c < bw), v[b0 + (c < bw ? c : 0)], a0);
+        a1 = fma(load_sel(L + i, (int64_t)(b0 + c + 1) * d, c + 1 < bw), v[b0 + (c + 1 < bw ? c + 1 : 0)], a1);
+      }
+      v[i] -= a0 + a1;
     }
     __syncthreads();
   }
-  // backward: L^T x = y, row blocks [i0, i0 + kSB) from the bottom; B holds
-  // rows i0..i0+iw-1 of L transposed: B[j + r * d] = L(i0 + r, j), j <= i0 + r
-  for (int i1 = d; i1 > 0; i1 -= kSB) {
-    const int i0 = i1 - kSB > 0 ? i1 - kSB : 0;
-    const int iw = i1 - i0;
-    for (int j = tid; j < i1; j += kST) {  // column j of L, rows i0..i1-1: iw independent loads
-      double g[kSB];
+  // backward: L^T x = y
+  for (int b1 = d; b1 > 0; b1 -= kSB) {
+    const int b0 = b1 - kSB > 0 ? b1 - kSB : 0;
+    const int bw = b1 - b0;
+    if (warp == 0) {
+      const bool in = lane < bw;
+      double lcol[kSB];  // L(b0 + c, b0 + lane) = L^T(b0 + lane, b0 + c)
 #pragma unroll
-      for (int r = 0; r < kSB; ++r) g[r] = (r < iw && j <= i0 + r) ? L[(i0 + r) + (int64_t)j * d] : 0.0;
+      for (int c = 0; c < kSB; ++c)
+        lcol[c] = load_sel(L + (int64_t)(b0 + lane) * d, (int64_t)(b0 + c), in && c < bw && c > lane);
+      const double rd = in ? 1.0 / L[(b0 + lane) + (int64_t)(b0 + lane) * d] : 0.0;
+      double xi = in ? v[b0 + lane] : 0.0;
 #pragma unroll
-      for (int r = 0; r < kSB; ++r)
-        if (r < iw) B[j + r * d] = g[r];
+      for (int c = kSB - 1; c >= 0; --c) {
+        if (c < bw) {
+          if (lane == c) xi *= rd;
+          const double xc = __shfl_sync(0xffffffffu, xi, c);
+          if (lane < c) xi = fma(-lcol[c], xc, xi);
+        }
+      }
+      if (in) v[b0 + lane] = xi;
     }
     __syncthreads();
-    for (int r = iw - 1; r >= 0; --r) {
-      const int i = i0 + r;
-      const double xi = v[i] / B[i + r * d];
-      for (int j = tid; j < i; j += kST) v[j] -= B[j + r * d] * xi;
-      __syncthreads();
-      if (tid == 0) v[i] = xi;
+    for (int i = tid; i < b0; i += kST) {  // v(i) -= L(block, i)^T x(block)
+      double a0 = 0.0, a1 = 0.0;
+      const double* li = L + (int64_t)i * d + b0;  // column i of L, rows b0..
+#pragma unroll
+      for (int c = 0; c < kSB; c += 2) {
+        a0 = fma(load_sel(li, c, c < bw), v[b0 + (c < bw ? c : 0)], a0);
+        a1 = fma(load_sel(li, c + 1, c + 1 < bw), v[b0 + (c + 1 < bw ? c + 1 : 0)], a1);
+      }
+      v[i] -= a0 + a1;
     }
     __syncthreads();
   }
@@ -312,19 +395,17 @@ static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, dou
   double dmax = 0.0;
   for (int64_t i = 0; i < (d < 500 ? d : 500); ++i) dmax = hs[i] > dmax ? hs[i] : dmax;
   const double tol2 = 1e-20 * dmax;
-  const size_t smem = sizeof(double) * ((size_t)(d + 1) * kPW + (size_t)d);  // panel + original diagonal
-  SLRA_CUDA(cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(8 * d * (kSB + 1))));
+  const size_t smem = sizeof(double) * ((size_t)(d + 1) * kPW + (size_t)d + kPW);  // panel, diagonal, 1/L(j,j)
   SLRA_CUDA(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SLRA_TIMED(cx, "lsr_solve", cholesky_kernel<<<1, kLT, smem, st>>>(G, (int)d, tol2, d_status);)
   SLRA_CHECK_LAUNCH(cx);
   // x = G^{-1} g, then one refinement step x += G^{-1} FA^T (Fb - FA x)
-  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, kST, 8 * d * (kSB + 1), st>>>(G, (int)d, g, x_hat, d_status, 0);)
+  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, kST, 8 * d, st>>>(G, (int)d, g, x_hat, d_status, 0);)
   SLRA_CHECK_LAUNCH(cx);
   SLRA_TIMED(cx, "lsr_solve", lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);)
   SLRA_CHECK_LAUNCH(cx);
   SLRA_TRY(launch_gemm(cx, 1, 0, d, 1, k, 1.0, FW, k, r, k, 0.0, cvec, d));
-  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, kST, 8 * d * (kSB + 1), st>>>(G, (int)d, cvec, x_hat, d_status, 1);)
+  SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, kST, 8 * d, st>>>(G, (int)d, cvec, x_hat, d_status, 1);)
   SLRA_CHECK_LAUNCH(cx);
   // sketched residual ||FA x - Fb|| by a direct pass
   SLRA_TIMED(cx, "lsr_solve", lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);)
