@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kCQ) gram_partial_kernel(const double* __restr
 #pragma unroll 4
   for (int e = tid; e < kGR * NP; e += kCQ) {
     const int i = e % kGR, c = e / kGR;
-    T[i + c * ldt] = (i < rows && c < n) ? Y[(r0 + i) + (int64_t)c * ldy] : 0.0;
+    T[i + c * ldt] = load_sel(Y, (r0 + i) + (int64_t)c * ldy, i < rows && c < n);
   }
   __syncthreads();
   double* out = P + b * sP + (int64_t)k * NP * NP;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(128) trsm_rows_kernel(const double* __restrict
   if (i >= m) return;
   double zr[NP];
 #pragma unroll
-  for (int c = 0; c < NP; ++c) zr[c] = c < n ? Y[i + (int64_t)c * ldy] : 0.0;
+  for (int c = 0; c < NP; ++c) zr[c] = load_sel(Y + i, (int64_t)c * ldy, c < n);
 #pragma unroll
   for (int c = 0; c < NP; ++c) {
     const double z = zr[c] * ri[c];
