@@ -16,7 +16,7 @@ namespace cg = cooperative_groups;
 namespace slra_dev {
 
 constexpr int kMT = 256;   // threads per CTA
-constexpr int kMRB = 128;  // max rows per CTA
+constexpr int kMRB = 256;  // max rows per CTA (one row per thread: fewer CTAs, fewer candidates per step)
 constexpr int kMR = 64;    // max r
 
 struct MaxvolLargeArgs {
@@ -181,8 +181,16 @@ __global__ void __launch_bounds__(kMT) maxvol_large_kernel(MaxvolLargeArgs a) {
       if (chosen[i]) continue;
       double* wi = W + i * ldw;
       if (r - k > 1 && t != 0.0) {
-        double w = 0.0;
-        for (int j = k + 1; j < r; ++j) w += vv[j] * wi[j];
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;  // four chains (FP64 FMA latency ~24)
+        int j = k + 1;
+        for (; j + 3 < r; j += 4) {
+          w0 = fma(vv[j], wi[j], w0);
+          w1 = fma(vv[j + 1], wi[j + 1], w1);
+          w2 = fma(vv[j + 2], wi[j + 2], w2);
+          w3 = fma(vv[j + 3], wi[j + 3], w3);
+        }
+        for (; j < r; ++j) w0 = fma(vv[j], wi[j], w0);
+        double w = (w0 + w1) + (w2 + w3);
         w += wi[k];
         wi[k] -= t * w;
         for (int j = k + 1; j < r; ++j) wi[j] -= t * vv[j] * w;
@@ -280,10 +288,8 @@ __global__ void __launch_bounds__(kMT) maxvol_large_kernel(MaxvolLargeArgs a) {
 }
 
 static int maxvol_large_grid(int num_sms, int64_t m) {
-  int64_t G = (m + kMRB - 1) / kMRB;
-  const int64_t floor_g = num_sms < m ? num_sms : m;
-  if (G < floor_g) G = floor_g;
-  return (int)G;
+  (void)num_sms;  // as few CTAs as the rows allow: fewer candidates to reduce per step
+  return (int)((m + kMRB - 1) / kMRB);
 }
 
 static size_t maxvol_large_smem() {
