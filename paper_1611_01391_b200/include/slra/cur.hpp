@@ -52,7 +52,8 @@ struct CaTrace {
 };
 
 /// cross_approx (cur.cpp:201-255). The whole loop runs in one CTA-resident
-/// kernel; stop_tol (posterior estimate) is not on the device path yet.
+/// kernel; with stop_tol the half-sweeps are host-driven over the device
+/// primitives and posterior_error_estimate (lra.cpp:88-127) runs on the device.
 std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r, Index k, Index l,
                                                   IndexSet init_rows, int loops, double h,
                                                   std::optional<double> stop_tol, Rng& rng);

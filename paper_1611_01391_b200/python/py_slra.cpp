@@ -155,11 +155,11 @@ PYBIND11_MODULE(_slra, m) {
     return d;
   });
   m.def("cross_approx", [](const FArray& A, Index r, Index k, Index l, const std::vector<Index>& init_rows, int loops,
-                           double h, Rng& rng) {
+                           double h, Rng& rng, std::optional<double> stop_tol) {
     Matrix M = from_np(A);
     DenseOracle o(M);
     IndexSet init = init_rows.empty() ? IndexSet() : mkset(init_rows, M.rows());
-    auto [c, trace] = cross_approx(o, r, k, l, std::move(init), loops, h, std::nullopt, rng);
+    auto [c, trace] = cross_approx(o, r, k, l, std::move(init), loops, h, stop_tol, rng);
     py::dict d = cur_dict(c);
     py::list steps;
     for (auto& s : trace.steps) {
@@ -168,13 +168,15 @@ PYBIND11_MODULE(_slra, m) {
       sd["rows"] = s.rows;
       sd["cols"] = s.cols;
       sd["volume_proxy"] = s.volume_proxy;
+      if (s.error_estimate) sd["error_estimate"] = *s.error_estimate;
+      else sd["error_estimate"] = py::none();
       steps.append(sd);
     }
     d["trace"] = steps;
     d["accesses"] = o.accesses();
     return d;
   }, py::arg("A"), py::arg("r"), py::arg("k"), py::arg("l"), py::arg("init_rows"), py::arg("loops"), py::arg("h"),
-     py::arg("rng"));
+     py::arg("rng"), py::arg("stop_tol") = py::none());
   m.def("cur_evaluate", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
                            const FArray& U) {
     Matrix M = from_np(A);

@@ -147,6 +147,82 @@ CurDecomposition primitive_cur(const Matrix& M, IndexSet I, IndexSet J, Index r,
   return primitive_cur(o, std::move(I), std::move(J), r, qr_nucleus);
 }
 
+// cross_approx with the early stop (cur.cpp:235-249): after every horizontal
+// half-sweep, primitive_cur probes the current generator and
+// posterior_error_estimate (lra.cpp:88-127) samples q x s = 20 x 20 entries
+// of M - C U R; the loop stops once the estimate is <= stop_tol. Host-driven
+// half-sweeps over the device primitives (gather -> select_rows_spanning with
+// its volume proxy); the sampled residual is a device GEMM + residual pass.
+// The rng draws happen exactly where the reference draws them (only after a
+// successful probe), so the caller's Rng stream matches.
+static std::pair<CurDecomposition, CaTrace> cross_approx_stop(const EntryOracle& M, Index r, Index k, Index l,
+                                                              IndexSet I, int loops, double h, double stop_tol,
+                                                              Rng& rng) {
+  slra_ctx cx = device_context();
+  const DeviceMatrix& dA = M.device();
+  const Index m = M.rows(), n = M.cols();
+  DevBuf<int64_t> dI(to64(I)), dJ(static_cast<size_t>(l));
+  DevBuf<double> ones(std::vector<double>(static_cast<size_t>(k), 1.0));
+  DevBuf<double> RT(static_cast<size_t>(n * k)), Cm(static_cast<size_t>(m * l)), vol(1);
+  CaTrace trace;
+  IndexSet J;
+  unsigned long long reads = 0;
+  auto download_set = [](DevBuf<int64_t>& d, Index bound) {
+    auto v = d.download();
+    return IndexSet(std::vector<Index>(v.begin(), v.end()), bound);
+  };
+  for (int loop = 0; loop < loops; ++loop) {
+    // J = select_rows_spanning(A(I,:)^T, l)
+    check(slra_sketch_rows_shard(cx, dA.data(), dA.ld(), 0, m, n, dI.get(), ones.get(), 1, k, RT.get(), n, 1),
+          "cross_approx");
+    check(slra_select_rows_spanning(cx, RT.get(), n, n, k, l, h, dJ.get(), vol.get()), "cross_approx");
+    J = download_set(dJ, n);
+    CaStep sv;
+    sv.horizontal = false;
+    sv.rows.assign(I.begin(), I.end());
+    sv.cols.assign(J.begin(), J.end());
+    sv.volume_proxy = vol.download()[0];
+    trace.steps.push_back(std::move(sv));
+    // I = select_rows_spanning(A(:,J), k)
+    check(slra_gather_cols(cx, dA.data(), dA.ld(), m, n, dJ.get(), l, Cm.get(), m), "cross_approx");
+    check(slra_select_rows_spanning(cx, Cm.get(), m, m, l, k, h, dI.get(), vol.get()), "cross_approx");
+    I = download_set(dI, m);
+    reads += static_cast<unsigned long long>(k * n + m * l);
+    CaStep st;
+    st.horizontal = true;
+    st.rows.assign(I.begin(), I.end());
+    st.cols.assign(J.begin(), J.end());
+    st.volume_proxy = vol.download()[0];
+    try {
+      const CurDecomposition probe = primitive_cur(M, I, J, r);
+      // f.U = M(:,J) nucleus, f.V = M(I,:): sample q x s entries of M - U V
+      const Index q = std::min<Index>(20, m), s = std::min<Index>(20, n);
+      DevBuf<int64_t> dIs(to64(IndexSet(rng.distinct_indices(q, m), m)));
+      DevBuf<int64_t> dJs(to64(IndexSet(rng.distinct_indices(s, n), n)));
+      DeviceMatrix Xs(q, l), Rs(k, s), Ms(q, s), P(q, k);
+      DeviceMatrix U = DeviceMatrix::upload(probe.nucleus);
+      check(slra_gather_block(cx, dA.data(), dA.ld(), m, n, dIs.get(), q, dJ.get(), l, Xs.data(), q), "estimate");
+      check(slra_gather_block(cx, dA.data(), dA.ld(), m, n, dI.get(), k, dJs.get(), s, Rs.data(), k), "estimate");
+      check(slra_gather_block(cx, dA.data(), dA.ld(), m, n, dIs.get(), q, dJs.get(), s, Ms.data(), q), "estimate");
+      check(slra_gemm(cx, 0, 0, q, k, l, 1.0, Xs.data(), q, U.data(), l, 0.0, P.data(), q), "estimate");
+      DevBuf<double> out(2);
+      check(slra_lowrank_residual(cx, Ms.data(), q, q, s, P.data(), q, Rs.data(), k, k, out.get()), "estimate");
+      const double sumsq = out.download()[0];
+      st.error_estimate = std::sqrt(static_cast<double>(m) * static_cast<double>(n) * sumsq /
+                                    static_cast<double>(q * s));
+      reads += static_cast<unsigned long long>(m * l + k * n + q * s);
+    } catch (const GeneratorRankFailure&) {
+      st.error_estimate.reset();
+    }
+    const bool stop = st.error_estimate && *st.error_estimate <= stop_tol;
+    trace.steps.push_back(std::move(st));
+    if (stop) break;
+  }
+  M.count(reads);
+  auto c = primitive_cur(M, std::move(I), std::move(J), r);
+  return {std::move(c), std::move(trace)};
+}
+
 std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r, Index k, Index l,
                                                   IndexSet init_rows, int loops, double h,
                                                   std::optional<double> stop_tol, Rng& rng) {
@@ -154,9 +230,10 @@ std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r,
   const Index m = M.rows(), n = M.cols();
   if (k < r || l < r || r < 0) throw std::invalid_argument("cross_approx: need k, l >= r >= 1");
   if (loops < 1) throw std::invalid_argument("cross_approx: need loops >= 1");
-  if (stop_tol) throw std::invalid_argument("cross_approx: stop_tol is not on the device path yet");
+  if (stop_tol && r < 1) throw std::invalid_argument("cross_approx: stop_tol needs a fixed r >= 1");
   IndexSet I = (init_rows.size() == k && init_rows.bound() == m) ? std::move(init_rows)
                                                                  : IndexSet(rng.distinct_indices(k, m), m);
+  if (stop_tol) return cross_approx_stop(M, r, k, l, std::move(I), loops, h, *stop_tol, rng);
   const DeviceMatrix& dA = M.device();
   DevBuf<int64_t> dI0(to64(I)), dI(static_cast<size_t>(k)), dJ(static_cast<size_t>(l));
   DevBuf<int64_t> trows(static_cast<size_t>(2 * loops * k)), tcols(static_cast<size_t>(2 * loops * l));

@@ -520,6 +520,42 @@ def test_sketch_solve_known_answers(slra):  # test_lsr.cpp:59-90
         slra.sketch_solve(np.zeros((32, 4)) + 0.0, b, Z)
 
 
+# ---------------------------------------------------------------- C-A early stop (a15)
+@pytest.mark.parametrize("seed,tol", [(0, 1e-3), (1, 0.0), (2, 1e-6)])
+def test_cross_approx_stop_tol_parity(slra, oracle, seed, tol):
+    """cross_approx with stop_tol (cur.cpp:235-249): the posterior estimate
+    (lra.cpp:88-127, 20 x 20 sampled entries) after every horizontal
+    half-sweep; same trace length, index sets, estimates and Rng stream."""
+    A = slra.gen_factor_gaussian(256, 256, 8, 1e-8, slra.Rng(40 + seed))
+    nA = np.linalg.norm(A)
+    init = slra.Rng(60 + seed).distinct_indices(16, 256)
+    rg, ro = slra.Rng(7), oracle.Rng(7)
+    g = slra.cross_approx(A, 8, 16, 16, init, 4, 1.1, rg, tol * nA)
+    o = oracle.cross_approx(A, 8, 16, 16, init, 4, 1.1, tol * nA, ro)
+    assert len(g["trace"]) == len(o["trace"])
+    assert g["I"] == o["I"] and g["J"] == o["J"]
+    for sg, so in zip(g["trace"], o["trace"]):
+        assert sg["rows"] == so["rows"] and sg["cols"] == so["cols"]
+        if so["error_estimate"] is None:
+            assert sg["error_estimate"] is None
+        else:
+            assert abs(sg["error_estimate"] - so["error_estimate"]) <= 1e-6 * so["error_estimate"] + 1e-12 * nA
+    assert rg.next_u64() == ro.next_u64()  # the caller's stream advanced identically
+    if tol > 0:
+        assert len(o["trace"]) < 8  # stopped early
+
+
+def test_cross_approx_stop_tol_probe_failure(slra, oracle):
+    """r above the generator rank: every probe fails (no estimate, no draws)
+    and the final primitive_cur raises GeneratorRankFailure, as the reference."""
+    A = slra.gen_factor_gaussian(128, 128, 5, 0.0, slra.Rng(3))
+    init = slra.Rng(4).distinct_indices(12, 128)
+    with pytest.raises(slra.GeneratorRankFailure):
+        slra.cross_approx(A, 8, 12, 12, init, 2, 1.1, slra.Rng(0), 1e-3)
+    with pytest.raises(oracle.GeneratorRankFailure):
+        oracle.cross_approx(A, 8, 12, 12, init, 2, 1.1, 1e-3, oracle.Rng(0))
+
+
 # ---------------------------------------------------------------- edge cases
 def test_select_rows_spanning_padding_branch(slra, oracle):  # cur.cpp:125-134
     A = oracle.Rng(41).gaussian_matrix(200, 10)
