@@ -36,7 +36,8 @@ enum slra_status {
   SLRA_ERR_GENERATOR_RANK_FAILURE = 5,/* GeneratorRankFailure(cur.cpp:157)*/
   SLRA_ERR_CUDA = 6,                  /* CUDA runtime error               */
   SLRA_ERR_NO_DEVICE = 7,             /* no CUDA device / wrong arch      */
-  SLRA_ERR_UNSUPPORTED = 8            /* shape outside the device kernels */
+  SLRA_ERR_UNSUPPORTED = 8,           /* shape outside the device kernels */
+  SLRA_ERR_PREMULT_RANK_FAILURE = 9   /* PremultRankFailure  (lra.cpp:47) */
 };
 
 typedef struct slra_context* slra_ctx;
@@ -221,6 +222,32 @@ int slra_range_finder_batched(slra_ctx ctx, const double* d_M, int64_t ldm, int6
                               int64_t l, int64_t r, int variant, double* const* h_U, int64_t ldu,
                               double* const* h_V, int64_t ldv, double* d_out, double* d_sigma,
                               int32_t* h_status);
+
+/* ------------------------------------------------------------ §8f range-finder variants
+ * pseudo_inverse (linalg.cpp:111-121): P = A^+ (n x m) through the SVD,
+ * sigma below rank_tol * sigma_0 dropped; *h_rank = the kept count (so with
+ * rank_tol = tol it is numerical_rank(A, tol, Relative)). min(m,n) <= 64. */
+int slra_pinv(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, double rank_tol,
+              double* d_P, int64_t ldp, int64_t* h_rank);
+/* lra_premult (lra.cpp:41-52): U = range_basis(M, H, r, variant) as in
+ * slra_range_finder (H: right plan, l outputs), then V = (F U)^+ (F M) with F
+ * a compiled LEFT plan of s rows (see slra_sketch_rows). U is m x l (variant
+ * 0) or m x r (variant 1); V is that many rows x n. d_out (optional) gets
+ * ||M - U V||_F^2 and ||M||_F^2. SLRA_ERR_RANGE_FAILURE as range_finder;
+ * SLRA_ERR_PREMULT_RANK_FAILURE when numerical_rank(F U, 1e-10, Relative) < r.
+ * min(s, cols of U) <= 64. Blocks. */
+int slra_lra_premult(slra_ctx ctx, const double* d_M, int64_t ldm, int64_t m, int64_t n,
+                     const int64_t* d_hsrc, const double* d_hcoef, const int32_t* d_hq,
+                     int64_t h_width, int h_tree, int64_t l, const int64_t* d_fsrc,
+                     const double* d_fcoef, const int32_t* d_fq, int64_t f_width, int f_tree,
+                     int64_t s, int64_t r, int variant, double* d_U, int64_t ldu, double* d_V,
+                     int64_t ldv, double* d_out);
+/* two_stage_truncate (lra.cpp:54-63): Q R = thin_qr(U) (U m x l), core =
+ * svd(R V) (V l x n), U' = Q S_r diag(sigma_r) (m x r), V' = T_r^T (r x n).
+ * 1 <= r <= min(l, n), l <= min(m, 64). */
+int slra_two_stage_truncate(slra_ctx ctx, const double* d_U, int64_t ldu, int64_t m, int64_t l,
+                            const double* d_V, int64_t ldv, int64_t n, int64_t r, double* d_Uo,
+                            int64_t lduo, double* d_Vo, int64_t ldvo);
 
 /* ------------------------------------------------------------ a11/a12 LSR
  * sketch_solve (lsr.cpp:37-67): FW = F (A|b) through a compiled left-side

@@ -267,6 +267,8 @@ enum class RangeVariant { BasisQr, TruncatedRankR };
 LowRankFactors range_finder(const Matrix& M, const SketchOperator& H, Index r,
                             RangeVariant variant = RangeVariant::BasisQr);
 LowRankFactors two_stage_truncate(const LowRankFactors& f, Index r);
+LowRankFactors lra_premult(const Matrix& M, const SketchOperator& F, const SketchOperator& H, Index r,
+                           RangeVariant variant = RangeVariant::BasisQr);
 struct LraErrorEstimate {
   double estimate_frobenius = 0;
   Index sample_rows = 0, sample_cols = 0;

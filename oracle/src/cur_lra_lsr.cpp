@@ -230,6 +230,21 @@ LowRankFactors range_finder(const Matrix& M, const SketchOperator& H, Index r, R
   return out;
 }
 
+// lra.cpp:41-52: U as range_finder's, V = (F U)^+ (F M); PremultRankFailure
+// when numerical_rank(F U, 1e-10, Relative) < r.
+LowRankFactors lra_premult(const Matrix& M, const SketchOperator& F, const SketchOperator& H, Index r,
+                           RangeVariant variant) {
+  if (F.cols() != M.rows()) throw std::invalid_argument("lra_premult: F cols != m");
+  LowRankFactors out;
+  out.U = range_basis(M, H, r, variant);
+  const Matrix FU = apply(F, out.U, Side::Left);
+  if (numerical_rank(FU, 1e-10, RankMode::Relative) < r)
+    throw PremultRankFailure("lra_premult: F U has numerical rank below target");
+  out.V = matmul(pseudo_inverse(FU), apply(F, M, Side::Left));
+  out.target_rank = r;
+  return out;
+}
+
 // lra.cpp:54-63
 LowRankFactors two_stage_truncate(const LowRankFactors& f, Index r) {
   if (r < 1 || r > f.U.cols()) throw std::invalid_argument("two_stage_truncate: need 1 <= r <= l");

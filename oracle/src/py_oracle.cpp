@@ -207,6 +207,11 @@ PYBIND11_MODULE(_oracle, m) {
   m.def("lowrank_residual_frobenius", [](const FArray& M, const FArray& U, const FArray& V) {
     return frobenius_norm(sub(from_np(M), matmul(from_np(U), from_np(V))));
   });
+  m.def("lra_premult", [](const FArray& M, const PyOp& F, const PyOp& H, Index r, bool truncated) {
+    LowRankFactors f = lra_premult(from_np(M), *F.p, *H.p, r,
+                                   truncated ? RangeVariant::TruncatedRankR : RangeVariant::BasisQr);
+    return py::make_tuple(to_np(f.U), to_np(f.V));
+  }, py::arg("M"), py::arg("F"), py::arg("H"), py::arg("r"), py::arg("truncated") = false);
   m.def("two_stage_truncate", [](const FArray& U, const FArray& V, Index r) {
     LowRankFactors f{from_np(U), from_np(V), 0};
     LowRankFactors g = two_stage_truncate(f, r);

@@ -15,6 +15,8 @@
 namespace slra_dev {
 
 // ------------------------------------------------------------------ context
+constexpr int kArenaSlots = 10;
+
 struct Context {
   int device = 0;
   int num_sms = 148;
@@ -35,9 +37,9 @@ struct Context {
   void* hsmall = nullptr;
   // independent growable device arenas for multi-kernel orchestrations
   // (0: range finder, 1: cur residual, 2: lsr, 3: svd, 4: large C-A, 5: factored residual,
-  //  6: wide-svd transpose, 7: tall maxvol/select)
-  void* arena[8] = {};
-  size_t arena_bytes[8] = {};
+  //  6: wide-svd transpose, 7: tall maxvol/select, 8: pinv, 9: premult / two-stage truncate)
+  void* arena[kArenaSlots] = {};
+  size_t arena_bytes[kArenaSlots] = {};
   // opt-in per-kernel-family timing (CUDA events on the context stream)
   bool timing = false;
   struct Rec {

@@ -770,13 +770,18 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
         {  // two accumulators per product: FP64 FMA latency is ~24 cycles on sm_100
           double a1 = 0.0, b1 = 0.0, g1 = 0.0;
 #pragma unroll
-          for (int r = 0; r < RPG; r += 2) {
+          for (int r = 0; r + 1 < RPG; r += 2) {
             aa = fma(x[r], x[r], aa);
             bb = fma(y[r], y[r], bb);
             gg = fma(x[r], y[r], gg);
             a1 = fma(x[r + 1], x[r + 1], a1);
             b1 = fma(y[r + 1], y[r + 1], b1);
             g1 = fma(x[r + 1], y[r + 1], g1);
+          }
+          if (RPG & 1) {  // odd rows per lane: the last one (no read past x/y)
+            aa = fma(x[RPG - 1], x[RPG - 1], aa);
+            bb = fma(y[RPG - 1], y[RPG - 1], bb);
+            gg = fma(x[RPG - 1], y[RPG - 1], gg);
           }
           aa += a1;
           bb += b1;

@@ -106,14 +106,17 @@ int slra_cur_residual_factored(slra_ctx ctx, const double* A, int64_t lda, int64
 // thin QR / TSQR) -> SVD(R_s) (batched, one CTA each) -> one rank check for
 // all -> U_s, V_s -> residuals. Host-array arguments (h_*) hold per-sketch
 // device pointers / sizes.
-int slra_range_finder_batched(slra_ctx ctx, const double* M, int64_t ldm, int64_t m, int64_t n, int nsk,
-                              const int64_t* const* h_src, const double* const* h_coef, const int32_t* const* h_q,
-                              const int64_t* h_width, const int* h_tree, int64_t l, int64_t r, int variant,
-                              double* const* h_U, int64_t ldu, double* const* h_V, int64_t ldv, double* d_out,
-                              double* d_sigma, int32_t* h_status) {
-  if (!ctx || ldm < m || l < 1 || r < 1 || r > l || l > m || l > 64 || nsk < 1 || nsk > 64)
+}  // extern "C"
+
+namespace slra_dev {
+// want_v = false: the basis only (range_basis, lra.cpp:14-28) for lra_premult.
+int range_finder_core(Context* cx, const double* M, int64_t ldm, int64_t m, int64_t n, int nsk,
+                      const int64_t* const* h_src, const double* const* h_coef, const int32_t* const* h_q,
+                      const int64_t* h_width, const int* h_tree, int64_t l, int64_t r, int variant,
+                      double* const* h_U, int64_t ldu, double* const* h_V, int64_t ldv, double* d_out,
+                      double* d_sigma, int32_t* h_status, bool want_v) {
+  if (ldm < m || l < 1 || r < 1 || r > l || l > m || l > 64 || nsk < 1 || nsk > 64)
     return SLRA_ERR_INVALID_ARGUMENT;
-  Context* cx = C(ctx);
   const int64_t ucols = variant == 1 ? r : l;
   if (ldu < m || ldv < ucols) return SLRA_ERR_INVALID_ARGUMENT;
   const size_t tw = tsqr_workspace_doubles(m, (int)l);
@@ -197,19 +200,34 @@ int slra_range_finder_batched(slra_ctx ctx, const double* M, int64_t ldm, int64_
                                                                                     dptr + nsk, m);)
     SLRA_CHECK_LAUNCH(cx);
     for (int s = 0; s < nsk; ++s)
-      if (ok[s]) SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, r, n, m, 1.0, Qm + s * sMH, m, M, ldm, 0.0, h_V[s], ldv));
+      if (ok[s] && want_v)
+        SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, r, n, m, 1.0, Qm + s * sMH, m, M, ldm, 0.0, h_V[s], ldv));
   } else {
     // BasisQr: U = Q (thin_qr sign rule already applied), V = U^T M
     for (int s = 0; s < nsk; ++s) {
       SLRA_CUDA(cudaMemcpy2DAsync(h_U[s], 8 * ldu, Qm + s * sMH, 8 * m, 8 * m, l, cudaMemcpyDeviceToDevice,
                                   cx->stream));
-      if (ok[s]) SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, l, n, m, 1.0, h_U[s], ldu, M, ldm, 0.0, h_V[s], ldv));
+      if (ok[s] && want_v)
+        SLRA_TRY(launch_gemm_fam(cx, "gemm_v", 1, 0, l, n, m, 1.0, h_U[s], ldu, M, ldm, 0.0, h_V[s], ldv));
     }
   }
-  if (d_out)
+  if (d_out && want_v)
     for (int s = 0; s < nsk; ++s)
       if (ok[s]) SLRA_TRY(launch_lowrank_residual(cx, M, ldm, m, n, h_U[s], ldu, h_V[s], ldv, ucols, d_out + 2 * s));
   return SLRA_OK;
+}
+}  // namespace slra_dev
+
+extern "C" {
+
+int slra_range_finder_batched(slra_ctx ctx, const double* M, int64_t ldm, int64_t m, int64_t n, int nsk,
+                              const int64_t* const* h_src, const double* const* h_coef, const int32_t* const* h_q,
+                              const int64_t* h_width, const int* h_tree, int64_t l, int64_t r, int variant,
+                              double* const* h_U, int64_t ldu, double* const* h_V, int64_t ldv, double* d_out,
+                              double* d_sigma, int32_t* h_status) {
+  if (!ctx) return SLRA_ERR_INVALID_ARGUMENT;
+  return range_finder_core(C(ctx), M, ldm, m, n, nsk, h_src, h_coef, h_q, h_width, h_tree, l, r, variant, h_U, ldu,
+                           h_V, ldv, d_out, d_sigma, h_status, true);
 }
 
 int slra_range_finder(slra_ctx ctx, const double* M, int64_t ldm, int64_t m, int64_t n, const int64_t* src,

@@ -98,6 +98,7 @@ const char* slra_status_string(int s) {
     case SLRA_ERR_SKETCH_RANK_FAILURE: return "sketch_solve: sketched matrix FA is rank deficient";
     case SLRA_ERR_SELECTION_FAILURE: return "maxvol_rows: singular pivot block";
     case SLRA_ERR_GENERATOR_RANK_FAILURE: return "primitive_cur: generator rank below target";
+    case SLRA_ERR_PREMULT_RANK_FAILURE: return "lra_premult: F U has numerical rank below target";
     case SLRA_ERR_CUDA: return "CUDA error";
     case SLRA_ERR_NO_DEVICE: return "no usable CUDA device (sm_100a required)";
     case SLRA_ERR_UNSUPPORTED: return "shape not supported by the device kernels";
@@ -152,7 +153,7 @@ int slra_ctx_destroy(slra_ctx ctx) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->partials) cudaFree(c->partials);
   if (c->dsmall) cudaFree(c->dsmall);
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < kArenaSlots; ++i)
     if (c->arena[i]) cudaFree(c->arena[i]);
   for (auto& r : c->records) {
     cudaEventDestroy(r.start);

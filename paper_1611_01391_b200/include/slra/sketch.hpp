@@ -70,6 +70,11 @@ OpPtr make_product(std::vector<OpPtr> ops);
 OpPtr take_columns(OpPtr op, IndexSet columns);
 OpPtr take_columns(OpPtr op, Index l, ColumnMode mode, Rng& rng);
 
+/// Dense operator G (reference GaussianOp, used by the tests): full-width
+/// list plans, not a hot-path operator.
+OpPtr make_gaussian(Matrix G);
+OpPtr gen_gaussian(Index rows, Index cols, Rng& rng);
+
 OpPtr gen_permutation(Index n, Rng& rng);
 OpPtr gen_sign_diagonal(Index n, Rng& rng);
 OpPtr gen_sparse_circulant(Index n, Index s, Rng& rng);

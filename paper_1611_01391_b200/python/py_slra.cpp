@@ -229,6 +229,8 @@ PYBIND11_MODULE(_slra, m) {
   m.def("take_columns_random", [](const PyOp& op, Index l, Rng& rng) {
     return PyOp{take_columns(op.p, l, ColumnMode::Random, rng)};
   });
+  m.def("make_gaussian", [](const FArray& G) { return PyOp{make_gaussian(from_np(G))}; });
+  m.def("gen_gaussian", [](Index a, Index b, Rng& r) { return PyOp{gen_gaussian(a, b, r)}; });
   m.def("gen_permutation", [](Index n, Rng& r) { return PyOp{gen_permutation(n, r)}; });
   m.def("gen_sign_diagonal", [](Index n, Rng& r) { return PyOp{gen_sign_diagonal(n, r)}; });
   m.def("gen_sparse_circulant", [](Index n, Index s, Rng& r) { return PyOp{gen_sparse_circulant(n, s, r)}; });
@@ -244,6 +246,19 @@ PYBIND11_MODULE(_slra, m) {
     LowRankFactors f = range_finder(from_np(M), *H.p, r, truncated ? RangeVariant::TruncatedRankR : RangeVariant::BasisQr);
     return py::make_tuple(to_np(f.U), to_np(f.V));
   }, py::arg("M"), py::arg("H"), py::arg("r"), py::arg("truncated") = false);
+  m.def("lra_premult", [](const FArray& M, const PyOp& F, const PyOp& H, Index r, bool truncated) {
+    LowRankFactors f = lra_premult(from_np(M), *F.p, *H.p, r,
+                                   truncated ? RangeVariant::TruncatedRankR : RangeVariant::BasisQr);
+    return py::make_tuple(to_np(f.U), to_np(f.V));
+  }, py::arg("M"), py::arg("F"), py::arg("H"), py::arg("r"), py::arg("truncated") = false);
+  m.def("two_stage_truncate", [](const FArray& U, const FArray& V, Index r) {
+    LowRankFactors f;
+    f.U = from_np(U);
+    f.V = from_np(V);
+    f.target_rank = f.U.cols();
+    LowRankFactors g = two_stage_truncate(f, r);
+    return py::make_tuple(to_np(g.U), to_np(g.V));
+  });
   m.def("sketch_solve", [](const FArray& A, const FArray& b, const PyOp& F, bool with_true) {
     LsrReport rep = sketch_solve(LsrProblem{from_np(A), np_vec(b)}, *F.p, with_true);
     py::dict d;

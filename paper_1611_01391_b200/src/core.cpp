@@ -23,6 +23,7 @@ void check(int status, const char* where) {
     case SLRA_ERR_SKETCH_RANK_FAILURE: throw SketchRankFailure(msg);
     case SLRA_ERR_SELECTION_FAILURE: throw SelectionFailure(msg);
     case SLRA_ERR_GENERATOR_RANK_FAILURE: throw GeneratorRankFailure(msg);
+    case SLRA_ERR_PREMULT_RANK_FAILURE: throw PremultRankFailure(msg);
     case SLRA_ERR_UNSUPPORTED: throw std::invalid_argument(msg);
     default: throw DeviceError(msg + " (" + slra_last_error() + ")");
   }

@@ -45,19 +45,11 @@ Svd svd(const Matrix& A) {  // linalg.cpp:81-98
 }
 
 Matrix pseudo_inverse(const Matrix& A, double rank_tol) {  // linalg.cpp:111-121
-  const Svd f = svd(A);
-  Matrix out(A.cols(), A.rows());
-  if (f.sigma.empty() || f.sigma[0] == 0.0) return out;
-  const double cut = rank_tol * f.sigma[0];
-  Index rho = 0;
-  while (rho < static_cast<Index>(f.sigma.size()) && f.sigma[static_cast<size_t>(rho)] > cut) ++rho;
-  if (rho == 0) return out;
-  Matrix TS(A.cols(), rho), St(rho, A.rows());
-  for (Index j = 0; j < rho; ++j)
-    for (Index i = 0; i < A.cols(); ++i) TS(i, j) = f.T(i, j) / f.sigma[static_cast<size_t>(j)];
-  for (Index i = 0; i < A.rows(); ++i)
-    for (Index j = 0; j < rho; ++j) St(j, i) = f.S(i, j);
-  return matmul(TS, St);
+  DeviceMatrix dA = DeviceMatrix::upload(A), dP(A.cols(), A.rows());
+  int64_t rho = 0;
+  check(slra_pinv(device_context(), dA.data(), dA.ld(), A.rows(), A.cols(), rank_tol, dP.data(), dP.ld(), &rho),
+        "slra_pinv");
+  return dP.download();
 }
 
 Index numerical_rank(const Matrix& A, double tol, RankMode mode) {  // linalg.cpp:123-132
@@ -334,6 +326,46 @@ LowRankFactors range_finder(const Matrix& M, const SketchOperator& H, Index r, R
   f.V = dV.download();
   f.target_rank = r;
   return f;
+}
+
+LowRankFactors lra_premult(const Matrix& M, const SketchOperator& F, const SketchOperator& H, Index r,
+                           RangeVariant variant) {  // lra.cpp:41-52
+  if (F.cols() != M.rows()) throw std::invalid_argument("lra_premult: F cols != m");
+  if (H.rows() != M.cols()) throw std::invalid_argument("range_finder: H rows != n");
+  const Index l = H.cols();
+  if (r < 1 || r > l) throw std::invalid_argument("range_finder: need 1 <= r <= l");
+  const SketchPlan ph = compile_plan(H, Side::Right), pf = compile_plan(F, Side::Left);
+  DevBuf<int64_t> hs(ph.src), fs(pf.src);
+  DevBuf<double> hc(ph.coef), fc(pf.coef);
+  DevBuf<int32_t> hq(ph.q), fq(pf.q);
+  DeviceMatrix dM = DeviceMatrix::upload(M);
+  const Index uc = variant == RangeVariant::TruncatedRankR ? r : l;
+  DeviceMatrix dU(M.rows(), uc), dV(uc, M.cols());
+  check(slra_lra_premult(device_context(), dM.data(), dM.ld(), M.rows(), M.cols(), hs.get(), hc.get(), hq.get(),
+                         ph.width, ph.tree, ph.count, fs.get(), fc.get(), fq.get(), pf.width, pf.tree, pf.count, r,
+                         variant == RangeVariant::TruncatedRankR ? 1 : 0, dU.data(), dU.ld(), dV.data(), dV.ld(),
+                         nullptr),
+        "lra_premult");
+  LowRankFactors f;
+  f.U = dU.download();
+  f.V = dV.download();
+  f.target_rank = r;
+  return f;
+}
+
+LowRankFactors two_stage_truncate(const LowRankFactors& f, Index r) {  // lra.cpp:54-63
+  if (r < 1 || r > f.l()) throw std::invalid_argument("two_stage_truncate: need 1 <= r <= l");
+  const Index m = f.U.rows(), n = f.V.cols();
+  if (f.V.rows() != f.l()) throw std::invalid_argument("two_stage_truncate: U, V inner dimensions differ");
+  DeviceMatrix dU = DeviceMatrix::upload(f.U), dV = DeviceMatrix::upload(f.V), dUo(m, r), dVo(r, n);
+  check(slra_two_stage_truncate(device_context(), dU.data(), dU.ld(), m, f.l(), dV.data(), dV.ld(), n, r, dUo.data(),
+                                dUo.ld(), dVo.data(), dVo.ld()),
+        "two_stage_truncate");
+  LowRankFactors out;
+  out.U = dUo.download();
+  out.V = dVo.download();
+  out.target_rank = r;
+  return out;
 }
 
 }  // namespace slra

@@ -254,6 +254,40 @@ OpPtr make_abridged_hadamard(Index n, int d) { return std::make_shared<AbridgedH
 OpPtr make_sparse_circulant(Index n, double f, std::vector<std::pair<Index, double>> nz) {
   return std::make_shared<SparseCirculantOp>(n, f, std::move(nz));
 }
+// Dense operator (sketch.cpp GaussianOp, tests only): every output is the
+// full list combination of the rows, coefficients G(i, :) in column order.
+class GaussianOp final : public SketchOperator {
+ public:
+  explicit GaussianOp(Matrix G) : G_(std::move(G)) {}
+  Index rows() const override { return G_.rows(); }
+  Index cols() const override { return G_.cols(); }
+  std::string kind() const override { return "gaussian"; }
+  RowExpr row_of_apply(Index i) const override {
+    RowExpr e;
+    e.tree = SLRA_TREE_LIST;
+    for (Index j = 0; j < G_.cols(); ++j) {
+      e.src.push_back(j);
+      e.coef.push_back(G_(i, j));
+    }
+    return e;
+  }
+  RowExpr row_of_apply_transpose(Index j) const override {
+    RowExpr e;
+    e.tree = SLRA_TREE_LIST;
+    for (Index i = 0; i < G_.rows(); ++i) {
+      e.src.push_back(i);
+      e.coef.push_back(G_(i, j));
+    }
+    return e;
+  }
+
+ private:
+  Matrix G_;
+};
+
+OpPtr make_gaussian(Matrix G) { return std::make_shared<GaussianOp>(std::move(G)); }
+OpPtr gen_gaussian(Index rows, Index cols, Rng& rng) { return make_gaussian(rng.gaussian_matrix(rows, cols)); }
+
 OpPtr make_sub_identity(IndexSet selected, Index total) {
   return std::make_shared<SubIdentityOp>(std::move(selected), total);
 }

@@ -111,7 +111,11 @@ def test_thin_qr_rank_deficient_tsqr(slra, oracle):
     assert np.linalg.norm(Q @ R - A) <= 1e-13 * np.linalg.norm(A) * 64
 
 
-@pytest.mark.parametrize("shape", [(2, 2), (7, 5), (5, 7), (64, 64), (32, 32), (256, 48), (4096, 48), (48, 300)])
+# every rows-per-lane instantiation of the Jacobi kernel (p = 1..64 -> RPG 1..8,
+# odd RPG included) on the one-CTA, tall (QR + square Jacobi) and wide paths
+@pytest.mark.parametrize("shape", [(2, 2), (7, 5), (5, 7), (64, 64), (32, 32), (256, 48), (4096, 48), (48, 300),
+                                   (17, 9), (9, 17), (20, 20), (33, 33), (40, 23), (56, 50), (61, 61),
+                                   (300, 20), (4096, 20), (1000, 33), (20, 700), (5000, 57)])
 def test_svd_vs_oracle(slra, oracle, shape):
     A = oracle.Rng(sum(shape) + 5).gaussian_matrix(*shape)
     S, sig, T = slra.svd(A)

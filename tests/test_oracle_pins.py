@@ -404,6 +404,85 @@ def test_range_finder_graded_spectrum_asph(oracle):  # test_lra.cpp:32-44 (5 tri
     assert tot / 5 <= 1e-6
 
 
+def test_premult_identity_matches_range_finder(oracle):  # test_lra.cpp:98-108
+    rng = oracle.Rng(25)
+    m, n = 30, 24
+    M = rng.gaussian_matrix(m, n)
+    H = oracle.gen_gaussian(n, 6, rng)
+    F = oracle.make_sub_identity(list(range(m)), m)
+    Ua, Va = oracle.range_finder(M, H, 4)
+    Ub, Vb = oracle.lra_premult(M, F, H, 4)
+    assert np.linalg.norm(Ua - Ub, 2) <= 1e-12
+    assert np.linalg.norm(Va - Vb, 2) <= 1e-12
+
+
+def test_premult_exact_rank(oracle):  # test_lra.cpp:110-120
+    for t in range(10):
+        rng = oracle.Rng(900 + t)
+        m, n, r, l, k = 48, 40, 5, 8, 12
+        M = oracle.gen_factor_gaussian(m, n, r, 0.0, rng)
+        H = oracle.gen_gaussian(n, l, rng)
+        F = oracle.gen_gaussian(k, m, rng)
+        U, V = oracle.lra_premult(M, F, H, r)
+        assert np.linalg.norm(M - U @ V, 2) <= 1e-9 * np.linalg.norm(M, 2)
+
+
+def test_premult_residual_identity_and_impact(oracle):  # test_lra.cpp:122-142
+    rng = oracle.Rng(26)
+    m, n, r, l, k = 8, 8, 2, 3, 5
+    for _ in range(20):
+        M = rng.gaussian_matrix(m, n)
+        Hd = rng.gaussian_matrix(n, l)
+        Fd = rng.gaussian_matrix(k, m)
+        U, V = oracle.lra_premult(M, oracle.make_gaussian(Fd), oracle.make_gaussian(Hd), r)
+        FU = Fd @ U
+        P = np.eye(m) - U @ np.linalg.pinv(FU, rcond=1e-10) @ Fd
+        resid = P @ (M - U @ (U.T @ M))
+        assert np.linalg.norm(M - U @ V - resid, 2) <= 1e-9 * np.linalg.norm(M, 2)
+        impact = np.linalg.norm(P, 2)
+        bound = 1 + np.linalg.norm(U, 2) * np.linalg.norm(np.linalg.pinv(FU, rcond=1e-10), 2) * np.linalg.norm(Fd, 2)
+        assert impact <= bound * (1 + 1e-12)
+
+
+def test_premult_rank_failure(oracle):  # test_lra.cpp:144-150
+    rng = oracle.Rng(27)
+    M = oracle.gen_factor_gaussian(16, 16, 3, 0.0, rng)
+    H = oracle.gen_gaussian(16, 4, rng)
+    F = oracle.make_gaussian(np.zeros((5, 16)))
+    with pytest.raises(oracle.PremultRankFailure):
+        oracle.lra_premult(M, F, H, 3)
+
+
+def test_two_stage_truncate(oracle):  # test_lra.cpp:152-170
+    rng = oracle.Rng(28)
+    m, n, l = 40, 32, 8
+    U = rng.gaussian_matrix(m, l)
+    V = rng.gaussian_matrix(l, n)
+    P = U @ V
+    Us, Vs = oracle.two_stage_truncate(U, V, l)
+    assert np.linalg.norm(P - Us @ Vs, 2) <= 1e-12 * np.linalg.norm(P, 2)
+    U3, V3 = oracle.two_stage_truncate(U, V, 3)
+    S, sig, Tt = np.linalg.svd(P)
+    dense3 = (S[:, :3] * sig[:3]) @ Tt[:3]
+    assert np.linalg.norm(U3 @ V3 - dense3, 2) <= 1e-9 * np.linalg.norm(P, 2)
+    with pytest.raises(Exception):
+        oracle.two_stage_truncate(U, V, l + 1)
+
+
+def test_two_stage_truncation_bound(oracle):  # test_lra.cpp:172-193 (25 of the 100 trials)
+    for t in range(25):
+        rng = oracle.Rng(1000 + t)
+        n, r, l = 64, 4, 8
+        M = oracle.gen_factor_gaussian(n, n, r, 1e-4, rng)
+        H = oracle.gen_gaussian(n, l, rng)
+        U, V = oracle.range_finder(M, H, r)
+        Ug, Vg = oracle.two_stage_truncate(U, V, r)
+        sig = np.linalg.svd(M, compute_uv=False)
+        tau = np.sqrt(np.sum(sig[r:] ** 2))
+        lhs = np.linalg.norm(M - Ug @ Vg)
+        assert lhs <= (tau + 2 * np.linalg.norm(M - U @ V)) * (1 + 1e-8)
+
+
 def test_lsr_full_permutation_exact(oracle):  # test_lsr.cpp:59-69
     rng = oracle.Rng(13)
     A = rng.gaussian_matrix(30, 3)
