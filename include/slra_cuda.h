@@ -116,8 +116,9 @@ int slra_sketch_rows_shard(slra_ctx ctx, const double* d_W, int64_t ldw, int64_t
 int slra_thin_qr(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t c,
                  double* d_Q, int64_t ldq, double* d_R, int64_t ldr);
 /* svd (linalg.cpp:81-98): compact SVD, sigma nonincreasing, largest-|.|
- * entry of each left vector >= 0. min(m,n) <= 64. S is m x p, T is n x p,
- * p = min(m, n). */
+ * entry of each left vector >= 0. S is m x p, T is n x p, p = min(m, n).
+ * min(m,n) <= 64: one CTA (QR pre-reduction for tall inputs); larger: a
+ * multi-CTA one-sided Jacobi in HBM (p <= 16384). Blocks only on arena growth. */
 int slra_svd(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
              double* d_S, int64_t lds, double* d_sigma, double* d_T, int64_t ldt);
 
@@ -226,7 +227,7 @@ int slra_range_finder_batched(slra_ctx ctx, const double* d_M, int64_t ldm, int6
 /* ------------------------------------------------------------ §8f range-finder variants
  * pseudo_inverse (linalg.cpp:111-121): P = A^+ (n x m) through the SVD,
  * sigma below rank_tol * sigma_0 dropped; *h_rank = the kept count (so with
- * rank_tol = tol it is numerical_rank(A, tol, Relative)). min(m,n) <= 64. */
+ * rank_tol = tol it is numerical_rank(A, tol, Relative)). Shapes as slra_svd. */
 int slra_pinv(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, double rank_tol,
               double* d_P, int64_t ldp, int64_t* h_rank);
 /* lra_premult (lra.cpp:41-52): U = range_basis(M, H, r, variant) as in
@@ -248,6 +249,46 @@ int slra_lra_premult(slra_ctx ctx, const double* d_M, int64_t ldm, int64_t m, in
 int slra_two_stage_truncate(slra_ctx ctx, const double* d_U, int64_t ldu, int64_t m, int64_t l,
                             const double* d_V, int64_t ldv, int64_t n, int64_t r, double* d_Uo,
                             int64_t lduo, double* d_Vo, int64_t ldvo);
+
+/* ------------------------------------------------------------ §8f HSS (hss.cpp)
+ * Packed, level-major HSS representation of an n x n matrix at depth L
+ * (n divisible by 2^L, leaf = n / 2^L >= r): at level l the 2^(l+1)
+ * off-diagonal blocks (node t: upper block b = 2t, rows [t s, t s + s/2) x
+ * cols [t s + s/2, (t+1) s); lower b = 2t + 1, the transposed position;
+ * s = n / 2^l) have disjoint row ranges tiling [0, n) and disjoint column
+ * ranges, so
+ *   d_F  + l n r : F_l  (n x r, ld n), F_l(row0_b + i, a) = F_b(i, a)
+ *   d_HT + l n r : HT_l (n x r, ld n), HT_l(col0_b + j, a) = H_b(a, j)
+ *   d_D          : n x leaf (ld n), D(i, j) = M(i, leaf0(i) + j)
+ *   rank[g]      : g = 2^(l+1) - 2 + b (level-major), rank_b <= r.
+ * The reference's block order (hss.cpp:151-160, preorder: upper, lower,
+ * left subtree, right subtree) is a permutation of g.
+ *
+ * build_hss(M, L, r, tol, Svd) (hss.cpp:69-96, 143-185): every block's SVD
+ * (one-CTA Jacobi for s/2 <= 64, multi-CTA otherwise), the smallest rank
+ * <= min(r, s/2) whose discarded tail is <= tol ||sigma||, overflow flags
+ * (h_overflow[g]) where rank r misses tol. h_rank/h_overflow are HOST arrays
+ * of 2^(L+1) - 2 entries. Blocks (one host read of the singular values). */
+int slra_hss_build_svd(slra_ctx ctx, const double* d_M, int64_t ldm, int64_t n, int L, int64_t r,
+                       double tol, double* d_D, double* d_F, double* d_HT, int64_t* h_rank,
+                       int32_t* h_overflow);
+/* The dense diagonal leaves only (hss.cpp:145-148), as d_D above. */
+int slra_hss_leaves(slra_ctx ctx, const double* d_M, int64_t ldm, int64_t n, int L, double* d_D);
+/* hss_matvec (hss.cpp:193-212): y = HSS x; d_rank is the DEVICE copy of the
+ * rank array. Two kernels: the 2^(L+1)-2 projections H_b x_b, then one
+ * thread per row adds its leaf product and its L generator terms in the
+ * reference's order (leaf first, then by level). */
+int slra_hss_matvec(slra_ctx ctx, int64_t n, int L, int64_t r, const double* d_D, const double* d_F,
+                    const double* d_HT, const int64_t* d_rank, const double* d_x, double* d_y);
+/* hss_reconstruct (hss.cpp:214-221) into d_out (n x n, ld ldo); with d_M
+ * non-null writes M - reconstruction instead (hss_error's operand). */
+int slra_hss_reconstruct(slra_ctx ctx, int64_t n, int L, int64_t r, const double* d_D, const double* d_F,
+                         const double* d_HT, const int64_t* d_rank, const double* d_M, int64_t ldm,
+                         double* d_out, int64_t ldo);
+/* matrix_norm (linalg.cpp:134-151): kind 0 spectral (largest singular
+ * value), 1 Frobenius, 2 Chebyshev (max |a_ij|). Blocks; *h_out on the host. */
+int slra_matrix_norm(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, int kind,
+                     double* h_out);
 
 /* ------------------------------------------------------------ a11/a12 LSR
  * sketch_solve (lsr.cpp:37-67): FW = F (A|b) through a compiled left-side

@@ -294,6 +294,31 @@ double residual_norm(const LsrProblem& p, const Vector& x);
 double residual_ratio(const LsrProblem& p, const Vector& x_hat);
 LsrReport sketch_solve(const LsrProblem& p, const SketchOperator& F, bool with_true_residual = false);
 
+// ---------------------------------------------------------------- hss
+// hss.hpp:11-52
+struct HssBlock {
+  Index row0 = 0, col0 = 0, rows = 0, cols = 0;
+  Matrix F, H;
+  bool rank_overflow = false;
+};
+struct HssLeaf {
+  Index row0 = 0, col0 = 0;
+  Matrix D;
+};
+struct HssMatrix {
+  Index n = 0;
+  int depth = 0;
+  Index leaf = 0, r = 0;
+  std::vector<HssLeaf> diag;
+  std::vector<HssBlock> off;
+  bool any_overflow = false;
+};
+enum class HssStrategy { Svd, CurCa };
+HssMatrix build_hss(const EntryOracle& M, int L, Index r, double tol, HssStrategy strategy, Rng& rng);
+Vector hss_matvec(const HssMatrix& H, const Vector& x);
+Matrix hss_reconstruct(const HssMatrix& H);
+double hss_error(const HssMatrix& H, const Matrix& M, NormKind norm);
+
 // ---------------------------------------------------------------- testgen
 Matrix random_orthonormal(Index rows, Index cols, Rng& rng);                  // testgen.cpp:41-43
 Matrix gen_svd_profile(Index n, Index r, Rng& rng);                           // :100-108

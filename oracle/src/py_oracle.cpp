@@ -39,6 +39,64 @@ static Vector np_vec(const FArray& a) { return Vector(a.data(), a.data() + a.siz
 struct PyOp { OpPtr p; };
 static IndexSet mkset(const std::vector<Index>& v, Index bound) { return IndexSet(v, bound); }
 
+
+static py::dict hss_dict(const HssMatrix& h) {
+  py::dict d;
+  d["n"] = h.n;
+  d["depth"] = h.depth;
+  d["leaf"] = h.leaf;
+  d["r"] = h.r;
+  d["any_overflow"] = h.any_overflow;
+  py::list diag, off;
+  for (const HssLeaf& l : h.diag) diag.append(py::make_tuple(l.row0, l.col0, to_np(l.D)));
+  for (const HssBlock& b : h.off) {
+    py::dict e;
+    e["row0"] = b.row0;
+    e["col0"] = b.col0;
+    e["rows"] = b.rows;
+    e["cols"] = b.cols;
+    e["F"] = to_np(b.F);
+    e["H"] = to_np(b.H);
+    e["rank_overflow"] = b.rank_overflow;
+    off.append(e);
+  }
+  d["diag"] = diag;
+  d["off"] = off;
+  return d;
+}
+
+static HssMatrix hss_from(const py::dict& d) {
+  HssMatrix h;
+  h.n = d["n"].cast<Index>();
+  h.depth = d["depth"].cast<int>();
+  h.leaf = d["leaf"].cast<Index>();
+  h.r = d["r"].cast<Index>();
+  h.any_overflow = d["any_overflow"].cast<bool>();
+  for (auto t : d["diag"].cast<py::list>()) {
+    auto tp = t.cast<py::tuple>();
+    HssLeaf l;
+    l.row0 = tp[0].cast<Index>();
+    l.col0 = tp[1].cast<Index>();
+    l.D = from_np(tp[2].cast<FArray>());
+    h.diag.push_back(std::move(l));
+  }
+  for (auto e : d["off"].cast<py::list>()) {
+    auto b = e.cast<py::dict>();
+    HssBlock k;
+    k.row0 = b["row0"].cast<Index>();
+    k.col0 = b["col0"].cast<Index>();
+    k.rows = b["rows"].cast<Index>();
+    k.cols = b["cols"].cast<Index>();
+    k.F = from_np(b["F"].cast<FArray>());
+    k.H = from_np(b["H"].cast<FArray>());
+    if (k.F.cols() == 0) k.F = Matrix(k.rows, 0);
+    if (k.H.rows() == 0) k.H = Matrix(0, k.cols);
+    k.rank_overflow = b["rank_overflow"].cast<bool>();
+    h.off.push_back(std::move(k));
+  }
+  return h;
+}
+
 static py::dict cur_dict(const CurDecomposition& c) {
   py::dict d;
   d["I"] = c.row_set.indices();
@@ -223,6 +281,24 @@ PYBIND11_MODULE(_oracle, m) {
     LowRankFactors f{from_np(U), from_np(V), 0};
     LraErrorEstimate e = posterior_error_estimate(o, f, q, s, rng);
     return py::make_tuple(e.estimate_frobenius, e.ci_lo, e.ci_hi, e.has_interval);
+  });
+
+  // ---- hss (hss.hpp:44-52)
+  m.def("build_hss", [](const FArray& M, int L, Index r, double tol, const std::string& strategy, Rng& rng) {
+    Matrix A = from_np(M);
+    DenseOracle o(A);
+    if (strategy != "svd" && strategy != "cur_ca") throw std::invalid_argument("strategy: svd | cur_ca");
+    HssMatrix h = build_hss(o, L, r, tol, strategy == "svd" ? HssStrategy::Svd : HssStrategy::CurCa, rng);
+    py::dict d = hss_dict(h);
+    d["accesses"] = o.accesses();
+    return d;
+  });
+  m.def("hss_matvec", [](const py::dict& h, const FArray& x) { return vec_np(hss_matvec(hss_from(h), np_vec(x))); });
+  m.def("hss_reconstruct", [](const py::dict& h) { return to_np(hss_reconstruct(hss_from(h))); });
+  m.def("hss_error", [](const py::dict& h, const FArray& M, const std::string& norm) {
+    const NormKind k = norm == "spectral" ? NormKind::Spectral : norm == "chebyshev" ? NormKind::Chebyshev
+                                                                                      : NormKind::Frobenius;
+    return hss_error(hss_from(h), from_np(M), k);
   });
 
   // ---- lsr

@@ -15,7 +15,7 @@
 namespace slra_dev {
 
 // ------------------------------------------------------------------ context
-constexpr int kArenaSlots = 10;
+constexpr int kArenaSlots = 12;
 
 struct Context {
   int device = 0;
@@ -37,7 +37,8 @@ struct Context {
   void* hsmall = nullptr;
   // independent growable device arenas for multi-kernel orchestrations
   // (0: range finder, 1: cur residual, 2: lsr, 3: svd, 4: large C-A, 5: factored residual,
-  //  6: wide-svd transpose, 7: tall maxvol/select, 8: pinv, 9: premult / two-stage truncate)
+  //  6: wide-svd transpose, 7: tall maxvol/select, 8: pinv, 9: premult / two-stage truncate,
+  //  10: large (multi-CTA Jacobi) svd, 11: hss)
   void* arena[kArenaSlots] = {};
   size_t arena_bytes[kArenaSlots] = {};
   // opt-in per-kernel-family timing (CUDA events on the context stream)

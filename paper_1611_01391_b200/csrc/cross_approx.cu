@@ -350,7 +350,9 @@ int launch_maxvol_large(Context* cx, const double* Q, int64_t ldq, int64_t m, in
                         int64_t* d_idx, double* d_vol, double* scratch);
 
 static bool ca_fits(int m, int n, int k, int l) {
-  return k >= 1 && l >= 1 && k <= 64 && l <= 64 && k <= m && l <= n &&
+  // the CTA-resident strip QR forms Q in registers for at most 256 rows
+  // (cta_form_q); taller strips take the TSQR + grid-wide maxvol path
+  return k >= 1 && l >= 1 && k <= 64 && l <= 64 && k <= m && l <= n && m <= 256 && n <= 256 &&
          ca_smem_bytes(m, n, k, l) <= 227 * 1024;
 }
 

@@ -425,11 +425,21 @@ int launch_transpose(Context* cx, const double* A, int64_t lda, int64_t m, int64
 
 // General SVD with min(m, n) <= 64: small -> one CTA; tall -> thin_qr then
 // Jacobi on R and S = Q U_R (plus the sign rule on S); wide -> via A^T.
+size_t svd_large_workspace_doubles(int64_t m, int64_t n, int nb);
+int launch_svd_large_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int m, int n, int nb,
+                             double* S, int64_t lds, int64_t sS, double* sigma, int64_t sSig, double* T, int64_t ldt,
+                             int64_t sT, double* ws);
+
 int launch_svd(Context* cx, const double* A, int64_t lda, int64_t m, int64_t n, double* S, int64_t lds,
                double* sigma, double* T, int64_t ldt) {
   const int64_t q = m < n ? m : n;
-  if (q > 64) return SLRA_ERR_UNSUPPORTED;
-  if (svd_smem((int)m, (int)n) <= 200 * 1024 && (m > n ? m : n) <= 256)
+  if (q > 64 && m >= n) {  // multi-CTA Jacobi in HBM (svd_large.cu)
+    if (m > INT32_MAX / 2 || n > 16384) return SLRA_ERR_UNSUPPORTED;
+    double* ws = static_cast<double*>(arena(cx, 10, sizeof(double) * svd_large_workspace_doubles(m, n, 1)));
+    if (!ws) return SLRA_ERR_CUDA;
+    return launch_svd_large_batched(cx, A, lda, 0, (int)m, (int)n, 1, S, lds, 0, sigma, 0, T, ldt, 0, ws);
+  }
+  if (q <= 64 && svd_smem((int)m, (int)n) <= 200 * 1024 && (m > n ? m : n) <= 256)
     return launch_svd_small(cx, A, lda, (int)m, (int)n, S, lds, sigma, T, ldt, 0.0);
   if (m < n) {
     // wide: A^T = S' Sigma T'^T (tall path), so A = T' Sigma S'^T; the sign

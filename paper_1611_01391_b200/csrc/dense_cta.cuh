@@ -505,9 +505,11 @@ __device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h
     if (swap == max_swaps) return SLRA_OK;
     const int j = (int)(best.i / m), piv = (int)(best.i % m);
     const int ts = iperm[j];
+    // the pivot is read by every thread BEFORE the barrier: after it, the
+    // thread owning row piv overwrites W(piv, :)
+    const double p = W[piv + ts * ldw];
     for (int t2 = tid; t2 < r; t2 += NT) g[t2] = W[piv + t2 * ldw] - (t2 == ts ? 1.0 : 0.0);
     __syncthreads();
-    const double p = W[piv + ts * ldw];
     if (tid == 0) I[j] = piv;
     for (int i = tid; i < m; i += NT) {
       const double f = W[i + ts * ldw] / p;

@@ -100,7 +100,6 @@ extern "C" {
 int slra_pinv(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, double rank_tol, double* P,
               int64_t ldp, int64_t* h_rank) {
   if (!ctx || m < 1 || n < 1 || lda < m || ldp < n || !(rank_tol >= 0.0)) return SLRA_ERR_INVALID_ARGUMENT;
-  if ((m < n ? m : n) > 64) return SLRA_ERR_UNSUPPORTED;
   Context* cx = C(ctx);
   double* ws = static_cast<double*>(arena(cx, 8, sizeof(double) * pinv_workspace_doubles(m, n)));
   if (!ws) return SLRA_ERR_CUDA;

@@ -21,6 +21,18 @@ class DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (p_) {
+        slra_ctx_synchronize(device_context());
+        slra_device_free(device_context(), p_);
+      }
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+    }
+    return *this;
+  }
   ~DevBuf() {
     if (p_) {
       slra_ctx_synchronize(device_context());

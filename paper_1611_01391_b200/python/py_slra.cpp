@@ -9,6 +9,7 @@
 #include "slra/devbuf.hpp"
 #include "slra/device.hpp"
 #include "slra/errors.hpp"
+#include "slra/hss.hpp"
 #include "slra/lra.hpp"
 #include "slra/lsr.hpp"
 #include "slra/sketch.hpp"
@@ -48,6 +49,70 @@ struct PyOp {
 template <typename T>
 static T* ptr(uintptr_t p) {
   return reinterpret_cast<T*>(p);
+}
+
+static py::dict hss_dict(const HssMatrix& h) {
+  py::dict d;
+  d["n"] = h.n;
+  d["depth"] = h.depth;
+  d["leaf"] = h.leaf;
+  d["r"] = h.r;
+  d["any_overflow"] = h.any_overflow;
+  py::list diag, off;
+  for (const HssLeaf& l : h.diag) diag.append(py::make_tuple(l.row0, l.col0, to_np(l.D)));
+  for (const HssBlock& b : h.off) {
+    py::dict e;
+    e["row0"] = b.row0;
+    e["col0"] = b.col0;
+    e["rows"] = b.rows;
+    e["cols"] = b.cols;
+    e["F"] = to_np(b.F);
+    e["H"] = to_np(b.H);
+    e["rank_overflow"] = b.rank_overflow;
+    off.append(e);
+  }
+  d["diag"] = diag;
+  d["off"] = off;
+  return d;
+}
+
+static HssMatrix hss_from(const py::dict& d) {
+  HssMatrix h;
+  h.n = d["n"].cast<Index>();
+  h.depth = d["depth"].cast<int>();
+  h.leaf = d["leaf"].cast<Index>();
+  h.r = d["r"].cast<Index>();
+  h.any_overflow = d["any_overflow"].cast<bool>();
+  for (auto t : d["diag"].cast<py::list>()) {
+    auto tp = t.cast<py::tuple>();
+    HssLeaf l;
+    l.row0 = tp[0].cast<Index>();
+    l.col0 = tp[1].cast<Index>();
+    l.D = from_np(tp[2].cast<FArray>());
+    h.diag.push_back(std::move(l));
+  }
+  for (auto e : d["off"].cast<py::list>()) {
+    auto b = e.cast<py::dict>();
+    HssBlock k;
+    k.row0 = b["row0"].cast<Index>();
+    k.col0 = b["col0"].cast<Index>();
+    k.rows = b["rows"].cast<Index>();
+    k.cols = b["cols"].cast<Index>();
+    k.F = from_np(b["F"].cast<FArray>());
+    k.H = from_np(b["H"].cast<FArray>());
+    if (k.F.cols() == 0) k.F = Matrix(k.rows, 0);
+    if (k.H.rows() == 0) k.H = Matrix(0, k.cols);
+    k.rank_overflow = b["rank_overflow"].cast<bool>();
+    h.off.push_back(std::move(k));
+  }
+  return h;
+}
+
+static NormKind norm_kind(const std::string& s) {
+  if (s == "spectral") return NormKind::Spectral;
+  if (s == "frobenius") return NormKind::Frobenius;
+  if (s == "chebyshev") return NormKind::Chebyshev;
+  throw std::invalid_argument("norm: spectral | frobenius | chebyshev");
 }
 
 static py::dict cur_dict(const CurDecomposition& c) {
@@ -139,6 +204,37 @@ PYBIND11_MODULE(_slra, m) {
     return numerical_rank(from_np(A), tol, relative ? RankMode::Relative : RankMode::Absolute);
   }, py::arg("A"), py::arg("tol"), py::arg("relative") = false);
   m.def("frobenius_norm", [](const FArray& A) { return frobenius_norm(from_np(A)); });
+  m.def("spectral_norm", [](const FArray& A) { return spectral_norm(from_np(A)); });
+  m.def("chebyshev_norm", [](const FArray& A) { return chebyshev_norm(from_np(A)); });
+  m.def("matrix_norm", [](const FArray& A, const std::string& k) { return matrix_norm(from_np(A), norm_kind(k)); });
+
+  // ---- hss (hss.hpp:44-52)
+  m.def("build_hss", [](const FArray& M, int L, Index r, double tol, const std::string& strategy, Rng& rng) {
+    if (strategy != "svd" && strategy != "cur_ca") throw std::invalid_argument("strategy: svd | cur_ca");
+    Matrix A = from_np(M);
+    DenseOracle o(A);
+    HssMatrix h = build_hss(o, L, r, tol, strategy == "svd" ? HssStrategy::Svd : HssStrategy::CurCa, rng);
+    py::dict d = hss_dict(h);
+    d["accesses"] = o.accesses();
+    return d;
+  });
+  m.def("hss_matvec", [](const py::dict& h, const FArray& x) { return vec_np(hss_matvec(hss_from(h), np_vec(x))); });
+  m.def("hss_reconstruct", [](const py::dict& h) { return to_np(hss_reconstruct(hss_from(h))); });
+  m.def("hss_error", [](const py::dict& h, const FArray& M, const std::string& norm) {
+    return hss_error(hss_from(h), from_np(M), norm_kind(norm));
+  });
+  m.def("hss_serialize", [](const py::dict& h) { return hss_from(h).serialize(); });
+  m.def("hss_deserialize", [](const std::string& s) { return hss_dict(HssMatrix::deserialize(s)); });
+  // device-resident: build once, multiply a batch of HBM vectors (bench)
+  m.def("hss_matvec_timed", [](const FArray& M, int L, Index r, double tol, const std::string& strategy, Rng& rng,
+                               uintptr_t d_x, uintptr_t d_y, int reps) {
+    Matrix A = from_np(M);
+    DenseOracle o(A);
+    HssDevice h = build_hss_device(o, L, r, tol, strategy == "svd" ? HssStrategy::Svd : HssStrategy::CurCa, rng);
+    for (int t = 0; t < reps; ++t) hss_matvec_device(h, ptr<double>(d_x), ptr<double>(d_y));
+    check(slra_ctx_synchronize(device_context()), "hss_matvec_timed");
+    return reps;
+  });
 
   // ---- cur
   m.def("t_factor", &t_factor);

@@ -62,6 +62,17 @@ Index numerical_rank(const Matrix& A, double tol, RankMode mode) {  // linalg.cp
   return count;
 }
 
+double matrix_norm(const Matrix& A, NormKind kind) {  // linalg.cpp:134-151 on the device
+  if (A.rows() == 0 || A.cols() == 0) return 0.0;
+  DeviceMatrix dA = DeviceMatrix::upload(A);
+  double v = 0.0;
+  const int k = kind == NormKind::Spectral ? 0 : kind == NormKind::Frobenius ? 1 : 2;
+  check(slra_matrix_norm(device_context(), dA.data(), dA.ld(), A.rows(), A.cols(), k, &v), "matrix_norm");
+  return v;
+}
+double spectral_norm(const Matrix& A) { return matrix_norm(A, NormKind::Spectral); }
+double chebyshev_norm(const Matrix& A) { return matrix_norm(A, NormKind::Chebyshev); }
+
 double frobenius_norm(const Matrix& A) {  // linalg.cpp:139, one device pass
   DeviceMatrix dA = DeviceMatrix::upload(A);
   DevBuf<double> out(2);

@@ -530,3 +530,80 @@ def test_solve_exact_vs_lapack(oracle):
     A, b = oracle.gen_lsr_gaussian(200, 12, 0.01, rng)
     x = oracle.solve_exact(A, b)
     assert np.allclose(x, np.linalg.lstsq(A, b, rcond=None)[0], atol=1e-12)
+
+
+# ---------------------------------------------------------------- HSS (test_hss.cpp)
+from hss_inputs import block_diagonal, cauchy_kernel, gen_fd_inverse, gravity_kernel, tridiagonal  # noqa: E402
+
+
+def test_hss_block_diagonal_exact(oracle):  # test_hss.cpp:34-41
+    rng = oracle.Rng(48)
+    M = block_diagonal(rng, 8, 8)
+    h = oracle.build_hss(M, 3, 4, 1e-10, "svd", rng)
+    assert oracle.hss_error(h, M, "spectral") <= 1e-12
+    assert not h["any_overflow"]
+    assert all(b["F"].shape[1] == 0 for b in h["off"])
+
+
+def test_hss_tridiagonal_rank_one_blocks(oracle):  # test_hss.cpp:43-50
+    rng = oracle.Rng(49)
+    M = tridiagonal(64, rng)
+    h = oracle.build_hss(M, 3, 2, 1e-12, "svd", rng)
+    assert oracle.hss_error(h, M, "spectral") <= 1e-10 * np.linalg.norm(M, 2)
+    assert all(b["F"].shape[1] <= 1 for b in h["off"])
+
+
+def test_hss_cauchy_superfast(oracle):  # test_hss.cpp:52-58
+    M = cauchy_kernel(512)
+    h = oracle.build_hss(M, 4, 16, 1e-7, "cur_ca", oracle.Rng(50))
+    assert oracle.hss_error(h, M, "spectral") <= 1e-5 * np.linalg.norm(M, 2)
+    assert all(b["F"].shape[1] <= 16 for b in h["off"])
+
+
+def test_hss_matvec(oracle):  # test_hss.cpp:60-86 (flop budget: op_counter not restated)
+    rng = oracle.Rng(51)
+    M = gen_fd_inverse(64, 64)
+    h = oracle.build_hss(M, 3, 6, 1e-9, "svd", rng)
+    assert np.linalg.norm(oracle.hss_matvec(h, np.zeros(64))) == 0.0
+    R = oracle.hss_reconstruct(h)
+    scale = np.linalg.norm(R, 2)
+    for _ in range(20):
+        x = rng.gaussian_vector(64)
+        assert np.linalg.norm(oracle.hss_matvec(h, x) - R @ x) <= 1e-10 * scale * np.linalg.norm(x)
+    B = block_diagonal(rng, 4, 8)
+    hb = oracle.build_hss(B, 2, 2, 1e-10, "svd", rng)
+    x = rng.gaussian_vector(32)
+    assert np.linalg.norm(oracle.hss_matvec(hb, x) - B @ x) <= 1e-10 * np.linalg.norm(B, 2) * np.linalg.norm(x)
+
+
+def test_hss_norm_sanity(oracle):  # test_hss.cpp:88-95
+    M = gravity_kernel(64, 64)
+    h = oracle.build_hss(M, 2, 4, 1e-4, "svd", oracle.Rng(52))
+    assert oracle.hss_error(h, M, "chebyshev") <= oracle.hss_error(h, M, "spectral") * 64 * (1 + 1e-12)
+
+
+def test_hss_strategy_comparison(oracle):  # test_hss.cpp:97-110 (20 of the 100 seeds)
+    M = gravity_kernel(128, 128)
+    es = oracle.hss_error(oracle.build_hss(M, 3, 8, 1e-5, "svd", oracle.Rng(0)), M, "frobenius")
+    ok = sum(oracle.hss_error(oracle.build_hss(M, 3, 8, 1e-5, "cur_ca", oracle.Rng(3200 + t)), M, "frobenius")
+             <= 10 * es for t in range(20))
+    assert ok >= 18
+
+
+def test_hss_superfast_reads_vanishing_fraction(oracle):  # test_hss.cpp:112-124
+    prev = float("inf")
+    for n in (128, 256, 512):
+        h = oracle.build_hss(cauchy_kernel(n), 3, 8, 1e-6, "cur_ca", oracle.Rng(53))
+        ratio = h["accesses"] / (n * n)
+        assert ratio < prev
+        prev = ratio
+
+
+def test_hss_validation(oracle):  # test_hss.cpp:126-137
+    rng = oracle.Rng(54)
+    M = rng.gaussian_matrix(64, 64)
+    h = oracle.build_hss(M, 3, 4, 1e-3, "svd", rng)
+    assert sum(D.size for _, _, D in h["diag"]) <= 2 * (64 + 64) * h["leaf"]
+    for args in ((rng.gaussian_matrix(60, 60), 3, 4), (rng.gaussian_matrix(64, 32), 3, 4), (M, 5, 4)):
+        with pytest.raises(ValueError):
+            oracle.build_hss(args[0], args[1], args[2], 1e-3, "svd", rng)
