@@ -288,11 +288,15 @@ struct LsrReport {
   double sketched_residual = 0;
   std::optional<double> true_residual, ratio;
   Index k = 0;
+  bool validated = true;
+  int attempts = 1;
 };
 Vector solve_exact(const LsrProblem& p);
 double residual_norm(const LsrProblem& p, const Vector& x);
 double residual_ratio(const LsrProblem& p, const Vector& x_hat);
 LsrReport sketch_solve(const LsrProblem& p, const SketchOperator& F, bool with_true_residual = false);
+LsrReport solve_with_retries(const LsrProblem& p, OpPtr base_F, const std::vector<OpPtr>& q_family,
+                             int max_retries, double accept_tol, Rng& rng);  // lsr.cpp:69-113
 
 // ---------------------------------------------------------------- hss
 // hss.hpp:11-52

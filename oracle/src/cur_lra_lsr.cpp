@@ -372,6 +372,58 @@ LsrReport sketch_solve(const LsrProblem& p, const SketchOperator& F, bool with_t
   return rep;
 }
 
+// lsr.cpp:69-113: sketch-and-solve with re-randomised retries, each solution
+// validated against an independently drawn sketch of the same shape.
+LsrReport solve_with_retries(const LsrProblem& p, OpPtr base_F, const std::vector<OpPtr>& q_family,
+                             int max_retries, double accept_tol, Rng& rng) {
+  validate(p);
+  const Index m = p.A.rows();
+  LsrReport best;
+  double best_score = std::numeric_limits<double>::infinity();
+  bool have_best = false;
+  for (int attempt = 0; attempt <= max_retries; ++attempt) {
+    OpPtr F = base_F;
+    if (attempt > 0) {
+      OpPtr Q = q_family.empty() ? gen_permutation(m, rng)
+                                 : q_family[static_cast<size_t>((attempt - 1) % static_cast<int>(q_family.size()))];
+      F = make_product({base_F, Q});
+    }
+    LsrReport rep;
+    try {
+      rep = sketch_solve(p, *F);
+    } catch (const SketchRankFailure&) {
+      continue;
+    }
+    rep.attempts = attempt + 1;
+    OpPtr Fv = make_product({base_F, gen_permutation(m, rng)});
+    const Matrix VA = Fv->apply(p.A);
+    Matrix bm(m, 1);
+    for (Index i = 0; i < m; ++i) bm(i, 0) = p.b[static_cast<size_t>(i)];
+    const Matrix vb = Fv->apply(bm);
+    double rv = 0, vn = 0;
+    for (Index i = 0; i < VA.rows(); ++i) {
+      double s = 0;
+      for (Index j = 0; j < VA.cols(); ++j) s += VA(i, j) * rep.x_hat[static_cast<size_t>(j)];
+      const double e = s - vb(i, 0);
+      rv += e * e;
+      vn += vb(i, 0) * vb(i, 0);
+    }
+    const double r_val = std::sqrt(rv);
+    const double score = r_val / std::max(rep.sketched_residual, 1e-300);
+    const bool ok = r_val <= 1e-12 * std::sqrt(vn) || score <= accept_tol;
+    rep.validated = ok;
+    if (ok) return rep;
+    if (score < best_score) {
+      best_score = score;
+      best = rep;
+      have_best = true;
+    }
+  }
+  if (!have_best) throw SketchRankFailure("solve_with_retries: all attempts rank deficient");
+  best.validated = false;
+  return best;
+}
+
 // ---------------------------------------------------------------- testgen.cpp
 Matrix random_orthonormal(Index rows, Index cols, Rng& rng) {  // testgen.cpp:41-43
   return thin_qr(rng.gaussian_matrix(rows, cols)).first;

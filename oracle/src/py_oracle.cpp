@@ -313,6 +313,20 @@ PYBIND11_MODULE(_oracle, m) {
     d["k"] = r.k;
     return d;
   }, py::arg("A"), py::arg("b"), py::arg("F"), py::arg("with_true_residual") = false);
+  m.def("solve_with_retries", [](const FArray& A, const FArray& b, const PyOp& F, const std::vector<PyOp>& qf,
+                                 int max_retries, double accept_tol, Rng& rng) {
+    LsrProblem p{from_np(A), np_vec(b)};
+    std::vector<OpPtr> q;
+    for (auto& o : qf) q.push_back(o.p);
+    LsrReport r = solve_with_retries(p, F.p, q, max_retries, accept_tol, rng);
+    py::dict d;
+    d["x_hat"] = vec_np(r.x_hat);
+    d["sketched_residual"] = r.sketched_residual;
+    d["k"] = r.k;
+    d["validated"] = r.validated;
+    d["attempts"] = r.attempts;
+    return d;
+  });
   m.def("solve_exact", [](const FArray& A, const FArray& b) {
     return vec_np(solve_exact(LsrProblem{from_np(A), np_vec(b)}));
   });

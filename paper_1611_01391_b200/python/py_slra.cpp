@@ -355,6 +355,19 @@ PYBIND11_MODULE(_slra, m) {
     LowRankFactors g = two_stage_truncate(f, r);
     return py::make_tuple(to_np(g.U), to_np(g.V));
   });
+  m.def("solve_with_retries", [](const FArray& A, const FArray& b, const PyOp& F, const std::vector<PyOp>& qf,
+                                 int max_retries, double accept_tol, Rng& rng) {
+    std::vector<OpPtr> q;
+    for (auto& o : qf) q.push_back(o.p);
+    LsrReport r = solve_with_retries(LsrProblem{from_np(A), np_vec(b)}, F.p, q, max_retries, accept_tol, rng);
+    py::dict d;
+    d["x_hat"] = vec_np(r.x_hat);
+    d["sketched_residual"] = r.sketched_residual;
+    d["k"] = r.k;
+    d["validated"] = r.validated;
+    d["attempts"] = r.attempts;
+    return d;
+  });
   m.def("sketch_solve", [](const FArray& A, const FArray& b, const PyOp& F, bool with_true) {
     LsrReport rep = sketch_solve(LsrProblem{from_np(A), np_vec(b)}, *F.p, with_true);
     py::dict d;

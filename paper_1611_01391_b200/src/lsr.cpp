@@ -13,7 +13,87 @@ void validate(const LsrProblem& p) {  // lsr.cpp:13-17
   if (p.A.rows() <= p.A.cols() || p.A.cols() < 1) throw std::invalid_argument("lsr: need m > d >= 1");
   if (static_cast<Index>(p.b.size()) != p.A.rows()) throw std::invalid_argument("lsr: b length mismatch");
 }
+
+// sketch_solve on an HBM-resident (A, b): one plan, one C-ABI call.
+LsrReport sketch_solve_resident(const DeviceMatrix& dA, const double* db, const SketchOperator& F) {
+  const Index d = dA.cols(), m = dA.rows();
+  if (F.cols() != m) throw std::invalid_argument("sketch_solve: F cols != m");
+  if (F.rows() <= d) throw std::invalid_argument("sketch_solve: need k > d");
+  const SketchPlan plan = compile_plan(F, Side::Left);
+  DevBuf<double> dx(static_cast<size_t>(d));
+  DevBuf<int64_t> src(plan.src);
+  DevBuf<double> coef(plan.coef);
+  DevBuf<int32_t> q(plan.q);
+  LsrReport rep;
+  check(slra_sketch_solve(device_context(), dA.data(), dA.ld(), m, d, db, src.get(), coef.get(), q.get(), plan.width,
+                          plan.tree, plan.count, dx.get(), &rep.sketched_residual),
+        "sketch_solve");
+  rep.x_hat = dx.download();
+  rep.k = F.rows();
+  return rep;
+}
 }  // namespace
+
+// lsr.cpp:69-113: retries re-randomise the sketch as F Q (Q a fresh random
+// permutation, or the caller's family in turn); every solution is validated
+// against an independently drawn F P: ||(F P A) x_hat - F P b|| versus the
+// sketched residual. (A, b) stay in HBM across attempts; each validation is
+// a plan gather of the k sketched rows plus one device residual pass.
+LsrReport solve_with_retries(const LsrProblem& p, OpPtr base_F, const std::vector<OpPtr>& q_family,
+                             int max_retries, double accept_tol, Rng& rng) {
+  validate(p);
+  const Index m = p.A.rows(), d = p.A.cols();
+  slra_ctx cx = device_context();
+  DeviceMatrix dA = DeviceMatrix::upload(p.A);
+  DevBuf<double> db(p.b);
+  LsrReport best;
+  double best_score = std::numeric_limits<double>::infinity();
+  bool have_best = false;
+  for (int attempt = 0; attempt <= max_retries; ++attempt) {
+    OpPtr F = base_F;
+    if (attempt > 0) {
+      OpPtr Q = q_family.empty() ? gen_permutation(m, rng)
+                                 : q_family[static_cast<size_t>((attempt - 1) % static_cast<int>(q_family.size()))];
+      F = make_product({base_F, Q});
+    }
+    LsrReport rep;
+    try {
+      rep = sketch_solve_resident(dA, db.get(), *F);
+    } catch (const SketchRankFailure&) {
+      continue;
+    }
+    rep.attempts = attempt + 1;
+    OpPtr Fv = make_product({base_F, gen_permutation(m, rng)});
+    const SketchPlan pv = compile_plan(*Fv, Side::Left);
+    const Index k = pv.count;
+    DevBuf<int64_t> src(pv.src);
+    DevBuf<double> coef(pv.coef);
+    DevBuf<int32_t> q(pv.q);
+    DevBuf<double> VA(static_cast<size_t>(k * d)), vb(static_cast<size_t>(k)), x(rep.x_hat), out(2), zero(
+        std::vector<double>(static_cast<size_t>(d), 0.0));
+    check(slra_sketch_rows(cx, dA.data(), dA.ld(), m, d, src.get(), coef.get(), q.get(), pv.width, pv.tree, k,
+                           VA.get(), k),
+          "solve_with_retries");
+    check(slra_sketch_rows(cx, db.get(), m, m, 1, src.get(), coef.get(), q.get(), pv.width, pv.tree, k, vb.get(), k),
+          "solve_with_retries");
+    check(slra_lsr_residual(cx, VA.get(), k, k, d, vb.get(), x.get(), out.get()), "solve_with_retries");
+    const double r_val = std::sqrt(out.download()[0]);
+    check(slra_lsr_residual(cx, VA.get(), k, k, d, vb.get(), zero.get(), out.get()), "solve_with_retries");
+    const double vb_norm = std::sqrt(out.download()[0]);
+    const double score = r_val / std::max(rep.sketched_residual, 1e-300);
+    const bool ok = r_val <= 1e-12 * vb_norm || score <= accept_tol;
+    rep.validated = ok;
+    if (ok) return rep;
+    if (score < best_score) {
+      best_score = score;
+      best = rep;
+      have_best = true;
+    }
+  }
+  if (!have_best) throw SketchRankFailure("solve_with_retries: all attempts rank deficient");
+  best.validated = false;
+  return best;
+}
 
 double residual_norm(const LsrProblem& p, const Vector& x) {  // lsr.cpp:26-28
   validate(p);
@@ -27,21 +107,11 @@ double residual_norm(const LsrProblem& p, const Vector& x) {  // lsr.cpp:26-28
 
 LsrReport sketch_solve(const LsrProblem& p, const SketchOperator& F, bool with_true_residual) {  // lsr.cpp:37-67
   validate(p);
-  const Index d = p.A.cols(), m = p.A.rows();
-  if (F.cols() != m) throw std::invalid_argument("sketch_solve: F cols != m");
-  if (F.rows() <= d) throw std::invalid_argument("sketch_solve: need k > d");
-  const SketchPlan plan = compile_plan(F, Side::Left);
+  if (F.cols() != p.A.rows()) throw std::invalid_argument("sketch_solve: F cols != m");
+  if (F.rows() <= p.A.cols()) throw std::invalid_argument("sketch_solve: need k > d");
   DeviceMatrix dA = DeviceMatrix::upload(p.A);
-  DevBuf<double> db(p.b), dx(static_cast<size_t>(d));
-  DevBuf<int64_t> src(plan.src);
-  DevBuf<double> coef(plan.coef);
-  DevBuf<int32_t> q(plan.q);
-  LsrReport rep;
-  check(slra_sketch_solve(device_context(), dA.data(), dA.ld(), m, d, db.get(), src.get(), coef.get(), q.get(),
-                          plan.width, plan.tree, plan.count, dx.get(), &rep.sketched_residual),
-        "sketch_solve");
-  rep.x_hat = dx.download();
-  rep.k = F.rows();
+  DevBuf<double> db(p.b);
+  LsrReport rep = sketch_solve_resident(dA, db.get(), F);
   if (with_true_residual) {
     rep.true_residual = residual_norm(p, rep.x_hat);
     rep.ratio = residual_ratio(p, rep.x_hat);

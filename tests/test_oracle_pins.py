@@ -607,3 +607,51 @@ def test_hss_validation(oracle):  # test_hss.cpp:126-137
     for args in ((rng.gaussian_matrix(60, 60), 3, 4), (rng.gaussian_matrix(64, 32), 3, 4), (M, 5, 4)):
         with pytest.raises(ValueError):
             oracle.build_hss(args[0], args[1], args[2], 1e-3, "svd", rng)
+
+
+# ---------------------------------------------------------------- solve_with_retries (test_lsr.cpp:176-226)
+def coherent_problem(m, d, seed):
+    """A coherent LSR input built here (signal on the first d rows, weak
+    elsewhere): a stand-in for gen_lsr_family(Coherent), which is not restated."""
+    rng = np.random.default_rng(seed)
+    A = 1e-3 * rng.standard_normal((m, d))
+    A[:d, :] += np.eye(d) * 10.0
+    b = A @ rng.standard_normal(d) + 1e-2 * rng.standard_normal(m)
+    return np.asfortranarray(A), b
+
+
+def test_retries_blind_sub_identity(oracle):  # test_lsr.cpp:176-195
+    m = 32
+    A = np.zeros((m, 1))
+    A[20, 0] = 1.0
+    b = 3.0 * A[:, 0]
+    base = oracle.make_sub_identity(list(range(8)), m)
+    rep = oracle.solve_with_retries(A, b, base, [], 40, 1.5, oracle.Rng(17))
+    assert rep["attempts"] > 1 and rep["validated"]
+    assert rep["x_hat"][0] == pytest.approx(3.0, rel=1e-12)
+    with pytest.raises(oracle.SketchRankFailure):
+        oracle.solve_with_retries(A, b, base, [], 0, 1.5, oracle.Rng(18))
+
+
+def test_retries_validate_first_attempt(oracle):  # test_lsr.cpp:197-208
+    first = 0
+    for t in range(50):
+        rng = oracle.Rng(600 + t)
+        A, b = oracle.gen_lsr_gaussian(128, 6, 0.01, rng)
+        base = oracle.gen_gaussian(36, 128, rng)
+        rep = oracle.solve_with_retries(A, b, base, [], 3, 2.0, rng)
+        assert rep["validated"]
+        first += rep["attempts"] == 1
+    assert first >= 47
+
+
+def test_retries_coherent_family(oracle):  # test_lsr.cpp:210-226 (own coherent input)
+    m, d = 64, 4
+    A, b = coherent_problem(m, d, 19)
+    base = oracle.make_sub_identity(list(range(d, d + 48)), m)
+    rng = oracle.Rng(19)
+    qf = [oracle.gen_permutation(m, rng) for _ in range(6)]
+    rep = oracle.solve_with_retries(A, b, base, qf, 30, 2.0, rng)
+    assert rep["attempts"] > 1
+    x = np.linalg.lstsq(A, b, rcond=None)[0]
+    assert np.linalg.norm(A @ rep["x_hat"] - b) / np.linalg.norm(A @ x - b) < 3.0
