@@ -290,6 +290,20 @@ int slra_hss_reconstruct(slra_ctx ctx, int64_t n, int L, int64_t r, const double
 int slra_matrix_norm(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, int kind,
                      double* h_out);
 
+/* ------------------------------------------------------------ §8f leverage-score CUR
+ * (leverage.cpp:12-149) elementwise passes; the SVDs are slra_svd, the
+ * gathers slra_gather_*, the sampling itself draws from the host Rng.
+ * out[i] = sum_j A(i,j)^2 / divisor (svd_leverage_scores: divisor = r). */
+int slra_row_sqnorms(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, double divisor,
+                     double* d_out);
+/* B = diag(dr) A diag(dc), evaluated (dr_i A_ij) dc_j; null dr/dc = identity.
+ * B may alias A when ldb == lda. */
+int slra_scale_rows_cols(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
+                         const double* d_dr, const double* d_dc, double* d_B, int64_t ldb);
+/* B = A^T (n x m, ld ldb), 32 x 32 shared-memory tiles. */
+int slra_transpose(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, double* d_B,
+                   int64_t ldb);
+
 /* ------------------------------------------------------------ a11/a12 LSR
  * sketch_solve (lsr.cpp:37-67): FW = F (A|b) through a compiled left-side
  * plan (k rows), column-pivoted Householder QR of FA (threshold 1e-10;

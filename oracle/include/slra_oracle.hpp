@@ -298,6 +298,33 @@ LsrReport sketch_solve(const LsrProblem& p, const SketchOperator& F, bool with_t
 LsrReport solve_with_retries(const LsrProblem& p, OpPtr base_F, const std::vector<OpPtr>& q_family,
                              int max_retries, double accept_tol, Rng& rng);  // lsr.cpp:69-113
 
+// ---------------------------------------------------------------- leverage
+// leverage.hpp:11-70, cur.hpp (lra_to_top_svd)
+struct LeverageScores {
+  Vector p;
+  double beta = 1.0;
+  Index r = 0;
+};
+struct SampleRescale {
+  std::vector<Index> indices;
+  Vector d;
+};
+enum class SampleMode { Exactly, Expected };
+LeverageScores svd_leverage_scores(const Matrix& T_r, double beta = 1.0);
+SampleRescale sample_exactly(const LeverageScores& scores, Index l, Rng& rng);
+SampleRescale sample_expected(const LeverageScores& scores, Index l, Rng& rng);
+SampleRescale collapse_duplicates(const SampleRescale& s);
+CurDecomposition cur_via_leverage(const EntryOracle& M, Index r, Index k, Index l, double beta, double beta_bar,
+                                  SampleMode mode, const std::optional<LeverageScores>& scores, Rng& rng,
+                                  bool plain_nucleus = false);
+Svd lra_to_top_svd(const LowRankFactors& f, Index r);
+CurDecomposition refine_lra(const EntryOracle& M, const LowRankFactors& crude, Index r, Index k, Index l, Rng& rng);
+LeverageScores uniform_scores(Index n);
+double gaussian_score_gap(const Matrix& G);
+double sample_bound_quadratic(Index r, double eps, double beta);
+double sample_bound_loglinear(Index r, double eps, double beta, double cbar);
+double epsilon_for_sample(Index r, Index l, double delta);
+
 // ---------------------------------------------------------------- hss
 // hss.hpp:11-52
 struct HssBlock {

@@ -283,6 +283,61 @@ PYBIND11_MODULE(_oracle, m) {
     return py::make_tuple(e.estimate_frobenius, e.ci_lo, e.ci_hi, e.has_interval);
   });
 
+  // ---- leverage (leverage.hpp)
+  auto scores_from = [](const FArray& p, double beta, Index r) {
+    LeverageScores s;
+    s.p = np_vec(p);
+    s.beta = beta;
+    s.r = r;
+    return s;
+  };
+  auto sr_dict = [](const SampleRescale& s) {
+    py::dict d;
+    d["indices"] = s.indices;
+    d["d"] = vec_np(s.d);
+    return d;
+  };
+  m.def("svd_leverage_scores", [](const FArray& T, double beta) {
+    LeverageScores s = svd_leverage_scores(from_np(T), beta);
+    return py::make_tuple(vec_np(s.p), s.beta, s.r);
+  }, py::arg("T"), py::arg("beta") = 1.0);
+  m.def("sample_exactly", [=](const FArray& p, Index l, Rng& rng) { return sr_dict(sample_exactly(scores_from(p, 1.0, 1), l, rng)); });
+  m.def("sample_expected", [=](const FArray& p, Index l, Rng& rng) { return sr_dict(sample_expected(scores_from(p, 1.0, 1), l, rng)); });
+  m.def("collapse_duplicates", [=](const std::vector<Index>& idx, const FArray& d) {
+    SampleRescale s;
+    s.indices = idx;
+    s.d = np_vec(d);
+    return sr_dict(collapse_duplicates(s));
+  });
+  m.def("cur_via_leverage", [=](const FArray& M, Index r, Index k, Index l, double beta, double beta_bar,
+                                const std::string& mode, std::optional<FArray> scores, Rng& rng, bool plain) {
+    Matrix A = from_np(M);
+    DenseOracle o(A);
+    std::optional<LeverageScores> sc;
+    if (scores) sc = scores_from(*scores, beta, r);
+    CurDecomposition c = cur_via_leverage(o, r, k, l, beta, beta_bar,
+                                          mode == "exactly" ? SampleMode::Exactly : SampleMode::Expected, sc, rng, plain);
+    return cur_dict(c);
+  }, py::arg("M"), py::arg("r"), py::arg("k"), py::arg("l"), py::arg("beta"), py::arg("beta_bar"), py::arg("mode"),
+     py::arg("scores"), py::arg("rng"), py::arg("plain_nucleus") = false);
+  m.def("lra_to_top_svd", [](const FArray& U, const FArray& V, Index r) {
+    LowRankFactors f{from_np(U), from_np(V), 0};
+    Svd t = lra_to_top_svd(f, r);
+    return py::make_tuple(to_np(t.S), vec_np(t.sigma), to_np(t.T));
+  });
+  m.def("refine_lra", [](const FArray& M, const FArray& U, const FArray& V, Index target, Index r, Index k, Index l,
+                         Rng& rng) {
+    Matrix A = from_np(M);
+    DenseOracle o(A);
+    LowRankFactors f{from_np(U), from_np(V), target};
+    return cur_dict(refine_lra(o, f, r, k, l, rng));
+  });
+  m.def("uniform_scores", [](Index n) { return vec_np(uniform_scores(n).p); });
+  m.def("gaussian_score_gap", [](const FArray& G) { return gaussian_score_gap(from_np(G)); });
+  m.def("sample_bound_quadratic", &sample_bound_quadratic);
+  m.def("sample_bound_loglinear", &sample_bound_loglinear);
+  m.def("epsilon_for_sample", &epsilon_for_sample);
+
   // ---- hss (hss.hpp:44-52)
   m.def("build_hss", [](const FArray& M, int L, Index r, double tol, const std::string& strategy, Rng& rng) {
     Matrix A = from_np(M);

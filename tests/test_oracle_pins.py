@@ -655,3 +655,105 @@ def test_retries_coherent_family(oracle):  # test_lsr.cpp:210-226 (own coherent 
     assert rep["attempts"] > 1
     x = np.linalg.lstsq(A, b, rcond=None)[0]
     assert np.linalg.norm(A @ rep["x_hat"] - b) / np.linalg.norm(A @ x - b) < 3.0
+
+
+# ---------------------------------------------------------------- leverage (test_leverage.cpp)
+def sampled_matrix(W, s):
+    return W[:, s["indices"]] * s["d"]
+
+
+def test_leverage_scores_known(oracle):  # test_leverage.cpp:23-43
+    T = np.zeros((8, 3))
+    T[0, 0] = T[1, 1] = T[2, 2] = 1.0
+    p, _, _ = oracle.svd_leverage_scores(T)
+    assert np.allclose(p[:3], 1 / 3, rtol=1e-14) and np.all(p[3:] == 0)
+    rng = oracle.Rng(41)
+    Q, _ = oracle.thin_qr(rng.gaussian_matrix(20, 4))
+    q, _, _ = oracle.svd_leverage_scores(Q)
+    assert q.sum() == pytest.approx(1.0, rel=1e-12) and q.min() >= 0
+    O, _ = oracle.thin_qr(rng.gaussian_matrix(4, 4))
+    q2, _, _ = oracle.svd_leverage_scores(Q @ O)
+    assert np.abs(q - q2).max() <= 1e-12
+    with pytest.raises(ValueError):
+        oracle.svd_leverage_scores(rng.gaussian_matrix(20, 4))
+
+
+def test_sample_exactly_known(oracle):  # test_leverage.cpp:45-85 (1000 -> 200 seeds in the mean check)
+    rng = oracle.Rng(42)
+    s = oracle.sample_exactly(np.array([1.0, 0, 0]), 3, rng)
+    assert s["indices"] == [0, 0, 0] and np.allclose(s["d"], 1 / np.sqrt(3), rtol=1e-14)
+    n, draws = 16, 10000
+    s = oracle.sample_exactly(oracle.uniform_scores(n), draws, rng)
+    cnt = np.bincount(s["indices"], minlength=n)
+    assert np.all(np.abs(cnt - draws / n) <= 4 * np.sqrt(draws * (1 / n) * (1 - 1 / n)))
+    assert np.allclose(s["d"][:20], np.sqrt(n / draws), rtol=1e-14)
+    W = oracle.Rng(43).gaussian_matrix(16, 16)
+    p, _, _ = oracle.svd_leverage_scores(oracle.thin_qr(W.T.copy())[0])
+    tot = sum(np.linalg.norm(sampled_matrix(W, oracle.sample_exactly(p, 16, oracle.Rng(2000 + t)))) ** 2
+              for t in range(200))
+    assert tot / 200 == pytest.approx(np.linalg.norm(W) ** 2, rel=0.1)
+
+
+def test_sample_expected_known(oracle):  # test_leverage.cpp:87-152
+    s = oracle.sample_expected(oracle.uniform_scores(8), 8, oracle.Rng(44))
+    assert len(s["indices"]) == 8 and np.all(s["d"] == 1.0)
+    threw = False
+    for t in range(200):
+        try:
+            oracle.sample_expected(np.full(1000, 1e-3), 1, oracle.Rng(2300 + t))
+        except oracle.EmptySample:
+            threw = True
+            break
+    assert threw
+
+
+def test_collapse_duplicates_gram(oracle):  # test_leverage.cpp:154-163
+    rng = oracle.Rng(45)
+    W = rng.gaussian_matrix(12, 10)
+    _, _, T = oracle.svd(W)
+    p, _, _ = oracle.svd_leverage_scores(T[:, :4].copy())
+    raw = oracle.sample_exactly(p, 30, rng)
+    merged = oracle.collapse_duplicates(raw["indices"], raw["d"])
+    assert len(merged["indices"]) < len(raw["indices"])
+    A, B = sampled_matrix(W, raw), sampled_matrix(W, merged)
+    assert np.linalg.norm(A @ A.T - B @ B.T, 2) <= 1e-10
+
+
+def test_cur_via_leverage_exact(oracle):  # test_leverage.cpp:165-183 (40 of 100 seeds)
+    ok = done = 0
+    for t in range(40):
+        rng = oracle.Rng(2400 + t)
+        M = oracle.gen_factor_gaussian(64, 64, 3, 0.0, rng)
+        try:
+            c = oracle.cur_via_leverage(M, 3, 12, 12, 1.0, 1.0, "exactly", None, rng)
+        except (oracle.GeneratorRankFailure, oracle.EmptySample):
+            continue
+        done += 1
+        C = M[:, c["J"]] @ c["nucleus"] @ M[c["I"], :]
+        ok += np.linalg.norm(M - C, 2) <= 1e-8 * np.linalg.norm(M, 2)
+    assert ok >= 38 and ok <= done
+
+
+def test_refine_lra_truthful(oracle):  # test_leverage.cpp:225-245 (40 of 100 seeds)
+    ok = 0
+    for t in range(40):
+        rng = oracle.Rng(2800 + t)
+        M = oracle.gen_factor_gaussian(64, 64, 4, 1e-6, rng)
+        S, s, Tt = np.linalg.svd(M)
+        U, V = S[:, :4] * s[:4], Tt[:4].copy()
+        crude_err = np.linalg.norm(M - U @ V)
+        try:
+            c = oracle.refine_lra(M, U, V, 4, 4, 24, 24, rng)
+        except (oracle.GeneratorRankFailure, oracle.EmptySample):
+            continue
+        ok += np.linalg.norm(M - M[:, c["J"]] @ c["nucleus"] @ M[c["I"], :]) <= 1.5 * crude_err
+    assert ok >= 36
+
+
+def test_score_gap_and_bounds(oracle):  # test_leverage.cpp:292-320
+    assert np.all(oracle.uniform_scores(4) == 0.25)
+    Q, _ = oracle.thin_qr(oracle.Rng(47).gaussian_matrix(64, 4))
+    assert oracle.gaussian_score_gap(np.sqrt(64.0) * Q.T) <= 1e-12
+    assert oracle.sample_bound_quadratic(2, 1.0, 1.0) == pytest.approx(12800.0)
+    assert oracle.sample_bound_loglinear(8, 1.0, 1.0, 100.0) == pytest.approx(100.0 * 8 * np.log(8.0))
+    assert oracle.epsilon_for_sample(2, 16, 0.1) == pytest.approx(np.sqrt(8.0 * np.log(40.0) / 16.0))
