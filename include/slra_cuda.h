@@ -300,6 +300,12 @@ int slra_row_sqnorms(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, in
  * B may alias A when ldb == lda. */
 int slra_scale_rows_cols(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n,
                          const double* d_dr, const double* d_dc, double* d_B, int64_t ldb);
+/* InverseBidiagonalOp (sketch.cpp:286-331) on the c columns of X (n rows):
+ * forward y_0 = x_0, y_i = x_i + b[i-1] y_{i-1}; backward y_{n-1} = x_{n-1},
+ * y_i = x_i + b[i] y_{i+1}. Sequential per column in the reference's order
+ * (bit-exact for b = +-1); Y may alias X. */
+int slra_bidiag_scan(slra_ctx ctx, const double* d_X, int64_t ldx, int64_t n, int64_t c,
+                     const double* d_b, int forward, double* d_Y, int64_t ldy);
 /* B = A^T (n x m, ld ldb), 32 x 32 shared-memory tiles. */
 int slra_transpose(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, double* d_B,
                    int64_t ldb);

@@ -222,6 +222,10 @@ OpPtr make_sign_diagonal(Vector d);
 OpPtr make_abridged_hadamard(Index n, int d);
 OpPtr make_sparse_circulant(Index n, double f, std::vector<std::pair<Index, double>> nz);
 OpPtr make_gaussian(Matrix G);
+OpPtr make_inverse_bidiagonal(Vector subdiag, bool lower = true);                      // sketch.cpp:286-331
+OpPtr make_householder_chain(std::vector<Vector> w, std::vector<std::vector<Index>> perms);  // :335-383
+OpPtr gen_inverse_bidiagonal(Index n, Rng& rng);
+OpPtr gen_householder_chain(Index n, Index q, Rng& rng);
 OpPtr make_sub_identity(IndexSet selected, Index total);
 OpPtr make_product(std::vector<OpPtr> ops);
 OpPtr take_columns(OpPtr op, IndexSet columns);

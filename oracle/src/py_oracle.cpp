@@ -228,6 +228,10 @@ PYBIND11_MODULE(_oracle, m) {
   m.def("make_sparse_circulant", [](Index n, double f, std::vector<std::pair<Index, double>> nz) {
     return PyOp{make_sparse_circulant(n, f, std::move(nz))};
   });
+  m.def("make_inverse_bidiagonal", [](const FArray& b, bool lower) { return PyOp{make_inverse_bidiagonal(np_vec(b), lower)}; },
+        py::arg("subdiag"), py::arg("lower") = true);
+  m.def("gen_inverse_bidiagonal", [](Index n, Rng& r) { return PyOp{gen_inverse_bidiagonal(n, r)}; });
+  m.def("gen_householder_chain", [](Index n, Index q, Rng& r) { return PyOp{gen_householder_chain(n, q, r)}; });
   m.def("make_gaussian", [](const FArray& G) { return PyOp{make_gaussian(from_np(G))}; });
   m.def("make_sub_identity", [](const std::vector<Index>& sel, Index total) {
     return PyOp{make_sub_identity(mkset(sel, total), total)};

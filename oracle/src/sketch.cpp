@@ -288,6 +288,116 @@ OpPtr make_abridged_hadamard(Index n, int d) { return std::make_shared<AbridgedH
 OpPtr make_sparse_circulant(Index n, double f, std::vector<std::pair<Index, double>> nz) {
   return std::make_shared<SparseCirculantOp>(n, f, std::move(nz));
 }
+// sketch.cpp:286-331: x_1 = v_1, x_i = v_i + b_{i-1} x_{i-1} (lower), the
+// mirrored backward recurrence when upper; the transpose runs the other way.
+class InverseBidiagonalOp final : public SketchOperator {
+ public:
+  InverseBidiagonalOp(Vector b, bool lower) : b_(std::move(b)), lower_(lower) {}
+  Index rows() const override { return static_cast<Index>(b_.size()) + 1; }
+  Index cols() const override { return rows(); }
+  std::string kind() const override { return "inverse_bidiagonal"; }
+  Matrix apply(const Matrix& M) const override { return run(M, lower_); }
+  Matrix apply_transpose(const Matrix& M) const override { return run(M, !lower_); }
+
+ private:
+  Matrix run(const Matrix& M, bool forward) const {
+    require(M.rows() == rows(), "inverse bidiagonal apply: dims");
+    Matrix out = M;
+    const Index n = rows();
+    for (Index j = 0; j < M.cols(); ++j) {
+      if (forward) {
+        for (Index i = 1; i < n; ++i) out(i, j) += b_[static_cast<size_t>(i - 1)] * out(i - 1, j);
+      } else {
+        for (Index i = n - 2; i >= 0; --i) out(i, j) += b_[static_cast<size_t>(i)] * out(i + 1, j);
+      }
+    }
+    return out;
+  }
+  Vector b_;
+  bool lower_;
+};
+
+// sketch.cpp:335-383: op = P_1 R_1 ... P_q R_q, R = I - 2 w w^T / (w^T w)
+class HouseholderChainOp final : public SketchOperator {
+ public:
+  HouseholderChainOp(std::vector<Vector> w, std::vector<std::vector<Index>> perms)
+      : w_(std::move(w)), perms_(std::move(perms)) {
+    require(!w_.empty() && w_.size() == perms_.size(), "householder chain: size mismatch");
+    n_ = static_cast<Index>(w_[0].size());
+    for (auto& v : w_) {
+      double s = 0;
+      for (double x : v) s += x * x;
+      require(static_cast<Index>(v.size()) == n_ && s > 0, "householder chain: bad reflector");
+    }
+    for (auto& p : perms_) IndexSet(p, n_);
+  }
+  Index rows() const override { return n_; }
+  Index cols() const override { return n_; }
+  std::string kind() const override { return "householder_chain"; }
+  Matrix apply(const Matrix& M) const override {
+    require(M.rows() == n_, "householder chain apply: dims");
+    Matrix X = M;
+    for (size_t t = w_.size(); t-- > 0;) {
+      reflect(w_[t], X);
+      Matrix Y(n_, X.cols());
+      for (Index j = 0; j < X.cols(); ++j)
+        for (Index i = 0; i < n_; ++i) Y(i, j) = X(perms_[t][static_cast<size_t>(i)], j);
+      X = std::move(Y);
+    }
+    return X;
+  }
+  Matrix apply_transpose(const Matrix& M) const override {
+    require(M.rows() == n_, "householder chain apply: dims");
+    Matrix X = M;
+    for (size_t t = 0; t < w_.size(); ++t) {
+      Matrix Y(n_, X.cols());
+      for (Index j = 0; j < X.cols(); ++j)
+        for (Index i = 0; i < n_; ++i) Y(perms_[t][static_cast<size_t>(i)], j) = X(i, j);
+      reflect(w_[t], Y);
+      X = std::move(Y);
+    }
+    return X;
+  }
+
+ private:
+  // X -= w ((2 / w^T w) (w^T X))
+  static void reflect(const Vector& w, Matrix& X) {
+    double ww = 0;
+    for (double x : w) ww += x * x;
+    const double c = 2.0 / ww;
+    for (Index j = 0; j < X.cols(); ++j) {
+      double s = 0;
+      for (Index i = 0; i < X.rows(); ++i) s += w[static_cast<size_t>(i)] * X(i, j);
+      const double cs = c * s;
+      for (Index i = 0; i < X.rows(); ++i) X(i, j) -= w[static_cast<size_t>(i)] * cs;
+    }
+  }
+  std::vector<Vector> w_;
+  std::vector<std::vector<Index>> perms_;
+  Index n_ = 0;
+};
+
+OpPtr make_inverse_bidiagonal(Vector subdiag, bool lower) {
+  return std::make_shared<InverseBidiagonalOp>(std::move(subdiag), lower);
+}
+OpPtr make_householder_chain(std::vector<Vector> w, std::vector<std::vector<Index>> perms) {
+  return std::make_shared<HouseholderChainOp>(std::move(w), std::move(perms));
+}
+OpPtr gen_inverse_bidiagonal(Index n, Rng& rng) {  // sketch.cpp:652-656
+  Vector b(static_cast<size_t>(n - 1));
+  for (Index i = 0; i < n - 1; ++i) b[static_cast<size_t>(i)] = rng.sign();
+  return make_inverse_bidiagonal(std::move(b), true);
+}
+OpPtr gen_householder_chain(Index n, Index q, Rng& rng) {  // sketch.cpp:657-665
+  std::vector<Vector> w;
+  std::vector<std::vector<Index>> perms;
+  for (Index t = 0; t < q; ++t) {
+    w.push_back(rng.gaussian_vector(n));
+    perms.push_back(rng.permutation(n));
+  }
+  return make_householder_chain(std::move(w), std::move(perms));
+}
+
 OpPtr make_gaussian(Matrix G) { return std::make_shared<GaussianOp>(std::move(G)); }
 OpPtr make_sub_identity(IndexSet selected, Index total) {
   return std::make_shared<SubIdentityOp>(std::move(selected), total);

@@ -75,3 +75,68 @@ int slra_transpose(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- inverse bidiagonal
+// InverseBidiagonalOp (sketch.cpp:286-331): per column the recurrence
+// y_i = x_i + b_{i-1} y_{i-1} (forward) or y_i = x_i + b_i y_{i+1}
+// (backward), in the reference's sequential order (bit-exact for b = +-1).
+// One warp owns 32 columns: 32 x 32 tiles are staged through shared memory
+// so global loads/stores are row-contiguous (coalesced), and each lane then
+// walks its column through the tile carrying y across tiles.
+namespace slra_dev {
+namespace {
+__global__ void bidiag_scan_kernel(const double* __restrict__ X, int64_t ldx, int64_t n, int64_t c,
+                                   const double* __restrict__ b, int forward, double* __restrict__ Y, int64_t ldy) {
+  __shared__ double tile[4][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c0 = ((int64_t)blockIdx.x * 4 + w) * 32;
+  if (c0 >= c) return;
+  double (*t)[33] = tile[w];
+  const int64_t col = c0 + lane;
+  const int ncol = (int)((c - c0) < 32 ? (c - c0) : 32);
+  double y = 0.0;
+  const int64_t ntiles = (n + 31) / 32;
+  for (int64_t tt = 0; tt < ntiles; ++tt) {
+    const int64_t tile_idx = forward ? tt : ntiles - 1 - tt;
+    const int64_t r0 = tile_idx * 32;
+    const int nr = (int)((n - r0) < 32 ? (n - r0) : 32);
+    for (int j = 0; j < ncol; ++j)
+      if (lane < nr) t[lane][j] = X[r0 + lane + (c0 + j) * ldx];
+    __syncwarp();
+    if (lane < ncol) {
+      if (forward) {
+        for (int i = 0; i < nr; ++i) {
+          const int64_t gi = r0 + i;
+          const double v = t[i][lane];
+          y = gi == 0 ? v : v + b[gi - 1] * y;
+          t[i][lane] = y;
+        }
+      } else {
+        for (int i = nr - 1; i >= 0; --i) {
+          const int64_t gi = r0 + i;
+          const double v = t[i][lane];
+          y = gi == n - 1 ? v : v + b[gi] * y;
+          t[i][lane] = y;
+        }
+      }
+    }
+    __syncwarp();
+    for (int j = 0; j < ncol; ++j)
+      if (lane < nr) Y[r0 + lane + (c0 + j) * ldy] = t[lane][j];
+    __syncwarp();
+  }
+  (void)col;
+}
+}  // namespace
+}  // namespace slra_dev
+
+extern "C" int slra_bidiag_scan(slra_ctx ctx, const double* X, int64_t ldx, int64_t n, int64_t c, const double* b,
+                                int forward, double* Y, int64_t ldy) {
+  if (!ctx || n < 1 || c < 0 || ldx < n || ldy < n) return SLRA_ERR_INVALID_ARGUMENT;
+  if (c == 0) return SLRA_OK;
+  slra_dev::Context* cx = slra_dev::C(ctx);
+  const unsigned g = (unsigned)slra_dev::ceil_div(c, 128);
+  SLRA_TIMED(cx, "sketch", slra_dev::bidiag_scan_kernel<<<g, 128, 0, cx->stream>>>(X, ldx, n, c, b, forward, Y, ldy);)
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}

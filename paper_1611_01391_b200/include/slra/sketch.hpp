@@ -57,6 +57,13 @@ class SketchOperator {
   /// op * M and op^T * M on the device (host in, host out).
   Matrix apply(const Matrix& M) const;
   Matrix apply_transpose(const Matrix& M) const;
+  /// False for the operators that are not signed row combinations (the
+  /// inverse-bidiagonal scan, the Householder chain, and composites holding
+  /// one): they cannot compile to a plan and run apply_device instead.
+  virtual bool plannable() const { return true; }
+  /// Y = op X (transpose: op^T X) on HBM-resident operands; Y preallocated
+  /// (rows() or cols() x X.cols()). Default: the compiled plan.
+  virtual void apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const;
 };
 
 using OpPtr = std::shared_ptr<const SketchOperator>;
@@ -74,6 +81,13 @@ OpPtr take_columns(OpPtr op, Index l, ColumnMode mode, Rng& rng);
 /// list plans, not a hot-path operator.
 OpPtr make_gaussian(Matrix G);
 OpPtr gen_gaussian(Index rows, Index cols, Rng& rng);
+
+/// sketch.cpp:286-383: inverse unit bidiagonal (a scan) and a chain of
+/// permuted Householder reflections: not plans, applied on the device.
+OpPtr make_inverse_bidiagonal(Vector subdiag, bool lower = true);
+OpPtr make_householder_chain(std::vector<Vector> reflectors, std::vector<std::vector<Index>> perms);
+OpPtr gen_inverse_bidiagonal(Index n, Rng& rng);
+OpPtr gen_householder_chain(Index n, Index q, Rng& rng);
 
 OpPtr gen_permutation(Index n, Rng& rng);
 OpPtr gen_sign_diagonal(Index n, Rng& rng);

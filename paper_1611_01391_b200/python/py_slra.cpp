@@ -394,6 +394,10 @@ PYBIND11_MODULE(_slra, m) {
   m.def("take_columns_random", [](const PyOp& op, Index l, Rng& rng) {
     return PyOp{take_columns(op.p, l, ColumnMode::Random, rng)};
   });
+  m.def("make_inverse_bidiagonal", [](const FArray& b, bool lower) { return PyOp{make_inverse_bidiagonal(np_vec(b), lower)}; },
+        py::arg("subdiag"), py::arg("lower") = true);
+  m.def("gen_inverse_bidiagonal", [](Index n, Rng& r) { return PyOp{gen_inverse_bidiagonal(n, r)}; });
+  m.def("gen_householder_chain", [](Index n, Index q, Rng& r) { return PyOp{gen_householder_chain(n, q, r)}; });
   m.def("make_gaussian", [](const FArray& G) { return PyOp{make_gaussian(from_np(G))}; });
   m.def("gen_gaussian", [](Index a, Index b, Rng& r) { return PyOp{gen_gaussian(a, b, r)}; });
   m.def("gen_permutation", [](Index n, Rng& r) { return PyOp{gen_permutation(n, r)}; });

@@ -19,6 +19,25 @@ LsrReport sketch_solve_resident(const DeviceMatrix& dA, const double* db, const 
   const Index d = dA.cols(), m = dA.rows();
   if (F.cols() != m) throw std::invalid_argument("sketch_solve: F cols != m");
   if (F.rows() <= d) throw std::invalid_argument("sketch_solve: need k > d");
+  if (!F.plannable()) {
+    // F holds a non-plan factor (inverse bidiagonal, Householder chain): the
+    // sketched system F (A | b) is formed by F's device application into the
+    // two column blocks of FW, then solved as the row-sharded path does
+    const Index k = F.rows();
+    DeviceMatrix FW(k, d + 1);
+    DeviceMatrix FA = DeviceMatrix::view(FW.data(), k, d, FW.ld());
+    DeviceMatrix Fb = DeviceMatrix::view(FW.data() + FW.ld() * d, k, 1, FW.ld());
+    const DeviceMatrix bv = DeviceMatrix::view(const_cast<double*>(db), m, 1, m);
+    F.apply_device(dA, false, FA);
+    F.apply_device(bv, false, Fb);
+    DevBuf<double> dx(static_cast<size_t>(d));
+    LsrReport rep;
+    check(slra_lsr_solve_sketched(device_context(), FW.data(), FW.ld(), k, d, dx.get(), &rep.sketched_residual),
+          "sketch_solve");
+    rep.x_hat = dx.download();
+    rep.k = k;
+    return rep;
+  }
   const SketchPlan plan = compile_plan(F, Side::Left);
   DevBuf<double> dx(static_cast<size_t>(d));
   DevBuf<int64_t> src(plan.src);

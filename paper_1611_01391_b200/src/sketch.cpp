@@ -214,6 +214,33 @@ class ProductOp final : public SketchOperator {
       e = substitute(e, [&](Index y) { return ops_[k]->row_of_apply_transpose(y); });
     return e;
   }
+  bool plannable() const override {
+    for (auto& o : ops_)
+      if (!o->plannable()) return false;
+    return true;
+  }
+  // a chain holding a non-plan factor: factor by factor on the device, right
+  // to left (the transpose left to right), as the reference applies it
+  void apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const override {
+    if (plannable()) {
+      SketchOperator::apply_device(X, transpose, Y);
+      return;
+    }
+    const size_t L = ops_.size();
+    DeviceMatrix cur;
+    const DeviceMatrix* in = &X;
+    for (size_t s = 0; s < L; ++s) {
+      const SketchOperator& f = transpose ? *ops_[s] : *ops_[L - 1 - s];
+      if (s + 1 == L) {
+        f.apply_device(*in, transpose, Y);
+        return;
+      }
+      DeviceMatrix nxt(transpose ? f.cols() : f.rows(), X.cols());
+      f.apply_device(*in, transpose, nxt);
+      cur = std::move(nxt);
+      in = &cur;
+    }
+  }
 
  private:
   std::vector<OpPtr> ops_;
@@ -238,6 +265,22 @@ class ColumnSliceOp final : public SketchOperator {
   }
   // apply_transpose: select_rows(inner^T M, cols)
   RowExpr row_of_apply_transpose(Index t) const override { return inner_->row_of_apply_transpose(cols_[t]); }
+  bool plannable() const override { return inner_->plannable(); }
+  void apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const override {
+    if (plannable()) {
+      SketchOperator::apply_device(X, transpose, Y);
+      return;
+    }
+    const SubIdentityOp sel(cols_, inner_->cols());  // l x n: picks rows cols_
+    DeviceMatrix Z(inner_->cols(), X.cols());
+    if (!transpose) {  // inner * (X scattered to the rows cols_)
+      sel.apply_device(X, true, Z);
+      inner_->apply_device(Z, false, Y);
+    } else {  // rows cols_ of inner^T X
+      inner_->apply_device(X, true, Z);
+      sel.apply_device(Z, false, Y);
+    }
+  }
 
  private:
   OpPtr inner_;
@@ -245,9 +288,127 @@ class ColumnSliceOp final : public SketchOperator {
   std::vector<Index> pos_;
 };
 
+// sketch.cpp:286-331: the inverse of a unit bidiagonal matrix, applied as a
+// recurrence down (lower) or up (upper) every column (slra_bidiag_scan);
+// apply_transpose runs the other direction.
+class InverseBidiagonalOp final : public SketchOperator {
+ public:
+  InverseBidiagonalOp(Vector b, bool lower) : b_(std::move(b)), lower_(lower) {}
+  Index rows() const override { return static_cast<Index>(b_.size()) + 1; }
+  Index cols() const override { return rows(); }
+  std::string kind() const override { return "inverse_bidiagonal"; }
+  RowExpr row_of_apply(Index) const override { throw std::logic_error("inverse_bidiagonal: not a plan operator"); }
+  RowExpr row_of_apply_transpose(Index) const override {
+    throw std::logic_error("inverse_bidiagonal: not a plan operator");
+  }
+  bool plannable() const override { return false; }
+  void apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const override {
+    require(X.rows() == rows(), "inverse bidiagonal apply: dims");
+    if (!db_.get() && !b_.empty()) db_ = DevBuf<double>(b_);
+    check(slra_bidiag_scan(device_context(), X.data(), X.ld(), rows(), X.cols(), db_.get(),
+                           (lower_ != transpose) ? 1 : 0, Y.data(), Y.ld()),
+          "inverse_bidiagonal");
+  }
+
+ private:
+  Vector b_;
+  bool lower_;
+  mutable DevBuf<double> db_;
+};
+
+// sketch.cpp:335-383: op = P_1 R_1 ... P_q R_q with R = I - 2 w w^T / w^T w.
+// Each reflection is two DMMA GEMMs (s = c w^T X with c = 2 / w^T w, then
+// X - w s as a rank-1 update with beta = 1), each permutation a row gather.
+class HouseholderChainOp final : public SketchOperator {
+ public:
+  HouseholderChainOp(std::vector<Vector> w, std::vector<std::vector<Index>> perms)
+      : w_(std::move(w)), perms_(std::move(perms)) {
+    require(!w_.empty() && w_.size() == perms_.size(), "householder chain: size mismatch");
+    n_ = static_cast<Index>(w_[0].size());
+    for (auto& v : w_) {
+      double ss = 0;
+      for (double x : v) ss += x * x;
+      require(static_cast<Index>(v.size()) == n_ && ss > 0, "householder chain: bad reflector");
+      c_.push_back(2.0 / ss);
+    }
+    for (auto& p : perms_) {
+      IndexSet(p, n_);  // validates
+      std::vector<int64_t> inv(static_cast<size_t>(n_));
+      for (Index i = 0; i < n_; ++i) inv[static_cast<size_t>(p[static_cast<size_t>(i)])] = i;
+      inv_.push_back(std::move(inv));
+    }
+  }
+  Index rows() const override { return n_; }
+  Index cols() const override { return n_; }
+  std::string kind() const override { return "householder_chain"; }
+  RowExpr row_of_apply(Index) const override { throw std::logic_error("householder_chain: not a plan operator"); }
+  RowExpr row_of_apply_transpose(Index) const override {
+    throw std::logic_error("householder_chain: not a plan operator");
+  }
+  bool plannable() const override { return false; }
+  void apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const override {
+    require(X.rows() == n_, "householder chain apply: dims");
+    slra_ctx cx = device_context();
+    const Index c = X.cols();
+    DeviceMatrix A(n_, c), B(n_, c);
+    DevBuf<double> s(static_cast<size_t>(c));
+    // copies are unit rescalings (one coalesced pass)
+    check(slra_scale_rows_cols(cx, X.data(), X.ld(), n_, c, nullptr, nullptr, A.data(), A.ld()), "householder_chain");
+    const size_t q = w_.size();
+    for (size_t k = 0; k < q; ++k) {
+      const size_t t = transpose ? k : q - 1 - k;
+      DevBuf<double> w(w_[t]);
+      if (!transpose) {
+        reflect(cx, w.get(), c_[t], A, s.get());
+        DevBuf<int64_t> p(std::vector<int64_t>(perms_[t].begin(), perms_[t].end()));  // Y(i) = X(perm[i])
+        check(slra_gather_rows(cx, A.data(), A.ld(), n_, c, p.get(), n_, B.data(), B.ld()), "householder_chain");
+      } else {
+        DevBuf<int64_t> p(inv_[t]);  // Y(perm[i]) = X(i)  <=>  Y(j) = X(inv[j])
+        check(slra_gather_rows(cx, A.data(), A.ld(), n_, c, p.get(), n_, B.data(), B.ld()), "householder_chain");
+        reflect(cx, w.get(), c_[t], B, s.get());
+      }
+      std::swap(A, B);
+    }
+    check(slra_scale_rows_cols(cx, A.data(), A.ld(), n_, c, nullptr, nullptr, Y.data(), Y.ld()), "householder_chain");
+  }
+
+ private:
+  // X -= w ((2 / w^T w) (w^T X)): s = c (w^T X) (1 x c), then X + (-1) w s
+  static void reflect(slra_ctx cx, const double* w, double cf, DeviceMatrix& X, double* s) {
+    const Index n = X.rows(), c = X.cols();
+    check(slra_gemm(cx, 1, 0, 1, c, n, cf, w, n, X.data(), X.ld(), 0.0, s, 1), "householder_chain");
+    check(slra_gemm(cx, 0, 0, n, c, 1, -1.0, w, n, s, 1, 1.0, X.data(), X.ld()), "householder_chain");
+  }
+  std::vector<Vector> w_;
+  std::vector<std::vector<Index>> perms_;
+  std::vector<std::vector<int64_t>> inv_;
+  std::vector<double> c_;
+  Index n_ = 0;
+};
+
 }  // namespace
 
 // ---------------------------------------------------------------- factories
+OpPtr make_inverse_bidiagonal(Vector subdiag, bool lower) {
+  return std::make_shared<InverseBidiagonalOp>(std::move(subdiag), lower);
+}
+OpPtr make_householder_chain(std::vector<Vector> w, std::vector<std::vector<Index>> perms) {
+  return std::make_shared<HouseholderChainOp>(std::move(w), std::move(perms));
+}
+OpPtr gen_inverse_bidiagonal(Index n, Rng& rng) {  // sketch.cpp:652-656
+  Vector b(static_cast<size_t>(n - 1));
+  for (Index i = 0; i < n - 1; ++i) b[static_cast<size_t>(i)] = rng.sign();
+  return make_inverse_bidiagonal(std::move(b), true);
+}
+OpPtr gen_householder_chain(Index n, Index q, Rng& rng) {  // sketch.cpp:657-665
+  std::vector<Vector> w;
+  std::vector<std::vector<Index>> perms;
+  for (Index t = 0; t < q; ++t) {
+    w.push_back(rng.gaussian_vector(n));
+    perms.push_back(rng.permutation(n));
+  }
+  return make_householder_chain(std::move(w), std::move(perms));
+}
 OpPtr make_permutation(std::vector<Index> sigma) { return std::make_shared<PermutationOp>(std::move(sigma)); }
 OpPtr make_sign_diagonal(Vector d) { return std::make_shared<SignDiagonalOp>(std::move(d)); }
 OpPtr make_abridged_hadamard(Index n, int d) { return std::make_shared<AbridgedHadamardOp>(n, d); }
@@ -361,51 +522,72 @@ SketchPlan compile_plan(const SketchOperator& op, Side side) {
 
 namespace {
 
-Matrix run_plan(const SketchPlan& p, const Matrix& M, bool rows_mode, Index out_rows, Index out_cols) {
+void run_plan_device(const SketchPlan& p, const DeviceMatrix& X, bool rows_mode, DeviceMatrix& out) {
   slra_ctx ctx = device_context();
-  DeviceMatrix dM = DeviceMatrix::upload(M);
-  DeviceMatrix out(out_rows, out_cols);
   DevBuf<int64_t> src(p.src);
   DevBuf<double> coef(p.coef);
   DevBuf<int32_t> q(p.q);
   if (rows_mode)
-    check(slra_sketch_rows(ctx, dM.data(), dM.ld(), M.rows(), M.cols(), src.get(), coef.get(), q.get(), p.width,
+    check(slra_sketch_rows(ctx, X.data(), X.ld(), X.rows(), X.cols(), src.get(), coef.get(), q.get(), p.width,
                            p.tree, p.count, out.data(), out.ld()),
           "slra_sketch_rows");
   else
-    check(slra_sketch_cols(ctx, dM.data(), dM.ld(), M.rows(), M.cols(), src.get(), coef.get(), q.get(), p.width,
+    check(slra_sketch_cols(ctx, X.data(), X.ld(), X.rows(), X.cols(), src.get(), coef.get(), q.get(), p.width,
                            p.tree, p.count, out.data(), out.ld()),
           "slra_sketch_cols");
-  return out.download();
+}
+
+// the transpose of an operator as an operator (rows of op^T M: a left plan)
+struct TransposeView final : SketchOperator {
+  const SketchOperator& o;
+  explicit TransposeView(const SketchOperator& x) : o(x) {}
+  Index rows() const override { return o.cols(); }
+  Index cols() const override { return o.rows(); }
+  std::string kind() const override { return "transpose"; }
+  RowExpr row_of_apply(Index i) const override { return o.row_of_apply_transpose(i); }
+  RowExpr row_of_apply_transpose(Index i) const override { return o.row_of_apply(i); }
+};
+
+Matrix host_transpose(const Matrix& M) {  // data movement only
+  Matrix T(M.cols(), M.rows());
+  for (Index j = 0; j < M.cols(); ++j)
+    for (Index i = 0; i < M.rows(); ++i) T(j, i) = M(i, j);
+  return T;
 }
 
 }  // namespace
 
+void SketchOperator::apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const {
+  if (transpose) {
+    TransposeView t(*this);
+    run_plan_device(compile_plan(t, Side::Left), X, true, Y);
+  } else {
+    run_plan_device(compile_plan(*this, Side::Left), X, true, Y);
+  }
+}
+
 Matrix SketchOperator::apply(const Matrix& M) const {
   require(M.rows() == cols(), "sketch apply: dims");
-  return run_plan(compile_plan(*this, Side::Left), M, true, rows(), M.cols());
+  DeviceMatrix dM = DeviceMatrix::upload(M), out(rows(), M.cols());
+  apply_device(dM, false, out);
+  return out.download();
 }
 
 Matrix SketchOperator::apply_transpose(const Matrix& M) const {
   require(M.rows() == rows(), "sketch apply: dims");
-  // rows of op^T M: a left plan of the transpose
-  struct T final : SketchOperator {
-    const SketchOperator& o;
-    explicit T(const SketchOperator& x) : o(x) {}
-    Index rows() const override { return o.cols(); }
-    Index cols() const override { return o.rows(); }
-    std::string kind() const override { return "transpose"; }
-    RowExpr row_of_apply(Index i) const override { return o.row_of_apply_transpose(i); }
-    RowExpr row_of_apply_transpose(Index i) const override { return o.row_of_apply(i); }
-  } t(*this);
-  return run_plan(compile_plan(t, Side::Left), M, true, cols(), M.cols());
+  DeviceMatrix dM = DeviceMatrix::upload(M), out(cols(), M.cols());
+  apply_device(dM, true, out);
+  return out.download();
 }
 
 Matrix apply(const SketchOperator& op, const Matrix& M, Side side) {
   if (side == Side::Left) return op.apply(M);
   // M * op = (op^T M^T)^T: column t of M*op combines columns of M.
   require(M.cols() == op.rows(), "sketch apply: dims");
-  return run_plan(compile_plan(op, Side::Right), M, false, M.rows(), op.cols());
+  if (!op.plannable()) return host_transpose(op.apply_transpose(host_transpose(M)));
+  DeviceMatrix dM = DeviceMatrix::upload(M), out(M.rows(), op.cols());
+  run_plan_device(compile_plan(op, Side::Right), dM, false, out);
+  return out.download();
 }
 
 Matrix materialize(const SketchOperator& op, Index cap) {

@@ -757,3 +757,32 @@ def test_score_gap_and_bounds(oracle):  # test_leverage.cpp:292-320
     assert oracle.sample_bound_quadratic(2, 1.0, 1.0) == pytest.approx(12800.0)
     assert oracle.sample_bound_loglinear(8, 1.0, 1.0, 100.0) == pytest.approx(100.0 * 8 * np.log(8.0))
     assert oracle.epsilon_for_sample(2, 16, 0.1) == pytest.approx(np.sqrt(8.0 * np.log(40.0) / 16.0))
+
+
+# ---------------------------------------------------------------- remaining operators (test_sketch.cpp:119-158)
+def test_inverse_bidiagonal_known(oracle):
+    X = oracle.Rng(3).gaussian_matrix(6, 2)
+    assert np.array_equal(oracle.make_inverse_bidiagonal(np.zeros(5)).apply(X), X)
+    rng = oracle.Rng(4)
+    n = 64
+    op = oracle.gen_inverse_bidiagonal(n, rng)
+    B = oracle.materialize(op)
+    L = np.linalg.inv(B)
+    assert np.linalg.norm(L @ B - np.eye(n)) < 1e-10
+    for i in range(n):
+        for j in range(i + 2, min(n - 1, i + 3) + 1):
+            assert abs(L[j, i]) < 1e-12
+    assert np.linalg.cond(B) <= np.sqrt(2) * n * (1 + 1e-8)
+    Y = rng.gaussian_matrix(n, 3)
+    assert np.linalg.norm(op.apply_transpose(Y) - B.T @ Y) < 1e-11 * np.linalg.norm(B) * np.linalg.norm(Y)
+    U = oracle.materialize(oracle.make_inverse_bidiagonal(np.ones(3), False))
+    assert abs(U[0, 3] - 1.0) < 1e-14 and np.allclose(U, np.triu(U))
+
+
+def test_householder_chain_orthogonal(oracle):
+    rng = oracle.Rng(6)
+    op = oracle.gen_householder_chain(16, 4, rng)
+    R = oracle.materialize(op)
+    assert np.linalg.norm(R @ R.T - np.eye(16)) < 1e-12
+    X = rng.gaussian_matrix(16, 3)
+    assert np.linalg.norm(op.apply_transpose(X) - R.T @ X) < 1e-12
