@@ -57,6 +57,27 @@ def test_no_cpu_fallback(slra):
         slra.thin_qr(np.eye(3))
     with pytest.raises(slra.DeviceError):
         slra.cross_approx(np.eye(8), 1, 2, 2, [0, 1], 1, 1.1, slra.Rng(0))
+    # the §8f rows fail the same way (no host path behind them)
+    rng = slra.Rng(1)
+    with pytest.raises(slra.DeviceError):
+        slra.build_hss(np.eye(16), 2, 2, 1e-6, "svd", rng)
+    with pytest.raises(slra.DeviceError):
+        slra.lra_premult(np.eye(8), slra.gen_gaussian(4, 8, rng), slra.gen_gaussian(8, 3, rng), 2)
+    with pytest.raises(slra.DeviceError):
+        slra.cur_via_leverage(np.eye(8), 1, 2, 2, 1.0, 1.0, "exactly", slra.uniform_scores(8), rng)
+    with pytest.raises(slra.DeviceError):
+        slra.gen_inverse_bidiagonal(8, rng).apply(np.eye(8))
+
+
+def test_shared_libstdcxx_and_import_order(oracle):
+    """libslra.so and the binding link the shared libstdc++ (a static copy
+    crashes iostream/locale use once another C++ extension is loaded)."""
+    for lib in (os.path.join(ROOT, "paper_1611_01391_b200", "lib", "libslra.so"),):
+        assert "libstdc++.so.6" in os.popen(f"readelf -d {lib}").read()
+    import paper_1611_01391_b200 as s  # imported after the oracle (conftest loads it first)
+    h = s.hss_deserialize("hss 4 1 2 0 0 1 0 leaf 0 0 2 2 1 2 3 4")
+    assert h["n"] == 4 and h["diag"][0][2].tolist() == [[1.0, 3.0], [2.0, 4.0]]
+    assert s.hss_deserialize(s.hss_serialize(h))["diag"][0][2].tolist() == [[1.0, 3.0], [2.0, 4.0]]
 
 
 def test_rng_bit_identical(slra, oracle):
