@@ -59,6 +59,10 @@ int64_t slra_ctx_launch_count(slra_ctx ctx);
  * "family=ms,launches;..." summed since then. */
 int slra_ctx_set_timing(slra_ctx ctx, int on);
 int slra_ctx_timing_report(slra_ctx ctx, char* buf, int64_t len);
+/* Stream-ordered device memory (cudaMallocAsync / cudaFreeAsync on the
+ * context stream, pooled): a buffer may be freed right after the calls that
+ * use it are issued on the context stream; other streams must synchronise
+ * with slra_ctx_stream first. */
 int slra_device_alloc(slra_ctx ctx, int64_t bytes, void** d_out);
 int slra_device_free(slra_ctx ctx, void* d_ptr);
 int slra_memcpy_h2d(slra_ctx ctx, void* d_dst, const void* h_src, int64_t bytes);

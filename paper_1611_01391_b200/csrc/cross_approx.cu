@@ -36,16 +36,24 @@ struct CaParams {
   double* Sr_out = nullptr;    // problem 0: S_r (k x r, ld k), nullable
 };
 
+// Shared-memory plan of one C-A block. Only S is strip-sized (mm x c): it
+// holds the gathered strip, its basis Q and then B = Q G^-1 in place, and at
+// the end the staged C / R^T strips of the residual factors. Everything else
+// is c x c or mm-vectors, so a 256 x 256 block with k = l = 32 needs ~110 KB
+// and two blocks share an SM (the kernel is latency bound: two resident CTAs
+// hide each other's dependent chains).
 struct CaSmem {
-  double *S, *W, *R, *Gt, *V, *tau, *v, *nu, *nd, *sigma, *sgn, *rv, *Tm, *Sm;
-  int *p2r, *Icur, *Jcur, *perm, *order, *flag, *tmpidx;
+  double *S, *W, *R, *Gt, *V, *tau, *v, *nu, *nd, *rn, *sigma, *sgn, *rv, *Tm, *Sm, *volv;
+  int *p2r, *r2p, *Icur, *Jcur, *perm, *order, *flag, *tmpidx;
   int64_t* ri;
 };
 
 __host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
-  size_t d = 2 * (size_t)mm * c + 4 * (size_t)c * c + 8 * (size_t)c + 2 * (size_t)mm + 40;  // + odd-ld padding of W, V
-  size_t i = (size_t)mm + 4 * (size_t)c + 8 + (size_t)c;
+  // S (mm c + c), W (c+1) c, Gt c^2, V (c+1) c, 4 c-vectors, nu/nd/rn (mm each), rv 40, volv + slack
+  size_t d = (size_t)mm * c + (size_t)c + 2 * (size_t)(c + 1) * c + (size_t)c * c + 4 * (size_t)c +
+             3 * (size_t)mm + 40 + 8 + 2 * (size_t)c;
+  size_t i = 2 * (size_t)mm + 5 * (size_t)c + 8;
   return d * 8 + 33 * 8 + i * 4 + 64;
 }
 
@@ -53,24 +61,29 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
   CaSmem s;
   double* d = reinterpret_cast<double*>(base);
-  s.S = d; d += (size_t)mm * c;
-  s.W = d; d += (size_t)mm * c + c;  // room for ld = p | 1
-  s.R = d; d += c * c;
+  s.S = d; d += (size_t)mm * c + c;
+  s.W = d; d += (size_t)(c + 1) * c;  // the nucleus' Jacobi operand (ld p | 1, p <= c)
+  s.R = nullptr;
   s.Gt = d; d += c * c;
-  s.V = d; d += c * c + c;  // room for ld = q | 1
-  s.Tm = s.R;  // R (the selection's QR factor) is dead once the nucleus starts
-  s.Sm = d; d += c * c;
+  s.V = d; d += (size_t)(c + 1) * c;  // room for ld = q | 1
+  // the nucleus factors T_r Sigma_r^-1 and S_r are written after
+  // cta_svd_finish, when the Jacobi operands V and W are dead
+  s.Tm = s.V;
+  s.Sm = s.W;
   s.tau = d; d += c;
   s.v = d; d += c;
   s.sigma = d; d += c;
   s.sgn = d; d += c;
   s.nu = d; d += mm;
   s.nd = d; d += mm;
+  s.rn = d; d += mm;
   s.rv = d; d += 40;
+  s.volv = d; d += 8;
   d += 2 * c;  // slack
   s.ri = reinterpret_cast<int64_t*>(d);
   int* ip = reinterpret_cast<int*>(s.ri + 33);
   s.p2r = ip; ip += mm;
+  s.r2p = ip; ip += mm;
   s.Icur = ip; ip += c;
   s.Jcur = ip; ip += c;
   s.perm = ip; ip += c;
@@ -82,7 +95,7 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
 
 // select_rows_spanning(strip, count, h) where strip (len x nidx) is gathered
 // from A: rows_strip -> strip = A(idx_in, :)^T (len = n), else A(:, idx_in).
-template <int NT>
+template <int NT, int CMAX>
 __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_strip, const int* idx_in, int nidx,
                             int len, int count, double h, int* idx_out, double* vol_out) {
   const int tid = threadIdx.x;
@@ -99,13 +112,25 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
     }
   }
   __syncthreads();
-  cta_thin_qr<NT>(s.S, len, len, nidx, s.W, len, s.R, nidx, s.tau, s.rv);  // Q -> W
+  // ONE len x nidx array carries the strip, its basis Q (in place) and then
+  // B = Q G^-1 (in place): the pivot order is taken with the working copy in
+  // registers, and the volume |det Q[idx, :]| is tracked through the swaps.
+  cta_thin_qr_inplace<NT, CMAX>(s.S, len, len, nidx, s.tau, s.rv);
   const int rq = count < nidx ? count : nidx;
-  ColPivScratch cs{s.S, len, s.p2r, s.nu, s.nd, s.v, s.tau, s.rv, s.ri};
-  cta_colpiv_init<NT>(s.W, len, len, rq, cs, s.tmpidx);
+  if (count > rq) {  // the padding branch needs the basis row norms (cur.cpp:125-134)
+    for (int i = tid; i < len; i += NT) {
+      double acc = 0.0;
+      for (int j = 0; j < nidx; ++j) acc += s.S[i + j * len] * s.S[i + j * len];
+      s.rn[i] = sqrt(acc);
+    }
+  }
+  if (rq <= 16) cta_colpiv_init_regs<NT, 16>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx);
+  else if (rq <= 32) cta_colpiv_init_regs<NT, 32>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx);
+  else if constexpr (CMAX > 32)
+    cta_colpiv_init_regs<NT, 64>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx);
   __syncthreads();
-  const int st = cta_maxvol_swaps<NT>(s.W, len, len, rq, h, 4 * rq, s.tmpidx, s.S, len, s.Gt, rq, s.perm, s.tau,
-                                      s.nu, s.nd, s.rv, s.ri, s.flag);
+  const int st = cta_maxvol_swaps<NT>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, s.S, len, s.Gt, rq, s.perm, s.tau,
+                                      s.nu, s.nd, s.rv, s.ri, s.flag, s.volv);
   if (st != SLRA_OK) return st;
   __syncthreads();
   for (int t = tid; t < rq; t += NT) idx_out[t] = s.tmpidx[t];
@@ -113,18 +138,12 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
   if (count > rq) {
     // pad with the largest remaining rows of the basis (cur.cpp:125-134);
     // equal norms: lower index first.
-    for (int i = tid; i < len; i += NT) {
-      double acc = 0.0;
-      for (int j = 0; j < nidx; ++j) acc += s.W[i + j * len] * s.W[i + j * len];
-      s.nu[i] = sqrt(acc);
-    }
-    __syncthreads();
     for (int t = rq; t < count; ++t) {
       ArgMax a{-1.0, INT64_MAX};
       for (int i = tid; i < len; i += NT) {
         bool used = false;
         for (int u = 0; u < t; ++u) used |= (idx_out[u] == i);
-        if (!used) a = argmax_merge(a, ArgMax{s.nu[i], i});
+        if (!used) a = argmax_merge(a, ArgMax{s.rn[i], i});
       }
       a = block_argmax<NT>(a, s.rv, s.ri);
       if (tid == 0) idx_out[t] = (int)a.i;
@@ -133,19 +152,9 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
   }
   // volume proxy |det Q[idx,:]| (cur.cpp:192-197), only when square
   if (vol_out) {
-    if (count == nidx) {
-      for (int e = tid; e < count * nidx; e += NT) {
-        const int a = e % count, b = e / count;
-        s.Gt[a + b * count] = s.W[idx_out[a] + b * len];
-      }
-      __syncthreads();
-      if (tid < 32) {
-        const double dv = warp_abs_det(s.Gt, count, count);
-        if (tid == 0) *vol_out = dv;
-      }
-    } else if (tid == 0) {
-      *vol_out = 0.0;
-    }
+    // |det Q[idx, :]| = the swap loop's tracked volume (round-0 QR of G times
+    // the pivot magnitudes of the swaps)
+    if (tid == 0) *vol_out = count == nidx ? *s.volv : 0.0;
     __syncthreads();
   }
   return SLRA_OK;
@@ -154,7 +163,7 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
 // primitive_cur nucleus from G = A(I, J) (k x l). Writes r, nucleus (l x k)
 // and the factors Tm = T_r Sigma_r^-1 (l x r, ld l) and Sm = S_r (k x r, ld k)
 // into smem. Returns status.
-template <int NT>
+template <int NT, int CMAX>
 __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I, int k, const int* J, int l,
                            int r_req, int* r_out) {
   const int tid = threadIdx.x;
@@ -173,7 +182,7 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
   // column norm jointly carry less than that, so pairs of two such columns
   // are not rotated (the noise directions of rank-deficient generators, as in
   // configs 3 and 5, otherwise keep the sweeps going to the cap).
-  cta_jacobi<NT>(s.W, p | 1, p, q, s.V, q | 1, s.flag, 1e-10 / sqrt((double)q));
+  cta_jacobi<NT, CMAX>(s.W, p | 1, p, q, s.V, q | 1, s.flag, 1e-10 / sqrt((double)q));
   // finish into S (p x q, ld p) and Gt (q x q, ld q): for tall G the left
   // vectors are in S; for wide G (SVD of G^T) they are the rows of V.
   cta_svd_finish<NT>(s.W, p | 1, p, q, s.V, q | 1, s.sigma, s.order, s.S, p, s.Gt, q, s.sgn);
@@ -220,7 +229,11 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
   return SLRA_OK;
 }
 
-__global__ void __launch_bounds__(kCT) ca_block_kernel(CaParams P) {
+// two resident CTAs per SM (<= 128 registers): the block is latency bound
+// CMAX = 32 (k, l <= 32): register variants sized for 32 columns so that
+// two CTAs fit an SM; CMAX = 64: one CTA per SM
+template <int CMAX>
+__global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaParams P) {
   extern __shared__ __align__(16) char smem_raw[];
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
@@ -232,14 +245,14 @@ __global__ void __launch_bounds__(kCT) ca_block_kernel(CaParams P) {
     __syncthreads();
     for (int loop = 0; loop < P.loops && status == SLRA_OK; ++loop) {
       double* vol = (b == 0 && P.trace_vol) ? P.trace_vol + 2 * loop : nullptr;
-      status = select_strip<kCT>(s, A, P.lda, true, s.Icur, P.k, P.n, P.l, P.h, s.Jcur, vol);
+      status = select_strip<kCT, CMAX>(s, A, P.lda, true, s.Icur, P.k, P.n, P.l, P.h, s.Jcur, vol);
       if (status != SLRA_OK) break;
       if (b == 0 && P.trace_rows) {
         for (int t = tid; t < P.k; t += kCT) P.trace_rows[(int64_t)(2 * loop) * P.k + t] = s.Icur[t];
         for (int t = tid; t < P.l; t += kCT) P.trace_cols[(int64_t)(2 * loop) * P.l + t] = s.Jcur[t];
       }
       vol = (b == 0 && P.trace_vol) ? P.trace_vol + 2 * loop + 1 : nullptr;
-      status = select_strip<kCT>(s, A, P.lda, false, s.Jcur, P.l, P.m, P.k, P.h, s.Icur, vol);
+      status = select_strip<kCT, CMAX>(s, A, P.lda, false, s.Jcur, P.l, P.m, P.k, P.h, s.Icur, vol);
       if (status != SLRA_OK) break;
       if (b == 0 && P.trace_rows) {
         for (int t = tid; t < P.k; t += kCT) P.trace_rows[(int64_t)(2 * loop + 1) * P.k + t] = s.Icur[t];
@@ -253,7 +266,7 @@ __global__ void __launch_bounds__(kCT) ca_block_kernel(CaParams P) {
     __syncthreads();
   }
   int r = 0;
-  if (status == SLRA_OK) status = cta_nucleus<kCT>(s, A, P.lda, s.Icur, P.k, s.Jcur, P.l, P.r, &r);
+  if (status == SLRA_OK) status = cta_nucleus<kCT, CMAX>(s, A, P.lda, s.Icur, P.k, s.Jcur, P.l, P.r, &r);
   if (tid == 0) {
     P.status[b] = status;
     P.r_out[b] = status == SLRA_OK ? r : 0;
@@ -284,9 +297,9 @@ __global__ void __launch_bounds__(kCT) ca_block_kernel(CaParams P) {
   }
   if (P.P) {
     // P = A(:,J) Tm (m x rq, zero beyond r), Q = Sm^T A(I,:) (rq x n). The
-    // strips are staged once in shared memory (S and W are free after the
-    // nucleus): C = A(:,J) in S (m x l, coalesced columns), R^T = A(I,:)^T
-    // in W (n x k); then a thread per row of P / column of Q, with r
+    // strips are staged in shared memory one after the other (S is free
+    // after the nucleus): C = A(:,J) (m x l, coalesced columns), then
+    // R^T = A(I,:)^T (n x k); a thread per row of P / column of Q, with r
     // independent FMA chains each.
     double* Pb = P.P + (int64_t)b * P.m * P.rq;
     double* Qb = P.Q + (int64_t)b * P.rq * P.n;
@@ -295,39 +308,47 @@ __global__ void __launch_bounds__(kCT) ca_block_kernel(CaParams P) {
       const int i = e % P.m, t = e / P.m;
       s.S[i + t * P.m] = __ldg(A + i + (int64_t)s.Jcur[t] * P.lda);
     }
+    __syncthreads();
+    // accumulators in chunks of kCH outputs (registers stay within the
+    // two-CTAs-per-SM budget); each chunk re-reads its strip from smem
+    constexpr int kCH = 16;
+    for (int i = tid; i < P.m; i += kCT) {
+      for (int j0 = 0; j0 < P.rq; j0 += kCH) {
+        double acc[kCH];
+#pragma unroll
+        for (int j = 0; j < kCH; ++j) acc[j] = 0.0;
+        for (int t = 0; t < P.l; ++t) {
+          const double cv = s.S[i + t * P.m];
+#pragma unroll
+          for (int j = 0; j < kCH; ++j)
+            if (j0 + j < r) acc[j] = fma(cv, s.Tm[t + (j0 + j) * P.l], acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kCH; ++j)
+          if (j0 + j < P.rq) Pb[i + (int64_t)(j0 + j) * P.m] = acc[j];  // zero beyond r
+      }
+    }
+    __syncthreads();  // every row of P is done with C: stage R^T over it
     for (int e = tid; e < P.n * P.k; e += kCT) {
       const int t = e % P.k, c = e / P.k;
-      s.W[c + t * P.n] = __ldg(A + s.Icur[t] + (int64_t)c * P.lda);
+      s.S[c + t * P.n] = __ldg(A + s.Icur[t] + (int64_t)c * P.lda);
     }
     __syncthreads();
-    constexpr int kRQ = 64;  // rq <= min(k, l) <= 64
-    for (int i = tid; i < P.m; i += kCT) {
-      double acc[kRQ];
-#pragma unroll
-      for (int j = 0; j < kRQ; ++j) acc[j] = 0.0;
-      for (int t = 0; t < P.l; ++t) {
-        const double cv = s.S[i + t * P.m];
-#pragma unroll
-        for (int j = 0; j < kRQ; ++j)
-          if (j < r) acc[j] = fma(cv, s.Tm[t + j * P.l], acc[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < kRQ; ++j)
-        if (j < P.rq) Pb[i + (int64_t)j * P.m] = acc[j];  // zero beyond r
-    }
     for (int c = tid; c < P.n; c += kCT) {
-      double acc[kRQ];
+      for (int j0 = 0; j0 < P.rq; j0 += kCH) {
+        double acc[kCH];
 #pragma unroll
-      for (int j = 0; j < kRQ; ++j) acc[j] = 0.0;
-      for (int t = 0; t < P.k; ++t) {
-        const double rv = s.W[c + t * P.n];
+        for (int j = 0; j < kCH; ++j) acc[j] = 0.0;
+        for (int t = 0; t < P.k; ++t) {
+          const double rv = s.S[c + t * P.n];
 #pragma unroll
-        for (int j = 0; j < kRQ; ++j)
-          if (j < r) acc[j] = fma(s.Sm[t + j * P.k], rv, acc[j]);
+          for (int j = 0; j < kCH; ++j)
+            if (j0 + j < r) acc[j] = fma(s.Sm[t + (j0 + j) * P.k], rv, acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kCH; ++j)
+          if (j0 + j < P.rq) Qb[j0 + j + (int64_t)c * P.rq] = acc[j];
       }
-#pragma unroll
-      for (int j = 0; j < kRQ; ++j)
-        if (j < P.rq) Qb[j + (int64_t)c * P.rq] = acc[j];
     }
   }
 }
@@ -358,8 +379,13 @@ static bool ca_fits(int m, int n, int k, int l) {
 
 int launch_ca_block(Context* c, const CaParams& p, int nprob) {
   const size_t smem = ca_smem_bytes(p.m, p.n, p.k, p.l);
-  SLRA_CUDA(cudaFuncSetAttribute(ca_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SLRA_TIMED(c, "cross_approx", ca_block_kernel<<<nprob, kCT, smem, c->stream>>>(p);)
+  if (p.k <= 32 && p.l <= 32) {
+    SLRA_CUDA(cudaFuncSetAttribute(ca_block_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLRA_TIMED(c, "cross_approx", ca_block_kernel<32><<<nprob, kCT, smem, c->stream>>>(p);)
+  } else {
+    SLRA_CUDA(cudaFuncSetAttribute(ca_block_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLRA_TIMED(c, "cross_approx", ca_block_kernel<64><<<nprob, kCT, smem, c->stream>>>(p);)
+  }
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }

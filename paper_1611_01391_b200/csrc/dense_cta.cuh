@@ -143,11 +143,12 @@ __device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, doub
 // stored below the diagonal of V (ld ldv) and tau, written to Q (ld ldq, smem
 // or global, must not alias V). Column j = H_0 ... H_j e_j is built in the
 // registers of the warp that owns it (RPL rows per lane): no block barriers.
-template <int NT, int RPL>
-__device__ void cta_form_q_regs(const double* V, int ldv, int m, int c, const double* tau, double* Q, int ldq) {
+template <int NT, int RPL, int CMAX = 64>
+__device__ void cta_form_q_regs(const double* V, int ldv, int m, int c, const double* tau, double* Q, int ldq,
+                                bool inplace = false, const double* colsign = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = NT / 32;
-  constexpr int CPW = (64 + NW - 1) / NW;  // c <= 64
+  constexpr int CPW = (CMAX + NW - 1) / NW;  // c <= CMAX
   // all columns of this warp travel together: one read of each reflector,
   // interleaved butterflies
   double y[CPW][RPL];
@@ -188,14 +189,18 @@ __device__ void cta_form_q_regs(const double* V, int ldv, int m, int c, const do
       }
     }
   }
+  // in place (Q aliases V): every warp has read its last reflector before
+  // any column of Q overwrites them
+  if (inplace) __syncthreads();
 #pragma unroll
   for (int q = 0; q < CPW; ++q) {
     const int j = warp + q * NW;
     if (j < c) {
+      const double f = colsign ? colsign[j] : 1.0;
 #pragma unroll
       for (int r = 0; r < RPL; ++r) {
         const int i = lane + 32 * r;
-        if (i < m) Q[i + (int64_t)j * ldq] = y[q][r];
+        if (i < m) Q[i + (int64_t)j * ldq] = f * y[q][r];
       }
     }
   }
@@ -227,6 +232,26 @@ __device__ void cta_thin_qr(double* A, int lda, int m, int c, double* Q, int ldq
   for (int e = threadIdx.x; e < m * c; e += NT) {
     const int i = e % m, j = e / m;
     if (A[j + j * lda] < 0.0) Q[i + (int64_t)j * ldq] = -Q[i + (int64_t)j * ldq];  // and column i of Q
+  }
+  __syncthreads();
+}
+
+// thin_qr's Q (sign-fixed so R(i,i) >= 0) written over A itself (m <= 256):
+// Householder QR in place, the column signs of R read off its diagonal into
+// `red`, then Q built in registers and stored over the reflectors. R is not
+// kept (the selection path only needs the basis). red >= c + 8 doubles.
+template <int NT, int CMAX = 64>
+__device__ void cta_thin_qr_inplace(double* A, int lda, int m, int c, double* tau, double* red) {
+  cta_house_qr<NT>(A, lda, m, c, tau, red);
+  __syncthreads();
+  for (int j = threadIdx.x; j < c; j += NT) red[j] = A[j + j * lda] < 0.0 ? -1.0 : 1.0;
+  __syncthreads();
+  if (CMAX <= 32 || c <= 32) {  // half the register columns (the C-A kernel's two-CTA budget)
+    if (m <= 64) cta_form_q_regs<NT, 2, 32>(A, lda, m, c, tau, A, lda, true, red);
+    else cta_form_q_regs<NT, 8, 32>(A, lda, m, c, tau, A, lda, true, red);
+  } else if constexpr (CMAX > 32) {
+    if (m <= 64) cta_form_q_regs<NT, 2>(A, lda, m, c, tau, A, lda, true, red);
+    else cta_form_q_regs<NT, 8>(A, lda, m, c, tau, A, lda, true, red);  // m <= 256 (callers enforce)
   }
   __syncthreads();
 }
@@ -326,6 +351,122 @@ __device__ void cta_colpiv_init(const double* Q, int ldq, int m, int r, const Co
           s.nu[p] = s.nd[p];
         } else {
           s.nu[p] = nu * sqrt(temp);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// The same pivot order with the working copy of Q^T in REGISTERS: thread t
+// owns row t of Q (m <= NT, r <= RMAX), so no m x r shared scratch is needed
+// (the C-A kernel then fits two CTAs per SM). Rows keep their thread while
+// positions are swapped through p2r / r2p; each row's update is the same
+// arithmetic, in the same order, as cta_colpiv_init.
+template <int NT, int RMAX>
+__device__ void cta_colpiv_init_regs(const double* Q, int ldq, int m, int r, double* nu, double* nd, int* p2r,
+                                     int* r2p, double* vbuf, double* tauv, double* rv, int64_t* ri, int* I_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double sqrt_eps = 1.4901161193847656e-08;  // sqrt(DBL_EPSILON)
+  double x[RMAX];
+  const bool own = tid < m;
+  {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) {
+      x[j] = (own && j < r) ? Q[tid + j * ldq] : 0.0;
+      acc += x[j] * x[j];
+    }
+    if (own) {
+      nu[tid] = nd[tid] = sqrt(acc);
+      p2r[tid] = tid;
+      r2p[tid] = tid;
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    ArgMax a{-1.0, INT64_MAX};
+    for (int p = k + tid; p < m; p += NT) a = argmax_merge(a, ArgMax{nu[p], p});
+    a = block_argmax<NT>(a, rv, ri);
+    const int big = static_cast<int>(a.i);
+    if (tid == 0 && big != k) {
+      const int rk = p2r[k], rb = p2r[big];
+      p2r[k] = rb;
+      p2r[big] = rk;
+      r2p[rb] = k;
+      r2p[rk] = big;
+      double tv = nu[k]; nu[k] = nu[big]; nu[big] = tv;
+      tv = nd[k]; nd[k] = nd[big]; nd[big] = tv;
+    }
+    __syncthreads();
+    const int row = p2r[k];
+    if (tid == row) {
+#pragma unroll
+      for (int j = 0; j < RMAX; ++j)
+        if (j >= k && j < r) vbuf[j] = x[j];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double tail = 0.0;
+      for (int j = k + 1 + lane; j < r; j += 32) tail += vbuf[j] * vbuf[j];
+      tail = warp_sum(tail);
+      const double c0 = vbuf[k];
+      double t;
+      __syncwarp();
+      if (tail <= DBL_MIN) {
+        t = 0.0;
+        for (int j = k + 1 + lane; j < r; j += 32) vbuf[j] = 0.0;
+      } else {
+        double beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        const double den = c0 - beta;
+        for (int j = k + 1 + lane; j < r; j += 32) vbuf[j] = vbuf[j] / den;
+        t = (beta - c0) / beta;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        tauv[0] = t;
+        I_out[k] = row;
+      }
+    }
+    __syncthreads();
+    const double t = tauv[0];
+    const int p = own ? r2p[tid] : -1;
+    if (p > k) {
+      if (r - k > 1 && t != 0.0) {
+        double w = 0.0;
+#pragma unroll
+        for (int j = 0; j < RMAX; ++j)
+          if (j > k && j < r) w += vbuf[j] * x[j];
+#pragma unroll
+        for (int j = 0; j < RMAX; ++j)
+          if (j == k) w += x[j];
+#pragma unroll
+        for (int j = 0; j < RMAX; ++j) {
+          if (j == k) x[j] -= t * w;
+          if (j > k && j < r) x[j] -= t * vbuf[j] * w;
+        }
+      }
+      const double nuv = nu[p];
+      if (nuv != 0.0) {
+        double xk = 0.0;
+#pragma unroll
+        for (int j = 0; j < RMAX; ++j)
+          if (j == k) xk = x[j];
+        double temp = fabs(xk) / nuv;
+        temp = (1.0 + temp) * (1.0 - temp);
+        temp = temp < 0.0 ? 0.0 : temp;
+        const double ratio = nuv / nd[p];
+        const double temp2 = temp * ratio * ratio;
+        if (temp2 <= sqrt_eps) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < RMAX; ++j)
+            if (j > k && j < r) acc += x[j] * x[j];
+          nd[p] = sqrt(acc);
+          nu[p] = nd[p];
+        } else {
+          nu[p] = nuv * sqrt(temp);
         }
       }
     }
@@ -450,7 +591,7 @@ __device__ inline SmallColPiv warp_colpiv_qr(double* G, int ldg, int n, double t
 template <int NT>
 __device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h, int max_swaps, int* I,
                                 double* W, int ldw, double* Gt, int ldg, int* perm, double* tau, double* nu,
-                                double* nd, double* rv, int64_t* ri, int* shared_flag) {
+                                double* nd, double* rv, int64_t* ri, int* shared_flag, double* vol_out = nullptr) {
   const int tid = threadIdx.x, warp = tid >> 5;
   // swap round 0 exactly as the reference: ColPivQR(G^T) and its solve for
   // every row. G^T(c, t) = A(I[t], c)
@@ -465,6 +606,14 @@ __device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h
   }
   __syncthreads();
   if (shared_flag[0]) return SLRA_ERR_SELECTION_FAILURE;
+  // |det A(I, :)| = prod |R_ii| of the round-0 QR (Q orthogonal), then times
+  // |B(piv, j)| per swap (the maxvol volume update): thread 0 keeps it, so the
+  // caller may overwrite A with B (W == A) and still get the volume proxy
+  double vol = 0.0;
+  if (vol_out && tid == 0) {
+    vol = 1.0;
+    for (int i = 0; i < r; ++i) vol *= fabs(Gt[i + i * ldg]);
+  }
   // W(i, t) holds B(i, perm[t]) (storage order of the solve)
   for (int i = tid; i < m; i += NT) {
     double* c = W + i;  // row i of W as a strided vector (stride ldw)
@@ -501,8 +650,10 @@ __device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h
       for (int t2 = 0; t2 < r; ++t2)
         best = argmax_merge(best, ArgMax{fabs(W[i + t2 * ldw]), (int64_t)perm[t2] * m + i});
     best = block_argmax<NT>(best, rv, ri);
-    if (best.v <= h) return SLRA_OK;
-    if (swap == max_swaps) return SLRA_OK;
+    if (best.v <= h || swap == max_swaps) {
+      if (vol_out && tid == 0) *vol_out = vol;
+      return SLRA_OK;
+    }
     const int j = (int)(best.i / m), piv = (int)(best.i % m);
     const int ts = iperm[j];
     // the pivot is read by every thread BEFORE the barrier: after it, the
@@ -510,7 +661,10 @@ __device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h
     const double p = W[piv + ts * ldw];
     for (int t2 = tid; t2 < r; t2 += NT) g[t2] = W[piv + t2 * ldw] - (t2 == ts ? 1.0 : 0.0);
     __syncthreads();
-    if (tid == 0) I[j] = piv;
+    if (tid == 0) {
+      I[j] = piv;
+      vol *= fabs(p);
+    }
     for (int i = tid; i < m; i += NT) {
       const double f = W[i + ts * ldw] / p;
       for (int t2 = 0; t2 < r; ++t2) W[i + t2 * ldw] -= f * g[t2];
@@ -831,21 +985,25 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
   }
 }
 
-template <int NT>
+// PMAX < 256: only the rows-per-lane variants up to PMAX / 8 are instantiated
+// (callers with a register budget, p <= PMAX guaranteed).
+template <int NT, int PMAX = 256>
 __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate = 0.0) {
   if (p <= 64) {
     const int rpg = (p + 7) / 8;
     const bool exact = p == 8 * rpg && n == p;
 #define SLRA_G8(R)                                                                   \
-  if (rpg == R) {                                                                    \
-    if (exact) cta_jacobi_g8<NT, R, true>(W, ldw, p, n, V, ldv, flag, deflate);      \
-    else cta_jacobi_g8<NT, R, false>(W, ldw, p, n, V, ldv, flag, deflate);           \
-    return;                                                                          \
+  if constexpr (R <= (PMAX + 7) / 8) {                                               \
+    if (rpg == R) {                                                                  \
+      if (exact) cta_jacobi_g8<NT, R, true>(W, ldw, p, n, V, ldv, flag, deflate);    \
+      else cta_jacobi_g8<NT, R, false>(W, ldw, p, n, V, ldv, flag, deflate);         \
+      return;                                                                        \
+    }                                                                                \
   }
     SLRA_G8(1) SLRA_G8(2) SLRA_G8(3) SLRA_G8(4) SLRA_G8(5) SLRA_G8(6) SLRA_G8(7) SLRA_G8(8)
 #undef SLRA_G8
   }
-  else cta_jacobi_t<NT, 8>(W, ldw, p, n, V, ldv, flag, deflate);  // p <= 256 (callers enforce)
+  else if constexpr (PMAX > 64) cta_jacobi_t<NT, 8>(W, ldw, p, n, V, ldv, flag, deflate);  // p <= 256 (callers enforce)
 }
 
 // Finish an SVD after cta_jacobi: sigma_j = ||w_j||, descending stable order

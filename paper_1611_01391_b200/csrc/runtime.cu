@@ -137,6 +137,13 @@ int slra_ctx_create(int device, void* stream, slra_ctx* out) {
     }
     c->owns_stream = true;
   }
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;  // keep freed blocks for reuse
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (cudaMalloc(&c->dsmall, 4096) != cudaSuccess || cudaMallocHost(&c->hsmall, 4096) != cudaSuccess) {
     delete c;
     return SLRA_ERR_CUDA;
@@ -219,16 +226,18 @@ int slra_ctx_timing_report(slra_ctx ctx, char* buf, int64_t len) {
   return SLRA_OK;
 }
 
+// Stream-ordered allocations from the device's default pool (release
+// threshold raised at context creation): the host layer's many short-lived
+// operands cost no cudaMalloc/cudaFree round trip and no device sync.
 int slra_device_alloc(slra_ctx ctx, int64_t bytes, void** d_out) {
-  (void)ctx;
-  if (!d_out || bytes < 0) return SLRA_ERR_INVALID_ARGUMENT;
-  SLRA_CUDA(cudaMalloc(d_out, bytes > 0 ? bytes : 8));
+  if (!ctx || !d_out || bytes < 0) return SLRA_ERR_INVALID_ARGUMENT;
+  SLRA_CUDA(cudaMallocAsync(d_out, bytes > 0 ? bytes : 8, C(ctx)->stream));
   return SLRA_OK;
 }
 
 int slra_device_free(slra_ctx ctx, void* p) {
-  (void)ctx;
-  if (p) SLRA_CUDA(cudaFree(p));
+  if (!ctx) return SLRA_ERR_INVALID_ARGUMENT;
+  if (p) SLRA_CUDA(cudaFreeAsync(p, C(ctx)->stream));
   return SLRA_OK;
 }
 

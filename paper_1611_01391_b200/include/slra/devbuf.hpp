@@ -23,10 +23,7 @@ class DevBuf {
   DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
-      if (p_) {
-        slra_ctx_synchronize(device_context());
-        slra_device_free(device_context(), p_);
-      }
+      if (p_) slra_device_free(device_context(), p_);
       p_ = o.p_;
       n_ = o.n_;
       o.p_ = nullptr;
@@ -34,10 +31,7 @@ class DevBuf {
     return *this;
   }
   ~DevBuf() {
-    if (p_) {
-      slra_ctx_synchronize(device_context());
-      slra_device_free(device_context(), p_);
-    }
+    if (p_) slra_device_free(device_context(), p_);  // stream-ordered: no sync
   }
   T* get() const { return p_; }
   size_t size() const { return n_; }

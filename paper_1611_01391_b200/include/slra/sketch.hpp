@@ -64,6 +64,9 @@ class SketchOperator {
   /// Y = op X (transpose: op^T X) on HBM-resident operands; Y preallocated
   /// (rows() or cols() x X.cols()). Default: the compiled plan.
   virtual void apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const;
+  /// Compiled plans, cached (operators are immutable): [0] left, [1] right,
+  /// [2] left plan of the transpose. Filled by compile_plan / apply_device.
+  mutable std::shared_ptr<const SketchPlan> plan_cache[3];
 };
 
 using OpPtr = std::shared_ptr<const SketchOperator>;

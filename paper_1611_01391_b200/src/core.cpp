@@ -121,10 +121,7 @@ DeviceMatrix& DeviceMatrix::operator=(DeviceMatrix&& o) noexcept {
 }
 
 DeviceMatrix::~DeviceMatrix() {
-  if (owns_ && p_) {
-    slra_ctx_synchronize(device_context());
-    slra_device_free(device_context(), p_);
-  }
+  if (owns_ && p_) slra_device_free(device_context(), p_);  // stream-ordered: no sync
 }
 
 Matrix DeviceMatrix::download() const {

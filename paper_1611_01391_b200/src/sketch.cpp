@@ -486,7 +486,15 @@ OpPtr gen_asph(Index n, int d, Rng& rng) {
 }
 
 // ---------------------------------------------------------------- plans
+static SketchPlan compile_plan_uncached(const SketchOperator& op, Side side);
+
 SketchPlan compile_plan(const SketchOperator& op, Side side) {
+  auto& slot = op.plan_cache[side == Side::Left ? 0 : 1];
+  if (!slot) slot = std::make_shared<const SketchPlan>(compile_plan_uncached(op, side));
+  return *slot;
+}
+
+static SketchPlan compile_plan_uncached(const SketchOperator& op, Side side) {
   const Index count = side == Side::Left ? op.rows() : op.cols();
   std::vector<RowExpr> rows;
   rows.reserve(static_cast<size_t>(count));
@@ -559,8 +567,11 @@ Matrix host_transpose(const Matrix& M) {  // data movement only
 
 void SketchOperator::apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const {
   if (transpose) {
-    TransposeView t(*this);
-    run_plan_device(compile_plan(t, Side::Left), X, true, Y);
+    if (!plan_cache[2]) {
+      TransposeView t(*this);
+      plan_cache[2] = std::make_shared<const SketchPlan>(compile_plan(t, Side::Left));
+    }
+    run_plan_device(*plan_cache[2], X, true, Y);
   } else {
     run_plan_device(compile_plan(*this, Side::Left), X, true, Y);
   }
