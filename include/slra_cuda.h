@@ -308,6 +308,14 @@ int slra_scale_rows_cols(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m
  * forward y_0 = x_0, y_i = x_i + b[i-1] y_{i-1}; backward y_{n-1} = x_{n-1},
  * y_i = x_i + b[i] y_{i+1}. Sequential per column in the reference's order
  * (bit-exact for b = +-1); Y may alias X. */
+/* AbridgedFourierOp (sketch.cpp:137-211) on a complex n x c operand held as
+ * real / imaginary planes (ld, ldo): d butterfly levels (transpose = 0:
+ * af_recurse, 1: af_recurse_transpose). d_twr / d_twi hold the twiddles
+ * exp(i 2 pi k / L) level after level (L = n >> s, k < L / 2), as the
+ * reference computes them on the host. 2^d must divide n. */
+int slra_af_apply(slra_ctx ctx, const double* d_re, const double* d_im, int64_t ld, int64_t n, int64_t c,
+                  int d, const double* d_twr, const double* d_twi, int transpose, double* d_ore,
+                  double* d_oim, int64_t ldo);
 int slra_bidiag_scan(slra_ctx ctx, const double* d_X, int64_t ldx, int64_t n, int64_t c,
                      const double* d_b, int forward, double* d_Y, int64_t ldy);
 /* B = A^T (n x m, ld ldb), 32 x 32 shared-memory tiles. */

@@ -206,6 +206,14 @@ struct OpCount {
 OpCount& op_counter();
 inline void reset_op_counter() { op_counter() = OpCount{}; }
 
+// Complex matrices as real and imaginary planes (Eigen::MatrixXcd, matrix.hpp:12);
+// element arithmetic goes through std::complex<double>.
+struct CMatrix {
+  Matrix re, im;
+  Index rows() const { return re.rows(); }
+  Index cols() const { return re.cols(); }
+};
+
 class SketchOperator {
  public:
   virtual ~SketchOperator() = default;
@@ -214,6 +222,12 @@ class SketchOperator {
   virtual std::string kind() const = 0;
   virtual Matrix apply(const Matrix& M) const = 0;
   virtual Matrix apply_transpose(const Matrix& M) const = 0;
+  // sketch.hpp:36-43, sketch.cpp:26-37: a real operator acts on both parts
+  virtual bool is_complex() const { return false; }
+  virtual CMatrix apply_complex(const CMatrix& M) const { return {apply(M.re), apply(M.im)}; }
+  virtual CMatrix apply_transpose_complex(const CMatrix& M) const {
+    return {apply_transpose(M.re), apply_transpose(M.im)};
+  }
 };
 using OpPtr = std::shared_ptr<const SketchOperator>;
 
@@ -238,6 +252,8 @@ OpPtr gen_aph(Index n, int d, Rng& rng);
 OpPtr gen_asph(Index n, int d, Rng& rng);
 Matrix apply(const SketchOperator& op, const Matrix& M, Side side);
 Matrix materialize(const SketchOperator& op, Index cap = 4096);
+OpPtr make_abridged_fourier(Index n, int d);                                   // sketch.cpp:137-211
+CMatrix materialize_complex(const SketchOperator& op, Index cap = 4096);      // sketch.cpp:690-693
 
 // ---------------------------------------------------------------- cur
 // cur.hpp:16-73

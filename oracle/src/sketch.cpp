@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <complex>
+
 #include "slra_oracle.hpp"
 
 namespace slra_oracle {
@@ -248,9 +250,126 @@ class ProductOp final : public SketchOperator {
     for (auto& op : ops_) out = op->apply_transpose(out);
     return out;
   }
+  bool is_complex() const override {  // sketch.cpp:511-512, 530-540
+    for (auto& o : ops_)
+      if (o->is_complex()) return true;
+    return false;
+  }
+  CMatrix apply_complex(const CMatrix& M) const override {
+    CMatrix out = M;
+    for (size_t i = ops_.size(); i-- > 0;) out = ops_[i]->apply_complex(out);
+    return out;
+  }
+  CMatrix apply_transpose_complex(const CMatrix& M) const override {
+    CMatrix out = M;
+    for (auto& op : ops_) out = op->apply_transpose_complex(out);
+    return out;
+  }
 
  private:
   std::vector<OpPtr> ops_;
+};
+
+// sketch.cpp:137-211: abridged Fourier, d radix-2 butterfly levels with
+// twiddles exp(i 2 pi k / L), outputs interleaved per level.
+using cd = std::complex<double>;
+using CRows = std::vector<std::vector<cd>>;  // rows x cols, row-major (rows move as units)
+
+void af_recurse(CRows& X, int depth) {
+  if (depth == 0) return;
+  const Index s = static_cast<Index>(X.size()) / 2, c = static_cast<Index>(X[0].size());
+  CRows u(static_cast<size_t>(s), std::vector<cd>(static_cast<size_t>(c)));
+  CRows w = u;
+  for (Index i = 0; i < s; ++i)
+    for (Index j = 0; j < c; ++j) {
+      u[i][j] = X[i][j] + X[i + s][j];
+      w[i][j] = X[i][j] - X[i + s][j];
+    }
+  const double theta = 2.0 * M_PI / static_cast<double>(2 * s);
+  for (Index i = 0; i < s; ++i) {
+    const cd t = std::exp(cd(0, theta * static_cast<double>(i)));
+    for (Index j = 0; j < c; ++j) w[i][j] *= t;
+  }
+  af_recurse(u, depth - 1);
+  af_recurse(w, depth - 1);
+  for (Index i = 0; i < s; ++i) {
+    X[2 * i] = u[i];
+    X[2 * i + 1] = w[i];
+  }
+}
+
+void af_recurse_transpose(CRows& X, int depth) {
+  if (depth == 0) return;
+  const Index s = static_cast<Index>(X.size()) / 2, c = static_cast<Index>(X[0].size());
+  CRows u(static_cast<size_t>(s)), w(static_cast<size_t>(s));
+  for (Index i = 0; i < s; ++i) {
+    u[i] = X[2 * i];
+    w[i] = X[2 * i + 1];
+  }
+  af_recurse_transpose(u, depth - 1);
+  af_recurse_transpose(w, depth - 1);
+  const double theta = 2.0 * M_PI / static_cast<double>(2 * s);
+  for (Index i = 0; i < s; ++i) {
+    const cd t = std::exp(cd(0, theta * static_cast<double>(i)));
+    for (Index j = 0; j < c; ++j) w[i][j] *= t;
+  }
+  for (Index i = 0; i < s; ++i)
+    for (Index j = 0; j < c; ++j) {
+      X[i][j] = u[i][j] + w[i][j];
+      X[i + s][j] = u[i][j] - w[i][j];
+    }
+}
+
+CRows to_rows(const CMatrix& M) {
+  CRows X(static_cast<size_t>(M.rows()), std::vector<cd>(static_cast<size_t>(M.cols())));
+  for (Index i = 0; i < M.rows(); ++i)
+    for (Index j = 0; j < M.cols(); ++j) X[i][j] = cd(M.re(i, j), M.im(i, j));
+  return X;
+}
+CMatrix from_rows(const CRows& X, Index cols) {
+  CMatrix M{Matrix(static_cast<Index>(X.size()), cols), Matrix(static_cast<Index>(X.size()), cols)};
+  for (Index i = 0; i < M.rows(); ++i)
+    for (Index j = 0; j < cols; ++j) {
+      M.re(i, j) = X[i][j].real();
+      M.im(i, j) = X[i][j].imag();
+    }
+  return M;
+}
+
+class AbridgedFourierOp final : public SketchOperator {
+ public:
+  AbridgedFourierOp(Index n, int d) : n_(n), d_(d) {
+    require(d >= 1, "abridged fourier: depth >= 1");
+    require(n % (Index(1) << d) == 0, "abridged fourier: 2^d must divide n");
+  }
+  Index rows() const override { return n_; }
+  Index cols() const override { return n_; }
+  std::string kind() const override { return "abridged_fourier"; }
+  bool is_complex() const override { return true; }
+  Matrix apply(const Matrix&) const override {
+    throw std::logic_error("abridged fourier is complex; use apply_complex");
+  }
+  Matrix apply_transpose(const Matrix&) const override {
+    throw std::logic_error("abridged fourier is complex; use apply_transpose_complex");
+  }
+  CMatrix apply_complex(const CMatrix& M) const override {
+    require(M.rows() == n_, "AF apply: dims");
+    if (M.cols() == 0) return M;
+    CRows X = to_rows(M);
+    af_recurse(X, d_);
+    return from_rows(X, M.cols());
+  }
+  CMatrix apply_transpose_complex(const CMatrix& M) const override {
+    require(M.rows() == n_, "AF apply: dims");
+    if (M.cols() == 0) return M;
+    CRows X = to_rows(M);
+    af_recurse_transpose(X, d_);
+    return from_rows(X, M.cols());
+  }
+
+ private:
+  Index n_;
+  int d_;
 };
 
 // sketch.cpp:545-583
@@ -446,6 +565,13 @@ Matrix apply(const SketchOperator& op, const Matrix& M, Side side) {
 Matrix materialize(const SketchOperator& op, Index cap) {
   require(op.rows() <= cap && op.cols() <= cap, "materialize: cap exceeded");
   return op.apply(Matrix::identity(op.cols(), op.cols()));
+}
+
+OpPtr make_abridged_fourier(Index n, int d) { return std::make_shared<AbridgedFourierOp>(n, d); }
+
+CMatrix materialize_complex(const SketchOperator& op, Index cap) {
+  require(op.rows() <= cap && op.cols() <= cap, "materialize: cap exceeded");
+  return op.apply_complex(CMatrix{Matrix::identity(op.cols(), op.cols()), Matrix(op.cols(), op.cols())});
 }
 
 }  // namespace slra_oracle

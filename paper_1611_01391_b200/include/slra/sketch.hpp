@@ -44,9 +44,24 @@ struct SketchPlan {
   std::vector<int32_t> q;     // count
 };
 
+/// Complex matrix (reference CMatrix = Eigen::MatrixXcd, matrix.hpp:12) as
+/// real and imaginary planes — the layout the device kernels use.
+struct CMatrix {
+  Matrix re, im;
+  Index rows() const { return re.rows(); }
+  Index cols() const { return re.cols(); }
+};
+
 class SketchOperator {
  public:
   virtual ~SketchOperator() = default;
+  /// sketch.hpp:36-43: complex operators (abridged Fourier) and the complex
+  /// application; a real operator acts on both planes (sketch.cpp:26-37).
+  virtual bool is_complex() const { return false; }
+  virtual CMatrix apply_complex(const CMatrix& M) const { return {apply(M.re), apply(M.im)}; }
+  virtual CMatrix apply_transpose_complex(const CMatrix& M) const {
+    return {apply_transpose(M.re), apply_transpose(M.im)};
+  }
   virtual Index rows() const = 0;
   virtual Index cols() const = 0;
   virtual std::string kind() const = 0;
@@ -91,6 +106,9 @@ OpPtr make_inverse_bidiagonal(Vector subdiag, bool lower = true);
 OpPtr make_householder_chain(std::vector<Vector> reflectors, std::vector<std::vector<Index>> perms);
 OpPtr gen_inverse_bidiagonal(Index n, Rng& rng);
 OpPtr gen_householder_chain(Index n, Index q, Rng& rng);
+/// sketch.cpp:137-211: complex abridged Fourier (apply_complex only).
+OpPtr make_abridged_fourier(Index n, int d);
+CMatrix materialize_complex(const SketchOperator& op, Index cap = 4096);
 
 OpPtr gen_permutation(Index n, Rng& rng);
 OpPtr gen_sign_diagonal(Index n, Rng& rng);

@@ -3,6 +3,7 @@
 // device pointers (e.g. torch tensor.data_ptr()) for HBM-resident runs.
 #include <chrono>
 
+#include <pybind11/complex.h>
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
@@ -398,6 +399,31 @@ PYBIND11_MODULE(_slra, m) {
         py::arg("subdiag"), py::arg("lower") = true);
   m.def("gen_inverse_bidiagonal", [](Index n, Rng& r) { return PyOp{gen_inverse_bidiagonal(n, r)}; });
   m.def("gen_householder_chain", [](Index n, Index q, Rng& r) { return PyOp{gen_householder_chain(n, q, r)}; });
+  m.def("make_abridged_fourier", [](Index n, int d) { return PyOp{make_abridged_fourier(n, d)}; });
+  using CArray = py::array_t<std::complex<double>, py::array::f_style | py::array::forcecast>;
+  auto cnp = [](const CMatrix& M) {
+    py::array_t<std::complex<double>, py::array::f_style> a({M.rows(), M.cols()});
+    auto* p = a.mutable_data();
+    for (Index j = 0; j < M.cols(); ++j)
+      for (Index i = 0; i < M.rows(); ++i) p[i + j * M.rows()] = {M.re(i, j), M.im(i, j)};
+    return a;
+  };
+  auto npc = [](const CArray& a) {
+    if (a.ndim() != 2) throw std::invalid_argument("expected a 2-D complex array");
+    CMatrix M{Matrix(a.shape(0), a.shape(1)), Matrix(a.shape(0), a.shape(1))};
+    const auto* p = a.data();
+    for (Index j = 0; j < M.cols(); ++j)
+      for (Index i = 0; i < M.rows(); ++i) {
+        M.re(i, j) = p[i + j * M.rows()].real();
+        M.im(i, j) = p[i + j * M.rows()].imag();
+      }
+    return M;
+  };
+  m.def("apply_complex", [=](const PyOp& op, const CArray& M) { return cnp(op.p->apply_complex(npc(M))); });
+  m.def("apply_transpose_complex", [=](const PyOp& op, const CArray& M) {
+    return cnp(op.p->apply_transpose_complex(npc(M)));
+  });
+  m.def("materialize_complex", [=](const PyOp& op) { return cnp(materialize_complex(*op.p)); });
   m.def("make_gaussian", [](const FArray& G) { return PyOp{make_gaussian(from_np(G))}; });
   m.def("gen_gaussian", [](Index a, Index b, Rng& r) { return PyOp{gen_gaussian(a, b, r)}; });
   m.def("gen_permutation", [](Index n, Rng& r) { return PyOp{gen_permutation(n, r)}; });

@@ -6,6 +6,7 @@
 #include "slra/sketch.hpp"
 
 #include <algorithm>
+#include <complex>
 #include <cmath>
 
 #include "slra/devbuf.hpp"
@@ -219,6 +220,21 @@ class ProductOp final : public SketchOperator {
       if (!o->plannable()) return false;
     return true;
   }
+  bool is_complex() const override {  // sketch.cpp:511-540
+    for (auto& o : ops_)
+      if (o->is_complex()) return true;
+    return false;
+  }
+  CMatrix apply_complex(const CMatrix& M) const override {
+    CMatrix out = M;
+    for (size_t i = ops_.size(); i-- > 0;) out = ops_[i]->apply_complex(out);
+    return out;
+  }
+  CMatrix apply_transpose_complex(const CMatrix& M) const override {
+    CMatrix out = M;
+    for (auto& o : ops_) out = o->apply_transpose_complex(out);
+    return out;
+  }
   // a chain holding a non-plan factor: factor by factor on the device, right
   // to left (the transpose left to right), as the reference applies it
   void apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const override {
@@ -386,9 +402,69 @@ class HouseholderChainOp final : public SketchOperator {
   Index n_ = 0;
 };
 
+// sketch.cpp:137-211: complex abridged Fourier (slra_af_apply). The twiddle
+// tables are the reference's exp(i theta k) with theta = 2 pi / (2 s) per
+// level, computed here on the host exactly as the reference computes them.
+class AbridgedFourierOp final : public SketchOperator {
+ public:
+  AbridgedFourierOp(Index n, int d) : n_(n), d_(d) {
+    require(d >= 1, "abridged fourier: depth >= 1");
+    require(n % (Index(1) << d) == 0, "abridged fourier: 2^d must divide n");
+    for (int lv = 0; lv < d; ++lv) {
+      const Index s = (n >> lv) / 2;
+      const double theta = 2.0 * 3.14159265358979323846 / static_cast<double>(2 * s);
+      for (Index i = 0; i < s; ++i) {
+        const std::complex<double> t = std::exp(std::complex<double>(0, theta * static_cast<double>(i)));
+        twr_.push_back(t.real());
+        twi_.push_back(t.imag());
+      }
+    }
+  }
+  Index rows() const override { return n_; }
+  Index cols() const override { return n_; }
+  std::string kind() const override { return "abridged_fourier"; }
+  bool is_complex() const override { return true; }
+  bool plannable() const override { return false; }
+  RowExpr row_of_apply(Index) const override { throw std::logic_error("abridged fourier is complex; use apply_complex"); }
+  RowExpr row_of_apply_transpose(Index) const override {
+    throw std::logic_error("abridged fourier is complex; use apply_transpose_complex");
+  }
+  void apply_device(const DeviceMatrix&, bool, DeviceMatrix&) const override {
+    throw std::logic_error("abridged fourier is complex; use apply_complex");
+  }
+  CMatrix apply_complex(const CMatrix& M) const override { return run(M, false); }
+  CMatrix apply_transpose_complex(const CMatrix& M) const override { return run(M, true); }
+
+ private:
+  CMatrix run(const CMatrix& M, bool transpose) const {
+    require(M.rows() == n_ && M.im.rows() == n_ && M.im.cols() == M.cols(), "AF apply: dims");
+    if (M.cols() == 0) return M;
+    if (!dtw_r_.get()) {
+      dtw_r_ = DevBuf<double>(twr_);
+      dtw_i_ = DevBuf<double>(twi_);
+    }
+    DeviceMatrix re = DeviceMatrix::upload(M.re), im = DeviceMatrix::upload(M.im);
+    DeviceMatrix ore(n_, M.cols()), oim(n_, M.cols());
+    check(slra_af_apply(device_context(), re.data(), im.data(), re.ld(), n_, M.cols(), d_, dtw_r_.get(),
+                        dtw_i_.get(), transpose ? 1 : 0, ore.data(), oim.data(), ore.ld()),
+          "abridged_fourier");
+    return CMatrix{ore.download(), oim.download()};
+  }
+  Index n_;
+  int d_;
+  std::vector<double> twr_, twi_;
+  mutable DevBuf<double> dtw_r_, dtw_i_;
+};
+
 }  // namespace
 
 // ---------------------------------------------------------------- factories
+OpPtr make_abridged_fourier(Index n, int d) { return std::make_shared<AbridgedFourierOp>(n, d); }
+
+CMatrix materialize_complex(const SketchOperator& op, Index cap) {  // sketch.cpp:690-693
+  require(op.rows() <= cap && op.cols() <= cap, "materialize: cap exceeded");
+  return op.apply_complex(CMatrix{Matrix::Identity(op.cols(), op.cols()), Matrix(op.cols(), op.cols())});
+}
 OpPtr make_inverse_bidiagonal(Vector subdiag, bool lower) {
   return std::make_shared<InverseBidiagonalOp>(std::move(subdiag), lower);
 }

@@ -95,3 +95,44 @@ def test_sketch_solve_through_non_plan_operators(slra, oracle):
     rep = slra.sketch_solve(A, b, Fb, False)
     ref = oracle.sketch_solve(A, b, Fbo, False)
     assert np.linalg.norm(rep["x_hat"] - ref["x_hat"]) <= 1e-9 * np.linalg.norm(ref["x_hat"])
+
+
+def test_abridged_fourier_displays(slra):  # test_sketch.cpp:50-80
+    F = slra.materialize_complex(slra.make_abridged_fourier(4, 2))
+    E = np.array([[1, 1, 1, 1], [1, 1j, -1, -1j], [1, -1, 1, -1], [1, -1j, -1, 1j]])
+    assert np.linalg.norm(F - E) < 1e-14
+    a = np.arange(8)
+    F8 = slra.materialize_complex(slra.make_abridged_fourier(8, 3))
+    assert np.abs(F8 - np.exp(2j * np.pi * np.outer(a, a) / 8)).max() < 1e-13
+    A = slra.materialize_complex(slra.make_abridged_fourier(8, 2))
+    assert np.linalg.norm(A @ A.conj().T - 4 * np.eye(8)) < 1e-12
+    assert all((np.abs(A[r]) > 1e-14).sum() == 4 for r in range(8))
+    X = slra.Rng(5).gaussian_matrix(8, 3).astype(complex)
+    op = slra.make_abridged_fourier(8, 2)
+    assert np.linalg.norm(slra.apply_transpose_complex(op, X) - A.T @ X) < 1e-12
+    with pytest.raises(RuntimeError):
+        op.apply(np.eye(8))  # complex operator: real application refused (std::logic_error)
+
+
+@pytest.mark.parametrize("n,d,c", [(8, 2, 3), (64, 6, 5), (4096, 3, 7), (1024, 10, 2), (96, 5, 4)])
+def test_abridged_fourier_bit_exact(slra, oracle, n, d, c):
+    rng = oracle.Rng(n + d)
+    X = rng.gaussian_matrix(n, c) + 1j * rng.gaussian_matrix(n, c)
+    op, oo = slra.make_abridged_fourier(n, d), oracle.make_abridged_fourier(n, d)
+    assert np.array_equal(slra.apply_complex(op, X), oracle.apply_complex(oo, X))
+    assert np.array_equal(slra.apply_transpose_complex(op, X), oracle.apply_transpose_complex(oo, X))
+
+
+def test_complex_products(slra, oracle):
+    """A real operator acts on both planes; products chain complex factors
+    (sketch.cpp:26-37, 511-540)."""
+    n = 256
+    rp, ro = slra.Rng(3), oracle.Rng(3)
+    sp, so = rp.distinct_indices(32, n), ro.distinct_indices(32, n)
+    Fp = slra.make_product([slra.make_sub_identity(sp, n), slra.make_abridged_fourier(n, 3), slra.gen_sign_diagonal(n, rp)])
+    Fo = oracle.make_product([oracle.make_sub_identity(so, n), oracle.make_abridged_fourier(n, 3),
+                              oracle.gen_sign_diagonal(n, ro)])
+    X = oracle.Rng(4).gaussian_matrix(n, 3) + 0j
+    assert np.array_equal(slra.apply_complex(Fp, X), oracle.apply_complex(Fo, X))
+    Y = oracle.Rng(5).gaussian_matrix(32, 2) + 1j * oracle.Rng(6).gaussian_matrix(32, 2)
+    assert np.array_equal(slra.apply_transpose_complex(Fp, Y), oracle.apply_transpose_complex(Fo, Y))

@@ -786,3 +786,18 @@ def test_householder_chain_orthogonal(oracle):
     assert np.linalg.norm(R @ R.T - np.eye(16)) < 1e-12
     X = rng.gaussian_matrix(16, 3)
     assert np.linalg.norm(op.apply_transpose(X) - R.T @ X) < 1e-12
+
+
+def test_abridged_fourier_displays(oracle):  # test_sketch.cpp:50-80
+    F = oracle.materialize_complex(oracle.make_abridged_fourier(4, 2))
+    E = np.array([[1, 1, 1, 1], [1, 1j, -1, -1j], [1, -1, 1, -1], [1, -1j, -1, 1j]])
+    assert np.linalg.norm(F - E) < 1e-14
+    a = np.arange(8)
+    F8 = oracle.materialize_complex(oracle.make_abridged_fourier(8, 3))
+    assert np.abs(F8 - np.exp(2j * np.pi * np.outer(a, a) / 8)).max() < 1e-13
+    A = oracle.materialize_complex(oracle.make_abridged_fourier(8, 2))
+    assert np.linalg.norm(A @ A.conj().T - 4 * np.eye(8)) < 1e-12
+    assert all((np.abs(A[r]) > 1e-14).sum() == 4 for r in range(8))
+    X = oracle.Rng(5).gaussian_matrix(8, 3).astype(complex)
+    op = oracle.make_abridged_fourier(8, 2)
+    assert np.linalg.norm(oracle.apply_transpose_complex(op, X) - A.T @ X) < 1e-12
