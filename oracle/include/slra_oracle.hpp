@@ -274,6 +274,10 @@ struct CaTrace {
 Matrix cur_reconstruct(const Matrix& M, const CurDecomposition& c);
 double cur_evaluate(const Matrix& M, const CurDecomposition& c, NormKind norm);
 double t_factor(Index q, Index s, double h);
+enum class CurSelector { Deterministic, Sampled };
+CurDecomposition cynical_cur(const EntryOracle& M, Index p, Index q, Index k, Index l, Index r, Rng& rng);
+CurDecomposition top_svd_to_cur(const Svd& f, Index k, Index l, double h, CurSelector selector, Rng& rng);
+double condition_number(const Matrix& A, double rank_tol = 1e-10);
 IndexSet maxvol_rows(const Matrix& A, double h = 1.1, Index max_swaps = 0);
 IndexSet select_rows_spanning(const Matrix& A, Index count, double h = 1.1);
 CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r);
@@ -338,6 +342,8 @@ CurDecomposition cur_via_leverage(const EntryOracle& M, Index r, Index k, Index 
                                   SampleMode mode, const std::optional<LeverageScores>& scores, Rng& rng,
                                   bool plain_nucleus = false);
 Svd lra_to_top_svd(const LowRankFactors& f, Index r);
+Svd lra_to_top_svd(const Matrix& A, const Matrix& W, const Matrix& B, Index r);
+std::pair<double, double> deterministic_error_diagnostic(const Matrix& M, const SketchOperator& H, Index r);
 CurDecomposition refine_lra(const EntryOracle& M, const LowRankFactors& crude, Index r, Index k, Index l, Rng& rng);
 LeverageScores uniform_scores(Index n);
 double gaussian_score_gap(const Matrix& G);

@@ -216,6 +216,32 @@ PYBIND11_MODULE(_oracle, m) {
     return cur_evaluate(M, c, k);
   }, py::arg("A"), py::arg("I"), py::arg("J"), py::arg("U"), py::arg("norm") = "frobenius");
 
+  // ---- remaining CUR / LRA entry points (cur.cpp:170-323, linalg.cpp:153-161, lra.cpp:65-86)
+  m.def("condition_number", [](const FArray& A, double tol) { return condition_number(from_np(A), tol); },
+        py::arg("A"), py::arg("rank_tol") = 1e-10);
+  m.def("truncate_rank", [](const FArray& A, Index rho) {
+    LowRankFactors f = truncate_rank(from_np(A), rho);
+    return py::make_tuple(to_np(f.U), to_np(f.V));
+  });
+  m.def("cynical_cur", [](const FArray& A, Index p, Index q, Index k, Index l, Index r, Rng& rng) {
+    Matrix M = from_np(A);
+    DenseOracle o(M);
+    return cur_dict(cynical_cur(o, p, q, k, l, r, rng));
+  });
+  m.def("top_svd_to_cur", [](const FArray& S, const FArray& sigma, const FArray& T, Index k, Index l, double h,
+                             const std::string& sel, Rng& rng) {
+    Svd f{from_np(S), np_vec(sigma), from_np(T)};
+    return cur_dict(top_svd_to_cur(f, k, l, h, sel == "sampled" ? CurSelector::Sampled : CurSelector::Deterministic, rng));
+  });
+  m.def("lra_to_top_svd3", [](const FArray& A, const FArray& W, const FArray& B, Index r) {
+    Svd t = lra_to_top_svd(from_np(A), from_np(W), from_np(B), r);
+    return py::make_tuple(to_np(t.S), vec_np(t.sigma), to_np(t.T));
+  });
+  m.def("deterministic_error_diagnostic", [](const FArray& M, const PyOp& H, Index r) {
+    auto [b, a] = deterministic_error_diagnostic(from_np(M), *H.p, r);
+    return py::make_tuple(b, a);
+  });
+
   // ---- sketch operators
   py::class_<PyOp>(m, "SketchOperator", py::module_local())
       .def("rows", [](const PyOp& o) { return o.p->rows(); })

@@ -31,6 +31,16 @@ double cur_evaluate(const Matrix& M, const CurDecomposition& c, NormKind norm);
 double cur_evaluate(const EntryOracle& M, const CurDecomposition& c, NormKind norm);
 
 double t_factor(Index q, Index s, double h);
+
+/// cur.cpp:170-188: maxvol selections inside the top-r factors of a random
+/// p x q sub-block, then primitive_cur on M.
+CurDecomposition cynical_cur(const EntryOracle& M, Index p, Index q, Index k, Index l, Index r, Rng& rng);
+/// cur.cpp:257-272: top-r SVD of A W B through two thin QRs.
+Svd lra_to_top_svd(const Matrix& A, const Matrix& W, const Matrix& B, Index r);
+enum class CurSelector { Deterministic, Sampled };
+/// cur.cpp:278-323: index sets from the singular factors (maxvol or
+/// norm-square sampling), nucleus pinv(T_J^T) Sigma^-1 pinv(S_I).
+CurDecomposition top_svd_to_cur(const Svd& f, Index k, Index l, double h, CurSelector selector, Rng& rng);
 IndexSet maxvol_rows(const Matrix& A, double h = 1.1, Index max_swaps = 0);
 IndexSet select_rows_spanning(const Matrix& A, Index count, double h = 1.1);
 

@@ -344,10 +344,44 @@ PYBIND11_MODULE(_slra, m) {
   }, py::arg("A"), py::arg("r"), py::arg("k"), py::arg("l"), py::arg("init_rows"), py::arg("loops"), py::arg("h"),
      py::arg("rng"), py::arg("stop_tol") = py::none());
   m.def("cur_evaluate", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
-                           const FArray& U) {
+                           const FArray& U, const std::string& norm) {
     Matrix M = from_np(A);
     CurDecomposition c{mkset(I, M.rows()), mkset(J, M.cols()), from_np(U), 0, false};
-    return cur_evaluate(M, c, NormKind::Frobenius);
+    return cur_evaluate(M, c, norm_kind(norm));
+  }, py::arg("A"), py::arg("I"), py::arg("J"), py::arg("U"), py::arg("norm") = "frobenius");
+  // ---- remaining CUR / LRA entry points (cur.cpp:170-323, linalg.cpp:100-161, lra.cpp:65-127)
+  m.def("condition_number", [](const FArray& A, double tol) { return condition_number(from_np(A), tol); },
+        py::arg("A"), py::arg("rank_tol") = 1e-10);
+  m.def("truncate_rank", [](const FArray& A, Index rho) {
+    LowRankFactors f = truncate_rank(from_np(A), rho);
+    return py::make_tuple(to_np(f.U), to_np(f.V));
+  });
+  m.def("cynical_cur", [](const FArray& A, Index p, Index q, Index k, Index l, Index r, Rng& rng) {
+    Matrix M = from_np(A);
+    DenseOracle o(M);
+    return cur_dict(cynical_cur(o, p, q, k, l, r, rng));
+  });
+  m.def("top_svd_to_cur", [](const FArray& S, const FArray& sigma, const FArray& T, Index k, Index l, double h,
+                             const std::string& sel, Rng& rng) {
+    Svd f{from_np(S), np_vec(sigma), from_np(T)};
+    return cur_dict(top_svd_to_cur(f, k, l, h, sel == "sampled" ? CurSelector::Sampled : CurSelector::Deterministic, rng));
+  });
+  m.def("lra_to_top_svd3", [](const FArray& A, const FArray& W, const FArray& B, Index r) {
+    Svd t = lra_to_top_svd(from_np(A), from_np(W), from_np(B), r);
+    return py::make_tuple(to_np(t.S), vec_np(t.sigma), to_np(t.T));
+  });
+  m.def("posterior_error_estimate", [](const FArray& M, const FArray& U, const FArray& V, Index q, Index s, Rng& rng) {
+    Matrix A = from_np(M);
+    DenseOracle o(A);
+    LowRankFactors f;
+    f.U = from_np(U);
+    f.V = from_np(V);
+    LraErrorEstimate e = posterior_error_estimate(o, f, q, s, rng);
+    return py::make_tuple(e.estimate_frobenius, e.ci_lo, e.ci_hi, e.has_interval);
+  });
+  m.def("deterministic_error_diagnostic", [](const FArray& M, const PyOp& H, Index r) {
+    auto [b, a] = deterministic_error_diagnostic(from_np(M), *H.p, r);
+    return py::make_tuple(b, a);
   });
   m.def("cur_evaluate_factored", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
                                     const FArray& T, const FArray& S) {

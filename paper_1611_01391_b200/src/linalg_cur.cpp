@@ -273,10 +273,26 @@ std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r,
 }
 
 double cur_evaluate(const EntryOracle& M, const CurDecomposition& c, NormKind norm) {  // cur.cpp:80-82
-  if (norm != NormKind::Frobenius)
-    throw std::invalid_argument("cur_evaluate: only the Frobenius norm is on the device path");
   const DeviceMatrix& dA = M.device();
   DevBuf<int64_t> dI(to64(c.row_set)), dJ(to64(c.col_set));
+  if (norm != NormKind::Frobenius) {
+    // E = M - (C U) R formed on the device (cur.cpp:76-82), then its
+    // spectral (SVD) or Chebyshev (max |e_ij|) norm
+    slra_ctx cx = device_context();
+    const Index m = M.rows(), n = M.cols(), k = c.row_set.size(), l = c.col_set.size();
+    DeviceMatrix Cm(m, l), R(k, n), P(m, k), E(m, n), dU = DeviceMatrix::upload(c.nucleus);
+    check(slra_gather_cols(cx, dA.data(), dA.ld(), m, n, dJ.get(), l, Cm.data(), Cm.ld()), "cur_evaluate");
+    check(slra_gather_rows(cx, dA.data(), dA.ld(), m, n, dI.get(), k, R.data(), R.ld()), "cur_evaluate");
+    check(slra_gemm(cx, 0, 0, m, k, l, 1.0, Cm.data(), Cm.ld(), dU.data(), dU.ld(), 0.0, P.data(), P.ld()),
+          "cur_evaluate");
+    check(slra_scale_rows_cols(cx, dA.data(), dA.ld(), m, n, nullptr, nullptr, E.data(), E.ld()), "cur_evaluate");
+    check(slra_gemm(cx, 0, 0, m, n, k, -1.0, P.data(), P.ld(), R.data(), R.ld(), 1.0, E.data(), E.ld()),
+          "cur_evaluate");
+    M.count(static_cast<unsigned long long>(m * n + m * l + k * n));
+    double v = 0.0;
+    check(slra_matrix_norm(cx, E.data(), E.ld(), m, n, norm == NormKind::Spectral ? 0 : 2, &v), "cur_evaluate");
+    return v;
+  }
   if (c.r > 0 && c.tsig.cols() == c.r && c.sr.cols() == c.r) {
     // factored nucleus: the pass over M runs at inner dimension r
     DeviceMatrix dT = DeviceMatrix::upload(c.tsig), dS = DeviceMatrix::upload(c.sr);
