@@ -318,6 +318,10 @@ int slra_af_apply(slra_ctx ctx, const double* d_re, const double* d_im, int64_t 
                   double* d_oim, int64_t ldo);
 int slra_bidiag_scan(slra_ctx ctx, const double* d_X, int64_t ldx, int64_t n, int64_t c,
                      const double* d_b, int forward, double* d_Y, int64_t ldy);
+/* Y = alpha X + beta Y, one rounding per entry (SumOp accumulation,
+ * sketch.cpp:469-475). beta = 0 ignores Y's previous contents. */
+int slra_axpby(slra_ctx ctx, double alpha, const double* d_X, int64_t ldx, double beta, double* d_Y,
+               int64_t ldy, int64_t m, int64_t n);
 /* B = A^T (n x m, ld ldb), 32 x 32 shared-memory tiles. */
 int slra_transpose(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, double* d_B,
                    int64_t ldb);

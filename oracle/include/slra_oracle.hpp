@@ -242,6 +242,12 @@ OpPtr gen_inverse_bidiagonal(Index n, Rng& rng);
 OpPtr gen_householder_chain(Index n, Index q, Rng& rng);
 OpPtr make_sub_identity(IndexSet selected, Index total);
 OpPtr make_product(std::vector<OpPtr> ops);
+OpPtr make_sum(std::vector<OpPtr> ops, std::vector<int> signs);                 // sketch.cpp:446-500
+OpPtr gen_scaled_diagonal(Index n, Rng& rng);                                   // :640-645
+Matrix bidiagonal_factor(Index n, const std::vector<int>& signs);               // :697-703
+Matrix gen_bidiagonal_product(Index n, Index T, Rng& rng, bool standardize = true);  // :740-758
+Vector bidiagonal_product_column(Index n, Index T, Index j, Rng& rng);           // :760-766
+std::pair<double, bool> ks_normality(const std::vector<double>& sample);         // :768-791
 OpPtr take_columns(OpPtr op, IndexSet columns);
 OpPtr take_columns(OpPtr op, Index l, ColumnMode mode, Rng& rng);
 OpPtr gen_permutation(Index n, Rng& rng);
@@ -249,7 +255,7 @@ OpPtr gen_sign_diagonal(Index n, Rng& rng);
 OpPtr gen_sparse_circulant(Index n, Index s, Rng& rng);
 OpPtr gen_gaussian(Index rows, Index cols, Rng& rng);
 OpPtr gen_aph(Index n, int d, Rng& rng);
-OpPtr gen_asph(Index n, int d, Rng& rng);
+OpPtr gen_asph(Index n, int d, Rng& rng, bool scaled_diag = false);
 Matrix apply(const SketchOperator& op, const Matrix& M, Side side);
 Matrix materialize(const SketchOperator& op, Index cap = 4096);
 OpPtr make_abridged_fourier(Index n, int d);                                   // sketch.cpp:137-211

@@ -285,6 +285,17 @@ PYBIND11_MODULE(_oracle, m) {
     return cnp(op.p->apply_transpose_complex(npc(M)));
   });
   m.def("materialize_complex", [=](const PyOp& op) { return cnp(materialize_complex(*op.p)); });
+  m.def("make_sum", [](const std::vector<PyOp>& ops, const std::vector<int>& signs) {
+    std::vector<OpPtr> v;
+    for (auto& o : ops) v.push_back(o.p);
+    return PyOp{make_sum(std::move(v), signs)};
+  });
+  m.def("gen_scaled_diagonal", [](Index n, Rng& r) { return PyOp{gen_scaled_diagonal(n, r)}; });
+  m.def("bidiagonal_factor", [](Index n, const std::vector<int>& s) { return to_np(bidiagonal_factor(n, s)); });
+  m.def("gen_bidiagonal_product", [](Index n, Index T, Rng& r, bool st) { return to_np(gen_bidiagonal_product(n, T, r, st)); },
+        py::arg("n"), py::arg("T"), py::arg("rng"), py::arg("standardize") = true);
+  m.def("bidiagonal_product_column", [](Index n, Index T, Index j, Rng& r) { return vec_np(bidiagonal_product_column(n, T, j, r)); });
+  m.def("ks_normality", [](const std::vector<double>& x) { return ks_normality(x); });
   m.def("make_gaussian", [](const FArray& G) { return PyOp{make_gaussian(from_np(G))}; });
   m.def("make_sub_identity", [](const std::vector<Index>& sel, Index total) {
     return PyOp{make_sub_identity(mkset(sel, total), total)};
@@ -305,7 +316,8 @@ PYBIND11_MODULE(_oracle, m) {
   m.def("gen_sparse_circulant", [](Index n, Index s, Rng& r) { return PyOp{gen_sparse_circulant(n, s, r)}; });
   m.def("gen_gaussian", [](Index a, Index b, Rng& r) { return PyOp{gen_gaussian(a, b, r)}; });
   m.def("gen_aph", [](Index n, int d, Rng& r) { return PyOp{gen_aph(n, d, r)}; });
-  m.def("gen_asph", [](Index n, int d, Rng& r) { return PyOp{gen_asph(n, d, r)}; });
+  m.def("gen_asph", [](Index n, int d, Rng& r, bool scaled) { return PyOp{gen_asph(n, d, r, scaled)}; },
+        py::arg("n"), py::arg("d"), py::arg("rng"), py::arg("scaled_diag") = false);
   m.def("apply", [](const PyOp& op, const FArray& M, const std::string& side) {
     return to_np(apply(*op.p, from_np(M), side == "right" ? Side::Right : Side::Left));
   });

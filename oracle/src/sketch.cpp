@@ -517,6 +517,163 @@ OpPtr gen_householder_chain(Index n, Index q, Rng& rng) {  // sketch.cpp:657-665
   return make_householder_chain(std::move(w), std::move(perms));
 }
 
+// sketch.cpp:446-500: signed sum of equally-shaped operators
+class SumOp final : public SketchOperator {
+ public:
+  SumOp(std::vector<OpPtr> ops, std::vector<int> signs) : ops_(std::move(ops)), signs_(std::move(signs)) {
+    require(!ops_.empty() && ops_.size() == signs_.size(), "sum: size mismatch");
+    for (auto& op : ops_)
+      require(op->rows() == ops_[0]->rows() && op->cols() == ops_[0]->cols(), "sum: dimension mismatch");
+    for (int s : signs_) require(s == 1 || s == -1, "sum: signs must be +-1");
+  }
+  Index rows() const override { return ops_[0]->rows(); }
+  Index cols() const override { return ops_[0]->cols(); }
+  std::string kind() const override { return "sum"; }
+  bool is_complex() const override {
+    for (auto& o : ops_)
+      if (o->is_complex()) return true;
+    return false;
+  }
+  Matrix apply(const Matrix& M) const override { return run([&](const OpPtr& o) { return o->apply(M); }); }
+  Matrix apply_transpose(const Matrix& M) const override {
+    return run([&](const OpPtr& o) { return o->apply_transpose(M); });
+  }
+  CMatrix apply_complex(const CMatrix& M) const override {
+    CMatrix out;
+    for (size_t i = 0; i < ops_.size(); ++i) {
+      CMatrix y = ops_[i]->apply_complex(M);
+      acc(out.re, y.re, i);
+      acc(out.im, y.im, i);
+    }
+    return out;
+  }
+  CMatrix apply_transpose_complex(const CMatrix& M) const override {
+    CMatrix out;
+    for (size_t i = 0; i < ops_.size(); ++i) {
+      CMatrix y = ops_[i]->apply_transpose_complex(M);
+      acc(out.re, y.re, i);
+      acc(out.im, y.im, i);
+    }
+    return out;
+  }
+
+ private:
+  // out = s_0 Y_0, then out += s_i Y_i
+  void acc(Matrix& out, const Matrix& y, size_t i) const {
+    const double s = static_cast<double>(signs_[i]);
+    if (i == 0) {
+      out = Matrix(y.rows(), y.cols());
+      for (Index e = 0; e < y.size(); ++e) out.v[static_cast<size_t>(e)] = s * y.v[static_cast<size_t>(e)];
+    } else {
+      for (Index e = 0; e < y.size(); ++e) out.v[static_cast<size_t>(e)] += s * y.v[static_cast<size_t>(e)];
+    }
+  }
+  template <class F>
+  Matrix run(F&& f) const {
+    Matrix out;
+    for (size_t i = 0; i < ops_.size(); ++i) acc(out, f(ops_[i]), i);
+    return out;
+  }
+  std::vector<OpPtr> ops_;
+  std::vector<int> signs_;
+};
+
+OpPtr make_sum(std::vector<OpPtr> ops, std::vector<int> signs) {
+  return std::make_shared<SumOp>(std::move(ops), std::move(signs));
+}
+OpPtr gen_scaled_diagonal(Index n, Rng& rng) {  // sketch.cpp:640-645
+  Vector d(static_cast<size_t>(n));
+  for (Index i = 0; i < n; ++i)
+    d[static_cast<size_t>(i)] = static_cast<double>(rng.sign()) * static_cast<double>(1 + rng.uniform_index(4));
+  return make_sign_diagonal(std::move(d));
+}
+
+// sketch.cpp:695-791: bidiagonal-product pseudo-Gaussian generator and the KS check
+Matrix bidiagonal_factor(Index n, const std::vector<int>& signs) {
+  require(static_cast<Index>(signs.size()) == n, "bidiagonal_factor: need n signs");
+  Matrix B = Matrix::identity(n, n);
+  B(0, n - 1) = signs[0];
+  for (Index i = 1; i < n; ++i) B(i, i - 1) = signs[static_cast<size_t>(i)];
+  return B;
+}
+namespace {
+struct BidiagFactor {
+  std::vector<int> signs;
+  std::vector<Index> colperm;
+};
+std::vector<BidiagFactor> draw_factors(Index n, Index T, Rng& rng) {
+  std::vector<BidiagFactor> fs;
+  for (Index t = 0; t < T; ++t) {
+    BidiagFactor f;
+    f.signs.resize(static_cast<size_t>(n));
+    for (Index i = 0; i < n; ++i) f.signs[static_cast<size_t>(i)] = rng.sign();
+    f.colperm = rng.permutation(n);
+    fs.push_back(std::move(f));
+  }
+  return fs;
+}
+Vector factor_times(const BidiagFactor& f, const Vector& x) {
+  const Index n = static_cast<Index>(x.size());
+  Vector p(static_cast<size_t>(n)), y(static_cast<size_t>(n));
+  for (Index i = 0; i < n; ++i) p[static_cast<size_t>(i)] = x[static_cast<size_t>(f.colperm[static_cast<size_t>(i)])];
+  y[0] = p[0] + f.signs[0] * p[static_cast<size_t>(n - 1)];
+  for (Index i = 1; i < n; ++i)
+    y[static_cast<size_t>(i)] = p[static_cast<size_t>(i)] + f.signs[static_cast<size_t>(i)] * p[static_cast<size_t>(i - 1)];
+  return y;
+}
+}  // namespace
+Matrix gen_bidiagonal_product(Index n, Index T, Rng& rng, bool standardize) {
+  auto fs = draw_factors(n, T, rng);
+  Matrix G(n, n);
+  for (Index j = 0; j < n; ++j) {
+    Vector v(static_cast<size_t>(n), 0.0);
+    v[static_cast<size_t>(j)] = 1.0;
+    for (Index t = T; t-- > 0;) v = factor_times(fs[static_cast<size_t>(t)], v);
+    for (Index i = 0; i < n; ++i) G(i, j) = v[static_cast<size_t>(i)];
+  }
+  if (standardize && T > 0) {
+    for (Index j = 0; j < n; ++j) {
+      double mean = 0;
+      for (Index i = 0; i < n; ++i) mean += G(i, j);
+      mean /= static_cast<double>(n);
+      double var = 0;
+      for (Index i = 0; i < n; ++i) var += (G(i, j) - mean) * (G(i, j) - mean);
+      var /= static_cast<double>(n);
+      if (var > 0)
+        for (Index i = 0; i < n; ++i) G(i, j) = (G(i, j) - mean) / std::sqrt(var);
+    }
+  }
+  return G;
+}
+Vector bidiagonal_product_column(Index n, Index T, Index j, Rng& rng) {
+  auto fs = draw_factors(n, T, rng);
+  Vector v(static_cast<size_t>(n), 0.0);
+  v[static_cast<size_t>(j)] = 1.0;
+  for (Index t = T; t-- > 0;) v = factor_times(fs[static_cast<size_t>(t)], v);
+  return v;
+}
+std::pair<double, bool> ks_normality(const std::vector<double>& sample) {
+  require(sample.size() >= 30, "ks_normality: need at least 30 samples");
+  const auto n = sample.size();
+  double mean = 0;
+  for (double x : sample) mean += x;
+  mean /= static_cast<double>(n);
+  double var = 0;
+  for (double x : sample) var += (x - mean) * (x - mean);
+  var /= static_cast<double>(n);
+  if (var <= 0) throw std::invalid_argument("ks_normality: degenerate sample");
+  std::vector<double> z(sample);
+  for (double& x : z) x = (x - mean) / std::sqrt(var);
+  std::sort(z.begin(), z.end());
+  double d = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const double cdf = 0.5 * std::erfc(-z[i] / 1.4142135623730951);
+    d = std::max(d, std::abs(cdf - static_cast<double>(i + 1) / static_cast<double>(n)));
+    d = std::max(d, std::abs(cdf - static_cast<double>(i) / static_cast<double>(n)));
+  }
+  return {d, d < 1.36 / std::sqrt(static_cast<double>(n))};
+}
+
 OpPtr make_gaussian(Matrix G) { return std::make_shared<GaussianOp>(std::move(G)); }
 OpPtr make_sub_identity(IndexSet selected, Index total) {
   return std::make_shared<SubIdentityOp>(std::move(selected), total);
@@ -552,8 +709,8 @@ OpPtr gen_gaussian(Index rows, Index cols, Rng& rng) { return make_gaussian(rng.
 OpPtr gen_aph(Index n, int d, Rng& rng) {
   return make_product({gen_permutation(n, rng), make_abridged_hadamard(n, d)});
 }
-OpPtr gen_asph(Index n, int d, Rng& rng) {
-  OpPtr diag = gen_sign_diagonal(n, rng);
+OpPtr gen_asph(Index n, int d, Rng& rng, bool scaled_diag) {  // sketch.cpp:672-675
+  OpPtr diag = scaled_diag ? gen_scaled_diagonal(n, rng) : gen_sign_diagonal(n, rng);
   return make_product({gen_permutation(n, rng), std::move(diag), make_abridged_hadamard(n, d)});
 }
 

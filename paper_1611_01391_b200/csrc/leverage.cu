@@ -140,3 +140,30 @@ extern "C" int slra_bidiag_scan(slra_ctx ctx, const double* X, int64_t ldx, int6
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
 }
+
+// Y = alpha X + beta Y (one rounding per entry: fma(alpha, x, beta y)); the
+// signed accumulation of SumOp (sketch.cpp:469-475) with alpha = +-1, beta = 1.
+namespace slra_dev {
+namespace {
+__global__ void axpby_kernel(double alpha, const double* __restrict__ X, int64_t ldx, double beta,
+                             double* __restrict__ Y, int64_t ldy, int64_t m, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    const double y = beta == 0.0 ? 0.0 : beta * Y[i + j * ldy];
+    Y[i + j * ldy] = fma(alpha, X[i + j * ldx], y);
+  }
+}
+}  // namespace
+}  // namespace slra_dev
+
+extern "C" int slra_axpby(slra_ctx ctx, double alpha, const double* X, int64_t ldx, double beta, double* Y,
+                          int64_t ldy, int64_t m, int64_t n) {
+  if (!ctx || m < 0 || n < 0 || ldx < m || ldy < m) return SLRA_ERR_INVALID_ARGUMENT;
+  if (m == 0 || n == 0) return SLRA_OK;
+  slra_dev::Context* cx = slra_dev::C(ctx);
+  int64_t g = slra_dev::ceil_div(m * n, 256);
+  if (g > cx->num_sms * 8) g = cx->num_sms * 8;
+  SLRA_TIMED(cx, "sketch", slra_dev::axpby_kernel<<<(unsigned)g, 256, 0, cx->stream>>>(alpha, X, ldx, beta, Y, ldy, m, n);)
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}

@@ -114,7 +114,11 @@ OpPtr gen_permutation(Index n, Rng& rng);
 OpPtr gen_sign_diagonal(Index n, Rng& rng);
 OpPtr gen_sparse_circulant(Index n, Index s, Rng& rng);
 OpPtr gen_aph(Index n, int d, Rng& rng);
-OpPtr gen_asph(Index n, int d, Rng& rng);
+OpPtr gen_asph(Index n, int d, Rng& rng, bool scaled_diag = false);
+/// Signed sum of equally-shaped operators (sketch.cpp:446-500; device
+/// application + accumulation, never a plan) and the +-{1..4} diagonal.
+OpPtr make_sum(std::vector<OpPtr> ops, std::vector<int> signs);
+OpPtr gen_scaled_diagonal(Index n, Rng& rng);
 
 /// Plans: the columns of M*op (Side::Right, one output per op column) or the
 /// rows of op*W (Side::Left, one output per op row).

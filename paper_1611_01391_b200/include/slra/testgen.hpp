@@ -18,4 +18,16 @@ Matrix gen_cauchy_block(Index m, Index n, Rng& rng);
 /// K_ij = 0.5 log((dx)^2 + (dy)^2) = log|p_i - q_j|.
 Matrix gen_log_kernel_block(Index m, Index n, Rng& rng);
 
+/// Bidiagonal-product pseudo-Gaussian generator (sketch.hpp:92-112,
+/// sketch.cpp:695-791): host generators and the KS normality check, drawing
+/// in the reference's order.
+Matrix bidiagonal_factor(Index n, const std::vector<int>& signs);
+Matrix gen_bidiagonal_product(Index n, Index T, Rng& rng, bool standardize = true);
+Vector bidiagonal_product_column(Index n, Index T, Index j, Rng& rng);
+struct KsResult {
+  double statistic = 0;
+  bool pass = false;
+};
+KsResult ks_normality(const std::vector<double>& sample);
+
 }  // namespace slra

@@ -456,9 +456,75 @@ class AbridgedFourierOp final : public SketchOperator {
   mutable DevBuf<double> dtw_r_, dtw_i_;
 };
 
+// sketch.cpp:446-500: signed sum of equally-shaped operators. Each term is
+// applied on the device and accumulated as out = s_0 Y_0, out += s_i Y_i
+// (slra_axpby), the reference's order; a sum is never compiled into a plan
+// (a concatenated plan would sum the terms in a different order).
+class SumOp final : public SketchOperator {
+ public:
+  SumOp(std::vector<OpPtr> ops, std::vector<int> signs) : ops_(std::move(ops)), signs_(std::move(signs)) {
+    require(!ops_.empty() && ops_.size() == signs_.size(), "sum: size mismatch");
+    for (auto& op : ops_)
+      require(op->rows() == ops_[0]->rows() && op->cols() == ops_[0]->cols(), "sum: dimension mismatch");
+    for (int sg : signs_) require(sg == 1 || sg == -1, "sum: signs must be +-1");
+  }
+  Index rows() const override { return ops_[0]->rows(); }
+  Index cols() const override { return ops_[0]->cols(); }
+  std::string kind() const override { return "sum"; }
+  RowExpr row_of_apply(Index) const override { throw std::logic_error("sum: not a plan operator"); }
+  RowExpr row_of_apply_transpose(Index) const override { throw std::logic_error("sum: not a plan operator"); }
+  bool plannable() const override { return false; }
+  bool is_complex() const override {
+    for (auto& o : ops_)
+      if (o->is_complex()) return true;
+    return false;
+  }
+  void apply_device(const DeviceMatrix& X, bool transpose, DeviceMatrix& Y) const override {
+    slra_ctx cx = device_context();
+    DeviceMatrix T(Y.rows(), Y.cols());
+    for (size_t i = 0; i < ops_.size(); ++i) {
+      ops_[i]->apply_device(X, transpose, T);
+      check(slra_axpby(cx, static_cast<double>(signs_[i]), T.data(), T.ld(), i == 0 ? 0.0 : 1.0, Y.data(), Y.ld(),
+                       Y.rows(), Y.cols()),
+            "sum");
+    }
+  }
+  CMatrix apply_complex(const CMatrix& M) const override { return accumulate(M, false); }
+  CMatrix apply_transpose_complex(const CMatrix& M) const override { return accumulate(M, true); }
+
+ private:
+  CMatrix accumulate(const CMatrix& M, bool transpose) const {
+    slra_ctx cx = device_context();
+    DeviceMatrix ore, oim;
+    for (size_t i = 0; i < ops_.size(); ++i) {
+      const CMatrix y = transpose ? ops_[i]->apply_transpose_complex(M) : ops_[i]->apply_complex(M);
+      DeviceMatrix yr = DeviceMatrix::upload(y.re), yi = DeviceMatrix::upload(y.im);
+      if (i == 0) {
+        ore = DeviceMatrix(y.rows(), y.cols());
+        oim = DeviceMatrix(y.rows(), y.cols());
+      }
+      const double sg = static_cast<double>(signs_[i]), beta = i == 0 ? 0.0 : 1.0;
+      check(slra_axpby(cx, sg, yr.data(), yr.ld(), beta, ore.data(), ore.ld(), y.rows(), y.cols()), "sum");
+      check(slra_axpby(cx, sg, yi.data(), yi.ld(), beta, oim.data(), oim.ld(), y.rows(), y.cols()), "sum");
+    }
+    return CMatrix{ore.download(), oim.download()};
+  }
+  std::vector<OpPtr> ops_;
+  std::vector<int> signs_;
+};
+
 }  // namespace
 
 // ---------------------------------------------------------------- factories
+OpPtr make_sum(std::vector<OpPtr> ops, std::vector<int> signs) {
+  return std::make_shared<SumOp>(std::move(ops), std::move(signs));
+}
+OpPtr gen_scaled_diagonal(Index n, Rng& rng) {  // sketch.cpp:640-645
+  Vector d(static_cast<size_t>(n));
+  for (Index i = 0; i < n; ++i)
+    d[static_cast<size_t>(i)] = static_cast<double>(rng.sign()) * static_cast<double>(1 + rng.uniform_index(4));
+  return make_sign_diagonal(std::move(d));
+}
 OpPtr make_abridged_fourier(Index n, int d) { return std::make_shared<AbridgedFourierOp>(n, d); }
 
 CMatrix materialize_complex(const SketchOperator& op, Index cap) {  // sketch.cpp:690-693
@@ -556,8 +622,9 @@ OpPtr gen_sparse_circulant(Index n, Index s, Rng& rng) {
   return make_sparse_circulant(n, f, std::move(nz));
 }
 OpPtr gen_aph(Index n, int d, Rng& rng) { return make_product({gen_permutation(n, rng), make_abridged_hadamard(n, d)}); }
-OpPtr gen_asph(Index n, int d, Rng& rng) {
-  OpPtr diag = gen_sign_diagonal(n, rng);  // drawn before the permutation, as sketch.cpp:673
+OpPtr gen_asph(Index n, int d, Rng& rng, bool scaled_diag) {
+  // drawn before the permutation, as sketch.cpp:672-675
+  OpPtr diag = scaled_diag ? gen_scaled_diagonal(n, rng) : gen_sign_diagonal(n, rng);
   return make_product({gen_permutation(n, rng), std::move(diag), make_abridged_hadamard(n, d)});
 }
 

@@ -136,3 +136,41 @@ def test_complex_products(slra, oracle):
     assert np.array_equal(slra.apply_complex(Fp, X), oracle.apply_complex(Fo, X))
     Y = oracle.Rng(5).gaussian_matrix(32, 2) + 1j * oracle.Rng(6).gaussian_matrix(32, 2)
     assert np.array_equal(slra.apply_transpose_complex(Fp, Y), oracle.apply_transpose_complex(Fo, Y))
+
+
+def test_sum_operator(slra, oracle):
+    """Signed sums (sketch.cpp:446-500): device applications accumulated in
+    the reference's order; alone, in products, transposed and complex."""
+    n = 128
+    rp, ro = slra.Rng(21), oracle.Rng(21)
+    Sp = slra.make_sum([slra.gen_sparse_circulant(n, 3, rp), slra.gen_asph(n, 2, rp, True),
+                        slra.gen_householder_chain(n, 2, rp)], [1, -1, 1])
+    So = oracle.make_sum([oracle.gen_sparse_circulant(n, 3, ro), oracle.gen_asph(n, 2, ro, True),
+                          oracle.gen_householder_chain(n, 2, ro)], [1, -1, 1])
+    X = oracle.Rng(2).gaussian_matrix(n, 4)
+    for f, g in ((Sp.apply, So.apply), (Sp.apply_transpose, So.apply_transpose)):
+        assert np.linalg.norm(f(X) - g(X)) <= 1e-13 * np.linalg.norm(g(X))
+    sel = list(range(0, n, 4))
+    Fp = slra.make_product([slra.make_sub_identity(sel, n), Sp])
+    Fo = oracle.make_product([oracle.make_sub_identity(sel, n), So])
+    assert np.linalg.norm(Fp.apply(X) - Fo.apply(X)) <= 1e-13 * np.linalg.norm(Fo.apply(X))
+    Z = X + 1j * oracle.Rng(3).gaussian_matrix(n, 4)
+    Cp = slra.make_sum([slra.make_abridged_fourier(n, 3), slra.gen_sign_diagonal(n, slra.Rng(4))], [1, -1])
+    Co = oracle.make_sum([oracle.make_abridged_fourier(n, 3), oracle.gen_sign_diagonal(n, oracle.Rng(4))], [1, -1])
+    assert np.array_equal(slra.apply_complex(Cp, Z), oracle.apply_complex(Co, Z))
+    with pytest.raises(ValueError):
+        slra.make_sum([slra.gen_sign_diagonal(n, rp), slra.gen_sign_diagonal(n, rp)], [1, 2])
+
+
+def test_generators_match_oracle(slra, oracle):
+    assert np.array_equal(slra.gen_bidiagonal_product(64, 6, slra.Rng(9), True),
+                          oracle.gen_bidiagonal_product(64, 6, oracle.Rng(9), True))
+    assert np.array_equal(slra.bidiagonal_product_column(64, 6, 5, slra.Rng(9)),
+                          oracle.bidiagonal_product_column(64, 6, 5, oracle.Rng(9)))
+    x = [slra.Rng(3).gaussian() for _ in range(1)]
+    r = slra.Rng(1000)
+    sample = [r.gaussian() for _ in range(10000)]
+    assert slra.ks_normality(sample) == oracle.ks_normality(sample)
+    X = oracle.Rng(1).gaussian_matrix(64, 3)
+    Dp, Do = slra.gen_scaled_diagonal(64, slra.Rng(2)), oracle.gen_scaled_diagonal(64, oracle.Rng(2))
+    assert np.array_equal(Dp.apply(X), Do.apply(X))

@@ -801,3 +801,25 @@ def test_abridged_fourier_displays(oracle):  # test_sketch.cpp:50-80
     X = oracle.Rng(5).gaussian_matrix(8, 3).astype(complex)
     op = oracle.make_abridged_fourier(8, 2)
     assert np.linalg.norm(oracle.apply_transpose_complex(op, X) - A.T @ X) < 1e-12
+
+
+def test_bidiagonal_product_generator(oracle):  # test_sketch.cpp:292-317
+    assert np.linalg.norm(oracle.gen_bidiagonal_product(5, 0, oracle.Rng(1), False) - np.eye(5)) == 0.0
+    B = oracle.bidiagonal_factor(3, [1, 1, 1])
+    assert B[0, 2] == 1.0 and B[1, 0] == 1.0 and B[2, 1] == 1.0 and np.all(np.diag(B) == 1.0)
+    G = oracle.gen_bidiagonal_product(16, 5, oracle.Rng(77), False)
+    assert np.linalg.norm(G[:, 7] - oracle.bidiagonal_product_column(16, 5, 7, oracle.Rng(77))) == 0.0
+    S = oracle.gen_bidiagonal_product(32, 8, oracle.Rng(78), True)
+    assert np.all(np.abs(S.mean(axis=0)) < 1e-12) and np.all(np.abs((S ** 2).mean(axis=0) - 1) < 1e-10)
+
+
+def test_ks_normality(oracle):  # test_sketch.cpp:319-334 (20 of the 100 seeds)
+    passes = 0
+    for t in range(20):
+        r = oracle.Rng(1000 + t)
+        passes += oracle.ks_normality([r.gaussian() for _ in range(10000)])[1]
+    assert passes >= 18
+    with pytest.raises(ValueError):
+        oracle.ks_normality([1.0] * 100)
+    r = oracle.Rng(5)
+    assert not oracle.ks_normality([r.uniform() for _ in range(10000)])[1]
