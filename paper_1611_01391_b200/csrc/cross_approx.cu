@@ -93,6 +93,27 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   return s;
 }
 
+// S (len x nidx, ld len) <- the strip A(idx, :)^T (rows_strip) or A(:, idx):
+// a thread per strip row, eight independent global loads in flight before
+// the shared-memory stores (no per-element integer division)
+template <int NT>
+__device__ void stage_strip(double* S, const double* A, int64_t lda, bool rows_strip, const int* idx, int nidx,
+                            int len) {
+  for (int i = threadIdx.x; i < len; i += NT) {
+    for (int t0 = 0; t0 < nidx; t0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u < nidx ? t0 + u : nidx - 1;
+        v[u] = rows_strip ? __ldg(A + idx[t] + (int64_t)i * lda) : __ldg(A + i + (int64_t)idx[t] * lda);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (t0 + u < nidx) S[i + (t0 + u) * len] = v[u];
+    }
+  }
+}
+
 // select_rows_spanning(strip, count, h) where strip (len x nidx) is gathered
 // from A: rows_strip -> strip = A(idx_in, :)^T (len = n), else A(:, idx_in).
 template <int NT, int CMAX>
@@ -100,17 +121,9 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
                             int len, int count, double h, int* idx_out, double* vol_out) {
   const int tid = threadIdx.x;
   // gather (each element of the strip is an entry read of the oracle)
-  if (rows_strip) {
-    for (int e = tid; e < len * nidx; e += NT) {
-      const int t = e % nidx, j = e / nidx;
-      s.S[j + t * len] = __ldg(A + idx_in[t] + (int64_t)j * lda);
-    }
-  } else {
-    for (int e = tid; e < len * nidx; e += NT) {
-      const int i = e % len, t = e / len;
-      s.S[i + t * len] = __ldg(A + i + (int64_t)idx_in[t] * lda);
-    }
-  }
+  // 2-D loops (no integer division per element), unrolled so that several
+  // independent global loads are in flight before the shared-memory stores
+  stage_strip<NT>(s.S, A, lda, rows_strip, idx_in, nidx, len);
   __syncthreads();
   // ONE len x nidx array carries the strip, its basis Q (in place) and then
   // B = Q G^-1 (in place): the pivot order is taken with the working copy in
@@ -304,10 +317,7 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
     double* Pb = P.P + (int64_t)b * P.m * P.rq;
     double* Qb = P.Q + (int64_t)b * P.rq * P.n;
     __syncthreads();
-    for (int e = tid; e < P.m * P.l; e += kCT) {
-      const int i = e % P.m, t = e / P.m;
-      s.S[i + t * P.m] = __ldg(A + i + (int64_t)s.Jcur[t] * P.lda);
-    }
+    stage_strip<kCT>(s.S, A, P.lda, false, s.Jcur, P.l, P.m);
     __syncthreads();
     // accumulators in chunks of kCH outputs (registers stay within the
     // two-CTAs-per-SM budget); each chunk re-reads its strip from smem
@@ -329,10 +339,7 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
       }
     }
     __syncthreads();  // every row of P is done with C: stage R^T over it
-    for (int e = tid; e < P.n * P.k; e += kCT) {
-      const int t = e % P.k, c = e / P.k;
-      s.S[c + t * P.n] = __ldg(A + s.Icur[t] + (int64_t)c * P.lda);
-    }
+    stage_strip<kCT>(s.S, A, P.lda, true, s.Icur, P.k, P.n);
     __syncthreads();
     for (int c = tid; c < P.n; c += kCT) {
       for (int j0 = 0; j0 < P.rq; j0 += kCH) {
