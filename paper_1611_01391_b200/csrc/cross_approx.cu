@@ -50,8 +50,8 @@ struct CaSmem {
 
 __host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
-  // S (mm c + c), W (c+1) c, Gt c^2, V (c+1) c, 4 c-vectors, nu/nd/rn (mm each), rv 40, volv + slack
-  size_t d = (size_t)mm * c + (size_t)c + 2 * (size_t)(c + 1) * c + (size_t)c * c + 4 * (size_t)c +
+  // S (mm c + c), W (c+1) c, Gt (c+1) c, V (c+1) c, 4 c-vectors, nu/nd/rn (mm each), rv 40, volv + slack
+  size_t d = (size_t)mm * c + (size_t)c + 3 * (size_t)(c + 1) * c + 4 * (size_t)c +
              3 * (size_t)mm + 40 + 8 + 2 * (size_t)c;
   size_t i = 2 * (size_t)mm + 5 * (size_t)c + 8;
   return d * 8 + 33 * 8 + i * 4 + 64;
@@ -64,7 +64,7 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   s.S = d; d += (size_t)mm * c + c;
   s.W = d; d += (size_t)(c + 1) * c;  // the nucleus' Jacobi operand (ld p | 1, p <= c)
   s.R = nullptr;
-  s.Gt = d; d += c * c;
+  s.Gt = d; d += (size_t)(c + 1) * c;  // room for the odd ld of the maxvol QR (rq | 1)
   s.V = d; d += (size_t)(c + 1) * c;  // room for ld = q | 1
   // the nucleus factors T_r Sigma_r^-1 and S_r are written after
   // cta_svd_finish, when the Jacobi operands V and W are dead
@@ -142,7 +142,9 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
   else if constexpr (CMAX > 32)
     cta_colpiv_init_regs<NT, 64>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx);
   __syncthreads();
-  const int st = cta_maxvol_swaps<NT>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, s.S, len, s.Gt, rq, s.perm, s.tau,
+  // Gt with an odd leading dimension: warp_colpiv_qr gives each lane a
+  // column, and ld = rq (even) put all 32 lanes on the same shared bank
+  const int st = cta_maxvol_swaps<NT>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, s.S, len, s.Gt, rq | 1, s.perm, s.tau,
                                       s.nu, s.nd, s.rv, s.ri, s.flag, s.volv);
   if (st != SLRA_OK) return st;
   __syncthreads();
