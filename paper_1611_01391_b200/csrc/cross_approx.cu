@@ -128,6 +128,8 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
   // ONE len x nidx array carries the strip, its basis Q (in place) and then
   // B = Q G^-1 (in place): the pivot order is taken with the working copy in
   // registers, and the volume |det Q[idx, :]| is tracked through the swaps.
+  // The pivot phase's reflectors are those of maxvol round 0's ColPivQR(G^T)
+  // (G = Q(I, :)), so round 0 continues from them instead of refactorising.
   cta_thin_qr_inplace<NT, CMAX>(s.S, len, len, nidx, s.tau, s.rv);
   const int rq = count < nidx ? count : nidx;
   if (count > rq) {  // the padding branch needs the basis row norms (cur.cpp:125-134)
@@ -137,15 +139,18 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
       s.rn[i] = sqrt(acc);
     }
   }
-  if (rq <= 16) cta_colpiv_init_regs<NT, 16>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx);
-  else if (rq <= 32) cta_colpiv_init_regs<NT, 32>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx);
+  if (rq <= 16) cta_colpiv_init_regs<NT, 16>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx,
+                                     s.S, s.Gt, rq | 1, s.sigma);
+  else if (rq <= 32) cta_colpiv_init_regs<NT, 32>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx,
+                                     s.S, s.Gt, rq | 1, s.sigma);
   else if constexpr (CMAX > 32)
-    cta_colpiv_init_regs<NT, 64>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx);
+    cta_colpiv_init_regs<NT, 64>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx,
+                                     s.S, s.Gt, rq | 1, s.sigma);
   __syncthreads();
   // Gt with an odd leading dimension: warp_colpiv_qr gives each lane a
   // column, and ld = rq (even) put all 32 lanes on the same shared bank
   const int st = cta_maxvol_swaps<NT>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, s.S, len, s.Gt, rq | 1, s.perm, s.tau,
-                                      s.nu, s.nd, s.rv, s.ri, s.flag, s.volv);
+                                      s.nu, s.nd, s.rv, s.ri, s.flag, s.volv, s.r2p, s.sigma);
   if (st != SLRA_OK) return st;
   __syncthreads();
   for (int t = tid; t < rq; t += NT) idx_out[t] = s.tmpidx[t];

@@ -365,7 +365,17 @@ __device__ void cta_colpiv_init(const double* Q, int ldq, int m, int r, const Co
 // arithmetic, in the same order, as cta_colpiv_init.
 template <int NT, int RMAX>
 __device__ void cta_colpiv_init_regs(const double* Q, int ldq, int m, int r, double* nu, double* nd, int* p2r,
-                                     int* r2p, double* vbuf, double* tauv, double* rv, int64_t* ri, int* I_out) {
+                                     int* r2p, double* vbuf, double* tauv, double* rv, int64_t* ri, int* I_out,
+                                     double* Wx = nullptr, double* Rsv = nullptr, int ldr = 0,
+                                     double* pv = nullptr) {
+  // Wx / Rsv / pv (optional): keep the factorisation for maxvol round 0.
+  // The first r pivots are the rows I, so these reflectors are those of
+  // ColPivQR(Q(I, :)^T) with the identity permutation (same columns, same
+  // arithmetic in the same order as warp_colpiv_qr): Rsv (r x r, ld ldr)
+  // gets R on and above the diagonal and the Householder vectors below it,
+  // tauv[k] the k-th tau, pv[k] the k-th pivot norm, and Wx (= Q in place,
+  // ld ldq) every row after the reflectors applied to it (all r for the
+  // other rows, those before its own step for a pivot row).
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double sqrt_eps = 1.4901161193847656e-08;  // sqrt(DBL_EPSILON)
   double x[RMAX];
@@ -389,6 +399,7 @@ __device__ void cta_colpiv_init_regs(const double* Q, int ldq, int m, int r, dou
     for (int p = k + tid; p < m; p += NT) a = argmax_merge(a, ArgMax{nu[p], p});
     a = block_argmax<NT>(a, rv, ri);
     const int big = static_cast<int>(a.i);
+    if (pv && tid == 0) pv[k] = a.v;
     if (tid == 0 && big != k) {
       const int rk = p2r[k], rb = p2r[big];
       p2r[k] = rb;
@@ -413,24 +424,28 @@ __device__ void cta_colpiv_init_regs(const double* Q, int ldq, int m, int r, dou
       const double c0 = vbuf[k];
       double t;
       __syncwarp();
+      double beta = c0;
       if (tail <= DBL_MIN) {
         t = 0.0;
         for (int j = k + 1 + lane; j < r; j += 32) vbuf[j] = 0.0;
       } else {
-        double beta = sqrt(c0 * c0 + tail);
+        beta = sqrt(c0 * c0 + tail);
         if (c0 >= 0.0) beta = -beta;
         const double den = c0 - beta;
         for (int j = k + 1 + lane; j < r; j += 32) vbuf[j] = vbuf[j] / den;
         t = (beta - c0) / beta;
       }
       __syncwarp();
+      if (Rsv)
+        for (int j = k + 1 + lane; j < r; j += 32) Rsv[j + k * ldr] = vbuf[j];
       if (lane == 0) {
-        tauv[0] = t;
+        tauv[k] = t;
         I_out[k] = row;
+        if (Rsv) Rsv[k + k * ldr] = beta;
       }
     }
     __syncthreads();
-    const double t = tauv[0];
+    const double t = tauv[k];
     const int p = own ? r2p[tid] : -1;
     if (p > k) {
       if (r - k > 1 && t != 0.0) {
@@ -472,6 +487,15 @@ __device__ void cta_colpiv_init_regs(const double* Q, int ldq, int m, int r, dou
     }
     __syncthreads();
   }
+  if (Wx && own) {
+    const int p = r2p[tid];
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) {
+      if (j < r) Wx[tid + j * ldq] = x[j];
+      if (p < r && j < p) Rsv[j + p * ldr] = x[j];  // R(0:p, p): final entries of pivot row p
+    }
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- small ColPivQR (one warp)
@@ -591,18 +615,39 @@ __device__ inline SmallColPiv warp_colpiv_qr(double* G, int ldg, int n, double t
 template <int NT>
 __device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h, int max_swaps, int* I,
                                 double* W, int ldw, double* Gt, int ldg, int* perm, double* tau, double* nu,
-                                double* nd, double* rv, int64_t* ri, int* shared_flag, double* vol_out = nullptr) {
+                                double* nd, double* rv, int64_t* ri, int* shared_flag, double* vol_out = nullptr,
+                                const int* pre_r2p = nullptr, const double* pre_pv = nullptr) {
   const int tid = threadIdx.x, warp = tid >> 5;
   // swap round 0 exactly as the reference: ColPivQR(G^T) and its solve for
-  // every row. G^T(c, t) = A(I[t], c)
-  for (int e = tid; e < r * r; e += NT) {
-    const int cc = e % r, t = e / r;
-    Gt[cc + t * ldg] = A[I[t] + cc * lda];
-  }
-  __syncthreads();
-  if (warp == 0) {
-    SmallColPiv q = warp_colpiv_qr(Gt, ldg, r, 1e-12, perm, tau, nu, nd);
-    if ((tid & 31) == 0) shared_flag[0] = q.rank < r ? 1 : 0;  // rank == r implies r nonzero pivots
+  // every row. G^T(c, t) = A(I[t], c). Prefactored (pre_r2p): the pivoted-QR
+  // initialisation already holds that factorisation (cta_colpiv_init_regs
+  // with Wx = W = A, Rsv = Gt): identity permutation, and each row continues
+  // from the reflectors already applied to it.
+  if (pre_r2p) {
+    if (tid == 0) {
+      // warp_colpiv_qr's nonzero-pivot and rank rules on the saved pivot norms
+      const double thr_helper = (pre_pv[0] * kEps) * (pre_pv[0] * kEps) / (double)r;
+      int nonzero = r;
+      double maxpivot = 0.0;
+      for (int k = 0; k < r; ++k) {
+        if (nonzero == r && pre_pv[k] * pre_pv[k] < thr_helper * (double)(r - k)) nonzero = k;
+        maxpivot = fmax(maxpivot, fabs(Gt[k + k * ldg]));
+      }
+      int rank = 0;
+      for (int i = 0; i < nonzero; ++i) rank += (fabs(Gt[i + i * ldg]) > fabs(maxpivot) * 1e-12) ? 1 : 0;
+      shared_flag[0] = rank < r ? 1 : 0;
+    }
+    for (int t = tid; t < r; t += NT) perm[t] = t;
+  } else {
+    for (int e = tid; e < r * r; e += NT) {
+      const int cc = e % r, t = e / r;
+      Gt[cc + t * ldg] = A[I[t] + cc * lda];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      SmallColPiv q = warp_colpiv_qr(Gt, ldg, r, 1e-12, perm, tau, nu, nd);
+      if ((tid & 31) == 0) shared_flag[0] = q.rank < r ? 1 : 0;  // rank == r implies r nonzero pivots
+    }
   }
   __syncthreads();
   if (shared_flag[0]) return SLRA_ERR_SELECTION_FAILURE;
@@ -617,8 +662,13 @@ __device__ int cta_maxvol_swaps(const double* A, int lda, int m, int r, double h
   // W(i, t) holds B(i, perm[t]) (storage order of the solve)
   for (int i = tid; i < m; i += NT) {
     double* c = W + i;  // row i of W as a strided vector (stride ldw)
-    for (int j = 0; j < r; ++j) c[j * ldw] = A[i + j * lda];
-    for (int k = 0; k < r; ++k) {
+    int k0 = 0;
+    if (pre_r2p) {
+      k0 = pre_r2p[i] < r ? pre_r2p[i] : r;  // reflectors 0..k0-1 already applied (in place)
+    } else {
+      for (int j = 0; j < r; ++j) c[j * ldw] = A[i + j * lda];
+    }
+    for (int k = k0; k < r; ++k) {
       const double t = tau[k];
       if (r - k == 1) {
         c[k * ldw] *= (1.0 - t);
