@@ -27,20 +27,26 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---------------------------------------------------------------- residual
+// Each CTA walks a contiguous range of 128 x 32 tiles of A, row block by
+// row block. Each warp owns 16 rows of the block, and its P fragments (16
+// rows x 32 inner, the whole m16n8k16 A operand for every tile of the row
+// block) stay in REGISTERS, so per tile only the A tile and the 32 x 32 Q
+// tile stream through shared memory (cp.async, NS stages in flight). Two
+// CTAs per SM: one CTA's MMAs run while the other sits in its epilogue or
+// barrier (ncu: with one CTA per SM the DMMA pipe idled through every
+// epilogue, 52 % active).
 namespace rs {
-constexpr int NT = 256;        // 8 warps: 4 (rows) x 2 (cols), warp tile 32 x 16
-constexpr int TM = 64;         // tile rows (4 row-warps x MI m16 blocks)
+constexpr int NT = 256;        // 8 warps, 16 * MI rows each
+constexpr int MI = 1;          // m16 blocks per warp
+constexpr int TM = 8 * 16 * MI;  // tile rows (row block)
 constexpr int TN = 32;         // tile cols
 constexpr int KP = 32;         // inner dimension (padded)
-constexpr int LDU = TM + 2;    // Us[k][row]
-constexpr int LDV = KP + 4;    // Vs[col][k]
-constexpr int LDM = TM + 2;    // Ms[col][row]
-constexpr int U_D = KP * LDU;  // doubles per U buffer
-constexpr int V_D = TN * LDV;
-constexpr int M_D = TN * LDM;
-constexpr int NS = 2;          // cp.async pipeline depth (tiles in flight); 2 CTAs per SM
-constexpr int MI = TM / 64;    // m16 row blocks per warp
-constexpr size_t SMEM = sizeof(double) * NS * (U_D + V_D + M_D);
+constexpr int LDV = KP + 4;    // Vs[col][k]: conflict-free B fragment reads
+constexpr int LDM = TM + 2;    // Ms[col][row]: conflict-free epilogue reads
+constexpr int V_D = TN * LDV;  // doubles per Q stage
+constexpr int M_D = TN * LDM;  // doubles per A stage
+constexpr int NS = 2;          // tiles in flight (two CTAs per SM)
+constexpr size_t SMEM = sizeof(double) * NS * (V_D + M_D);
 }  // namespace rs
 
 struct StreamResidualArgs {
@@ -54,11 +60,13 @@ struct StreamResidualArgs {
   double* part;  // 2 per CTA
 };
 
-__device__ __forceinline__ void rs_stage(const StreamResidualArgs& a, int64_t i0, int64_t j0, bool load_v, double* Us,
-                                         double* Vs, double* Ms) {
+__device__ __forceinline__ void rs_stage(const StreamResidualArgs& a, int64_t i0, int64_t j0, double* Vs,
+                                         double* Ms) {
   using namespace rs;
   const int tid = threadIdx.x;
-  // M tile: TN columns x TM rows, 16-byte chunks of 2 rows
+  // A tile: TN columns x TM rows in 16-byte chunks of 2 rows (a column is
+  // 2 KB contiguous in HBM)
+#pragma unroll 4
   for (int e = tid; e < TN * (TM / 2); e += NT) {
     const int col = e / (TM / 2), ch = e % (TM / 2);
     const int64_t r = i0 + 2 * ch, cc = j0 + col;
@@ -70,105 +78,98 @@ __device__ __forceinline__ void rs_stage(const StreamResidualArgs& a, int64_t i0
     }
     cp_async16(Ms + col * LDM + 2 * ch, src, bytes);
   }
-  // U tile: k-major (columns of P), TM rows
-  for (int e = tid; e < KP * (TM / 2); e += NT) {
-    const int k = e / (TM / 2), ch = e % (TM / 2);
-    const int64_t r = i0 + 2 * ch;
+  // Q tile: per column the inner entries are contiguous
+  for (int e = tid; e < TN * (KP / 2); e += NT) {
+    const int col = e / (KP / 2), ch = e % (KP / 2);
+    const int k = 2 * ch;
+    const int64_t cc = j0 + col;
     int bytes = 0;
-    const double* src = a.P;
-    if (k < a.inner && r < a.m) {
-      bytes = (r + 1 < a.m) ? 16 : 8;
-      src = a.P + r + (int64_t)k * a.ldp;
+    const double* src = a.Q;
+    if (cc < a.n && k < a.inner) {
+      bytes = (k + 1 < a.inner) ? 16 : 8;
+      src = a.Q + k + cc * a.ldq;
     }
-    cp_async16(Us + k * LDU + 2 * ch, src, bytes);
-  }
-  if (load_v) {
-    // V tile: per column, the inner entries are contiguous
-    for (int e = tid; e < TN * (KP / 2); e += NT) {
-      const int col = e / (KP / 2), ch = e % (KP / 2);
-      const int k = 2 * ch;
-      const int64_t cc = j0 + col;
-      int bytes = 0;
-      const double* src = a.Q;
-      if (cc < a.n && k < a.inner) {
-        bytes = (k + 1 < a.inner) ? 16 : 8;
-        src = a.Q + k + cc * a.ldq;
-      }
-      cp_async16(Vs + col * LDV + k, src, bytes);
-    }
+    cp_async16(Vs + col * LDV + k, src, bytes);
   }
 }
 
 __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidualArgs a) {
   using namespace rs;
   extern __shared__ __align__(16) double smem[];
-  // stage slot s of U / V / M (pointer arithmetic, no local-memory pointer arrays)
-#define UB(s) (smem + (s) * U_D)
-#define VB(s) (smem + NS * U_D + (s) * V_D)
-#define MB(s) (smem + NS * U_D + NS * V_D + (s) * M_D)
+#define VB(s) (smem + (s) * V_D)
+#define MB(s) (smem + NS * V_D + (s) * M_D)
   __shared__ double red[40];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t tiles_m = (a.m + TM - 1) / TM, tiles_n = (a.n + TN - 1) / TN;
   const int64_t tiles = tiles_m * tiles_n;
-  // contiguous tile range per CTA; NS tiles in flight (cp.async groups),
-  // so the HBM latency of a tile hides behind NS - 1 tiles of DMMA work
+  // contiguous tile range per CTA, row-block major (the P fragments change
+  // only when the range crosses into the next row block)
   const int64_t t0 = tiles * blockIdx.x / gridDim.x, t1 = tiles * (blockIdx.x + 1) / gridDim.x;
-  const int kc16 = (a.inner + 15) & ~15;
+  const int nkk = (a.inner + 15) >> 4;  // k16 steps (0, 1 or 2)
   double rsum = 0.0, nsum = 0.0;
 #pragma unroll
   for (int s = 0; s < NS - 1; ++s) {
     const int64_t t = t0 + s;
-    if (t < t1) rs_stage(a, (t % tiles_m) * TM, (t / tiles_m) * TN, true, UB(s), VB(s), MB(s));
+    if (t < t1) rs_stage(a, (t / tiles_n) * TM, (t % tiles_n) * TN, VB(s), MB(s));
     cp_async_commit();
   }
+  double af[MI][2][8];  // [m16 block][k16 step][fragment]
+  int64_t rb_loaded = -1;
   int slot = 0;
   for (int64_t t = t0; t < t1; ++t) {
     {  // prefetch tile t + NS - 1 into the slot freed by tile t - 1
       const int64_t tp = t + NS - 1;
       const int sp = (slot + NS - 1) % NS;
-      if (tp < t1) rs_stage(a, (tp % tiles_m) * TM, (tp / tiles_m) * TN, true, UB(sp), VB(sp), MB(sp));
+      if (tp < t1) rs_stage(a, (tp / tiles_n) * TM, (tp % tiles_n) * TN, VB(sp), MB(sp));
       cp_async_commit();
+    }
+    const int64_t rb = t / tiles_n;
+    if (rb != rb_loaded) {  // P fragments of this warp's 32 rows (zero outside P)
+      rb_loaded = rb;
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const int64_t row = rb * TM + warp * 16 * MI + mi * 16 + g + 8 * (v & 1);
+            const int k = kk * 16 + t4 + 4 * (v >> 1);
+            af[mi][kk][v] = (row < a.m && k < a.inner) ? __ldg(a.P + row + (int64_t)k * a.ldp) : 0.0;
+          }
     }
     cp_async_wait<NS - 1>();
     __syncthreads();
-    const double* Us = UB(slot);
     const double* Vs = VB(slot);
-    const double* Ms = MB(slot);
-    // warp tile 32 x 16 = 2 (16-row) x 2 (8-col) m16n8k16 blocks; K padded
-    // to 16 (the staged U / V tiles are zero-filled up to KP)
-    double acc[MI][2][4];
+    const double* Ms = MB(slot) + warp * 16 * MI;
+    double acc[MI][4][4];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[mi][ni][v] = 0.0;
-    for (int kk = 0; kk < kc16; kk += 16) {
-      double af[MI][8], bf[2][4];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi)
+    for (int kk = 0; kk < 2; ++kk) {
+      if (kk < nkk) {
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          af[mi][v] = Us[(kk + t4 + 4 * (v >> 1)) * LDU + wm * (TM / 4) + mi * 16 + g + 8 * (v & 1)];
+        for (int ni = 0; ni < 4; ++ni) {
+          double bf[4];
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+          for (int v = 0; v < 4; ++v) bf[v] = Vs[(ni * 8 + g) * LDV + kk * 16 + t4 + 4 * v];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) bf[ni][v] = Vs[(wn * 16 + ni * 8 + g) * LDV + kk + t4 + 4 * v];
-#pragma unroll
-      for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma_16x8x16(acc[mi][ni], af[mi], bf[ni]);
+          for (int mi = 0; mi < MI; ++mi) dmma_16x8x16(acc[mi][ni], af[mi][kk], bf);
+        }
+      }
     }
-    double r0 = 0.0, r1 = 0.0, n0 = 0.0, n1 = 0.0;  // short chains (FP64 FMA latency ~24)
+    double r0 = 0.0, r1 = 0.0, n0 = 0.0, n1 = 0.0;  // short chains (FP64 FMA latency)
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
         for (int v = 0; v < 4; v += 2) {
-          const int row = wm * (TM / 4) + mi * 16 + g + 8 * (v >> 1), col = wn * 16 + ni * 8 + 2 * t4;
+          const int row = mi * 16 + g + 8 * (v >> 1), col = ni * 8 + 2 * t4;
           const double x0 = Ms[col * LDM + row], x1 = Ms[(col + 1) * LDM + row];  // zero outside A
           const double d0 = x0 - acc[mi][ni][v], d1 = x1 - acc[mi][ni][v + 1];
           r0 = fma(d0, d0, r0);
@@ -182,7 +183,6 @@ __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidu
     slot = (slot + 1) % NS;
   }
   cp_async_wait<0>();
-#undef UB
 #undef VB
 #undef MB
   rsum = block_sum<NT>(rsum, red);
@@ -216,7 +216,7 @@ int launch_residual_stream(Context* c, const double* A, int64_t lda, int64_t m, 
                        (ldp % 2 == 0) && ((uintptr_t)Q % 16 == 0) && (ldq % 2 == 0)));
   if (!aligned || inner > rs::KP || m < 1 || n < 1) return SLRA_ERR_UNSUPPORTED;
   const int64_t tiles = ((m + rs::TM - 1) / rs::TM) * ((n + rs::TN - 1) / rs::TN);
-  int grid = 2 * c->num_sms;  // two co-resident CTAs per SM: their sync phases interleave
+  int grid = 2 * c->num_sms;  // two co-resident CTAs per SM: their epilogues and barriers interleave
   if (tiles < grid) grid = (int)tiles;
   double* part = partials(c, 2 * grid);
   if (!part) return SLRA_ERR_CUDA;
