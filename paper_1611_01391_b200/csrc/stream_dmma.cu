@@ -118,12 +118,11 @@ __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidu
   int64_t rb_loaded = -1;
   int slot = 0;
   for (int64_t t = t0; t < t1; ++t) {
-    {  // prefetch tile t + NS - 1 into the slot freed by tile t - 1
-      const int64_t tp = t + NS - 1;
-      const int sp = (slot + NS - 1) % NS;
-      if (tp < t1) rs_stage(a, (tp / tiles_n) * TM, (tp % tiles_n) * TN, VB(sp), MB(sp));
-      cp_async_commit();
-    }
+    // tile t landed (NS - 2 newer groups may still fly); after the barrier
+    // every warp is past tile t - 1, so its slot can take tile t + NS - 1
+    // (prefetched below, behind this tile's DMMAs): one barrier per tile
+    cp_async_wait<NS - 2>();
+    __syncthreads();
     const int64_t rb = t / tiles_n;
     if (rb != rb_loaded) {  // P fragments of this warp's 32 rows (zero outside P)
       rb_loaded = rb;
@@ -138,8 +137,6 @@ __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidu
             af[mi][kk][v] = (row < a.m && k < a.inner) ? __ldg(a.P + row + (int64_t)k * a.ldp) : 0.0;
           }
     }
-    cp_async_wait<NS - 1>();
-    __syncthreads();
     const double* Vs = VB(slot);
     const double* Ms = MB(slot) + warp * 16 * MI;
     double acc[MI][4][4];
@@ -162,6 +159,12 @@ __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidu
         }
       }
     }
+    {  // prefetch tile t + NS - 1 while the DMMAs above drain (issued after them in program order)
+      const int64_t tp = t + NS - 1;
+      const int sp = (slot + NS - 1) % NS;
+      if (tp < t1) rs_stage(a, (tp / tiles_n) * TM, (tp % tiles_n) * TN, VB(sp), MB(sp));
+      cp_async_commit();
+    }
     double r0 = 0.0, r1 = 0.0, n0 = 0.0, n1 = 0.0;  // short chains (FP64 FMA latency)
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
@@ -179,7 +182,6 @@ __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidu
         }
     rsum += r0 + r1;
     nsum += n0 + n1;
-    __syncthreads();  // this slot is refilled by the prefetch of the next iteration
     slot = (slot + 1) % NS;
   }
   cp_async_wait<0>();
