@@ -14,6 +14,40 @@
 
 namespace slra_dev {
 
+// Jacobi rotation (c, s) from the pair's Gram entries a = |x|^2, b = |y|^2,
+// g = x.y: t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), d = b - a, c = 1 /
+// sqrt(1 + t^2), s = c t. Only the orthogonality of the rotation matters for
+// the one-sided Jacobi result (sigma are the final column norms, checked by
+// the orthogonality threshold); the angle itself may be off by the hardware
+// seed's ~2^-22, which the next sweep absorbs. So t comes from the MUFU
+// rsqrt / rcp seeds (rsqrt.approx.f64, rcp.approx.ftz.f64: one instruction
+// each instead of the IEEE sqrt and division sequences), while c is refined
+// to full precision (two Newton steps) so that c^2 + s^2 = 1 to rounding.
+__device__ __forceinline__ double mufu_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ double mufu_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ void jacobi_rotation(double a, double b, double g, double& cs, double& sn) {
+  const double d = b - a, g2 = 2.0 * g;
+  const double h = fma(d, d, g2 * g2);
+  const double rr = (g2 * g2 < 1e-17 * (d * d)) ? fabs(d) : h * mufu_rsqrt(h);
+  const double t = copysign(1.0, d) * g2 * mufu_rcp(fabs(d) + rr);
+  const double q = fma(t, t, 1.0);
+  double y = mufu_rsqrt(q);
+  const double hq = 0.5 * q;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) y = y * fma(-hq * y, y, 1.5);  // y <- y (3 - q y^2) / 2
+  cs = y;
+  sn = y * t;
+}
+
+
 // ------------------------------------------------------------------ context
 constexpr int kArenaSlots = 12;
 

@@ -1004,16 +1004,11 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
         // |g| <= tol sqrt(a b), squared (no sqrt on the chain)
         if (!valid || gg == 0.0 || gg * gg <= tol2 * (aa * bb)) continue;
         if (aa < thr2 && bb < thr2) continue;
-        // t = sign(z) / (|z| + sqrt(1 + z^2)), z = (b - a) / (2g), written as
-        // t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), d = b - a: one sqrt, one
-        // division, one rsqrt on the dependent chain
-        const double d = bb - aa, g2 = 2.0 * gg;
-        // late sweeps: (2g/d)^2 below eps makes sqrt(d^2 + 4g^2) == |d| in
-        // FP64, so t = g / d exactly as rounded — skip the sqrt
-        const double rr = (g2 * g2 < 1e-17 * (d * d)) ? fabs(d) : sqrt(fma(d, d, g2 * g2));
-        const double t = copysign(1.0, d) * g2 / (fabs(d) + rr);
-        const double cs = rsqrt(fma(t, t, 1.0));
-        const double sn = cs * t;
+        // t = sign(z) / (|z| + sqrt(1 + z^2)), z = (b - a) / (2g), from the
+        // hardware rsqrt / rcp seeds; c refined to full precision
+        // (common.cuh: jacobi_rotation). This chain is most of a round.
+        double cs, sn;
+        jacobi_rotation(aa, bb, gg, cs, sn);
 #pragma unroll
         for (int r = 0; r < RPG; ++r) {
           const int i = sub + 8 * r;
