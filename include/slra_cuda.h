@@ -68,6 +68,11 @@ int slra_device_free(slra_ctx ctx, void* d_ptr);
 int slra_memcpy_h2d(slra_ctx ctx, void* d_dst, const void* h_src, int64_t bytes);
 int slra_memcpy_d2h(slra_ctx ctx, void* h_dst, const void* d_src, int64_t bytes); /* syncs */
 int slra_memcpy_d2d(slra_ctx ctx, void* d_dst, const void* d_src, int64_t bytes);
+/* Page-locked host memory (cudaHostAlloc / cudaFreeHost) for results that
+ * cross the bus on every call: a D2H copy into it runs at the link's rate
+ * instead of through the driver's pageable staging. */
+int slra_host_alloc(int64_t bytes, void** h_out);
+int slra_host_free(void* h_ptr);
 
 /* ------------------------------------------------------------ a2/a14 gathers
  * EntryOracle::rows_of / cols_of / block (testgen.cpp:11-30) and

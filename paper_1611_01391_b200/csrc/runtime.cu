@@ -254,6 +254,19 @@ int slra_memcpy_d2h(slra_ctx ctx, void* h, const void* d, int64_t bytes) {
   return SLRA_OK;
 }
 
+int slra_host_alloc(int64_t bytes, void** h_out) {
+  if (!h_out || bytes < 0) return SLRA_ERR_INVALID_ARGUMENT;
+  *h_out = nullptr;
+  if (bytes == 0) return SLRA_OK;
+  SLRA_CUDA(cudaHostAlloc(h_out, (size_t)bytes, cudaHostAllocDefault));
+  return SLRA_OK;
+}
+
+int slra_host_free(void* h) {
+  if (h) SLRA_CUDA(cudaFreeHost(h));
+  return SLRA_OK;
+}
+
 int slra_memcpy_d2d(slra_ctx ctx, void* d, const void* s, int64_t bytes) {
   if (bytes <= 0) return SLRA_OK;
   SLRA_CUDA(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, C(ctx)->stream));

@@ -2,6 +2,8 @@
 // points mirror the reference signatures; *_device entry points take raw
 // device pointers (e.g. torch tensor.data_ptr()) for HBM-resident runs.
 #include <chrono>
+#include <mutex>
+#include <unordered_map>
 
 #include <pybind11/complex.h>
 #include <pybind11/numpy.h>
@@ -38,6 +40,41 @@ static Matrix from_np(const FArray& a) {
 static FArray to_np(const Matrix& M) {
   FArray a({M.rows(), M.cols()});
   std::copy(M.data(), M.data() + M.size(), a.mutable_data());
+  return a;
+}
+// Result arrays of the host-buffer entry points, backed by page-locked
+// blocks: the D2H copy lands in the returned array at the link's rate (no
+// pageable staging, no second host copy). A block returns to a free list
+// keyed by size when its array dies, so steady-state calls allocate nothing.
+static std::mutex pin_mu;
+static std::unordered_multimap<size_t, void*>* pin_free = new std::unordered_multimap<size_t, void*>();
+static FArray pinned_np(Index rows, Index cols) {
+  const size_t bytes = sizeof(double) * static_cast<size_t>(rows) * static_cast<size_t>(cols);
+  void* p = nullptr;
+  {
+    std::lock_guard<std::mutex> g(pin_mu);
+    auto it = pin_free->find(bytes);
+    if (it != pin_free->end()) {
+      p = it->second;
+      pin_free->erase(it);
+    }
+  }
+  if (!p) check(slra_host_alloc(static_cast<int64_t>(bytes ? bytes : 8), &p), "pinned result buffer");
+  py::capsule hold(new std::pair<void*, size_t>(p, bytes), [](void* h) {
+    auto* ph = static_cast<std::pair<void*, size_t>*>(h);
+    {
+      std::lock_guard<std::mutex> g(pin_mu);
+      pin_free->emplace(ph->second, ph->first);
+    }
+    delete ph;
+  });
+  return FArray({rows, cols}, {static_cast<py::ssize_t>(sizeof(double)), static_cast<py::ssize_t>(sizeof(double) * rows)},
+                static_cast<double*>(p), hold);
+}
+static FArray download_pinned(const DeviceMatrix& M) {
+  if (M.ld() != M.rows()) return to_np(M.download());
+  FArray a = pinned_np(M.rows(), M.cols());
+  check(slra_memcpy_d2h(device_context(), a.mutable_data(), M.data(), 8 * M.rows() * M.cols()), "download");
   return a;
 }
 static py::array_t<double> vec_np(const Vector& v) {
@@ -615,7 +652,7 @@ PYBIND11_MODULE(_slra, m) {
     const auto o = out.download();
     py::list res;
     for (int s = 0; s < nsk; ++s)
-      res.append(py::make_tuple(to_np(dU[s].download()), to_np(dV[s].download()), o[2 * s], o[2 * s + 1]));
+      res.append(py::make_tuple(download_pinned(dU[s]), download_pinned(dV[s]), o[2 * s], o[2 * s + 1]));
     return res;
   });
 
