@@ -124,8 +124,14 @@ __global__ void __launch_bounds__(kCQ) chol_small_kernel(const double* __restric
       if (tid == 0) fail = 1;
       break;
     }
-    const double ljj = sqrt(piv);
-    const double inv = 1.0 / ljj;
+    // 1/sqrt(piv) from the hardware seed and two Newton steps (~1 ulp),
+    // L(j,j) = piv / sqrt(piv): no IEEE sqrt and division sequences on the
+    // column-to-column dependent chain
+    double inv = mufu_rsqrt(piv);
+    const double hp = 0.5 * piv;
+#pragma unroll
+    for (int it = 0; it < 2; ++it) inv = inv * fma(-hp * inv, inv, 1.5);
+    const double ljj = piv * inv;
     const bool row = ti > j && ti < NP;
     const double lij = row ? L[ti + j * ld] * inv : 0.0;
     double lcj[kQ], cur[kQ];
