@@ -9,6 +9,7 @@
 // A grid of such blocks is the batched superfast-multipole workload
 // (config 5; hss.cpp:47-55 pattern) with no inter-block communication.
 #include "dense_cta.cuh"
+#include "select_regs.cuh"
 
 namespace slra_dev {
 
@@ -34,6 +35,7 @@ struct CaParams {
   int mode;                  // 0 = cross_approx, 1 = primitive_cur only (I,J given in I_out/J_out)
   double* Tsig_out = nullptr;  // problem 0: T_r Sigma_r^-1 (l x r, ld l), nullable
   double* Sr_out = nullptr;    // problem 0: S_r (k x r, ld k), nullable
+  double* pairs = nullptr;     // nprob x 2: fused (||B - CUR||^2, ||B||^2) (nullable; needs m, n % 8 == 0)
 };
 
 // Shared-memory plan of one C-A block. Only S is strip-sized (mm x c): it
@@ -48,11 +50,15 @@ struct CaSmem {
   int64_t* ri;
 };
 
+__host__ __device__ inline size_t ca_even(size_t d) { return (d + 1) & ~(size_t)1; }
+
+// every region starts 16-byte aligned (the selection reads v as double2)
 __host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
-  // S (mm c + c), W (c+1) c, Gt (c+1) c, V (c+1) c, 4 c-vectors, nu/nd/rn (mm each), rv 40, volv + slack
-  size_t d = (size_t)mm * c + (size_t)c + 3 * (size_t)(c + 1) * c + 4 * (size_t)c +
-             3 * (size_t)mm + 40 + 8 + 2 * (size_t)c;
+  // S (mm c + c), W / Gt / V ((c+1) c each), tau / sigma / sgn (c), v (64),
+  // nu / nd / rn (mm each), rv 40, volv 8 + slack 2c
+  size_t d = ca_even((size_t)mm * ((c + 3) & ~3) + c) + 3 * ca_even((size_t)(c + 1) * c) + 3 * ca_even(c) + 64 +
+             3 * ca_even(mm > 16 ? mm : 16) + 40 + 8 + ca_even(2 * (size_t)c);
   size_t i = 2 * (size_t)mm + 5 * (size_t)c + 8;
   return d * 8 + 33 * 8 + i * 4 + 64;
 }
@@ -61,25 +67,26 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
   CaSmem s;
   double* d = reinterpret_cast<double*>(base);
-  s.S = d; d += (size_t)mm * c + c;
-  s.W = d; d += (size_t)(c + 1) * c;  // the nucleus' Jacobi operand (ld p | 1, p <= c)
+  s.S = d; d += ca_even((size_t)mm * ((c + 3) & ~3) + c);  // + the fused residual's Q fragments (n x 4 ceil(r/4))
+  s.W = d; d += ca_even((size_t)(c + 1) * c);  // the nucleus' Jacobi operand (ld p | 1, p <= c)
   s.R = nullptr;
-  s.Gt = d; d += (size_t)(c + 1) * c;  // room for the odd ld of the maxvol QR (rq | 1)
-  s.V = d; d += (size_t)(c + 1) * c;  // room for ld = q | 1
+  s.Gt = d; d += ca_even((size_t)(c + 1) * c);  // room for the odd ld of the maxvol QR (rq | 1)
+  s.V = d; d += ca_even((size_t)(c + 1) * c);  // room for ld = q | 1
   // the nucleus factors T_r Sigma_r^-1 and S_r are written after
   // cta_svd_finish, when the Jacobi operands V and W are dead
   s.Tm = s.V;
   s.Sm = s.W;
-  s.tau = d; d += c;
-  s.v = d; d += c;
-  s.sigma = d; d += c;
-  s.sgn = d; d += c;
-  s.nu = d; d += mm;
-  s.nd = d; d += mm;
-  s.rn = d; d += mm;
+  s.tau = d; d += ca_even(c);
+  s.v = d; d += 64;  // the selection's reflector: RMAX entries
+  s.sigma = d; d += ca_even(c);
+  s.sgn = d; d += ca_even(c);
+  const int mv = mm > 16 ? mm : 16;  // nu doubles as the selection's argmax slots
+  s.nu = d; d += ca_even(mv);
+  s.nd = d; d += ca_even(mv);
+  s.rn = d; d += ca_even(mv);
   s.rv = d; d += 40;
   s.volv = d; d += 8;
-  d += 2 * c;  // slack
+  d += ca_even(2 * (size_t)c);  // slack
   s.ri = reinterpret_cast<int64_t*>(d);
   int* ip = reinterpret_cast<int*>(s.ri + 33);
   s.p2r = ip; ip += mm;
@@ -139,19 +146,28 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
       s.rn[i] = sqrt(acc);
     }
   }
-  if (rq <= 16) cta_colpiv_init_regs<NT, 16>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx,
-                                     s.S, s.Gt, rq | 1, s.sigma);
-  else if (rq <= 32) cta_colpiv_init_regs<NT, 32>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx,
-                                     s.S, s.Gt, rq | 1, s.sigma);
-  else if constexpr (CMAX > 32)
-    cta_colpiv_init_regs<NT, 64>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx,
-                                     s.S, s.Gt, rq | 1, s.sigma);
-  __syncthreads();
-  // Gt with an odd leading dimension: warp_colpiv_qr gives each lane a
-  // column, and ld = rq (even) put all 32 lanes on the same shared bank
-  const int st = cta_maxvol_swaps<NT>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, s.S, len, s.Gt, rq | 1, s.perm, s.tau,
-                                      s.nu, s.nd, s.rv, s.ri, s.flag, s.volv, s.r2p, s.sigma);
-  if (st != SLRA_OK) return st;
+  double vol = 0.0;
+  if (rq <= 32) {
+    // pivoted-QR initialisation, maxvol round 0 and the swaps with the basis
+    // rows in registers (select_regs.cuh)
+    const SelScratch ss{s.nu, s.p2r, s.v, s.Gt, (rq + 1) & ~1, s.sigma, s.rv, s.tau, s.flag};
+    const int st = rq <= 16 ? cta_select_regs<NT, 16>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, ss)
+                            : cta_select_regs<NT, 32>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, ss);
+    if (st != SLRA_OK) return st;
+    vol = s.tau[1];
+  } else {
+    if constexpr (CMAX > 32)
+      cta_colpiv_init_regs<NT, 64>(s.S, len, len, rq, s.nu, s.nd, s.p2r, s.r2p, s.v, s.tau, s.rv, s.ri, s.tmpidx,
+                                   s.S, s.Gt, rq | 1, s.sigma);
+    __syncthreads();
+    // Gt with an odd leading dimension: warp_colpiv_qr gives each lane a
+    // column, and ld = rq (even) put all 32 lanes on the same shared bank
+    const int st = cta_maxvol_swaps<NT>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, s.S, len, s.Gt, rq | 1, s.perm,
+                                        s.tau, s.nu, s.nd, s.rv, s.ri, s.flag, s.volv, s.r2p, s.sigma);
+    if (st != SLRA_OK) return st;
+    __syncthreads();
+    vol = *s.volv;
+  }
   __syncthreads();
   for (int t = tid; t < rq; t += NT) idx_out[t] = s.tmpidx[t];
   __syncthreads();
@@ -174,7 +190,7 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
   if (vol_out) {
     // |det Q[idx, :]| = the swap loop's tracked volume (round-0 QR of G times
     // the pivot magnitudes of the swaps)
-    if (tid == 0) *vol_out = count == nidx ? *s.volv : 0.0;
+    if (tid == 0) *vol_out = count == nidx ? vol : 0.0;
     __syncthreads();
   }
   return SLRA_OK;
@@ -249,6 +265,122 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
   return SLRA_OK;
 }
 
+// ||B - P Q||_F^2 and ||B||_F^2 of one block inside the C-A kernel (the
+// residual of cur_evaluate, cur.cpp:76-82, with the nucleus factored:
+// C U R = (C T_r Sigma_r^-1)(S_r^T R) = P Q, inner dimension r). P (m x r) is
+// computed a row per thread and moved into DMMA A-fragments by shuffles
+// (warp w owns rows 32w..32w+31, exactly the rows its threads computed);
+// Q (r x n) a column per thread, stored in shared memory in the B-fragment
+// order ((n-tile, k-step) -> 32 consecutive doubles, one per lane: conflict
+// free). The block is then streamed once from global memory in C-fragment
+// order (8 rows x 4 column pairs per load: full sectors) and E = B - P Q is
+// formed by DMMA 8x8x4 with -P as the A operand. KS = k-steps (r <= 4 KS),
+// MTP = m-tiles per pass (a warp's 4 m-tiles in 4 / MTP passes).
+template <int NT, int KS, int MTP>
+__device__ void fused_block_residual(const double* A, int64_t lda, int m, int n, const int* I, int k, const int* J,
+                                     int l, const double* Tm, const double* Sm, int r, double* QS, double* red,
+                                     double* out_pair) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int RP = 4 * KS;
+  const int ksn = (r + 3) >> 2;  // k-steps in use (QS holds n x 4 ksn doubles)
+  // P(i, :) = A(i, J) Tm, row i = tid (zero for j >= r)
+  double p[RP];
+#pragma unroll
+  for (int j = 0; j < RP; ++j) p[j] = 0.0;
+  if (tid < m) {
+    for (int t = 0; t < l; ++t) {
+      const double c = __ldg(A + tid + (int64_t)J[t] * lda);
+#pragma unroll
+      for (int j = 0; j < RP; ++j)
+        if (j < r) p[j] = fma(c, Tm[t + j * l], p[j]);
+    }
+  }
+  // Q(:, col) = Sm^T A(I, col), col = tid, into the B-fragment layout
+  if (tid < n) {
+    double q[RP];
+#pragma unroll
+    for (int j = 0; j < RP; ++j) q[j] = 0.0;
+    for (int t = 0; t < k; ++t) {
+      const double a = __ldg(A + I[t] + (int64_t)tid * lda);
+#pragma unroll
+      for (int j = 0; j < RP; ++j)
+        if (j < r) q[j] = fma(Sm[t + j * k], a, q[j]);
+    }
+    const int nt = tid >> 3, g = tid & 7;
+#pragma unroll
+    for (int j = 0; j < RP; ++j)
+      if ((j >> 2) < ksn) QS[((nt * ksn) + (j >> 2)) * 32 + g * 4 + (j & 3)] = q[j];
+  }
+  __syncthreads();
+  const int g = lane >> 2, q4 = lane & 3;
+  double rs = 0.0, ns = 0.0;
+#pragma unroll
+  for (int pass = 0; pass < 4 / MTP; ++pass) {
+    // A-fragments of -P for this pass' m-tiles: lane (g, q4) of m-tile mt
+    // needs P(32 warp + 8 mt + g, 4 ks + q4), held by lane 8 mt + g as p[4 ks + q4]
+    double af[MTP][KS];
+#pragma unroll
+    for (int u = 0; u < MTP; ++u) {
+      const int src = 8 * (pass * MTP + u) + g;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        double v = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          const double t = __shfl_sync(0xffffffffu, p[4 * ks + qq], src);
+          if (qq == q4) v = t;
+        }
+        af[u][ks] = -v;
+      }
+    }
+    const int row0 = 32 * warp + 8 * pass * MTP;
+    if (row0 < m) {
+      for (int nt = 0; nt < (n >> 3); ++nt) {
+        double c[MTP][2];
+        const int col = 8 * nt + 2 * q4;
+#pragma unroll
+        for (int u = 0; u < MTP; ++u) {
+          const int row = row0 + 8 * u + g;
+          const bool ok = row < m;
+          c[u][0] = load_sel(A, row + (int64_t)col * lda, ok);
+          c[u][1] = load_sel(A, row + (int64_t)(col + 1) * lda, ok);
+          ns = fma(c[u][0], c[u][0], ns);
+          ns = fma(c[u][1], c[u][1], ns);
+        }
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          if (ks < ksn) {
+            const double bf = QS[(nt * ksn + ks) * 32 + lane];
+#pragma unroll
+            for (int u = 0; u < MTP; ++u) dmma_8x8x4(c[u][0], c[u][1], af[u][ks], bf);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < MTP; ++u) {
+          rs = fma(c[u][0], c[u][0], rs);
+          rs = fma(c[u][1], c[u][1], rs);
+        }
+      }
+    }
+  }
+  rs = warp_sum(rs);
+  ns = warp_sum(ns);
+  if (lane == 0) {
+    red[2 * warp] = rs;
+    red[2 * warp + 1] = ns;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b2 = 0.0;
+    for (int w = 0; w < NT / 32; ++w) {
+      a += red[2 * w];
+      b2 += red[2 * w + 1];
+    }
+    out_pair[0] = a;
+    out_pair[1] = b2;
+  }
+}
+
 // two resident CTAs per SM (<= 128 registers): the block is latency bound
 // CMAX = 32 (k, l <= 32): register variants sized for 32 columns so that
 // two CTAs fit an SM; CMAX = 64: one CTA per SM
@@ -296,6 +428,12 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
     for (int t = tid; t < P.l; t += kCT) P.J_out[(int64_t)b * P.l + t] = s.Jcur[t];
   }
   if (status != SLRA_OK) {
+    if (P.pairs) {  // a failed block's residual is ||B|| (r = 0)
+      __syncthreads();
+      fused_block_residual<kCT, 4, 4>(A, P.lda, P.m, P.n, s.Icur, P.k, s.Jcur, P.l, s.Tm, s.Sm, 0, s.S, s.rv,
+                                      P.pairs + 2 * (int64_t)b);
+      return;
+    }
     // zero the residual factors so a batched residual of a failed block is ||B||
     if (P.P) {
       for (int64_t e = tid; e < (int64_t)P.m * P.rq; e += kCT) P.P[(int64_t)b * P.m * P.rq + e] = 0.0;
@@ -314,6 +452,14 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
     double acc = 0.0;
     for (int j = 0; j < r; ++j) acc += s.Tm[a + j * P.l] * s.Sm[c + j * P.k];
     U[a + (int64_t)c * P.l] = acc;
+  }
+  if (P.pairs) {
+    __syncthreads();
+    if (r <= 16) fused_block_residual<kCT, 4, 4>(A, P.lda, P.m, P.n, s.Icur, P.k, s.Jcur, P.l, s.Tm, s.Sm, r, s.S,
+                                                 s.rv, P.pairs + 2 * (int64_t)b);
+    else fused_block_residual<kCT, 8, 2>(A, P.lda, P.m, P.n, s.Icur, P.k, s.Jcur, P.l, s.Tm, s.Sm, r, s.S, s.rv,
+                                         P.pairs + 2 * (int64_t)b);
+    return;
   }
   if (P.P) {
     // P = A(:,J) Tm (m x rq, zero beyond r), Q = Sm^T A(I,:) (rq x n). The
@@ -500,18 +646,23 @@ int slra_cross_approx_batched(slra_ctx ctx, const double* A, int64_t lda, int64_
   if (nblocks == 0) return SLRA_OK;
   Context* cx = C(ctx);
   const int rq = (int)(k < l ? k : l);
-  // per-block residual factors + result pairs in the workspace
-  const size_t fac = (size_t)nblocks * ((size_t)m * rq + (size_t)rq * n);
+  // k, l <= 32, m, n multiples of 8: the residual runs inside the C-A kernel
+  // (each block streamed once more from HBM, no factors written); otherwise
+  // per-block residual factors P, Q and a separate batched residual pass
+  const bool fused = k <= 32 && l <= 32 && m % 8 == 0 && n % 8 == 0 && m <= 256 && n <= 256;
+  const size_t fac = fused ? 0 : (size_t)nblocks * ((size_t)m * rq + (size_t)rq * n);
   double* ws = static_cast<double*>(workspace(cx, sizeof(double) * (fac + 2 * (size_t)nblocks)));
   if (!ws) return SLRA_ERR_CUDA;
-  double* Pf = ws;
-  double* Qf = ws + (size_t)nblocks * m * rq;
+  double* Pf = fused ? nullptr : ws;
+  double* Qf = fused ? nullptr : ws + (size_t)nblocks * m * rq;
   double* pairs = ws + fac;
   CaParams p{A, lda, stride, (int)m, (int)n, (int)r, (int)k, (int)l, loops, h, init_rows, I_out, J_out, nucleus,
              r_out, status, nullptr, nullptr, nullptr, Pf, Qf, rq, 0};
+  if (fused) p.pairs = pairs;
   SLRA_TRY(launch_ca_block(cx, p, (int)nblocks));
-  SLRA_TRY(launch_lowrank_residual_batched(cx, A, lda, stride, m, n, Pf, m, (int64_t)m * rq, Qf, rq,
-                                           (int64_t)rq * n, rq, nblocks, pairs));
+  if (!fused)
+    SLRA_TRY(launch_lowrank_residual_batched(cx, A, lda, stride, m, n, Pf, m, (int64_t)m * rq, Qf, rq,
+                                             (int64_t)rq * n, rq, nblocks, pairs));
   // split pairs -> resid_sq / norm_sq
   if (resid_sq) SLRA_CUDA(cudaMemcpy2DAsync(resid_sq, 8, pairs, 16, 8, nblocks, cudaMemcpyDeviceToDevice, cx->stream));
   if (norm_sq) SLRA_CUDA(cudaMemcpy2DAsync(norm_sq, 8, pairs + 1, 16, 8, nblocks, cudaMemcpyDeviceToDevice, cx->stream));

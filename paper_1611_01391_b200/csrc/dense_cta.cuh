@@ -26,7 +26,7 @@ constexpr double kEps = 2.220446049250313e-16;
 // Householder parts below, tau[0..min(m,c)). Warp w owns columns j = w mod
 // NW; the owner of column j+1 accumulates its next tail norm while applying
 // reflector j, so each column costs two block barriers. `red` >= c + 8.
-template <int NT, int RPL>
+template <int NT, int RPL, int CMAX = 64>
 __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
@@ -83,7 +83,7 @@ __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, do
     // this warp's columns right of j: k0, k0 + NW, ... — processed together
     // (one read of the reflector, interleaved butterflies)
     const int k0 = j + 1 + ((warp - (j + 1) % NW + NW) % NW);
-    constexpr int CPW = (64 + NW - 1) / NW;  // c <= 64
+    constexpr int CPW = (CMAX + NW - 1) / NW;  // c <= CMAX
     double xr[RPL];
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
@@ -132,11 +132,16 @@ __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, do
   }
 }
 
-template <int NT>
+template <int NT, int CMAX = 64>
 __device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, double* red) {
-  if (m <= 64) cta_house_qr_t<NT, 2>(A, lda, m, c, tau, red);
-  else if (m <= 256) cta_house_qr_t<NT, 8>(A, lda, m, c, tau, red);
-  else cta_house_qr_t<NT, 16>(A, lda, m, c, tau, red);  // m <= 512 (callers enforce)
+  if constexpr (CMAX <= 32) {  // c <= 32 (callers enforce): half the per-warp column slots
+    if (m <= 64) cta_house_qr_t<NT, 2, 32>(A, lda, m, c, tau, red);
+    else cta_house_qr_t<NT, 8, 32>(A, lda, m, c, tau, red);  // m <= 256
+  } else {
+    if (m <= 64) cta_house_qr_t<NT, 2>(A, lda, m, c, tau, red);
+    else if (m <= 256) cta_house_qr_t<NT, 8>(A, lda, m, c, tau, red);
+    else cta_house_qr_t<NT, 16>(A, lda, m, c, tau, red);  // m <= 512 (callers enforce)
+  }
 }
 
 // Explicit thin Q = H_0 H_1 ... H_{c-1} [I_c; 0] (m x c) from the reflectors
@@ -242,7 +247,8 @@ __device__ void cta_thin_qr(double* A, int lda, int m, int c, double* Q, int ldq
 // kept (the selection path only needs the basis). red >= c + 8 doubles.
 template <int NT, int CMAX = 64>
 __device__ void cta_thin_qr_inplace(double* A, int lda, int m, int c, double* tau, double* red) {
-  cta_house_qr<NT>(A, lda, m, c, tau, red);
+  if (CMAX <= 32 || c <= 32) cta_house_qr<NT, 32>(A, lda, m, c, tau, red);
+  else if constexpr (CMAX > 32) cta_house_qr<NT>(A, lda, m, c, tau, red);
   __syncthreads();
   for (int j = threadIdx.x; j < c; j += NT) red[j] = A[j + j * lda] < 0.0 ? -1.0 : 1.0;
   __syncthreads();

@@ -1,0 +1,279 @@
+// Row selection of select_rows_spanning (cur.cpp:88-135) on an orthonormal
+// strip basis Q (m x r, m <= NT, r <= RMAX), one row of Q per thread held in
+// registers for the whole selection:
+//
+//   1. ColPivHouseholderQR(Q^T) and its first r pivots (cur.cpp:95-98): the
+//      columns of Q^T are the rows of Q, so every thread owns one column of
+//      the factorisation. Eigen's column order is tracked as a per-thread
+//      position (the transposition k <-> big of step k is a register update
+//      in every thread), the pivot is the first maximum of the updated norms
+//      in that order, and the norms follow LAPACK xGEQP3's downdate with the
+//      sqrt(eps) recompute guard.
+//   2. maxvol round 0 (cur.cpp:100-106): B = Q G^-1 with G = Q(I,:) solved
+//      through ColPivQR(G^T). The pivots of step 1 are I in order, so that
+//      factorisation is step 1's (same columns, identity permutation): every
+//      thread applies every reflector to its own row (what the solve does to
+//      each right-hand side), then back-substitutes with R.
+//   3. The swap rounds (cur.cpp:107-114): argmax |B| in column-major order,
+//      first maximum wins; B is updated by the rank-1 formula (the same B the
+//      reference re-solves each round).
+//
+// Two block barriers per pivot step (argmax, reflector) and two per swap.
+// The reflector v of step k is kept with its unit head and zeros above it,
+// so the dot product and the update run over whole 8-wide chunks of the
+// register row (chunks entirely above k are skipped on a uniform branch)
+// with four independent accumulators.
+#pragma once
+
+#include "dense_cta.cuh"
+
+namespace slra_dev {
+
+struct SelScratch {
+  double* av;   // 2 * (NT / 32) argmax values (double-buffered)
+  int* ai;      // 2 * (NT / 32) argmax keys
+  double* v;    // RMAX: reflector of the current step
+  double* R;    // r x r (ld ldr, even, 16-byte aligned): R of ColPivQR(G^T), on and above the diagonal
+  int ldr;
+  double* pv;   // r: pivot norms (nonzero-pivot rule)
+  double* g;    // RMAX + 1: pivot-row snapshot of a swap round, [RMAX] = pivot value
+  double* tau;  // [0]: tau of the current step; [1]: volume
+  int* flag;    // [0]: SelectionFailure
+};
+
+__host__ __device__ constexpr size_t sel_scratch_doubles(int nt, int rmax) {
+  return 2 * (size_t)(nt / 32) + (size_t)rmax + (size_t)rmax * (rmax | 1) + rmax + rmax + 1 + 2;
+}
+
+struct ArgMaxI {
+  double v;
+  int i;
+};
+__device__ __forceinline__ ArgMaxI argmaxi_merge(ArgMaxI a, ArgMaxI b) {
+  return (b.v > a.v || (b.v == a.v && b.i < a.i)) ? b : a;
+}
+__device__ __forceinline__ ArgMaxI warp_argmaxi(ArgMaxI a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMaxI b;
+    b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+    b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+    a = argmaxi_merge(a, b);
+  }
+  return a;
+}
+// Block argmax with ONE barrier: warp results go to slot buffer `buf` and
+// every thread reduces the NW entries itself. Consecutive calls must
+// alternate `buf` (a slot is rewritten only after the next barrier).
+template <int NT>
+__device__ __forceinline__ ArgMaxI block_argmaxi(ArgMaxI a, double* av, int* ai, int buf) {
+  constexpr int NW = NT / 32;
+  a = warp_argmaxi(a);
+  if ((threadIdx.x & 31) == 0) {
+    av[buf * NW + (threadIdx.x >> 5)] = a.v;
+    ai[buf * NW + (threadIdx.x >> 5)] = a.i;
+  }
+  __syncthreads();
+  ArgMaxI r{av[buf * NW], ai[buf * NW]};
+#pragma unroll
+  for (int w = 1; w < NW; ++w) r = argmaxi_merge(r, ArgMaxI{av[buf * NW + w], ai[buf * NW + w]});
+  return r;
+}
+
+// Returns SLRA_OK / SLRA_ERR_SELECTION_FAILURE; I_out (smem, r entries) gets
+// the selected rows in order; the volume |det Q(I,:)| goes to s.tau[1].
+template <int NT, int RMAX>
+__device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h, int max_swaps, int* I_out,
+                               const SelScratch& s) {
+  static_assert(RMAX % 8 == 0, "chunked register rows");
+  constexpr int NCH = RMAX / 8;
+  const int tid = threadIdx.x;
+  const bool own = tid < m;
+  const double sqrt_eps = 1.4901161193847656e-08;
+  double x[RMAX];
+  double nu, nd;
+  {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int j = 0; j < RMAX; j += 4) {
+      x[j] = (own && j < r) ? Q[tid + j * ldq] : 0.0;
+      x[j + 1] = (own && j + 1 < r) ? Q[tid + (j + 1) * ldq] : 0.0;
+      x[j + 2] = (own && j + 2 < r) ? Q[tid + (j + 2) * ldq] : 0.0;
+      x[j + 3] = (own && j + 3 < r) ? Q[tid + (j + 3) * ldq] : 0.0;
+      a0 = fma(x[j], x[j], a0);
+      a1 = fma(x[j + 1], x[j + 1], a1);
+      a2 = fma(x[j + 2], x[j + 2], a2);
+      a3 = fma(x[j + 3], x[j + 3], a3);
+    }
+    nd = sqrt((a0 + a1) + (a2 + a3));
+    nu = nd;
+  }
+  int pos = tid;  // position of this row (= column of Q^T) in Eigen's permuted order
+  int buf = 0;
+  for (int k = 0; k < r; ++k) {
+    // ---- pivot: first maximum of the updated norms over positions >= k
+    const bool cand = own && pos >= k;
+    const ArgMaxI best = block_argmaxi<NT>(ArgMaxI{cand ? nu : -1.0, cand ? pos : INT32_MAX}, s.av, s.ai, buf);
+    buf ^= 1;
+    const int big = best.i;
+    if (pos == big) pos = k;
+    else if (pos == k) pos = big;
+    // ---- the winner builds H_k from its row's tail x[k..r) (Eigen makeHouseholder)
+    if (own && pos == k) {
+      double tail = 0.0, c0 = 0.0;
+#pragma unroll
+      for (int j = 0; j < RMAX; ++j) {
+        if (j == k) c0 = x[j];
+        if (j > k && j < r) tail = fma(x[j], x[j], tail);
+      }
+      double t, beta = c0, rden = 0.0;
+      if (tail <= DBL_MIN) {
+        t = 0.0;
+      } else {
+        beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        rden = 1.0 / (c0 - beta);
+        t = (beta - c0) / beta;
+      }
+#pragma unroll
+      for (int j = 0; j < RMAX; ++j) {
+        s.v[j] = j < k ? 0.0 : (j == k ? 1.0 : (j < r ? x[j] * rden : 0.0));
+        if (j < k) s.R[j + k * s.ldr] = x[j];  // R(0:k, k): this pivot column after H_0..H_{k-1}
+      }
+      s.R[k + k * s.ldr] = beta;
+      s.tau[0] = t;
+      s.pv[k] = best.v;
+      I_out[k] = tid;
+    }
+    __syncthreads();
+    // ---- apply H_k to every row (non-pivot rows: the factorisation; pivot
+    // rows: the solve's Q_g^T applied to that right-hand side)
+    const double t = s.tau[0];
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      if (8 * c + 7 >= k) {
+        const double2 v01 = *reinterpret_cast<const double2*>(s.v + 8 * c);
+        const double2 v23 = *reinterpret_cast<const double2*>(s.v + 8 * c + 2);
+        const double2 v45 = *reinterpret_cast<const double2*>(s.v + 8 * c + 4);
+        const double2 v67 = *reinterpret_cast<const double2*>(s.v + 8 * c + 6);
+        w0 = fma(v01.x, x[8 * c], w0);
+        w1 = fma(v01.y, x[8 * c + 1], w1);
+        w2 = fma(v23.x, x[8 * c + 2], w2);
+        w3 = fma(v23.y, x[8 * c + 3], w3);
+        w0 = fma(v45.x, x[8 * c + 4], w0);
+        w1 = fma(v45.y, x[8 * c + 5], w1);
+        w2 = fma(v67.x, x[8 * c + 6], w2);
+        w3 = fma(v67.y, x[8 * c + 7], w3);
+      }
+    }
+    const double tw = t * ((w0 + w1) + (w2 + w3));
+    double xk = 0.0, rest = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      if (8 * c + 7 >= k) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = 8 * c + u;
+          x[j] = fma(-tw, s.v[j], x[j]);
+          if (j == k) xk = x[j];
+        }
+      }
+    }
+    // ---- xGEQP3 norm downdate of the remaining candidates
+    if (own && pos > k && nu != 0.0) {
+      double temp = fabs(xk) / nu;
+      temp = (1.0 + temp) * (1.0 - temp);
+      temp = temp < 0.0 ? 0.0 : temp;
+      const double ratio = nu / nd;
+      if (temp * ratio * ratio <= sqrt_eps) {
+#pragma unroll
+        for (int j = 0; j < RMAX; ++j)
+          if (j > k && j < r) rest = fma(x[j], x[j], rest);
+        nd = sqrt(rest);
+        nu = nd;
+      } else {
+        nu = nu * sqrt(temp);
+      }
+    }
+  }
+  // ---- rank of R with the solve's threshold (ColPivQR(G^T), cur.cpp:103-106)
+  if (tid == 0) {
+    const double thr_helper = (s.pv[0] * kEps) * (s.pv[0] * kEps) / (double)r;
+    int nonzero = r;
+    double maxpivot = 0.0;
+    for (int k = 0; k < r; ++k) {
+      if (nonzero == r && s.pv[k] * s.pv[k] < thr_helper * (double)(r - k)) nonzero = k;
+      maxpivot = fmax(maxpivot, fabs(s.R[k + k * s.ldr]));
+    }
+    int rank = 0;
+    double vol = 1.0;
+    for (int i = 0; i < nonzero; ++i) rank += (fabs(s.R[i + i * s.ldr]) > maxpivot * 1e-12) ? 1 : 0;
+    for (int i = 0; i < r; ++i) vol *= fabs(s.R[i + i * s.ldr]);
+    s.flag[0] = rank < r ? 1 : 0;
+    s.tau[1] = vol;
+  }
+  if (tid < r) s.g[tid] = 1.0 / s.R[tid + tid * s.ldr];  // pivot reciprocals for the back substitution
+  __syncthreads();
+  if (s.flag[0]) return SLRA_ERR_SELECTION_FAILURE;
+  // ---- round 0: B(i,:) = R^-1 (Q_g^T a_i), column-oriented back substitution
+#pragma unroll
+  for (int tt = RMAX - 1; tt >= 0; --tt) {
+    if (tt < r) {
+      x[tt] *= s.g[tt];
+      const double2* rc = reinterpret_cast<const double2*>(s.R + tt * s.ldr);  // ldr even: 16-byte columns
+#pragma unroll
+      for (int u = 0; u < tt; u += 2) {
+        const double2 rr = rc[u >> 1];
+        x[u] = fma(-rr.x, x[tt], x[u]);
+        if (u + 1 < tt) x[u + 1] = fma(-rr.y, x[tt], x[u + 1]);
+      }
+    }
+    asm volatile("" ::: "memory");  // one column of R live at a time
+  }
+  // ---- swap rounds
+  double vol = s.tau[1];
+  for (int sw = 0; sw <= max_swaps; ++sw) {
+    ArgMaxI mine{-1.0, INT32_MAX};
+    if (own) {
+#pragma unroll
+      for (int tt = 0; tt < RMAX; ++tt) {
+        const double a = fabs(x[tt]);
+        if (tt < r && a > mine.v) {  // column-major order within the row: lower column first
+          mine.v = a;
+          mine.i = tt * m + tid;
+        }
+      }
+    }
+    const ArgMaxI best = block_argmaxi<NT>(mine, s.av, s.ai, buf);
+    buf ^= 1;
+    if (best.v <= h || sw == max_swaps) break;
+    const int j = best.i / m, piv = best.i % m;
+    if (tid == piv) {
+      double p = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < RMAX; ++tt)
+        if (tt == j) p = x[tt];
+#pragma unroll
+      for (int tt = 0; tt < RMAX; ++tt) s.g[tt] = x[tt] - (tt == j ? 1.0 : 0.0);
+      s.g[RMAX] = p;
+      I_out[j] = piv;
+    }
+    __syncthreads();
+    const double p = s.g[RMAX];
+    vol *= fabs(p);
+    double bij = 0.0;
+#pragma unroll
+    for (int tt = 0; tt < RMAX; ++tt)
+      if (tt == j) bij = x[tt];
+    const double f = bij / p;
+#pragma unroll
+    for (int tt = 0; tt < RMAX; ++tt) x[tt] = fma(-f, s.g[tt], x[tt]);
+  }
+  __syncthreads();
+  if (tid == 0) s.tau[1] = vol;
+  __syncthreads();
+  return SLRA_OK;
+}
+
+}  // namespace slra_dev
