@@ -283,16 +283,23 @@ __device__ void fused_block_residual(const double* A, int64_t lda, int m, int n,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int RP = 4 * KS;
   const int ksn = (r + 3) >> 2;  // k-steps in use (QS holds n x 4 ksn doubles)
+  constexpr int NB = KS <= 4 ? 8 : 2;  // global loads in flight per thread (register budget)
   // P(i, :) = A(i, J) Tm, row i = tid (zero for j >= r)
   double p[RP];
 #pragma unroll
   for (int j = 0; j < RP; ++j) p[j] = 0.0;
   if (tid < m) {
-    for (int t = 0; t < l; ++t) {
-      const double c = __ldg(A + tid + (int64_t)J[t] * lda);
+    for (int t0 = 0; t0 < l; t0 += NB) {
+      double c[NB];
 #pragma unroll
-      for (int j = 0; j < RP; ++j)
-        if (j < r) p[j] = fma(c, Tm[t + j * l], p[j]);
+      for (int u = 0; u < NB; ++u) c[u] = __ldg(A + tid + (int64_t)J[t0 + u < l ? t0 + u : l - 1] * lda);
+#pragma unroll
+      for (int u = 0; u < NB; ++u)
+        if (t0 + u < l) {
+#pragma unroll
+          for (int j = 0; j < RP; ++j)
+            if (j < r) p[j] = fma(c[u], Tm[t0 + u + j * l], p[j]);
+        }
     }
   }
   // Q(:, col) = Sm^T A(I, col), col = tid, into the B-fragment layout
@@ -300,11 +307,17 @@ __device__ void fused_block_residual(const double* A, int64_t lda, int m, int n,
     double q[RP];
 #pragma unroll
     for (int j = 0; j < RP; ++j) q[j] = 0.0;
-    for (int t = 0; t < k; ++t) {
-      const double a = __ldg(A + I[t] + (int64_t)tid * lda);
+    for (int t0 = 0; t0 < k; t0 += NB) {
+      double a[NB];
 #pragma unroll
-      for (int j = 0; j < RP; ++j)
-        if (j < r) q[j] = fma(Sm[t + j * k], a, q[j]);
+      for (int u = 0; u < NB; ++u) a[u] = __ldg(A + I[t0 + u < k ? t0 + u : k - 1] + (int64_t)tid * lda);
+#pragma unroll
+      for (int u = 0; u < NB; ++u)
+        if (t0 + u < k) {
+#pragma unroll
+          for (int j = 0; j < RP; ++j)
+            if (j < r) q[j] = fma(Sm[t0 + u + j * k], a[u], q[j]);
+        }
     }
     const int nt = tid >> 3, g = tid & 7;
 #pragma unroll
@@ -393,6 +406,14 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
   const double* A = P.A + (int64_t)b * P.stride;
   int status = SLRA_OK;
   if (P.mode == 0) {
+    if (P.pairs) {
+      // the block is read by every half-sweep's strip gather and by the fused
+      // residual: pull it into L2 once, in full lines, before the first gather
+      for (int j = tid; j < P.n * ((P.m + 15) / 16); j += kCT) {
+        const int c = j / ((P.m + 15) / 16), i = 16 * (j % ((P.m + 15) / 16));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(A + i + (int64_t)c * P.lda));
+      }
+    }
     for (int t = tid; t < P.k; t += kCT) s.Icur[t] = (int)P.init_rows[(int64_t)b * P.k + t];
     __syncthreads();
     for (int loop = 0; loop < P.loops && status == SLRA_OK; ++loop) {

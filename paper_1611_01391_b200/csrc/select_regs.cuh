@@ -120,12 +120,19 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
     else if (pos == k) pos = big;
     // ---- the winner builds H_k from its row's tail x[k..r) (Eigen makeHouseholder)
     if (own && pos == k) {
-      double tail = 0.0, c0 = 0.0;
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0, c0 = 0.0;
 #pragma unroll
-      for (int j = 0; j < RMAX; ++j) {
+      for (int j = 0; j < RMAX; j += 4) {  // four independent chains (FP64 FMA latency)
         if (j == k) c0 = x[j];
-        if (j > k && j < r) tail = fma(x[j], x[j], tail);
+        if (j + 1 == k) c0 = x[j + 1];
+        if (j + 2 == k) c0 = x[j + 2];
+        if (j + 3 == k) c0 = x[j + 3];
+        if (j > k && j < r) t0 = fma(x[j], x[j], t0);
+        if (j + 1 > k && j + 1 < r) t1 = fma(x[j + 1], x[j + 1], t1);
+        if (j + 2 > k && j + 2 < r) t2 = fma(x[j + 2], x[j + 2], t2);
+        if (j + 3 > k && j + 3 < r) t3 = fma(x[j + 3], x[j + 3], t3);
       }
+      const double tail = (t0 + t1) + (t2 + t3);
       double t, beta = c0, rden = 0.0;
       if (tail <= DBL_MIN) {
         t = 0.0;
