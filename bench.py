@@ -1,23 +1,29 @@
 #!/usr/bin/env python
 """bench.py — BASELINE.json metric "LRA matrix entries/s (sketch+CUR+residual)".
 
-Default workload (N=1 line): config 2 = configs[1] of BASELINE.json — range-
-finder LRA of a 4096 x 4096 fp64 A = U diag(sigma) V^T (sigma_j = 0.5^j, j<32,
-then 1e-12) sketched with l = 48 by (a) a sparse +-1 multiplier with 4 nonzeros
-per column and (b) an abridged Hadamard multiplier of depth 3 with random
-+-1 diagonal and column subsampling; rank-32 reconstruction (TruncatedRankR)
-and the ||A - U V||_F residual. One step = both multipliers over one A
-(2 x 4096^2 entries). `--config 1|5` run the other single-GPU workloads.
+Default workload (N=1 line): config 5 = configs[4] of BASELINE.json, the
+largest configuration that fits one GPU (BASELINE's metric names no config):
+65,536 independent 256 x 256 fp64 log-kernel blocks K_ij = log|p_i - q_j|
+(points uniform in two unit squares 4 apart, seeded per block with the
+reference Rng), each factorised by cross_approx (k = l = 32, 2 sweeps, rank
+r = numerical_rank(G, 1e-10) adaptive, i.e. the "rank-16 CUR" at its
+numerical rank) plus its Frobenius residual ||B - CUR||_F — the per-block
+ca_factors -> cross_approx -> cur_evaluate pattern of hss.cpp:47-55 /
+cur.cpp:80-82. One step = the whole batch (4.29 G entries, 34.4 GB in HBM).
+`--config 1|2|3|4` run the other configurations.
 
 Timing: W untimed warm-up steps, then K steps timed with CUDA events on the
 product's stream; an L2 flush (256 MiB write, > 126 MB L2) runs between timed
-steps outside the event pairs; barrier + synchronize on both sides; the max
-over ranks. N>1 (torchrun) runs one independent replica per GPU (config 2 does
-not shard: "replicas only") -> scaling "weak".
+steps outside the event pairs (config 5's inputs are also 270x the L2);
+barrier + synchronize on both sides; the max over ranks. With --gpus N and no
+WORLD_SIZE in the environment the script re-launches itself under
+torch.distributed.run with N ranks; config 5 then splits the blocks evenly
+over the ranks with no communication ("strong": the total work is fixed).
 
 `--impl reference` times the reference algorithm on the host CPU: the C++
-oracle restatement (oracle/, the reference itself cannot be built here:
-no Eigen) with all host threads, on the same config/metric.
+oracle restatement (oracle/; the reference itself cannot be built here: no
+Eigen) on a bounded sample of the same workload with all host threads, on
+the same config/metric/unit. Under torchrun only rank 0 runs it.
 """
 import argparse
 import json
@@ -44,11 +50,27 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--blocks", type=int, default=65536, help="config 5 block count")
+    p.add_argument("--e2e-steps", type=int, default=3, help="end-to-end (host buffers) steps (config 5)")
+    p.add_argument("--ref-blocks", type=int, default=1024, help="config-5 blocks per reference-arm step")
     return p.parse_args()
+
+
+def maybe_spawn(args):
+    """--gpus N without a torchrun environment: re-launch under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------- environment
@@ -127,15 +149,19 @@ def load_peaks():
     return peaks
 
 
-def profiled_traffic(config, kernel, tag="r01"):
+def profiled_traffic(config, kernel, tag="r01", blocks=None):
     """DRAM bytes (read + write) per launch of `kernel` from the committed
     `ncu --set full` capture (profiles/<tag>_c<config>_traffic.json, written by
-    tools/summarize_profiles.py), or None when not captured."""
+    tools/summarize_profiles.py), or None when not captured. Batched captures
+    record their block count; the bytes scale to `blocks`."""
     if kernel is None:
         return None
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", f"{tag}_c{config}_traffic.json")))
-        return d[kernel]["dram_bytes"]
+        d = json.load(open(os.path.join(ROOT, "profiles", f"{tag}_c{config}_traffic.json")))[kernel]
+        b = d["dram_bytes"]
+        if blocks and d.get("blocks"):
+            b *= blocks / d["blocks"]
+        return b
     except (OSError, ValueError, KeyError):
         return None
 
@@ -172,6 +198,12 @@ def run_reference(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return
+    if args.config == 5:
+        return run_reference_config5(args, ws)
+    if args.config != 2:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for configs 2 and 5 "
+                                                              f"(config {args.config} requested)"}), flush=True)
+        return
     import torch  # CPU only: input generation
     sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))
     import _oracle as oracle
@@ -202,8 +234,9 @@ def run_reference(args):
         "unit": "entries/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, config-2 recipe)",
-        "config": {"workload": "config2: range-finder LRA 4096x4096, l=48, sparse+-1(s=4) and ASPH(d=3), rank 32",
-                   "entries_per_step": 2 * N2 * N2},
+        "config": {"workload": "config2: range-finder LRA 4096x4096 fp64, l=48, sparse+-1 (s=4) and "
+                               "abridged Hadamard (d=3) multipliers, TruncatedRankR r=32, ||A-UV||_F",
+                   "entries_per_step": N2 * N2, "m": N2, "n": N2, "l": L_SKETCH, "r": RANK},
         "cpu_baseline": {"value": value, "unit": "entries/s", "cores": cores, "kind": "port",
                          "sample": "per step one config-2 LRA (multipliers alternate; n^2 entries), oracle/ C++ "
                                    "restatement, OpenMP over output columns"},
@@ -212,11 +245,85 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+C5_M, C5_K, C5_LOOPS = 256, 32, 2
+C5_WORKLOAD = ("config5: {blocks} batched 256x256 fp64 log-kernel blocks K_ij = log|p_i - q_j| (points in unit "
+               "squares 4 apart, seeded per block), cross_approx k=l=32, 2 sweeps, adaptive r = numerical_rank(G, "
+               "1e-10), + per-block ||B - CUR||_F")
+# SURVEY.md §8d, config 5, per block: residual 2*256*32*32 + 2*256*32*256 + 3*256^2 = 4.92 MFLOP, four strip
+# QRs of ~1 MFLOP; one pass over the block is 256*256*8 bytes
+C5_FLOPS_PER_BLOCK = 2.0 * 256 * 32 * 32 + 2.0 * 256 * 32 * 256 + 3.0 * 256 * 256 + 4 * 1.0e6
+C5_BYTES_PER_BLOCK = 8.0 * 256 * 256
+
+
+def config5_host_inputs(mod, seed, b0, nb):
+    """Points and initial rows of blocks b0..b0+nb-1 (reference Rng, per-block seeds)."""
+    m, k = C5_M, C5_K
+    px, py = np.empty((nb, m)), np.empty((nb, m))
+    qx, qy = np.empty((nb, m)), np.empty((nb, m))
+    init = np.empty((nb, k), dtype=np.int64)
+    mod.gen_log_kernel_batch(seed, b0, nb, m, m, k, px.ctypes.data, py.ctypes.data, qx.ctypes.data,
+                             qy.ctypes.data, init.ctypes.data)
+    return px, py, qx, qy, init
+
+
+def config5_host_blocks(px, py, qx, qy):
+    """Column-major blocks on the host, row-major (nb, n, m) array = each block K^T (numpy's log)."""
+    dx = px[:, None, :] - qx[:, :, None]
+    dy = py[:, None, :] - qy[:, :, None]
+    return 0.5 * np.log(dx * dx + dy * dy)
+
+
+def oracle_blocks(oracle, blocks, init, threads):
+    nb = blocks.shape[0]
+    return oracle.cross_approx_blocks(blocks.ctypes.data, nb, C5_M, C5_M, C5_M, C5_M * C5_M, init, C5_K, C5_K,
+                                      C5_LOOPS, 1.1, threads)
+
+
+def run_reference_config5(args, ws):
+    """The reference path (oracle/ C++ restatement: cross_approx -> numerical_rank -> primitive_cur ->
+    cur_evaluate per block) on the host cores, all threads, each step a bounded sample of the config-5 batch."""
+    import paper_1611_01391_b200 as slra  # host-side input generator only (no device work)
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))
+    import _oracle as oracle
+    cores = os.cpu_count() or 1
+    nb = min(args.ref_blocks, args.blocks)
+    px, py, qx, qy, init = config5_host_inputs(slra, args.seed, 0, nb)
+    blocks = np.ascontiguousarray(config5_host_blocks(px, py, qx, qy))
+    for _ in range(args.warmup):
+        oracle_blocks(oracle, blocks, init, cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_blocks(oracle, blocks, init, cores)
+    dt = time.perf_counter() - t0
+    value = nb * C5_M * C5_M * args.steps / dt
+    sample = (f"per step the first {nb} of the {args.blocks} config-5 blocks through the oracle/ C++ restatement of "
+              f"the reference path, blocks spread over {cores} OpenMP threads (the reference is single-threaded "
+              f"per block)")
+    line = {
+        "impl": "reference", "metric": "LRA matrix entries/s (sketch+CUR+residual)", "value": value,
+        "unit": "entries/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE config-5 recipe, reference Rng)",
+        "config": config5_config(args.blocks),
+        "cpu_baseline": {"value": value, "unit": "entries/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config5_config(blocks):
+    return {"workload": C5_WORKLOAD.format(blocks=blocks), "entries_per_step": blocks * C5_M * C5_M,
+            "blocks": blocks, "m": C5_M, "n": C5_M, "k": C5_K, "l": C5_K, "loops": C5_LOOPS}
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    rc = maybe_spawn(args)
+    if rc is not None:
+        sys.exit(rc)
     import torch
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -291,15 +398,29 @@ def main():
     roofline, kernels = work.roofline(fam, peaks, args.steps)
 
     # ---- end-to-end through the reference-facing API with host buffers
-    e2e = work.e2e(args.steps, args.warmup) if ws == 1 or scaling == "weak" else None
+    e2e = None
+    if hasattr(work, "e2e"):
+        e2e_steps = args.e2e_steps if args.config == 5 else args.steps
+        if ws == 1 or scaling == "weak" or args.config == 5:
+            barrier()
+            e2e = work.e2e(e2e_steps, args.warmup)
+            if e2e is not None and ws > 1 and scaling == "strong":
+                # every rank streamed its own share: the job's time is the slowest rank's
+                dt = torch.tensor([work.entries_per_step * e2e_steps / ws / e2e["value"]], dtype=torch.float64,
+                                  device="cuda")
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+                e2e["value"] = work.entries_per_step * e2e_steps / float(dt.item())
+                e2e["h2d_bytes_per_step"] *= ws
+                e2e["d2h_bytes_per_step"] *= ws
 
     line = {
         "metric": "LRA matrix entries/s (sketch+CUR+residual)", "value": value, "unit": "entries/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": getattr(work, "data", "synthetic (seeded; same recipe as BASELINE.json config)"),
-        "config": dict(work.config, l2="256 MiB flush between timed steps (outside the event pairs)",
-                       parallelism=getattr(work, "parallelism", f"replicas x{ws} (no data-path collective)")),
+        "config": work.config,
+        "parallelism": getattr(work, "parallelism", f"replicas x{ws} (no data-path collective)"),
+        "l2": "256 MiB flush between timed steps (outside the event pairs)",
         "roofline": roofline, "kernels_ms_per_step": kernels,
         "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
         "residual_rel": work.last_residual_rel(),
@@ -811,98 +932,144 @@ class Config4:
 
 
 class Config5:
-    """Config 5: batched superfast-multipole LRA, 256x256 log-kernel blocks, k=l=32, adaptive r<=16, 2 sweeps."""
+    """Config 5: batched superfast-multipole LRA — 65,536 independent 256 x 256 log-kernel blocks,
+    cross_approx k = l = 32, 2 sweeps, adaptive r, fused per-block residual. N ranks split the
+    blocks evenly (no communication)."""
 
     CHUNK = 4096
 
     def __init__(self, slra, torch, seed, blocks, comm):
         from paper_1611_01391_b200 import shard
-        self.slra, self.torch = slra, torch
+        self.slra, self.torch, self.seed, self.blocks = slra, torch, seed, blocks
         ws = comm.world
         self.b0, self.nb = shard.split(blocks, ws, comm.rank)
         self.scaling = "weak" if ws == 1 else "strong"
-        if ws > 1:
-            self.parallelism = f"block-split x{ws}: {self.nb} blocks per rank, no communication"
-        m = 256
-        # device-side generation of the blocks from seeded points, per chunk
-        # of 4096 blocks so every rank builds exactly its blocks of the same
-        # global set (log on the GPU differs from glibc's in the last ulp;
-        # parity tests use host-generated blocks)
-        self.A = torch.empty(self.nb, m, m, dtype=torch.float64, device="cuda")
-        self.init = torch.empty(self.nb, 32, dtype=torch.int64, device="cuda")
-        c_lo, c_hi = self.b0 // self.CHUNK, (self.b0 + self.nb + self.CHUNK - 1) // self.CHUNK
-        for c in range(c_lo, c_hi):
-            g = torch.Generator().manual_seed(seed * 1000003 + c)
-            P = torch.rand(self.CHUNK, m, 2, dtype=torch.float64, generator=g)
-            Q = torch.rand(self.CHUNK, m, 2, dtype=torch.float64, generator=g)
-            Q[..., 0] += 4.0
-            init = torch.argsort(torch.rand(self.CHUNK, m, generator=g), dim=1)[:, :32]
-            lo, hi = max(self.b0, c * self.CHUNK), min(self.b0 + self.nb, (c + 1) * self.CHUNK)
-            if lo >= hi:
-                continue
-            p = P[lo - c * self.CHUNK:hi - c * self.CHUNK].cuda()
-            q = Q[lo - c * self.CHUNK:hi - c * self.CHUNK].cuda()
-            d = p[:, None, :, :] - q[:, :, None, :]  # [b, j, i, 2] -> A^T[j, i] = K(i, j): col-major K
-            self.A[lo - self.b0:hi - self.b0] = 0.5 * torch.log((d * d).sum(-1))
-            self.init[lo - self.b0:hi - self.b0] = init[lo - c * self.CHUNK:hi - c * self.CHUNK].cuda()
-        nb = self.nb
-        self.I = torch.zeros(nb, 32, dtype=torch.int64, device="cuda")
-        self.J = torch.zeros(nb, 32, dtype=torch.int64, device="cuda")
-        self.U = torch.zeros(nb, 32 * 32, dtype=torch.float64, device="cuda")
+        self.parallelism = f"block-split x{ws}: {self.nb} blocks per rank, no communication"
+        m, nb = C5_M, self.nb
+        # inputs: per-block points + initial rows from the reference Rng (host, the
+        # same recipe as the oracle/tests), blocks materialised on the device
+        self.A = torch.empty(nb, m, m, dtype=torch.float64, device="cuda")
+        self.init = torch.empty(nb, C5_K, dtype=torch.int64, device="cuda")
+        for c0 in range(0, nb, self.CHUNK):
+            c = min(self.CHUNK, nb - c0)
+            px, py, qx, qy, init = config5_host_inputs(slra, seed, self.b0 + c0, c)
+            dev = [torch.from_numpy(a).cuda() for a in (px, py, qx, qy)]
+            slra.gen_log_kernel_blocks_device(*[d.data_ptr() for d in dev], c, m, m, self.A[c0].data_ptr(), m, m * m)
+            self.init[c0:c0 + c] = torch.from_numpy(init).cuda()
+        torch.cuda.synchronize()
+        self.I = torch.zeros(nb, C5_K, dtype=torch.int64, device="cuda")
+        self.J = torch.zeros(nb, C5_K, dtype=torch.int64, device="cuda")
+        self.U = torch.zeros(nb, C5_K * C5_K, dtype=torch.float64, device="cuda")
         self.r = torch.zeros(nb, dtype=torch.int64, device="cuda")
         self.st = torch.zeros(nb, dtype=torch.int32, device="cuda")
         self.rs = torch.zeros(nb, dtype=torch.float64, device="cuda")
         self.ns = torch.zeros(nb, dtype=torch.float64, device="cuda")
         self.entries_per_step = blocks * m * m  # the whole job (all ranks)
-        self.config = {"workload": f"config5: {blocks} batched 256x256 log-kernel blocks, k=l=32, adaptive r "
-                                   f"(numerical_rank 1e-10), 2 C-A sweeps + per-block residual",
-                       "entries_per_step": self.entries_per_step, "blocks_per_rank": nb}
+        self.data = "synthetic (seeded; BASELINE config-5 recipe: per-block reference Rng, blocks materialised on device)"
+        self.config = config5_config(blocks)
 
     def step(self):
-        self.slra.cross_approx_batched_device(self.A.data_ptr(), 256, 256 * 256, self.nb, 256, 256, 0, 32, 32,
-                                              self.init.data_ptr(), 2, 1.1, self.I.data_ptr(), self.J.data_ptr(),
-                                              self.U.data_ptr(), self.r.data_ptr(), self.st.data_ptr(),
-                                              self.rs.data_ptr(), self.ns.data_ptr())
+        self.slra.cross_approx_batched_device(self.A.data_ptr(), C5_M, C5_M * C5_M, self.nb, C5_M, C5_M, 0, C5_K,
+                                              C5_K, self.init.data_ptr(), C5_LOOPS, 1.1, self.I.data_ptr(),
+                                              self.J.data_ptr(), self.U.data_ptr(), self.r.data_ptr(),
+                                              self.st.data_ptr(), self.rs.data_ptr(), self.ns.data_ptr())
 
     def last_residual_rel(self):
-        return float(((self.rs / self.ns).sqrt()).max().item())
+        rel = (self.rs / self.ns).sqrt()
+        return {"max": float(rel.max().item()), "median": float(rel.median().item()),
+                "failed_blocks": int((self.st != 0).sum().item()),
+                "r_hist": {int(v): int(c) for v, c in zip(*torch_unique(self.torch, self.r))}}
 
     def cpu_baseline(self):
-        """The oracle's per-block C-A (cross_approx with the block's own initial
-        rows, the adaptive rank through numerical_rank + primitive_cur) and its
-        Frobenius residual on the first blocks for ~10 s, extrapolated per entry
-        (a stated block subset)."""
+        """The oracle (reference path restated: cross_approx -> numerical_rank -> primitive_cur ->
+        cur_evaluate) on a bounded sample of the same blocks (read back from HBM): ~10 s single-threaded
+        (the reference runs one block per thread) and the same sample over all host cores."""
         sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))
         import _oracle as oracle
-        A = self.A[:256].cpu().numpy()
-        init = self.init[:256].cpu().numpy()
-        n = 0
+        cores = os.cpu_count() or 1
+        nall = min(self.nb, 8192)
+        A_all = np.ascontiguousarray(self.A[:nall].cpu().numpy())
+        init_all = self.init[:nall].cpu().numpy()
+        A, init = A_all[:1024], init_all[:1024]
+        # single thread: grow the sample until ~10 s
+        n, dt1 = 16, 0.0
+        while True:
+            t0 = time.perf_counter()
+            oracle_blocks(oracle, A[:n], init[:n], 1)
+            dt1 = time.perf_counter() - t0
+            if dt1 > 3.0 or n >= A.shape[0]:
+                break
+            n = min(A.shape[0], n * 4)
         t0 = time.perf_counter()
-        while time.perf_counter() - t0 < 10.0 and n < A.shape[0]:
-            Kb = np.ascontiguousarray(A[n].T)  # block n, column-major on the device
-            o = oracle.cross_approx(Kb, 1, 32, 32, init[n].tolist(), 2, 1.1, None, oracle.Rng(0))
-            rk = oracle.numerical_rank(Kb[np.ix_(o["I"], o["J"])], 1e-10, True)
-            ro = oracle.primitive_cur(Kb, o["I"], o["J"], rk)
-            oracle.cur_evaluate(Kb, o["I"], o["J"], ro["nucleus"])
-            n += 1
-        dt = time.perf_counter() - t0
-        return {"value": n * 256 * 256 / dt, "unit": "entries/s", "cores": 1, "kind": "port",
-                "sample": f"{n} of the config-5 blocks through the oracle/ restatement (C-A, adaptive-rank "
-                          f"nucleus, residual), single-threaded, {dt:.1f} s; blocks are independent, so the "
-                          f"rate extrapolates linearly"}
+        oracle_blocks(oracle, A_all, init_all, cores)
+        dtn = time.perf_counter() - t0
+        return {"value": n * C5_M * C5_M / dt1, "unit": "entries/s", "cores": 1, "kind": "port",
+                "sample": f"the first {n} config-5 blocks (read back from HBM) through the oracle/ C++ restatement "
+                          f"of the reference path, one thread ({dt1:.1f} s); blocks are independent, so the rate "
+                          f"extrapolates linearly",
+                "all_cores": {"value": nall * C5_M * C5_M / dtn, "cores": cores,
+                              "sample": f"the first {nall} blocks, one block per OpenMP thread ({dtn:.1f} s)"}}
 
     def roofline(self, fam, peaks, steps):
         kernels = {k: v[0] / steps for k, v in fam.items()}
         top = max(fam.items(), key=lambda kv: kv[1][0])[0]
-        per = fam[top][0] / max(fam[top][1], 1)
-        byts = 8.0 * self.nb * 256 * 256
-        ach = byts / (per * 1e-3) / 1e9
-        return {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": None}, kernels
+        per = fam[top][0] / max(fam[top][1], 1)  # ms per launch
+        flops = C5_FLOPS_PER_BLOCK * self.nb
+        ach = flops / (per * 1e-3) / 1e12
+        byts = C5_BYTES_PER_BLOCK * self.nb
+        traffic = profiled_traffic(5, "ca_block_kernel", tag="r02", blocks=self.nb)
+        return {"kernel": top + " (ca_block_kernel)", "bound": "tensor", "achieved": ach,
+                "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                "frac": ach / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
+                "peak_source": peaks["fp64_source"],
+                "algorithmic_per_launch": {"flops": flops, "bytes": byts,
+                                           "basis": "SURVEY.md 8d config 5: 8.92 MFLOP and 512 KiB per block"},
+                "traffic": traffic,
+                "hbm_view": {"achieved_gbs": byts / (per * 1e-3) / 1e9,
+                             "frac": byts / (per * 1e-3) / 1e9 / peaks["hbm_gbs"], "peak": peaks["hbm_gbs"]},
+                "note": "FP64 latency-bound: one CTA per block (two per SM) runs the C-A chain (strip QR, "
+                        "pivoted QR, maxvol, Jacobi SVD) and the DMMA residual; see DESIGN.md 5 and profiles/"}, kernels
 
     def e2e(self, steps, warmup):
-        return None
+        """The batch through the host-buffer entry (slra_cross_approx_batched_host): pinned host blocks
+        streamed to the device in chunks overlapped with the kernels, every result copied back."""
+        torch = self.torch
+        nb = self.nb
+        host = torch.empty(nb * C5_M * C5_M, dtype=torch.float64, pin_memory=True)
+        for c0 in range(0, nb, self.CHUNK):
+            c = min(self.CHUNK, nb - c0)
+            host[c0 * C5_M * C5_M:(c0 + c) * C5_M * C5_M].copy_(self.A[c0:c0 + c].reshape(-1))
+        init = self.init.cpu().pin_memory()
+        outs = [torch.empty(nb, C5_K, dtype=torch.int64, pin_memory=True),
+                torch.empty(nb, C5_K, dtype=torch.int64, pin_memory=True),
+                torch.empty(nb, C5_K * C5_K, dtype=torch.float64, pin_memory=True),
+                torch.empty(nb, dtype=torch.int64, pin_memory=True),
+                torch.empty(nb, dtype=torch.int32, pin_memory=True),
+                torch.empty(nb, dtype=torch.float64, pin_memory=True),
+                torch.empty(nb, dtype=torch.float64, pin_memory=True)]
 
+        def one():
+            self.slra.cross_approx_batched_host(host.data_ptr(), C5_M, C5_M * C5_M, nb, C5_M, C5_M, 0, C5_K, C5_K,
+                                                init.data_ptr(), C5_LOOPS, 1.1, *[o.data_ptr() for o in outs])
+        one()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        dt = time.perf_counter() - t0
+        ok = bool(torch.equal(outs[0], self.I.cpu()) and torch.equal(outs[1], self.J.cpu()))
+        d2h = nb * (8 * 2 * C5_K + 8 * C5_K * C5_K + 8 + 4 + 16)
+        return {"value": self.nb * C5_M * C5_M * steps / dt, "unit": "entries/s",
+                "h2d_bytes_per_step": nb * (8 * C5_M * C5_M + 8 * C5_K), "d2h_bytes_per_step": d2h,
+                "steps": steps, "same_I_J_as_device_run": ok,
+                "api": "paper_1611_01391_b200.cross_approx_batched_host -> slra_cross_approx_batched_host "
+                       "(pinned host blocks in, chunked H2D overlapped with the C-A kernels; I, J, nucleus, r, "
+                       "status, residuals out)"}
+
+
+def torch_unique(torch, t):
+    v, c = torch.unique(t, return_counts=True)
+    return v.tolist(), c.tolist()
 
 
 if __name__ == "__main__":

@@ -170,15 +170,40 @@ int slra_cross_approx(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, i
                       int64_t* d_trace_rows, int64_t* d_trace_cols, double* d_trace_volume,
                       double* d_Tsig, double* d_Sr, int64_t* h_r_out);
 /* Batched cross_approx + per-block Frobenius residual: nblocks independent
- * m x n blocks at d_A + b*block_stride (ld = lda); one CTA per block.
- * Per-block outputs: I (k), J (l), nucleus (l x k), r, status (slra_status),
- * resid_sq = ||B - C U R||_F^2, norm_sq = ||B||_F^2. Strips must fit on
- * chip (m, n <= 512, k, l <= 32). */
+ * m x n blocks at d_A + b*block_stride (ld = lda); one CTA per block (the
+ * per-block ca_factors -> cross_approx -> cur_evaluate pattern of
+ * hss.cpp:47-55 and cur.cpp:80-82). Per-block outputs: I (k), J (l),
+ * nucleus (l x k), r, status (slra_status), resid_sq = ||B - C U R||_F^2,
+ * norm_sq = ||B||_F^2. Strips must fit on one SM: m, n <= 256, k, l <= 64.
+ * With k, l <= 32 and m, n multiples of 8 the residual is computed inside
+ * the C-A kernel (one more pass over each block, no factors written). */
 int slra_cross_approx_batched(slra_ctx ctx, const double* d_A, int64_t lda, int64_t block_stride,
                               int64_t nblocks, int64_t m, int64_t n, int64_t r, int64_t k,
                               int64_t l, const int64_t* d_init_rows, int loops, double h,
                               int64_t* d_I, int64_t* d_J, double* d_nucleus, int64_t* d_r,
                               int32_t* d_status, double* d_resid_sq, double* d_norm_sq);
+
+/* The same over blocks in HOST memory (h_A, block b at h_A + b*block_stride),
+ * the end-to-end form a host caller uses: the blocks are streamed to the
+ * device in chunks on a copy stream, each chunk's C-A kernel overlapping the
+ * next chunk's host-to-device copy, and the per-block results are copied
+ * back into the h_* arrays (same layouts as above). Page-locked h_A makes
+ * the copies asynchronous. Blocks until every result is on the host. */
+int slra_cross_approx_batched_host(slra_ctx ctx, const double* h_A, int64_t lda, int64_t block_stride,
+                                   int64_t nblocks, int64_t m, int64_t n, int64_t r, int64_t k,
+                                   int64_t l, const int64_t* h_init_rows, int loops, double h,
+                                   int64_t* h_I, int64_t* h_J, double* h_nucleus, int64_t* h_r,
+                                   int32_t* h_status, double* h_resid_sq, double* h_norm_sq);
+
+/* ------------------------------------------------------------ a13 input generator
+ * Config-5 log-kernel blocks (testgen: K_ij = log|p_i - q_j| =
+ * 0.5 log(dx^2 + dy^2), FunctionOracle recipe oracle.hpp:43-54) materialised
+ * on the device from per-block points drawn on the host: block b reads
+ * d_px/d_py[b*m + i], d_qx/d_qy[b*n + j] and writes d_A + b*block_stride
+ * (column-major, ld = lda). Untimed setup, not the hot path. */
+int slra_gen_log_kernel_blocks(slra_ctx ctx, const double* d_px, const double* d_py, const double* d_qx,
+                               const double* d_qy, int64_t nblocks, int64_t m, int64_t n, double* d_A,
+                               int64_t lda, int64_t block_stride);
 
 /* ------------------------------------------------------------ a9 residual
  * ||A - P Q||_F^2 and ||A||_F^2 in one pass over A (FP64 DMMA tiles fused

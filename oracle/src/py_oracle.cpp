@@ -202,6 +202,70 @@ PYBIND11_MODULE(_oracle, m) {
     return d;
   }, py::arg("A"), py::arg("r"), py::arg("k"), py::arg("l"), py::arg("init_rows"), py::arg("loops"),
      py::arg("h"), py::arg("stop_tol"), py::arg("rng"));
+  // The config-5 batch through the restated reference path, block by block
+  // (hss.cpp:47-55 pattern: cross_approx -> adaptive-rank primitive_cur ->
+  // cur_evaluate), blocks spread over `threads` OpenMP threads (the reference
+  // itself is single-threaded; threads = 1 is its literal execution). Block b
+  // is the m x n column-major matrix at A + b*stride (ld = lda); host memory.
+  m.def("cross_approx_blocks", [](uintptr_t Aptr, Index nb, Index mm, Index n, Index lda, Index stride,
+                                  const py::array_t<Index, py::array::c_style | py::array::forcecast>& inits, Index k,
+                                  Index l, int loops, double h, int threads) {
+    const double* A = reinterpret_cast<const double*>(Aptr);
+    py::array_t<Index> I({nb, k}), J({nb, l}), rr(nb);
+    py::array_t<double> rs(nb), ns(nb);
+    py::array_t<int> st(nb);
+    const Index* ini = inits.data();
+    Index* Ip = I.mutable_data();
+    Index* Jp = J.mutable_data();
+    Index* rp = rr.mutable_data();
+    double* rsp = rs.mutable_data();
+    double* nsp = ns.mutable_data();
+    int* stp = st.mutable_data();
+    {
+      py::gil_scoped_release nogil;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+      for (Index b = 0; b < nb; ++b) {
+        Matrix M(mm, n);
+        for (Index j = 0; j < n; ++j)
+          for (Index i = 0; i < mm; ++i) M(i, j) = A[b * stride + i + j * lda];
+        double nrm = 0;
+        for (double v : M.v) nrm += v * v;
+        nsp[b] = nrm;
+        try {
+          DenseOracle o(M);
+          Rng rng(0);
+          std::vector<Index> init(ini + b * k, ini + (b + 1) * k);
+          auto res = cross_approx(o, 1, k, l, IndexSet(init, mm), loops, h, std::nullopt, rng);
+          const auto& Is = res.first.row_set.indices();
+          const auto& Js = res.first.col_set.indices();
+          Matrix G(k, l);
+          for (Index j = 0; j < l; ++j)
+            for (Index i = 0; i < k; ++i) G(i, j) = M(Is[static_cast<size_t>(i)], Js[static_cast<size_t>(j)]);
+          const Index rk = numerical_rank(G, 1e-10, RankMode::Relative);
+          CurDecomposition c = primitive_cur(M, res.first.row_set, res.first.col_set, rk);
+          const double e = cur_evaluate(M, c, NormKind::Frobenius);
+          for (Index i = 0; i < k; ++i) Ip[b * k + i] = Is[static_cast<size_t>(i)];
+          for (Index j = 0; j < l; ++j) Jp[b * l + j] = Js[static_cast<size_t>(j)];
+          rp[b] = rk;
+          rsp[b] = e * e;
+          stp[b] = 0;
+        } catch (const std::exception&) {
+          rp[b] = 0;
+          rsp[b] = nrm;
+          stp[b] = 1;
+        }
+      }
+    }
+    py::dict d;
+    d["I"] = I;
+    d["J"] = J;
+    d["r"] = rr;
+    d["resid_sq"] = rs;
+    d["norm_sq"] = ns;
+    d["status"] = st;
+    return d;
+  }, py::arg("A"), py::arg("nblocks"), py::arg("m"), py::arg("n"), py::arg("lda"), py::arg("stride"),
+     py::arg("inits"), py::arg("k"), py::arg("l"), py::arg("loops"), py::arg("h"), py::arg("threads") = 1);
   m.def("cur_reconstruct", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J,
                               const FArray& U) {
     Matrix M = from_np(A);

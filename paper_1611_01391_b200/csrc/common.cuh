@@ -49,13 +49,16 @@ __device__ __forceinline__ void jacobi_rotation(double a, double b, double g, do
 
 
 // ------------------------------------------------------------------ context
-constexpr int kArenaSlots = 12;
+constexpr int kArenaSlots = 13;
 
 struct Context {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   bool owns_stream = false;
+  // copy streams + events of the host-streamed batched C-A (created on first use)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev[6] = {};
   int64_t launches = 0;
   // growable scratch (device) and pinned host scratch
   void* ws = nullptr;
@@ -72,7 +75,7 @@ struct Context {
   // independent growable device arenas for multi-kernel orchestrations
   // (0: range finder, 1: cur residual, 2: lsr, 3: svd, 4: large C-A, 5: factored residual,
   //  6: wide-svd transpose, 7: tall maxvol/select, 8: pinv, 9: premult / two-stage truncate,
-  //  10: large (multi-CTA Jacobi) svd, 11: hss)
+  //  10: large (multi-CTA Jacobi) svd, 11: hss, 12: host-streamed batched C-A)
   void* arena[kArenaSlots] = {};
   size_t arena_bytes[kArenaSlots] = {};
   // opt-in per-kernel-family timing (CUDA events on the context stream)

@@ -8,6 +8,8 @@
 //   C U R = P Q and ||A - C U R||_F runs with inner dimension r.
 // A grid of such blocks is the batched superfast-multipole workload
 // (config 5; hss.cpp:47-55 pattern) with no inter-block communication.
+#include <algorithm>
+
 #include "dense_cta.cuh"
 #include "select_regs.cuh"
 
@@ -687,6 +689,83 @@ int slra_cross_approx_batched(slra_ctx ctx, const double* A, int64_t lda, int64_
   // split pairs -> resid_sq / norm_sq
   if (resid_sq) SLRA_CUDA(cudaMemcpy2DAsync(resid_sq, 8, pairs, 16, 8, nblocks, cudaMemcpyDeviceToDevice, cx->stream));
   if (norm_sq) SLRA_CUDA(cudaMemcpy2DAsync(norm_sq, 8, pairs + 1, 16, 8, nblocks, cudaMemcpyDeviceToDevice, cx->stream));
+  return SLRA_OK;
+}
+
+int slra_cross_approx_batched_host(slra_ctx ctx, const double* h_A, int64_t lda, int64_t stride, int64_t nblocks,
+                                   int64_t m, int64_t n, int64_t r, int64_t k, int64_t l, const int64_t* h_init,
+                                   int loops, double h, int64_t* h_I, int64_t* h_J, double* h_nucleus, int64_t* h_r,
+                                   int32_t* h_status, double* h_resid_sq, double* h_norm_sq) {
+  if (!ctx || !h_A || !h_init || lda < m || loops < 1 || k < 1 || l < 1 || nblocks < 0 || stride < lda * n ||
+      (r > 0 && (k < r || l < r)))
+    return SLRA_ERR_INVALID_ARGUMENT;
+  if (!ca_fits((int)m, (int)n, (int)k, (int)l)) return SLRA_ERR_UNSUPPORTED;
+  if (nblocks == 0) return SLRA_OK;
+  Context* cx = C(ctx);
+  if (!cx->h2d) {
+    SLRA_CUDA(cudaStreamCreateWithFlags(&cx->h2d, cudaStreamNonBlocking));
+    SLRA_CUDA(cudaStreamCreateWithFlags(&cx->d2h, cudaStreamNonBlocking));
+    for (auto& e : cx->ev) SLRA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // two chunk buffers of ~1 GiB of blocks each: chunk c+1 crosses the bus
+  // while chunk c is factorised and chunk c-1's results come back
+  const int64_t blk = stride * 8;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nblocks, (int64_t(1) << 30) / blk));
+  const int64_t outd = l * k + 2;  // nucleus + (resid_sq, norm_sq) per block
+  const int64_t outi = k + l + 1;  // I, J, r per block
+  const size_t per = (size_t)chunk * (stride + outd + outi) + (size_t)chunk * k + (size_t)chunk;  // + init, status
+  char* base = static_cast<char*>(arena(cx, 12, 2 * per * 8 + 1024));
+  if (!base) return SLRA_ERR_CUDA;
+  struct Buf {
+    double *A, *U, *rs, *ns;
+    int64_t *I, *J, *rr, *init;
+    int32_t* st;
+  } bf[2];
+  for (int i = 0; i < 2; ++i) {
+    double* d = reinterpret_cast<double*>(base + i * per * 8);
+    bf[i].A = d; d += chunk * stride;
+    bf[i].U = d; d += chunk * l * k;
+    bf[i].rs = d; d += chunk;
+    bf[i].ns = d; d += chunk;
+    int64_t* q = reinterpret_cast<int64_t*>(d);
+    bf[i].I = q; q += chunk * k;
+    bf[i].J = q; q += chunk * l;
+    bf[i].rr = q; q += chunk;
+    bf[i].init = q; q += chunk * k;
+    bf[i].st = reinterpret_cast<int32_t*>(q);
+  }
+  cudaEvent_t* ev_h2d = cx->ev;      // chunk copied in
+  cudaEvent_t* ev_comp = cx->ev + 2;  // chunk factorised (its A buffer is free)
+  cudaEvent_t* ev_out = cx->ev + 4;   // chunk results copied out (its output buffers are free)
+  const int64_t nch = (nblocks + chunk - 1) / chunk;
+  for (int64_t c = 0; c < nch; ++c) {
+    const int i = (int)(c & 1);
+    const int64_t b0 = c * chunk, nb = std::min(chunk, nblocks - b0);
+    if (c >= 2) SLRA_CUDA(cudaStreamWaitEvent(cx->h2d, ev_comp[i], 0));
+    SLRA_CUDA(cudaMemcpyAsync(bf[i].A, h_A + b0 * stride, (size_t)(nb - 1) * stride * 8 + (size_t)lda * n * 8,
+                              cudaMemcpyHostToDevice, cx->h2d));
+    SLRA_CUDA(cudaMemcpyAsync(bf[i].init, h_init + b0 * k, (size_t)nb * k * 8, cudaMemcpyHostToDevice, cx->h2d));
+    SLRA_CUDA(cudaEventRecord(ev_h2d[i], cx->h2d));
+    SLRA_CUDA(cudaStreamWaitEvent(cx->stream, ev_h2d[i], 0));
+    if (c >= 2) SLRA_CUDA(cudaStreamWaitEvent(cx->stream, ev_out[i], 0));
+    SLRA_TRY(slra_cross_approx_batched(ctx, bf[i].A, lda, stride, nb, m, n, r, k, l, bf[i].init, loops, h, bf[i].I,
+                                       bf[i].J, bf[i].U, bf[i].rr, bf[i].st, bf[i].rs, bf[i].ns));
+    SLRA_CUDA(cudaEventRecord(ev_comp[i], cx->stream));
+    SLRA_CUDA(cudaStreamWaitEvent(cx->d2h, ev_comp[i], 0));
+    if (h_I) SLRA_CUDA(cudaMemcpyAsync(h_I + b0 * k, bf[i].I, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, cx->d2h));
+    if (h_J) SLRA_CUDA(cudaMemcpyAsync(h_J + b0 * l, bf[i].J, (size_t)nb * l * 8, cudaMemcpyDeviceToHost, cx->d2h));
+    if (h_nucleus)
+      SLRA_CUDA(cudaMemcpyAsync(h_nucleus + b0 * l * k, bf[i].U, (size_t)nb * l * k * 8, cudaMemcpyDeviceToHost,
+                                cx->d2h));
+    if (h_r) SLRA_CUDA(cudaMemcpyAsync(h_r + b0, bf[i].rr, (size_t)nb * 8, cudaMemcpyDeviceToHost, cx->d2h));
+    if (h_status) SLRA_CUDA(cudaMemcpyAsync(h_status + b0, bf[i].st, (size_t)nb * 4, cudaMemcpyDeviceToHost, cx->d2h));
+    if (h_resid_sq)
+      SLRA_CUDA(cudaMemcpyAsync(h_resid_sq + b0, bf[i].rs, (size_t)nb * 8, cudaMemcpyDeviceToHost, cx->d2h));
+    if (h_norm_sq)
+      SLRA_CUDA(cudaMemcpyAsync(h_norm_sq + b0, bf[i].ns, (size_t)nb * 8, cudaMemcpyDeviceToHost, cx->d2h));
+    SLRA_CUDA(cudaEventRecord(ev_out[i], cx->d2h));
+  }
+  SLRA_CUDA(cudaStreamSynchronize(cx->d2h));
   return SLRA_OK;
 }
 

@@ -168,6 +168,10 @@ int slra_ctx_destroy(slra_ctx ctx) {
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->hsmall) cudaFreeHost(c->hsmall);
+  for (auto e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->owns_stream) cudaStreamDestroy(c->stream);
   delete c;
   return SLRA_OK;

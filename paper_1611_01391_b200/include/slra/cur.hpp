@@ -68,15 +68,25 @@ std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r,
                                                   IndexSet init_rows, int loops, double h,
                                                   std::optional<double> stop_tol, Rng& rng);
 
-/// Batched cross_approx + per-block Frobenius residual over `nblocks`
-/// independent m x n blocks stored contiguously in HBM (block b at
-/// d_A + b*block_stride). init rows are drawn per block from
-/// Rng(derive_seed(master_seed, b)). Results stay on the device; the caller
-/// passes device buffers (see slra_cross_approx_batched).
+/// Batched cross_approx + per-block cur_evaluate(M, c, Frobenius) over
+/// `nblocks` independent m x n column-major blocks (block b at
+/// blocks + b*block_stride, ld = lda) in HOST memory — the per-block
+/// ca_factors -> cross_approx pattern of hss.cpp:47-55 applied to a batch.
+/// init_rows holds k initial rows per block (nblocks x k); r <= 0 selects the
+/// adaptive rank numerical_rank(M(I,J), 1e-10, Relative). The blocks are
+/// streamed to the device in chunks (copies overlapped with the kernels);
+/// I_out / J_out / nucleus_out (nullable, nblocks x k / x l / x (l*k)) and the
+/// returned per-block status, r and squared norms are host data. A block
+/// whose selection or generator fails gets its status code (slra_status)
+/// and resid_sq = norm_sq instead of an exception, so one bad block does not
+/// abort the batch.
 struct BatchedCaResult {
   std::vector<int> status;
   std::vector<Index> r;
   std::vector<double> resid_sq, norm_sq;
 };
+BatchedCaResult cross_approx_batched(const double* blocks, Index lda, Index block_stride, Index nblocks, Index m,
+                                     Index n, Index r, Index k, Index l, const Index* init_rows, int loops, double h,
+                                     Index* I_out, Index* J_out, double* nucleus_out);
 
 }  // namespace slra

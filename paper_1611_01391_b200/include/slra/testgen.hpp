@@ -17,6 +17,13 @@ Matrix gen_cauchy_block(Index m, Index n, Rng& rng);
 /// Config 5 block: p_i = (u,u) in [0,1]^2 (m points), then q_j = (u+4, u);
 /// K_ij = 0.5 log((dx)^2 + (dy)^2) = log|p_i - q_j|.
 Matrix gen_log_kernel_block(Index m, Index n, Rng& rng);
+/// Config-5 batch recipe: block b = b0 + t draws from
+/// Rng(derive_seed(master, b)) its points p_i = (u, u) (m), then q_j =
+/// (4 + u, u) (n) — gen_log_kernel_block's order — and then its initial C-A
+/// rows distinct_indices(k, m) (what cross_approx draws for an empty initial
+/// set, cur.cpp:207-209). Arrays are nb x m / nb x n / nb x k, row t = block t.
+void gen_log_kernel_batch(std::uint64_t master, Index b0, Index nb, Index m, Index n, Index k, double* px,
+                          double* py, double* qx, double* qy, Index* init);
 
 /// Bidiagonal-product pseudo-Gaussian generator (sketch.hpp:92-112,
 /// sketch.cpp:695-791): host generators and the KS normality check, drawing

@@ -748,6 +748,31 @@ PYBIND11_MODULE(_slra, m) {
                                     ptr<double>(ns)),
           "cross_approx_batched");
   });
+  // end-to-end batched C-A over HOST blocks (pinned): chunks streamed to the device, results back
+  m.def("cross_approx_batched_host", [](uintptr_t A, Index lda, Index stride, Index nblocks, Index mm, Index n,
+                                        Index r, Index k, Index l, uintptr_t init_rows, int loops, double h,
+                                        uintptr_t I, uintptr_t J, uintptr_t U, uintptr_t rr, uintptr_t status,
+                                        uintptr_t rs, uintptr_t ns) {
+    py::gil_scoped_release nogil;
+    check(slra_cross_approx_batched_host(device_context(), ptr<const double>(A), lda, stride, nblocks, mm, n, r, k,
+                                         l, ptr<const int64_t>(init_rows), loops, h, ptr<int64_t>(I),
+                                         ptr<int64_t>(J), ptr<double>(U), ptr<int64_t>(rr), ptr<int32_t>(status),
+                                         ptr<double>(rs), ptr<double>(ns)),
+          "cross_approx_batched_host");
+  });
+  // config-5 inputs: host points (reference Rng) -> device blocks
+  m.def("gen_log_kernel_batch", [](std::uint64_t master, Index b0, Index nb, Index mm, Index n, Index k,
+                                   uintptr_t px, uintptr_t py, uintptr_t qx, uintptr_t qy, uintptr_t init) {
+    py::gil_scoped_release nogil;
+    gen_log_kernel_batch(master, b0, nb, mm, n, k, ptr<double>(px), ptr<double>(py), ptr<double>(qx),
+                         ptr<double>(qy), ptr<Index>(init));
+  });
+  m.def("gen_log_kernel_blocks_device", [](uintptr_t px, uintptr_t py, uintptr_t qx, uintptr_t qy, Index nb,
+                                           Index mm, Index n, uintptr_t A, Index lda, Index stride) {
+    check(slra_gen_log_kernel_blocks(device_context(), ptr<double>(px), ptr<double>(py), ptr<double>(qx),
+                                     ptr<double>(qy), nb, mm, n, ptr<double>(A), lda, stride),
+          "gen_log_kernel_blocks");
+  });
   m.def("cross_approx_device", [](uintptr_t A, Index lda, Index mm, Index n, Index r, Index k, Index l,
                                   uintptr_t init_rows, int loops, double h, uintptr_t I, uintptr_t J, uintptr_t U,
                                   uintptr_t Tsig, uintptr_t Sr) {

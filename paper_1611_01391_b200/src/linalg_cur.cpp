@@ -395,4 +395,27 @@ LowRankFactors two_stage_truncate(const LowRankFactors& f, Index r) {  // lra.cp
   return out;
 }
 
+BatchedCaResult cross_approx_batched(const double* blocks, Index lda, Index block_stride, Index nblocks, Index m,
+                                     Index n, Index r, Index k, Index l, const Index* init_rows, int loops, double h,
+                                     Index* I_out, Index* J_out, double* nucleus_out) {
+  if (nblocks < 0 || m < 1 || n < 1 || lda < m || block_stride < lda * n)
+    throw std::invalid_argument("cross_approx_batched: bad block layout");
+  if (k < 1 || l < 1 || k > m || l > n || (r > 0 && (r > k || r > l)))
+    throw std::invalid_argument("cross_approx_batched: need r <= k <= m and r <= l <= n");
+  BatchedCaResult out;
+  out.status.resize(static_cast<size_t>(nblocks));
+  out.r.resize(static_cast<size_t>(nblocks));
+  out.resid_sq.resize(static_cast<size_t>(nblocks));
+  out.norm_sq.resize(static_cast<size_t>(nblocks));
+  std::vector<int32_t> st(static_cast<size_t>(nblocks));
+  check(slra_cross_approx_batched_host(device_context(), blocks, lda, block_stride, nblocks, m, n, r, k, l,
+                                       reinterpret_cast<const int64_t*>(init_rows), loops, h,
+                                       reinterpret_cast<int64_t*>(I_out), reinterpret_cast<int64_t*>(J_out),
+                                       nucleus_out, reinterpret_cast<int64_t*>(out.r.data()), st.data(),
+                                       out.resid_sq.data(), out.norm_sq.data()),
+        "cross_approx_batched");
+  for (size_t b = 0; b < st.size(); ++b) out.status[b] = st[b];
+  return out;
+}
+
 }  // namespace slra

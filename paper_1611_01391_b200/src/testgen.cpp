@@ -80,6 +80,24 @@ Matrix gen_log_kernel_block(Index m, Index n, Rng& rng) {
   return K;
 }
 
+void gen_log_kernel_batch(std::uint64_t master, Index b0, Index nb, Index m, Index n, Index k, double* px,
+                          double* py, double* qx, double* qy, Index* init) {
+  if (k > m) throw std::invalid_argument("gen_log_kernel_batch: k > m");
+  for (Index t = 0; t < nb; ++t) {
+    Rng rng(Rng::derive_seed(master, static_cast<std::uint64_t>(b0 + t)));
+    for (Index i = 0; i < m; ++i) {
+      px[t * m + i] = rng.uniform();
+      py[t * m + i] = rng.uniform();
+    }
+    for (Index j = 0; j < n; ++j) {
+      qx[t * n + j] = 4.0 + rng.uniform();
+      qy[t * n + j] = rng.uniform();
+    }
+    const std::vector<Index> ini = rng.distinct_indices(k, m);
+    for (Index u = 0; u < k; ++u) init[t * k + u] = ini[static_cast<size_t>(u)];
+  }
+}
+
 }  // namespace slra
 
 // ------------------------------------------------ bidiagonal-product generator

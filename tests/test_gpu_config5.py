@@ -1,0 +1,201 @@
+"""Config 5 (batched superfast-multipole LRA) at scale, on the bench's own
+inputs: 65,536 blocks in the benchmark, >= 1024 here, generated exactly as
+bench.py generates them (per-block reference Rng points and initial rows,
+blocks materialised on the device by slra_gen_log_kernel_blocks).
+
+The log-kernel strips are numerically rank deficient (eps-rank ~13 of 32):
+their trailing basis vectors are rounding noise in ANY QR implementation,
+so pivots after the first few pick among noise directions (the oracle's own
+Householder basis and LAPACK's already disagree there —
+test_half_sweep_stable_prefix measures it per strip). The contract there is
+(SURVEY.md §7 hard part 1):
+  * replay parity: the oracle's adaptive rank, nucleus and residual on the
+    GPU's I, J equal the GPU's within 1e-10 ||B||_F plus the conditioning
+    term eps ||C|| ||U|| ||R||;
+  * quality: the GPU's residual is as small as the oracle's own C-A run;
+  * per half-sweep, the selection agrees with the oracle on every leading
+    pivot that the reference itself decides stably (independently of the QR
+    implementation).
+On well-posed blocks of the same shape (Gaussian, full-rank strips) the same
+kernel must reproduce the oracle's ordered I, J bit for bit in every block.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+M, K, LOOPS = 256, 32, 2
+
+
+@pytest.fixture(scope="module")
+def slra():
+    import paper_1611_01391_b200 as s
+    return s
+
+
+@pytest.fixture(scope="module")
+def bench():
+    import bench as b
+    return b
+
+
+def _run_batched(slra, torch, A, init):
+    nb = A.shape[0]
+    out = dict(I=torch.zeros((nb, K), dtype=torch.int64, device="cuda"),
+               J=torch.zeros((nb, K), dtype=torch.int64, device="cuda"),
+               U=torch.zeros((nb, K * K), dtype=torch.float64, device="cuda"),
+               r=torch.zeros(nb, dtype=torch.int64, device="cuda"),
+               st=torch.zeros(nb, dtype=torch.int32, device="cuda"),
+               rs=torch.zeros(nb, dtype=torch.float64, device="cuda"),
+               ns=torch.zeros(nb, dtype=torch.float64, device="cuda"))
+    slra.cross_approx_batched_device(A.data_ptr(), M, M * M, nb, M, M, 0, K, K, init.data_ptr(), LOOPS, 1.1,
+                                     out["I"].data_ptr(), out["J"].data_ptr(), out["U"].data_ptr(),
+                                     out["r"].data_ptr(), out["st"].data_ptr(), out["rs"].data_ptr(),
+                                     out["ns"].data_ptr())
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def _bench_blocks(slra, bench, torch, b0, nb, seed=0):
+    px, py, qx, qy, init = bench.config5_host_inputs(slra, seed, b0, nb)
+    A = torch.empty(nb, M, M, dtype=torch.float64, device="cuda")
+    dev = [torch.from_numpy(a).cuda() for a in (px, py, qx, qy)]
+    slra.gen_log_kernel_blocks_device(*[d.data_ptr() for d in dev], nb, M, M, A.data_ptr(), M, M * M)
+    torch.cuda.synchronize()
+    return A, init, (px, py, qx, qy)
+
+
+def test_generator_matches_host_recipe(slra, bench, oracle):
+    """Device-materialised blocks equal the host testgen recipe to the last ulp of log."""
+    import torch
+    A, init, (px, py, qx, qy) = _bench_blocks(slra, bench, torch, 5, 4)
+    for t in range(4):
+        Kb = slra.gen_log_kernel_block(M, M, slra.Rng(slra.Rng.derive_seed(0, 5 + t)))
+        dev = A[t].cpu().numpy().T  # column-major block
+        assert np.allclose(dev, Kb, rtol=4e-16, atol=0)
+        r = slra.Rng(slra.Rng.derive_seed(0, 5 + t))
+        for _ in range(4 * M):
+            r.uniform()
+        assert list(init[t]) == r.distinct_indices(K, M)
+
+
+def _factored_residual(Kb, I, J, rk):
+    """||B - (C T_r S_r^-1)(S_r^T R)||_F with numpy's SVD of G = B(I, J)."""
+    G = Kb[np.ix_(I, J)]
+    U, s, Vt = np.linalg.svd(G)
+    P = Kb[:, J] @ (Vt[:rk].T / s[:rk])
+    Q = U[:, :rk].T @ Kb[I, :]
+    return np.linalg.norm(Kb - P @ Q)
+
+
+def test_config5_bench_blocks_parity(slra, bench, oracle):
+    """1024 blocks generated as bench.py does: status, adaptive rank, replay
+    parity of the fused residual, ||B||, and residual quality vs the oracle's
+    own cross_approx on the same blocks."""
+    import torch
+    nb = 1024
+    A, init, _ = _bench_blocks(slra, bench, torch, 0, nb)
+    g = _run_batched(slra, torch, A, torch.from_numpy(init).cuda())
+    blocks = np.ascontiguousarray(A.cpu().numpy())
+    own = bench.oracle_blocks(oracle, blocks, init, os.cpu_count() or 1)
+    assert (g["st"] == 0).all() and (own["status"] == 0).all()
+    exact = 0
+    worst_ratio = 0.0
+    for b in range(nb):
+        Kb = np.asfortranarray(blocks[b].T)
+        Ib, Jb = g["I"][b].tolist(), g["J"][b].tolist()
+        assert sorted(set(Ib)) == sorted(Ib) and sorted(set(Jb)) == sorted(Jb)
+        exact += (Ib == own["I"][b].tolist() and Jb == own["J"][b].tolist())
+        G = Kb[np.ix_(Ib, Jb)]
+        rk = oracle.numerical_rank(G, 1e-10, True)
+        assert rk == g["r"][b]
+        ro = oracle.primitive_cur(Kb, Ib, Jb, rk)
+        eo = oracle.cur_evaluate(Kb, Ib, Jb, ro["nucleus"])
+        nK = np.linalg.norm(Kb)
+        cond = 64 * 2.2e-16 * np.linalg.norm(Kb[:, Jb]) * np.linalg.norm(ro["nucleus"], 2) * np.linalg.norm(Kb[Ib, :])
+        eg = np.sqrt(g["rs"][b])
+        assert abs(eg - eo) <= TOL * nK + cond, (b, eg, eo)
+        assert abs(np.sqrt(g["ns"][b]) - nK) <= 1e-13 * nK
+        # the nucleus itself: the oracle's CUR product on the GPU's sets
+        Ug = g["U"][b].reshape(K, K).T
+        Cg = oracle.cur_reconstruct(Kb, Ib, Jb, Ug)
+        Co = oracle.cur_reconstruct(Kb, Ib, Jb, ro["nucleus"])
+        assert np.linalg.norm(Cg - Co) <= TOL * nK + cond
+        # quality: the GPU's selection approximates the block as well as the
+        # oracle's own C-A run does, both evaluated by the same well-conditioned
+        # factored evaluator (the oracle's (C U) R carries an eps ||C|| ||U|| ||R||
+        # rounding term ~1e-7 ||B|| at r_eff, far above either selection's error)
+        en_g = _factored_residual(Kb, Ib, Jb, rk)
+        Io, Jo = own["I"][b].tolist(), own["J"][b].tolist()
+        en_o = _factored_residual(Kb, Io, Jo, int(own["r"][b]))
+        assert abs(eg - en_g) <= TOL * nK, (b, eg, en_g)
+        assert en_g <= 10.0 * en_o + 1e-12 * nK, (b, en_g, en_o)
+        worst_ratio = max(worst_ratio, en_g / max(en_o, 1e-300))
+        assert eg / nK < 1e-9
+    print(f"config-5 bench blocks: {exact}/{nb} with I,J identical to the oracle's own run; "
+          f"worst residual ratio gpu/oracle {worst_ratio:.2f}")
+
+
+def test_config5_well_posed_bit_exact(slra, oracle):
+    """Full-rank strips (Gaussian 256 x 256 blocks, k = l = 32, 2 sweeps,
+    adaptive r = 32): the same batched kernel reproduces the oracle's ordered
+    I and J in every one of 1024 blocks; residuals within 1e-10 ||B||_F."""
+    import torch
+    nb = 1024
+    rng = np.random.default_rng(7)
+    blocks = rng.standard_normal((nb, M, M))  # (b, j, i): column-major blocks
+    init = np.stack([rng.permutation(M)[:K] for _ in range(nb)]).astype(np.int64)
+    g = _run_batched(slra, torch, torch.from_numpy(blocks).cuda(), torch.from_numpy(init).cuda())
+    own = oracle.cross_approx_blocks(np.ascontiguousarray(blocks).ctypes.data, nb, M, M, M, M * M, init, K, K, LOOPS,
+                                     1.1, os.cpu_count() or 1)
+    assert (g["st"] == 0).all() and (own["status"] == 0).all()
+    assert np.array_equal(g["I"], own["I"]) and np.array_equal(g["J"], own["J"])
+    assert np.array_equal(g["r"], own["r"])
+    nK = np.sqrt(g["ns"])
+    assert np.all(np.abs(np.sqrt(g["rs"]) - np.sqrt(own["resid_sq"])) <= TOL * nK)
+
+
+def _stable_prefix(oracle, strip, count, trials=6):
+    """Leading pivots of select_rows_spanning that the reference decides
+    stably: the common prefix of the oracle's selection on the strip, on
+    LAPACK's basis of the strip, and on the strip with relative rounding-level
+    perturbations (1e-15). Pivots beyond it flip under an ulp of change."""
+    Qo = oracle.thin_qr(strip)[0]
+    ref = oracle.maxvol_rows(np.asfortranarray(Qo[:, :count]), 1.1, 0)
+    alts = [oracle.maxvol_rows(np.asfortranarray(np.linalg.qr(strip)[0][:, :count]), 1.1, 0)]
+    rng = np.random.default_rng(11)
+    for _ in range(trials):
+        S = np.asfortranarray(strip * (1.0 + 1e-15 * rng.standard_normal(strip.shape)))
+        alts.append(oracle.maxvol_rows(np.asfortranarray(oracle.thin_qr(S)[0][:, :count]), 1.1, 0))
+    p = 0
+    while p < count and all(a[p] == ref[p] for a in alts):
+        p += 1
+    return p, ref
+
+
+@pytest.mark.parametrize("b", range(6))
+def test_half_sweep_stable_prefix(slra, bench, oracle, b):
+    """Per half-sweep of a config-5 block (the CTA-resident C-A kernel, traced):
+    replay the GPU's previous index set through the oracle's
+    select_rows_spanning on the same strip; the GPU's selection must agree on
+    the stable prefix and be a set of distinct rows."""
+    px, py, qx, qy, init = bench.config5_host_inputs(slra, 0, b, 1)
+    Kb = np.asfortranarray(bench.config5_host_blocks(px, py, qx, qy)[0].T)
+    g = slra.cross_approx(Kb, 0, K, K, list(init[0]), LOOPS, 1.1, slra.Rng(0))
+    prefixes = []
+    for t, st in enumerate(g["trace"]):
+        if t % 2 == 0:  # vertical: J = select_rows_spanning(A(I,:)^T, l) (cur.cpp:215-224)
+            strip, got = np.asfortranarray(Kb[st["rows"], :].T), st["cols"]
+        else:  # horizontal: I = select_rows_spanning(A(:,J), k) (cur.cpp:227-236)
+            strip, got = np.asfortranarray(Kb[:, st["cols"]]), st["rows"]
+        p, ref = _stable_prefix(oracle, strip, K)
+        assert got[:p] == ref[:p], (t, p, got[:p], ref[:p])
+        assert len(set(got)) == K
+        prefixes.append(p)
+    print(f"block {b}: stable prefixes per half-sweep {prefixes}")
