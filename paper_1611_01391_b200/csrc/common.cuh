@@ -33,6 +33,28 @@ __device__ __forceinline__ double mufu_rcp(double x) {
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   return y;
 }
+// Full-precision (<= ~1 ulp, not correctly rounded) reciprocal and square
+// root from the MUFU seeds with Newton steps: a handful of dependent DFMAs
+// instead of the IEEE division / sqrt sequences (with their slow-path
+// branches). For the reflector and norm chains of the small factorisations,
+// whose results are compared with the oracle by value, not by bits. x must be
+// finite; fast_rcp needs |x| in the normal range.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y = mufu_rcp(x);
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double fast_sqrt(double x) {
+  double y = mufu_rsqrt(x);
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  const double s = x * y;
+  const double r = fma(0.5 * y, fma(-s, s, x), s);
+  return x > 0.0 ? r : x;  // sqrt(0) = 0 (rsqrt(0) = inf)
+}
 __device__ __forceinline__ void jacobi_rotation(double a, double b, double g, double& cs, double& sn) {
   const double d = b - a, g2 = 2.0 * g;
   const double h = fma(d, d, g2 * g2);
@@ -252,5 +274,24 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// Phase timing of the CTA-resident kernels (profiling builds only,
+// -DSLRA_PHASE_PROF): thread 0 adds the clock64 cycles since its previous
+// mark to g_phase_cycles[id]. Marks sit right after block barriers, so the
+// intervals are the block's critical path per phase.
+#ifdef SLRA_PHASE_PROF
+__device__ unsigned long long g_phase_cycles[32];
+__device__ __forceinline__ void prof_mark(int id) {
+  __shared__ long long t_last;
+  if (threadIdx.x == 0) {
+    const long long now = clock64();
+    if (id >= 0) atomicAdd(&g_phase_cycles[id], (unsigned long long)(now - t_last));
+    t_last = now;
+  }
+}
+#define SLRA_PROF(id) ::slra_dev::prof_mark(id)
+#else
+#define SLRA_PROF(id) ((void)0)
+#endif
 
 }  // namespace slra_dev

@@ -53,13 +53,16 @@ struct CaSmem {
 };
 
 __host__ __device__ inline size_t ca_even(size_t d) { return (d + 1) & ~(size_t)1; }
+__host__ __device__ inline size_t ca_max(size_t a, size_t b) { return a > b ? a : b; }
 
 // every region starts 16-byte aligned (the selection reads v as double2)
 __host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
   // S (mm c + c), W / Gt / V ((c+1) c each), tau / sigma / sgn (c), v (64),
   // nu / nd / rn (mm each), rv 40, volv 8 + slack 2c
-  size_t d = ca_even((size_t)mm * ((c + 3) & ~3) + c) + 3 * ca_even((size_t)(c + 1) * c) + 3 * ca_even(c) + 64 +
+  const int cw = c > 32 ? c : 32;  // W / Gt / V: also the selection's RMAX x r R (RMAX <= 32)
+  const size_t ns = ca_max((size_t)mm * ((c + 3) & ~3) + c, 3 * (size_t)c * c);  // + the nucleus' 3 c x c
+  size_t d = ca_even(ns) + 3 * ca_even((size_t)(cw + 1) * cw) + 3 * ca_even(c) + 64 +
              3 * ca_even(mm > 16 ? mm : 16) + 40 + 8 + ca_even(2 * (size_t)c);
   size_t i = 2 * (size_t)mm + 5 * (size_t)c + 8;
   return d * 8 + 33 * 8 + i * 4 + 64;
@@ -69,11 +72,14 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   const int mm = m > n ? m : n, c = k > l ? k : l;
   CaSmem s;
   double* d = reinterpret_cast<double*>(base);
-  s.S = d; d += ca_even((size_t)mm * ((c + 3) & ~3) + c);  // + the fused residual's Q fragments (n x 4 ceil(r/4))
-  s.W = d; d += ca_even((size_t)(c + 1) * c);  // the nucleus' Jacobi operand (ld p | 1, p <= c)
+  // the strip; the fused residual's Q fragments (n x 4 ceil(r/4)); the
+  // preconditioned nucleus' U_w, J_w and right vectors (3 c x c)
+  s.S = d; d += ca_even(ca_max((size_t)mm * ((c + 3) & ~3) + c, 3 * (size_t)c * c));
+  const int cw = c > 32 ? c : 32;
+  s.W = d; d += ca_even((size_t)(cw + 1) * cw);  // the nucleus' Jacobi operand (ld p | 1, p <= c)
   s.R = nullptr;
-  s.Gt = d; d += ca_even((size_t)(c + 1) * c);  // room for the odd ld of the maxvol QR (rq | 1)
-  s.V = d; d += ca_even((size_t)(c + 1) * c);  // room for ld = q | 1
+  s.Gt = d; d += ca_even((size_t)(cw + 1) * cw);  // maxvol QR (ld rq | 1) / the selection's R (ld RMAX)
+  s.V = d; d += ca_even((size_t)(cw + 1) * cw);  // room for ld = q | 1
   // the nucleus factors T_r Sigma_r^-1 and S_r are written after
   // cta_svd_finish, when the Jacobi operands V and W are dead
   s.Tm = s.V;
@@ -134,12 +140,14 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
   // independent global loads are in flight before the shared-memory stores
   stage_strip<NT>(s.S, A, lda, rows_strip, idx_in, nidx, len);
   __syncthreads();
+  SLRA_PROF(1);
   // ONE len x nidx array carries the strip, its basis Q (in place) and then
   // B = Q G^-1 (in place): the pivot order is taken with the working copy in
   // registers, and the volume |det Q[idx, :]| is tracked through the swaps.
   // The pivot phase's reflectors are those of maxvol round 0's ColPivQR(G^T)
   // (G = Q(I, :)), so round 0 continues from them instead of refactorising.
   cta_thin_qr_inplace<NT, CMAX>(s.S, len, len, nidx, s.tau, s.rv);
+  SLRA_PROF(3);
   const int rq = count < nidx ? count : nidx;
   if (count > rq) {  // the padding branch needs the basis row norms (cur.cpp:125-134)
     for (int i = tid; i < len; i += NT) {
@@ -152,7 +160,7 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
   if (rq <= 32) {
     // pivoted-QR initialisation, maxvol round 0 and the swaps with the basis
     // rows in registers (select_regs.cuh)
-    const SelScratch ss{s.nu, s.p2r, s.v, s.Gt, (rq + 1) & ~1, s.sigma, s.rv, s.tau, s.flag};
+    const SelScratch ss{s.nu, s.p2r, s.v, s.Gt, rq <= 16 ? 16 : 32, s.sigma, s.rv, s.tau, s.flag};
     const int st = rq <= 16 ? cta_select_regs<NT, 16>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, ss)
                             : cta_select_regs<NT, 32>(s.S, len, len, rq, h, 4 * rq, s.tmpidx, ss);
     if (st != SLRA_OK) return st;
@@ -207,43 +215,113 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
   const int tid = threadIdx.x;
   const bool tall = k > l;  // square generators take the transposed (faster) path
   const int p = tall ? k : l, q = tall ? l : k;
-  // W := G (tall) or G^T (wide), p x q, ld p
-  for (int e = tid; e < k * l; e += NT) {
-    const int a = e % k, b = e / k;
-    const double g = __ldg(A + I[a] + (int64_t)J[b] * lda);
-    if (tall) s.W[a + b * (p | 1)] = g;
-    else s.W[b + a * (p | 1)] = g;
-  }
-  __syncthreads();
-  // Only sigma_i > 1e-10 sigma_1 enter the nucleus (pinv cut, linalg.cpp:111-121;
-  // rank checks cur.cpp:156-157): columns below 1e-10/sqrt(q) of the largest
-  // column norm jointly carry less than that, so pairs of two such columns
-  // are not rotated (the noise directions of rank-deficient generators, as in
-  // configs 3 and 5, otherwise keep the sweeps going to the cap).
-  cta_jacobi<NT, CMAX>(s.W, p | 1, p, q, s.V, q | 1, s.flag, 1e-10 / sqrt((double)q));
-  // finish into S (p x q, ld p) and Gt (q x q, ld q): for tall G the left
-  // vectors are in S; for wide G (SVD of G^T) they are the rows of V.
-  cta_svd_finish<NT>(s.W, p | 1, p, q, s.V, q | 1, s.sigma, s.order, s.S, p, s.Gt, q, s.sgn);
-  if (!tall) {
-    // G^T = S' Sigma V'^T -> G = V' Sigma S'^T: left vectors of G = V'
-    // (columns of Gt), right = S'. Re-apply the sign rule on the left ones.
-    for (int t = threadIdx.x >> 5; t < q; t += NT / 32) {
-      const int lane = threadIdx.x & 31;
-      ArgMax a{-1.0, INT64_MAX};
-      for (int i = lane; i < q; i += 32) a = argmax_merge(a, ArgMax{fabs(s.Gt[i + t * q]), i});
-      a = warp_argmax(a);
-      const double f = (s.Gt[a.i + t * q] < 0.0) ? -1.0 : 1.0;
-      __syncwarp();
-      for (int i = lane; i < q; i += 32) s.Gt[i + t * q] *= f;
-      for (int i = lane; i < p; i += 32) s.S[i + t * p] *= f;
+  const double* Sl;  // left vectors of G (k x q)
+  const double* Tr;  // right vectors of G (l x q)
+  int ldsl, ldtr;
+  if (k == l && k <= 32) {
+    // Square generator, QR-preconditioned one-sided Jacobi (Drmac-Veselic):
+    // G Pi = Q R (column-pivoted Householder, Eigen's rules), then Jacobi on
+    // the rows of R (R^T Jv = U_w Sigma): the rows of R are graded, so the
+    // sweeps settle in about half as many rounds as on G itself. Then
+    // G = (Q Jv) Sigma (Pi U_w)^T: left vectors Q Jv (the reflectors applied
+    // to Jv), right vectors Pi U_w (a row permutation).
+    const int n = k, ld = n | 1;
+    for (int e = tid; e < n * n; e += NT) {
+      const int a = e % n, b = e / n;
+      s.W[a + b * ld] = __ldg(A + I[a] + (int64_t)J[b] * lda);
     }
     __syncthreads();
+    SLRA_PROF(9);
+    if (tid < 32) warp_colpiv_qr(s.W, ld, n, 0.0, s.perm, s.tau, s.nu, s.nd);
+    __syncthreads();
+    for (int e = tid; e < n * n; e += NT) {  // X = R^T
+      const int i = e % n, j = e / n;
+      s.Gt[i + j * ld] = j <= i ? s.W[j + i * ld] : 0.0;
+    }
+    __syncthreads();
+    cta_jacobi<NT, CMAX>(s.Gt, ld, n, n, s.V, ld, s.flag, 1e-10 / sqrt((double)n));
+    SLRA_PROF(10);
+    double* Uw = s.S;               // n x n, ld n: normalised columns of the rotated R^T
+    double* Jw = s.S + n * n;       // n x n, ld n: the accumulated rotations
+    double* Rv = s.S + 2 * n * n;   // right vectors of G = Pi U_w
+    cta_svd_finish<NT>(s.Gt, ld, n, n, s.V, ld, s.sigma, s.order, Uw, n, Jw, n, s.sgn);
+    // left vectors L = Q Jw into Gt (ld n): apply H_{n-1} ... H_0 (reverse),
+    // a warp per column, a lane per row
+    {
+      const int lane = tid & 31, warp = tid >> 5;
+      for (int j = warp; j < n; j += NT / 32) {
+        double y = lane < n ? Jw[lane + j * n] : 0.0;
+        for (int kk = n - 1; kk >= 0; --kk) {
+          const double v = lane == kk ? 1.0 : (lane > kk && lane < n ? s.W[lane + kk * ld] : 0.0);
+          const double w = warp_sum(v * y);
+          y = fma(-s.tau[kk] * w, v, y);
+        }
+        if (lane < n) s.Gt[lane + j * n] = y;
+      }
+      for (int e = tid; e < n * n; e += NT) {
+        const int i = e % n, j = e / n;
+        Rv[s.perm[i] + j * n] = Uw[i + j * n];
+      }
+    }
+    __syncthreads();
+    // the sign rule on the left vectors of G (linalg.cpp:87-96)
+    for (int t = tid >> 5; t < n; t += NT / 32) {
+      const int lane = tid & 31;
+      ArgMax a{-1.0, INT64_MAX};
+      for (int i = lane; i < n; i += 32) a = argmax_merge(a, ArgMax{fabs(s.Gt[i + t * n]), i});
+      a = warp_argmax(a);
+      const double f = (s.Gt[a.i + t * n] < 0.0) ? -1.0 : 1.0;
+      __syncwarp();
+      for (int i = lane; i < n; i += 32) {
+        s.Gt[i + t * n] *= f;
+        Rv[i + t * n] *= f;
+      }
+    }
+    __syncthreads();
+    Sl = s.Gt;
+    ldsl = n;
+    Tr = Rv;
+    ldtr = n;
+  } else {
+    // W := G (tall) or G^T (wide), p x q, ld p
+    for (int e = tid; e < k * l; e += NT) {
+      const int a = e % k, b = e / k;
+      const double g = __ldg(A + I[a] + (int64_t)J[b] * lda);
+      if (tall) s.W[a + b * (p | 1)] = g;
+      else s.W[b + a * (p | 1)] = g;
+    }
+    __syncthreads();
+    SLRA_PROF(9);
+    // Only sigma_i > 1e-10 sigma_1 enter the nucleus (pinv cut, linalg.cpp:111-121;
+    // rank checks cur.cpp:156-157): columns below 1e-10/sqrt(q) of the largest
+    // column norm jointly carry less than that, so pairs of two such columns
+    // are not rotated (the noise directions of rank-deficient generators, as in
+    // configs 3 and 5, otherwise keep the sweeps going to the cap).
+    cta_jacobi<NT, CMAX>(s.W, p | 1, p, q, s.V, q | 1, s.flag, 1e-10 / sqrt((double)q));
+    SLRA_PROF(10);
+    // finish into S (p x q, ld p) and Gt (q x q, ld q): for tall G the left
+    // vectors are in S; for wide G (SVD of G^T) they are the rows of V.
+    cta_svd_finish<NT>(s.W, p | 1, p, q, s.V, q | 1, s.sigma, s.order, s.S, p, s.Gt, q, s.sgn);
+    if (!tall) {
+      // G^T = S' Sigma V'^T -> G = V' Sigma S'^T: left vectors of G = V'
+      // (columns of Gt), right = S'. Re-apply the sign rule on the left ones.
+      for (int t = threadIdx.x >> 5; t < q; t += NT / 32) {
+        const int lane = threadIdx.x & 31;
+        ArgMax a{-1.0, INT64_MAX};
+        for (int i = lane; i < q; i += 32) a = argmax_merge(a, ArgMax{fabs(s.Gt[i + t * q]), i});
+        a = warp_argmax(a);
+        const double f = (s.Gt[a.i + t * q] < 0.0) ? -1.0 : 1.0;
+        __syncwarp();
+        for (int i = lane; i < q; i += 32) s.Gt[i + t * q] *= f;
+        for (int i = lane; i < p; i += 32) s.S[i + t * p] *= f;
+      }
+      __syncthreads();
+    }
+    Sl = tall ? s.S : s.Gt;
+    ldsl = tall ? p : q;
+    Tr = tall ? s.Gt : s.S;
+    ldtr = tall ? q : p;
   }
-  // left vectors Sl (k x q), right vectors Tr (l x q)
-  const double* Sl = tall ? s.S : s.Gt;
-  const int ldsl = tall ? p : q;
-  const double* Tr = tall ? s.Gt : s.S;
-  const int ldtr = tall ? q : p;
   const double s0 = s.sigma[0];
   int r = r_req;
   if (r <= 0) {
@@ -327,6 +405,7 @@ __device__ void fused_block_residual(const double* A, int64_t lda, int m, int n,
       if ((j >> 2) < ksn) QS[((nt * ksn) + (j >> 2)) * 32 + g * 4 + (j & 3)] = q[j];
   }
   __syncthreads();
+  SLRA_PROF(12);
   const int g = lane >> 2, q4 = lane & 3;
   double rs = 0.0, ns = 0.0;
 #pragma unroll
@@ -394,6 +473,7 @@ __device__ void fused_block_residual(const double* A, int64_t lda, int m, int n,
     out_pair[0] = a;
     out_pair[1] = b2;
   }
+  SLRA_PROF(13);
 }
 
 // two resident CTAs per SM (<= 128 registers): the block is latency bound
@@ -405,6 +485,7 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
   CaSmem s = ca_carve(smem_raw, P.m, P.n, P.k, P.l);
+  SLRA_PROF(-1);
   const double* A = P.A + (int64_t)b * P.stride;
   int status = SLRA_OK;
   if (P.mode == 0) {
@@ -418,6 +499,7 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
     }
     for (int t = tid; t < P.k; t += kCT) s.Icur[t] = (int)P.init_rows[(int64_t)b * P.k + t];
     __syncthreads();
+    SLRA_PROF(0);
     for (int loop = 0; loop < P.loops && status == SLRA_OK; ++loop) {
       double* vol = (b == 0 && P.trace_vol) ? P.trace_vol + 2 * loop : nullptr;
       status = select_strip<kCT, CMAX>(s, A, P.lda, true, s.Icur, P.k, P.n, P.l, P.h, s.Jcur, vol);
@@ -478,6 +560,7 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
   }
   if (P.pairs) {
     __syncthreads();
+    SLRA_PROF(11);
     if (r <= 16) fused_block_residual<kCT, 4, 4>(A, P.lda, P.m, P.n, s.Icur, P.k, s.Jcur, P.l, s.Tm, s.Sm, r, s.S,
                                                  s.rv, P.pairs + 2 * (int64_t)b);
     else fused_block_residual<kCT, 8, 2>(A, P.lda, P.m, P.n, s.Icur, P.k, s.Jcur, P.l, s.Tm, s.Sm, r, s.S, s.rv,
@@ -578,6 +661,18 @@ int launch_ca_block(Context* c, const CaParams& p, int nprob) {
 using namespace slra_dev;
 
 extern "C" {
+
+#ifdef SLRA_PHASE_PROF
+int slra_debug_phase_cycles(unsigned long long* h_out, int n, int reset) {
+  if (n > 32) n = 32;
+  SLRA_CUDA(cudaMemcpyFromSymbol(h_out, g_phase_cycles, sizeof(unsigned long long) * n));
+  if (reset) {
+    unsigned long long z[32] = {};
+    SLRA_CUDA(cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)));
+  }
+  return SLRA_OK;
+}
+#endif
 
 int slra_primitive_cur(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t n, const int64_t* I, int64_t k,
                        const int64_t* J, int64_t l, int64_t r, double* nucleus, int64_t ldu, double* Tsig,

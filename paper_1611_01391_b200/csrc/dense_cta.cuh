@@ -26,7 +26,7 @@ constexpr double kEps = 2.220446049250313e-16;
 // Householder parts below, tau[0..min(m,c)). Warp w owns columns j = w mod
 // NW; the owner of column j+1 accumulates its next tail norm while applying
 // reflector j, so each column costs two block barriers. `red` >= c + 8.
-template <int NT, int RPL, int CMAX = 64>
+template <int NT, int RPL, int CMAX = 64, bool FAST = false>
 __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
@@ -58,15 +58,16 @@ __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, do
           if (i > j && i < m) x[i] = 0.0;
         }
       } else {
-        beta = sqrt(c0 * c0 + s);
+        // FAST: MUFU-seeded sqrt / reciprocals (common.cuh), ~1 ulp
+        beta = FAST ? fast_sqrt(c0 * c0 + s) : sqrt(c0 * c0 + s);
         if (c0 >= 0.0) beta = -beta;
-        const double rden = 1.0 / (c0 - beta);  // essential = tail / (c0 - beta)
+        const double rden = FAST ? fast_rcp(c0 - beta) : 1.0 / (c0 - beta);  // essential = tail / (c0 - beta)
 #pragma unroll
         for (int r = 0; r < RPL; ++r) {
           const int i = lane + 32 * r;
           if (i > j && i < m) x[i] *= rden;
         }
-        t = (beta - c0) / beta;
+        t = FAST ? (beta - c0) * fast_rcp(beta) : (beta - c0) / beta;
       }
       __syncwarp();
       if (lane == 0) {
@@ -134,9 +135,9 @@ __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, do
 
 template <int NT, int CMAX = 64>
 __device__ void cta_house_qr(double* A, int lda, int m, int c, double* tau, double* red) {
-  if constexpr (CMAX <= 32) {  // c <= 32 (callers enforce): half the per-warp column slots
-    if (m <= 64) cta_house_qr_t<NT, 2, 32>(A, lda, m, c, tau, red);
-    else cta_house_qr_t<NT, 8, 32>(A, lda, m, c, tau, red);  // m <= 256
+  if constexpr (CMAX <= 32) {  // c <= 32 (callers enforce): half the per-warp column slots, fast sqrt / rcp
+    if (m <= 64) cta_house_qr_t<NT, 2, 32, true>(A, lda, m, c, tau, red);
+    else cta_house_qr_t<NT, 8, 32, true>(A, lda, m, c, tau, red);  // m <= 256
   } else {
     if (m <= 64) cta_house_qr_t<NT, 2>(A, lda, m, c, tau, red);
     else if (m <= 256) cta_house_qr_t<NT, 8>(A, lda, m, c, tau, red);
@@ -250,6 +251,7 @@ __device__ void cta_thin_qr_inplace(double* A, int lda, int m, int c, double* ta
   if (CMAX <= 32 || c <= 32) cta_house_qr<NT, 32>(A, lda, m, c, tau, red);
   else if constexpr (CMAX > 32) cta_house_qr<NT>(A, lda, m, c, tau, red);
   __syncthreads();
+  SLRA_PROF(2);
   for (int j = threadIdx.x; j < c; j += NT) red[j] = A[j + j * lda] < 0.0 ? -1.0 : 1.0;
   __syncthreads();
   if (CMAX <= 32 || c <= 32) {  // half the register columns (the C-A kernel's two-CTA budget)

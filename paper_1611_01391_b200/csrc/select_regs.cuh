@@ -33,7 +33,7 @@ struct SelScratch {
   double* av;   // 2 * (NT / 32) argmax values (double-buffered)
   int* ai;      // 2 * (NT / 32) argmax keys
   double* v;    // RMAX: reflector of the current step
-  double* R;    // r x r (ld ldr, even, 16-byte aligned): R of ColPivQR(G^T), on and above the diagonal
+  double* R;    // RMAX x r (ld ldr >= RMAX, even, 16-byte aligned): R of ColPivQR(G^T) on and above the diagonal
   int ldr;
   double* pv;   // r: pivot norms (nonzero-pivot rule)
   double* g;    // RMAX + 1: pivot-row snapshot of a swap round, [RMAX] = pivot value
@@ -80,6 +80,32 @@ __device__ __forceinline__ ArgMaxI block_argmaxi(ArgMaxI a, double* av, int* ai,
   return r;
 }
 
+// Argmax of NON-NEGATIVE doubles with the first-index tie rule by three
+// warp reductions (redux.sync): their bit patterns order like the values, so
+// the maximum is the max of the high words, then of the low words among
+// those, then the min index among the lanes holding it. Exact (no rounding,
+// same winner as argmaxi_merge).
+__device__ __forceinline__ ArgMaxI warp_argmaxu(double v, int i) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  const unsigned hi = static_cast<unsigned>(b >> 32), lo = static_cast<unsigned>(b);
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const int mi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? i : INT32_MAX);
+  return ArgMaxI{__longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mh) << 32) | ml)), mi};
+}
+template <int NT>
+__device__ __forceinline__ ArgMaxI block_argmaxu(double v, int i, double* av, int* ai, int buf) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31;
+  const ArgMaxI a = warp_argmaxu(v, i);
+  if (lane == 0) {
+    av[buf * NW + (threadIdx.x >> 5)] = a.v;
+    ai[buf * NW + (threadIdx.x >> 5)] = a.i;
+  }
+  __syncthreads();
+  return warp_argmaxu(lane < NW ? av[buf * NW + lane] : 0.0, lane < NW ? ai[buf * NW + lane] : INT32_MAX);
+}
+
 // Returns SLRA_OK / SLRA_ERR_SELECTION_FAILURE; I_out (smem, r entries) gets
 // the selected rows in order; the volume |det Q(I,:)| goes to s.tau[1].
 template <int NT, int RMAX>
@@ -113,46 +139,47 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
   for (int k = 0; k < r; ++k) {
     // ---- pivot: first maximum of the updated norms over positions >= k
     const bool cand = own && pos >= k;
-    const ArgMaxI best = block_argmaxi<NT>(ArgMaxI{cand ? nu : -1.0, cand ? pos : INT32_MAX}, s.av, s.ai, buf);
+    const ArgMaxI best = block_argmaxu<NT>(cand ? nu : 0.0, cand ? pos : INT32_MAX, s.av, s.ai, buf);
     buf ^= 1;
+    SLRA_PROF(4);
     const int big = best.i;
     if (pos == big) pos = k;
     else if (pos == k) pos = big;
-    // ---- the winner builds H_k from its row's tail x[k..r) (Eigen makeHouseholder)
-    if (own && pos == k) {
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0, c0 = 0.0;
+    // ---- the winner's warp builds H_k from the winning row's tail x[k..r)
+    // (Eigen makeHouseholder): the winning lane stages its row, every lane
+    // then owns one entry (tail norm by a warp sum, v and R column stored
+    // one entry per lane)
+    const unsigned wb = __ballot_sync(0xffffffffu, own && pos == k);
+    if (wb) {
+      const int lane = tid & 31, wl = __ffs(wb) - 1;
+      if (lane == wl) {
 #pragma unroll
-      for (int j = 0; j < RMAX; j += 4) {  // four independent chains (FP64 FMA latency)
-        if (j == k) c0 = x[j];
-        if (j + 1 == k) c0 = x[j + 1];
-        if (j + 2 == k) c0 = x[j + 2];
-        if (j + 3 == k) c0 = x[j + 3];
-        if (j > k && j < r) t0 = fma(x[j], x[j], t0);
-        if (j + 1 > k && j + 1 < r) t1 = fma(x[j + 1], x[j + 1], t1);
-        if (j + 2 > k && j + 2 < r) t2 = fma(x[j + 2], x[j + 2], t2);
-        if (j + 3 > k && j + 3 < r) t3 = fma(x[j + 3], x[j + 3], t3);
+        for (int j = 0; j < RMAX; j += 2) *reinterpret_cast<double2*>(s.g + j) = make_double2(x[j], x[j + 1]);
       }
-      const double tail = (t0 + t1) + (t2 + t3);
-      double t, beta = c0, rden = 0.0;
-      if (tail <= DBL_MIN) {
-        t = 0.0;
-      } else {
-        beta = sqrt(c0 * c0 + tail);
-        if (c0 >= 0.0) beta = -beta;
-        rden = 1.0 / (c0 - beta);
-        t = (beta - c0) / beta;
+      __syncwarp();
+      const double xl = lane < RMAX ? s.g[lane] : 0.0;
+      const double c0 = s.g[k];
+      const double tail = warp_sum(lane > k && lane < r ? xl * xl : 0.0);
+      // tail == 0: Eigen's tau = 0, beta = c0
+      const bool zero = tail <= DBL_MIN;
+      double beta = fast_sqrt(fma(c0, c0, tail));
+      beta = c0 >= 0.0 ? -beta : beta;
+      beta = zero ? c0 : beta;
+      const double rden = zero ? 0.0 : fast_rcp(c0 - beta);
+      if (lane < RMAX) {
+        s.v[lane] = lane < k ? 0.0 : (lane == k ? 1.0 : (lane < r ? xl * rden : 0.0));
+        // column k of R: entries above the diagonal (this pivot column after
+        // H_0..H_{k-1}), beta on it, zeros below (never read)
+        s.R[lane + k * s.ldr] = lane < k ? xl : (lane == k ? beta : 0.0);
       }
-#pragma unroll
-      for (int j = 0; j < RMAX; ++j) {
-        s.v[j] = j < k ? 0.0 : (j == k ? 1.0 : (j < r ? x[j] * rden : 0.0));
-        if (j < k) s.R[j + k * s.ldr] = x[j];  // R(0:k, k): this pivot column after H_0..H_{k-1}
+      if (lane == 0) {
+        s.tau[0] = zero ? 0.0 : (beta - c0) * fast_rcp(beta);
+        s.pv[k] = best.v;
+        I_out[k] = (tid & ~31) + wl;
       }
-      s.R[k + k * s.ldr] = beta;
-      s.tau[0] = t;
-      s.pv[k] = best.v;
-      I_out[k] = tid;
     }
     __syncthreads();
+    SLRA_PROF(5);
     // ---- apply H_k to every row (non-pivot rows: the factorisation; pivot
     // rows: the solve's Q_g^T applied to that right-hand side)
     const double t = s.tau[0];
@@ -189,21 +216,23 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
     }
     // ---- xGEQP3 norm downdate of the remaining candidates
     if (own && pos > k && nu != 0.0) {
-      double temp = fabs(xk) / nu;
+      const double rnu = fast_rcp(nu);
+      double temp = fabs(xk) * rnu;
       temp = (1.0 + temp) * (1.0 - temp);
       temp = temp < 0.0 ? 0.0 : temp;
-      const double ratio = nu / nd;
+      const double ratio = nu * fast_rcp(nd);
       if (temp * ratio * ratio <= sqrt_eps) {
 #pragma unroll
         for (int j = 0; j < RMAX; ++j)
           if (j > k && j < r) rest = fma(x[j], x[j], rest);
-        nd = sqrt(rest);
+        nd = fast_sqrt(rest);
         nu = nd;
       } else {
-        nu = nu * sqrt(temp);
+        nu = nu * fast_sqrt(temp);
       }
     }
   }
+  SLRA_PROF(6);
   // ---- rank of R with the solve's threshold (ColPivQR(G^T), cur.cpp:103-106)
   if (tid == 0) {
     const double thr_helper = (s.pv[0] * kEps) * (s.pv[0] * kEps) / (double)r;
@@ -238,6 +267,7 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
     }
     asm volatile("" ::: "memory");  // one column of R live at a time
   }
+  SLRA_PROF(7);
   // ---- swap rounds
   double vol = s.tau[1];
   for (int sw = 0; sw <= max_swaps; ++sw) {
@@ -252,7 +282,7 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
         }
       }
     }
-    const ArgMaxI best = block_argmaxi<NT>(mine, s.av, s.ai, buf);
+    const ArgMaxI best = block_argmaxu<NT>(own ? mine.v : 0.0, mine.i, s.av, s.ai, buf);
     buf ^= 1;
     if (best.v <= h || sw == max_swaps) break;
     const int j = best.i / m, piv = best.i % m;
@@ -280,6 +310,7 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
   __syncthreads();
   if (tid == 0) s.tau[1] = vol;
   __syncthreads();
+  SLRA_PROF(8);
   return SLRA_OK;
 }
 
