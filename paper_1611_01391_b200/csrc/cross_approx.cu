@@ -232,40 +232,66 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
     }
     __syncthreads();
     SLRA_PROF(9);
-    if (tid < 32) warp_colpiv_qr(s.W, ld, n, 0.0, s.perm, s.tau, s.nu, s.nd);
+    for (int e = tid; e < n * ld; e += NT) s.Gt[e] = 0.0;  // R^T: zeros above its diagonal
     __syncthreads();
-    for (int e = tid; e < n * n; e += NT) {  // X = R^T
-      const int i = e % n, j = e / n;
-      s.Gt[i + j * ld] = j <= i ? s.W[j + i * ld] : 0.0;
+    // G Pi = Q R by one warp (columns in registers): R^T into Gt, the
+    // reflectors into V (the G copy in W is not needed afterwards)
+    if (tid < 32) warp_colpiv_regs(s.W, ld, n, s.Gt, ld, s.V, ld, s.tau, s.perm, s.v);
+    __syncthreads();
+    // Rows of R below 1e-15 of the largest row norm are dropped: they move
+    // every singular value by less than 1e-15 sqrt(n) sigma_1 — below the
+    // Jacobi's own absolute accuracy on the small ones, and nine orders under
+    // the 1e-10 rank cut — and the Jacobi then runs on nr <= n columns.
+    if (tid < 32) {
+      const int lane = tid;
+      double rn = 0.0;
+      if (lane < n)
+        for (int j = lane; j < n; ++j) rn = fma(s.Gt[j + lane * ld], s.Gt[j + lane * ld], rn);
+      const double mx = __shfl_sync(0xffffffffu, rn, 0);  // row 0 carries the largest pivot
+      double rmax = rn;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      (void)mx;
+      const unsigned keep = __ballot_sync(0xffffffffu, lane < n && rn > 1e-30 * rmax);
+      if (lane == 0) s.flag[4] = keep ? 32 - __clz(keep) : 1;
     }
     __syncthreads();
-    cta_jacobi<NT, CMAX>(s.Gt, ld, n, n, s.V, ld, s.flag, 1e-10 / sqrt((double)n));
+    const int nr = s.flag[4];
+    // Jacobi on X = R(0:nr, :)^T (the first nr columns of Gt), rotations into W
+    cta_jacobi<NT, CMAX>(s.Gt, ld, n, nr, s.W, ld, s.flag, 1e-10 / sqrt((double)nr));
     SLRA_PROF(10);
-    double* Uw = s.S;               // n x n, ld n: normalised columns of the rotated R^T
-    double* Jw = s.S + n * n;       // n x n, ld n: the accumulated rotations
+#ifdef SLRA_PHASE_PROF
+    if (tid == 0) {
+      atomicAdd(&g_phase_cycles[20], (unsigned long long)s.flag[2]);
+      atomicAdd(&g_phase_cycles[21], (unsigned long long)nr);
+    }
+#endif
+    double* Uw = s.S;               // n x nr, ld n: normalised columns of the rotated R^T
+    double* Jw = s.S + n * n;       // nr x nr, ld n: the accumulated rotations
     double* Rv = s.S + 2 * n * n;   // right vectors of G = Pi U_w
-    cta_svd_finish<NT>(s.Gt, ld, n, n, s.V, ld, s.sigma, s.order, Uw, n, Jw, n, s.sgn);
-    // left vectors L = Q Jw into Gt (ld n): apply H_{n-1} ... H_0 (reverse),
-    // a warp per column, a lane per row
+    cta_svd_finish<NT>(s.Gt, ld, n, nr, s.W, ld, s.sigma, s.order, Uw, n, Jw, n, s.sgn);
+    for (int i = nr + tid; i < n; i += NT) s.sigma[i] = 0.0;
+    // left vectors L = Q [Jw; 0] into Gt (ld n): apply H_{n-1} ... H_0
+    // (reverse), a warp per column, a lane per row
     {
       const int lane = tid & 31, warp = tid >> 5;
-      for (int j = warp; j < n; j += NT / 32) {
-        double y = lane < n ? Jw[lane + j * n] : 0.0;
+      for (int j = warp; j < nr; j += NT / 32) {
+        double y = lane < nr ? Jw[lane + j * n] : 0.0;
         for (int kk = n - 1; kk >= 0; --kk) {
-          const double v = lane == kk ? 1.0 : (lane > kk && lane < n ? s.W[lane + kk * ld] : 0.0);
+          const double v = lane < n ? s.V[lane + kk * ld] : 0.0;  // unit head, zeros above
           const double w = warp_sum(v * y);
           y = fma(-s.tau[kk] * w, v, y);
         }
         if (lane < n) s.Gt[lane + j * n] = y;
       }
-      for (int e = tid; e < n * n; e += NT) {
+      for (int e = tid; e < n * nr; e += NT) {
         const int i = e % n, j = e / n;
         Rv[s.perm[i] + j * n] = Uw[i + j * n];
       }
     }
     __syncthreads();
     // the sign rule on the left vectors of G (linalg.cpp:87-96)
-    for (int t = tid >> 5; t < n; t += NT / 32) {
+    for (int t = tid >> 5; t < nr; t += NT / 32) {
       const int lane = tid & 31;
       ArgMax a{-1.0, INT64_MAX};
       for (int i = lane; i < n; i += 32) a = argmax_merge(a, ArgMax{fabs(s.Gt[i + t * n]), i});

@@ -26,12 +26,53 @@ constexpr double kEps = 2.220446049250313e-16;
 // Householder parts below, tau[0..min(m,c)). Warp w owns columns j = w mod
 // NW; the owner of column j+1 accumulates its next tail norm while applying
 // reflector j, so each column costs two block barriers. `red` >= c + 8.
+// Reflector j from column j (its tail norm s = sum_{i>j} A(i,j)^2 given),
+// built by the warp that owns the column: Eigen makeHouseholder.
+template <int RPL, bool FAST>
+__device__ __forceinline__ void house_make(double* x, int j, int m, double s, double* tau) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();  // the column was just written by the lanes of this warp
+  const double c0 = x[j];
+  double t, beta;
+  if (s <= DBL_MIN) {  // Eigen makeHouseholder: tau = 0, beta = c0
+    t = 0.0;
+    beta = c0;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i > j && i < m) x[i] = 0.0;
+    }
+  } else {
+    // FAST: MUFU-seeded sqrt / reciprocals (common.cuh), ~1 ulp
+    beta = FAST ? fast_sqrt(c0 * c0 + s) : sqrt(c0 * c0 + s);
+    if (c0 >= 0.0) beta = -beta;
+    const double rden = FAST ? fast_rcp(c0 - beta) : 1.0 / (c0 - beta);  // essential = tail / (c0 - beta)
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i > j && i < m) x[i] *= rden;
+    }
+    t = FAST ? (beta - c0) * fast_rcp(beta) : (beta - c0) / beta;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    x[j] = beta;
+    tau[j] = t;
+  }
+}
+
+// A (m x c, ld lda) in smem. On exit: R on/above the diagonal, essential
+// Householder parts below, tau[0..min(m,c)). Warp w owns columns j = w mod
+// NW. ONE block barrier per column: after it every warp applies H_j to its
+// columns, and the owner of column j+1 — which updates that column first and
+// accumulates its next tail norm on the way — builds H_{j+1} right away,
+// overlapping the other warps' updates.
 template <int NT, int RPL, int CMAX = 64, bool FAST = false>
 __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   const int size = m < c ? m : c;
-  double* tn = red;  // tn[j] = sum_{i>j} A(i,j)^2 when step j starts
+  (void)red;
   if (size > 0 && warp == 0) {
     double s = 0.0;
 #pragma unroll
@@ -40,42 +81,11 @@ __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, do
       if (i >= 1 && i < m) s += A[i] * A[i];
     }
     s = warp_sum(s);
-    if (lane == 0) tn[0] = s;
+    house_make<RPL, FAST>(A, 0, m, s, tau);
   }
   __syncthreads();
   for (int j = 0; j < size; ++j) {
     double* x = A + j * lda;
-    if (warp == j % NW) {
-      const double s = tn[j];
-      const double c0 = x[j];
-      double t, beta;
-      if (s <= DBL_MIN) {  // Eigen makeHouseholder: tau = 0, beta = c0
-        t = 0.0;
-        beta = c0;
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          const int i = lane + 32 * r;
-          if (i > j && i < m) x[i] = 0.0;
-        }
-      } else {
-        // FAST: MUFU-seeded sqrt / reciprocals (common.cuh), ~1 ulp
-        beta = FAST ? fast_sqrt(c0 * c0 + s) : sqrt(c0 * c0 + s);
-        if (c0 >= 0.0) beta = -beta;
-        const double rden = FAST ? fast_rcp(c0 - beta) : 1.0 / (c0 - beta);  // essential = tail / (c0 - beta)
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          const int i = lane + 32 * r;
-          if (i > j && i < m) x[i] *= rden;
-        }
-        t = FAST ? (beta - c0) * fast_rcp(beta) : (beta - c0) / beta;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        x[j] = beta;
-        tau[j] = t;
-      }
-    }
-    __syncthreads();
     // tau = 0 (identity reflector, incl. the rows()==1 case) leaves every
     // column unchanged through the same arithmetic, so the code below has no
     // data-dependent branches around its shuffles (those would be compiled
@@ -128,7 +138,7 @@ __device__ void cta_house_qr_t(double* A, int lda, int m, int c, double* tau, do
       }
     }
     s = warp_sum(s);
-    if (lane == 0 && k0 == j + 1 && k0 < c) tn[k0] = s;
+    if (k0 == j + 1 && k0 < size) house_make<RPL, FAST>(A + k0 * lda, k0, m, s, tau);
     __syncthreads();
   }
 }
@@ -515,6 +525,7 @@ struct SmallColPiv {
   int rank;
 };
 
+template <bool SPLIT = false>
 __device__ inline SmallColPiv warp_colpiv_qr(double* G, int ldg, int n, double threshold, int* perm, double* tau,
                                       double* nu, double* nd) {
   const int lane = threadIdx.x & 31;
@@ -583,7 +594,20 @@ __device__ inline SmallColPiv warp_colpiv_qr(double* G, int ldg, int n, double t
       for (int j = k + 1 + lane; j < n; j += 32) {
         double* a2 = G + j * ldg;
         double w = 0.0;
-        for (int i = k + 1; i < n; ++i) w += x[i] * a2[i];
+        if (SPLIT) {  // four independent chains (a preconditioner: order-insensitive)
+          double w1 = 0.0, w2 = 0.0, w3 = 0.0;
+          int i = k + 1;
+          for (; i + 3 < n; i += 4) {
+            w = fma(x[i], a2[i], w);
+            w1 = fma(x[i + 1], a2[i + 1], w1);
+            w2 = fma(x[i + 2], a2[i + 2], w2);
+            w3 = fma(x[i + 3], a2[i + 3], w3);
+          }
+          for (; i < n; ++i) w = fma(x[i], a2[i], w);
+          w = (w + w1) + (w2 + w3);
+        } else {
+          for (int i = k + 1; i < n; ++i) w += x[i] * a2[i];
+        }
         w += a2[k];
         a2[k] -= t * w;
         for (int i = k + 1; i < n; ++i) a2[i] -= t * x[i] * w;

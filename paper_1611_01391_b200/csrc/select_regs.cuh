@@ -314,4 +314,111 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
   return SLRA_OK;
 }
 
+// Column-pivoted Householder QR of a small square G (n x n, n <= 32, ld ldg,
+// smem) by ONE warp, each column in a lane's registers — the preconditioner
+// of the generator SVD (G Pi = Q R). Eigen's rules as in cta_select_regs
+// (first maximum of the updated norms in position order, xGEQP3 downdate),
+// no block barriers. Writes R^T (n x n, ld ldr: row k = column k of R, zeros
+// above the diagonal of R^T must be pre-filled by the caller), the unit-lower
+// reflectors V (n x n, ld ldv), tau[k], perm[k] = original column at position
+// k. `vb` (32 doubles, 16-byte aligned) is scratch.
+__device__ inline void warp_colpiv_regs(const double* G, int ldg, int n, double* Rt, int ldr, double* V, int ldv,
+                                        double* tau, int* perm, double* vb) {
+  const int lane = threadIdx.x & 31;
+  const bool own = lane < n;
+  const double sqrt_eps = 1.4901161193847656e-08;
+  double x[32];
+  double nu, nd;
+  {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      x[i] = (own && i < n) ? G[i + lane * ldg] : 0.0;
+      x[i + 1] = (own && i + 1 < n) ? G[i + 1 + lane * ldg] : 0.0;
+      a0 = fma(x[i], x[i], a0);
+      a1 = fma(x[i + 1], x[i + 1], a1);
+    }
+    nd = fast_sqrt(a0 + a1);
+    nu = nd;
+  }
+  int pos = lane;
+  for (int k = 0; k < n; ++k) {
+    const bool cand = own && pos >= k;
+    const ArgMaxI best = warp_argmaxu(cand ? nu : 0.0, cand ? pos : INT32_MAX);
+    const int big = best.i;
+    if (pos == big) pos = k;
+    else if (pos == k) pos = big;
+    const unsigned wb = __ballot_sync(0xffffffffu, own && pos == k);
+    const int wl = __ffs(wb) - 1;
+    if (lane == wl) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) *reinterpret_cast<double2*>(vb + i) = make_double2(x[i], x[i + 1]);
+      perm[k] = lane;
+    }
+    __syncwarp();
+    const double xl = vb[lane];
+    const double c0 = vb[k];
+    const double tail = warp_sum(lane > k && lane < n ? xl * xl : 0.0);
+    const bool zero = tail <= DBL_MIN;
+    double beta = fast_sqrt(fma(c0, c0, tail));
+    beta = c0 >= 0.0 ? -beta : beta;
+    beta = zero ? c0 : beta;
+    const double rden = zero ? 0.0 : fast_rcp(c0 - beta);
+    const double t = zero ? 0.0 : (beta - c0) * fast_rcp(beta);
+    const double vl = lane < k ? 0.0 : (lane == k ? 1.0 : (lane < n ? xl * rden : 0.0));
+    if (own) {
+      V[lane + k * ldv] = vl;
+      if (lane <= k) Rt[k + lane * ldr] = lane < k ? xl : beta;
+    }
+    if (lane == 0) tau[k] = t;
+    __syncwarp();
+    vb[lane] = vl;  // the reflector for every lane's dot product
+    __syncwarp();
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (8 * c + 7 >= k) {
+#pragma unroll
+        for (int u = 0; u < 8; u += 4) {
+          const double2 va = *reinterpret_cast<const double2*>(vb + 8 * c + u);
+          const double2 vc = *reinterpret_cast<const double2*>(vb + 8 * c + u + 2);
+          w0 = fma(va.x, x[8 * c + u], w0);
+          w1 = fma(va.y, x[8 * c + u + 1], w1);
+          w2 = fma(vc.x, x[8 * c + u + 2], w2);
+          w3 = fma(vc.y, x[8 * c + u + 3], w3);
+        }
+      }
+    }
+    const double tw = t * ((w0 + w1) + (w2 + w3));
+    double xk = 0.0, rest = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (8 * c + 7 >= k) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = 8 * c + u;
+          x[i] = fma(-tw, vb[i], x[i]);
+          if (i == k) xk = x[i];
+        }
+      }
+    }
+    if (own && pos > k && nu != 0.0) {
+      double temp = fabs(xk) * fast_rcp(nu);
+      temp = (1.0 + temp) * (1.0 - temp);
+      temp = temp < 0.0 ? 0.0 : temp;
+      const double ratio = nu * fast_rcp(nd);
+      if (temp * ratio * ratio <= sqrt_eps) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i > k && i < n) rest = fma(x[i], x[i], rest);
+        nd = fast_sqrt(rest);
+        nu = nd;
+      } else {
+        nu = nu * fast_sqrt(temp);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace slra_dev

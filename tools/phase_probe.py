@@ -35,6 +35,7 @@ w.step()
 torch.cuda.synchronize()
 lib.slra_debug_phase_cycles(buf, 32, 1)
 cyc = np.array(buf[:len(NAMES)], dtype=np.float64) / nb
+print(f"nucleus: mean Jacobi sweeps {buf[20] / nb:.2f}, mean kept rows of R {buf[21] / nb:.2f}")
 tot = cyc.sum()
 print(f"{nb} blocks: {tot:.0f} cycles per block on the critical path")
 for n, c in zip(NAMES, cyc):
