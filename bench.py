@@ -788,20 +788,14 @@ class Config4:
         ws = comm.world
         self.scaling = "weak" if ws == 1 else "strong"
         self.row0, self.mloc = shard.split(M4, ws, comm.rank)
-        # device-side seeded Gaussians, generated per 4096-row chunk so every
-        # rank builds exactly its rows of the same global A, b
-        gx = torch.Generator(device="cuda").manual_seed(seed * 1000003 + 7)
-        self.x0 = torch.randn(D4, dtype=torch.float64, device="cuda", generator=gx)
-        self.At = torch.empty(D4, self.mloc, dtype=torch.float64, device="cuda")  # (d, m_local) column-major
-        self.b = torch.empty(self.mloc, dtype=torch.float64, device="cuda")
-        c0 = self.row0 // self.CHUNK
-        for c in range(c0, c0 + (self.mloc + self.CHUNK - 1) // self.CHUNK):
-            g = torch.Generator(device="cuda").manual_seed(seed * 1000003 + 11 + c)
-            blk = torch.randn(self.CHUNK, D4, dtype=torch.float64, device="cuda", generator=g)  # rows x d
-            e = torch.randn(self.CHUNK, dtype=torch.float64, device="cuda", generator=g)
-            lo = c * self.CHUNK - self.row0
-            self.At[:, lo:lo + self.CHUNK] = blk.T
-            self.b[lo:lo + self.CHUNK] = blk @ self.x0 + 1e-6 * e
+        # the reference generator (gen_lsr_family pattern, testgen.cpp:159-193,
+        # noise 1e-6): A column-major Gaussian, x0, e from one Rng stream —
+        # the inputs tests/test_gpu_config4.py checks against the oracle. The
+        # stream is sequential, so every rank draws the whole A and keeps its rows.
+        A_h, b_h = slra.gen_lsr_gaussian(M4, D4, 1e-6, slra.Rng(2024 + seed))
+        self.At = torch.from_numpy(np.ascontiguousarray(A_h[self.row0:self.row0 + self.mloc].T)).cuda()
+        self.b = torch.from_numpy(np.ascontiguousarray(b_h[self.row0:self.row0 + self.mloc])).cuda()
+        del A_h, b_h
         ru = slra.Rng(slra.Rng.derive_seed(seed, 41))
         Fu = slra.make_sub_identity(ru.distinct_indices(K4, M4), M4)
         rs = slra.Rng(slra.Rng.derive_seed(seed, 42))
@@ -820,7 +814,7 @@ class Config4:
         self.tres = [0.0] * len(self.plans)
         self.dev_ops = shard.DeviceOps(slra, torch)
         self.entries_per_step = 2 * M4 * (D4 + 1)
-        self.data = "synthetic (seeded torch Gaussians on the device, config-4 shapes and noise 1e-6)"
+        self.data = "synthetic (seeded; reference generator gen_lsr_gaussian, noise 1e-6)"
         if ws > 1:
             self.parallelism = f"row-sharded x{ws}: per-rank sketch contributions + one allreduce (NCCL)"
         self.config = {"workload": "config4: sketched LSR, A 1048576x256 fp64 Gaussian, b = A x0 + 1e-6 e, "

@@ -358,9 +358,13 @@ int slra_transpose(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int6
 
 /* ------------------------------------------------------------ a11/a12 LSR
  * sketch_solve (lsr.cpp:37-67): FW = F (A|b) through a compiled left-side
- * plan (k rows), column-pivoted Householder QR of FA (threshold 1e-10;
- * SLRA_ERR_SKETCH_RANK_FAILURE when rank < d), x_hat = solve(Fb).
- * h_sketched_residual = ||FA x_hat - Fb||. d <= 256, k <= 8192. Blocks. */
+ * plan (k rows), then min ||FA x - Fb||: a Gram/Cholesky solve with one
+ * refinement step when FA is well conditioned (every Cholesky pivot above
+ * 1e-6 of its column's squared norm), otherwise the reference's own
+ * column-pivoted Householder QR of FA (threshold 1e-10;
+ * SLRA_ERR_SKETCH_RANK_FAILURE exactly when its rank() < d) and its solve.
+ * h_sketched_residual = ||FA x_hat - Fb||. d <= 768. Blocks (one host
+ * synchronisation, at the end). */
 int slra_sketch_solve(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
                       const double* d_b, const int64_t* d_src, const double* d_coef,
                       const int32_t* d_q, int64_t width, int tree, int64_t k, double* d_x_hat,
@@ -370,6 +374,14 @@ int slra_sketch_solve(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, i
  * all-reduces the per-rank sketch contributions and then calls this. */
 int slra_lsr_solve_sketched(slra_ctx ctx, const double* d_FW, int64_t ldfw, int64_t k, int64_t d,
                             double* d_x_hat, double* h_sketched_residual);
+/* solve_exact (lsr.cpp:21-24): x = pinv(A) b, the minimum-norm least-squares
+ * solution with the pseudo-inverse's cut sigma_i > 1e-10 sigma_1
+ * (linalg.cpp:111-121). Well-conditioned A: the normal-equation solve (one
+ * refinement step); otherwise the column-pivoted Householder QR A P = Q R and
+ * pinv(R) (sigma(R) = sigma(A)). Never reports a rank failure; *h_rank = the
+ * kept singular values (d on the fast path). d <= 768. Blocks. */
+int slra_lsq_exact(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d, const double* d_b,
+                   double* d_x, int64_t* h_rank);
 /* residual_norm (lsr.cpp:26-28): ||A x - b||^2 into d_out[0] (device). */
 int slra_lsr_residual(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
                       const double* d_b, const double* d_x, double* d_out);

@@ -71,7 +71,7 @@ __device__ __forceinline__ void jacobi_rotation(double a, double b, double g, do
 
 
 // ------------------------------------------------------------------ context
-constexpr int kArenaSlots = 13;
+constexpr int kArenaSlots = 14;
 
 struct Context {
   int device = 0;
@@ -97,7 +97,8 @@ struct Context {
   // independent growable device arenas for multi-kernel orchestrations
   // (0: range finder, 1: cur residual, 2: lsr, 3: svd, 4: large C-A, 5: factored residual,
   //  6: wide-svd transpose, 7: tall maxvol/select, 8: pinv, 9: premult / two-stage truncate,
-  //  10: large (multi-CTA Jacobi) svd, 11: hss, 12: host-streamed batched C-A)
+  //  10: large (multi-CTA Jacobi) svd, 11: hss, 12: host-streamed batched C-A,
+  //  13: exact (column-pivoted QR) least squares)
   void* arena[kArenaSlots] = {};
   size_t arena_bytes[kArenaSlots] = {};
   // opt-in per-kernel-family timing (CUDA events on the context stream)

@@ -2,18 +2,23 @@
 // pass (residual_norm, lsr.cpp:26-28).
 //
 // Device formulation: FW = F (A|b) through a compiled left plan (one pass,
-// only the k sampled/sketched rows are touched), the Gram matrix
-// [FA Fb]^T [FA Fb] on the DMMA GEMM (split-K, deterministic), a blocked
-// Cholesky of FA^T FA in one CTA (right-looking, 32-column panels), two
-// triangular solves, one step of iterative refinement, and the sketched
-// residual ||FA x - Fb|| by a direct pass (never from the Gram identity).
-// Rank test: a Cholesky pivot that is non-positive, below
-// (1e-10 * max_i ||FA(:,i)||)^2, or below 64 eps ||FA(:,j)||^2 reports
-// SketchRankFailure — the analogue of ColPivHouseholderQR's rank() < d with
-// threshold 1e-10 (lsr.cpp:52-55). The Gram resolves dependence only to the
-// sqrt(eps) level, so exactly dependent columns fail as in the reference,
-// while sketches with sigma_min / sigma_max between 1e-10 and ~1e-7 also
-// fail here (the reference solves those); DESIGN.md §8.
+// only the k sampled/sketched rows are touched), then two solvers:
+//  * fast path — the Gram [FA Fb]^T [FA Fb] on the DMMA GEMM (split-K,
+//    deterministic), a blocked Cholesky of FA^T FA in one CTA (right-looking,
+//    32-column panels), two triangular solves, one step of iterative
+//    refinement, and the sketched residual ||FA x - Fb|| by a direct pass.
+//    It is taken only when the sketch is well conditioned: every Cholesky
+//    pivot above 1e-6 of its column's squared norm (the sine of the angle
+//    between a column and the span of the earlier ones above 1e-3), so that
+//    the reference's rank() == d and one refinement step reaches ~eps.
+//  * exact path — otherwise (near or exact dependence): Eigen's
+//    ColPivHouseholderQR of FA itself (colpiv_lsq_kernel: first maximum of
+//    the updated norms, xGEQP3 downdate, nonzero-pivot rule, rank() with
+//    threshold 1e-10 → SketchRankFailure exactly where the reference throws,
+//    lsr.cpp:52-55), Q^T Fb carried along as an extra column, and the solve
+//    x = P R^-1 (Q^T Fb). The same kernel (without the rank test) gives R
+//    and Q^T b for solve_exact's pseudo-inverse (lsr.cpp:21-24).
+// One host synchronisation at the end of the fast path (status, residual).
 #include "common.cuh"
 
 namespace slra_dev {
@@ -33,16 +38,34 @@ constexpr int kPW = 32;  // Cholesky panel width
 // written back, and the trailing lower triangle is updated
 // G22 -= L21 L21^T with L21 read from shared memory.
 // status[0] = 0 ok, 1 rank failure.
-__global__ void __launch_bounds__(kLT) cholesky_kernel(double* __restrict__ G, int d, double tol2,
+__global__ void __launch_bounds__(kLT) cholesky_kernel(double* __restrict__ G, int d, double tol_rel,
                                                        int32_t* __restrict__ status) {
   extern __shared__ __align__(16) double P[];  // rows x kPW panel, ld = d + 1 (odd: row-threads conflict-free)
-  __shared__ int fail;
+  __shared__ int fail, illc;
+  __shared__ double red[33];
   const int tid = threadIdx.x;
   const int ldp = d + 1;
   double* gdiag = P + (size_t)ldp * kPW;  // original diagonal ||FA(:,j)||^2
-  for (int i = tid; i < d; i += kLT) gdiag[i] = G[i + (int64_t)i * d];
-  if (tid == 0) fail = 0;
-  __syncthreads();
+  double dm = 0.0;
+  for (int i = tid; i < d; i += kLT) {
+    gdiag[i] = G[i + (int64_t)i * d];
+    dm = fmax(dm, gdiag[i]);
+  }
+  if (tid == 0) fail = illc = 0;
+  // the rank floor from the largest squared column norm of FA (all d columns)
+  {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    if ((tid & 31) == 0) red[tid >> 5] = dm;
+    __syncthreads();
+    if (tid == 0) {
+      double mx = 0.0;
+      for (int w = 0; w < kLT / 32; ++w) mx = fmax(mx, red[w]);
+      red[32] = mx;
+    }
+    __syncthreads();
+  }
+  const double tol2 = tol_rel * red[32];
   for (int p0 = 0; p0 < d; p0 += kPW) {
     const int pw = (d - p0) < kPW ? (d - p0) : kPW;
     const int rows = d - p0;
@@ -71,6 +94,7 @@ __global__ void __launch_bounds__(kLT) cholesky_kernel(double* __restrict__ G, i
           if (tid == 0) fail = 1;
           break;
         }
+        if (!(piv > 1e-6 * gdiag[p0 + j]) && tid == 0) illc = 1;  // leave to the exact path
         const double ljj = sqrt(piv);
         const double inv = 1.0 / ljj;
         const bool row = ti > j && ti < pw;
@@ -170,7 +194,10 @@ __global__ void __launch_bounds__(kLT) cholesky_kernel(double* __restrict__ G, i
     }
     __syncthreads();
   }
-  if (tid == 0) *status = fail;
+  if (tid == 0) {
+    status[0] = fail;
+    status[1] = illc;
+  }
 }
 
 // x (+)= (L L^T)^{-1} rhs for the lower Cholesky factor L (ld d), one CTA,
@@ -357,11 +384,173 @@ int slra_lsr_residual(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
 
 namespace slra_dev {
 
+// Eigen ColPivHouseholderQR (linalg.cpp restated in oracle/src/linalg.cpp:
+// computeInPlace with the LAPACK xGEQP3 norm downdate) of W(:, 0:d) for a
+// k x (d+1) column-major W in global memory (L2-resident), the last column
+// receiving every reflector (Q^T b). One CTA of kQT threads: block argmax
+// for the pivot (first maximum in position order), block reduction for the
+// reflector, a warp per trailing column for its update and norm downdate.
+// On exit W holds R (and the essential parts), hc the taus, perm the column
+// permutation (position -> original column), piv[0] = the nonzero-pivot
+// count, piv[1] = max |R_ii|. Then, with `solve` set: the rank with
+// threshold 1e-10 (rank() < d -> status SketchRankFailure, the reference's
+// throw, lsr.cpp:52-55), otherwise x = P R^-1 (Q^T b)(0:d).
+constexpr int kQT = 1024;
+__global__ void __launch_bounds__(kQT) colpiv_lsq_kernel(double* __restrict__ W, int64_t k, int d,
+                                                         double* __restrict__ nu, double* __restrict__ nd,
+                                                         int* __restrict__ perm, double* __restrict__ hc,
+                                                         double* __restrict__ piv, int solve, double* __restrict__ x,
+                                                         int32_t* __restrict__ status) {
+  __shared__ double rv[33];
+  __shared__ int64_t ri[33];
+  __shared__ double sc[4];
+  __shared__ int s_nonzero;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kQT / 32;
+  const double eps = 2.220446049250313e-16, sqrt_eps = 1.4901161193847656e-08;
+  for (int c = warp; c < d; c += NW) {
+    double acc = 0.0;
+    for (int64_t i = lane; i < k; i += 32) acc = fma(W[i + c * k], W[i + c * k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) nu[c] = nd[c] = sqrt(acc);
+  }
+  for (int c = tid; c < d; c += kQT) perm[c] = c;
+  __syncthreads();
+  double maxnorm = 0.0;
+  {
+    ArgMax a{-1.0, INT64_MAX};
+    for (int c = tid; c < d; c += kQT) a = argmax_merge(a, ArgMax{nu[c], c});
+    maxnorm = block_argmax<kQT>(a, rv, ri).v;
+  }
+  const double thr_helper = (maxnorm * eps) * (maxnorm * eps) / (double)k;
+  const int size = (int64_t)d < k ? d : (int)k;
+  if (tid == 0) {
+    s_nonzero = size;
+    sc[3] = 0.0;  // max |beta|
+  }
+  for (int j = 0; j < size; ++j) {
+    ArgMax a{-1.0, INT64_MAX};
+    for (int c = j + tid; c < d; c += kQT) a = argmax_merge(a, ArgMax{nu[c], c});
+    a = block_argmax<kQT>(a, rv, ri);
+    const int big = (int)a.i;
+    if (tid == 0 && s_nonzero == size && a.v * a.v < thr_helper * (double)(k - j)) s_nonzero = j;
+    if (big != j) {
+      for (int64_t i = tid; i < k; i += kQT) {
+        const double t = W[i + j * k];
+        W[i + j * k] = W[i + big * k];
+        W[i + big * k] = t;
+      }
+      if (tid == 0) {
+        double t = nu[j]; nu[j] = nu[big]; nu[big] = t;
+        t = nd[j]; nd[j] = nd[big]; nd[big] = t;
+        const int p = perm[j]; perm[j] = perm[big]; perm[big] = p;
+      }
+    }
+    __syncthreads();
+    // reflector of column j, rows j..k-1 (Eigen makeHouseholder)
+    double* xj = W + j * k;
+    double tl = 0.0;
+    for (int64_t i = j + 1 + tid; i < k; i += kQT) tl = fma(xj[i], xj[i], tl);
+    tl = block_sum<kQT>(tl, rv);
+    const double c0 = xj[j];
+    double tau, beta;
+    if (tl <= DBL_MIN) {
+      tau = 0.0;
+      beta = c0;
+      for (int64_t i = j + 1 + tid; i < k; i += kQT) xj[i] = 0.0;
+    } else {
+      beta = sqrt(c0 * c0 + tl);
+      if (c0 >= 0.0) beta = -beta;
+      const double den = c0 - beta;
+      for (int64_t i = j + 1 + tid; i < k; i += kQT) xj[i] /= den;
+      tau = (beta - c0) / beta;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      xj[j] = beta;
+      hc[j] = tau;
+      sc[3] = fmax(sc[3], fabs(beta));
+    }
+    // apply to columns j+1 .. d (the last is b), a warp per column; then the
+    // xGEQP3 downdate of the column norms (re-computed when it cancels)
+    for (int c = j + 1 + warp; c <= d; c += NW) {
+      double* xc = W + (int64_t)c * k;
+      if (k - j == 1) {
+        if (lane == 0) xc[j] *= (1.0 - tau);
+      } else if (tau != 0.0) {
+        double w = 0.0;
+        for (int64_t i = j + 1 + lane; i < k; i += 32) w = fma(xj[i], xc[i], w);
+        w = warp_sum(w) + xc[j];
+        if (lane == 0) xc[j] -= tau * w;
+        for (int64_t i = j + 1 + lane; i < k; i += 32) xc[i] -= tau * xj[i] * w;
+      }
+      if (c < d) {
+        __syncwarp();
+        const double nuv = nu[c];
+        if (nuv != 0.0) {
+          double temp = fabs(xc[j]) / nuv;
+          temp = (1.0 + temp) * (1.0 - temp);
+          temp = temp < 0.0 ? 0.0 : temp;
+          const double ratio = nuv / nd[c];
+          if (temp * ratio * ratio <= sqrt_eps) {
+            double acc = 0.0;
+            for (int64_t i = j + 1 + lane; i < k; i += 32) acc = fma(xc[i], xc[i], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) nu[c] = nd[c] = sqrt(acc);
+          } else if (lane == 0) {
+            nu[c] = nuv * sqrt(temp);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    piv[0] = (double)s_nonzero;
+    piv[1] = sc[3];
+  }
+  if (!solve) return;
+  // rank() with threshold 1e-10 over the nonzero pivots
+  if (tid == 0) {
+    const double pre = sc[3] * 1e-10;
+    int rank = 0;
+    for (int i = 0; i < s_nonzero; ++i) rank += fabs(W[i + (int64_t)i * k]) > pre ? 1 : 0;
+    *status = rank < d ? SLRA_ERR_SKETCH_RANK_FAILURE : SLRA_OK;
+    sc[0] = rank < d ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (sc[0] != 0.0) return;
+  // back substitution R y = (Q^T b)(0:d), column-oriented, then x(perm) = y
+  double* cvec = W + (int64_t)d * k;  // Q^T b
+  for (int t = d - 1; t >= 0; --t) {
+    if (tid == 0) cvec[t] /= W[t + (int64_t)t * k];
+    __syncthreads();
+    const double yt = cvec[t];
+    for (int i = tid; i < t; i += kQT) cvec[i] -= W[i + (int64_t)t * k] * yt;
+    __syncthreads();
+  }
+  for (int i = tid; i < d; i += kQT) x[perm[i]] = cvec[i];
+}
+
+int launch_colpiv_lsq(Context* cx, double* W, int64_t k, int d, double* ws, int solve, double* x, int32_t* status) {
+  double* nu = ws;
+  double* nd = nu + d;
+  double* hc = nd + d;
+  double* piv = hc + d;
+  int* perm = reinterpret_cast<int*>(piv + 2);
+  SLRA_TIMED(cx, "lsr_exact_qr", colpiv_lsq_kernel<<<1, kQT, 0, cx->stream>>>(W, k, d, nu, nd, perm, hc, piv, solve, x,
+                                                                             status);)
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}
+
 // Solve min ||FA x - Fb|| for a sketched system FW = (FA | Fb) (k x (d+1),
 // ld k). FW == nullptr: the caller has already written FW into the arena
 // (returned through *fw_slot when fw_slot != nullptr on a first call).
+// fallback = 0: return SLRA_ERR_UNSUPPORTED instead of running the exact
+// path when the fast path declines (the caller has its own).
 static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, double* x_hat,
-                     double* h_sketched_residual, double** fw_slot) {
+                     double* h_sketched_residual, double** fw_slot, int fallback = 1) {
   const int64_t dc = d + 1;
   const int rgrid = (int)((k + 31) / 32);  // lsq_residual_kernel: 32 rows per CTA
   // arena 2: FW (k x dc) | Gw (dc x dc) | G (d x d) | g (d) | r (k) | c (d) | y (2d) | part | out
@@ -384,20 +573,14 @@ static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, dou
     return SLRA_OK;
   }
   if (FWext) SLRA_CUDA(cudaMemcpyAsync(FW, FWext, 8 * (size_t)k * dc, cudaMemcpyDeviceToDevice, st));
-  // Gram [FA Fb]^T [FA Fb] (dc x dc); G = leading d x d block, g = FA^T Fb
+  // ---- fast path: Gram [FA Fb]^T [FA Fb] (dc x dc); G = leading d x d block, g = FA^T Fb
   SLRA_TRY(launch_gemm(cx, 1, 0, dc, dc, k, 1.0, FW, k, FW, k, 0.0, Gw, dc));
   SLRA_CUDA(cudaMemcpy2DAsync(G, 8 * d, Gw, 8 * dc, 8 * d, d, cudaMemcpyDeviceToDevice, st));
   SLRA_CUDA(cudaMemcpyAsync(g, Gw + (size_t)d * dc, 8 * d, cudaMemcpyDeviceToDevice, st));
-  // rank tolerance from the largest column norm of FA
-  double* hs = static_cast<double*>(cx->hsmall);
-  SLRA_CUDA(cudaMemcpy2DAsync(hs, 8, Gw, 8 * (dc + 1), 8, (d < 500 ? d : 500), cudaMemcpyDeviceToHost, st));
-  SLRA_CUDA(cudaStreamSynchronize(st));
-  double dmax = 0.0;
-  for (int64_t i = 0; i < (d < 500 ? d : 500); ++i) dmax = hs[i] > dmax ? hs[i] : dmax;
-  const double tol2 = 1e-20 * dmax;
   const size_t smem = sizeof(double) * ((size_t)(d + 1) * kPW + (size_t)d + kPW);  // panel, diagonal, 1/L(j,j)
   SLRA_CUDA(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SLRA_TIMED(cx, "lsr_solve", cholesky_kernel<<<1, kLT, smem, st>>>(G, (int)d, tol2, d_status);)
+  // rank floor (1e-10 max_i ||FA(:,i)||)^2 from the Gram diagonal on the device (all d columns)
+  SLRA_TIMED(cx, "lsr_solve", cholesky_kernel<<<1, kLT, smem, st>>>(G, (int)d, 1e-20, d_status);)
   SLRA_CHECK_LAUNCH(cx);
   // x = G^{-1} g, then one refinement step x += G^{-1} FA^T (Fb - FA x)
   SLRA_TIMED(cx, "lsr_solve", chol_solve_kernel<<<1, kST, 8 * d, st>>>(G, (int)d, g, x_hat, d_status, 0);)
@@ -412,6 +595,26 @@ static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, dou
   SLRA_CHECK_LAUNCH(cx);
   SLRA_TIMED(cx, "reduce", sum_kernel<<<1, 256, 0, st>>>(part, rgrid, out);)
   SLRA_CHECK_LAUNCH(cx);
+  double* hs = static_cast<double*>(cx->hsmall);
+  SLRA_CUDA(cudaMemcpyAsync(hs, out, 8, cudaMemcpyDeviceToHost, st));
+  SLRA_CUDA(cudaMemcpyAsync(hs + 1, d_status, 8, cudaMemcpyDeviceToHost, st));
+  SLRA_CUDA(cudaStreamSynchronize(st));
+  const int32_t* hst = reinterpret_cast<const int32_t*>(hs + 1);
+  if (hst[0] == 0 && hst[1] == 0) {
+    if (h_sketched_residual) *h_sketched_residual = sqrt(hs[0]);
+    return SLRA_OK;
+  }
+  if (!fallback) return SLRA_ERR_UNSUPPORTED;
+  // ---- exact path (ill-conditioned or dependent sketch): the reference's
+  // ColPivHouseholderQR on a copy of FW, its rank rule, its solve
+  double* Wq = static_cast<double*>(arena(cx, 13, sizeof(double) * ((size_t)k * dc + 4 * (size_t)d + 64)));
+  if (!Wq) return SLRA_ERR_CUDA;
+  SLRA_CUDA(cudaMemcpyAsync(Wq, FW, 8 * (size_t)k * dc, cudaMemcpyDeviceToDevice, st));
+  SLRA_TRY(launch_colpiv_lsq(cx, Wq, k, (int)d, Wq + (size_t)k * dc, 1, x_hat, d_status));
+  SLRA_TIMED(cx, "lsr_solve", lsq_residual_kernel<<<rgrid, 256, 0, st>>>(FW, k, (int)d, x_hat, r, part);)
+  SLRA_CHECK_LAUNCH(cx);
+  SLRA_TIMED(cx, "reduce", sum_kernel<<<1, 256, 0, st>>>(part, rgrid, out);)
+  SLRA_CHECK_LAUNCH(cx);
   SLRA_CUDA(cudaMemcpyAsync(hs, out, 8, cudaMemcpyDeviceToHost, st));
   SLRA_CUDA(cudaMemcpyAsync(hs + 1, d_status, 4, cudaMemcpyDeviceToHost, st));
   SLRA_CUDA(cudaStreamSynchronize(st));
@@ -420,9 +623,62 @@ static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, dou
   return SLRA_OK;
 }
 
+__global__ void upper_copy_kernel(const double* __restrict__ W, int64_t ldw, int d, double* __restrict__ R) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)d * d; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % d), j = (int)(e / d);
+    R[e] = i <= j ? W[i + j * ldw] : 0.0;
+  }
+}
+__global__ void perm_scatter_kernel(const double* __restrict__ y, const int* __restrict__ perm, int d,
+                                    double* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) x[perm[i]] = y[i];
+}
+
 }  // namespace slra_dev
 
 extern "C" {
+
+int slra_pinv(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, double rank_tol, double* d_P,
+              int64_t ldp, int64_t* h_rank);
+
+int slra_lsq_exact(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t d, const double* b, double* x,
+                   int64_t* h_rank) {
+  if (!ctx || lda < m || m <= d || d < 1) return SLRA_ERR_INVALID_ARGUMENT;
+  if (d > 768) return SLRA_ERR_UNSUPPORTED;
+  Context* cx = C(ctx);
+  cudaStream_t st = cx->stream;
+  double* FW = nullptr;
+  SLRA_TRY(lsr_solve(cx, nullptr, m, d, nullptr, nullptr, &FW));
+  SLRA_CUDA(cudaMemcpy2DAsync(FW, 8 * m, A, 8 * lda, 8 * m, d, cudaMemcpyDeviceToDevice, st));
+  SLRA_CUDA(cudaMemcpyAsync(FW + (size_t)m * d, b, 8 * m, cudaMemcpyDeviceToDevice, st));
+  // well-conditioned A: the normal-equation solve is pinv(A) b (full rank, every sigma above the cut)
+  const int fs = lsr_solve(cx, nullptr, m, d, x, nullptr, nullptr, 0);
+  if (fs == SLRA_OK) {
+    if (h_rank) *h_rank = d;
+    return SLRA_OK;
+  }
+  if (fs != SLRA_ERR_UNSUPPORTED) return fs;
+  // otherwise pinv(A) b = Pi pinv(R) (Q^T b)(0:d) from the column-pivoted QR
+  // A Pi = Q R (sigma(R) = sigma(A): the same 1e-10 cut as the reference's
+  // SVD of A, linalg.cpp:111-121), the minimum-norm solution
+  const size_t dc = (size_t)d + 1;
+  double* Wq = static_cast<double*>(arena(cx, 13, sizeof(double) * ((size_t)m * dc + 4 * (size_t)d + 64)));
+  double* R = static_cast<double*>(arena(cx, 9, sizeof(double) * (2 * (size_t)d * d + 2 * (size_t)d)));
+  if (!Wq || !R) return SLRA_ERR_CUDA;
+  double* P = R + (size_t)d * d;
+  double* y = P + (size_t)d * d;
+  SLRA_CUDA(cudaMemcpyAsync(Wq, FW, 8 * (size_t)m * dc, cudaMemcpyDeviceToDevice, st));
+  double* qws = Wq + (size_t)m * dc;
+  SLRA_TRY(launch_colpiv_lsq(cx, Wq, m, (int)d, qws, 0, nullptr, static_cast<int32_t*>(cx->dsmall)));
+  upper_copy_kernel<<<64, 256, 0, st>>>(Wq, m, (int)d, R);
+  SLRA_CHECK_LAUNCH(cx);
+  SLRA_TRY(slra_pinv(ctx, R, d, d, d, 1e-10, P, d, h_rank));
+  SLRA_TRY(launch_gemm(cx, 0, 0, d, 1, d, 1.0, P, d, Wq + (size_t)m * d, m, 0.0, y, d));
+  const int* perm = reinterpret_cast<const int*>(qws + 3 * d + 2);
+  perm_scatter_kernel<<<1, 256, 0, st>>>(y, perm, (int)d, x);
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}
 
 int slra_sketch_solve(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t d, const double* b,
                       const int64_t* src, const double* coef, const int32_t* q, int64_t width, int tree, int64_t k,

@@ -138,13 +138,14 @@ LsrReport sketch_solve(const LsrProblem& p, const SketchOperator& F, bool with_t
   return rep;
 }
 
-Vector solve_exact(const LsrProblem& p) {  // lsr.cpp:21-24 (device normal-equation solve)
+Vector solve_exact(const LsrProblem& p) {  // lsr.cpp:21-24: pseudo_inverse(A) * b
   validate(p);
-  // exact LS = sketch_solve with the identity sketch (all m rows, in order)
-  std::vector<Index> all(static_cast<size_t>(p.A.rows()));
-  for (Index i = 0; i < p.A.rows(); ++i) all[static_cast<size_t>(i)] = i;
-  const auto F = make_sub_identity(IndexSet(all, p.A.rows()), p.A.rows());
-  return sketch_solve(p, *F, false).x_hat;
+  DeviceMatrix dA = DeviceMatrix::upload(p.A);
+  DevBuf<double> db(p.b), dx(static_cast<size_t>(p.A.cols()));
+  int64_t rank = 0;
+  check(slra_lsq_exact(device_context(), dA.data(), dA.ld(), p.A.rows(), p.A.cols(), db.get(), dx.get(), &rank),
+        "solve_exact");
+  return dx.download();
 }
 
 double residual_ratio(const LsrProblem& p, const Vector& x_hat) {  // lsr.cpp:30-35
