@@ -386,6 +386,29 @@ int slra_lsq_exact(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int6
 int slra_lsr_residual(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
                       const double* d_b, const double* d_x, double* d_out);
 
+/* ------------------------------------------------------------ §8b/§8e multi-GPU
+ * NCCL collectives (NVLink / NVSwitch on one box) on the context's stream
+ * for the row-sharded configurations: config 4's single all-reduce of the
+ * k x (d+1) sketched rows (lsr.cpp:44-50 sharded by rows), config 3's
+ * per-half-sweep strip exchange (cur.cpp:215-236) and the residual partials.
+ * One process per GPU; rank 0 makes the id and hands it to the others out of
+ * band (e.g. over the launcher's store). NCCL is loaded at first use
+ * (dlopen libnccl.so.2); without it these return SLRA_ERR_UNSUPPORTED.
+ * Collectives order with the kernels on the same stream (no host sync). */
+typedef struct slra_comm_s* slra_comm;
+#define SLRA_COMM_ID_BYTES 128
+int slra_comm_available(void);
+int slra_comm_unique_id(void* h_id); /* SLRA_COMM_ID_BYTES bytes */
+int slra_comm_init(slra_ctx ctx, int nranks, int rank, const void* h_id, slra_comm* out);
+int slra_comm_destroy(slra_comm comm);
+int slra_comm_size(slra_comm comm);
+int slra_comm_rank(slra_comm comm);
+int slra_comm_allreduce_sum(slra_comm comm, const double* d_send, double* d_recv, int64_t count);
+int slra_comm_allreduce_max(slra_comm comm, const double* d_send, double* d_recv, int64_t count);
+/* d_recv = the ranks' d_send blocks (count_per_rank each) in rank order */
+int slra_comm_allgather(slra_comm comm, const double* d_send, double* d_recv, int64_t count_per_rank);
+int slra_comm_broadcast(slra_comm comm, double* d_buf, int64_t count, int root);
+
 #ifdef __cplusplus
 }
 #endif

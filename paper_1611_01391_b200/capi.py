@@ -18,6 +18,7 @@ _CTYPES = {
     "double": ctypes.c_double,
     "void": None,
     "slra_ctx": ctypes.c_void_p,
+    "slra_comm": ctypes.c_void_p,
     "const char*": ctypes.c_char_p,
 }
 
@@ -25,7 +26,7 @@ STATUS = {
     "SLRA_OK": 0, "SLRA_ERR_INVALID_ARGUMENT": 1, "SLRA_ERR_RANGE_FAILURE": 2,
     "SLRA_ERR_SKETCH_RANK_FAILURE": 3, "SLRA_ERR_SELECTION_FAILURE": 4,
     "SLRA_ERR_GENERATOR_RANK_FAILURE": 5, "SLRA_ERR_CUDA": 6, "SLRA_ERR_NO_DEVICE": 7,
-    "SLRA_ERR_UNSUPPORTED": 8,
+    "SLRA_ERR_UNSUPPORTED": 8, "SLRA_ERR_PREMULT_RANK_FAILURE": 9,
 }
 
 

@@ -58,6 +58,14 @@ __device__ __forceinline__ double fast_sqrt(double x) {
 __device__ __forceinline__ void jacobi_rotation(double a, double b, double g, double& cs, double& sn) {
   const double d = b - a, g2 = 2.0 * g;
   const double h = fma(d, d, g2 * g2);
+  if (!(h < DBL_MAX) || h < DBL_MIN) {
+    // overflowing (column norms above ~1e154) or subnormal Gram entries: the
+    // IEEE sqrt / divide (the MUFU seeds would give inf * 0 or flush to zero)
+    const double t = (g2 * g2 < 1e-17 * (d * d)) ? g2 / (2.0 * d) : copysign(1.0, d) * g2 / (fabs(d) + sqrt(h));
+    cs = 1.0 / sqrt(fma(t, t, 1.0));
+    sn = cs * t;
+    return;
+  }
   const double rr = (g2 * g2 < 1e-17 * (d * d)) ? fabs(d) : h * mufu_rsqrt(h);
   const double t = copysign(1.0, d) * g2 * mufu_rcp(fabs(d) + rr);
   const double q = fma(t, t, 1.0);

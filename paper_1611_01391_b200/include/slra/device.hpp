@@ -12,6 +12,9 @@ namespace slra {
 /// (DeviceError) when no sm_100 device is usable — there is no CPU path.
 slra_ctx device_context();
 /// Re-target the default context (e.g. torch's current device/stream).
+/// Registered release hooks run first, while the old context is still
+/// current, so buffers tied to it are freed through it.
 void set_device(int device, void* stream = nullptr);
+void on_context_release(void (*hook)());
 
 }  // namespace slra

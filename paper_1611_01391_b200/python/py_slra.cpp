@@ -48,6 +48,19 @@ static FArray to_np(const Matrix& M) {
 // keyed by size when its array dies, so steady-state calls allocate nothing.
 static std::mutex pin_mu;
 static std::unordered_multimap<size_t, void*>* pin_free = new std::unordered_multimap<size_t, void*>();
+static size_t pin_free_bytes = 0;
+constexpr size_t kPinPoolCap = size_t(1) << 30;  // page-locked bytes kept for reuse
+// HBM staging buffers of the host-buffer entry points (one per entry),
+// released through the old context when set_device replaces it
+static DeviceMatrix* g_staging = new DeviceMatrix[4];
+static DeviceMatrix& staging(int slot, Index rows, Index cols) {
+  DeviceMatrix& s = g_staging[slot];
+  if (s.rows() != rows || s.cols() != cols) s = DeviceMatrix(rows, cols);
+  return s;
+}
+static void release_staging() {
+  for (int i = 0; i < 4; ++i) g_staging[i] = DeviceMatrix();
+}
 static FArray pinned_np(Index rows, Index cols) {
   const size_t bytes = sizeof(double) * static_cast<size_t>(rows) * static_cast<size_t>(cols);
   void* p = nullptr;
@@ -57,15 +70,22 @@ static FArray pinned_np(Index rows, Index cols) {
     if (it != pin_free->end()) {
       p = it->second;
       pin_free->erase(it);
+      pin_free_bytes -= bytes;
     }
   }
   if (!p) check(slra_host_alloc(static_cast<int64_t>(bytes ? bytes : 8), &p), "pinned result buffer");
   py::capsule hold(new std::pair<void*, size_t>(p, bytes), [](void* h) {
     auto* ph = static_cast<std::pair<void*, size_t>*>(h);
+    bool keep = false;
     {
       std::lock_guard<std::mutex> g(pin_mu);
-      pin_free->emplace(ph->second, ph->first);
+      if (pin_free_bytes + ph->second <= kPinPoolCap) {  // bounded: beyond the cap, give it back
+        pin_free->emplace(ph->second, ph->first);
+        pin_free_bytes += ph->second;
+        keep = true;
+      }
     }
+    if (!keep) slra_host_free(ph->first);
     delete ph;
   });
   return FArray({rows, cols}, {static_cast<py::ssize_t>(sizeof(double)), static_cast<py::ssize_t>(sizeof(double) * rows)},
@@ -191,6 +211,7 @@ PYBIND11_MODULE(_slra, m) {
   py::register_local_exception<EmptySample>(m, "EmptySample", base.ptr());
   py::register_local_exception<DeviceError>(m, "DeviceError", base.ptr());
 
+  on_context_release(&release_staging);
   m.def("set_device", [](int dev, uintptr_t stream) { set_device(dev, reinterpret_cast<void*>(stream)); },
         py::arg("device") = 0, py::arg("stream") = 0);
   m.def("launch_count", []() { return slra_ctx_launch_count(device_context()); });
@@ -586,9 +607,7 @@ PYBIND11_MODULE(_slra, m) {
   // straight from the caller's (pinned) host buffer, U/V returned to the host.
   m.def("range_finder_host", [](uintptr_t M_host, Index mm, Index n, const PyOp& H, Index r, bool truncated) {
     const SketchPlan plan = compile_plan(*H.p, Side::Right);
-    static DeviceMatrix* staging = new DeviceMatrix();  // reused HBM staging buffer (never freed)
-    if (staging->rows() != mm || staging->cols() != n) *staging = DeviceMatrix(mm, n);
-    DeviceMatrix& dM = *staging;
+    DeviceMatrix& dM = staging(0, mm, n);
     check(slra_memcpy_h2d(device_context(), dM.data(), reinterpret_cast<const void*>(M_host), 8 * mm * n),
           "range_finder_host");
     const Index uc = truncated ? r : H.p->cols();
@@ -608,8 +627,7 @@ PYBIND11_MODULE(_slra, m) {
     const int nsk = static_cast<int>(Hs.size());
     if (nsk < 1) throw std::invalid_argument("range_finder_batched_host: no sketches");
     const Index l = Hs[0].p->cols();
-    static DeviceMatrix* staging = new DeviceMatrix();  // reused HBM staging buffer (never freed)
-    if (staging->rows() != mm || staging->cols() != n) *staging = DeviceMatrix(mm, n);
+    DeviceMatrix* staging = &::staging(1, mm, n);  // reused HBM staging buffer
     check(slra_memcpy_h2d(device_context(), staging->data(), reinterpret_cast<const void*>(M_host), 8 * mm * n),
           "range_finder_batched_host");
     std::vector<SketchPlan> plans;
@@ -661,8 +679,7 @@ PYBIND11_MODULE(_slra, m) {
   // (pinned) host buffers; x_hat and both residuals come back to the host.
   m.def("sketch_solve_host", [](uintptr_t A_host, uintptr_t b_host, Index mm, Index d, const PyOp& F) {
     const SketchPlan plan = compile_plan(*F.p, Side::Left);
-    static DeviceMatrix* staging = new DeviceMatrix();  // reused HBM staging buffer (never freed)
-    if (staging->rows() != mm || staging->cols() != d + 1) *staging = DeviceMatrix(mm, d + 1);
+    DeviceMatrix* staging = &::staging(3, mm, d + 1);  // reused HBM staging buffer
     slra_ctx cx = device_context();
     double* dA = staging->data();
     double* db = dA + mm * d;
@@ -686,8 +703,7 @@ PYBIND11_MODULE(_slra, m) {
   // nucleus and the residual come back to the host.
   m.def("cross_approx_host", [](uintptr_t M_host, Index mm, Index n, Index r, Index k, Index l,
                                 const std::vector<Index>& init_rows, int loops, double h) {
-    static DeviceMatrix* staging = new DeviceMatrix();  // reused HBM staging buffer (never freed)
-    if (staging->rows() != mm || staging->cols() != n) *staging = DeviceMatrix(mm, n);
+    DeviceMatrix* staging = &::staging(2, mm, n);  // reused HBM staging buffer
     check(slra_memcpy_h2d(device_context(), staging->data(), reinterpret_cast<const void*>(M_host), 8 * mm * n),
           "cross_approx_host");
     DeviceOracle o(staging->data(), mm, n, mm);
@@ -748,6 +764,44 @@ PYBIND11_MODULE(_slra, m) {
                                     ptr<double>(ns)),
           "cross_approx_batched");
   });
+  // §8e multi-GPU over the C-ABI's NCCL communicator (one process per GPU)
+  m.def("comm_available", []() { return slra_comm_available() != 0; });
+  m.def("comm_unique_id", []() {
+    std::string id(SLRA_COMM_ID_BYTES, '\0');
+    check(slra_comm_unique_id(id.data()), "comm_unique_id");
+    return py::bytes(id);
+  });
+  m.def("comm_init", [](int nranks, int rank, const py::bytes& id) {
+    std::string s = id;
+    if (s.size() != SLRA_COMM_ID_BYTES) throw std::invalid_argument("comm_init: id must be 128 bytes");
+    slra_comm c = nullptr;
+    {
+      py::gil_scoped_release nogil;
+      check(slra_comm_init(device_context(), nranks, rank, s.data(), &c), "comm_init");
+    }
+    return reinterpret_cast<uintptr_t>(c);
+  });
+  m.def("comm_destroy", [](uintptr_t c) { check(slra_comm_destroy(reinterpret_cast<slra_comm>(c)), "comm_destroy"); });
+  m.def("comm_allreduce_sum", [](uintptr_t c, uintptr_t send, uintptr_t recv, int64_t count) {
+    check(slra_comm_allreduce_sum(reinterpret_cast<slra_comm>(c), ptr<const double>(send), ptr<double>(recv), count),
+          "comm_allreduce_sum");
+  });
+  m.def("comm_allgather", [](uintptr_t c, uintptr_t send, uintptr_t recv, int64_t count) {
+    check(slra_comm_allgather(reinterpret_cast<slra_comm>(c), ptr<const double>(send), ptr<double>(recv), count),
+          "comm_allgather");
+  });
+  m.def("sketch_solve_sharded", [](uintptr_t c, uintptr_t A, Index lda, Index m_local, Index d, uintptr_t b,
+                                   Index row0, Index m_global, const PyOp& F, bool with_true) {
+    LsrReport r = sketch_solve_sharded(reinterpret_cast<slra_comm>(c), ptr<const double>(A), lda, m_local, d,
+                                       ptr<const double>(b), row0, m_global, *F.p, with_true);
+    py::dict out;
+    out["x_hat"] = vec_np(r.x_hat);
+    out["sketched_residual"] = r.sketched_residual;
+    out["true_residual"] = r.true_residual ? py::cast(*r.true_residual) : py::none();
+    out["k"] = r.k;
+    return out;
+  }, py::arg("comm"), py::arg("A"), py::arg("lda"), py::arg("m_local"), py::arg("d"), py::arg("b"), py::arg("row0"),
+     py::arg("m_global"), py::arg("F"), py::arg("with_true_residual") = false);
   // end-to-end batched C-A over HOST blocks (pinned): chunks streamed to the device, results back
   m.def("cross_approx_batched_host", [](uintptr_t A, Index lda, Index stride, Index nblocks, Index mm, Index n,
                                         Index r, Index k, Index l, uintptr_t init_rows, int loops, double h,

@@ -77,9 +77,49 @@ class DeviceOps:
 
     def __init__(self, slra, torch):
         self.s, self.torch = slra, torch
+        # the C-ABI kernels and torch.distributed's collectives must share one
+        # stream on this rank's device: bind the slra context to torch's
+        # current stream (collectives then order after the kernels that write
+        # their buffers, with no host synchronisation)
+        # (torch's legacy default stream has handle 0, which the C-ABI reads as
+        # "make a private stream": pass cudaStreamLegacy = 1 instead)
+        handle = torch.cuda.current_stream().cuda_stream or 1
+        if slra.stream_ptr() != handle:
+            slra.set_device(torch.cuda.current_device(), handle)
+        self.stream = handle
+        self._check_stream()
+
+    def _check_stream(self):
+        assert self.s.stream_ptr() == (self.torch.cuda.current_stream().cuda_stream or 1), \
+            "slra context stream != torch current stream: collectives would race the kernels"
 
     def _f64(self, *shape):
         return self.torch.empty(*shape, dtype=self.torch.float64, device="cuda")
+
+    def ca_blocks(self, seed, b0, nb, m, k, loops, h):
+        """Config-5 blocks b0..b0+nb-1: host points / initial rows from the
+        reference Rng (per-block seeds), blocks materialised on the device,
+        one batched C-A + fused residual launch. Per-block results (device)."""
+        import numpy as np
+        torch = self.torch
+        px, py, qx, qy = (np.empty((nb, m)) for _ in range(4))
+        init = np.empty((nb, k), dtype=np.int64)
+        self.s.gen_log_kernel_batch(seed, b0, nb, m, m, k, px.ctypes.data, py.ctypes.data, qx.ctypes.data,
+                                    qy.ctypes.data, init.ctypes.data)
+        dev = [torch.from_numpy(a).cuda() for a in (px, py, qx, qy)]
+        A = self._f64(nb, m, m)
+        self.s.gen_log_kernel_blocks_device(*[d.data_ptr() for d in dev], nb, m, m, A.data_ptr(), m, m * m)
+        init_d = torch.from_numpy(init).cuda()
+        out = {"I": torch.empty(nb, k, dtype=torch.int64, device="cuda"),
+               "J": torch.empty(nb, k, dtype=torch.int64, device="cuda"),
+               "U": self._f64(nb, k * k), "r": torch.empty(nb, dtype=torch.int64, device="cuda"),
+               "status": torch.empty(nb, dtype=torch.int32, device="cuda"),
+               "resid_sq": self._f64(nb), "norm_sq": self._f64(nb)}
+        self.s.cross_approx_batched_device(A.data_ptr(), m, m * m, nb, m, m, 0, k, k, init_d.data_ptr(), loops, h,
+                                           out["I"].data_ptr(), out["J"].data_ptr(), out["U"].data_ptr(),
+                                           out["r"].data_ptr(), out["status"].data_ptr(), out["resid_sq"].data_ptr(),
+                                           out["norm_sq"].data_ptr())
+        return out
 
     def rows_shard(self, W_t, row0, src, coef, width, k, transpose, out=None):
         ncols, mloc = W_t.shape
@@ -199,3 +239,17 @@ def sketch_solve(ops, comm, A_t, b, row0, d, src, coef, width, k, torch):
     part = ops.lsr_residual_partial(A_t, b, x)
     comm.allreduce_(part)
     return x, sres, float(part[0].item()) ** 0.5
+
+
+def cross_approx_blocks(ops, comm, seed, nblocks, torch, m=256, k=32, loops=2, h=1.1):
+    """Config 5 over the ranks: rank r factorises the
+    contiguous block range split(nblocks, world, r) of the seeded batch — the
+    per-block seeds derive_seed(seed, b) make every block's input and result
+    independent of the rank count — with no communication on the data path.
+    One allgather of the per-block scalars at the end. Returns a
+    (nblocks, 4) float64 tensor: r, ||B - CUR||^2, ||B||^2, status."""
+    b0, nb = split(nblocks, comm.world, comm.rank)
+    res = ops.ca_blocks(seed, b0, nb, m, k, loops, h)
+    loc = torch.stack([res["r"].double(), res["resid_sq"], res["norm_sq"], res["status"].double()], 0)  # (4, nb)
+    counts = [split(nblocks, comm.world, r)[1] for r in range(comm.world)]
+    return comm.allgather_cols(loc.contiguous(), counts).T.contiguous()

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <numbers>
 #include <string>
 
@@ -33,6 +34,7 @@ void check(int status, const char* where) {
 namespace {
 std::mutex g_mu;
 slra_ctx g_ctx = nullptr;
+std::vector<void (*)()>* g_hooks = new std::vector<void (*)()>();
 }  // namespace
 
 slra_ctx device_context() {
@@ -41,7 +43,21 @@ slra_ctx device_context() {
   return g_ctx;
 }
 
+void on_context_release(void (*hook)()) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_hooks->push_back(hook);
+}
+
 void set_device(int device, void* stream) {
+  std::vector<void (*)()> hooks;
+  bool live = false;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    hooks = *g_hooks;
+    live = g_ctx != nullptr;
+  }
+  if (live)
+    for (auto f : hooks) f();
   std::lock_guard<std::mutex> lk(g_mu);
   if (g_ctx) slra_ctx_destroy(g_ctx);
   g_ctx = nullptr;

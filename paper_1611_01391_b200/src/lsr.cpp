@@ -156,4 +156,39 @@ double residual_ratio(const LsrProblem& p, const Vector& x_hat) {  // lsr.cpp:30
   return residual_norm(p, x_hat) / opt;
 }
 
+LsrReport sketch_solve_sharded(slra_comm comm, const double* dA, Index lda, Index m_local, Index d, const double* db,
+                               Index row0, Index m_global, const SketchOperator& F, bool with_true_residual) {
+  if (!comm) throw std::invalid_argument("sketch_solve_sharded: no communicator");
+  if (F.cols() != m_global) throw std::invalid_argument("sketch_solve: F cols != m");
+  if (F.rows() <= d) throw std::invalid_argument("sketch_solve: need k > d");
+  if (row0 < 0 || m_local < 0 || row0 + m_local > m_global || lda < m_local)
+    throw std::invalid_argument("sketch_solve_sharded: bad row range");
+  slra_ctx cx = device_context();
+  const SketchPlan plan = compile_plan(F, Side::Left);
+  if (plan.tree) throw std::invalid_argument("sketch_solve_sharded: butterfly (abridged Hadamard) plans do not shard");
+  const Index k = plan.count;
+  DevBuf<int64_t> src(plan.src);
+  DevBuf<double> coef(plan.coef);
+  // per-rank contributions to F (A | b): foreign rows are skipped (exact zeros)
+  DevBuf<double> FW(static_cast<size_t>(k * (d + 1)));
+  check(slra_sketch_rows_shard(cx, dA, lda, row0, m_local, d, src.get(), coef.get(), plan.width, k, FW.get(), k, 0),
+        "sketch_solve_sharded");
+  check(slra_sketch_rows_shard(cx, db, m_local, row0, m_local, 1, src.get(), coef.get(), plan.width, k,
+                               FW.get() + k * d, k, 0),
+        "sketch_solve_sharded");
+  check(slra_comm_allreduce_sum(comm, FW.get(), FW.get(), k * (d + 1)), "sketch_solve_sharded: allreduce");
+  DevBuf<double> dx(static_cast<size_t>(d));
+  LsrReport rep;
+  check(slra_lsr_solve_sketched(cx, FW.get(), k, k, d, dx.get(), &rep.sketched_residual), "sketch_solve");
+  rep.x_hat = dx.download();
+  rep.k = F.rows();
+  if (with_true_residual) {
+    DevBuf<double> out(2);
+    check(slra_lsr_residual(cx, dA, lda, m_local, d, db, dx.get(), out.get()), "residual_norm");
+    check(slra_comm_allreduce_sum(comm, out.get(), out.get(), 1), "residual_norm: allreduce");
+    rep.true_residual = std::sqrt(out.download()[0]);
+  }
+  return rep;
+}
+
 }  // namespace slra

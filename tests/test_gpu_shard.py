@@ -113,7 +113,16 @@ def _lsr_worker(slra, torch, dist, rank, world):
     return {"x": x.tolist(), "sres": sres, "tres": tres}
 
 
-WORKERS = {"ca": _ca_worker, "lsr": _lsr_worker}
+NB5 = 301  # config-5 blocks for the split test (ragged over two ranks)
+
+
+def _blocks_worker(slra, torch, dist, rank, world):
+    from paper_1611_01391_b200 import shard
+    out = shard.cross_approx_blocks(shard.DeviceOps(slra, torch), shard.Comm(dist), 0, NB5, torch)
+    return out.cpu().numpy().tolist()
+
+
+WORKERS = {"ca": _ca_worker, "lsr": _lsr_worker, "blocks": _blocks_worker}
 
 
 @pytest.fixture(scope="module")
@@ -165,3 +174,51 @@ def test_sharded_sketch_solve_two_ranks_one_gpu(slra):
     assert out[0]["sres"] == sres
     r = (At.T @ x - b).norm().item()
     assert abs(out[0]["tres"] - r) <= 1e-10 * b.norm().item()
+
+
+def test_config5_block_split_two_ranks_one_gpu(slra):
+    """Config 5 split over two ranks sharing the GPU: the gathered per-block
+    ranks, residuals and norms equal the single-process batched run bit for bit."""
+    import torch
+    from paper_1611_01391_b200 import shard
+    out = _spawn("blocks")
+    assert all(isinstance(v, list) for v in out.values()), out
+    single = shard.cross_approx_blocks(shard.DeviceOps(slra, torch), shard.Comm(None), 0, NB5, torch).cpu().numpy()
+    for r in (0, 1):
+        assert np.array_equal(np.array(out[r]), single)
+    assert (single[:, 3] == 0).all()
+
+
+def test_comm_single_rank_sketch_solve(slra):
+    """The C-ABI's NCCL communicator (slra_comm_*), one rank on this GPU: the
+    sharded driver sketch_solve_sharded (one allreduce of the sketch, one of
+    the residual partials) equals sketch_solve on the same data."""
+    import torch
+    if not slra.comm_available():
+        pytest.skip("libnccl.so.2 not loadable")
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    slra.set_device(0, stream.cuda_stream)
+    comm = slra.comm_init(1, 0, slra.comm_unique_id())
+    try:
+        m, d, k = 20000, 48, 1024
+        rng = slra.Rng(31)
+        A, b = slra.gen_lsr_gaussian(m, d, 1e-6, rng)
+        F = slra.make_product([slra.make_sub_identity(rng.distinct_indices(k, m), m),
+                               slra.gen_sparse_circulant(m, 2, rng), slra.gen_sign_diagonal(m, rng)])
+        At = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+        bd = torch.from_numpy(b).cuda()
+        got = slra.sketch_solve_sharded(comm, At.data_ptr(), m, m, d, bd.data_ptr(), 0, m, F, True)
+        ref = slra.sketch_solve(A, b, F, True)
+        assert np.array_equal(got["x_hat"], ref["x_hat"])
+        assert abs(got["true_residual"] - ref["true_residual"]) <= 1e-12 * np.linalg.norm(b)
+        # allreduce / allgather on one rank are copies
+        x = torch.arange(10, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        slra.comm_allreduce_sum(comm, x.data_ptr(), y.data_ptr(), 10)
+        slra.comm_allgather(comm, x.data_ptr(), y.data_ptr(), 10)
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+    finally:
+        slra.comm_destroy(comm)

@@ -38,6 +38,15 @@ class OracleOps:
     def __init__(self, oracle):
         self.o = oracle
 
+    def ca_blocks(self, seed, b0, nb, m, k, loops, h):
+        import bench
+        import paper_1611_01391_b200 as slra  # host-side input generator only
+        px, py, qx, qy, init = bench.config5_host_inputs(slra, seed, b0, nb)
+        blocks = np.ascontiguousarray(bench.config5_host_blocks(px, py, qx, qy))
+        d = bench.oracle_blocks(self.o, blocks, init, 1)
+        return {"r": torch.from_numpy(d["r"]), "resid_sq": torch.from_numpy(d["resid_sq"]),
+                "norm_sq": torch.from_numpy(d["norm_sq"]), "status": torch.from_numpy(d["status"])}
+
     def rows_shard(self, W_t, row0, src, coef, width, k, transpose, out=None):
         W = W_t.numpy()  # (ncols, mloc): W[j, i] = row (row0 + i), column j
         ncols, mloc = W.shape
@@ -234,3 +243,26 @@ def test_sharded_sketch_solve_matches_oracle(oracle, kind):
     x = np.array(out[0]["x"])
     assert np.linalg.norm(x - rep["x_hat"]) <= 1e-10 * np.linalg.norm(rep["x_hat"])
     assert abs(out[0]["tres"] - np.linalg.norm(A @ rep["x_hat"] - b)) <= 1e-10 * np.linalg.norm(b)
+
+
+NB5 = 9
+
+
+def _blocks_worker(rank, world):
+    oracle = _oracle()
+    out = shard.cross_approx_blocks(OracleOps(oracle), shard.Comm(dist), 3, NB5, torch)
+    return out.numpy().tolist()
+
+
+def test_config5_block_split_world2(oracle):
+    """Config 5 split over two ranks (ragged: 5 + 4 blocks): the gathered
+    per-block ranks and residuals equal the single-process run bit for bit
+    (per-block seeds, no data-path communication)."""
+    out = _spawn(_blocks_worker)
+    assert all(isinstance(v, list) for v in out.values()), out
+    single = shard.cross_approx_blocks(OracleOps(oracle), shard.Comm(None), 3, NB5, torch).numpy()
+    for r in (0, 1):
+        got = np.array(out[r])
+        assert got.shape == (NB5, 4)
+        assert np.array_equal(got, single)
+    assert (single[:, 3] == 0).all() and (single[:, 0] >= 1).all()
