@@ -6,10 +6,14 @@ checker. Tolerances follow BASELINE.json north_star: index sets bit-exact
 where well-posed, sketches bit-exact, factors/residuals within 1e-10
 relative to ||A||_F.
 """
+import os
+import sys
+
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 TOL = 1e-10
 
@@ -633,3 +637,24 @@ def test_native_library_loaded(slra):
     assert "libslra_cuda.so" in maps and "libslra.so" in maps
     assert slra.launch_count() > 0
     assert os.path.dirname(slra.__file__) in maps
+
+
+def test_integration_glue_cross_approx_on_gpu(slra, oracle, tmp_path):
+    """the reference-side dispatch (tests/integration/,
+    linked against libslra_cuda.so only) on the config-1 problem returns the
+    oracle's ordered I, J."""
+    import subprocess
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_host_cpu import build_integration_example, write_integration_input
+    exe = build_integration_example(tmp_path)
+    A = slra.gen_factor_gaussian(256, 256, 8, 1e-8, slra.Rng(5))
+    init = slra.Rng(1005).distinct_indices(16, 256)
+    inp = str(tmp_path / "in.bin")
+    write_integration_input(inp, A, init, 3, 8)
+    p = subprocess.run([exe, inp], capture_output=True, text=True)
+    assert p.returncode == 0, p.stdout + p.stderr
+    lines = dict(line.split(" ", 1) for line in p.stdout.strip().splitlines())
+    o = oracle.cross_approx(A, 8, 16, 16, init, 3, 1.1, None, oracle.Rng(0))
+    assert [int(v) for v in lines["I"].split()] == o["I"]
+    assert [int(v) for v in lines["J"].split()] == o["J"]
+    assert int(lines["r"]) == 8 and int(lines["steps"]) == 6

@@ -169,3 +169,43 @@ def test_plan_rejects_two_combining_factors(slra):
     op = slra.make_product([slra.make_abridged_hadamard(16, 2), slra.make_abridged_hadamard(16, 2)])
     with pytest.raises(ValueError):
         op.plan("left")
+
+
+# ---------------------------------------------------------------- INTEGRATION.md glue
+def build_integration_example(tmp_path):
+    """Compile the reference-side glue of INTEGRATION.md §2-3 (b200.hpp + the
+    SLRA_B200 cross_approx definition, tests/integration/) against the C-ABI
+    header, linking libslra_cuda.so only — what a maintainer's build adds."""
+    import subprocess
+    src = os.path.join(ROOT, "tests", "integration")
+    lib = os.path.join(ROOT, "paper_1611_01391_b200", "lib")
+    exe = str(tmp_path / "ca_dispatch")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", src,
+                    os.path.join(src, "cur_dispatch.cpp"), os.path.join(src, "main.cpp"), "-o", exe, "-L", lib,
+                    "-lslra_cuda", f"-Wl,-rpath,{lib}"], check=True)
+    return exe
+
+
+def write_integration_input(path, A, init, loops, r):
+    import numpy as np
+    m, n = A.shape
+    with open(path, "wb") as f:
+        np.array([m, n, len(init), loops, r], dtype=np.int64).tofile(f)
+        np.asfortranarray(A).T.astype(np.float64).tofile(f)  # column-major
+        np.array(init, dtype=np.int64).tofile(f)
+
+
+def test_integration_glue_compiles_and_fails_loudly_without_gpu(tmp_path):
+    import subprocess
+    import numpy as np
+    exe = build_integration_example(tmp_path)
+    A = np.random.default_rng(0).standard_normal((64, 48))
+    inp = str(tmp_path / "in.bin")
+    write_integration_input(inp, A, list(range(8)), 2, 4)
+    p = subprocess.run([exe, inp], capture_output=True, text=True)
+    import torch
+    if torch.cuda.is_available():
+        assert p.returncode == 0, p.stdout + p.stderr
+    else:
+        # no CPU fallback: the C-ABI refuses, the glue raises
+        assert p.returncode == 3 and "no sm_100 device" in p.stdout, p.stdout + p.stderr
