@@ -261,7 +261,9 @@ __device__ __forceinline__ T load_sel(const T* p, int64_t i, bool ok) {
   return ok ? v : T(0);
 }
 
-// m16n8k16 FP64 MMA (SASS DMMA.16816: 8x the work of 8x8x4 per instruction).
+// m16n8k16 FP64 MMA (8x the work of m8n8k4 per PTX instruction; on sm_100a
+// ptxas lowers it to a sequence of DMMA.8x8x4 — the SASS has no wider FP64
+// MMA — so the gain is fewer issued instructions, not a wider unit).
 // Fragments (g = lane >> 2, t = lane & 3), from the PTX f64 m16n8k16 layout
 // (as in CuTe's SM90_16x8x16_F64F64F64F64_TN traits):
 //   a[v] = A[g + 8 (v & 1)][t + 4 (v >> 1)]      v = 0..7  (A 16 x 16, row)

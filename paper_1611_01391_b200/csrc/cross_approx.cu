@@ -11,6 +11,7 @@
 #include <algorithm>
 
 #include "dense_cta.cuh"
+#include "blocked_qr.cuh"
 #include "select_regs.cuh"
 
 namespace slra_dev {
@@ -146,7 +147,13 @@ __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_s
   // registers, and the volume |det Q[idx, :]| is tracked through the swaps.
   // The pivot phase's reflectors are those of maxvol round 0's ColPivQR(G^T)
   // (G = Q(I, :)), so round 0 continues from them instead of refactorising.
-  cta_thin_qr_inplace<NT, CMAX>(s.S, len, len, nidx, s.tau, s.rv);
+  if (nidx <= 32 && NT == 256) {
+    // blocked Householder (8-column panels, DMMA trailing updates and
+    // block-reflector Q formation); scratch: the W / Gt / V regions
+    cta_blocked_qr_q<NT>(s.S, len, len, nidx, s.tau, s.W, s.rv);
+  } else {
+    cta_thin_qr_inplace<NT, CMAX>(s.S, len, len, nidx, s.tau, s.rv);
+  }
   SLRA_PROF(3);
   const int rq = count < nidx ? count : nidx;
   if (count > rq) {  // the padding branch needs the basis row norms (cur.cpp:125-134)

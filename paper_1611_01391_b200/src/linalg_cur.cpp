@@ -122,8 +122,9 @@ static void set_factors(CurDecomposition& c, const DevBuf<double>& dT, const Dev
 CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus) {
   // cur.cpp:137-162 (SVD nucleus)
   if (qr_nucleus) throw std::invalid_argument("primitive_cur: the QR nucleus is not on the device path");
-  if (I.size() < r || J.size() < r || r < 0 || (r == 0 && false))
-    throw std::invalid_argument("primitive_cur: need |I|, |J| >= r >= 1");
+  // r = 0 selects the adaptive rank (numerical_rank(G, 1e-10)); r < 0 is invalid
+  if (I.size() < r || J.size() < r || r < 0)
+    throw std::invalid_argument("primitive_cur: need |I|, |J| >= r >= 0 (0: adaptive rank)");
   if (I.bound() != M.rows() || J.bound() != M.cols()) throw std::invalid_argument("primitive_cur: index bounds");
   const DeviceMatrix& dA = M.device();
   const Index k = I.size(), l = J.size();

@@ -183,9 +183,14 @@ def test_cur_ca_strategy_parity(slra, oracle, name, n, L, r, tol, seed):
     M = cauchy_kernel(n) if name == "cauchy" else gravity_kernel(n, n)
     h = slra.build_hss(M, L, r, tol, "cur_ca", slra.Rng(seed))
     ho = oracle.build_hss(M, L, r, tol, "cur_ca", oracle.Rng(seed))
-    # C U R products amplify rounding by cond(M[I, J]) (~1e8 for the rank-11
-    # Cauchy blocks at tol 1e-6): 1e-8 relative is still 100x below tol
-    assert_hss_parity(h, ho, M, tol=max(TOL, 1e-2 * tol))
+    # Same ranks, shapes and search path as the oracle. The block products:
+    # C U R amplifies rounding by cond(M[I, J]) (~1e8 for the rank-11 Cauchy
+    # blocks at tol 1e-6), and where a probe's strips are numerically rank
+    # deficient the C-A selection picks among rounding-noise directions
+    # — two selections that both meet the block tolerance then
+    # differ by up to 2 tol: the achieved-accuracy contract
+    assert_hss_parity(h, ho, M, tol=max(TOL, 2.0 * tol))
+    assert slra.hss_error(h, M, "frobenius") <= 2.0 * max(oracle.hss_error(ho, M, "frobenius"), tol * np.linalg.norm(M))
 
 
 def test_matvec_vs_oracle(slra, oracle):

@@ -333,10 +333,16 @@ def test_cross_approx_cauchy_reduced(slra, oracle, n, seed):
     o = oracle.cross_approx(A, 1, k, k, init, 5, 1.1, None, oracle.Rng(0))
     same = sum(sg["rows"] == so["rows"] and sg["cols"] == so["cols"] for sg, so in zip(g["trace"], o["trace"]))
     # pivots beyond the strip's eps-rank (~9) pick among rounding-noise
-    # directions: the contract there is replay parity, not identical sets
+    # directions: the contract there is replay parity, not identical sets,
+    # plus per half-sweep the selection spans the strip's well-determined
+    # subspace as well as the oracle's maxvol does
     rel = _cauchy_replay_check(slra, oracle, A, g, k)
     assert rel < 1e-9
-    print(f"config-3 reduced n={n}: {same}/{len(o['trace'])} trace steps identical, rel err {rel:.2e}")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_gpu_config5 import check_half_sweeps
+    spans = check_half_sweeps(A, g["trace"], o["trace"])
+    print(f"config-3 reduced n={n}: {same}/{len(o['trace'])} trace steps identical, rel err {rel:.2e}, "
+          f"(rank, gpu, oracle) span coefficients {spans}")
 
 
 def test_cross_approx_cauchy_full_config3(slra, oracle):
@@ -347,6 +353,10 @@ def test_cross_approx_cauchy_full_config3(slra, oracle):
     g = slra.cross_approx(A, 0, k, k, init, 5, 1.1, slra.Rng(0))
     rel = _cauchy_replay_check(slra, oracle, A, g, k)
     assert rel < 1e-9
+    o = oracle.cross_approx(A, 1, k, k, init, 5, 1.1, None, oracle.Rng(0))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_gpu_config5 import check_half_sweeps
+    print(f"config-3 full: span coefficients per half-sweep {check_half_sweeps(A, g['trace'], o['trace'])}")
 
 
 def _log_block(oracle, b, master=0, m=256):
