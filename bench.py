@@ -401,7 +401,7 @@ def main():
     e2e = None
     if hasattr(work, "e2e"):
         e2e_steps = args.e2e_steps if args.config == 5 else args.steps
-        if ws == 1 or scaling == "weak" or args.config == 5:
+        if e2e_steps > 0 and (ws == 1 or scaling == "weak" or args.config == 5):
             barrier()
             e2e = work.e2e(e2e_steps, args.warmup)
             if e2e is not None and ws > 1 and scaling == "strong":
