@@ -46,6 +46,12 @@ __device__ __forceinline__ double fast_rcp(double x) {
   e = fma(-x, y, 1.0);
   return fma(y, e, y);
 }
+__device__ __forceinline__ double fast_rsqrt(double x) {  // x > 0, normal
+  double y = mufu_rsqrt(x);
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
 __device__ __forceinline__ double fast_sqrt(double x) {
   double y = mufu_rsqrt(x);
   const double hx = 0.5 * x;

@@ -134,6 +134,9 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
     nd = sqrt((a0 + a1) + (a2 + a3));
     nu = nd;
   }
+  // reciprocals of the two norms, kept in step with them (the downdate then
+  // needs one rsqrt on its chain instead of two divisions and a sqrt)
+  double rnu = nu > 0.0 ? 1.0 / nu : 0.0, rnd = rnu;
   int pos = tid;  // position of this row (= column of Q^T) in Eigen's permuted order
   int buf = 0;
   for (int k = 0; k < r; ++k) {
@@ -183,25 +186,19 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
     // ---- apply H_k to every row (non-pivot rows: the factorisation; pivot
     // rows: the solve's Q_g^T applied to that right-hand side)
     const double t = s.tau[0];
-    double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+    double w[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // eight chains: 4 deep for RMAX = 32
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
       if (8 * c + 7 >= k) {
-        const double2 v01 = *reinterpret_cast<const double2*>(s.v + 8 * c);
-        const double2 v23 = *reinterpret_cast<const double2*>(s.v + 8 * c + 2);
-        const double2 v45 = *reinterpret_cast<const double2*>(s.v + 8 * c + 4);
-        const double2 v67 = *reinterpret_cast<const double2*>(s.v + 8 * c + 6);
-        w0 = fma(v01.x, x[8 * c], w0);
-        w1 = fma(v01.y, x[8 * c + 1], w1);
-        w2 = fma(v23.x, x[8 * c + 2], w2);
-        w3 = fma(v23.y, x[8 * c + 3], w3);
-        w0 = fma(v45.x, x[8 * c + 4], w0);
-        w1 = fma(v45.y, x[8 * c + 5], w1);
-        w2 = fma(v67.x, x[8 * c + 6], w2);
-        w3 = fma(v67.y, x[8 * c + 7], w3);
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const double2 vv = *reinterpret_cast<const double2*>(s.v + 8 * c + u);
+          w[u] = fma(vv.x, x[8 * c + u], w[u]);
+          w[u + 1] = fma(vv.y, x[8 * c + u + 1], w[u + 1]);
+        }
       }
     }
-    const double tw = t * ((w0 + w1) + (w2 + w3));
+    const double tw = t * (((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7])));
     double xk = 0.0, rest = 0.0;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
@@ -216,19 +213,21 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
     }
     // ---- xGEQP3 norm downdate of the remaining candidates
     if (own && pos > k && nu != 0.0) {
-      const double rnu = fast_rcp(nu);
       double temp = fabs(xk) * rnu;
       temp = (1.0 + temp) * (1.0 - temp);
       temp = temp < 0.0 ? 0.0 : temp;
-      const double ratio = nu * fast_rcp(nd);
+      const double ratio = nu * rnd;
       if (temp * ratio * ratio <= sqrt_eps) {
 #pragma unroll
         for (int j = 0; j < RMAX; ++j)
           if (j > k && j < r) rest = fma(x[j], x[j], rest);
         nd = fast_sqrt(rest);
         nu = nd;
-      } else {
-        nu = nu * fast_sqrt(temp);
+        rnd = rnu = nd > 0.0 ? fast_rcp(nd) : 0.0;
+      } else {  // temp > sqrt_eps / ratio^2 > 0 here
+        const double y = fast_rsqrt(temp);
+        nu = nu * (temp * y);
+        rnu = rnu * y;
       }
     }
   }

@@ -9,7 +9,7 @@ set -u
 CFG=${1:-2}
 TAG=${2:-r01}
 source tools/my_kernels.sh
-BENCH="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline"
+BENCH="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0"
 $BENCH > gpurun_out/${TAG}_c${CFG}_bench.log 2>&1 || { echo "bench failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base function -k "$MYK" -c 400 --csv \
   --log-file gpurun_out/${TAG}_c${CFG}_launches.csv $BENCH > gpurun_out/${TAG}_c${CFG}_ncu_launch.log 2>&1

@@ -82,8 +82,11 @@ for rep in sorted(glob.glob(os.path.join(OUT, f"{TAG}_c{CFG}_full_*.ncu-rep"))):
         v = d.get(key, "0").replace(",", "")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.get(key, "byte"), 1)
         return float(v) * scale
+    dur = float(d.get("gpu__time_duration.sum", "0").replace(",", ""))
+    dur_ms = dur * {"ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3}.get(
+        u.get("gpu__time_duration.sum", "ms"), 1.0)
     traffic[name] = {"dram_bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
-                     "duration_us": float(d.get("gpu__time_duration.sum", "0"))}
+                     "duration_ms": dur_ms, "grid": d.get("launch__grid_size", "")}
 with open(os.path.join(PROF, f"{TAG}_c{CFG}_ncu_full.md"), "w") as f:
     f.writelines(lines)
 with open(os.path.join(PROF, f"{TAG}_c{CFG}_traffic.json"), "w") as f:
