@@ -522,12 +522,16 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
   const double* A = P.A + (int64_t)b * P.stride;
   int status = SLRA_OK;
   if (P.mode == 0) {
-    if (P.pairs) {
+#ifndef SLRA_C5_L2
+#define SLRA_C5_L2 2
+#endif
+    if (P.pairs && SLRA_C5_L2 > 0) {
       // the block is read by every half-sweep's strip gather and by the fused
       // residual: pull it into L2 once, in full lines, before the first gather
       for (int j = tid; j < P.n * ((P.m + 15) / 16); j += kCT) {
         const int c = j / ((P.m + 15) / 16), i = 16 * (j % ((P.m + 15) / 16));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(A + i + (int64_t)c * P.lda));
+        if (SLRA_C5_L2 == 2) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(A + i + (int64_t)c * P.lda));
+        else asm volatile("prefetch.global.L2 [%0];" ::"l"(A + i + (int64_t)c * P.lda));
       }
     }
     for (int t = tid; t < P.k; t += kCT) s.Icur[t] = (int)P.init_rows[(int64_t)b * P.k + t];
@@ -594,6 +598,14 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
   if (P.pairs) {
     __syncthreads();
     SLRA_PROF(11);
+    if (SLRA_C5_L2 == 2) {
+      // the block's last pass follows: its lines go back to normal priority
+      // as they are consumed (the next blocks' prefetches may evict them)
+      for (int j = tid; j < P.n * ((P.m + 15) / 16); j += kCT) {
+        const int c = j / ((P.m + 15) / 16), i = 16 * (j % ((P.m + 15) / 16));
+        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(A + i + (int64_t)c * P.lda));
+      }
+    }
     if (r <= 16) fused_block_residual<kCT, 4, 4>(A, P.lda, P.m, P.n, s.Icur, P.k, s.Jcur, P.l, s.Tm, s.Sm, r, s.S,
                                                  s.rv, P.pairs + 2 * (int64_t)b);
     else fused_block_residual<kCT, 8, 2>(A, P.lda, P.m, P.n, s.Icur, P.k, s.Jcur, P.l, s.Tm, s.Sm, r, s.S, s.rv,

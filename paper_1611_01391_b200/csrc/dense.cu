@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kDT) colsign_kernel(double* __restrict__ S, in
 int launch_colsign_batched(Context* cx, double* S, int64_t lds, int64_t sS, int64_t m, double* T, int64_t ldt,
                            int64_t sT, int64_t n, int64_t cols, int nb) {
   if (cols <= 0) return SLRA_OK;
-  SLRA_TIMED(cx, "svd", colsign_kernel<<<dim3((unsigned)cols, nb), kDT, 0, cx->stream>>>(S, lds, sS, m, T, ldt, sT,
+  SLRA_TIMED(cx, "colsign", colsign_kernel<<<dim3((unsigned)cols, nb), kDT, 0, cx->stream>>>(S, lds, sS, m, T, ldt, sT,
                                                                                         n);)
   SLRA_CHECK_LAUNCH(cx);
   return SLRA_OK;
