@@ -689,7 +689,11 @@ static bool ca_fits(int m, int n, int k, int l) {
 }
 
 int launch_ca_block(Context* c, const CaParams& p, int nprob) {
+#ifdef SLRA_ONE_CTA_PER_SM  // profiling experiment: occupancy one block per SM
+  const size_t smem = 160 * 1024;
+#else
   const size_t smem = ca_smem_bytes(p.m, p.n, p.k, p.l);
+#endif
   if (p.k <= 32 && p.l <= 32) {
     SLRA_CUDA(cudaFuncSetAttribute(ca_block_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SLRA_TIMED(c, "cross_approx", ca_block_kernel<32><<<nprob, kCT, smem, c->stream>>>(p);)

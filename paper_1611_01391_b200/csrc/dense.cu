@@ -10,13 +10,38 @@
 //   * svd (linalg.cpp:81-98): one-sided Jacobi (on A^T for square inputs,
 //     which converges in far fewer sweeps on the graded triangles the QR
 //     pre-reduction produces), QR pre-reduction for tall inputs.
-#include "dense_cta.cuh"
+#include "blocked_qr.cuh"
 
 namespace slra_dev {
 
 constexpr int kDT = 512;
 constexpr int kLeaf = 256;  // TSQR leaf rows
 constexpr int kSVT = 256;   // threads of the one-CTA SVD (8-lane group per Jacobi pair)
+
+// cta_thin_qr with the panel-blocked factorisation (blocked_qr.cuh, m <= 256,
+// c <= 64): same reflectors, the trailing updates on DMMA, one barrier per
+// column. ws: qr_ws_doubles<NT>() doubles of shared memory.
+template <int NT>
+__device__ void cta_thin_qr_blk(double* A, int lda, int m, int c, double* Q, int ldq, double* R, int ldr, double* tau,
+                                double* red, double* ws) {
+  cta_blocked_house_qr<NT>(A, lda, m, c, tau, ws);
+  __syncthreads();
+  cta_form_q<NT>(A, lda, m, c, tau, Q, ldq);
+  for (int e = threadIdx.x; e < c * c; e += NT) {
+    const int i = e % c, j = e / c;
+    const double rii = A[i + i * lda];
+    double v = (i <= j) ? A[i + j * lda] : 0.0;
+    if (rii < 0.0) v = -v;  // flip row i of R
+    R[i + j * ldr] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * c; e += NT) {
+    const int i = e % m, j = e / m;
+    if (A[j + j * lda] < 0.0) Q[i + (int64_t)j * ldq] = -Q[i + (int64_t)j * ldq];  // and column i of Q
+  }
+  __syncthreads();
+}
+constexpr int kQWS = qr_ws_doubles<kDT>();
 
 // ---------------------------------------------------------------- single-CTA thin QR
 __global__ void __launch_bounds__(kDT) thin_qr_cta_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
@@ -28,13 +53,15 @@ __global__ void __launch_bounds__(kDT) thin_qr_cta_kernel(const double* __restri
   double* Rs = S + (size_t)m * c;  // c x c
   double* tau = Rs + c * c;        // c
   double* red = tau + c;           // >= c + 8
+  double* ws = red + c + 8;        // blocked-QR scratch (m <= 256, c <= 64)
   const int64_t b = blockIdx.x;
   A += b * sA;
   Q += b * sQ;
   for (int j = 0; j < c; ++j)
     for (int i = threadIdx.x; i < m; i += kDT) S[i + j * m] = A[i + (int64_t)j * lda];
   __syncthreads();
-  cta_thin_qr<kDT>(S, m, m, c, Q, (int)ldq, Rs, c, tau, red);
+  if (m <= 256 && c <= 64) cta_thin_qr_blk<kDT>(S, m, m, c, Q, (int)ldq, Rs, c, tau, red, ws);
+  else cta_thin_qr<kDT>(S, m, m, c, Q, (int)ldq, Rs, c, tau, red);
   if (R)
     for (int j = 0; j < c; ++j)
       for (int i = threadIdx.x; i < c; i += kDT) R[b * sR + i + (int64_t)j * ldr] = Rs[i + j * c];
@@ -51,7 +78,8 @@ __global__ void __launch_bounds__(kDT) tsqr_reduce_kernel(const double* __restri
   extern __shared__ __align__(16) double sm[];
   double* S = sm;
   double* tau = S + (size_t)Lp * c;
-  double* red = tau + c;
+  double* red = tau + c;          // >= c + 8 (cta_house_qr)
+  double* ws = red + c + 8;       // blocked-QR scratch (Lp <= 256)
   const int64_t b = blockIdx.x, pb = blockIdx.y;
   X += pb * sX;
   Xn += pb * sXn;
@@ -60,7 +88,9 @@ __global__ void __launch_bounds__(kDT) tsqr_reduce_kernel(const double* __restri
   for (int j = 0; j < c; ++j)
     for (int i = threadIdx.x; i < Lp; i += kDT) S[i + j * Lp] = i < nr ? X[(r0 + i) + (int64_t)j * ldx] : 0.0;
   __syncthreads();
-  cta_house_qr<kDT>(S, Lp, Lp, c, tau, red);
+  if (Lp <= 256) cta_blocked_house_qr<kDT>(S, Lp, Lp, c, tau, ws);
+  else cta_house_qr<kDT>(S, Lp, Lp, c, tau, red);
+  __syncthreads();
   const int64_t nblk = gridDim.x;
   double* V = Vst + pb * sV + b * (int64_t)Lp * c;
   double* T = taust + pb * (nblk * c) + b * c;
@@ -80,12 +110,14 @@ __global__ void __launch_bounds__(kDT) tsqr_top_kernel(const double* __restrict_
   double* Rs = S + (size_t)Lp * c;  // c x c
   double* tau = Rs + c * c;
   double* red = tau + c;
+  double* ws = red + c + 8;
   const int64_t pb = blockIdx.x;
   X += pb * sX;
   for (int j = 0; j < c; ++j)
     for (int i = threadIdx.x; i < rows; i += kDT) S[i + j * rows] = X[i + (int64_t)j * ldx];
   __syncthreads();
-  cta_thin_qr<kDT>(S, rows, rows, c, Qt + pb * sQt, (int)ldqt, Rs, c, tau, red);
+  if (rows <= 256) cta_thin_qr_blk<kDT>(S, rows, rows, c, Qt + pb * sQt, (int)ldqt, Rs, c, tau, red, ws);
+  else cta_thin_qr<kDT>(S, rows, rows, c, Qt + pb * sQt, (int)ldqt, Rs, c, tau, red);
   if (R)
     for (int j = 0; j < c; ++j)
       for (int i = threadIdx.x; i < c; i += kDT) R[pb * sR + i + (int64_t)j * ldr] = Rs[i + j * c];
@@ -165,11 +197,13 @@ __global__ void __launch_bounds__(kDT) tsqr_expand_kernel(const double* __restri
   }
 }
 
-static size_t qr_cta_smem(int m, int c) { return sizeof(double) * ((size_t)m * c + (size_t)c * c + c + 112); }
+static size_t qr_cta_smem(int m, int c) {
+  return sizeof(double) * ((size_t)m * c + (size_t)c * c + c + 112 + (m <= 256 && c <= 64 ? kQWS : 0));
+}
 
 // Workspace doubles needed by launch_thin_qr_batched for one problem.
 size_t tsqr_workspace_doubles(int64_t m, int c) {
-  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 256) return 0;
+  if (qr_cta_smem((int)m, c) <= 227 * 1024 && m <= 256) return 0;
   const int Lp = kLeaf > c ? kLeaf : c;
   size_t total = 0;
   int64_t rows = m, first_upper = -1;
@@ -187,7 +221,7 @@ size_t tsqr_workspace_doubles(int64_t m, int c) {
 // be null -> context workspace) holds nb * tsqr_workspace_doubles(m, c).
 int launch_thin_qr_batched(Context* cx, const double* A, int64_t lda, int64_t sA, int64_t m, int c, double* Q,
                            int64_t ldq, int64_t sQ, double* R, int64_t ldr, int64_t sR, int nb, double* ws) {
-  if (qr_cta_smem((int)m, c) <= 200 * 1024 && m <= 256) {
+  if (qr_cta_smem((int)m, c) <= 227 * 1024 && m <= 256) {
     const size_t smem = qr_cta_smem((int)m, c);
     SLRA_CUDA(cudaFuncSetAttribute(thin_qr_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SLRA_TIMED(cx, "thin_qr", thin_qr_cta_kernel<<<nb, kDT, smem, cx->stream>>>(A, lda, sA, (int)m, c, Q, ldq, sQ, R,
@@ -225,7 +259,7 @@ int launch_thin_qr_batched(Context* cx, const double* A, int64_t lda, int64_t sA
   const int64_t qup = level_rows.size() > 1 ? level_rows[1] : top_rows;
   double* qbuf[2] = {cur, cur + (size_t)qup * c * nb};
   double* Qtop = cur + 2 * (size_t)qup * c * nb;
-  const size_t sm_red = sizeof(double) * ((size_t)Lp * c + c + 112);
+  const size_t sm_red = sizeof(double) * ((size_t)Lp * c + 2 * (size_t)c + 8 + (Lp <= 256 ? kQWS : 0) + 8);
   SLRA_CUDA(cudaFuncSetAttribute(tsqr_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_red));
   const double* Xc = A;
   int64_t ldx = lda, sX = sA;
@@ -240,7 +274,7 @@ int launch_thin_qr_batched(Context* cx, const double* A, int64_t lda, int64_t sA
     ldx = nblk * c;
     sX = sXl[lv];
   }
-  const size_t sm_top = sizeof(double) * ((size_t)Lp * c + (size_t)c * c + c + 112);
+  const size_t sm_top = sizeof(double) * ((size_t)Lp * c + (size_t)c * c + c + 112 + kQWS);
   SLRA_CUDA(cudaFuncSetAttribute(tsqr_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_top));
   SLRA_TIMED(cx, "thin_qr",
              tsqr_top_kernel<<<nb, kDT, sm_top, cx->stream>>>(Xc, ldx, sX, (int)top_rows, c, Lp, Qtop, top_rows,

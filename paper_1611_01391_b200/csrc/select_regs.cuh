@@ -204,10 +204,13 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
     for (int c = 0; c < NCH; ++c) {
       if (8 * c + 7 >= k) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 8; u += 2) {
           const int j = 8 * c + u;
-          x[j] = fma(-tw, s.v[j], x[j]);
+          const double2 vv = *reinterpret_cast<const double2*>(s.v + j);
+          x[j] = fma(-tw, vv.x, x[j]);
+          x[j + 1] = fma(-tw, vv.y, x[j + 1]);
           if (j == k) xk = x[j];
+          if (j + 1 == k) xk = x[j + 1];
         }
       }
     }
