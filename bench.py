@@ -490,7 +490,7 @@ class Config2:
             rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                   "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                   "algorithmic_bytes_per_launch": byts,
-                  "traffic": profiled_traffic(2, {"svd": "svd_cta_kernel"}.get(top)),
+                  "traffic": profiled_traffic(2, {"svd": "svd_cta_kernel"}.get(top), tag="r02"),
                   "note": "latency-bound: one CTA per sketch runs a serial chain (Jacobi rounds, FP64 FMA "
                           "latency ~24 cycles); see kernels_ms_per_step and profiles/"}
         # the HBM/FP64-tensor kernels on their own rooflines, always reported
@@ -499,13 +499,13 @@ class Config2:
             ach = flops / (per_launch_ms["residual"] * 1e-3) / 1e12
             rl["residual_kernel"] = {"achieved_tflops": ach, "frac_fp64": ach / peaks["fp64_tflops"],
                                      "achieved_gbs": 8.0 * m * n / (per_launch_ms["residual"] * 1e-3) / 1e9,
-                                     "traffic": profiled_traffic(2, "residual_stream_kernel")}
+                                     "traffic": profiled_traffic(2, "residual_stream_kernel", tag="r02")}
         if "gemm_v" in fam:
             flops = 2.0 * m * n * RANK
             ach = flops / (per_launch_ms["gemm_v"] * 1e-3) / 1e12
             rl["gemm_v_kernel"] = {"achieved_tflops": ach, "frac_fp64": ach / peaks["fp64_tflops"],
                                    "achieved_gbs": 8.0 * m * n / (per_launch_ms["gemm_v"] * 1e-3) / 1e9,
-                                   "traffic": profiled_traffic(2, "tn_skinny_kernel")}
+                                   "traffic": profiled_traffic(2, "tn_skinny_kernel", tag="r02")}
         return rl, kernels
 
     def e2e(self, steps, warmup):
@@ -582,8 +582,16 @@ class Config1:
     def roofline(self, fam, peaks, steps):
         kernels = {k: v[0] / steps for k, v in fam.items()}
         top = max(fam.items(), key=lambda kv: kv[1][0])[0]
-        return {"kernel": top, "bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
-                "traffic": None, "note": "config 1 is launch/latency bound (SURVEY 8d)"}, kernels
+        per = fam[top][0] / max(fam[top][1], 1)
+        # 2*256*16*16 + 2*256*16*256 + 3*256^2 ~ 2.42 MFLOP, ~11 B per entry
+        flops = 2.0 * 256 * 16 * 16 + 2.0 * 256 * 16 * 256 + 3.0 * 256 * 256
+        ach = flops / (per * 1e-3) / 1e12
+        return {"kernel": top, "bound": "tensor", "achieved": ach, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                "frac": ach / peaks["fp64_tflops"] if peaks["fp64_tflops"] else None,
+                "peak_source": peaks["fp64_source"], "algorithmic_per_launch": {"flops": flops},
+                "traffic": profiled_traffic(1, "ca_block_kernel", tag="r02"),
+                "note": "config 1 is one 256x256 problem: one CTA's dependent chain (launch/latency bound, "
+                        "SURVEY 8d); the FP64 fraction is reported for completeness"}, kernels
 
     def e2e(self, steps, warmup):
         s = self.slra
@@ -678,7 +686,9 @@ class Config3:
         ach = b / (per[top] * 1e-3) / 1e9
         rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
               "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-              "algorithmic_bytes_per_launch": b, "traffic": None}
+              "algorithmic_bytes_per_launch": b,
+              "traffic": profiled_traffic(3, {"thin_qr": "tsqr_top_kernel", "maxvol": "maxvol_large_kernel",
+                                              "residual": "residual_stream_kernel"}.get(top), tag="r02")}
         if "residual" in per:
             rb = 8.0 * n * n + 16.0 * n * r
             rl["residual_kernel"] = {"achieved_gbs": rb / (per["residual"] * 1e-3) / 1e9,
@@ -874,8 +884,7 @@ class Config4:
         ach = b / (per[top] * 1e-3) / 1e9
         rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
               "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-              "algorithmic_bytes_per_launch": b, "traffic": profiled_traffic(4, {"lsr_residual": "lsr_residual_kernel",
-                                                                                "lsr_solve": "cholesky_kernel"}.get(top))}
+              "algorithmic_bytes_per_launch": b, "traffic": profiled_traffic(4, {"lsr_residual": "lsr_residual_kernel", "lsr_solve": "cholesky_kernel"}.get(top), tag="r02")}
         if top == "lsr_solve":
             rl["note"] = ("latency-bound: the 256 x 256 Cholesky and the triangular solves run on one CTA "
                           "(FP64 dependent chains); per-launch mean over the family's kernels")
@@ -883,7 +892,7 @@ class Config4:
             rb = 8.0 * self.mloc * (D4 + 1)
             rl["lsr_residual_kernel"] = {"achieved_gbs": rb / (per["lsr_residual"] * 1e-3) / 1e9,
                                          "frac_hbm": rb / (per["lsr_residual"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
-                                         "traffic": profiled_traffic(4, "lsr_residual_kernel")}
+                                         "traffic": profiled_traffic(4, "lsr_residual_kernel", tag="r02")}
         return rl, kernels
 
     def e2e(self, steps, warmup):
