@@ -210,3 +210,100 @@ def test_half_sweep_selection_quality(slra, bench, oracle, b):
     g = slra.cross_approx(Kb, 0, K, K, list(init[0]), LOOPS, 1.1, slra.Rng(0))
     o = oracle.cross_approx(Kb, 1, K, K, list(init[0]), LOOPS, 1.1, None, oracle.Rng(0))
     print(f"block {b}: (rank, gpu, oracle) span coefficients per half-sweep {check_half_sweeps(Kb, g['trace'], o['trace'])}")
+
+
+# ---------------------------------------------------------------- edge cases of the batched entries
+def _oracle_block(oracle, Kb, init, k, l, loops):
+    o = oracle.cross_approx(Kb, 1, k, l, list(init), loops, 1.1, None, oracle.Rng(0))
+    G = Kb[np.ix_(o["I"], o["J"])]
+    rk = oracle.numerical_rank(G, 1e-10, True)
+    return o, rk
+
+
+def _batched(slra, torch, A, m, n, k, l, init, loops=2):
+    nb = A.shape[0]
+    out = dict(I=torch.zeros((nb, k), dtype=torch.int64, device="cuda"),
+               J=torch.zeros((nb, l), dtype=torch.int64, device="cuda"),
+               U=torch.zeros((nb, k * l), dtype=torch.float64, device="cuda"),
+               r=torch.zeros(nb, dtype=torch.int64, device="cuda"),
+               st=torch.zeros(nb, dtype=torch.int32, device="cuda"),
+               rs=torch.zeros(nb, dtype=torch.float64, device="cuda"),
+               ns=torch.zeros(nb, dtype=torch.float64, device="cuda"))
+    slra.cross_approx_batched_device(A.data_ptr(), m, m * n, nb, m, n, 0, k, l, init.data_ptr(), loops, 1.1,
+                                     out["I"].data_ptr(), out["J"].data_ptr(), out["U"].data_ptr(),
+                                     out["r"].data_ptr(), out["st"].data_ptr(), out["rs"].data_ptr(),
+                                     out["ns"].data_ptr())
+    torch.cuda.synchronize()
+    return {kk: v.cpu().numpy() for kk, v in out.items()}
+
+
+@pytest.mark.parametrize("m,n,k,l", [(200, 150, 12, 12), (97, 131, 7, 7), (256, 256, 48, 48), (64, 256, 16, 24)])
+def test_batched_ragged_and_wide_shapes(slra, oracle, m, n, k, l):
+    """Shapes off the fused path (m, n not multiples of 8; k, l > 32 -> the
+    64-column kernel and the separate residual pass; k != l -> the padding
+    branch): well-posed Gaussian blocks, I and J bit-exact vs the oracle in
+    every block, residuals within 1e-10 ||B||_F."""
+    import torch
+    rng = np.random.default_rng(m + n + k + l)
+    nb = 6
+    blocks = rng.standard_normal((nb, n, m))  # (b, j, i): column-major m x n blocks
+    init = np.stack([rng.permutation(m)[:k] for _ in range(nb)]).astype(np.int64)
+    g = _batched(slra, torch, torch.from_numpy(blocks).cuda(), m, n, k, l, torch.from_numpy(init).cuda())
+    for b in range(nb):
+        Kb = np.asfortranarray(blocks[b].T)
+        o, rk = _oracle_block(oracle, Kb, init[b], k, l, 2)
+        assert g["st"][b] == 0
+        assert g["I"][b].tolist() == o["I"] and g["J"][b].tolist() == o["J"], b
+        assert g["r"][b] == rk
+        c = oracle.primitive_cur(Kb, o["I"], o["J"], rk)
+        eo = oracle.cur_evaluate(Kb, o["I"], o["J"], c["nucleus"])
+        nK = np.linalg.norm(Kb)
+        assert abs(np.sqrt(g["rs"][b]) - eo) <= 1e-10 * nK
+        assert abs(np.sqrt(g["ns"][b]) - nK) <= 1e-13 * nK
+
+
+def test_batched_empty_zero_and_failing_blocks(slra, oracle):
+    """nblocks = 0 is a no-op; an all-zero block reports its failure per block
+    (GeneratorRankFailure, as the reference throws for it) with resid_sq =
+    norm_sq = 0 and r = 0; a rank-1 block gets the adaptive rank 1 and an
+    exact CUR; neither disturbs the good block beside them."""
+    import torch
+    m, k = 64, 8
+    nb = 3
+    rng = np.random.default_rng(3)
+    blocks = np.zeros((nb, m, m))
+    blocks[1] = rng.standard_normal((m, m))
+    u, v = rng.standard_normal(m), rng.standard_normal(m)
+    blocks[2] = np.outer(v, u)  # rank 1 (column-major storage of u v^T)
+    init = np.stack([rng.permutation(m)[:k] for _ in range(nb)]).astype(np.int64)
+    A = torch.from_numpy(blocks).cuda()
+    it = torch.from_numpy(init).cuda()
+    g0 = _batched(slra, torch, A[:0], m, m, k, k, it[:0])
+    assert all(v.size == 0 for v in g0.values())
+    g = _batched(slra, torch, A, m, m, k, k, it)
+    assert g["st"][0] == 5 and g["st"][1] == 0 and g["st"][2] == 0  # SLRA_ERR_GENERATOR_RANK_FAILURE
+    assert g["rs"][0] == g["ns"][0] == 0.0 and g["r"][0] == 0
+    with pytest.raises(oracle.GeneratorRankFailure):
+        oracle.cross_approx(np.asfortranarray(blocks[0].T), 1, k, k, list(init[0]), 2, 1.1, None, oracle.Rng(0))
+    K2 = np.asfortranarray(blocks[2].T)
+    assert g["r"][2] == 1 and np.sqrt(g["rs"][2]) <= 1e-13 * np.linalg.norm(K2)
+    Kb = np.asfortranarray(blocks[1].T)
+    o, rk = _oracle_block(oracle, Kb, init[1], k, k, 2)
+    assert g["I"][1].tolist() == o["I"] and g["J"][1].tolist() == o["J"]
+
+
+def test_batched_host_entry_chunks_and_pageable(slra, bench):
+    """The host-streamed entry on a batch that is not a multiple of its chunk,
+    from pageable (not page-locked) numpy memory: identical results to the
+    device-resident batched call."""
+    import torch
+    nb = 37
+    A, init, _ = _bench_blocks(slra, bench, torch, 100, nb)
+    g = _run_batched(slra, torch, A, torch.from_numpy(init).cuda())
+    host = np.ascontiguousarray(A.cpu().numpy())
+    out = dict(I=np.zeros((nb, K), np.int64), J=np.zeros((nb, K), np.int64), U=np.zeros((nb, K * K)),
+               r=np.zeros(nb, np.int64), st=np.zeros(nb, np.int32), rs=np.zeros(nb), ns=np.zeros(nb))
+    slra.cross_approx_batched_host(host.ctypes.data, M, M * M, nb, M, M, 0, K, K, init.ctypes.data, LOOPS, 1.1,
+                                   *[out[k].ctypes.data for k in ("I", "J", "U", "r", "st", "rs", "ns")])
+    for key in ("I", "J", "U", "r", "st", "rs", "ns"):
+        assert np.array_equal(out[key], g[key]), key
