@@ -16,7 +16,7 @@ NAMES = ["init+prefetch", "stage strip", "house_qr", "form_q", "sel argmax", "se
          "sel backsolve", "sel swaps", "nucleus load", "nucleus jacobi", "nucleus finish", "resid P/Q",
          "resid DMMA"]
 nb = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
-lib = ctypes.CDLL(os.path.join(ROOT, "tools", "prof_build", "lib", "libslra_cuda.so"))
+lib = ctypes.CDLL(os.environ.get("SLRA_PROF_LIB", os.path.join(ROOT, "tools", "prof_build", "lib", "libslra_cuda.so")))
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 slra.set_device(0, stream.cuda_stream)
