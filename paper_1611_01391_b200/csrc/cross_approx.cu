@@ -62,7 +62,8 @@ __host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
   // S (mm c + c), W / Gt / V ((c+1) c each), tau / sigma / sgn (c), v (64),
   // nu / nd / rn (mm each), rv 40, volv 8 + slack 2c
   const int cw = c > 32 ? c : 32;  // W / Gt / V: also the selection's RMAX x r R (RMAX <= 32)
-  const size_t ns = ca_max((size_t)mm * ((c + 3) & ~3) + c, 3 * (size_t)c * c);  // + the nucleus' 3 c x c
+  const size_t nn = c <= 32 ? 5 * (size_t)c * c + c : (size_t)c * c;  // the nucleus' c x c buffers
+  const size_t ns = ca_max((size_t)mm * ((c + 3) & ~3) + c, nn);
   size_t d = ca_even(ns) + 3 * ca_even((size_t)(cw + 1) * cw) + 3 * ca_even(c) + 64 +
              3 * ca_even(mm > 16 ? mm : 16) + 40 + 8 + ca_even(2 * (size_t)c);
   size_t i = 2 * (size_t)mm + 5 * (size_t)c + 8;
@@ -74,8 +75,8 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   CaSmem s;
   double* d = reinterpret_cast<double*>(base);
   // the strip; the fused residual's Q fragments (n x 4 ceil(r/4)); the
-  // preconditioned nucleus' U_w, J_w and right vectors (3 c x c)
-  s.S = d; d += ca_even(ca_max((size_t)mm * ((c + 3) & ~3) + c, 3 * (size_t)c * c));
+  // preconditioned nucleus' U_w, J_w, left / right vectors and rotations (5 c x c)
+  s.S = d; d += ca_even(ca_max((size_t)mm * ((c + 3) & ~3) + c, c <= 32 ? 5 * (size_t)c * c + c : (size_t)c * c));
   const int cw = c > 32 ? c : 32;
   s.W = d; d += ca_even((size_t)(cw + 1) * cw);  // the nucleus' Jacobi operand (ld p | 1, p <= c)
   s.R = nullptr;
@@ -264,8 +265,16 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
     }
     __syncthreads();
     const int nr = s.flag[4];
-    // Jacobi on X = R(0:nr, :)^T (the first nr columns of Gt), rotations into W
-    cta_jacobi<NT, CMAX>(s.Gt, ld, n, nr, s.W, ld, s.flag, 1e-10 / sqrt((double)nr));
+    // QLP: the second, unpivoted QR R_top^T = Q1 R1 (one warp; V1 over Gt,
+    // tau1 in rv), then the Jacobi on W = R1^T (nr x nr): on the twice
+    // QR-reduced factor the sweeps settle in ~4 instead of ~6.5
+    // (Drmac-Veselic), on columns of length nr instead of n.
+    double* Jrot = s.S + 3 * n * n;  // nr x nr rotations (ld ld), consumed by svd_finish
+    for (int e = tid; e < n * ld; e += NT) s.W[e] = 0.0;
+    __syncthreads();
+    if (tid < 32) warp_house_regs(s.Gt, ld, n, nr, s.W, ld, s.rv, s.v);
+    __syncthreads();
+    cta_jacobi<NT, CMAX>(s.W, ld, nr, nr, Jrot, ld, s.flag, 1e-10 / sqrt((double)nr));
     SLRA_PROF(10);
 #ifdef SLRA_PHASE_PROF
     if (tid == 0) {
@@ -273,27 +282,35 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
       atomicAdd(&g_phase_cycles[21], (unsigned long long)nr);
     }
 #endif
-    double* Uw = s.S;               // n x nr, ld n: normalised columns of the rotated R^T
-    double* Jw = s.S + n * n;       // nr x nr, ld n: the accumulated rotations
-    double* Rv = s.S + 2 * n * n;   // right vectors of G = Pi U_w
-    cta_svd_finish<NT>(s.Gt, ld, n, nr, s.W, ld, s.sigma, s.order, Uw, n, Jw, n, s.sgn);
+    // R1^T Jw = Uw Sigma  =>  G = (Q [Uw; 0]) Sigma (Pi Q1 [Jw; 0])^T
+    double* Uw = s.S;               // nr x nr, ld n
+    double* Jw = s.S + n * n;       // nr x nr, ld n
+    double* Lv = s.S + 2 * n * n;   // left vectors of G: Q [Uw; 0]  (n x nr, ld n)
+    double* Rv = s.S + 3 * n * n;   // right vectors of G: Pi Q1 [Jw; 0]
+    cta_svd_finish<NT>(s.W, ld, nr, nr, Jrot, ld, s.sigma, s.order, Uw, n, Jw, n, s.sgn);
     for (int i = nr + tid; i < n; i += NT) s.sigma[i] = 0.0;
-    // left vectors L = Q [Jw; 0] into Gt (ld n): apply H_{n-1} ... H_0
-    // (reverse), a warp per column, a lane per row
     {
       const int lane = tid & 31, warp = tid >> 5;
-      for (int j = warp; j < nr; j += NT / 32) {
-        double y = lane < nr ? Jw[lane + j * n] : 0.0;
-        for (int kk = n - 1; kk >= 0; --kk) {
-          const double v = lane < n ? s.V[lane + kk * ld] : 0.0;  // unit head, zeros above
-          const double w = warp_sum(v * y);
-          y = fma(-s.tau[kk] * w, v, y);
+      // a warp per column, a lane per row: the reflectors applied backwards
+      for (int j = warp; j < 2 * nr; j += NT / 32) {
+        const bool left = j < nr;
+        const int jj = left ? j : j - nr;
+        double y = lane < nr ? (left ? Uw : Jw)[lane + jj * n] : 0.0;
+        if (left) {
+          for (int kk = n - 1; kk >= 0; --kk) {  // Q = H_0 ... H_{n-1} (G Pi = Q R)
+            const double v = lane < n ? s.V[lane + kk * ld] : 0.0;  // unit head, zeros above
+            const double w = warp_sum(v * y);
+            y = fma(-s.tau[kk] * w, v, y);
+          }
+          if (lane < n) Lv[lane + jj * n] = y;
+        } else {
+          for (int kk = nr - 1; kk >= 0; --kk) {  // Q1 = H1_0 ... H1_{nr-1}
+            const double v = lane < n ? s.Gt[lane + kk * ld] : 0.0;
+            const double w = warp_sum(v * y);
+            y = fma(-s.rv[kk] * w, v, y);
+          }
+          if (lane < n) Rv[s.perm[lane] + jj * n] = y;  // (Jrot, under Rv, is consumed)
         }
-        if (lane < n) s.Gt[lane + j * n] = y;
-      }
-      for (int e = tid; e < n * nr; e += NT) {
-        const int i = e % n, j = e / n;
-        Rv[s.perm[i] + j * n] = Uw[i + j * n];
       }
     }
     __syncthreads();
@@ -301,17 +318,17 @@ __device__ int cta_nucleus(CaSmem& s, const double* A, int64_t lda, const int* I
     for (int t = tid >> 5; t < nr; t += NT / 32) {
       const int lane = tid & 31;
       ArgMax a{-1.0, INT64_MAX};
-      for (int i = lane; i < n; i += 32) a = argmax_merge(a, ArgMax{fabs(s.Gt[i + t * n]), i});
+      for (int i = lane; i < n; i += 32) a = argmax_merge(a, ArgMax{fabs(Lv[i + t * n]), i});
       a = warp_argmax(a);
-      const double f = (s.Gt[a.i + t * n] < 0.0) ? -1.0 : 1.0;
+      const double f = (Lv[a.i + t * n] < 0.0) ? -1.0 : 1.0;
       __syncwarp();
       for (int i = lane; i < n; i += 32) {
-        s.Gt[i + t * n] *= f;
+        Lv[i + t * n] *= f;
         Rv[i + t * n] *= f;
       }
     }
     __syncthreads();
-    Sl = s.Gt;
+    Sl = Lv;
     ldsl = n;
     Tr = Rv;
     ldtr = n;

@@ -423,4 +423,56 @@ __device__ inline void warp_colpiv_regs(const double* G, int ldg, int n, double*
   }
 }
 
+// Unpivoted Householder QR of a small X (n x nc, n <= 32, nc <= n, ld ldx,
+// smem) by ONE warp, a column per lane in registers: the second QR of the
+// QLP preconditioner (R_top^T = Q1 R1). Writes W = R1^T (nc x nc, ld ldw;
+// the caller zero-fills it), the unit-lower reflectors V1 over X itself
+// (ld ldx) and tau1 (nc). `vb` (32 doubles, 16-byte aligned) is scratch.
+__device__ inline void warp_house_regs(double* X, int ldx, int n, int nc, double* W, int ldw, double* tau1,
+                                       double* vb) {
+  const int lane = threadIdx.x & 31;
+  const bool own = lane < nc;
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (own && i < n) ? X[i + lane * ldx] : 0.0;
+  __syncwarp();  // every column read before the reflectors overwrite X
+  for (int k = 0; k < nc; ++k) {
+    if (lane == k) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) *reinterpret_cast<double2*>(vb + i) = make_double2(x[i], x[i + 1]);
+    }
+    __syncwarp();
+    const double xl = vb[lane];
+    const double c0 = vb[k];
+    const double tail = warp_sum(lane > k && lane < n ? xl * xl : 0.0);
+    const bool zero = tail <= DBL_MIN;
+    double beta = fast_sqrt(fma(c0, c0, tail));
+    beta = c0 >= 0.0 ? -beta : beta;
+    beta = zero ? c0 : beta;
+    const double rden = zero ? 0.0 : fast_rcp(c0 - beta);
+    const double t = zero ? 0.0 : (beta - c0) * fast_rcp(beta);
+    const double vl = lane < k ? 0.0 : (lane == k ? 1.0 : (lane < n ? xl * rden : 0.0));
+    if (lane < n) X[lane + k * ldx] = vl;
+    if (lane <= k) W[k + lane * ldw] = lane < k ? xl : beta;  // R1(lane, k) = W(k, lane)
+    if (lane == 0) tau1[k] = t;
+    __syncwarp();
+    vb[lane] = vl;
+    __syncwarp();
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const double2 va = *reinterpret_cast<const double2*>(vb + i);
+      const double2 vc = *reinterpret_cast<const double2*>(vb + i + 2);
+      w0 = fma(va.x, x[i], w0);
+      w1 = fma(va.y, x[i + 1], w1);
+      w2 = fma(vc.x, x[i + 2], w2);
+      w3 = fma(vc.y, x[i + 3], w3);
+    }
+    const double tw = t * ((w0 + w1) + (w2 + w3));
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = fma(-tw, vb[i], x[i]);
+    __syncwarp();
+  }
+}
+
 }  // namespace slra_dev
