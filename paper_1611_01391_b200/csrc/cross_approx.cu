@@ -413,25 +413,8 @@ __device__ void fused_block_residual(const double* A, int64_t lda, int m, int n,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int RP = 4 * KS;
   const int ksn = (r + 3) >> 2;  // k-steps in use (QS holds n x 4 ksn doubles)
-  constexpr int NB = KS <= 4 ? 8 : 2;  // global loads in flight per thread (register budget)
-  // P(i, :) = A(i, J) Tm, row i = tid (zero for j >= r)
-  double p[RP];
-#pragma unroll
-  for (int j = 0; j < RP; ++j) p[j] = 0.0;
-  if (tid < m) {
-    for (int t0 = 0; t0 < l; t0 += NB) {
-      double c[NB];
-#pragma unroll
-      for (int u = 0; u < NB; ++u) c[u] = __ldg(A + tid + (int64_t)J[t0 + u < l ? t0 + u : l - 1] * lda);
-#pragma unroll
-      for (int u = 0; u < NB; ++u)
-        if (t0 + u < l) {
-#pragma unroll
-          for (int j = 0; j < RP; ++j)
-            if (j < r) p[j] = fma(c[u], Tm[t0 + u + j * l], p[j]);
-        }
-    }
-  }
+  constexpr int NB = KS <= 4 ? 16 : 8;  // global loads in flight per thread (register budget)
+  // Q first, into shared memory, then P in registers: q and p never live together
   // Q(:, col) = Sm^T A(I, col), col = tid, into the B-fragment layout
   if (tid < n) {
     double q[RP];
@@ -453,6 +436,28 @@ __device__ void fused_block_residual(const double* A, int64_t lda, int m, int n,
 #pragma unroll
     for (int j = 0; j < RP; ++j)
       if ((j >> 2) < ksn) QS[((nt * ksn) + (j >> 2)) * 32 + g * 4 + (j & 3)] = q[j];
+  }
+#ifdef SLRA_PHASE_PROF
+  __syncthreads();
+  SLRA_PROF(14);
+#endif
+  // P(i, :) = A(i, J) Tm, row i = tid (zero for j >= r)
+  double p[RP];
+#pragma unroll
+  for (int j = 0; j < RP; ++j) p[j] = 0.0;
+  if (tid < m) {
+    for (int t0 = 0; t0 < l; t0 += NB) {
+      double c[NB];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) c[u] = __ldg(A + tid + (int64_t)J[t0 + u < l ? t0 + u : l - 1] * lda);
+#pragma unroll
+      for (int u = 0; u < NB; ++u)
+        if (t0 + u < l) {
+#pragma unroll
+          for (int j = 0; j < RP; ++j)
+            if (j < r) p[j] = fma(c[u], Tm[t0 + u + j * l], p[j]);
+        }
+    }
   }
   __syncthreads();
   SLRA_PROF(12);
@@ -479,30 +484,45 @@ __device__ void fused_block_residual(const double* A, int64_t lda, int m, int n,
     }
     const int row0 = 32 * warp + 8 * pass * MTP;
     if (row0 < m) {
-      for (int nt = 0; nt < (n >> 3); ++nt) {
-        double c[MTP][2];
-        const int col = 8 * nt + 2 * q4;
+      // NTU n-tiles per iteration, all their loads issued before any use
+      // (the block may come from DRAM: one round trip per NTU tiles)
+      constexpr int NTU = 2;
+      const int ntiles = n >> 3;
+      for (int nt0 = 0; nt0 < ntiles; nt0 += NTU) {
+        double c[NTU][MTP][2];
 #pragma unroll
-        for (int u = 0; u < MTP; ++u) {
-          const int row = row0 + 8 * u + g;
-          const bool ok = row < m;
-          c[u][0] = load_sel(A, row + (int64_t)col * lda, ok);
-          c[u][1] = load_sel(A, row + (int64_t)(col + 1) * lda, ok);
-          ns = fma(c[u][0], c[u][0], ns);
-          ns = fma(c[u][1], c[u][1], ns);
-        }
+        for (int q = 0; q < NTU; ++q) {
+          const int col = 8 * (nt0 + q) + 2 * q4;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          if (ks < ksn) {
-            const double bf = QS[(nt * ksn + ks) * 32 + lane];
-#pragma unroll
-            for (int u = 0; u < MTP; ++u) dmma_8x8x4(c[u][0], c[u][1], af[u][ks], bf);
+          for (int u = 0; u < MTP; ++u) {
+            const int row = row0 + 8 * u + g;
+            const bool ok = row < m && nt0 + q < ntiles;
+            c[q][u][0] = load_sel(A, row + (int64_t)col * lda, ok);
+            c[q][u][1] = load_sel(A, row + (int64_t)(col + 1) * lda, ok);
           }
         }
 #pragma unroll
-        for (int u = 0; u < MTP; ++u) {
-          rs = fma(c[u][0], c[u][0], rs);
-          rs = fma(c[u][1], c[u][1], rs);
+        for (int q = 0; q < NTU; ++q) {
+          if (nt0 + q < ntiles) {
+#pragma unroll
+            for (int u = 0; u < MTP; ++u) {
+              ns = fma(c[q][u][0], c[q][u][0], ns);
+              ns = fma(c[q][u][1], c[q][u][1], ns);
+            }
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+              if (ks < ksn) {
+                const double bf = QS[((nt0 + q) * ksn + ks) * 32 + lane];
+#pragma unroll
+                for (int u = 0; u < MTP; ++u) dmma_8x8x4(c[q][u][0], c[q][u][1], af[u][ks], bf);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < MTP; ++u) {
+              rs = fma(c[q][u][0], c[q][u][0], rs);
+              rs = fma(c[q][u][1], c[q][u][1], rs);
+            }
+          }
         }
       }
     }

@@ -13,8 +13,8 @@ import bench  # noqa: E402
 import paper_1611_01391_b200 as slra  # noqa: E402
 
 NAMES = ["init+prefetch", "stage strip", "house_qr", "form_q", "sel argmax", "sel reflector", "sel update",
-         "sel backsolve", "sel swaps", "nucleus load", "nucleus jacobi", "nucleus finish", "resid P/Q",
-         "resid DMMA"]
+         "sel backsolve", "sel swaps", "nucleus load", "nucleus jacobi", "nucleus finish", "resid P",
+         "resid DMMA", "resid Q"]
 nb = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 lib = ctypes.CDLL(os.environ.get("SLRA_PROF_LIB", os.path.join(ROOT, "tools", "prof_build", "lib", "libslra_cuda.so")))
 stream = torch.cuda.Stream()
@@ -35,6 +35,7 @@ w.step()
 torch.cuda.synchronize()
 lib.slra_debug_phase_cycles(buf, 32, 1)
 cyc = np.array(buf[:len(NAMES)], dtype=np.float64) / nb
+
 print(f"nucleus: mean Jacobi sweeps {buf[20] / nb:.2f}, mean kept rows of R {buf[21] / nb:.2f}")
 tot = cyc.sum()
 print(f"{nb} blocks: {tot:.0f} cycles per block on the critical path")
