@@ -818,7 +818,10 @@ class Config4:
             self.plans.append((name, p, dict(src=torch.tensor(p["src"], dtype=torch.int64, device="cuda"),
                                               coef=torch.tensor(p["coef"], dtype=torch.float64, device="cuda"),
                                               q=torch.tensor(p["q"], dtype=torch.int32, device="cuda"))))
-        self.x = [torch.zeros(D4, dtype=torch.float64, device="cuda") for _ in self.plans]
+        # both samplers' solutions side by side (D4 x 2, column-major): one
+        # residual pass over A certifies both (slra_lsr_residual_multi)
+        self.X = torch.zeros(len(self.plans), D4, dtype=torch.float64, device="cuda")
+        self.x = [self.X[i] for i in range(len(self.plans))]
         self.out = torch.zeros(len(self.plans), 2, dtype=torch.float64, device="cuda")
         self.sres = [0.0] * len(self.plans)
         self.tres = [0.0] * len(self.plans)
@@ -839,8 +842,9 @@ class Config4:
                 self.sres[i] = s.sketch_solve_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(),
                                                      d["src"].data_ptr(), d["coef"].data_ptr(), d["q"].data_ptr(),
                                                      p["width"], p["tree"], K4, self.x[i].data_ptr())
-                s.lsr_residual_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(), self.x[i].data_ptr(),
-                                      self.out[i].data_ptr())
+            # residual_norm of both solutions in ONE pass over A (out[i, 0])
+            s.lsr_residual_multi_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(), self.X.data_ptr(),
+                                        len(self.plans), self.out.data_ptr())
         else:
             for i, (_, p, d) in enumerate(self.plans):
                 x, self.sres[i], self.tres[i] = self.shard.sketch_solve(
@@ -853,7 +857,7 @@ class Config4:
         bn = self.b.norm().item()
         out = {}
         for i, (name, _, _) in enumerate(self.plans):
-            tres = self.out[i, 0].item() ** 0.5 if self.comm.world == 1 else self.tres[i]
+            tres = self.out.view(-1)[i].item() ** 0.5 if self.comm.world == 1 else self.tres[i]
             out[name] = {"sketched_residual": self.sres[i], "true_residual": tres, "rel_to_b": tres / bn}
         if self.comm.world == 1:
             # residual ratio against the exact LS solution (certification, untimed)

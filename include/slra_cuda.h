@@ -385,6 +385,11 @@ int slra_lsq_exact(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int6
 /* residual_norm (lsr.cpp:26-28): ||A x - b||^2 into d_out[0] (device). */
 int slra_lsr_residual(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
                       const double* d_b, const double* d_x, double* d_out);
+/* residual_norm (lsr.cpp:26-28) for nx <= 4 candidate solutions at once
+ * (the columns of d_X, ld d): d_out[s] = ||A x_s - b||^2, A read ONCE — the
+ * two samplers of config 4 certified in one pass over the 2^20 x 256 A. */
+int slra_lsr_residual_multi(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
+                            const double* d_b, const double* d_X, int64_t nx, double* d_out);
 
 /* ------------------------------------------------------------ §8b/§8e multi-GPU
  * NCCL collectives (NVLink / NVSwitch on one box) on the context's stream

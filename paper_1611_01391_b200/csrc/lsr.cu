@@ -310,62 +310,97 @@ __global__ void __launch_bounds__(256) lsq_residual_kernel(const double* __restr
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// out[b] = sum of part[b n .. b n + n) (one CTA per sum, fixed order)
 __global__ void sum_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
   __shared__ double red[40];
   double s = 0.0;
+  part += (int64_t)blockIdx.x * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
   s = block_sum<256>(s, red);
-  if (threadIdx.x == 0) out[0] = s;
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
-// ||A x - b||^2 over a tall column-major A (m x d): each thread owns rows,
-// walks the d columns (coalesced across the warp), deterministic partials.
+// ||A x_s - b||^2 for NX solutions x_s (columns of X, ld d) over a tall
+// column-major A (m x d) in ONE pass over A: each thread owns two rows and
+// walks the d columns with 128-bit loads (coalesced across the warp);
+// deterministic per-CTA partials part[s * gridDim.x + cta].
+template <int NX>
 __global__ void __launch_bounds__(256) lsr_residual_kernel(const double* __restrict__ A, int64_t lda, int64_t m,
                                                            int d, const double* __restrict__ b,
-                                                           const double* __restrict__ x, double* __restrict__ part) {
-  extern __shared__ double xs[];
+                                                           const double* __restrict__ X, double* __restrict__ part) {
+  extern __shared__ double xs[];  // xs[j * NX + s]
   __shared__ double red[40];
-  for (int j = threadIdx.x; j < d; j += blockDim.x) xs[j] = x[j];
+  for (int e = threadIdx.x; e < d * NX; e += blockDim.x) xs[(e % d) * NX + e / d] = X[e];
   __syncthreads();
-  double s = 0.0;
+  double sq[NX];
+#pragma unroll
+  for (int s = 0; s < NX; ++s) sq[s] = 0.0;
+  const bool vec = (lda % 2 == 0) && (((uintptr_t)A) % 16 == 0);
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x * 2; i0 < m; i0 += (int64_t)gridDim.x * blockDim.x * 2) {
     const int64_t i = i0 + 2 * threadIdx.x;
-    if (i + 1 < m && (lda % 2 == 0) && (((uintptr_t)A) % 16 == 0)) {
-      double a0 = 0.0, a1 = 0.0;
+    if (i + 1 < m && vec) {
+      double a0[NX], a1[NX];
+#pragma unroll
+      for (int s = 0; s < NX; ++s) a0[s] = a1[s] = 0.0;
       const double2* col = reinterpret_cast<const double2*>(A + i);
 #pragma unroll 8
       for (int j = 0; j < d; ++j) {
         const double2 v = __ldg(col + (int64_t)j * (lda / 2));
-        a0 += v.x * xs[j];
-        a1 += v.y * xs[j];
+#pragma unroll
+        for (int s = 0; s < NX; ++s) {
+          a0[s] += v.x * xs[j * NX + s];
+          a1[s] += v.y * xs[j * NX + s];
+        }
       }
-      const double e0 = a0 - b[i], e1 = a1 - b[i + 1];
-      s += e0 * e0 + e1 * e1;
+      const double b0 = b[i], b1 = b[i + 1];
+#pragma unroll
+      for (int s = 0; s < NX; ++s) {
+        const double e0 = a0[s] - b0, e1 = a1[s] - b1;
+        sq[s] += e0 * e0 + e1 * e1;
+      }
     } else {
       for (int64_t ii = i; ii < i + 2 && ii < m; ++ii) {
-        double a0 = 0.0;
-        for (int j = 0; j < d; ++j) a0 += A[ii + (int64_t)j * lda] * xs[j];
-        const double e0 = a0 - b[ii];
-        s += e0 * e0;
+#pragma unroll
+        for (int s = 0; s < NX; ++s) {
+          double a0 = 0.0;
+          for (int j = 0; j < d; ++j) a0 += A[ii + (int64_t)j * lda] * xs[j * NX + s];
+          const double e0 = a0 - b[ii];
+          sq[s] += e0 * e0;
+        }
       }
     }
   }
-  s = block_sum<256>(s, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+#pragma unroll
+  for (int s = 0; s < NX; ++s) {
+    const double t = block_sum<256>(sq[s], red);
+    if (threadIdx.x == 0) part[(int64_t)s * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+int launch_lsr_residual_multi(Context* c, const double* A, int64_t lda, int64_t m, int64_t d, const double* b,
+                              const double* X, int nx, double* d_out) {
+  if (nx < 1 || nx > 4) return SLRA_ERR_INVALID_ARGUMENT;
+  int grid = c->num_sms * 4;
+  const int64_t need = (m + 511) / 512;
+  if (need < grid) grid = (int)(need > 0 ? need : 1);
+  double* part = partials(c, grid * nx);
+  if (!part) return SLRA_ERR_CUDA;
+  const size_t sm = sizeof(double) * d * nx;
+  switch (nx) {
+    case 1: SLRA_TIMED(c, "lsr_residual", lsr_residual_kernel<1><<<grid, 256, sm, c->stream>>>(A, lda, m, (int)d, b, X, part);) break;
+    case 2: SLRA_TIMED(c, "lsr_residual", lsr_residual_kernel<2><<<grid, 256, sm, c->stream>>>(A, lda, m, (int)d, b, X, part);) break;
+    case 3: SLRA_TIMED(c, "lsr_residual", lsr_residual_kernel<3><<<grid, 256, sm, c->stream>>>(A, lda, m, (int)d, b, X, part);) break;
+    default: SLRA_TIMED(c, "lsr_residual", lsr_residual_kernel<4><<<grid, 256, sm, c->stream>>>(A, lda, m, (int)d, b, X, part);) break;
+  }
+  SLRA_CHECK_LAUNCH(c);
+  SLRA_TIMED(c, "reduce", sum_kernel<<<nx, 256, 0, c->stream>>>(part, grid, d_out);)
+  SLRA_CHECK_LAUNCH(c);
+  return SLRA_OK;
 }
 
 int launch_lsr_residual(Context* c, const double* A, int64_t lda, int64_t m, int64_t d, const double* b,
                         const double* x, double* d_out) {
-  int grid = c->num_sms * 4;
-  const int64_t need = (m + 511) / 512;
-  if (need < grid) grid = (int)(need > 0 ? need : 1);
-  double* part = partials(c, grid);
-  if (!part) return SLRA_ERR_CUDA;
-  SLRA_TIMED(c, "lsr_residual", lsr_residual_kernel<<<grid, 256, sizeof(double) * d, c->stream>>>(A, lda, m, (int)d, b, x, part);)
-  SLRA_CHECK_LAUNCH(c);
-  SLRA_TIMED(c, "reduce", sum_kernel<<<1, 256, 0, c->stream>>>(part, grid, d_out);)
-  SLRA_CHECK_LAUNCH(c);
-  return SLRA_OK;
+  return launch_lsr_residual_multi(c, A, lda, m, d, b, x, 1, d_out);
 }
 
 }  // namespace slra_dev
@@ -378,6 +413,12 @@ int slra_lsr_residual(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
                       const double* x, double* d_out) {
   if (!ctx || lda < m || d < 1 || d > 4096) return SLRA_ERR_INVALID_ARGUMENT;
   return launch_lsr_residual(C(ctx), A, lda, m, d, b, x, d_out);
+}
+
+int slra_lsr_residual_multi(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t d, const double* b,
+                            const double* X, int64_t nx, double* d_out) {
+  if (!ctx || lda < m || d < 1 || d > 4096 || nx < 1 || nx > 4) return SLRA_ERR_INVALID_ARGUMENT;
+  return launch_lsr_residual_multi(C(ctx), A, lda, m, d, b, X, (int)nx, d_out);
 }
 
 }  // extern "C"
@@ -549,12 +590,22 @@ int launch_colpiv_lsq(Context* cx, double* W, int64_t k, int d, double* ws, int 
 // (returned through *fw_slot when fw_slot != nullptr on a first call).
 // fallback = 0: return SLRA_ERR_UNSUPPORTED instead of running the exact
 // path when the fast path declines (the caller has its own).
+int launch_gram_tn(Context* c, const char* fam, int64_t m, int64_t n, int64_t K, double alpha, const double* X,
+                   int64_t ldx, const double* Y, int64_t ldy, double beta, double* Cm, int64_t ldc, int lower);
+int launch_chol_cluster(Context* c, const double* Gw, int d, const double* FW, int64_t k, double tol_rel, double* x,
+                        double* ws, double* out, int32_t* status);
+size_t lsr_cluster_ws_doubles(int d, int64_t k, int num_sms);
+static int lsr_exact(Context* cx, const double* FW, int64_t k, int64_t d, double* x_hat, double* h_sketched_residual,
+                     double* r, double* part, double* out, int rgrid);
+
 static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, double* x_hat,
                      double* h_sketched_residual, double** fw_slot, int fallback = 1) {
   const int64_t dc = d + 1;
   const int rgrid = (int)((k + 31) / 32);  // lsq_residual_kernel: 32 rows per CTA
   // arena 2: FW (k x dc) | Gw (dc x dc) | G (d x d) | g (d) | r (k) | c (d) | y (2d) | part | out
-  const size_t need = (size_t)k * dc + (size_t)dc * dc + (size_t)d * d + 4 * (size_t)d + (size_t)k + rgrid + 16;
+  const bool cluster = d <= 256 && k <= (int64_t)1 << 16;
+  const size_t need = (size_t)k * dc + (size_t)dc * dc + (size_t)d * d + 4 * (size_t)d + (size_t)k + rgrid + 16 +
+                      (cluster ? lsr_cluster_ws_doubles((int)d, k, cx->num_sms) + 2 : 0);
   double* ws = static_cast<double*>(arena(cx, 2, sizeof(double) * need));
   if (!ws) return SLRA_ERR_CUDA;
   double* FW = ws;
@@ -573,6 +624,27 @@ static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, dou
     return SLRA_OK;
   }
   if (FWext) SLRA_CUDA(cudaMemcpyAsync(FW, FWext, 8 * (size_t)k * dc, cudaMemcpyDeviceToDevice, st));
+  double* hs = static_cast<double*>(cx->hsmall);
+  if (cluster) {
+    // ---- cluster fast path (lsr_cluster.cu): the augmented Gram's lower
+    // tiles on DMMA, then Cholesky + solve + one refinement step on one
+    // 8-CTA cluster; no host synchronisation before the status read-back
+    int gs = launch_gram_tn(cx, "gemm", dc, dc, k, 1.0, FW, k, FW, k, 0.0, Gw, dc, 1);
+    if (gs == SLRA_ERR_UNSUPPORTED) gs = launch_gemm(cx, 1, 0, dc, dc, k, 1.0, FW, k, FW, k, 0.0, Gw, dc);
+    SLRA_TRY(gs);
+    double* lws = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(out + 16) + 15) & ~(uintptr_t)15);
+    SLRA_TRY(launch_chol_cluster(cx, Gw, (int)d, FW, k, 1e-20, x_hat, lws, out, d_status));
+    SLRA_CUDA(cudaMemcpyAsync(hs, out, 8, cudaMemcpyDeviceToHost, st));
+    SLRA_CUDA(cudaMemcpyAsync(hs + 1, d_status, 8, cudaMemcpyDeviceToHost, st));
+    SLRA_CUDA(cudaStreamSynchronize(st));
+    const int32_t* hst = reinterpret_cast<const int32_t*>(hs + 1);
+    if (hst[0] == 0 && hst[1] == 0) {
+      if (h_sketched_residual) *h_sketched_residual = sqrt(hs[0]);
+      return SLRA_OK;
+    }
+    if (!fallback) return SLRA_ERR_UNSUPPORTED;
+    return lsr_exact(cx, FW, k, d, x_hat, h_sketched_residual, r, part, out, rgrid);
+  }
   // ---- fast path: Gram [FA Fb]^T [FA Fb] (dc x dc); G = leading d x d block, g = FA^T Fb
   SLRA_TRY(launch_gemm(cx, 1, 0, dc, dc, k, 1.0, FW, k, FW, k, 0.0, Gw, dc));
   SLRA_CUDA(cudaMemcpy2DAsync(G, 8 * d, Gw, 8 * dc, 8 * d, d, cudaMemcpyDeviceToDevice, st));
@@ -595,7 +667,6 @@ static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, dou
   SLRA_CHECK_LAUNCH(cx);
   SLRA_TIMED(cx, "reduce", sum_kernel<<<1, 256, 0, st>>>(part, rgrid, out);)
   SLRA_CHECK_LAUNCH(cx);
-  double* hs = static_cast<double*>(cx->hsmall);
   SLRA_CUDA(cudaMemcpyAsync(hs, out, 8, cudaMemcpyDeviceToHost, st));
   SLRA_CUDA(cudaMemcpyAsync(hs + 1, d_status, 8, cudaMemcpyDeviceToHost, st));
   SLRA_CUDA(cudaStreamSynchronize(st));
@@ -605,8 +676,17 @@ static int lsr_solve(Context* cx, const double* FWext, int64_t k, int64_t d, dou
     return SLRA_OK;
   }
   if (!fallback) return SLRA_ERR_UNSUPPORTED;
-  // ---- exact path (ill-conditioned or dependent sketch): the reference's
-  // ColPivHouseholderQR on a copy of FW, its rank rule, its solve
+  return lsr_exact(cx, FW, k, d, x_hat, h_sketched_residual, r, part, out, rgrid);
+}
+
+// ---- exact path (ill-conditioned or dependent sketch): the reference's
+// ColPivHouseholderQR on a copy of FW, its rank rule, its solve
+static int lsr_exact(Context* cx, const double* FW, int64_t k, int64_t d, double* x_hat, double* h_sketched_residual,
+                     double* r, double* part, double* out, int rgrid) {
+  const int64_t dc = d + 1;
+  cudaStream_t st = cx->stream;
+  int32_t* d_status = static_cast<int32_t*>(cx->dsmall);
+  double* hs = static_cast<double*>(cx->hsmall);
   double* Wq = static_cast<double*>(arena(cx, 13, sizeof(double) * ((size_t)k * dc + 4 * (size_t)d + 64)));
   if (!Wq) return SLRA_ERR_CUDA;
   SLRA_CUDA(cudaMemcpyAsync(Wq, FW, 8 * (size_t)k * dc, cudaMemcpyDeviceToDevice, st));

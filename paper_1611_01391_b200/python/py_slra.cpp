@@ -904,6 +904,12 @@ PYBIND11_MODULE(_slra, m) {
                             ptr<double>(out)),
           "lsr_residual");
   });
+  m.def("lsr_residual_multi_device", [](uintptr_t A, Index lda, Index mm, Index d, uintptr_t b, uintptr_t X,
+                                        Index nx, uintptr_t out) {
+    check(slra_lsr_residual_multi(device_context(), ptr<double>(A), lda, mm, d, ptr<double>(b), ptr<double>(X), nx,
+                                  ptr<double>(out)),
+          "lsr_residual_multi");
+  });
   m.def("gemm_device", [](int ta, int tb, Index mm, Index n, Index k, double alpha, uintptr_t A, Index lda,
                           uintptr_t B, Index ldb, double beta, uintptr_t Cm, Index ldc) {
     check(slra_gemm(device_context(), ta, tb, mm, n, k, alpha, ptr<double>(A), lda, ptr<double>(B), ldb, beta,

@@ -150,3 +150,44 @@ def test_solve_exact_well_conditioned_fast_path(slra, oracle):
     xg = slra.solve_exact(A, b)
     xo = oracle.solve_exact(A, b)
     assert np.linalg.norm(xg - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("d,k", [(1, 64), (7, 300), (32, 512), (33, 700), (100, 1500), (255, 4096), (256, 4096),
+                                 (256, 65536)])
+def test_cluster_solve_shapes_vs_oracle(slra, oracle, d, k):
+    """The d <= 256 fast path (augmented Gram on DMMA, Cholesky + solve +
+    refinement on one 8-CTA cluster) on ragged panel counts (d not a
+    multiple of 32, one panel, a single column) and k up to the cluster
+    path's limit: x_hat and the sketched residual within 1e-10 of the
+    oracle's ColPivHouseholderQR solve (lsr.cpp:52-60)."""
+    rng = np.random.default_rng(d * 1000 + k)
+    m = max(2 * k, 4 * d)
+    A = np.asfortranarray(rng.standard_normal((m, d)) * np.exp(rng.uniform(-2, 2, d)))
+    b = A @ rng.standard_normal(d) + 1e-3 * rng.standard_normal(m)
+    rows = slra.Rng(d + k).distinct_indices(k, m)
+    g = slra.sketch_solve(A, b, slra.make_sub_identity(rows, m), False)
+    o = oracle.sketch_solve(A, b, oracle.make_sub_identity(rows, m), False)
+    xo = o["x_hat"]
+    assert np.linalg.norm(g["x_hat"] - xo) <= 1e-10 * np.linalg.norm(xo)
+    assert abs(g["sketched_residual"] - o["sketched_residual"]) <= 1e-10 * max(o["sketched_residual"], 1e-300) + \
+        1e-12 * np.linalg.norm(b)
+
+
+def test_residual_multi_matches_single(slra):
+    """slra_lsr_residual_multi: ||A x_s - b||^2 for two and four solutions in
+    one pass equals the one-solution pass bit for bit (same per-thread order)."""
+    import torch
+    rng = np.random.default_rng(11)
+    m, d = 100003, 67  # odd m: the scalar tail rows
+    A = torch.from_numpy(np.asfortranarray(rng.standard_normal((m, d))).T.copy()).cuda()  # A^T rows = columns of A
+    b = torch.from_numpy(rng.standard_normal(m)).cuda()
+    for nx in (2, 4):
+        X = torch.from_numpy(rng.standard_normal((nx, d))).cuda()
+        out = torch.zeros(nx, dtype=torch.float64, device="cuda")
+        slra.lsr_residual_multi_device(A.data_ptr(), m, m, d, b.data_ptr(), X.data_ptr(), nx, out.data_ptr())
+        for s in range(nx):
+            one = torch.zeros(1, dtype=torch.float64, device="cuda")
+            slra.lsr_residual_device(A.data_ptr(), m, m, d, b.data_ptr(), X[s].data_ptr(), one.data_ptr())
+            assert out[s].item() == one.item()
+            ref = torch.linalg.vector_norm(A.T @ X[s] - b).item() ** 2
+            assert abs(out[s].item() - ref) <= 1e-12 * ref
