@@ -94,17 +94,24 @@ __global__ void __launch_bounds__(kCQ) chol_small_kernel(const double* __restric
   R += b * sR;
   rinv += b * sRi;
   constexpr int NN = NP * NP;
-  for (int e = tid; e < NN; e += kCQ) {
-    const int i = e % NP, c = e / NP;
-    if (i > c) continue;
-    double s = 0.0;  // chunk order fixed; each batch of 8 loads in flight before the adds
+  // upper-triangle entries only, every chunk's partial of an entry in flight
+  // at once (the partials are L2 reads: this sum, not the factorisation, was
+  // most of the kernel), added in chunk order
+  constexpr int NU = NP * (NP + 1) / 2;
+  for (int u = tid; u < NU; u += kCQ) {
+    int c = (int)((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);  // u = c (c + 1) / 2 + i, i <= c
+    while ((c + 1) * (c + 2) / 2 <= u) ++c;
+    while (c * (c + 1) / 2 > u) --c;
+    const int i = u - c * (c + 1) / 2;
+    const int e = i + c * NP;
+    double s = 0.0;
     int k = 0;
-    for (; k + 8 <= nchunk; k += 8) {
-      double v[8];
+    for (; k + 16 <= nchunk; k += 16) {
+      double v[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = P[(k + u) * NN + e];
+      for (int t = 0; t < 16; ++t) v[t] = P[(k + t) * NN + e];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) s += v[u];
+      for (int t = 0; t < 16; ++t) s += v[t];
     }
     for (; k < nchunk; ++k) s += P[k * NN + e];
     L[c + i * ld] = s;  // lower: L(c, i) = G(i, c), c >= i
@@ -116,51 +123,56 @@ __global__ void __launch_bounds__(kCQ) chol_small_kernel(const double* __restric
   for (int i = tid; i < NP; i += kCQ) L[i + i * ld] = i < n ? L[i + i * ld] + shift_coef * tr : 1.0;
   if (tid == 0) fail = 0;
   __syncthreads();
-  constexpr int kQ = (NP + 3) / 4;
-  const int ti = tid & 63, tc = tid >> 6;
+  // Column-publishing right-looking factorisation (one barrier per column):
+  // thread (i = tid % 64, g = tid / 64) holds A(i, g + 4 v) in registers;
+  // column j, once final, sits in L(:, j) (published by its owner group at
+  // the end of step j - 1) and every thread applies A(i, c) -= A(i, j) A(c, j)
+  // / A(j, j) to all of its entries unconditionally — entries of published
+  // columns and above the diagonal take garbage that is never read (the
+  // owner of column j + 1 republishes only its unpublished columns). At the
+  // end L(i, c) = A(i, c) / sqrt(A(c, c)).
+  constexpr int kV = NP / 4;
+  __shared__ double piv_s[NP];
+  const int ti = tid & 63, tg = tid >> 6;
+  double a[kV];
+#pragma unroll
+  for (int v = 0; v < kV; ++v) {
+    const int c = tg + 4 * v;
+    a[v] = (ti < NP && ti >= c) ? L[ti + c * ld] : 0.0;
+  }
   for (int j = 0; j < NP; ++j) {
-    const double piv = L[j + j * ld];
+    const double* cj = L + j * ld;
+    const double piv = cj[j];
     if (!(piv > 0.0)) {  // uniform: every thread read the same pivot
       if (tid == 0) fail = 1;
       break;
     }
-    // 1/sqrt(piv) from the hardware seed and two Newton steps (~1 ulp),
-    // L(j,j) = piv / sqrt(piv): no IEEE sqrt and division sequences on the
-    // column-to-column dependent chain
-    double inv = mufu_rsqrt(piv);
-    const double hp = 0.5 * piv;
+    const double rp = piv >= DBL_MIN ? fast_rcp(piv) : 1.0 / piv;
+    const double f = (ti > j && ti < NP) ? -cj[ti] * rp : 0.0;
 #pragma unroll
-    for (int it = 0; it < 2; ++it) inv = inv * fma(-hp * inv, inv, 1.5);
-    const double ljj = piv * inv;
-    const bool row = ti > j && ti < NP;
-    const double lij = row ? L[ti + j * ld] * inv : 0.0;
-    double lcj[kQ], cur[kQ];
+    for (int v = 0; v < kV; ++v) a[v] = fma(f, cj[tg + 4 * v], a[v]);
+    const int jn = j + 1;
+    if (tg == (jn & 3) && ti < NP && jn < NP) {
+      const int vv = jn >> 2;
 #pragma unroll
-    for (int q = 0; q < kQ; ++q) {
-      const int c = tc + 4 * q;
-      const bool act = row && c > j && c <= ti;
-      lcj[q] = act ? L[c + j * ld] * inv : 0.0;
-      cur[q] = act ? L[ti + c * ld] : 0.0;
+      for (int v = 0; v < kV; ++v)
+        if (v >= vv) L[ti + (tg + 4 * v) * ld] = a[v];
     }
-    __syncthreads();
-    if (tc == 0 && ti >= j && ti < NP) L[ti + j * ld] = (ti == j) ? ljj : lij;
-#pragma unroll
-    for (int q = 0; q < kQ; ++q) {
-      const int c = tc + 4 * q;
-      if (row && c > j && c <= ti) L[ti + c * ld] = cur[q] - lij * lcj[q];
-    }
+    if (tid == 0) piv_s[j] = piv;
     __syncthreads();
   }
-  __syncthreads();
   if (fail) {
     if (tid == 0) status[b] = 1;
     return;
   }
+  // R(i, c) = L(c, i) = A(c, i) / sqrt(A(i, i)) for i < c, sqrt(A(i, i)) on the diagonal
   for (int e = tid; e < n * n; e += kCQ) {
-    const int i = e % n, c = e / n;  // R(i, c) = L(c, i) for i <= c
-    R[e] = (i <= c) ? L[c + i * ld] : 0.0;
+    const int i = e % n, c = e / n;
+    const double pi = piv_s[i];
+    const double r = fast_rsqrt(pi);
+    R[e] = (i < c) ? L[c + i * ld] * r : (i == c ? pi * r : 0.0);
   }
-  for (int i = tid; i < NP; i += kCQ) rinv[i] = 1.0 / L[i + i * ld];
+  for (int i = tid; i < NP; i += kCQ) rinv[i] = fast_rsqrt(piv_s[i]);
 }
 
 // Q(i, :) = Y(i, :) R^-1 for every row i, one thread per row; problem
