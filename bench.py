@@ -888,10 +888,14 @@ class Config4:
         ach = b / (per[top] * 1e-3) / 1e9
         rl = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
               "frac": ach / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-              "algorithmic_bytes_per_launch": b, "traffic": profiled_traffic(4, {"lsr_residual": "lsr_residual_kernel", "lsr_solve": "cholesky_kernel"}.get(top), tag="r02")}
+              "algorithmic_bytes_per_launch": b, "traffic": profiled_traffic(4, {"lsr_residual": "lsr_residual_kernel", "lsr_solve": "chol_cluster_kernel"}.get(top), tag="r02")}
         if top == "lsr_solve":
-            rl["note"] = ("latency-bound: the 256 x 256 Cholesky and the triangular solves run on one CTA "
+            rl["note"] = ("latency-bound: the 256 x 256 Cholesky, solves and refinement run on one 8-CTA cluster "
                           "(FP64 dependent chains); per-launch mean over the family's kernels")
+        else:
+            rl["note"] = ("one pass over A|b certifies both samplers' solutions (slra_lsr_residual_multi); "
+                          "the solve (Gram on DMMA + 8-CTA cluster Cholesky/solve/refinement) is "
+                          f"{kernels.get('lsr_solve', 0.0) + kernels.get('gemm', 0.0) + kernels.get('gemm_reduce', 0.0):.3f} ms/step")
         if "lsr_residual" in per:
             rb = 8.0 * self.mloc * (D4 + 1)
             rl["lsr_residual_kernel"] = {"achieved_gbs": rb / (per["lsr_residual"] * 1e-3) / 1e9,

@@ -343,13 +343,23 @@ __global__ void __launch_bounds__(256) lsr_residual_kernel(const double* __restr
 #pragma unroll
       for (int s = 0; s < NX; ++s) a0[s] = a1[s] = 0.0;
       const double2* col = reinterpret_cast<const double2*>(A + i);
-#pragma unroll 8
-      for (int j = 0; j < d; ++j) {
-        const double2 v = __ldg(col + (int64_t)j * (lda / 2));
+      // batches of kRB columns: every load of a batch is issued before its
+      // FMAs (ncu: long-scoreboard stalls with the loads interleaved)
+      constexpr int kRB = 12;
+      for (int j0 = 0; j0 < d; j0 += kRB) {
+        double2 v[kRB];
 #pragma unroll
-        for (int s = 0; s < NX; ++s) {
-          a0[s] += v.x * xs[j * NX + s];
-          a1[s] += v.y * xs[j * NX + s];
+        for (int u = 0; u < kRB; ++u) v[u] = __ldg(col + (int64_t)(j0 + u < d ? j0 + u : j0) * (lda / 2));
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+          if (j0 + u < d) {
+#pragma unroll
+            for (int s = 0; s < NX; ++s) {
+              const double xv = xs[(j0 + u) * NX + s];
+              a0[s] = fma(v[u].x, xv, a0[s]);
+              a1[s] = fma(v[u].y, xv, a1[s]);
+            }
+          }
         }
       }
       const double b0 = b[i], b1 = b[i + 1];
