@@ -144,19 +144,46 @@ __global__ void __launch_bounds__(kNT) sketch_cols_list_kernel(const double* __r
 
 // out(t, :) = combine_s coef[t,s] * W(src[t,s], :); thread per (t, j),
 // t fastest so stores coalesce.
+// columns per thread of sketch_rows_kernel (kJB * Wd gathers in flight)
+__host__ __device__ constexpr int sr_jb(int wd) { return wd <= 2 ? 8 : (wd <= 4 ? 4 : (wd <= 8 ? 2 : 1)); }
+
 template <int Wd, int TREE>
 __global__ void __launch_bounds__(kNT) sketch_rows_kernel(const double* __restrict__ Wm, int64_t ldw,
                                                           int64_t ncols, const int64_t* __restrict__ src,
                                                           const double* __restrict__ coef,
                                                           const int32_t* __restrict__ qv, int64_t k,
                                                           double* __restrict__ out, int64_t ldo) {
-  const int64_t total = k * ncols;
-  for (int64_t e = blockIdx.x * (int64_t)kNT + threadIdx.x; e < total; e += (int64_t)gridDim.x * kNT) {
-    const int64_t t = e % k, j = e / k;
-    double z[Wd];
+  // a thread per output row t and kJB consecutive columns: the plan entries
+  // of the row are read once and all kJB * Wd gathers are in flight together
+  // (the rows are scattered sectors; one load per thread per iteration left
+  // the kernel latency-bound); no 64-bit index division
+  constexpr int kJB = sr_jb(Wd);
+  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (t >= k) return;
+  const int64_t j0 = (int64_t)blockIdx.y * kJB;
+  int64_t sr[Wd];
+  double cf[Wd];
 #pragma unroll
-    for (int s = 0; s < Wd; ++s) z[s] = coef[t * Wd + s] * __ldg(Wm + src[t * Wd + s] + j * ldw);
-    out[t + j * ldo] = combine<Wd, TREE>(z, TREE == SLRA_TREE_FWHT ? qv[t] : 0);
+  for (int s = 0; s < Wd; ++s) {
+    sr[s] = src[t * Wd + s];
+    cf[s] = coef[t * Wd + s];
+  }
+  const int qt = TREE == SLRA_TREE_FWHT ? qv[t] : 0;
+  double z[kJB][Wd];
+#pragma unroll
+  for (int u = 0; u < kJB; ++u) {
+    const int64_t j = j0 + u < ncols ? j0 + u : j0;
+#pragma unroll
+    for (int s = 0; s < Wd; ++s) z[u][s] = __ldg(Wm + sr[s] + j * ldw);
+  }
+#pragma unroll
+  for (int u = 0; u < kJB; ++u) {
+    if (j0 + u < ncols) {
+      double zz[Wd];
+#pragma unroll
+      for (int s = 0; s < Wd; ++s) zz[s] = cf[s] * z[u][s];
+      out[t + (j0 + u) * ldo] = combine<Wd, TREE>(zz, qt);
+    }
   }
 }
 
@@ -288,20 +315,20 @@ int launch_sketch_rows(Context* c, const double* Wm, int64_t ldw, int64_t ncols,
   if (tree == SLRA_TREE_FWHT) {
     KernelTimer kt(c, "sketch");
     switch (width) {
-      case 1: sketch_rows_kernel<1, SLRA_TREE_FWHT><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
-      case 2: sketch_rows_kernel<2, SLRA_TREE_FWHT><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
-      case 4: sketch_rows_kernel<4, SLRA_TREE_FWHT><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
-      case 8: sketch_rows_kernel<8, SLRA_TREE_FWHT><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
-      case 16: sketch_rows_kernel<16, SLRA_TREE_FWHT><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 1: sketch_rows_kernel<1, SLRA_TREE_FWHT><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(1))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 2: sketch_rows_kernel<2, SLRA_TREE_FWHT><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(2))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 4: sketch_rows_kernel<4, SLRA_TREE_FWHT><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(4))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 8: sketch_rows_kernel<8, SLRA_TREE_FWHT><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(8))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 16: sketch_rows_kernel<16, SLRA_TREE_FWHT><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(16))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
       default: return SLRA_ERR_UNSUPPORTED;
     }
   } else {
     KernelTimer kt(c, "sketch");
     switch (width) {
-      case 1: sketch_rows_kernel<1, SLRA_TREE_LIST><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
-      case 2: sketch_rows_kernel<2, SLRA_TREE_LIST><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
-      case 3: sketch_rows_kernel<3, SLRA_TREE_LIST><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
-      case 4: sketch_rows_kernel<4, SLRA_TREE_LIST><<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 1: sketch_rows_kernel<1, SLRA_TREE_LIST><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(1))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 2: sketch_rows_kernel<2, SLRA_TREE_LIST><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(2))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 3: sketch_rows_kernel<3, SLRA_TREE_LIST><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(3))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
+      case 4: sketch_rows_kernel<4, SLRA_TREE_LIST><<<dim3(ceil_div(k, kNT), ceil_div(ncols, sr_jb(4))), kNT, 0, s>>>(Wm, ldw, ncols, src, coef, q, k, out, ldo); break;
       default: sketch_rows_list_kernel<<<g, kNT, 0, s>>>(Wm, ldw, ncols, src, coef, width, k, out, ldo); break;
     }
   }
