@@ -51,6 +51,7 @@ struct CaSmem {
   double *S, *W, *R, *Gt, *V, *tau, *v, *nu, *nd, *rn, *sigma, *sgn, *rv, *Tm, *Sm, *volv;
   int *p2r, *r2p, *Icur, *Jcur, *perm, *order, *flag, *tmpidx;
   int64_t* ri;
+  uint64_t* mbar;  // the bulk-copy (TMA) barrier of the column-strip staging
 };
 
 __host__ __device__ inline size_t ca_even(size_t d) { return (d + 1) & ~(size_t)1; }
@@ -67,7 +68,7 @@ __host__ __device__ inline size_t ca_smem_bytes(int m, int n, int k, int l) {
   size_t d = ca_even(ns) + 3 * ca_even((size_t)(cw + 1) * cw) + 3 * ca_even(c) + 64 +
              3 * ca_even(mm > 16 ? mm : 16) + 40 + 8 + ca_even(2 * (size_t)c);
   size_t i = 2 * (size_t)mm + 5 * (size_t)c + 8;
-  return d * 8 + 33 * 8 + i * 4 + 64;
+  return d * 8 + 34 * 8 + i * 4 + 64;
 }
 
 __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
@@ -98,7 +99,8 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   s.volv = d; d += 8;
   d += ca_even(2 * (size_t)c);  // slack
   s.ri = reinterpret_cast<int64_t*>(d);
-  int* ip = reinterpret_cast<int*>(s.ri + 33);
+  s.mbar = reinterpret_cast<uint64_t*>(s.ri + 33);
+  int* ip = reinterpret_cast<int*>(s.ri + 34);
   s.p2r = ip; ip += mm;
   s.r2p = ip; ip += mm;
   s.Icur = ip; ip += c;
@@ -110,12 +112,53 @@ __device__ CaSmem ca_carve(char* base, int m, int n, int k, int l) {
   return s;
 }
 
+// ---- TMA bulk copies (cp.async.bulk) for the contiguous column strips
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // S (len x nidx, ld len) <- the strip A(idx, :)^T (rows_strip) or A(:, idx):
 // a thread per strip row, eight independent global loads in flight before
 // the shared-memory stores (no per-element integer division)
 template <int NT>
 __device__ void stage_strip(double* S, const double* A, int64_t lda, bool rows_strip, const int* idx, int nidx,
-                            int len) {
+                            int len, uint64_t* mbar = nullptr, unsigned* phase = nullptr) {
+  if (!rows_strip && mbar && nidx <= 32 && (len & 1) == 0 && (lda & 1) == 0 && ((uintptr_t)A & 15) == 0) {
+    // column strip: nidx contiguous columns of len doubles -> one TMA bulk
+    // copy each (warp 0's lanes issue them), completion on the mbarrier.
+    // The callers' block barrier precedes this; the proxy fence orders the
+    // earlier generic accesses to S before the async-proxy writes.
+    if (threadIdx.x < 32) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(mbar, (unsigned)(nidx * len * 8));
+      __syncwarp();
+      if (threadIdx.x < nidx)
+        bulk_g2s(S + threadIdx.x * len, A + (int64_t)idx[threadIdx.x] * lda, (unsigned)(len * 8), mbar);
+    }
+    mbar_wait(mbar, *phase);
+    *phase ^= 1u;
+    return;
+  }
   for (int i = threadIdx.x; i < len; i += NT) {
     for (int t0 = 0; t0 < nidx; t0 += 8) {
       double v[8];
@@ -135,12 +178,12 @@ __device__ void stage_strip(double* S, const double* A, int64_t lda, bool rows_s
 // from A: rows_strip -> strip = A(idx_in, :)^T (len = n), else A(:, idx_in).
 template <int NT, int CMAX>
 __device__ int select_strip(CaSmem& s, const double* A, int64_t lda, bool rows_strip, const int* idx_in, int nidx,
-                            int len, int count, double h, int* idx_out, double* vol_out) {
+                            int len, int count, double h, int* idx_out, double* vol_out, unsigned* phase = nullptr) {
   const int tid = threadIdx.x;
   // gather (each element of the strip is an entry read of the oracle)
   // 2-D loops (no integer division per element), unrolled so that several
   // independent global loads are in flight before the shared-memory stores
-  stage_strip<NT>(s.S, A, lda, rows_strip, idx_in, nidx, len);
+  stage_strip<NT>(s.S, A, lda, rows_strip, idx_in, nidx, len, phase ? s.mbar : nullptr, phase);
   __syncthreads();
   SLRA_PROF(1);
   // ONE len x nidx array carries the strip, its basis Q (in place) and then
@@ -562,17 +605,38 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
 #ifndef SLRA_C5_L2
 #define SLRA_C5_L2 2
 #endif
+    if (tid == 0) {
+      mbar_init(s.mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const bool bulk = (P.m & 1) == 0 && (P.lda & 1) == 0 && ((uintptr_t)A & 15) == 0;
     if (P.pairs && SLRA_C5_L2 > 0) {
       // the block is read by every half-sweep's strip gather and by the fused
-      // residual: pull it into L2 once, in full lines, before the first gather
-      for (int j = tid; j < P.n * ((P.m + 15) / 16); j += kCT) {
-        const int c = j / ((P.m + 15) / 16), i = 16 * (j % ((P.m + 15) / 16));
-        if (SLRA_C5_L2 == 2) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(A + i + (int64_t)c * P.lda));
-        else asm volatile("prefetch.global.L2 [%0];" ::"l"(A + i + (int64_t)c * P.lda));
+      // residual: pull it into L2 once before the first gather — one TMA bulk
+      // prefetch per column (evict-last), else full-line prefetches
+      if (bulk) {
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        for (int c = tid; c < P.n; c += kCT) {
+          if (SLRA_C5_L2 == 2)
+            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(A + (int64_t)c * P.lda),
+                         "r"(P.m * 8), "l"(pol)
+                         : "memory");
+          else
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A + (int64_t)c * P.lda), "r"(P.m * 8)
+                         : "memory");
+        }
+      } else {
+        for (int j = tid; j < P.n * ((P.m + 15) / 16); j += kCT) {
+          const int c = j / ((P.m + 15) / 16), i = 16 * (j % ((P.m + 15) / 16));
+          if (SLRA_C5_L2 == 2) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(A + i + (int64_t)c * P.lda));
+          else asm volatile("prefetch.global.L2 [%0];" ::"l"(A + i + (int64_t)c * P.lda));
+        }
       }
     }
     for (int t = tid; t < P.k; t += kCT) s.Icur[t] = (int)P.init_rows[(int64_t)b * P.k + t];
     __syncthreads();
+    unsigned phase = 0;  // parity of the column-strip mbarrier
     SLRA_PROF(0);
     for (int loop = 0; loop < P.loops && status == SLRA_OK; ++loop) {
       double* vol = (b == 0 && P.trace_vol) ? P.trace_vol + 2 * loop : nullptr;
@@ -583,7 +647,8 @@ __global__ void __launch_bounds__(kCT, CMAX <= 32 ? 2 : 1) ca_block_kernel(CaPar
         for (int t = tid; t < P.l; t += kCT) P.trace_cols[(int64_t)(2 * loop) * P.l + t] = s.Jcur[t];
       }
       vol = (b == 0 && P.trace_vol) ? P.trace_vol + 2 * loop + 1 : nullptr;
-      status = select_strip<kCT, CMAX>(s, A, P.lda, false, s.Jcur, P.l, P.m, P.k, P.h, s.Icur, vol);
+      status = select_strip<kCT, CMAX>(s, A, P.lda, false, s.Jcur, P.l, P.m, P.k, P.h, s.Icur, vol,
+                                       bulk ? &phase : nullptr);
       if (status != SLRA_OK) break;
       if (b == 0 && P.trace_rows) {
         for (int t = tid; t < P.k; t += kCT) P.trace_rows[(int64_t)(2 * loop + 1) * P.k + t] = s.Icur[t];
