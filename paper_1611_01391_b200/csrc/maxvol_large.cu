@@ -33,7 +33,26 @@ struct MaxvolLargeArgs {
   int64_t* cand_pos;  // 2 x G
   int64_t* cand_row;  // 2 x G
   double* cand_vec;   // 2 x G x kMR
+  unsigned* gbar;     // grid barrier arrival counter (zeroed before the launch)
 };
+
+// Grid barrier for the co-resident (cooperatively launched) grid: one
+// arrival per CTA on a monotonic counter and a spin on its acquire load
+// (the cooperative-groups grid.sync was a third of each pivot step).
+// target = G * (number of barriers so far, this one included).
+__device__ __forceinline__ void grid_barrier(unsigned* gbar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(gbar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
 
 // Publish this CTA's candidate (value, key, global row, r-vector) into slot.
 __device__ __forceinline__ void publish(const MaxvolLargeArgs& a, int slot, int G, int b, double v, int64_t key,
@@ -120,20 +139,17 @@ __global__ void __launch_bounds__(kMT) maxvol_large_kernel(MaxvolLargeArgs a) {
   // them (cur.cpp:100-108).
   for (int k = 0; k < r; ++k) {
     const int slot = (sync_no++) & 1;
-    ArgMax best{-1.0, INT64_MAX};  // key: value, then lowest current position
+    // key: value, then the lowest current position; the local row rides in
+    // the key's low 16 bits (positions are unique, so the order is unchanged)
+    ArgMax best{-1.0, INT64_MAX};
     for (int i = tid; i < nr; i += kMT)
-      if (!chosen[i]) best = argmax_merge(best, ArgMax{nu[i], pos[i]});
+      if (!chosen[i]) best = argmax_merge(best, ArgMax{nu[i], (pos[i] << 16) | i});
     best = block_argmax<kMT>(best, rv, ri);
-    if (tid == 0) sflag[1] = -1;
-    __syncthreads();
-    for (int i = tid; i < nr; i += kMT)
-      if (!chosen[i] && pos[i] == best.i) sflag[1] = i;
-    __syncthreads();
-    const int li = sflag[1];
+    const int li = best.i == INT64_MAX ? -1 : (int)(best.i & 0xffff);
     publish(a, slot, G, b, best.v, best.i, li >= 0 ? row0 + li : -1, li >= 0 ? W + li * ldw : nullptr, r);
-    grid.sync();
+    grid_barrier(a.gbar, (unsigned)(G * sync_no));
     const int win = reduce_candidates(a, slot, G, rv, ri, sflag);
-    const int64_t big = ri[0];
+    const int64_t big = ri[0] >> 16;
     const double pivnorm = rv[0];
     const int64_t wrow = __ldcg(a.cand_row + slot * G + win);
     const double* xv = a.cand_vec + (size_t)(slot * G + win) * kMR;
@@ -254,7 +270,7 @@ __global__ void __launch_bounds__(kMT) maxvol_large_kernel(MaxvolLargeArgs a) {
     best = block_argmax<kMT>(best, rv, ri);
     const int64_t lrow = best.i == INT64_MAX ? -1 : (best.i % a.m);
     publish(a, slot, G, b, best.v, best.i, lrow, lrow >= 0 ? W + (lrow - row0) * ldw : nullptr, r);
-    grid.sync();
+    grid_barrier(a.gbar, (unsigned)(G * sync_no));
     const int win = reduce_candidates(a, slot, G, rv, ri, sflag);
     const double mx = rv[0];
     const int64_t lin = ri[0];
@@ -323,6 +339,8 @@ int launch_maxvol_large(Context* cx, const double* Q, int64_t ldq, int64_t m, in
   args.cand_pos = reinterpret_cast<int64_t*>(scratch + 2 * G);
   args.cand_row = reinterpret_cast<int64_t*>(scratch + 4 * G);
   args.cand_vec = scratch + 6 * G;
+  args.gbar = reinterpret_cast<unsigned*>(scratch + 6 * G + 2 * (size_t)G * kMR);
+  SLRA_CUDA(cudaMemsetAsync(args.gbar, 0, sizeof(unsigned), cx->stream));
   void* kargs[] = {&args};
   {
     KernelTimer kt(cx, "maxvol");
