@@ -425,6 +425,8 @@ def main():
         "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
         "residual_rel": work.last_residual_rel(),
     }
+    if hasattr(work, "function_oracle") and ws == 1 and args.e2e_steps > 0:
+        line["function_oracle"] = work.function_oracle(min(args.steps, 10), args.warmup)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = work.cpu_baseline()
     if rank == 0:
@@ -961,11 +963,15 @@ class Config5:
         # same recipe as the oracle/tests), blocks materialised on the device
         self.A = torch.empty(nb, m, m, dtype=torch.float64, device="cuda")
         self.init = torch.empty(nb, C5_K, dtype=torch.int64, device="cuda")
+        # the points too (px, py, qx, qy: nb x m each): the FunctionOracle form of the same blocks
+        self.pts = torch.empty(4, nb, m, dtype=torch.float64, device="cuda")
         for c0 in range(0, nb, self.CHUNK):
             c = min(self.CHUNK, nb - c0)
             px, py, qx, qy, init = config5_host_inputs(slra, seed, self.b0 + c0, c)
             dev = [torch.from_numpy(a).cuda() for a in (px, py, qx, qy)]
             slra.gen_log_kernel_blocks_device(*[d.data_ptr() for d in dev], c, m, m, self.A[c0].data_ptr(), m, m * m)
+            for i, d in enumerate(dev):
+                self.pts[i, c0:c0 + c] = d.view(c, m)
             self.init[c0:c0 + c] = torch.from_numpy(init).cuda()
         torch.cuda.synchronize()
         self.I = torch.zeros(nb, C5_K, dtype=torch.int64, device="cuda")
@@ -1040,6 +1046,55 @@ class Config5:
                              "frac": byts / (per * 1e-3) / 1e9 / peaks["hbm_gbs"], "peak": peaks["hbm_gbs"]},
                 "note": "FP64 latency-bound: one CTA per block (two per SM) runs the C-A chain (strip QR, "
                         "pivoted QR, maxvol, Jacobi SVD) and the DMMA residual; see DESIGN.md 5 and profiles/"}, kernels
+
+    def function_oracle(self, steps, warmup):
+        """The same batch with the blocks given by their points (FunctionOracle, oracle.hpp:43-54):
+        slra_cross_approx_batched_logkernel evaluates every entry the C-A reads (strips, generator, the
+        residual's full pass) from the points instead of reading a materialised block — bit-identical
+        entries, so identical results (checked). Device-resident points (CUDA events), then the
+        host-buffer entry (pinned points in, results out; wall clock)."""
+        torch, slra, nb = self.torch, self.slra, self.nb
+        outs = [torch.empty_like(t) for t in (self.I, self.J, self.U, self.r, self.st, self.rs, self.ns)]
+        P = [self.pts[i].data_ptr() for i in range(4)]
+
+        def dev():
+            slra.cross_approx_batched_logkernel_device(*P, nb, C5_M, C5_M, 0, C5_K, C5_K, self.init.data_ptr(),
+                                                       C5_LOOPS, 1.1, *[o.data_ptr() for o in outs])
+        for _ in range(max(warmup, 1)):
+            dev()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            dev()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        same = all(bool(torch.equal(a, b)) for a, b in zip(outs, (self.I, self.J, self.U, self.r, self.st, self.rs,
+                                                                    self.ns)))
+        hp = [self.pts[i].cpu().pin_memory() for i in range(4)]
+        hinit = self.init.cpu().pin_memory()
+        houts = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+
+        def host():
+            slra.cross_approx_batched_logkernel_host(*[h.data_ptr() for h in hp], nb, C5_M, C5_M, 0, C5_K, C5_K,
+                                                     hinit.data_ptr(), C5_LOOPS, 1.1, *[o.data_ptr() for o in houts])
+        host()
+        torch.cuda.synchronize()
+        hsteps = max(1, min(steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(hsteps):
+            host()
+        dt = time.perf_counter() - t0
+        same_host = bool(torch.equal(houts[0], self.I.cpu()) and torch.equal(houts[1], self.J.cpu()))
+        d2h = nb * (8 * 2 * C5_K + 8 * C5_K * C5_K + 8 + 4 + 16)
+        return {"value": nb * C5_M * C5_M / (ms * 1e-3), "unit": "entries/s", "ms_per_step": ms, "steps": steps,
+                "identical_to_dense_run": same,
+                "e2e": {"value": nb * C5_M * C5_M * hsteps / dt, "unit": "entries/s",
+                        "h2d_bytes_per_step": nb * 8 * (4 * C5_M + C5_K), "d2h_bytes_per_step": d2h,
+                        "steps": hsteps, "same_I_J_as_device_run": same_host},
+                "api": "paper_1611_01391_b200.cross_approx_batched_logkernel_{device,host} -> "
+                       "slra_cross_approx_batched_logkernel(_host) (points in; blocks never materialised)"}
 
     def e2e(self, steps, warmup):
         """The batch through the host-buffer entry (slra_cross_approx_batched_host): pinned host blocks

@@ -194,6 +194,29 @@ int slra_cross_approx_batched_host(slra_ctx ctx, const double* h_A, int64_t lda,
                                    int64_t l, const int64_t* h_init_rows, int loops, double h,
                                    int64_t* h_I, int64_t* h_J, double* h_nucleus, int64_t* h_r,
                                    int32_t* h_status, double* h_resid_sq, double* h_norm_sq);
+/* cross_approx_batched over log-kernel blocks given by their points
+ * (FunctionOracle, oracle.hpp:43-54; the config-5 recipe K_ij =
+ * 0.5 log((p_i - q_j)^2), hss.cpp:47-55 pattern): the same C-A per block as
+ * slra_cross_approx_batched, every entry the algorithm reads evaluated on
+ * the fly (the strips, the generator, the residual's full pass) instead of
+ * read from a materialised block — bit-identical entries to
+ * slra_gen_log_kernel_blocks, hence identical results. Points per block:
+ * px, py (nblocks x m), qx, qy (nblocks x n), device. k, l <= 32 and
+ * m, n multiples of 8 (the residual is fused), else SLRA_ERR_UNSUPPORTED. */
+int slra_cross_approx_batched_logkernel(slra_ctx ctx, const double* d_px, const double* d_py, const double* d_qx,
+                                        const double* d_qy, int64_t nblocks, int64_t m, int64_t n, int64_t r,
+                                        int64_t k, int64_t l, const int64_t* d_init_rows, int loops, double h,
+                                        int64_t* d_I, int64_t* d_J, double* d_nucleus, int64_t* d_r,
+                                        int32_t* d_status, double* d_resid_sq, double* d_norm_sq);
+/* The same from host buffers (pinned for overlap): the points stream to the
+ * device in eight chunks on a copy stream while the previous chunk is
+ * factorised; results come back as in slra_cross_approx_batched_host. */
+int slra_cross_approx_batched_logkernel_host(slra_ctx ctx, const double* h_px, const double* h_py,
+                                             const double* h_qx, const double* h_qy, int64_t nblocks, int64_t m,
+                                             int64_t n, int64_t r, int64_t k, int64_t l, const int64_t* h_init_rows,
+                                             int loops, double h, int64_t* h_I, int64_t* h_J, double* h_nucleus,
+                                             int64_t* h_r, int32_t* h_status, double* h_resid_sq,
+                                             double* h_norm_sq);
 
 /* ------------------------------------------------------------ a13 input generator
  * Config-5 log-kernel blocks (testgen: K_ij = log|p_i - q_j| =

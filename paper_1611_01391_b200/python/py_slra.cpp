@@ -814,6 +814,32 @@ PYBIND11_MODULE(_slra, m) {
                                          ptr<double>(rs), ptr<double>(ns)),
           "cross_approx_batched_host");
   });
+  // the same over log-kernel blocks given by their points (FunctionOracle): device / host buffers
+  m.def("cross_approx_batched_logkernel_device", [](uintptr_t px, uintptr_t py, uintptr_t qx, uintptr_t qy,
+                                                    Index nblocks, Index mm, Index n, Index r, Index k, Index l,
+                                                    uintptr_t init_rows, int loops, double h, uintptr_t I,
+                                                    uintptr_t J, uintptr_t U, uintptr_t rr, uintptr_t status,
+                                                    uintptr_t rs, uintptr_t ns) {
+    check(slra_cross_approx_batched_logkernel(device_context(), ptr<const double>(px), ptr<const double>(py),
+                                              ptr<const double>(qx), ptr<const double>(qy), nblocks, mm, n, r, k, l,
+                                              ptr<const int64_t>(init_rows), loops, h, ptr<int64_t>(I),
+                                              ptr<int64_t>(J), ptr<double>(U), ptr<int64_t>(rr),
+                                              ptr<int32_t>(status), ptr<double>(rs), ptr<double>(ns)),
+          "cross_approx_batched_logkernel");
+  });
+  m.def("cross_approx_batched_logkernel_host", [](uintptr_t px, uintptr_t py, uintptr_t qx, uintptr_t qy,
+                                                  Index nblocks, Index mm, Index n, Index r, Index k, Index l,
+                                                  uintptr_t init_rows, int loops, double h, uintptr_t I, uintptr_t J,
+                                                  uintptr_t U, uintptr_t rr, uintptr_t status, uintptr_t rs,
+                                                  uintptr_t ns) {
+    py::gil_scoped_release nogil;
+    check(slra_cross_approx_batched_logkernel_host(device_context(), ptr<const double>(px), ptr<const double>(py),
+                                                   ptr<const double>(qx), ptr<const double>(qy), nblocks, mm, n, r,
+                                                   k, l, ptr<const int64_t>(init_rows), loops, h, ptr<int64_t>(I),
+                                                   ptr<int64_t>(J), ptr<double>(U), ptr<int64_t>(rr),
+                                                   ptr<int32_t>(status), ptr<double>(rs), ptr<double>(ns)),
+          "cross_approx_batched_logkernel_host");
+  });
   // config-5 inputs: host points (reference Rng) -> device blocks
   m.def("gen_log_kernel_batch", [](std::uint64_t master, Index b0, Index nb, Index mm, Index n, Index k,
                                    uintptr_t px, uintptr_t py, uintptr_t qx, uintptr_t qy, uintptr_t init) {

@@ -307,3 +307,52 @@ def test_batched_host_entry_chunks_and_pageable(slra, bench):
                                    *[out[k].ctypes.data for k in ("I", "J", "U", "r", "st", "rs", "ns")])
     for key in ("I", "J", "U", "r", "st", "rs", "ns"):
         assert np.array_equal(out[key], g[key]), key
+
+
+def _run_logkernel(slra, torch, pts, init, host=False):
+    nb = init.shape[0]
+    out = dict(I=torch.zeros((nb, K), dtype=torch.int64), J=torch.zeros((nb, K), dtype=torch.int64),
+               U=torch.zeros((nb, K * K), dtype=torch.float64), r=torch.zeros(nb, dtype=torch.int64),
+               st=torch.zeros(nb, dtype=torch.int32), rs=torch.zeros(nb, dtype=torch.float64),
+               ns=torch.zeros(nb, dtype=torch.float64))
+    if host:
+        hp = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in pts]
+        hi = torch.from_numpy(np.ascontiguousarray(init)).pin_memory()
+        out = {k: v.pin_memory() for k, v in out.items()}
+        slra.cross_approx_batched_logkernel_host(*[a.data_ptr() for a in hp], nb, M, M, 0, K, K, hi.data_ptr(), LOOPS,
+                                                 1.1, *[out[k].data_ptr() for k in ("I", "J", "U", "r", "st", "rs",
+                                                                                     "ns")])
+    else:
+        dp = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in pts]
+        di = torch.from_numpy(np.ascontiguousarray(init)).cuda()
+        out = {k: v.cuda() for k, v in out.items()}
+        slra.cross_approx_batched_logkernel_device(*[a.data_ptr() for a in dp], nb, M, M, 0, K, K, di.data_ptr(),
+                                                   LOOPS, 1.1, *[out[k].data_ptr() for k in ("I", "J", "U", "r", "st",
+                                                                                            "rs", "ns")])
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_logkernel_oracle_bit_identical_to_dense(slra, bench, host):
+    """The FunctionOracle path (entries evaluated from the points where C-A
+    reads them, oracle.hpp:43-54) gives exactly the dense path's results on
+    the same bench blocks: the on-the-fly entries are bit-identical to the
+    materialised ones, so every selection, nucleus and residual is too. The
+    host variant streams the points in eight chunks (uneven last chunk)."""
+    import torch
+    nb = 1029 if host else 1024
+    A, init, pts = _bench_blocks(slra, bench, torch, 4096, nb)
+    dense = _run_batched(slra, torch, A, torch.from_numpy(init).cuda())
+    lk = _run_logkernel(slra, torch, pts, init, host=host)
+    for key in ("I", "J", "U", "r", "st", "rs", "ns"):
+        assert np.array_equal(dense[key], lk[key]), key
+
+
+def test_logkernel_rejects_unsupported_shapes(slra):
+    import torch
+    z = torch.zeros(64, dtype=torch.float64, device="cuda")
+    iz = torch.zeros(64, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        slra.cross_approx_batched_logkernel_device(z.data_ptr(), z.data_ptr(), z.data_ptr(), z.data_ptr(), 1, 12, 12,
+                                                   0, 4, 4, iz.data_ptr(), 1, 1.1, *([iz.data_ptr()] * 7))
