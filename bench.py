@@ -425,7 +425,7 @@ def main():
         "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
         "residual_rel": work.last_residual_rel(),
     }
-    if hasattr(work, "function_oracle") and ws == 1 and args.e2e_steps > 0:
+    if hasattr(work, "function_oracle") and ws == 1 and (args.e2e_steps > 0 or args.config != 5):
         line["function_oracle"] = work.function_oracle(min(args.steps, 10), args.warmup)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = work.cpu_baseline()
@@ -719,6 +719,66 @@ class Config3:
                 "d2h_bytes_per_step": 8 * (2 * K3 + K3 * K3 + 2 * K3 * d["r"] + 2),
                 "api": "paper_1611_01391_b200.cross_approx_host -> slra::cross_approx + slra::cur_evaluate "
                        "(host pinned A in; I, J, nucleus, residual out)"}
+
+    def function_oracle(self, steps, warmup):
+        """The same step with A given by its points (FunctionOracle, oracle.hpp:43-54):
+        slra_cross_approx_cauchy + slra_cur_residual_factored_cauchy evaluate the strips, the
+        generator and the residual pass's tiles instead of reading the materialised 2 GiB matrix
+        (bit-identical results, checked). Device-resident points (CUDA events), then end to end:
+        pinned host points in, I, J, nucleus factors and the residual pair out (wall clock)."""
+        torch, slra = self.torch, self.slra
+        x, y = config3_points(slra, self.seed)
+        xd = torch.tensor(x, dtype=torch.float64, device="cuda")
+        yd = torch.tensor(y, dtype=torch.float64, device="cuda")
+        o = {k: torch.zeros_like(v) for k, v in (("I", self.I), ("J", self.J), ("U", self.U), ("T", self.T),
+                                                  ("S", self.S), ("out", self.out))}
+
+        def dev(xp, yp):
+            r = slra.cross_approx_cauchy_device(xp, yp, N3, N3, 0, K3, K3, self.init_d.data_ptr(), LOOPS3, 1.1,
+                                                o["I"].data_ptr(), o["J"].data_ptr(), o["U"].data_ptr(),
+                                                o["T"].data_ptr(), o["S"].data_ptr())
+            slra.cur_residual_factored_cauchy_device(xp, yp, N3, N3, o["I"].data_ptr(), K3, o["J"].data_ptr(), K3,
+                                                     o["T"].data_ptr(), o["S"].data_ptr(), r, o["out"].data_ptr())
+            return r
+        for _ in range(max(warmup, 1)):
+            dev(xd.data_ptr(), yd.data_ptr())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            r = dev(xd.data_ptr(), yd.data_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        same = r == self.r and all(bool(torch.equal(o[k], v)) for k, v in (("I", self.I), ("J", self.J),
+                                                                          ("U", self.U), ("out", self.out)))
+        hx = torch.tensor(x, dtype=torch.float64).pin_memory()
+        hy = torch.tensor(y, dtype=torch.float64).pin_memory()
+        hout = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in o.items()}
+
+        def e2e_one():
+            xs, ys = hx.to("cuda", non_blocking=True), hy.to("cuda", non_blocking=True)
+            rr = dev(xs.data_ptr(), ys.data_ptr())
+            for k in ("I", "J", "U", "out"):
+                hout[k].copy_(o[k], non_blocking=True)
+            n_r = K3 * rr
+            hout["T"][:n_r].copy_(o["T"][:n_r], non_blocking=True)
+            hout["S"][:n_r].copy_(o["S"][:n_r], non_blocking=True)
+            torch.cuda.synchronize()
+            return rr
+        e2e_one()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            rr = e2e_one()
+        dt = time.perf_counter() - t0
+        return {"value": self.entries_per_step / (ms * 1e-3), "unit": "entries/s", "ms_per_step": ms,
+                "steps": steps, "identical_to_dense_run": same,
+                "e2e": {"value": self.entries_per_step * steps / dt, "unit": "entries/s",
+                        "h2d_bytes_per_step": 16 * N3, "d2h_bytes_per_step": 8 * (2 * K3 + K3 * K3 + 2 * K3 * rr + 2),
+                        "steps": steps},
+                "api": "paper_1611_01391_b200.cross_approx_cauchy_device + cur_residual_factored_cauchy_device -> "
+                       "slra_cross_approx_cauchy / slra_cur_residual_factored_cauchy (points in; A never "
+                       "materialised)"}
 
     def cpu_baseline(self):
         sys.path.insert(0, os.path.join(ROOT, "oracle", "build"))

@@ -194,6 +194,22 @@ int slra_cross_approx_batched_host(slra_ctx ctx, const double* h_A, int64_t lda,
                                    int64_t l, const int64_t* h_init_rows, int loops, double h,
                                    int64_t* h_I, int64_t* h_J, double* h_nucleus, int64_t* h_r,
                                    int32_t* h_status, double* h_resid_sq, double* h_norm_sq);
+/* cross_approx (cur.cpp:201-255) over the Cauchy FunctionOracle A_ij =
+ * 1/(x_i - y_j) (config 3's FMM-style block, oracle.hpp:43-54): the same
+ * selections and nucleus as slra_cross_approx on the materialised matrix
+ * (bit for bit), with the strips and the generator evaluated from the
+ * points x (m), y (n) — device pointers — instead of gathered from HBM.
+ * k == l <= 64 when m or n > 256. */
+int slra_cross_approx_cauchy(slra_ctx ctx, const double* d_x, const double* d_y, int64_t m, int64_t n, int64_t r,
+                             int64_t k, int64_t l, const int64_t* d_init_rows, int loops, double h, int64_t* d_I,
+                             int64_t* d_J, double* d_nucleus, int64_t* d_trace_rows, int64_t* d_trace_cols,
+                             double* d_trace_vol, double* d_Tsig, double* d_Sr, int64_t* h_r_out);
+/* cur_evaluate(M, c, Frobenius) (cur.cpp:76-82) for the Cauchy oracle with
+ * the factored nucleus: C, R evaluated, the full pass over A evaluates its
+ * tiles (cauchy_residual_stream_kernel). d_out[0..1] = resid_sq, norm_sq. */
+int slra_cur_residual_factored_cauchy(slra_ctx ctx, const double* d_x, const double* d_y, int64_t m, int64_t n,
+                                      const int64_t* d_I, int64_t k, const int64_t* d_J, int64_t l,
+                                      const double* d_Tsig, const double* d_Sr, int64_t r, double* d_out);
 /* cross_approx_batched over log-kernel blocks given by their points
  * (FunctionOracle, oracle.hpp:43-54; the config-5 recipe K_ij =
  * 0.5 log((p_i - q_j)^2), hss.cpp:47-55 pattern): the same C-A per block as

@@ -58,16 +58,34 @@ struct StreamResidualArgs {
   int64_t ldq;
   int inner;
   double* part;  // 2 per CTA
+  // Cauchy FunctionOracle (config 3: A_ij = 1/(x_i - y_j), one IEEE
+  // division): the A tiles are evaluated instead of loaded (null: dense)
+  const double* cx = nullptr;
+  const double* cy = nullptr;
 };
 
+template <bool CAU>
 __device__ __forceinline__ void rs_stage(const StreamResidualArgs& a, int64_t i0, int64_t j0, double* Vs,
                                          double* Ms) {
   using namespace rs;
   const int tid = threadIdx.x;
+  if constexpr (CAU) {
+    // evaluated A tile: the same values the materialised matrix holds
+#pragma unroll 4
+    for (int e = tid; e < TN * (TM / 2); e += NT) {
+      const int col = e / (TM / 2), ch = e % (TM / 2);
+      const int64_t r = i0 + 2 * ch, cc = j0 + col;
+      const bool cin = cc < a.n;
+      const double yc = cin ? __ldg(a.cy + cc) : 0.0;
+      const double v0 = (cin && r < a.m) ? __ddiv_rn(1.0, __dsub_rn(__ldg(a.cx + r), yc)) : 0.0;
+      const double v1 = (cin && r + 1 < a.m) ? __ddiv_rn(1.0, __dsub_rn(__ldg(a.cx + r + 1), yc)) : 0.0;
+      *reinterpret_cast<double2*>(Ms + col * LDM + 2 * ch) = make_double2(v0, v1);
+    }
+  }
   // A tile: TN columns x TM rows in 16-byte chunks of 2 rows (a column is
   // 2 KB contiguous in HBM)
 #pragma unroll 4
-  for (int e = tid; e < TN * (TM / 2); e += NT) {
+  for (int e = tid; e < (CAU ? 0 : TN * (TM / 2)); e += NT) {
     const int col = e / (TM / 2), ch = e % (TM / 2);
     const int64_t r = i0 + 2 * ch, cc = j0 + col;
     int bytes = 0;
@@ -93,7 +111,8 @@ __device__ __forceinline__ void rs_stage(const StreamResidualArgs& a, int64_t i0
   }
 }
 
-__global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidualArgs a) {
+template <bool CAU>
+__device__ __forceinline__ void residual_stream_body(const StreamResidualArgs& a) {
   using namespace rs;
   extern __shared__ __align__(16) double smem[];
 #define VB(s) (smem + (s) * V_D)
@@ -111,7 +130,7 @@ __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidu
 #pragma unroll
   for (int s = 0; s < NS - 1; ++s) {
     const int64_t t = t0 + s;
-    if (t < t1) rs_stage(a, (t / tiles_n) * TM, (t % tiles_n) * TN, VB(s), MB(s));
+    if (t < t1) rs_stage<CAU>(a, (t / tiles_n) * TM, (t % tiles_n) * TN, VB(s), MB(s));
     cp_async_commit();
   }
   double af[MI][2][8];  // [m16 block][k16 step][fragment]
@@ -162,7 +181,7 @@ __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidu
     {  // prefetch tile t + NS - 1 while the DMMAs above drain (issued after them in program order)
       const int64_t tp = t + NS - 1;
       const int sp = (slot + NS - 1) % NS;
-      if (tp < t1) rs_stage(a, (tp / tiles_n) * TM, (tp % tiles_n) * TN, VB(sp), MB(sp));
+      if (tp < t1) rs_stage<CAU>(a, (tp / tiles_n) * TM, (tp % tiles_n) * TN, VB(sp), MB(sp));
       cp_async_commit();
     }
     double r0 = 0.0, r1 = 0.0, n0 = 0.0, n1 = 0.0;  // short chains (FP64 FMA latency)
@@ -193,6 +212,13 @@ __global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidu
     a.part[2 * blockIdx.x] = rsum;
     a.part[2 * blockIdx.x + 1] = nsum;
   }
+}
+
+__global__ void __launch_bounds__(rs::NT, 2) residual_stream_kernel(StreamResidualArgs a) {
+  residual_stream_body<false>(a);
+}
+__global__ void __launch_bounds__(rs::NT, 2) cauchy_residual_stream_kernel(StreamResidualArgs a) {
+  residual_stream_body<true>(a);
 }
 
 __global__ void reduce_pairs2_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
@@ -226,6 +252,29 @@ int launch_residual_stream(Context* c, const double* A, int64_t lda, int64_t m, 
                        part};
   SLRA_CUDA(cudaFuncSetAttribute(residual_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs::SMEM));
   SLRA_TIMED(c, "residual", residual_stream_kernel<<<grid, rs::NT, rs::SMEM, c->stream>>>(a);)
+  SLRA_CHECK_LAUNCH(c);
+  SLRA_TIMED(c, "residual_reduce", reduce_pairs2_kernel<<<1, 256, 0, c->stream>>>(part, grid, d_out);)
+  SLRA_CHECK_LAUNCH(c);
+  return SLRA_OK;
+}
+
+// ||A - P Q||^2 and ||A||^2 for the Cauchy block A_ij = 1/(x_i - y_j) (m x n).
+int launch_residual_stream_cauchy(Context* c, const double* x, const double* y, int64_t m, int64_t n,
+                                  const double* P, int64_t ldp, const double* Q, int64_t ldq, int64_t inner,
+                                  double* d_out) {
+  const bool aligned = inner == 0 || (((uintptr_t)P % 16 == 0) && (ldp % 2 == 0) && ((uintptr_t)Q % 16 == 0) &&
+                                      (ldq % 2 == 0));
+  if (!aligned || inner > rs::KP || m < 1 || n < 1) return SLRA_ERR_UNSUPPORTED;
+  const int64_t tiles = ((m + rs::TM - 1) / rs::TM) * ((n + rs::TN - 1) / rs::TN);
+  int grid = 2 * c->num_sms;
+  if (tiles < grid) grid = (int)tiles;
+  double* part = partials(c, 2 * grid);
+  if (!part) return SLRA_ERR_CUDA;
+  StreamResidualArgs a{x, 2, m, n, inner ? P : x, inner ? ldp : 2, inner ? Q : x, inner ? ldq : 2, (int)inner, part,
+                       x, y};
+  SLRA_CUDA(cudaFuncSetAttribute(cauchy_residual_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)rs::SMEM));
+  SLRA_TIMED(c, "residual", cauchy_residual_stream_kernel<<<grid, rs::NT, rs::SMEM, c->stream>>>(a);)
   SLRA_CHECK_LAUNCH(c);
   SLRA_TIMED(c, "residual_reduce", reduce_pairs2_kernel<<<1, 256, 0, c->stream>>>(part, grid, d_out);)
   SLRA_CHECK_LAUNCH(c);

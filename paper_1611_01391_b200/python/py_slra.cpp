@@ -814,6 +814,25 @@ PYBIND11_MODULE(_slra, m) {
                                          ptr<double>(rs), ptr<double>(ns)),
           "cross_approx_batched_host");
   });
+  // config 3's Cauchy block as a FunctionOracle (points on the device)
+  m.def("cross_approx_cauchy_device", [](uintptr_t x, uintptr_t y, Index mm, Index n, Index r, Index k, Index l,
+                                         uintptr_t init_rows, int loops, double h, uintptr_t I, uintptr_t J,
+                                         uintptr_t U, uintptr_t Tsig, uintptr_t Sr) {
+    int64_t rr = 0;
+    check(slra_cross_approx_cauchy(device_context(), ptr<const double>(x), ptr<const double>(y), mm, n, r, k, l,
+                                   ptr<const int64_t>(init_rows), loops, h, ptr<int64_t>(I), ptr<int64_t>(J),
+                                   ptr<double>(U), nullptr, nullptr, nullptr, ptr<double>(Tsig), ptr<double>(Sr), &rr),
+          "cross_approx_cauchy");
+    return rr;
+  });
+  m.def("cur_residual_factored_cauchy_device", [](uintptr_t x, uintptr_t y, Index mm, Index n, uintptr_t I, Index k,
+                                                  uintptr_t J, Index l, uintptr_t Tsig, uintptr_t Sr, Index r,
+                                                  uintptr_t out) {
+    check(slra_cur_residual_factored_cauchy(device_context(), ptr<const double>(x), ptr<const double>(y), mm, n,
+                                            ptr<const int64_t>(I), k, ptr<const int64_t>(J), l,
+                                            ptr<const double>(Tsig), ptr<const double>(Sr), r, ptr<double>(out)),
+          "cur_residual_factored_cauchy");
+  });
   // the same over log-kernel blocks given by their points (FunctionOracle): device / host buffers
   m.def("cross_approx_batched_logkernel_device", [](uintptr_t px, uintptr_t py, uintptr_t qx, uintptr_t qy,
                                                     Index nblocks, Index mm, Index n, Index r, Index k, Index l,

@@ -668,3 +668,42 @@ def test_integration_glue_cross_approx_on_gpu(slra, oracle, tmp_path):
     assert [int(v) for v in lines["I"].split()] == o["I"]
     assert [int(v) for v in lines["J"].split()] == o["J"]
     assert int(lines["r"]) == 8 and int(lines["steps"]) == 6
+
+
+@pytest.mark.parametrize("n,k,loops", [(4096, 64, 2), (200, 16, 3)])
+def test_cauchy_function_oracle_bit_identical(n, k, loops):
+    """Config 3's block as a FunctionOracle (slra_cross_approx_cauchy +
+    slra_cur_residual_factored_cauchy, oracle.hpp:43-54): strips, generator
+    and the residual pass evaluate 1/(x_i - y_j) instead of reading the
+    materialised matrix — the same selections, nucleus factors and residual
+    bits as the dense entry points."""
+    import torch
+    import paper_1611_01391_b200 as slra
+    rng = slra.Rng(123)
+    x = torch.tensor([rng.uniform() for _ in range(n)], dtype=torch.float64, device="cuda")
+    y = torch.tensor([2.0 + rng.uniform() for _ in range(n)], dtype=torch.float64, device="cuda")
+    At = (1.0 / (x[None, :] - y[:, None])).contiguous()  # column-major A: At[j, i] = A(i, j)
+    init = torch.tensor(slra.Rng(7).distinct_indices(k, n), dtype=torch.int64, device="cuda")
+
+    def bufs():
+        return dict(I=torch.zeros(k, dtype=torch.int64, device="cuda"), J=torch.zeros(k, dtype=torch.int64,
+                                                                                       device="cuda"),
+                    U=torch.zeros(k * k, dtype=torch.float64, device="cuda"),
+                    T=torch.zeros(k * k, dtype=torch.float64, device="cuda"),
+                    S=torch.zeros(k * k, dtype=torch.float64, device="cuda"),
+                    out=torch.zeros(2, dtype=torch.float64, device="cuda"))
+    d, c = bufs(), bufs()
+    rd = slra.cross_approx_device(At.data_ptr(), n, n, n, 0, k, k, init.data_ptr(), loops, 1.1, d["I"].data_ptr(),
+                                  d["J"].data_ptr(), d["U"].data_ptr(), d["T"].data_ptr(), d["S"].data_ptr())
+    slra.cur_residual_factored_device(At.data_ptr(), n, n, n, d["I"].data_ptr(), k, d["J"].data_ptr(), k,
+                                      d["T"].data_ptr(), d["S"].data_ptr(), rd, d["out"].data_ptr())
+    rc = slra.cross_approx_cauchy_device(x.data_ptr(), y.data_ptr(), n, n, 0, k, k, init.data_ptr(), loops, 1.1,
+                                         c["I"].data_ptr(), c["J"].data_ptr(), c["U"].data_ptr(), c["T"].data_ptr(),
+                                         c["S"].data_ptr())
+    slra.cur_residual_factored_cauchy_device(x.data_ptr(), y.data_ptr(), n, n, c["I"].data_ptr(), k,
+                                             c["J"].data_ptr(), k, c["T"].data_ptr(), c["S"].data_ptr(), rc,
+                                             c["out"].data_ptr())
+    torch.cuda.synchronize()
+    assert rd == rc
+    for key in ("I", "J", "U", "T", "S", "out"):
+        assert torch.equal(d[key], c[key]), key
