@@ -900,10 +900,12 @@ class Config4:
     def step(self):
         s = self.slra
         if self.comm.world == 1:
-            for i, (_, p, d) in enumerate(self.plans):
-                self.sres[i] = s.sketch_solve_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(),
-                                                     d["src"].data_ptr(), d["coef"].data_ptr(), d["q"].data_ptr(),
-                                                     p["width"], p["tree"], K4, self.x[i].data_ptr())
+            # both samplers' solves side by side (slra_sketch_solve_batched: a cluster per sketch)
+            self.sres = s.sketch_solve_batched_device(
+                self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(), [d["src"].data_ptr() for _, _, d in self.plans],
+                [d["coef"].data_ptr() for _, _, d in self.plans], [d["q"].data_ptr() for _, _, d in self.plans],
+                [p["width"] for _, p, _ in self.plans], [p["tree"] for _, p, _ in self.plans], K4,
+                [x.data_ptr() for x in self.x])
             # residual_norm of both solutions in ONE pass over A (out[i, 0])
             s.lsr_residual_multi_device(self.At.data_ptr(), M4, M4, D4, self.b.data_ptr(), self.X.data_ptr(),
                                         len(self.plans), self.out.data_ptr())

@@ -411,6 +411,16 @@ int slra_sketch_solve(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, i
 /* The solve half of sketch_solve (lsr.cpp:52-60) for an already sketched
  * system FW = (FA | Fb), k x (d+1), ld k — the row-sharded path (config 4)
  * all-reduces the per-rank sketch contributions and then calls this. */
+/* sketch_solve (lsr.cpp:37-67) for nsk <= 4 sketches F_s of the same (A, b)
+ * — config 4's two samplers: the per-sketch gathers and Grams, then one
+ * launch of each cluster kernel solves all of them side by side (a cluster
+ * per sketch) with one host synchronisation; results identical to nsk
+ * separate slra_sketch_solve calls. Host arrays of device pointers (src,
+ * coef, q, x_hat) and of sizes; h_sketched_residual[s] (host, nullable). */
+int slra_sketch_solve_batched(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t d,
+                              const double* d_b, int nsk, const int64_t* const* d_src,
+                              const double* const* d_coef, const int32_t* const* d_q, const int64_t* width,
+                              const int* tree, int64_t k, double* const* d_x_hat, double* h_sketched_residual);
 int slra_lsr_solve_sketched(slra_ctx ctx, const double* d_FW, int64_t ldfw, int64_t k, int64_t d,
                             double* d_x_hat, double* h_sketched_residual);
 /* solve_exact (lsr.cpp:21-24): x = pinv(A) b, the minimum-norm least-squares

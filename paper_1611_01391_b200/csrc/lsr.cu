@@ -19,6 +19,8 @@
 //    x = P R^-1 (Q^T Fb). The same kernel (without the rank test) gives R
 //    and Q^T b for solve_exact's pseudo-inverse (lsr.cpp:21-24).
 // One host synchronisation at the end of the fast path (status, residual).
+#include <cstring>
+
 #include "common.cuh"
 
 namespace slra_dev {
@@ -605,6 +607,9 @@ int launch_gram_tn(Context* c, const char* fam, int64_t m, int64_t n, int64_t K,
 int launch_chol_cluster(Context* c, const double* Gw, int d, const double* FW, int64_t k, double tol_rel, double* x,
                         double* ws, double* out, int32_t* status);
 size_t lsr_cluster_ws_doubles(int d, int64_t k, int num_sms);
+int launch_chol_cluster_batched(Context* c, int nprob, const double* const* Gw, int d, const double* const* FW,
+                                int64_t k, double tol_rel, double* const* x, double* const* ws, double* const* out,
+                                int32_t* const* status);
 static int lsr_exact(Context* cx, const double* FW, int64_t k, int64_t d, double* x_hat, double* h_sketched_residual,
                      double* r, double* part, double* out, int rgrid);
 
@@ -782,6 +787,76 @@ int slra_sketch_solve(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int
   SLRA_TRY(launch_sketch_rows(cx, A, lda, d, src, coef, q, width, tree, k, FW, k));
   SLRA_TRY(launch_sketch_rows(cx, b, m, 1, src, coef, q, width, tree, k, FW + (size_t)k * d, k));
   return lsr_solve(cx, nullptr, k, d, x_hat, h_sketched_residual, nullptr);
+}
+
+// sketch_solve (lsr.cpp:37-67) for nsk <= 4 sketches F_s of the same (A, b)
+// (config 4's two samplers): every F_s (A | b) gathered, every augmented
+// Gram formed, then ONE launch of each cluster kernel runs all the solves
+// side by side (a cluster per sketch) and one host synchronisation reads all
+// statuses; a sketch that needs the reference's ColPivQR path takes it
+// afterwards, alone. Same kernels and data as nsk separate calls, so the same
+// bits (tests/test_gpu_config4.py).
+int slra_sketch_solve_batched(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_t d, const double* b,
+                              int nsk, const int64_t* const* src, const double* const* coef,
+                              const int32_t* const* q, const int64_t* width, const int* tree, int64_t k,
+                              double* const* x_hat, double* h_sketched_residual) {
+  if (!ctx || lda < m || m <= d || d < 1 || k <= d || nsk < 1) return SLRA_ERR_INVALID_ARGUMENT;
+  if (d > 256 || k > ((int64_t)1 << 16) || nsk > 4) {
+    for (int s = 0; s < nsk; ++s)
+      SLRA_TRY(slra_sketch_solve(ctx, A, lda, m, d, b, src[s], coef[s], q[s], width[s], tree[s], k, x_hat[s],
+                                 h_sketched_residual ? h_sketched_residual + s : nullptr));
+    return SLRA_OK;
+  }
+  Context* cx = C(ctx);
+  cudaStream_t st = cx->stream;
+  const int64_t dc = d + 1;
+  const int rgrid = (int)((k + 31) / 32);
+  // per sketch: FW (k x dc) | Gw (dc x dc) | r (k) | part (rgrid) | out (16) | cluster ws (+2 for alignment)
+  const size_t wsd = lsr_cluster_ws_doubles((int)d, k, cx->num_sms) + 2;
+  const size_t per = ((size_t)k * dc + (size_t)dc * dc + (size_t)k + rgrid + 16 + wsd + 1) & ~(size_t)1;
+  double* base = static_cast<double*>(arena(cx, 2, sizeof(double) * per * nsk + 64));
+  if (!base) return SLRA_ERR_CUDA;
+  const double* FWc[4];
+  const double* Gwc[4];
+  double *FW[4], *Gw[4], *r[4], *part[4], *out[4], *lws[4];
+  int32_t* stt[4];
+  for (int s = 0; s < nsk; ++s) {
+    double* p0 = base + per * s;
+    FW[s] = p0;
+    Gw[s] = FW[s] + (size_t)k * dc;
+    r[s] = Gw[s] + (size_t)dc * dc;
+    part[s] = r[s] + k;
+    out[s] = part[s] + rgrid;
+    lws[s] = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(out[s] + 16) + 15) & ~(uintptr_t)15);
+    stt[s] = static_cast<int32_t*>(cx->dsmall) + 2 * s;
+    FWc[s] = FW[s];
+    Gwc[s] = Gw[s];
+    SLRA_TRY(launch_sketch_rows(cx, A, lda, d, src[s], coef[s], q[s], width[s], tree[s], k, FW[s], k));
+    SLRA_TRY(launch_sketch_rows(cx, b, m, 1, src[s], coef[s], q[s], width[s], tree[s], k, FW[s] + (size_t)k * d, k));
+    int gs = launch_gram_tn(cx, "gemm", dc, dc, k, 1.0, FW[s], k, FW[s], k, 0.0, Gw[s], dc, 1);
+    if (gs == SLRA_ERR_UNSUPPORTED) gs = launch_gemm(cx, 1, 0, dc, dc, k, 1.0, FW[s], k, FW[s], k, 0.0, Gw[s], dc);
+    SLRA_TRY(gs);
+  }
+  SLRA_TRY(launch_chol_cluster_batched(cx, nsk, Gwc, (int)d, FWc, k, 1e-20, x_hat, lws, out, stt));
+  double* hs = static_cast<double*>(cx->hsmall);  // [0..3] residuals, then the statuses
+  for (int s = 0; s < nsk; ++s) SLRA_CUDA(cudaMemcpyAsync(hs + s, out[s], 8, cudaMemcpyDeviceToHost, st));
+  SLRA_CUDA(cudaMemcpyAsync(hs + 4, cx->dsmall, 8 * nsk, cudaMemcpyDeviceToHost, st));
+  SLRA_CUDA(cudaStreamSynchronize(st));
+  double res[4];
+  int32_t sts[8];
+  for (int s = 0; s < nsk; ++s) res[s] = hs[s];
+  std::memcpy(sts, hs + 4, 8 * nsk);
+  for (int s = 0; s < nsk; ++s) {
+    if (sts[2 * s] == 0 && sts[2 * s + 1] == 0) {
+      if (h_sketched_residual) h_sketched_residual[s] = sqrt(res[s]);
+      continue;
+    }
+    // the reference's ColPivHouseholderQR, its rank rule, its solve
+    double one = 0.0;
+    SLRA_TRY(lsr_exact(cx, FW[s], k, d, x_hat[s], &one, r[s], part[s], out[s], rgrid));
+    if (h_sketched_residual) h_sketched_residual[s] = one;
+  }
+  return SLRA_OK;
 }
 
 int slra_lsr_solve_sketched(slra_ctx ctx, const double* FW, int64_t ldfw, int64_t k, int64_t d, double* x_hat,

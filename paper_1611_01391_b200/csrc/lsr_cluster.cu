@@ -267,6 +267,13 @@ struct CholArgs {
   double* out;      // [0] sketched residual^2
   int32_t* status;  // [0] rank failure, [1] ill-conditioned (-> exact path)
 };
+// up to kMaxProb independent solves in one launch of each kernel (config 4's
+// two samplers): cluster b / NC (K1, K3) or grid row blockIdx.y (K2) takes
+// problem p[b]; the clusters run side by side on different SMs
+constexpr int kMaxProb = 4;
+struct CholArgsN {
+  CholArgs p[kMaxProb];
+};
 
 // lane i of the calling warp ends with y_i of L11 y = t (FWD) or
 // L11^T y = t: the 32-step shuffle chain (used to form D_p).
@@ -491,8 +498,9 @@ __device__ __forceinline__ void backward_step(cg::cluster_group& cl, const doubl
   }
 }
 
-__global__ void __cluster_dims__(cc::NC, 1, 1) __launch_bounds__(cc::NT, 1) chol_cluster_kernel(CholArgs a) {
+__global__ void __cluster_dims__(cc::NC, 1, 1) __launch_bounds__(cc::NT, 1) chol_cluster_kernel(CholArgsN args) {
   using namespace cc;
+  const CholArgs a = args.p[blockIdx.x / NC];
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
   const int q = (int)cl.block_rank();
@@ -665,9 +673,14 @@ __global__ void __cluster_dims__(cc::NC, 1, 1) __launch_bounds__(cc::NT, 1) chol
 
 // ---- r0 = Fb - FA x0 and per-CTA partials of c = FA^T r0, ||r0||^2 (K2)
 constexpr int kRC = 32;  // rows per chunk
-__global__ void __launch_bounds__(256) lsq_refine_kernel(const double* __restrict__ FW, int64_t k, int d,
-                                                         const double* __restrict__ x, const int32_t* __restrict__ status,
-                                                         double* __restrict__ part) {
+__global__ void __launch_bounds__(256) lsq_refine_kernel(CholArgsN args) {
+  const CholArgs& pa = args.p[blockIdx.y];
+  const double* __restrict__ FW = pa.FW;
+  const int64_t k = pa.k;
+  const int d = pa.d;
+  const double* __restrict__ x = pa.x;
+  const int32_t* __restrict__ status = pa.status;
+  double* __restrict__ part = const_cast<double*>(pa.part);
   extern __shared__ double sm2[];
   double* xs = sm2;                   // d
   double* Ch = sm2 + d + 1;           // (d + 1) x (kRC + 1)
@@ -738,8 +751,9 @@ __global__ void __launch_bounds__(256) lsq_refine_kernel(const double* __restric
 }
 
 // ---- G delta = c on the cluster, x = x0 + delta (K3)
-__global__ void __cluster_dims__(cc::NC, 1, 1) __launch_bounds__(cc::NT, 1) chol_refine_kernel(CholArgs a) {
+__global__ void __cluster_dims__(cc::NC, 1, 1) __launch_bounds__(cc::NT, 1) chol_refine_kernel(CholArgsN args) {
   using namespace cc;
+  const CholArgs a = args.p[blockIdx.x / NC];
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
   if (a.status[0] | a.status[1]) return;  // uniform over the cluster (status is final)
@@ -858,26 +872,38 @@ size_t lsr_cluster_ws_doubles(int d, int64_t k, int num_sms) {
   return (size_t)np * cc::PANEL + (size_t)np * cc::PW * cc::LDD + (size_t)nparts * (d + 1) + 64;
 }
 
-int launch_chol_cluster(Context* c, const double* Gw, int d, const double* FW, int64_t k, double tol_rel, double* x,
-                        double* ws, double* out, int32_t* status) {
+// K1 + K2 + K3 for nprob <= kMaxProb independent solves of the same d and
+// k (one launch each). Per problem: Gw, FW, x, ws (lsr_cluster_ws_doubles),
+// out, status.
+int launch_chol_cluster_batched(Context* c, int nprob, const double* const* Gw, int d, const double* const* FW,
+                                int64_t k, double tol_rel, double* const* x, double* const* ws, double* const* out,
+                                int32_t* const* status) {
   using namespace cc;
-  if (d < 1 || d > NC * PW) return SLRA_ERR_UNSUPPORTED;
+  if (d < 1 || d > NC * PW || nprob < 1 || nprob > kMaxProb) return SLRA_ERR_UNSUPPORTED;
   const int np = (d + PW - 1) / PW;
   int nparts = (int)((k + kRC - 1) / kRC);
   if (nparts > 2 * c->num_sms) nparts = 2 * c->num_sms;
-  double* part = ws + (size_t)np * PANEL + (size_t)np * PW * LDD;
-  CholArgs a{Gw, d, FW, k, tol_rel, x, ws, part, nparts, out, status};
+  CholArgsN args{};
+  for (int b = 0; b < nprob; ++b) {
+    double* part = ws[b] + (size_t)np * PANEL + (size_t)np * PW * LDD;
+    args.p[b] = CholArgs{Gw[b], d, FW[b], k, tol_rel, x[b], ws[b], part, nparts, out[b], status[b]};
+  }
   SLRA_CUDA(cudaFuncSetAttribute(chol_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-  SLRA_TIMED(c, "lsr_solve", chol_cluster_kernel<<<NC, NT, SMEM, c->stream>>>(a);)
+  SLRA_TIMED(c, "lsr_solve", chol_cluster_kernel<<<NC * nprob, NT, SMEM, c->stream>>>(args);)
   SLRA_CHECK_LAUNCH(c);
   const size_t sm2 = sizeof(double) * ((size_t)d + 1 + (size_t)(d + 1) * (kRC + 1));
   SLRA_CUDA(cudaFuncSetAttribute(lsq_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-  SLRA_TIMED(c, "lsr_solve", lsq_refine_kernel<<<nparts, 256, sm2, c->stream>>>(FW, k, d, x, status, part);)
+  SLRA_TIMED(c, "lsr_solve", lsq_refine_kernel<<<dim3(nparts, nprob), 256, sm2, c->stream>>>(args);)
   SLRA_CHECK_LAUNCH(c);
   SLRA_CUDA(cudaFuncSetAttribute(chol_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_REFINE));
-  SLRA_TIMED(c, "lsr_solve", chol_refine_kernel<<<NC, NT, SMEM_REFINE, c->stream>>>(a);)
+  SLRA_TIMED(c, "lsr_solve", chol_refine_kernel<<<NC * nprob, NT, SMEM_REFINE, c->stream>>>(args);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
+}
+
+int launch_chol_cluster(Context* c, const double* Gw, int d, const double* FW, int64_t k, double tol_rel, double* x,
+                        double* ws, double* out, int32_t* status) {
+  return launch_chol_cluster_batched(c, 1, &Gw, d, &FW, k, tol_rel, &x, &ws, &out, &status);
 }
 
 }  // namespace slra_dev

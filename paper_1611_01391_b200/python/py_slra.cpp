@@ -949,6 +949,31 @@ PYBIND11_MODULE(_slra, m) {
                             ptr<double>(out)),
           "lsr_residual");
   });
+  m.def("sketch_solve_batched_device", [](uintptr_t A, Index lda, Index mm, Index d, uintptr_t b,
+                                          const std::vector<uintptr_t>& src, const std::vector<uintptr_t>& coef,
+                                          const std::vector<uintptr_t>& q, const std::vector<int64_t>& width,
+                                          const std::vector<int>& tree, Index k, const std::vector<uintptr_t>& x) {
+    const int nsk = (int)src.size();
+    if ((int)coef.size() != nsk || (int)q.size() != nsk || (int)width.size() != nsk || (int)tree.size() != nsk ||
+        (int)x.size() != nsk)
+      throw std::invalid_argument("sketch_solve_batched: list lengths differ");
+    std::vector<const int64_t*> ps(nsk);
+    std::vector<const double*> pc(nsk);
+    std::vector<const int32_t*> pq(nsk);
+    std::vector<double*> px(nsk);
+    for (int s = 0; s < nsk; ++s) {
+      ps[s] = ptr<const int64_t>(src[s]);
+      pc[s] = ptr<const double>(coef[s]);
+      pq[s] = ptr<const int32_t>(q[s]);
+      px[s] = ptr<double>(x[s]);
+    }
+    std::vector<double> res(nsk, 0.0);
+    check(slra_sketch_solve_batched(device_context(), ptr<const double>(A), lda, mm, d, ptr<const double>(b), nsk,
+                                    ps.data(), pc.data(), pq.data(), width.data(), tree.data(), k, px.data(),
+                                    res.data()),
+          "sketch_solve_batched");
+    return res;
+  });
   m.def("lsr_residual_multi_device", [](uintptr_t A, Index lda, Index mm, Index d, uintptr_t b, uintptr_t X,
                                         Index nx, uintptr_t out) {
     check(slra_lsr_residual_multi(device_context(), ptr<double>(A), lda, mm, d, ptr<double>(b), ptr<double>(X), nx,

@@ -191,3 +191,39 @@ def test_residual_multi_matches_single(slra):
             assert out[s].item() == one.item()
             ref = torch.linalg.vector_norm(A.T @ X[s] - b).item() ** 2
             assert abs(out[s].item() - ref) <= 1e-12 * ref
+
+
+def test_sketch_solve_batched_matches_separate_calls(slra):
+    """slra_sketch_solve_batched (a cluster per sketch, one launch) gives the
+    bits of separate slra_sketch_solve calls, for the config-4 sampler kinds
+    and for a sketch that takes the exact (ColPivQR) path."""
+    import torch
+    rng = np.random.default_rng(31)
+    m, d, k = 40000, 96, 1024
+    A = np.asfortranarray(rng.standard_normal((m, d)))
+    A[:, 7] = A[:, 3] + 1e-9 * rng.standard_normal(m)  # near-dependent pair: the exact path for every sketch
+    for near in (False, True):
+        Ause = A if near else np.asfortranarray(rng.standard_normal((m, d)))
+        b = Ause @ rng.standard_normal(d) + 1e-3 * rng.standard_normal(m)
+        At = torch.from_numpy(Ause.T.copy()).cuda()
+        bd = torch.from_numpy(b).cuda()
+        plans = []
+        for F in (slra.make_sub_identity(slra.Rng(5).distinct_indices(k, m), m),
+                  slra.make_product([slra.make_sub_identity(slra.Rng(6).distinct_indices(k, m), m),
+                                     slra.gen_sparse_circulant(m, 2, slra.Rng(7)), slra.gen_sign_diagonal(m, slra.Rng(8))])):
+            p = F.plan("left")
+            plans.append((p, torch.tensor(p["src"], dtype=torch.int64, device="cuda"),
+                          torch.tensor(p["coef"], dtype=torch.float64, device="cuda"),
+                          torch.tensor(p["q"], dtype=torch.int32, device="cuda")))
+        xs = [torch.zeros(d, dtype=torch.float64, device="cuda") for _ in plans]
+        xb = [torch.zeros(d, dtype=torch.float64, device="cuda") for _ in plans]
+        sep = [slra.sketch_solve_device(At.data_ptr(), m, m, d, bd.data_ptr(), s.data_ptr(), c.data_ptr(), q.data_ptr(),
+                                        p["width"], p["tree"], k, x.data_ptr()) for (p, s, c, q), x in zip(plans, xs)]
+        bat = slra.sketch_solve_batched_device(At.data_ptr(), m, m, d, bd.data_ptr(), [s.data_ptr() for _, s, _, _ in plans],
+                                               [c.data_ptr() for _, _, c, _ in plans], [q.data_ptr() for *_, q in plans],
+                                               [p["width"] for p, *_ in plans], [p["tree"] for p, *_ in plans], k,
+                                               [x.data_ptr() for x in xb])
+        torch.cuda.synchronize()
+        assert list(sep) == list(bat)
+        for a_, b_ in zip(xs, xb):
+            assert torch.equal(a_, b_)
