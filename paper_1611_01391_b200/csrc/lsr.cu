@@ -607,6 +607,9 @@ int launch_gram_tn(Context* c, const char* fam, int64_t m, int64_t n, int64_t K,
 int launch_chol_cluster(Context* c, const double* Gw, int d, const double* FW, int64_t k, double tol_rel, double* x,
                         double* ws, double* out, int32_t* status);
 size_t lsr_cluster_ws_doubles(int d, int64_t k, int num_sms);
+int launch_gram_tn_batched(Context* c, const char* fam, int nb, int64_t m, int64_t n, int64_t K, double alpha,
+                           const double* X, int64_t ldx, int64_t sX, const double* Y, int64_t ldy, int64_t sY,
+                           double beta, double* Cm, int64_t ldc, int64_t sC, int lower);
 int launch_chol_cluster_batched(Context* c, int nprob, const double* const* Gw, int d, const double* const* FW,
                                 int64_t k, double tol_rel, double* const* x, double* const* ws, double* const* out,
                                 int32_t* const* status);
@@ -833,10 +836,16 @@ int slra_sketch_solve_batched(slra_ctx ctx, const double* A, int64_t lda, int64_
     Gwc[s] = Gw[s];
     SLRA_TRY(launch_sketch_rows(cx, A, lda, d, src[s], coef[s], q[s], width[s], tree[s], k, FW[s], k));
     SLRA_TRY(launch_sketch_rows(cx, b, m, 1, src[s], coef[s], q[s], width[s], tree[s], k, FW[s] + (size_t)k * d, k));
-    int gs = launch_gram_tn(cx, "gemm", dc, dc, k, 1.0, FW[s], k, FW[s], k, 0.0, Gw[s], dc, 1);
-    if (gs == SLRA_ERR_UNSUPPORTED) gs = launch_gemm(cx, 1, 0, dc, dc, k, 1.0, FW[s], k, FW[s], k, 0.0, Gw[s], dc);
-    SLRA_TRY(gs);
   }
+  // every sketch's augmented Gram in one launch (the sketches sit `per` apart)
+  int gs = launch_gram_tn_batched(cx, "gemm", nsk, dc, dc, k, 1.0, FW[0], k, (int64_t)per, FW[0], k, (int64_t)per, 0.0,
+                                  Gw[0], dc, (int64_t)per, 1);
+  for (int s = 0; s < nsk && gs == SLRA_ERR_UNSUPPORTED; ++s) {
+    const int g1 = launch_gemm(cx, 1, 0, dc, dc, k, 1.0, FW[s], k, FW[s], k, 0.0, Gw[s], dc);
+    if (g1 != SLRA_OK) return g1;
+    if (s == nsk - 1) gs = SLRA_OK;
+  }
+  SLRA_TRY(gs);
   SLRA_TRY(launch_chol_cluster_batched(cx, nsk, Gwc, (int)d, FWc, k, 1e-20, x_hat, lws, out, stt));
   double* hs = static_cast<double*>(cx->hsmall);  // [0..3] residuals, then the statuses
   for (int s = 0; s < nsk; ++s) SLRA_CUDA(cudaMemcpyAsync(hs + s, out[s], 8, cudaMemcpyDeviceToHost, st));

@@ -76,6 +76,8 @@ struct GramArgs {
   int tiles_n, ntiles;
   int64_t kchunk;  // rows of K per z-slice (multiple of BK)
   double* part;    // [z][tile][BM * BN] partial tiles
+  // batched problems (blockIdx.z): X, Y, part, C advance by these strides
+  int64_t sX = 0, sY = 0, sP = 0, sC = 0;
 };
 
 __device__ __forceinline__ void gt_cp16(double* smem, const double* g, int bytes) {
@@ -125,6 +127,9 @@ __device__ __forceinline__ void gt_stage(const GramArgs& a, int64_t i0, int64_t 
 __global__ void __launch_bounds__(gt::NT, 2) gram_tn_kernel(GramArgs a) {
   using namespace gt;
   extern __shared__ __align__(16) double sm[];
+  a.X += blockIdx.z * a.sX;
+  a.Y += blockIdx.z * a.sY;
+  a.part += blockIdx.z * a.sP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;  // 32 x 16 per warp
@@ -181,6 +186,8 @@ __global__ void __launch_bounds__(gt::NT, 2) gram_tn_kernel(GramArgs a) {
 __global__ void gram_combine_kernel(GramArgs a, int nz, double alpha, double beta, double* __restrict__ Cm,
                                     int64_t ldc) {
   using namespace gt;
+  a.part += blockIdx.y * a.sP;
+  Cm += blockIdx.y * a.sC;
   const int64_t total = (int64_t)a.ntiles * BM * BN;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int t = (int)(e / (BM * BN)), w = (int)(e % (BM * BN));
@@ -196,33 +203,50 @@ __global__ void gram_combine_kernel(GramArgs a, int nz, double alpha, double bet
   }
 }
 
+int launch_gram_tn_batched(Context* c, const char* fam, int nb, int64_t m, int64_t n, int64_t K, double alpha,
+                           const double* X, int64_t ldx, int64_t sX, const double* Y, int64_t ldy, int64_t sY,
+                           double beta, double* Cm, int64_t ldc, int64_t sC, int lower);
+
 // C = alpha X^T Y + beta C (lower = 1: X == Y, only the lower triangle's
 // tiles — every entry on or below the diagonal — are written).
 // SLRA_ERR_UNSUPPORTED when the operands are not 16-byte aligned.
 int launch_gram_tn(Context* c, const char* fam, int64_t m, int64_t n, int64_t K, double alpha, const double* X,
                    int64_t ldx, const double* Y, int64_t ldy, double beta, double* Cm, int64_t ldc, int lower) {
+  return launch_gram_tn_batched(c, fam, 1, m, n, K, alpha, X, ldx, 0, Y, ldy, 0, beta, Cm, ldc, 0, lower);
+}
+
+// nb products of the same shape at fixed strides in one launch (grid z)
+int launch_gram_tn_batched(Context* c, const char* fam, int nb, int64_t m, int64_t n, int64_t K, double alpha,
+                           const double* X, int64_t ldx, int64_t sX, const double* Y, int64_t ldy, int64_t sY,
+                           double beta, double* Cm, int64_t ldc, int64_t sC, int lower) {
   using namespace gt;
-  if (m == 0 || n == 0) return SLRA_OK;
-  const bool aligned = ((uintptr_t)X % 16 == 0) && (ldx % 2 == 0) && ((uintptr_t)Y % 16 == 0) && (ldy % 2 == 0);
+  if (m == 0 || n == 0 || nb == 0) return SLRA_OK;
+  const bool aligned = ((uintptr_t)X % 16 == 0) && (ldx % 2 == 0) && ((uintptr_t)Y % 16 == 0) && (ldy % 2 == 0) &&
+                       (sX % 2 == 0) && (sY % 2 == 0);
   if (!aligned || K < 1) return SLRA_ERR_UNSUPPORTED;
   const int tm = ceil_div(m, BM), tn_ = ceil_div(n, BN);
   const int ntiles = lower ? tm * (tm + 1) / 2 : tm * tn_;
   // split K so that the grid fills about two CTAs per SM, >= 4 k-steps each
   const int64_t ksteps = (K + BK - 1) / BK;
-  int64_t nz = (2 * (int64_t)c->num_sms + ntiles - 1) / ntiles;
+  int64_t nz = (2 * (int64_t)c->num_sms + (int64_t)ntiles * nb - 1) / ((int64_t)ntiles * nb);
   if (nz > ksteps / 4) nz = ksteps / 4;
   if (nz < 1) nz = 1;
   const int64_t kchunk = (ksteps + nz - 1) / nz * BK;
   nz = (K + kchunk - 1) / kchunk;
-  double* part = static_cast<double*>(workspace(c, sizeof(double) * nz * ntiles * BM * BN));
+  const int64_t per = nz * ntiles * BM * BN;
+  double* part = static_cast<double*>(workspace(c, sizeof(double) * per * nb));
   if (!part) return SLRA_ERR_CUDA;
   GramArgs a{X, ldx, Y, ldy, m, n, K, lower, tn_, ntiles, kchunk, part};
+  a.sX = sX;
+  a.sY = sY;
+  a.sP = per;
+  a.sC = sC;
   SLRA_CUDA(cudaFuncSetAttribute(gram_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-  SLRA_TIMED(c, fam, gram_tn_kernel<<<dim3(ntiles, (unsigned)nz), NT, SMEM, c->stream>>>(a);)
+  SLRA_TIMED(c, fam, gram_tn_kernel<<<dim3(ntiles, (unsigned)nz, nb), NT, SMEM, c->stream>>>(a);)
   SLRA_CHECK_LAUNCH(c);
   int rg = ceil_div((int64_t)ntiles * BM * BN, 256);
   if (rg > c->num_sms * 4) rg = c->num_sms * 4;
-  SLRA_TIMED(c, "gemm_reduce", gram_combine_kernel<<<rg, 256, 0, c->stream>>>(a, (int)nz, alpha, beta, Cm, ldc);)
+  SLRA_TIMED(c, "gemm_reduce", gram_combine_kernel<<<dim3(rg, nb), 256, 0, c->stream>>>(a, (int)nz, alpha, beta, Cm, ldc);)
   SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }
