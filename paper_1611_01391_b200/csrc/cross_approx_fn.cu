@@ -72,7 +72,7 @@ struct DenseEntries {
   int64_t lda;
   __device__ __forceinline__ double get(int i, int j) const { return __ldg(A + i + (int64_t)j * lda); }
 };
-__device__ __forceinline__ double log_kernel_entry(double pxi, double pyi, double qxj, double qyj) {
+__device__ __noinline__ double log_kernel_entry(double pxi, double pyi, double qxj, double qyj) {
   const double dx = __dsub_rn(pxi, qxj);
   const double dy = __dsub_rn(pyi, qyj);
   return 0.5 * log(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
