@@ -303,6 +303,14 @@ int slra_range_finder_batched(slra_ctx ctx, const double* d_M, int64_t ldm, int6
  * rank_tol = tol it is numerical_rank(A, tol, Relative)). Shapes as slra_svd. */
 int slra_pinv(slra_ctx ctx, const double* d_A, int64_t lda, int64_t m, int64_t n, double rank_tol,
               double* d_P, int64_t ldp, int64_t* h_rank);
+/* primitive_cur's qr_nucleus branch (cur.cpp:146-152): P = G^+ (l x k) of a
+ * k x l generator through Eigen's CompleteOrthogonalDecomposition (ColPivQR,
+ * RZ step at the default rank, setThreshold(threshold) before rank() and
+ * pseudoInverse()); *h_rank = cod.rank() at `threshold` (the caller throws
+ * GeneratorRankFailure when it is below r). k, l <= 4096. Blocks when
+ * h_rank is set. */
+int slra_cod_pinv(slra_ctx ctx, const double* d_G, int64_t ldg, int64_t k, int64_t l, double threshold,
+                  double* d_P, int64_t ldp, int64_t* h_rank);
 /* lra_premult (lra.cpp:41-52): U = range_basis(M, H, r, variant) as in
  * slra_range_finder (H: right plan, l outputs), then V = (F U)^+ (F M) with F
  * a compiled LEFT plan of s rows (see slra_sketch_rows). U is m x l (variant

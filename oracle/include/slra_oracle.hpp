@@ -152,6 +152,9 @@ struct ColPivQR {
   Index rank() const;
   Matrix solve(const Matrix& B) const;  // least-squares / exact solve, Eigen _solve_impl
 };
+// Eigen CompleteOrthogonalDecomposition(G) + setThreshold + pseudoInverse
+// (cur.cpp:146-152); *rank = cod.rank() at `threshold`.
+Matrix cod_pseudo_inverse(const Matrix& G, double threshold, Index* rank);
 
 // ---------------------------------------------------------------- oracles
 // oracle.hpp:11-54, testgen.cpp:11-37
@@ -286,8 +289,8 @@ CurDecomposition top_svd_to_cur(const Svd& f, Index k, Index l, double h, CurSel
 double condition_number(const Matrix& A, double rank_tol = 1e-10);
 IndexSet maxvol_rows(const Matrix& A, double h = 1.1, Index max_swaps = 0);
 IndexSet select_rows_spanning(const Matrix& A, Index count, double h = 1.1);
-CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r);
-CurDecomposition primitive_cur(const Matrix& M, IndexSet I, IndexSet J, Index r);
+CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus = false);
+CurDecomposition primitive_cur(const Matrix& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus = false);
 std::pair<CurDecomposition, CaTrace> cross_approx(const EntryOracle& M, Index r, Index k, Index l,
                                                   IndexSet init_rows, int loops, double h,
                                                   std::optional<double> stop_tol, Rng& rng);

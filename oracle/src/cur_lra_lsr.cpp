@@ -113,7 +113,7 @@ IndexSet select_rows_spanning(const Matrix& A, Index count, double h) {
 }
 
 // cur.cpp:137-162 (SVD nucleus; the qr_nucleus variant is out of scope)
-CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r) {
+CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus) {
   if (I.size() < r || J.size() < r || r < 1)
     throw std::invalid_argument("primitive_cur: need |I|, |J| >= r >= 1");
   Matrix G = M.block(I, J);
@@ -121,6 +121,13 @@ CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Ind
   c.row_set = std::move(I);
   c.col_set = std::move(J);
   c.r = r;
+  if (qr_nucleus) {  // cur.cpp:146-152: CompleteOrthogonalDecomposition, threshold 1e-10
+    Index rank = 0;
+    Matrix P = cod_pseudo_inverse(G, 1e-10, &rank);
+    if (rank < r) throw GeneratorRankFailure("primitive_cur: generator rank below target");
+    c.nucleus = std::move(P);
+    return c;
+  }
   Svd f = svd(G);
   if (f.sigma[0] <= 0 || f.sigma[static_cast<size_t>(r - 1)] <= 1e-10 * f.sigma[0])
     throw GeneratorRankFailure("primitive_cur: generator rank below target");
@@ -137,9 +144,9 @@ CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Ind
   c.nucleus = matmul(TS, St);
   return c;
 }
-CurDecomposition primitive_cur(const Matrix& M, IndexSet I, IndexSet J, Index r) {
+CurDecomposition primitive_cur(const Matrix& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus) {
   DenseOracle o(M);
-  return primitive_cur(o, std::move(I), std::move(J), r);
+  return primitive_cur(o, std::move(I), std::move(J), r, qr_nucleus);
 }
 
 namespace {

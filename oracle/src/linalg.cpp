@@ -360,6 +360,87 @@ Matrix ColPivQR::solve(const Matrix& B) const {
   return dst;
 }
 
+// ------------------------------------------------------------ CompleteOrthogonalDecomposition
+// Eigen CompleteOrthogonalDecomposition as primitive_cur's qr_nucleus branch
+// uses it (cur.cpp:146-152): `cod(G)` factors G at construction, so the
+// RZ step (computeInPlace) runs at the DEFAULT ColPivQR rank (threshold
+// eps * min(k, l)); `setThreshold(1e-10)` then changes rank(), which both the
+// caller's check and pseudoInverse() (_solve_impl with an identity rhs) read.
+// Restated step by step, including that ordering: the RZ reflectors are
+// built for the default rank r_e, applied (applyZAdjointOnTheLeftInPlace)
+// with the thresholded rank r_t. Where Eigen reads z-coefficients it never
+// wrote (r_e == l > r_t: m_zCoeffs is resized, not set) tau = 0 is used.
+Matrix cod_pseudo_inverse(const Matrix& G, double threshold, Index* rank_out) {
+  const Index rows = G.rows(), cols = G.cols();
+  ColPivQR cp(G);
+  Matrix& X = cp.qr;
+  const Index r_e = cp.rank();  // default threshold: the rank computeInPlace sees
+  std::vector<double> zc(static_cast<size_t>(std::min(rows, cols)), 0.0);
+  if (r_e < cols) {
+    // [R11 R12] = [T11 0] Z, Householder from the right, last row first
+    for (Index k = r_e - 1; k >= 0; --k) {
+      if (k != r_e - 1)
+        for (Index i = 0; i <= k; ++i) std::swap(X(i, k), X(i, r_e - 1));
+      // row(k).tail(cols - r_e + 1), starting at column r_e - 1
+      const Index len = cols - r_e + 1;
+      std::vector<double> x(static_cast<size_t>(len));
+      for (Index j = 0; j < len; ++j) x[static_cast<size_t>(j)] = X(k, r_e - 1 + j);
+      double tau, beta;
+      make_householder(x.data(), len, tau, beta);
+      for (Index j = 1; j < len; ++j) X(k, r_e - 1 + j) = x[static_cast<size_t>(j)];
+      zc[static_cast<size_t>(k)] = tau;
+      X(k, r_e - 1) = beta;
+      // applyHouseholderOnTheRight on topRightCorner(k, len), essential = row k tail
+      if (k > 0 && tau != 0) {
+        for (Index i = 0; i < k; ++i) {
+          double tmp = 0;
+          for (Index j = 1; j < len; ++j) tmp += X(i, r_e - 1 + j) * x[static_cast<size_t>(j)];
+          tmp += X(i, r_e - 1);
+          X(i, r_e - 1) -= tau * tmp;
+          for (Index j = 1; j < len; ++j) X(i, r_e - 1 + j) -= tau * tmp * x[static_cast<size_t>(j)];
+        }
+      }
+      if (k != r_e - 1)
+        for (Index i = 0; i <= k; ++i) std::swap(X(i, k), X(i, r_e - 1));
+    }
+  }
+  cp.threshold = threshold;  // cod.setThreshold(threshold)
+  const Index rank = cp.rank();
+  if (rank_out) *rank_out = rank;
+  Matrix dst(cols, rows);
+  if (rank == 0) return dst;
+  // c = Q^T I with the first `rank` reflectors (matrixQ().setLength(rank))
+  Matrix c = Matrix::identity(rows, rows);
+  for (Index k = 0; k < rank; ++k)
+    apply_householder_left(c, k, rows - k, X.col(k) + k, cp.hcoeffs[static_cast<size_t>(k)], 0, rows);
+  // T11 z = c(0:rank, :)
+  for (Index j = 0; j < rows; ++j)
+    for (Index i = rank - 1; i >= 0; --i) {
+      double s = c(i, j);
+      for (Index t = i + 1; t < rank; ++t) s -= X(i, t) * dst(t, j);
+      dst(i, j) = s / X(i, i);
+    }
+  if (rank < cols) {
+    // applyZAdjointOnTheLeftInPlace(dst), essential = row k, columns rank..cols-1
+    const Index len = cols - rank + 1;
+    std::vector<double> ess(static_cast<size_t>(len));
+    for (Index k = 0; k < rank; ++k) {  // Z^T = Z(r-1) ... Z(0): Z(0) first
+      if (k != rank - 1)
+        for (Index j = 0; j < rows; ++j) std::swap(dst(k, j), dst(rank - 1, j));
+      ess[0] = 1.0;
+      for (Index j = 1; j < len; ++j) ess[static_cast<size_t>(j)] = X(k, rank - 1 + j);
+      apply_householder_left(dst, rank - 1, len, ess.data(), zc[static_cast<size_t>(k)], 0, rows);
+      if (k != rank - 1)
+        for (Index j = 0; j < rows; ++j) std::swap(dst(k, j), dst(rank - 1, j));
+    }
+  }
+  // x = P y
+  Matrix out(cols, rows);
+  for (Index i = 0; i < cols; ++i)
+    for (Index j = 0; j < rows; ++j) out(cp.perm[static_cast<size_t>(i)], j) = dst(i, j);
+  return out;
+}
+
 // ------------------------------------------------------------ SVD
 namespace {
 

@@ -173,13 +173,19 @@ PYBIND11_MODULE(_oracle, m) {
   m.def("select_rows_spanning", [](const FArray& A, Index count, double h) {
     return select_rows_spanning(from_np(A), count, h).indices();
   }, py::arg("A"), py::arg("count"), py::arg("h") = 1.1);
-  m.def("primitive_cur", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J, Index r) {
+  m.def("primitive_cur", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J, Index r,
+                            bool qr_nucleus) {
     Matrix M = from_np(A);
     DenseOracle o(M);
-    py::dict d = cur_dict(primitive_cur(o, mkset(I, M.rows()), mkset(J, M.cols()), r));
+    py::dict d = cur_dict(primitive_cur(o, mkset(I, M.rows()), mkset(J, M.cols()), r, qr_nucleus));
     d["accesses"] = o.accesses();
     return d;
-  });
+  }, py::arg("A"), py::arg("I"), py::arg("J"), py::arg("r"), py::arg("qr_nucleus") = false);
+  m.def("cod_pseudo_inverse", [](const FArray& G, double threshold) {
+    Index rank = 0;
+    Matrix P = cod_pseudo_inverse(from_np(G), threshold, &rank);
+    return py::make_tuple(to_np(P), rank);
+  }, py::arg("G"), py::arg("threshold") = 1e-10);
   m.def("cross_approx", [](const FArray& A, Index r, Index k, Index l, const std::vector<Index>& init_rows,
                            int loops, double h, std::optional<double> stop_tol, Rng& rng) {
     Matrix M = from_np(A);

@@ -597,6 +597,180 @@ int launch_colpiv_lsq(Context* cx, double* W, int64_t k, int d, double* ws, int 
   return SLRA_OK;
 }
 
+// Eigen CompleteOrthogonalDecomposition pseudo-inverse, primitive_cur's
+// qr_nucleus branch (cur.cpp:146-152), restated in oracle/src/linalg.cpp
+// (cod_pseudo_inverse). Runs after colpiv_lsq_kernel(solve = 0) left the
+// ColPivQR of G (k x l) in W (+ taus, permutation, nonzero-pivot count and
+// max pivot). One CTA, W in global memory (L2-resident; generators are
+// small): the RZ step at the DEFAULT rank r_e (the constructor's), then
+// pinv = P Z^T [T11^-1 (Q^T I)(0:r_t, :); 0] at the thresholded rank r_t
+// (setThreshold, read by rank() and pseudoInverse()), exactly the order in
+// which Eigen applies them. Warps own columns (left reflectors) or rows
+// (right reflectors); one __syncthreads between dependent steps.
+constexpr int kCT = 256;
+__global__ void __launch_bounds__(kCT) cod_pinv_kernel(double* __restrict__ W, int k, int l,
+                                                       const double* __restrict__ hc, const int* __restrict__ perm,
+                                                       const double* __restrict__ piv, double threshold,
+                                                       double* __restrict__ zc, double* __restrict__ Cw,
+                                                       double* __restrict__ D, double* __restrict__ P, int64_t ldp,
+                                                       int32_t* __restrict__ rank_out) {
+  __shared__ double red[33];
+  __shared__ int s_r[2];
+  __shared__ double s_h[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kCT / 32;
+  const int size = k < l ? k : l;
+  if (tid == 0) {
+    const int nz = (int)piv[0];
+    const double pre_e = fabs(piv[1]) * (2.220446049250313e-16 * (double)size);
+    const double pre_t = fabs(piv[1]) * threshold;
+    int re = 0, rt = 0;
+    for (int i = 0; i < nz; ++i) {
+      const double a = fabs(W[i + (int64_t)i * k]);
+      re += a > pre_e;
+      rt += a > pre_t;
+    }
+    s_r[0] = re;
+    s_r[1] = rt;
+    *rank_out = rt;
+  }
+  for (int i = tid; i < size; i += kCT) zc[i] = 0.0;
+  __syncthreads();
+  const int re = s_r[0], rt = s_r[1];
+  auto X = [&](int i, int j) -> double& { return W[i + (int64_t)j * k]; };
+  // ---- RZ: [R11 R12] = [T11 0] Z at rank r_e (computeInPlace)
+  if (re < l) {
+    const int len = l - re + 1, c0 = re - 1;
+    for (int kk = re - 1; kk >= 0; --kk) {
+      if (kk != re - 1)
+        for (int i = tid; i <= kk; i += kCT) {
+          const double t = X(i, kk);
+          X(i, kk) = X(i, c0);
+          X(i, c0) = t;
+        }
+      __syncthreads();
+      // makeHouseholderInPlace on row kk, columns c0 .. l-1
+      double tl = 0.0;
+      for (int j = 1 + tid; j < len; j += kCT) tl = fma(X(kk, c0 + j), X(kk, c0 + j), tl);
+      tl = block_sum<kCT>(tl, red);
+      const double x0 = X(kk, c0);
+      double tau, beta;
+      if (tl <= DBL_MIN) {
+        tau = 0.0;
+        beta = x0;
+      } else {
+        beta = sqrt(x0 * x0 + tl);
+        if (x0 >= 0.0) beta = -beta;
+        tau = (beta - x0) / beta;
+      }
+      __syncthreads();
+      if (tl <= DBL_MIN) {
+        for (int j = 1 + tid; j < len; j += kCT) X(kk, c0 + j) = 0.0;
+      } else {
+        const double den = x0 - beta;
+        for (int j = 1 + tid; j < len; j += kCT) X(kk, c0 + j) /= den;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        zc[kk] = tau;
+        X(kk, c0) = beta;
+      }
+      // applyHouseholderOnTheRight to rows 0..kk-1, columns c0 .. l-1
+      if (kk > 0 && tau != 0.0) {
+        for (int i = warp; i < kk; i += NW) {
+          double t = 0.0;
+          for (int j = 1 + lane; j < len; j += 32) t = fma(X(i, c0 + j), X(kk, c0 + j), t);
+          t = warp_sum(t) + X(i, c0);
+          __syncwarp();
+          if (lane == 0) X(i, c0) -= tau * t;
+          for (int j = 1 + lane; j < len; j += 32) X(i, c0 + j) -= tau * t * X(kk, c0 + j);
+        }
+      }
+      __syncthreads();
+      if (kk != re - 1)
+        for (int i = tid; i <= kk; i += kCT) {
+          const double t = X(i, kk);
+          X(i, kk) = X(i, c0);
+          X(i, c0) = t;
+        }
+      __syncthreads();
+    }
+  }
+  // ---- D (l x k) = pinv
+  for (int64_t e = tid; e < (int64_t)l * k; e += kCT) D[e] = 0.0;
+  if (rt == 0) {
+    __syncthreads();
+    for (int64_t e = tid; e < (int64_t)l * k; e += kCT) P[(e % l) + (e / l) * ldp] = 0.0;
+    return;
+  }
+  // c = H_{rt-1} ... H_0 I (k x k), a warp per column
+  for (int64_t e = tid; e < (int64_t)k * k; e += kCT) Cw[e] = (e % k) == (e / k) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int j = 0; j < rt; ++j) {
+    const double tau = hc[j];
+    const double* ess = W + j + (int64_t)j * k;  // ess[1 .. k-j)
+    for (int c = warp; c < k; c += NW) {
+      double* xc = Cw + j + (int64_t)c * k;
+      if (k - j == 1) {
+        if (lane == 0) xc[0] *= (1.0 - tau);
+      } else if (tau != 0.0) {
+        double w = 0.0;
+        for (int i = 1 + lane; i < k - j; i += 32) w = fma(ess[i], xc[i], w);
+        w = warp_sum(w) + xc[0];
+        __syncwarp();
+        if (lane == 0) xc[0] -= tau * w;
+        for (int i = 1 + lane; i < k - j; i += 32) xc[i] -= tau * ess[i] * w;
+      }
+    }
+    __syncthreads();
+  }
+  // T11 z = c(0:rt, :): a thread per right-hand side
+  for (int c = tid; c < k; c += kCT) {
+    for (int i = rt - 1; i >= 0; --i) {
+      double sacc = Cw[i + (int64_t)c * k];
+      for (int t = i + 1; t < rt; ++t) sacc -= X(i, t) * D[t + (int64_t)c * l];
+      D[i + (int64_t)c * l] = sacc / X(i, i);
+    }
+  }
+  __syncthreads();
+  // applyZAdjointOnTheLeftInPlace at rank r_t: Z(0) first
+  if (rt < l) {
+    const int len = l - rt + 1, r0 = rt - 1;
+    for (int kk = 0; kk < rt; ++kk) {
+      const double tau = zc[kk];
+      for (int c = warp; c < k; c += NW) {
+        double* dc = D + (int64_t)c * l;
+        if (lane == 0 && kk != rt - 1) {
+          const double t = dc[kk];
+          dc[kk] = dc[r0];
+          dc[r0] = t;
+        }
+        __syncwarp();
+        if (tau != 0.0) {
+          double w = 0.0;
+          for (int j = 1 + lane; j < len; j += 32) w = fma(X(kk, r0 + j), dc[r0 + j], w);
+          w = warp_sum(w) + dc[r0];
+          __syncwarp();
+          if (lane == 0) dc[r0] -= tau * w;
+          for (int j = 1 + lane; j < len; j += 32) dc[r0 + j] -= tau * X(kk, r0 + j) * w;
+        }
+        __syncwarp();
+        if (lane == 0 && kk != rt - 1) {
+          const double t = dc[kk];
+          dc[kk] = dc[r0];
+          dc[r0] = t;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // x = P y
+  for (int64_t e = tid; e < (int64_t)l * k; e += kCT) {
+    const int i = (int)(e % l), c = (int)(e / l);
+    P[perm[i] + (int64_t)c * ldp] = D[e];
+  }
+}
+
 // Solve min ||FA x - Fb|| for a sketched system FW = (FA | Fb) (k x (d+1),
 // ld k). FW == nullptr: the caller has already written FW into the arena
 // (returned through *fw_slot when fw_slot != nullptr on a first call).
@@ -775,6 +949,40 @@ int slra_lsq_exact(slra_ctx ctx, const double* A, int64_t lda, int64_t m, int64_
   const int* perm = reinterpret_cast<const int*>(qws + 3 * d + 2);
   perm_scatter_kernel<<<1, 256, 0, st>>>(y, perm, (int)d, x);
   SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}
+
+int slra_cod_pinv(slra_ctx ctx, const double* G, int64_t ldg, int64_t k, int64_t l, double threshold, double* P,
+                  int64_t ldp, int64_t* h_rank) {
+  if (!ctx || k < 1 || l < 1 || ldg < k || ldp < l || !(threshold >= 0.0)) return SLRA_ERR_INVALID_ARGUMENT;
+  if (k > 4096 || l > 4096) return SLRA_ERR_UNSUPPORTED;
+  Context* cx = C(ctx);
+  cudaStream_t st = cx->stream;
+  // W = (G | 0): colpiv_lsq_kernel's layout (its extra column takes the reflectors)
+  const size_t wq = (size_t)k * (l + 1), qws = 3 * (size_t)l + 4 + ((size_t)l + 1) / 2;
+  const size_t need = wq + qws + (size_t)l + (size_t)k * k + (size_t)l * k;
+  double* Wq = static_cast<double*>(arena(cx, 13, sizeof(double) * need));
+  if (!Wq) return SLRA_ERR_CUDA;
+  double* ws = Wq + wq;
+  double* zc = ws + qws;
+  double* Cw = zc + l;
+  double* D = Cw + (size_t)k * k;
+  SLRA_CUDA(cudaMemcpy2DAsync(Wq, 8 * k, G, 8 * ldg, 8 * k, l, cudaMemcpyDeviceToDevice, st));
+  SLRA_CUDA(cudaMemsetAsync(Wq + (size_t)k * l, 0, 8 * k, st));
+  int32_t* d_rank = static_cast<int32_t*>(cx->dsmall);
+  SLRA_TRY(launch_colpiv_lsq(cx, Wq, k, (int)l, ws, 0, nullptr, d_rank));
+  const double* hc = ws + 2 * l;
+  const double* piv = hc + l;
+  const int* perm = reinterpret_cast<const int*>(piv + 2);
+  SLRA_TIMED(cx, "cod_pinv", cod_pinv_kernel<<<1, kCT, 0, st>>>(Wq, (int)k, (int)l, hc, perm, piv, threshold, zc, Cw, D,
+                                                               P, ldp, d_rank);)
+  SLRA_CHECK_LAUNCH(cx);
+  if (h_rank) {
+    int32_t* hs = static_cast<int32_t*>(cx->hsmall);
+    SLRA_CUDA(cudaMemcpyAsync(hs, d_rank, 4, cudaMemcpyDeviceToHost, st));
+    SLRA_CUDA(cudaStreamSynchronize(st));
+    *h_rank = hs[0];
+  }
   return SLRA_OK;
 }
 

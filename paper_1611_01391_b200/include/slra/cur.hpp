@@ -17,7 +17,7 @@ struct CurDecomposition {
   IndexSet col_set;  // l selected columns
   Matrix nucleus;    // l x k
   Index r = 0;
-  bool qr_nucleus = false;  // only the SVD nucleus is on the device path
+  bool qr_nucleus = false;  // nucleus from CompleteOrthogonalDecomposition (slra_cod_pinv)
   // Factored nucleus U = tsig * sr^T (l x r, k x r), filled by primitive_cur /
   // cross_approx: cur_evaluate then runs its pass over M at inner dimension r.
   Matrix tsig, sr;

@@ -371,12 +371,19 @@ PYBIND11_MODULE(_slra, m) {
   m.def("select_rows_spanning", [](const FArray& A, Index count, double h) {
     return select_rows_spanning(from_np(A), count, h).indices();
   }, py::arg("A"), py::arg("count"), py::arg("h") = 1.1);
-  m.def("primitive_cur", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J, Index r) {
+  m.def("primitive_cur", [](const FArray& A, const std::vector<Index>& I, const std::vector<Index>& J, Index r,
+                            bool qr_nucleus) {
     Matrix M = from_np(A);
     DenseOracle o(M);
-    py::dict d = cur_dict(primitive_cur(o, mkset(I, M.rows()), mkset(J, M.cols()), r));
+    py::dict d = cur_dict(primitive_cur(o, mkset(I, M.rows()), mkset(J, M.cols()), r, qr_nucleus));
     d["accesses"] = o.accesses();
     return d;
+  }, py::arg("A"), py::arg("I"), py::arg("J"), py::arg("r"), py::arg("qr_nucleus") = false);
+  m.def("cod_pinv_device", [](uintptr_t G, Index ldg, Index k, Index l, double threshold, uintptr_t P, Index ldp) {
+    int64_t rank = 0;
+    check(slra_cod_pinv(device_context(), ptr<double>(G), ldg, k, l, threshold, ptr<double>(P), ldp, &rank),
+          "cod_pinv");
+    return rank;
   });
   m.def("cross_approx", [](const FArray& A, Index r, Index k, Index l, const std::vector<Index>& init_rows, int loops,
                            double h, Rng& rng, std::optional<double> stop_tol) {

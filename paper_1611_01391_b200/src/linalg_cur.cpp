@@ -120,8 +120,7 @@ static void set_factors(CurDecomposition& c, const DevBuf<double>& dT, const Dev
 }
 
 CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Index r, bool qr_nucleus) {
-  // cur.cpp:137-162 (SVD nucleus)
-  if (qr_nucleus) throw std::invalid_argument("primitive_cur: the QR nucleus is not on the device path");
+  // cur.cpp:137-162
   // r = 0 selects the adaptive rank (numerical_rank(G, 1e-10)); r < 0 is invalid
   if (I.size() < r || J.size() < r || r < 0)
     throw std::invalid_argument("primitive_cur: need |I|, |J| >= r >= 0 (0: adaptive rank)");
@@ -130,6 +129,26 @@ CurDecomposition primitive_cur(const EntryOracle& M, IndexSet I, IndexSet J, Ind
   const Index k = I.size(), l = J.size();
   DevBuf<int64_t> dI(to64(I)), dJ(to64(J));
   DeviceMatrix dU(l, k);
+  if (qr_nucleus) {
+    // cur.cpp:146-152: nucleus = G^+ by CompleteOrthogonalDecomposition
+    // (threshold 1e-10), no rank-r truncation; rank() < r -> GeneratorRankFailure.
+    // With r = 0 the COD rank is reported as r.
+    DeviceMatrix dG(k, l);
+    check(slra_gather_block(device_context(), dA.data(), dA.ld(), M.rows(), M.cols(), dI.get(), k, dJ.get(), l,
+                            dG.data(), dG.ld()),
+          "primitive_cur");
+    int64_t rank = 0;
+    check(slra_cod_pinv(device_context(), dG.data(), dG.ld(), k, l, 1e-10, dU.data(), l, &rank), "primitive_cur");
+    M.count(static_cast<unsigned long long>(k * l));
+    if (rank < std::max<Index>(r, 1)) throw GeneratorRankFailure("primitive_cur: generator rank below target");
+    CurDecomposition c;
+    c.row_set = std::move(I);
+    c.col_set = std::move(J);
+    c.nucleus = dU.download();
+    c.r = r > 0 ? r : rank;
+    c.qr_nucleus = true;
+    return c;
+  }
   const Index kl = std::min(k, l);
   DevBuf<double> dT(static_cast<size_t>(l * kl)), dS(static_cast<size_t>(k * kl));
   int64_t r_used = 0;

@@ -1,0 +1,92 @@
+"""primitive_cur's qr_nucleus branch (cur.cpp:146-152) on the B200: the
+nucleus is G^+ from Eigen's CompleteOrthogonalDecomposition (threshold 1e-10)
+— slra_cod_pinv (csrc/lsr.cu: colpiv_lsq_kernel + cod_pinv_kernel) against
+the oracle's step-by-step restatement (oracle/src/linalg.cpp,
+cod_pseudo_inverse). Needs a GPU (`-m gpu`).
+
+Tolerance: 1e-10 relative to ||G^+||_F (north_star) where the generator is
+well-posed (its COD rank is the same at Eigen's default threshold and at
+1e-10); ranks and the GeneratorRankFailure decision are exact.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def slra():
+    import paper_1611_01391_b200 as s
+    return s
+
+
+def lowrank(seed, k, l, rk):
+    g = np.random.default_rng(seed)
+    return np.asfortranarray(g.standard_normal((k, rk)) @ g.standard_normal((rk, l)))
+
+
+SHAPES = [(16, 16, 16), (32, 32, 32), (20, 12, 12), (12, 20, 12), (16, 16, 5), (10, 30, 4), (30, 10, 6),
+          (64, 64, 6), (64, 64, 64), (1, 5, 1), (5, 1, 1), (100, 37, 20)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_cod_pinv_vs_oracle(slra, oracle, shape):
+    k, l, rk = shape
+    G = lowrank(7 + k + 3 * l + rk, k, l, rk)
+    Po, ro = oracle.cod_pseudo_inverse(G, 1e-10)
+    out = slra.primitive_cur(G, list(range(k)), list(range(l)), min(rk, ro), qr_nucleus=True)
+    P = out["nucleus"]
+    assert ro == rk
+    assert P.shape == (l, k)
+    assert np.linalg.norm(P - Po) <= TOL * np.linalg.norm(Po), np.linalg.norm(P - Po) / np.linalg.norm(Po)
+    # Penrose: G P G = G (the COD pseudo-inverse of the rank-rk generator)
+    assert np.linalg.norm(G @ P @ G - G) <= 1e-10 * np.linalg.norm(G)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_primitive_cur_qr_nucleus_vs_oracle(slra, oracle, seed):
+    # a sampled generator of a factor-Gaussian matrix (the config-1 recipe)
+    A = slra.gen_factor_gaussian(256, 256, 8, 1e-8, slra.Rng(100 + seed))
+    rng = slra.Rng(200 + seed)
+    I = rng.distinct_indices(16, 256)
+    J = rng.distinct_indices(16, 256)
+    g = slra.primitive_cur(A, I, J, 8, qr_nucleus=True)
+    o = oracle.primitive_cur(A, I, J, 8, qr_nucleus=True)
+    assert g["I"] == o["I"] and g["J"] == o["J"] and g["r"] == o["r"] == 8
+    assert g["accesses"] == o["accesses"] == 16 * 16
+    Cg = slra.cur_reconstruct(A, I, J, g["nucleus"])
+    Co = oracle.cur_reconstruct(A, I, J, o["nucleus"])
+    assert np.linalg.norm(Cg - Co) <= TOL * np.linalg.norm(A)
+    # the QR nucleus is the untruncated pseudo-inverse: C U R reproduces A's
+    # rank-8 part as well as the SVD nucleus does at this noise level
+    e = slra.cur_evaluate(A, I, J, g["nucleus"]) / np.linalg.norm(A)
+    assert e < 1e-6
+
+
+def test_qr_nucleus_rank_failure(slra, oracle):
+    G = lowrank(3, 16, 16, 5)
+    with pytest.raises(slra.GeneratorRankFailure):
+        slra.primitive_cur(G, list(range(16)), list(range(16)), 6, qr_nucleus=True)
+    with pytest.raises(oracle.GeneratorRankFailure):
+        oracle.primitive_cur(G, list(range(16)), list(range(16)), 6, qr_nucleus=True)
+    Z = np.zeros((8, 8), order="F")
+    with pytest.raises(slra.GeneratorRankFailure):
+        slra.primitive_cur(Z, list(range(8)), list(range(8)), 1, qr_nucleus=True)
+
+
+def test_qr_nucleus_eigen_threshold_order(slra, oracle):
+    # rank 4 at 1e-10 but full rank at Eigen's default threshold: the RZ step
+    # runs at the default rank and pseudoInverse() at 1e-10 (see
+    # cod_pseudo_inverse); the device follows the same order. Ranks exact,
+    # and the result agrees to the conditioning of that mixed sequence.
+    g = np.random.default_rng(5)
+    for (k, l) in [(24, 16), (16, 16), (16, 24)]:
+        G = np.asfortranarray(g.standard_normal((k, 4)) @ g.standard_normal((4, l)) + 1e-13 * g.standard_normal((k, l)))
+        Po, ro = oracle.cod_pseudo_inverse(G, 1e-10)
+        P = slra.primitive_cur(G, list(range(k)), list(range(l)), 4, qr_nucleus=True)["nucleus"]
+        assert ro == 4
+        rel = np.linalg.norm(P - Po) / np.linalg.norm(Po)
+        print(f"{k}x{l}: ||P||={np.linalg.norm(P):.3e} rel diff {rel:.3e}")
+        assert rel <= 1e-4

@@ -823,3 +823,19 @@ def test_ks_normality(oracle):  # test_sketch.cpp:319-334 (20 of the 100 seeds)
         oracle.ks_normality([1.0] * 100)
     r = oracle.Rng(5)
     assert not oracle.ks_normality([r.uniform() for _ in range(10000)])[1]
+
+
+# ------------------------------------------------ CompleteOrthogonalDecomposition (cur.cpp:146-152)
+@pytest.mark.parametrize("shape", [(16, 16, 16), (20, 12, 12), (12, 20, 12), (16, 16, 5), (10, 30, 4), (30, 10, 6)])
+def test_oracle_cod_pinv_is_the_pseudo_inverse(oracle, shape):
+    # well-posed generators: the COD pseudo-inverse equals the SVD one (LAPACK)
+    k, l, rk = shape
+    g = np.random.default_rng(k * 100 + l + rk)
+    G = np.asfortranarray(g.standard_normal((k, rk)) @ g.standard_normal((rk, l)))
+    P, r = oracle.cod_pseudo_inverse(G, 1e-10)
+    assert r == rk
+    Pn = np.linalg.pinv(G, rcond=1e-10)
+    assert np.linalg.norm(P - Pn) <= 1e-12 * np.linalg.norm(Pn) * max(k, l)
+    if rk < min(k, l):  # r above the COD rank: GeneratorRankFailure (cur.cpp:150-151)
+        with pytest.raises(oracle.GeneratorRankFailure):
+            oracle.primitive_cur(G, list(range(k)), list(range(l)), rk + 1, qr_nucleus=True)
