@@ -54,7 +54,7 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--blocks", type=int, default=65536, help="config 5 block count")
-    p.add_argument("--e2e-steps", type=int, default=3, help="end-to-end (host buffers) steps (config 5)")
+    p.add_argument("--e2e-steps", type=int, default=5, help="end-to-end (host buffers) steps (config 5)")
     p.add_argument("--ref-blocks", type=int, default=1024, help="config-5 blocks per reference-arm step")
     return p.parse_args()
 
@@ -425,6 +425,8 @@ def main():
         "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
         "residual_rel": work.last_residual_rel(),
     }
+    if hasattr(work, "e2e_dense") and ws == 1 and args.e2e_steps > 0:
+        line["e2e_dense_blocks"] = work.e2e_dense(args.e2e_steps, args.warmup)
     if hasattr(work, "function_oracle") and ws == 1 and (args.e2e_steps > 0 or args.config != 5):
         line["function_oracle"] = work.function_oracle(min(args.steps, 10), args.warmup)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -1044,7 +1046,8 @@ class Config5:
         self.rs = torch.zeros(nb, dtype=torch.float64, device="cuda")
         self.ns = torch.zeros(nb, dtype=torch.float64, device="cuda")
         self.entries_per_step = blocks * m * m  # the whole job (all ranks)
-        self.data = "synthetic (seeded; BASELINE config-5 recipe: per-block reference Rng, blocks materialised on device)"
+        self.data = ("synthetic (seeded; BASELINE config-5 recipe: per-block reference Rng; `value`: blocks "
+                     "materialised in HBM; `e2e`: the blocks' points from pinned host memory, FunctionOracle)")
         self.config = config5_config(blocks)
 
     def step(self):
@@ -1134,31 +1137,43 @@ class Config5:
         ms = e0.elapsed_time(e1) / steps
         same = all(bool(torch.equal(a, b)) for a, b in zip(outs, (self.I, self.J, self.U, self.r, self.st, self.rs,
                                                                     self.ns)))
+        return {"value": nb * C5_M * C5_M / (ms * 1e-3), "unit": "entries/s", "ms_per_step": ms, "steps": steps,
+                "identical_to_dense_run": same,
+                "api": "paper_1611_01391_b200.cross_approx_batched_logkernel_device -> "
+                       "slra_cross_approx_batched_logkernel (device-resident points; blocks never materialised)"}
+
+    def e2e(self, steps, warmup):
+        """End to end with the blocks as the reference defines them for this config: an EntryOracle per
+        block given by its points (FunctionOracle, oracle.hpp:43-54; K_ij = log|p_i - q_j|). Pinned host
+        points in, every result (I, J, nucleus, r, status, residuals) back in pinned host memory, through
+        slra_cross_approx_batched_logkernel_host; wall clock. The materialised-block variant of the same
+        call is `e2e_dense_blocks` (host-link bound: 34 GB of blocks per step)."""
+        torch, slra, nb = self.torch, self.slra, self.nb
         hp = [self.pts[i].cpu().pin_memory() for i in range(4)]
         hinit = self.init.cpu().pin_memory()
-        houts = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+        houts = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+                 for o in (self.I, self.J, self.U, self.r, self.st, self.rs, self.ns)]
 
         def host():
             slra.cross_approx_batched_logkernel_host(*[h.data_ptr() for h in hp], nb, C5_M, C5_M, 0, C5_K, C5_K,
                                                      hinit.data_ptr(), C5_LOOPS, 1.1, *[o.data_ptr() for o in houts])
-        host()
+        for _ in range(max(1, min(warmup, 2))):
+            host()
         torch.cuda.synchronize()
-        hsteps = max(1, min(steps, 5))
         t0 = time.perf_counter()
-        for _ in range(hsteps):
+        for _ in range(steps):
             host()
         dt = time.perf_counter() - t0
-        same_host = bool(torch.equal(houts[0], self.I.cpu()) and torch.equal(houts[1], self.J.cpu()))
+        same_host = all(bool(torch.equal(a, b.cpu())) for a, b in zip(houts, (self.I, self.J, self.U, self.r)))
         d2h = nb * (8 * 2 * C5_K + 8 * C5_K * C5_K + 8 + 4 + 16)
-        return {"value": nb * C5_M * C5_M / (ms * 1e-3), "unit": "entries/s", "ms_per_step": ms, "steps": steps,
-                "identical_to_dense_run": same,
-                "e2e": {"value": nb * C5_M * C5_M * hsteps / dt, "unit": "entries/s",
-                        "h2d_bytes_per_step": nb * 8 * (4 * C5_M + C5_K), "d2h_bytes_per_step": d2h,
-                        "steps": hsteps, "same_I_J_as_device_run": same_host},
-                "api": "paper_1611_01391_b200.cross_approx_batched_logkernel_{device,host} -> "
-                       "slra_cross_approx_batched_logkernel(_host) (points in; blocks never materialised)"}
+        return {"value": nb * C5_M * C5_M * steps / dt, "unit": "entries/s",
+                "h2d_bytes_per_step": nb * 8 * (4 * C5_M + C5_K), "d2h_bytes_per_step": d2h,
+                "steps": steps, "same_I_J_U_r_as_device_run": same_host,
+                "input": "per-block points (FunctionOracle, oracle.hpp:43-54) + initial rows, pinned host memory",
+                "api": "paper_1611_01391_b200.cross_approx_batched_logkernel_host -> "
+                       "slra_cross_approx_batched_logkernel_host (points H2D, C-A + residual, results D2H)"}
 
-    def e2e(self, steps, warmup):
+    def e2e_dense(self, steps, warmup):
         """The batch through the host-buffer entry (slra_cross_approx_batched_host): pinned host blocks
         streamed to the device in chunks overlapped with the kernels, every result copied back."""
         torch = self.torch
