@@ -1,6 +1,7 @@
 // Shared device/runtime helpers for the sm_100a kernels behind slra_cuda.h.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -127,12 +128,15 @@ struct Context {
 
 cudaEvent_t pooled_event(Context* c);
 
-// Records start/stop events around one kernel launch when timing is on.
+// Records start/stop events around one kernel launch when timing is on, and
+// always an NVTX range named after the kernel family (header-only NVTX3: a
+// no-op unless a profiler injects itself, e.g. ncu --nvtx / nsys).
 struct KernelTimer {
   Context* c;
   const char* family;
   cudaEvent_t start = nullptr;
   KernelTimer(Context* ctx, const char* fam) : c(ctx), family(fam) {
+    nvtxRangePushA(fam);
     if (c->timing) {
       start = pooled_event(c);
       cudaEventRecord(start, c->stream);
@@ -144,6 +148,7 @@ struct KernelTimer {
       cudaEventRecord(stop, c->stream);
       c->records.push_back({family, start, stop});
     }
+    nvtxRangePop();
   }
 };
 

@@ -39,13 +39,20 @@ namespace rs {
 constexpr int NT = 256;        // 8 warps, 16 * MI rows each
 constexpr int MI = 1;          // m16 blocks per warp
 constexpr int TM = 8 * 16 * MI;  // tile rows (row block)
-constexpr int TN = 32;         // tile cols
+#ifndef SLRA_RS_TN
+#define SLRA_RS_TN 32
+#endif
+#ifndef SLRA_RS_NS
+#define SLRA_RS_NS 2
+#endif
+constexpr int TN = SLRA_RS_TN; // tile cols
+constexpr int NI = TN / 8;     // n8 fragments per tile
 constexpr int KP = 32;         // inner dimension (padded)
 constexpr int LDV = KP + 4;    // Vs[col][k]: conflict-free B fragment reads
 constexpr int LDM = TM + 2;    // Ms[col][row]: conflict-free epilogue reads
 constexpr int V_D = TN * LDV;  // doubles per Q stage
 constexpr int M_D = TN * LDM;  // doubles per A stage
-constexpr int NS = 2;          // tiles in flight (two CTAs per SM)
+constexpr int NS = SLRA_RS_NS; // stages (NS - 1 tiles in flight behind the current one)
 constexpr size_t SMEM = sizeof(double) * NS * (V_D + M_D);
 }  // namespace rs
 
@@ -158,18 +165,18 @@ __device__ __forceinline__ void residual_stream_body(const StreamResidualArgs& a
     }
     const double* Vs = VB(slot);
     const double* Ms = MB(slot) + warp * 16 * MI;
-    double acc[MI][4][4];
+    double acc[MI][NI][4];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[mi][ni][v] = 0.0;
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
       if (kk < nkk) {
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
+        for (int ni = 0; ni < NI; ++ni) {
           double bf[4];
 #pragma unroll
           for (int v = 0; v < 4; ++v) bf[v] = Vs[(ni * 8 + g) * LDV + kk * 16 + t4 + 4 * v];
@@ -188,7 +195,7 @@ __device__ __forceinline__ void residual_stream_body(const StreamResidualArgs& a
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int v = 0; v < 4; v += 2) {
           const int row = mi * 16 + g + 8 * (v >> 1), col = ni * 8 + 2 * t4;
