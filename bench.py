@@ -26,6 +26,7 @@ Eigen) on a bounded sample of the same workload with all host threads, on
 the same config/metric/unit. Under torchrun only rank 0 runs it.
 """
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -56,6 +57,8 @@ def parse():
     p.add_argument("--blocks", type=int, default=65536, help="config 5 block count")
     p.add_argument("--e2e-steps", type=int, default=5, help="end-to-end (host buffers) steps (config 5)")
     p.add_argument("--ref-blocks", type=int, default=1024, help="config-5 blocks per reference-arm step")
+    p.add_argument("--no-other-configs", action="store_true",
+                   help="skip the short configs 1-4 legs appended to the default (config 5, N=1) line")
     return p.parse_args()
 
 
@@ -431,10 +434,70 @@ def main():
         line["function_oracle"] = work.function_oracle(min(args.steps, 10), args.warmup)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = work.cpu_baseline()
+    if ws == 1 and args.config == 5 and not args.no_other_configs and args.blocks == 65536:
+        # the other BASELINE configs as short legs of the same run (same timing
+        # rules: W warm-ups, L2 flush between steps, CUDA events on the product's
+        # stream), so the default line carries a measurement of every config
+        del work
+        gc.collect()
+        torch.cuda.empty_cache()
+        line["other_configs"] = other_configs(slra, torch, args, comm, stream, flush_buf, peaks)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def other_configs(slra, torch, args, comm, stream, flush_buf, peaks):
+    """Configs 1-4 (BASELINE.json configs[0..3]) measured briefly after the
+    config-5 line: device-resident entries/s, the per-kernel family times, the
+    dominant kernel's roofline and the host-buffer e2e; no CPU baseline."""
+    out = {}
+    steps, warmup = 10, max(3, min(args.warmup, 5))
+    makers = {
+        "config1": lambda: Config1(slra, torch, args.seed),
+        "config2": lambda: Config2(slra, torch, args.seed),
+        "config3": lambda: Config3(slra, torch, args.seed),
+        "config4": lambda: Config4(slra, torch, args.seed, comm),
+    }
+    for name, make in makers.items():
+        try:
+            work = make()
+            for _ in range(warmup):
+                work.step()
+            torch.cuda.synchronize()
+            launches0 = slra.launch_count()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for i in range(steps):
+                flush_buf.fill_(float(i))
+                ev[i][0].record(stream)
+                work.step()
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            launches = slra.launch_count() - launches0
+            ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+            slra.set_timing(True)
+            for i in range(steps):
+                flush_buf.fill_(float(i))
+                work.step()
+            torch.cuda.synchronize()
+            fam = slra.timing_report()
+            slra.set_timing(False)
+            roofline, kernels = work.roofline(fam, peaks, steps)
+            e2e = work.e2e(steps, warmup)
+            out[name] = {
+                "workload": work.config.get("workload"), "entries_per_step": work.entries_per_step,
+                "value": work.entries_per_step / (ms * 1e-3), "unit": "entries/s", "ms_per_step": ms,
+                "steps": steps, "warmup": warmup, "gpu_launches": launches,
+                "roofline": roofline, "kernels_ms_per_step": kernels, "e2e": e2e,
+                "residual_rel": work.last_residual_rel(),
+            }
+            del work
+        except Exception as exc:  # a failed leg must not lose the headline line
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
 
 
 class Config2:
