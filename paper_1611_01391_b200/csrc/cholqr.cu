@@ -22,7 +22,13 @@
 // atomics), chol_small_kernel (sums the partials in a fixed order, shift,
 // Cholesky padded with the identity beyond n, 1/R(i,i)), trsm_rows_kernel
 // (Q = Y R^-1, a thread per row, right-looking in registers).
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace slra_dev {
 
@@ -264,6 +270,310 @@ __global__ void __launch_bounds__(kCQ) trmm3_upper_kernel(const double* __restri
   }
 }
 
+
+// ------------------------------------------------------------ fused cluster path
+// The three passes in ONE launch when the sketch fits the shared memory of an
+// 8-CTA thread-block cluster (config 2: 4096 x 48 -> 512 rows x 48 columns =
+// 198 KB per CTA): CTA q keeps rows q RC .. (q + 1) RC - 1 of the problem
+// resident for all three passes. Per pass: the chunk's Gram on DMMA (each
+// warp runs every upper 8 x 8 tile over its share of the 4-row steps: one
+// fragment load per 8 columns serves as A and B operand), a fixed-order sum
+// over the warps, a fixed-order sum of the eight CTAs' partials over DSMEM
+// (every CTA ends with the same bits), the 48-step Cholesky redundantly in
+// every CTA (no broadcast of the factor), and the row-parallel triangular
+// solve in place. Q leaves once, after pass 3; CTA 0 forms R = R3 R2 R1.
+#ifdef SLRA_CQC_PROF
+#define CQC_MARK(i) do { if (tid == 0 && q == 0 && b == 0) pt[i] = clock64(); } while (0)
+#else
+#define CQC_MARK(i) do { } while (0)
+#endif
+namespace cqc {
+constexpr int NC = 8;
+constexpr int NT = 256;
+constexpr int kMaxSmem = 227 * 1024;
+__host__ __device__ inline int chunk_rows(int64_t m) { return (int)((m + NC - 1) / NC); }
+// leading dimension of the chunk: >= rows, = 4 (mod 16) so the DMMA fragment
+// loads (lane (g, t) reads row k + t of column 8 I + g) hit 16 different banks
+__host__ __device__ inline int chunk_ld(int rc) { return ((rc + 11) / 16) * 16 + 4; }
+template <int NP>
+struct Lay {
+  static constexpr int LD = NP + 2;  // even: the solve reads pairs of R entries as double2
+  static constexpr int NTILE = NP / 8;
+  static constexpr int NUT = NTILE * (NTILE + 1) / 2;
+  static constexpr int L_D = NP * LD;
+  static constexpr int PU_D = NUT * 64;
+  static constexpr int SMALL_D = 2 * NP + 40 + 2;
+  static size_t bytes(int ldt) { return sizeof(double) * ((size_t)NP * ldt + L_D + PU_D + SMALL_D); }
+};
+}  // namespace cqc
+
+template <int NP>
+__global__ void __cluster_dims__(cqc::NC, 1, 1) __launch_bounds__(cqc::NT, 1)
+    cholqr3_cluster_kernel(const double* __restrict__ Y, int64_t ldy, int64_t sY, int64_t m, int n,
+                           double* __restrict__ Q, int64_t ldq, int64_t sQ, double* __restrict__ R, int64_t sR,
+                           double* __restrict__ Rws, int64_t sRws, double shift_coef, int ldt,
+                           int32_t* __restrict__ status) {
+  using namespace cqc;
+  using LY = Lay<NP>;
+  constexpr int LD = LY::LD, NTILE = LY::NTILE, NUT = LY::NUT;
+  extern __shared__ __align__(16) double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int b = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  Y += b * sY;
+  Q += b * sQ;
+  R += b * sR;
+  Rws += b * sRws;
+  const int RC = chunk_rows(m);
+  const int64_t r0 = (int64_t)q * RC;
+  const int rows = (int)(m - r0 < 0 ? 0 : (m - r0 < RC ? m - r0 : RC));
+  double* T = sm;                      // NP columns x ldt
+  double* L = T + (size_t)NP * ldt;    // NP x LD
+  double* PU = L + LY::L_D;            // this CTA's partial Gram, upper tiles in fragment order
+  double* piv_s = PU + LY::PU_D;       // NP
+  double* rinv = piv_s + NP;           // NP
+  double* red = rinv + NP;             // 40
+  int* fail = reinterpret_cast<int*>(red + 40);
+#ifdef SLRA_CQC_PROF
+  long long pt[32];
+#endif
+  CQC_MARK(0);
+  // the chunk, zero beyond the problem (rows >= rows, columns >= n)
+  for (int c = warp; c < NP; c += NT / 32) {
+    const double* yc = Y + r0 + (int64_t)c * ldy;
+    double* tc = T + (size_t)c * ldt;
+    for (int i = lane; i < ldt; i += 32) tc[i] = load_sel(yc, (int64_t)i, i < rows && c < n);
+  }
+  if (tid == 0) *fail = 0;
+  __syncthreads();
+  CQC_MARK(1);
+  const int ksteps = (RC + 3) / 4;
+  for (int pass = 0; pass < 3; ++pass) {
+    // ---- partial Gram of the chunk (upper tiles)
+    double acc[NUT][2];
+#pragma unroll
+    for (int u = 0; u < NUT; ++u) acc[u][0] = acc[u][1] = 0.0;
+    for (int ks = warp; ks < ksteps; ks += NT / 32) {
+      const double* tk = T + 4 * ks + t + (size_t)g * ldt;
+      double f[NTILE];
+#pragma unroll
+      for (int I = 0; I < NTILE; ++I) f[I] = tk[(size_t)(8 * I) * ldt];
+      int u = 0;
+#pragma unroll
+      for (int I = 0; I < NTILE; ++I)
+#pragma unroll
+        for (int J = I; J < NTILE; ++J) {
+          dmma_8x8x4(acc[u][0], acc[u][1], f[I], f[J]);
+          ++u;
+        }
+    }
+    CQC_MARK(2 + 8 * pass);
+    // warps summed in warp order (lane (g, t) holds entries (g, 2t), (g, 2t + 1) of each tile)
+    for (int w = 0; w < NT / 32; ++w) {
+      if (warp == w) {
+#pragma unroll
+        for (int u = 0; u < NUT; ++u) {
+          double2* dst = reinterpret_cast<double2*>(PU + u * 64 + 8 * g + 2 * t);
+          double2 v = make_double2(acc[u][0], acc[u][1]);
+          if (w > 0) {
+            const double2 o = *dst;
+            v.x += o.x;
+            v.y += o.y;
+          }
+          *dst = v;
+        }
+      }
+      __syncthreads();
+    }
+    CQC_MARK(3 + 8 * pass);
+    cl.sync();  // every CTA's partial is complete
+    CQC_MARK(4 + 8 * pass);
+    // ---- G = sum over the CTAs in rank order -> L (lower storage: L(c, i) = G(i, c))
+    for (int e = tid; e < NUT * 64; e += NT) {
+      int u = e >> 6, I = 0;
+      while (u >= NTILE - I) {
+        u -= NTILE - I;
+        ++I;
+      }
+      const int J = I + u;
+      const int i = 8 * I + ((e & 63) >> 3), c = 8 * J + (e & 7);
+      double v[NC];
+#pragma unroll
+      for (int rk = 0; rk < NC; ++rk) v[rk] = cl.map_shared_rank(PU, rk)[e];
+      double s = v[0];
+#pragma unroll
+      for (int rk = 1; rk < NC; ++rk) s += v[rk];
+      if (i <= c) L[c + i * LD] = s;
+    }
+    cl.sync();  // the partials may be overwritten (next pass); L is complete in this CTA
+    CQC_MARK(5 + 8 * pass);
+    double tr = 0.0;
+    for (int i = tid; i < n; i += NT) tr += L[i + i * LD];
+    tr = block_sum<NT>(tr, red);
+    const double shift = pass == 0 ? shift_coef * tr : 0.0;
+    for (int i = tid; i < NP; i += NT) L[i + i * LD] = i < n ? L[i + i * LD] + shift : 1.0;
+    __syncthreads();
+    CQC_MARK(6 + 8 * pass);
+    // ---- Cholesky (chol_small_kernel's column-publishing loop), redundantly per CTA
+    {
+      constexpr int kV = NP / 4;
+      const int ti = tid & 63, tg = tid >> 6;
+      double a[kV];
+#pragma unroll
+      for (int v = 0; v < kV; ++v) {
+        const int c = tg + 4 * v;
+        a[v] = (ti < NP && ti >= c) ? L[ti + c * LD] : 0.0;
+      }
+      for (int j = 0; j < NP; ++j) {
+        const double* cj = L + j * LD;
+        const double piv = cj[j];
+        if (!(piv > 0.0)) {  // uniform over the CTA and (same bits) over the cluster
+          if (tid == 0) *fail = 1;
+          break;
+        }
+        const double rp = piv >= DBL_MIN ? fast_rcp(piv) : 1.0 / piv;
+        const double f = (ti > j && ti < NP) ? -cj[ti] * rp : 0.0;
+#pragma unroll
+        for (int v = 0; v < kV; ++v) a[v] = fma(f, cj[tg + 4 * v], a[v]);
+        const int jn = j + 1;
+        if (tg == (jn & 3) && ti < NP && jn < NP) {
+          const int vv = jn >> 2;
+#pragma unroll
+          for (int v = 0; v < kV; ++v)
+            if (v >= vv) L[ti + (tg + 4 * v) * LD] = a[v];
+        }
+        if (tid == 0) piv_s[j] = piv;
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    CQC_MARK(7 + 8 * pass);
+    if (*fail) {
+      if (q == 0 && tid == 0) status[b] = 1;
+      return;  // cluster-uniform; no DSMEM access is pending (second cl.sync above)
+    }
+    // R^T in place: L(c2, c) <- R(c, c2) = A(c2, c) / sqrt(A(c, c)) below the diagonal
+    for (int e = tid; e < NP * NP; e += NT) {
+      const int c2 = e % NP, c = e / NP;
+      if (c2 > c) L[c2 + c * LD] *= fast_rsqrt(piv_s[c]);
+    }
+    for (int i = tid; i < NP; i += NT) rinv[i] = fast_rsqrt(piv_s[i]);
+    __syncthreads();
+    if (q == 0) {  // R_pass (n x n, ld n) for the final product
+      double* Rk = Rws + (int64_t)pass * n * n;
+      for (int e = tid; e < n * n; e += NT) {
+        const int i = e % n, c = e / n;
+        Rk[e] = (i < c) ? L[c + i * LD] : (i == c ? piv_s[i] * rinv[i] : 0.0);
+      }
+    }
+    CQC_MARK(8 + 8 * pass);
+    // ---- rows <- rows R^-1 in place (a thread per row, right-looking in registers)
+    for (int i = tid; i < rows; i += NT) {
+      double zr[NP];
+#pragma unroll
+      for (int c = 0; c < NP; ++c) zr[c] = T[i + (size_t)c * ldt];
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        const double z = zr[c] * rinv[c];
+        zr[c] = z;
+        const double* rc = L + c * LD;  // R(c, c2) at rc[c2], c2 > c
+        int c2 = c + 1;
+        if (c2 & 1) {
+          if (c2 < NP) zr[c2] = fma(-z, rc[c2], zr[c2]);
+          ++c2;
+        }
+#pragma unroll
+        for (; c2 + 1 < NP; c2 += 2) {
+          const double2 rr = *reinterpret_cast<const double2*>(rc + c2);
+          zr[c2] = fma(-z, rr.x, zr[c2]);
+          zr[c2 + 1] = fma(-z, rr.y, zr[c2 + 1]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NP; ++c) T[i + (size_t)c * ldt] = zr[c];
+    }
+    __syncthreads();
+    CQC_MARK(9 + 8 * pass);
+  }
+  // ---- Q out
+  for (int c = warp; c < n; c += NT / 32) {
+    double* qc = Q + r0 + (int64_t)c * ldq;
+    const double* tc = T + (size_t)c * ldt;
+    for (int i = lane; i < rows; i += 32) qc[i] = tc[i];
+  }
+  if (q != 0) return;
+  __syncthreads();
+  // ---- R = (R3 R2) R1 (upper triangular, ld n) by CTA 0, operands staged over the chunk
+  const int nn = n * n;
+  double* A = T;
+  double* B = T + nn;
+  double* C = T + 2 * nn;
+  for (int e = tid; e < nn; e += NT) {
+    A[e] = Rws[2 * (int64_t)nn + e];
+    B[e] = Rws[(int64_t)nn + e];
+  }
+  __syncthreads();
+  for (int e = tid; e < nn; e += NT) {
+    const int i = e % n, c = e / n;
+    double s = 0.0;
+    for (int k = i; k <= c; ++k) s = fma(A[i + k * n], B[k + c * n], s);
+    C[e] = s;
+  }
+  __syncthreads();
+  for (int e = tid; e < nn; e += NT) B[e] = Rws[e];
+  __syncthreads();
+  for (int e = tid; e < nn; e += NT) {
+    const int i = e % n, c = e / n;
+    double s = 0.0;
+    for (int k = i; k <= c; ++k) s = fma(C[i + k * n], B[k + c * n], s);
+    R[e] = i <= c ? s : 0.0;
+  }
+#ifdef SLRA_CQC_PROF
+  __syncthreads();
+  if (tid == 0 && b == 0) {
+    pt[26] = clock64();
+    printf("cqc load %lld |", pt[1] - pt[0]);
+    for (int p = 0; p < 3; ++p)
+      printf(" pass%d gram %lld wsum %lld clsync %lld dsum %lld shift %lld chol %lld rt %lld trsm %lld |", p,
+             pt[2 + 8 * p] - (p ? pt[1 + 8 * p] : pt[1]), pt[3 + 8 * p] - pt[2 + 8 * p], pt[4 + 8 * p] - pt[3 + 8 * p],
+             pt[5 + 8 * p] - pt[4 + 8 * p], pt[6 + 8 * p] - pt[5 + 8 * p], pt[7 + 8 * p] - pt[6 + 8 * p],
+             pt[8 + 8 * p] - pt[7 + 8 * p], pt[9 + 8 * p] - pt[8 + 8 * p]);
+    printf(" tail %lld total %lld\n", pt[26] - pt[25], pt[26] - pt[0]);
+  }
+#endif
+}
+
+// SLRA_NO_CLUSTER_CHOLQR=1: the multi-kernel path for every shape (tests of the fallback)
+static bool cluster_path_disabled() {
+  const char* e = getenv("SLRA_NO_CLUSTER_CHOLQR");
+  return e && e[0] == '1';
+}
+
+template <int NP>
+static bool cholqr3_cluster_fits(int64_t m, int n) {
+  if (m > (int64_t)cqc::NC * 4096) return false;
+  const int ldt = cqc::chunk_ld(cqc::chunk_rows(m));
+  return cqc::Lay<NP>::bytes(ldt) <= (size_t)cqc::kMaxSmem && 3 * (size_t)n * n <= (size_t)NP * ldt;
+}
+
+template <int NP>
+static int cholqr3_cluster(Context* cx, const double* Y, int64_t ldy, int64_t sY, int64_t m, int n, double* Q,
+                           int64_t ldq, int64_t sQ, double* R, int64_t sR, int nb, double* ws, int64_t per,
+                           int32_t* status) {
+  const int ldt = cqc::chunk_ld(cqc::chunk_rows(m));
+  const size_t smem = cqc::Lay<NP>::bytes(ldt);
+  const double shift_coef = 11.0 * ((double)m * n + (double)n * (n + 1)) * (2.220446049250313e-16 / 2);  // u = eps/2
+  SLRA_CUDA(cudaFuncSetAttribute(cholqr3_cluster_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SLRA_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * nb, cx->stream));
+  SLRA_TIMED(cx, "cholqr_cluster",
+             cholqr3_cluster_kernel<NP><<<dim3(cqc::NC, (unsigned)nb), cqc::NT, smem, cx->stream>>>(
+                 Y, ldy, sY, m, n, Q, ldq, sQ, R, sR, ws, per, shift_coef, ldt, status);)
+  SLRA_CHECK_LAUNCH(cx);
+  return SLRA_OK;
+}
+
 static int64_t gram_chunks(int64_t m) { return (m + kGR - 1) / kGR; }
 
 size_t cholqr3_workspace_doubles(int64_t m, int n) {
@@ -276,6 +586,8 @@ static int cholqr3_passes(Context* cx, const double* Y, int64_t ldy, int64_t sY,
                           int32_t* status) {
   const int64_t per = (int64_t)cholqr3_workspace_doubles(m, n);
   const int64_t nn = (int64_t)n * n, nch = gram_chunks(m);
+  if (cholqr3_cluster_fits<NP>(m, n) && !cluster_path_disabled())
+    return cholqr3_cluster<NP>(cx, Y, ldy, sY, m, n, Q, ldq, sQ, R, sR, nb, ws, per, status);
   // per problem: T (m x n) | partial Grams (nch x NP x NP) | R1 | R2 | R3 | rinv (NP)
   double* T = ws;
   double* P = ws + m * n;

@@ -489,6 +489,35 @@ def test_range_finder_batched_host_matches_single(slra):
         assert abs(np.sqrt(ns) - nA) <= 1e-13 * nA
 
 
+@pytest.mark.parametrize("cluster", [True, False])
+@pytest.mark.parametrize("m,n,l,r", [(1000, 300, 13, 9), (4096, 512, 48, 32), (1531, 200, 64, 40), (777, 200, 29, 17),
+                                     (523, 200, 64, 40), (64, 64, 8, 5), (16384, 128, 48, 20),
+                                     (40000, 96, 24, 12)])
+def test_range_finder_cholqr_paths_vs_oracle(slra, oracle, monkeypatch, cluster, m, n, l, r):
+    """The sketch's QR (shifted CholeskyQR3) on both of its paths — the fused
+    8-CTA cluster kernel (the sketch resident in shared memory for the three
+    passes) and the multi-kernel passes (SLRA_NO_CLUSTER_CHOLQR=1; also what
+    shapes beyond the cluster's shared memory or too short to stage the R
+    product take: the last four here) — against the oracle's Householder
+    thin_qr pipeline, on ragged shapes: m not a multiple of 8, l not a multiple
+    of 8, l = 64."""
+    monkeypatch.setenv("SLRA_NO_CLUSTER_CHOLQR", "0" if cluster else "1")
+    rg = np.random.default_rng(m + l)
+    sig = np.where(np.arange(r + 3) < r, 0.6 ** np.arange(r + 3), 1e-12)
+    A = (rg.standard_normal((m, r + 3)) * sig) @ rg.standard_normal((r + 3, n))
+    rp, ro = slra.Rng(5), oracle.Rng(5)
+    Hp = slra.take_columns_random(slra.gen_sparse_circulant(n, 4, rp), l, rp)
+    Ho = oracle.take_columns_random(oracle.gen_sparse_circulant(n, 4, ro), l, ro)
+    nA = np.linalg.norm(A)
+    for trunc in (True, False):
+        U, V = slra.range_finder(A, Hp, r, trunc)
+        Uo, Vo = oracle.range_finder(A, Ho, r, trunc)
+        assert U.shape == Uo.shape and V.shape == Vo.shape
+        assert np.linalg.norm(U @ V - Uo @ Vo) <= TOL * nA
+        if not trunc:  # BasisQr: U is the thin Q itself
+            assert np.linalg.norm(U.T @ U - np.eye(U.shape[1])) <= 1e-13 * np.sqrt(l) * 8
+
+
 def test_range_finder_rank_failure(slra):  # test_lra.cpp:24-30
     rng = slra.Rng(20)
     H = slra.take_columns_random(slra.gen_sparse_circulant(64, 3, rng), 8, rng)
