@@ -281,13 +281,45 @@ __global__ void __launch_bounds__(kCQ) trmm3_upper_kernel(const double* __restri
 // over the warps, a fixed-order sum of the eight CTAs' partials over DSMEM
 // (every CTA ends with the same bits), the 48-step Cholesky redundantly in
 // every CTA (no broadcast of the factor), and the row-parallel triangular
-// solve in place. Q leaves once, after pass 3; CTA 0 forms R = R3 R2 R1.
+// solve in place. Q leaves once, after pass 3; R = R3 (R2 R1) is formed along
+// the way, an eighth of the entries per CTA.
 #ifdef SLRA_CQC_PROF
 #define CQC_MARK(i) do { if (tid == 0 && q == 0 && b == 0) pt[i] = clock64(); } while (0)
 #else
 #define CQC_MARK(i) do { } while (0)
 #endif
 namespace cqc {
+// TMA bulk copies (cp.async.bulk) between the chunk's contiguous columns in
+// global memory and shared memory; completion of the loads on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
 constexpr int NC = 8;
 constexpr int NT = 256;
 constexpr int kMaxSmem = 227 * 1024;
@@ -302,7 +334,7 @@ struct Lay {
   static constexpr int NUT = NTILE * (NTILE + 1) / 2;
   static constexpr int L_D = NP * LD;
   static constexpr int PU_D = NUT * 64;
-  static constexpr int SMALL_D = 2 * NP + 40 + 2;
+  static constexpr int SMALL_D = 2 * NP + 40 + 2;  // pivots, 1/R(i,i), reduction scratch, fail flag, mbarrier
   static size_t bytes(int ldt) { return sizeof(double) * ((size_t)NP * ldt + L_D + PU_D + SMALL_D); }
 };
 }  // namespace cqc
@@ -340,13 +372,41 @@ __global__ void __cluster_dims__(cqc::NC, 1, 1) __launch_bounds__(cqc::NT, 1)
   long long pt[32];
 #endif
   CQC_MARK(0);
-  // the chunk, zero beyond the problem (rows >= rows, columns >= n)
-  for (int c = warp; c < NP; c += NT / 32) {
-    const double* yc = Y + r0 + (int64_t)c * ldy;
-    double* tc = T + (size_t)c * ldt;
-    for (int i = lane; i < ldt; i += 32) tc[i] = load_sel(yc, (int64_t)i, i < rows && c < n);
+  // the chunk, zero beyond the problem (rows >= rows, columns >= n): one TMA
+  // bulk copy per column when the alignment allows (16-byte source and size)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 41);
+  const bool bulk_in = rows > 0 && (rows & 1) == 0 && (ldy & 1) == 0 && ((uintptr_t)(Y + r0) & 15) == 0;
+  if (tid == 0) {
+    *fail = 0;
+    if (bulk_in) mbar_init(mbar, 1);
   }
-  if (tid == 0) *fail = 0;
+  __syncthreads();
+  if (bulk_in) {
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(mbar, (unsigned)(n * rows * 8));
+      __syncwarp();
+      for (int c = lane; c < n; c += 32)
+        bulk_g2s(T + (size_t)c * ldt, Y + r0 + (int64_t)c * ldy, (unsigned)(rows * 8), mbar);
+    }
+    for (int c = warp; c < NP; c += NT / 32) {
+      double* tc = T + (size_t)c * ldt;
+      for (int i = (c < n ? rows : 0) + lane; i < ldt; i += 32) tc[i] = 0.0;
+    }
+    mbar_wait(mbar, 0);
+  } else {
+    for (int c = warp; c < NP; c += NT / 32) {
+      const double* yc = Y + r0 + (int64_t)c * ldy;
+      double* tc = T + (size_t)c * ldt;
+      for (int i0 = lane; i0 < ldt; i0 += 32 * 8) {  // eight loads in flight per lane
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = load_sel(yc, (int64_t)(i0 + 32 * k), i0 + 32 * k < rows && c < n);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (i0 + 32 * k < ldt) tc[i0 + 32 * k] = v[k];
+      }
+    }
+  }
   __syncthreads();
   CQC_MARK(1);
   const int ksteps = (RC + 3) / 4;
@@ -391,21 +451,30 @@ __global__ void __cluster_dims__(cqc::NC, 1, 1) __launch_bounds__(cqc::NT, 1)
     cl.sync();  // every CTA's partial is complete
     CQC_MARK(4 + 8 * pass);
     // ---- G = sum over the CTAs in rank order -> L (lower storage: L(c, i) = G(i, c))
-    for (int e = tid; e < NUT * 64; e += NT) {
-      int u = e >> 6, I = 0;
-      while (u >= NTILE - I) {
-        u -= NTILE - I;
-        ++I;
+    {
+      constexpr int DS_IT = (NUT * 64 + NT - 1) / NT;
+      double v[DS_IT][NC];  // every remote load in flight before the first sum
+#pragma unroll
+      for (int it = 0; it < DS_IT; ++it) {
+        const int e = tid + it * NT;
+#pragma unroll
+        for (int rk = 0; rk < NC; ++rk) v[it][rk] = e < NUT * 64 ? cl.map_shared_rank(PU, rk)[e] : 0.0;
       }
-      const int J = I + u;
-      const int i = 8 * I + ((e & 63) >> 3), c = 8 * J + (e & 7);
-      double v[NC];
 #pragma unroll
-      for (int rk = 0; rk < NC; ++rk) v[rk] = cl.map_shared_rank(PU, rk)[e];
-      double s = v[0];
+      for (int it = 0; it < DS_IT; ++it) {
+        const int e = tid + it * NT;
+        int u = e >> 6, I = 0;
+        while (u >= NTILE - I && I < NTILE) {
+          u -= NTILE - I;
+          ++I;
+        }
+        const int J = I + u;
+        const int i = 8 * I + ((e & 63) >> 3), c = 8 * J + (e & 7);
+        double s = v[it][0];
 #pragma unroll
-      for (int rk = 1; rk < NC; ++rk) s += v[rk];
-      if (i <= c) L[c + i * LD] = s;
+        for (int rk = 1; rk < NC; ++rk) s += v[it][rk];
+        if (e < NUT * 64 && i <= c) L[c + i * LD] = s;
+      }
     }
     cl.sync();  // the partials may be overwritten (next pass); L is complete in this CTA
     CQC_MARK(5 + 8 * pass);
@@ -455,17 +524,44 @@ __global__ void __cluster_dims__(cqc::NC, 1, 1) __launch_bounds__(cqc::NT, 1)
       return;  // cluster-uniform; no DSMEM access is pending (second cl.sync above)
     }
     // R^T in place: L(c2, c) <- R(c, c2) = A(c2, c) / sqrt(A(c, c)) below the diagonal
-    for (int e = tid; e < NP * NP; e += NT) {
-      const int c2 = e % NP, c = e / NP;
-      if (c2 > c) L[c2 + c * LD] *= fast_rsqrt(piv_s[c]);
-    }
     for (int i = tid; i < NP; i += NT) rinv[i] = fast_rsqrt(piv_s[i]);
     __syncthreads();
-    if (q == 0) {  // R_pass (n x n, ld n) for the final product
-      double* Rk = Rws + (int64_t)pass * n * n;
-      for (int e = tid; e < n * n; e += NT) {
+    for (int e = tid; e < NP * NP; e += NT) {
+      const int c2 = e % NP, c = e / NP;
+      if (c2 > c) L[c2 + c * LD] *= rinv[c];
+    }
+    // R = R3 (R2 R1), an eighth of the entries per CTA: the left factor is this
+    // pass's R (in L), the right one (R1, then R2 R1) comes from global memory
+    // (written before the two cluster barriers of this pass) staged packed
+    // upper-triangular over the partial-Gram buffer, which is idle here
+    const int nn = n * n;
+    if (pass > 0) {
+      const double* Gs = Rws + (int64_t)(pass - 1) * nn;
+      for (int e = tid; e < nn; e += NT) {
+        const int k = e % n, c = e / n;
+        if (k <= c) PU[c * (c + 1) / 2 + k] = Gs[e];
+      }
+    }
+    __syncthreads();
+    if (pass == 0) {
+      if (q == 0)
+        for (int e = tid; e < nn; e += NT) {
+          const int i = e % n, c = e / n;
+          Rws[e] = (i < c) ? L[c + i * LD] : (i == c ? piv_s[i] * rinv[i] : 0.0);
+        }
+    } else {
+      const int per = (nn + NC - 1) / NC;
+      const int e1 = (q + 1) * per < nn ? (q + 1) * per : nn;
+      double* out = pass == 1 ? Rws + nn : R;
+      for (int e = q * per + tid; e < e1; e += NT) {
         const int i = e % n, c = e / n;
-        Rk[e] = (i < c) ? L[c + i * LD] : (i == c ? piv_s[i] * rinv[i] : 0.0);
+        double s = 0.0;
+        if (i <= c) {
+          const double* pc = PU + c * (c + 1) / 2;
+          s = piv_s[i] * rinv[i] * pc[i];
+          for (int k = i + 1; k <= c; ++k) s = fma(L[k + i * LD], pc[k], s);
+        }
+        out[e] = s;
       }
     }
     CQC_MARK(8 + 8 * pass);
@@ -497,42 +593,27 @@ __global__ void __cluster_dims__(cqc::NC, 1, 1) __launch_bounds__(cqc::NT, 1)
     __syncthreads();
     CQC_MARK(9 + 8 * pass);
   }
-  // ---- Q out
-  for (int c = warp; c < n; c += NT / 32) {
-    double* qc = Q + r0 + (int64_t)c * ldq;
-    const double* tc = T + (size_t)c * ldt;
-    for (int i = lane; i < rows; i += 32) qc[i] = tc[i];
-  }
-  if (q != 0) return;
-  __syncthreads();
-  // ---- R = (R3 R2) R1 (upper triangular, ld n) by CTA 0, operands staged over the chunk
-  const int nn = n * n;
-  double* A = T;
-  double* B = T + nn;
-  double* C = T + 2 * nn;
-  for (int e = tid; e < nn; e += NT) {
-    A[e] = Rws[2 * (int64_t)nn + e];
-    B[e] = Rws[(int64_t)nn + e];
-  }
-  __syncthreads();
-  for (int e = tid; e < nn; e += NT) {
-    const int i = e % n, c = e / n;
-    double s = 0.0;
-    for (int k = i; k <= c; ++k) s = fma(A[i + k * n], B[k + c * n], s);
-    C[e] = s;
-  }
-  __syncthreads();
-  for (int e = tid; e < nn; e += NT) B[e] = Rws[e];
-  __syncthreads();
-  for (int e = tid; e < nn; e += NT) {
-    const int i = e % n, c = e / n;
-    double s = 0.0;
-    for (int k = i; k <= c; ++k) s = fma(C[i + k * n], B[k + c * n], s);
-    R[e] = i <= c ? s : 0.0;
+  // ---- Q out (TMA bulk stores of the columns when aligned)
+  const bool bulk_out = rows > 0 && (rows & 1) == 0 && (ldq & 1) == 0 && ((uintptr_t)(Q + r0) & 15) == 0;
+  if (bulk_out) {
+    if (warp == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the solve's generic writes before the async reads
+      for (int c = lane; c < n; c += 32)
+        bulk_s2g(Q + r0 + (int64_t)c * ldq, T + (size_t)c * ldt, (unsigned)(rows * 8));
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the sources read; the writes land by grid end
+    }
+  } else {
+    for (int c = warp; c < n; c += NT / 32) {
+      double* qc = Q + r0 + (int64_t)c * ldq;
+      const double* tc = T + (size_t)c * ldt;
+#pragma unroll 8
+      for (int i = lane; i < rows; i += 32) qc[i] = tc[i];
+    }
   }
 #ifdef SLRA_CQC_PROF
   __syncthreads();
-  if (tid == 0 && b == 0) {
+  if (tid == 0 && b == 0 && q == 0) {
     pt[26] = clock64();
     printf("cqc load %lld |", pt[1] - pt[0]);
     for (int p = 0; p < 3; ++p)
@@ -555,7 +636,7 @@ template <int NP>
 static bool cholqr3_cluster_fits(int64_t m, int n) {
   if (m > (int64_t)cqc::NC * 4096) return false;
   const int ldt = cqc::chunk_ld(cqc::chunk_rows(m));
-  return cqc::Lay<NP>::bytes(ldt) <= (size_t)cqc::kMaxSmem && 3 * (size_t)n * n <= (size_t)NP * ldt;
+  return cqc::Lay<NP>::bytes(ldt) <= (size_t)cqc::kMaxSmem;
 }
 
 template <int NP>
