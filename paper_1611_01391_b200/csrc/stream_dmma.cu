@@ -289,21 +289,32 @@ int launch_residual_stream_cauchy(Context* c, const double* x, const double* y, 
 }
 
 // ---------------------------------------------------------------- C = W^T B
-// W (K x r, ld ldw), B (K x n, ld ldb), C (r x n, ld ldc), r <= 64.
-// CTA = 64 output columns x one K-slice; each warp owns a K sub-slice of the
-// staged K-tile and accumulates the full r x 64 output block (up to 8 x 8
-// fragments); warps reduce through smem at the end, K-slices through a
-// deterministic split-K combine.
+// W (K x r, ld ldw), B (K x n, ld ldb), C (r x n, ld ldc), r <= 56.
+// CTA = 64 output columns x one K-slice; warp w owns columns 8 w .. 8 w + 7
+// for ALL r rows (RF 8 x 8 fragments: 2 RF accumulator registers), so there
+// is no cross-warp reduction and the register footprint is small enough for
+// two co-resident CTAs per SM (one CTA's DMMAs run while the other waits on
+// its barrier or its loads). K streams through a 4-stage cp.async ring of
+// 32-row stages (one barrier per stage); per 4-row step a warp loads RF + 1
+// fragments for RF DMMAs. K-slices go through a deterministic split-K combine.
 namespace tn {
 constexpr int NT = 256;
-constexpr int TK = 64;         // K rows per stage
+#ifndef SLRA_TN_TK
+#define SLRA_TN_TK 64
+#endif
+#ifndef SLRA_TN_NS
+#define SLRA_TN_NS 2
+#endif
+#ifndef SLRA_TN_CTAS
+#define SLRA_TN_CTAS 2
+#endif
+constexpr int TK = SLRA_TN_TK; // K rows per stage
 constexpr int TN = 64;         // output columns per CTA
-constexpr int RP = 64;         // max r
-constexpr int LDW = RP + 4;    // Ws[k][r]   (W rows are strided in global: staged via k-major chunks)
-constexpr int LDB = TK + 4;    // Bs[col][k]
-constexpr int W_D = TK * LDW;
+constexpr int NS = SLRA_TN_NS; // stages
+constexpr int CTAS = SLRA_TN_CTAS;  // co-resident CTAs per SM the launch is sized for
+constexpr int LDB = TK + 4;    // [col][k]: fragment loads hit 16 different banks per half-warp
 constexpr int B_D = TN * LDB;
-constexpr size_t SMEM = sizeof(double) * 2 * (W_D + B_D);
+inline size_t smem_bytes(int RF) { return sizeof(double) * NS * (size_t)(RF * 8 * LDB + B_D); }
 }  // namespace tn
 
 struct TnArgs {
@@ -319,14 +330,13 @@ struct TnArgs {
   int64_t ldc;
 };
 
+template <int RF>
 __device__ __forceinline__ void tn_stage(const TnArgs& a, int64_t k0, int64_t j0, int64_t kend, double* Ws,
                                          double* Bs) {
   using namespace tn;
   const int tid = threadIdx.x;
-  // W rows k0..k0+TK, columns 0..r: W is column-major (K x r): for fixed
-  // column q the rows are contiguous -> chunks of 2 rows land at Ws[k][q],
-  // Ws[k+1][q] which are NOT contiguous; stage W^T instead: Ws[q][k].
-  for (int e = tid; e < RP * (TK / 2); e += NT) {
+  // W^T tile: Ws[q][k] (W is column-major K x r: a column's rows are contiguous)
+  for (int e = tid; e < RF * 8 * (TK / 2); e += NT) {
     const int q = e / (TK / 2), ch = e % (TK / 2);
     const int64_t k = k0 + 2 * ch;
     int bytes = 0;
@@ -337,6 +347,7 @@ __device__ __forceinline__ void tn_stage(const TnArgs& a, int64_t k0, int64_t j0
     }
     cp_async16(Ws + q * LDB + 2 * ch, src, bytes);
   }
+#pragma unroll
   for (int e = tid; e < TN * (TK / 2); e += NT) {
     const int col = e / (TK / 2), ch = e % (TK / 2);
     const int64_t k = k0 + 2 * ch, cc = j0 + col;
@@ -350,81 +361,70 @@ __device__ __forceinline__ void tn_stage(const TnArgs& a, int64_t k0, int64_t j0
   }
 }
 
-template <int RF>  // RF = r rounded up to 8, in fragments of 8 (1..8)
-__global__ void __launch_bounds__(tn::NT, 1) tn_skinny_kernel(TnArgs a) {
+template <int RF>  // RF = r rounded up to 8, in fragments of 8 (1..7)
+__global__ void __launch_bounds__(tn::NT, tn::CTAS) tn_skinny_kernel(TnArgs a) {
   using namespace tn;
   extern __shared__ __align__(16) double smem[];
-  // Ws is stored [q][k] with ld LDB (same shape as Bs: 64 x TK)
-#define WB(b) (smem + (b) * B_D)
-#define BB(b) (smem + (2 + (b)) * B_D)
+  constexpr int W_D = RF * 8 * LDB;
+#define WB(b) (smem + (b) * (W_D + B_D))
+#define BB(b) (smem + (b) * (W_D + B_D) + W_D)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t j0 = (int64_t)blockIdx.x * TN;
   const int64_t kb = (int64_t)blockIdx.y * a.kslice;
   int64_t ke = kb + a.kslice;
   if (ke > a.K) ke = a.K;
-  double acc[RF][8][2];
+  const int nst = kb < ke ? (int)((ke - kb + TK - 1) / TK) : 0;
+  double acc[RF][2];
 #pragma unroll
-  for (int mi = 0; mi < RF; ++mi)
+  for (int mi = 0; mi < RF; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
 #pragma unroll
-    for (int ni = 0; ni < 8; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  int buf = 0;
-  if (kb < ke) tn_stage(a, kb, j0, ke, WB(0), BB(0));
-  cp_async_commit();
-  for (int64_t k0 = kb; k0 < ke; k0 += TK) {
-    if (k0 + TK < ke) tn_stage(a, k0 + TK, j0, ke, WB(buf ^ 1), BB(buf ^ 1));
+  for (int s = 0; s < NS - 1; ++s) {
+    if (s < nst) tn_stage<RF>(a, kb + (int64_t)s * TK, j0, ke, WB(s), BB(s));
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  int slot = 0;
+  for (int st = 0; st < nst; ++st) {
+    // stage st landed (NS - 2 newer groups may still fly); after the barrier
+    // every warp is past stage st - 1, whose slot takes stage st + NS - 1
+    cp_async_wait<NS - 2>();
     __syncthreads();
-    const double* Ws = WB(buf);
-    const double* Bs = BB(buf);
-    // warp w takes k sub-slice [w*8, w*8+8) of this stage: two k4 steps
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int kk = warp * 8 + s * 4 + t4;
-      double af[RF], bf[8];
-#pragma unroll
-      for (int mi = 0; mi < RF; ++mi) af[mi] = Ws[(mi * 8 + g) * LDB + kk];
-#pragma unroll
-      for (int ni = 0; ni < 8; ++ni) bf[ni] = Bs[(ni * 8 + g) * LDB + kk];
-#pragma unroll
-      for (int mi = 0; mi < RF; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 8; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    {
+      const int sn = st + NS - 1;
+      const int sp = (slot + NS - 1) % NS;
+      if (sn < nst) tn_stage<RF>(a, kb + (int64_t)sn * TK, j0, ke, WB(sp), BB(sp));
+      cp_async_commit();
     }
-    __syncthreads();
-    buf ^= 1;
+    const double* Ws = WB(slot) + g * LDB + t4;
+    const double* Bs = BB(slot) + (warp * 8 + g) * LDB + t4;
+#pragma unroll
+    for (int s = 0; s < TK / 4; ++s) {
+      double af[RF];
+      const double bf = Bs[4 * s];
+#pragma unroll
+      for (int mi = 0; mi < RF; ++mi) af[mi] = Ws[mi * 8 * LDB + 4 * s];
+#pragma unroll
+      for (int mi = 0; mi < RF; ++mi) dmma_8x8x4(acc[mi][0], acc[mi][1], af[mi], bf);
+    }
+    slot = (slot + 1) % NS;
   }
   cp_async_wait<0>();
 #undef WB
 #undef BB
-  // cross-warp reduction of the r x 64 block through smem (fixed order)
-  double* red = smem;  // reuse: NT/32 x (RF*8 x 64)
-  __syncthreads();
-  const int blk = RF * 8 * TN;
+  // lane (g, t4) holds C(8 mi + g, 8 warp + 2 t4 + e)
 #pragma unroll
   for (int mi = 0; mi < RF; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 8; ++ni)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int row = mi * 8 + g, col = ni * 8 + 2 * t4 + e;
-        red[warp * blk + col * (RF * 8) + row] = acc[mi][ni][e];
+    for (int e = 0; e < 2; ++e) {
+      const int row = mi * 8 + g;
+      const int64_t cc = j0 + warp * 8 + 2 * t4 + e;
+      if (row < a.r && cc < a.n) {
+        if (a.part)
+          a.part[(int64_t)blockIdx.y * a.r * a.n + row + cc * a.r] = acc[mi][e];
+        else
+          a.C[row + cc * a.ldc] = acc[mi][e];
       }
-  __syncthreads();
-  for (int e = threadIdx.x; e < blk; e += NT) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < NT / 32; ++w) s += red[w * blk + e];
-    const int row = e % (RF * 8), col = e / (RF * 8);
-    const int64_t cc = j0 + col;
-    if (row < a.r && cc < a.n) {
-      if (a.part)
-        a.part[(int64_t)blockIdx.y * a.r * a.n + row + cc * a.r] = s;
-      else
-        a.C[row + cc * a.ldc] = s;
     }
-  }
 }
 
 __global__ void splitk_sum_kernel(const double* __restrict__ part, int64_t r, int64_t n, int nz, double alpha,
@@ -443,16 +443,17 @@ int launch_tn_skinny(Context* c, const char* fam, int64_t r, int64_t n, int64_t 
   const bool aligned = ((uintptr_t)W % 16 == 0) && (ldw % 2 == 0) && ((uintptr_t)B % 16 == 0) && (ldb % 2 == 0);
   if (!aligned || r < 1 || r > 56 || K < 256) return SLRA_ERR_UNSUPPORTED;  // r > 56 would spill
   const int gx = ceil_div(n, tn::TN);
-  // split-K so that the grid fills whole waves of one CTA per SM
-  int64_t maxz = K / 512;
+  // split-K so that the grid fills whole waves of tn::CTAS CTAs per SM; every
+  // extra slice costs a partial block (written here, read by the combine)
+  const int slots = tn::CTAS * c->num_sms;
+  int64_t maxz = K / 256;
   if (maxz < 1) maxz = 1;
   int nz = 1;
   double best = 1e30;
   for (int z = 1; z <= maxz && z <= 32; ++z) {
     const double ctas = (double)gx * z;
-    const double waves = ceil(ctas / c->num_sms);
-    const double eff = ctas / (waves * c->num_sms);  // fraction of busy SM-slots
-    const double cost = waves / (double)z + (eff < 0.5 ? 1.0 : 0.0);  // time ~ waves * (K / z)
+    const double waves = ceil(ctas / slots);
+    const double cost = waves / (double)z + 0.004 * z;  // time ~ waves * (K / z) + partial traffic
     if (cost < best - 1e-9) {
       best = cost;
       nz = z;
@@ -462,15 +463,13 @@ int launch_tn_skinny(Context* c, const char* fam, int64_t r, int64_t n, int64_t 
   ks = (ks + tn::TK - 1) / tn::TK * tn::TK;
   nz = (int)((K + ks - 1) / ks);
   double* part = nullptr;
-  if (nz > 1) {
+  if (nz > 1 || alpha != 1.0) {
     part = static_cast<double*>(workspace(c, sizeof(double) * r * n * nz));
     if (!part) return SLRA_ERR_CUDA;
   }
   TnArgs a{W, ldw, B, ldb, K, n, (int)r, ks, part, Cm, ldc};
-  const size_t smem_main = tn::SMEM;
   const int RF = (int)((r + 7) / 8);
-  const size_t smem_red = sizeof(double) * (tn::NT / 32) * RF * 8 * tn::TN;
-  const size_t smem = smem_main > smem_red ? smem_main : smem_red;
+  const size_t smem = tn::smem_bytes(RF);
   dim3 grid(gx, nz);
 #define SLRA_TN_CASE(RFV)                                                                                     \
   case RFV:                                                                                                   \
@@ -489,8 +488,7 @@ int launch_tn_skinny(Context* c, const char* fam, int64_t r, int64_t n, int64_t 
   }
 #undef SLRA_TN_CASE
   SLRA_CHECK_LAUNCH(c);
-  if (nz > 1 || alpha != 1.0) {
-    if (nz == 1) return SLRA_ERR_UNSUPPORTED;  // (alpha != 1 without split: not used on the path)
+  if (part) {
     int rg = ceil_div(r * n, 256);
     if (rg > c->num_sms * 8) rg = c->num_sms * 8;
     SLRA_TIMED(c, "gemm_reduce", splitk_sum_kernel<<<rg, 256, 0, c->stream>>>(part, r, n, nz, alpha, Cm, ldc);)
