@@ -294,9 +294,9 @@ int launch_residual_stream_cauchy(Context* c, const double* x, const double* y, 
 // for ALL r rows (RF 8 x 8 fragments: 2 RF accumulator registers), so there
 // is no cross-warp reduction and the register footprint is small enough for
 // two co-resident CTAs per SM (one CTA's DMMAs run while the other waits on
-// its barrier or its loads). K streams through a 4-stage cp.async ring of
-// 32-row stages (one barrier per stage); per 4-row step a warp loads RF + 1
-// fragments for RF DMMAs. K-slices go through a deterministic split-K combine.
+// its barrier or its loads). K streams through a cp.async ring of TK-row
+// stages (one barrier per stage); per 4-row step a warp loads RF + 1
+// fragments for RF DMMAs. The K dimension is split stream-K style (below).
 namespace tn {
 constexpr int NT = 256;
 #ifndef SLRA_TN_TK
@@ -324,11 +324,19 @@ struct TnArgs {
   int64_t ldb;
   int64_t K, n;
   int r;
-  int64_t kslice;
-  double* part;  // split-K partials: [z][r x n] (ld r), or null -> C directly
-  double* C;
-  int64_t ldc;
+  int S;         // stages per column tile (ceil(K / TK))
+  int64_t U;     // stage units in all: column tiles x S
+  double* part;  // partial blocks: [piece][r x n] (ld r)
 };
+// Stream-K split: the flattened (column tile, stage) units are cut into
+// gridDim.x equal contiguous ranges — every CTA runs the same number of
+// stages (+-1) whatever n and K are, so there is no partial last wave. A
+// range that crosses a tile boundary ends one partial block and starts the
+// next; the piece index of a segment is its CTA's distance from the first
+// CTA that touches the tile, so the combine adds the pieces of a tile in CTA
+// order (deterministic).
+__host__ __device__ inline int64_t tn_first_unit(int64_t i, int64_t U, int64_t G) { return i * U / G; }
+__host__ __device__ inline int64_t tn_owner(int64_t u, int64_t U, int64_t G) { return ((u + 1) * G - 1) / U; }
 
 template <int RF>
 __device__ __forceinline__ void tn_stage(const TnArgs& a, int64_t k0, int64_t j0, int64_t kend, double* Ws,
@@ -370,70 +378,89 @@ __global__ void __launch_bounds__(tn::NT, tn::CTAS) tn_skinny_kernel(TnArgs a) {
 #define BB(b) (smem + (b) * (W_D + B_D) + W_D)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int64_t j0 = (int64_t)blockIdx.x * TN;
-  const int64_t kb = (int64_t)blockIdx.y * a.kslice;
-  int64_t ke = kb + a.kslice;
-  if (ke > a.K) ke = a.K;
-  const int nst = kb < ke ? (int)((ke - kb + TK - 1) / TK) : 0;
-  double acc[RF][2];
+  const int64_t G = gridDim.x;
+  int64_t u = tn_first_unit(blockIdx.x, a.U, G);
+  const int64_t u1 = tn_first_unit(blockIdx.x + 1, a.U, G);
+  while (u < u1) {
+    const int64_t jt = u / a.S;
+    const int sa = (int)(u - jt * a.S);
+    const int nst = (int)((u1 - u) < (a.S - sa) ? (u1 - u) : (a.S - sa));
+    const int64_t j0 = jt * TN, kb = (int64_t)sa * TK, ke = a.K;
+    double acc[RF][2];
 #pragma unroll
-  for (int mi = 0; mi < RF; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
+    for (int mi = 0; mi < RF; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
 #pragma unroll
-  for (int s = 0; s < NS - 1; ++s) {
-    if (s < nst) tn_stage<RF>(a, kb + (int64_t)s * TK, j0, ke, WB(s), BB(s));
-    cp_async_commit();
-  }
-  int slot = 0;
-  for (int st = 0; st < nst; ++st) {
-    // stage st landed (NS - 2 newer groups may still fly); after the barrier
-    // every warp is past stage st - 1, whose slot takes stage st + NS - 1
-    cp_async_wait<NS - 2>();
-    __syncthreads();
-    {
-      const int sn = st + NS - 1;
-      const int sp = (slot + NS - 1) % NS;
-      if (sn < nst) tn_stage<RF>(a, kb + (int64_t)sn * TK, j0, ke, WB(sp), BB(sp));
+    for (int s = 0; s < NS - 1; ++s) {
+      if (s < nst) tn_stage<RF>(a, kb + (int64_t)s * TK, j0, ke, WB(s), BB(s));
       cp_async_commit();
     }
-    const double* Ws = WB(slot) + g * LDB + t4;
-    const double* Bs = BB(slot) + (warp * 8 + g) * LDB + t4;
+    int slot = 0;
+    for (int st = 0; st < nst; ++st) {
+      // stage st landed (NS - 2 newer groups may still fly); after the barrier
+      // every warp is past stage st - 1, whose slot takes stage st + NS - 1
+      cp_async_wait<NS - 2>();
+      __syncthreads();
+      {
+        const int sn = st + NS - 1;
+        const int sp = (slot + NS - 1) % NS;
+        if (sn < nst) tn_stage<RF>(a, kb + (int64_t)sn * TK, j0, ke, WB(sp), BB(sp));
+        cp_async_commit();
+      }
+      const double* Ws = WB(slot) + g * LDB + t4;
+      const double* Bs = BB(slot) + (warp * 8 + g) * LDB + t4;
 #pragma unroll
-    for (int s = 0; s < TK / 4; ++s) {
-      double af[RF];
-      const double bf = Bs[4 * s];
+      for (int s = 0; s < TK / 4; ++s) {
+        double af[RF];
+        const double bf = Bs[4 * s];
 #pragma unroll
-      for (int mi = 0; mi < RF; ++mi) af[mi] = Ws[mi * 8 * LDB + 4 * s];
+        for (int mi = 0; mi < RF; ++mi) af[mi] = Ws[mi * 8 * LDB + 4 * s];
 #pragma unroll
-      for (int mi = 0; mi < RF; ++mi) dmma_8x8x4(acc[mi][0], acc[mi][1], af[mi], bf);
+        for (int mi = 0; mi < RF; ++mi) dmma_8x8x4(acc[mi][0], acc[mi][1], af[mi], bf);
+      }
+      slot = (slot + 1) % NS;
     }
-    slot = (slot + 1) % NS;
+    cp_async_wait<0>();
+    // lane (g, t4) holds C(8 mi + g, 8 warp + 2 t4 + e) of this segment
+    const int64_t piece = (int64_t)blockIdx.x - tn_owner(jt * a.S, a.U, G);
+    double* out = a.part + piece * a.r * a.n;
+#pragma unroll
+    for (int mi = 0; mi < RF; ++mi)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = mi * 8 + g;
+        const int64_t cc = j0 + warp * 8 + 2 * t4 + e;
+        if (row < a.r && cc < a.n) out[row + cc * a.r] = acc[mi][e];
+      }
+    u += nst;
+    __syncthreads();  // every warp is done with the ring before the next segment refills it
   }
-  cp_async_wait<0>();
 #undef WB
 #undef BB
-  // lane (g, t4) holds C(8 mi + g, 8 warp + 2 t4 + e)
-#pragma unroll
-  for (int mi = 0; mi < RF; ++mi)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int row = mi * 8 + g;
-      const int64_t cc = j0 + warp * 8 + 2 * t4 + e;
-      if (row < a.r && cc < a.n) {
-        if (a.part)
-          a.part[(int64_t)blockIdx.y * a.r * a.n + row + cc * a.r] = acc[mi][e];
-        else
-          a.C[row + cc * a.ldc] = acc[mi][e];
-      }
-    }
 }
 
-__global__ void splitk_sum_kernel(const double* __restrict__ part, int64_t r, int64_t n, int nz, double alpha,
-                                  double* __restrict__ Cm, int64_t ldc) {
-  const int64_t total = r * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+// C = alpha * (sum of the pieces of each column tile, in CTA order). Block
+// (q, jt) takes a quarter (16 columns) of column tile jt: the piece count is
+// computed once per block and every piece's load is in flight before the sum.
+__global__ void __launch_bounds__(256) streamk_sum_kernel(const double* __restrict__ part, int r, int64_t n, int S,
+                                                          int64_t U, int64_t G, double alpha,
+                                                          double* __restrict__ Cm, int64_t ldc) {
+  const int64_t jt = blockIdx.y;
+  const int cnt = (int)(tn_owner(jt * S + S - 1, U, G) - tn_owner(jt * S, U, G)) + 1;
+  const int64_t total = (int64_t)r * n;
+  const int64_t c0 = jt * tn::TN + blockIdx.x * 16;
+  for (int e = threadIdx.x; e < 16 * r; e += 256) {
+    const int col = e / r, row = e - col * r;
+    const int64_t cc = c0 + col;
+    if (cc >= n) continue;
+    const double* p = part + row + cc * r;
     double s = 0.0;
-    for (int z = 0; z < nz; ++z) s += part[z * total + e];
-    Cm[(e % r) + (e / r) * ldc] = alpha * s;
+    int z = 0;
+    for (; z + 4 <= cnt; z += 4) {
+      const double v0 = p[z * total], v1 = p[(z + 1) * total], v2 = p[(z + 2) * total], v3 = p[(z + 3) * total];
+      s = ((s + v0) + v1) + v2 + v3;
+    }
+    for (; z < cnt; ++z) s += p[z * total];
+    Cm[row + cc * ldc] = alpha * s;
   }
 }
 
@@ -443,34 +470,22 @@ int launch_tn_skinny(Context* c, const char* fam, int64_t r, int64_t n, int64_t 
   const bool aligned = ((uintptr_t)W % 16 == 0) && (ldw % 2 == 0) && ((uintptr_t)B % 16 == 0) && (ldb % 2 == 0);
   if (!aligned || r < 1 || r > 56 || K < 256) return SLRA_ERR_UNSUPPORTED;  // r > 56 would spill
   const int gx = ceil_div(n, tn::TN);
-  // split-K so that the grid fills whole waves of tn::CTAS CTAs per SM; every
-  // extra slice costs a partial block (written here, read by the combine)
-  const int slots = tn::CTAS * c->num_sms;
-  int64_t maxz = K / 256;
-  if (maxz < 1) maxz = 1;
-  int nz = 1;
-  double best = 1e30;
-  for (int z = 1; z <= maxz && z <= 32; ++z) {
-    const double ctas = (double)gx * z;
-    const double waves = ceil(ctas / slots);
-    const double cost = waves / (double)z + 0.004 * z;  // time ~ waves * (K / z) + partial traffic
-    if (cost < best - 1e-9) {
-      best = cost;
-      nz = z;
-    }
+  if (gx > 65535) return SLRA_ERR_UNSUPPORTED;  // the combine's grid.y (caller falls back to the generic GEMM)
+  const int S = ceil_div(K, tn::TK);
+  const int64_t U = (int64_t)gx * S;
+  const int64_t slots = (int64_t)tn::CTAS * c->num_sms;
+  const int64_t G = U < slots ? U : slots;
+  int pmax = 1;  // most pieces of one column tile
+  for (int64_t jt = 0; jt < gx; ++jt) {
+    const int cnt = (int)(tn_owner(jt * S + S - 1, U, G) - tn_owner(jt * S, U, G)) + 1;
+    if (cnt > pmax) pmax = cnt;
   }
-  int64_t ks = (K + nz - 1) / nz;
-  ks = (ks + tn::TK - 1) / tn::TK * tn::TK;
-  nz = (int)((K + ks - 1) / ks);
-  double* part = nullptr;
-  if (nz > 1 || alpha != 1.0) {
-    part = static_cast<double*>(workspace(c, sizeof(double) * r * n * nz));
-    if (!part) return SLRA_ERR_CUDA;
-  }
-  TnArgs a{W, ldw, B, ldb, K, n, (int)r, ks, part, Cm, ldc};
+  double* part = static_cast<double*>(workspace(c, sizeof(double) * r * n * pmax));
+  if (!part) return SLRA_ERR_CUDA;
+  TnArgs a{W, ldw, B, ldb, K, n, (int)r, S, U, part};
   const int RF = (int)((r + 7) / 8);
   const size_t smem = tn::smem_bytes(RF);
-  dim3 grid(gx, nz);
+  dim3 grid((unsigned)G);
 #define SLRA_TN_CASE(RFV)                                                                                     \
   case RFV:                                                                                                   \
     SLRA_CUDA(cudaFuncSetAttribute(tn_skinny_kernel<RFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
@@ -488,12 +503,9 @@ int launch_tn_skinny(Context* c, const char* fam, int64_t r, int64_t n, int64_t 
   }
 #undef SLRA_TN_CASE
   SLRA_CHECK_LAUNCH(c);
-  if (part) {
-    int rg = ceil_div(r * n, 256);
-    if (rg > c->num_sms * 8) rg = c->num_sms * 8;
-    SLRA_TIMED(c, "gemm_reduce", splitk_sum_kernel<<<rg, 256, 0, c->stream>>>(part, r, n, nz, alpha, Cm, ldc);)
-    SLRA_CHECK_LAUNCH(c);
-  }
+  SLRA_TIMED(c, "gemm_reduce", streamk_sum_kernel<<<dim3(4, (unsigned)gx), 256, 0, c->stream>>>(part, (int)r, n, S, U,
+                                                                                              G, alpha, Cm, ldc);)
+  SLRA_CHECK_LAUNCH(c);
   return SLRA_OK;
 }
 
