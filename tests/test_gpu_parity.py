@@ -140,7 +140,12 @@ def test_numerical_rank_and_pinv(slra):
 
 
 @pytest.mark.parametrize("ta,tb,m,n,k", [(0, 0, 64, 64, 64), (1, 0, 32, 4096, 4096), (0, 1, 100, 37, 23),
-                                         (1, 1, 7, 9, 130), (0, 0, 4096, 48, 48), (1, 0, 257, 257, 4096)])
+                                         (1, 1, 7, 9, 130), (0, 0, 4096, 48, 48), (1, 0, 257, 257, 4096),
+                                         # the stream-K skinny W^T B kernel: ragged n and K, r = 1 .. 56, fewer
+                                         # stage units than CTAs, many column tiles over a short K, one tile
+                                         # over a long K; odd K (unaligned: the generic kernel)
+                                         (1, 0, 13, 1000, 1026), (1, 0, 56, 130, 4098), (1, 0, 1, 70, 256),
+                                         (1, 0, 48, 5000, 300), (1, 0, 33, 64, 20000), (1, 0, 8, 3, 777)])
 def test_gemm_vs_numpy(slra, ta, tb, m, n, k):
     import ctypes
     import torch
@@ -159,6 +164,14 @@ def test_gemm_vs_numpy(slra, ta, tb, m, n, k):
     torch.cuda.synchronize()
     ref = (A.t() if ta else A) @ (B.t() if tb else B)
     assert torch.allclose(C.t().cpu(), ref, atol=1e-12 * k ** 0.5 * 4)
+    # alpha != 1, and the same bits on a second call (fixed-order combines)
+    C2 = torch.zeros_like(C)
+    for out in (C, C2):
+        assert lib.slra_gemm(ctx, ta, tb, m, n, k, ctypes.c_double(-2.5), Af.data_ptr(), A.shape[0], Bf.data_ptr(),
+                             B.shape[0], ctypes.c_double(0.0), out.data_ptr(), m) == 0
+    torch.cuda.synchronize()
+    assert torch.allclose(C.t().cpu(), -2.5 * ref, atol=1e-12 * k ** 0.5 * 10)
+    assert torch.equal(C, C2)
     lib.slra_ctx_destroy(ctx)
 
 
