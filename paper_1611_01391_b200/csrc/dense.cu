@@ -334,7 +334,10 @@ __global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict_
   // odd leading dimensions for the Jacobi operands: the 8-lane groups of a
   // warp read four different columns, which an even ld would put on the
   // same banks
-  const int ldw = p | 1, ldv = q | 1;
+  // (square p = q in {16, 32, 48, 64}: even, and the Jacobi moves 16-byte row
+  // pairs — conflict-free for any pair of columns, dense_cta.cuh)
+  const bool vec = p == q && (p & 15) == 0 && p <= 64;
+  const int ldw = vec ? p : (p | 1), ldv = vec ? q : (q | 1);
   double* W = sm;                     // p x q (ld ldw)
   double* V = W + (size_t)ldw * q;    // q x q (ld ldv)
   double* Ss = V + (size_t)ldv * q;   // p x q
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(kSVT) svd_cta_kernel(const double* __restrict_
       else W[j + i * ldw] = x;
     }
   __syncthreads();
-  cta_jacobi<kSVT>(W, ldw, p, q, V, ldv, flag, deflate);
+  cta_jacobi<kSVT, 256, true>(W, ldw, p, q, V, ldv, flag, deflate);
   cta_svd_finish<kSVT>(W, ldw, p, q, V, ldv, sg, order, Ss, p, Ts, q, tmp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (!tall) {

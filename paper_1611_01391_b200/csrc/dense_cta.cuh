@@ -925,9 +925,15 @@ __device__ inline JacobiShared& jacobi_shared() {
   return s;
 }
 
-template <int NT, int RPG, bool EXACT>
+template <int NT, int RPG, bool EXACT, bool VEC2 = false>
 __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate) {
-  // RPG rows per lane (p <= 8 RPG, n <= p); EXACT: p == n == 8 RPG (no row predicates)
+  // RPG rows per lane (p <= 8 RPG, n <= p); EXACT: p == n == 8 RPG (no row predicates).
+  // VEC2 (EXACT, RPG even, even ldw / ldv): a lane owns row pairs 2 sub + 16 rr
+  // and moves them as 16-byte accesses — an 8-lane group then covers all 32
+  // banks once per access whatever columns the other groups of the warp read
+  // (with 8-byte accesses two groups of a half-warp collide on most column
+  // pairs: the load and store phases of a round were shared-memory bound)
+  static_assert(!VEC2 || (EXACT && RPG % 2 == 0), "VEC2 needs p == n == 8 RPG, RPG even");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = lane >> 3, sub = lane & 7;
   constexpr int NW = NT / 32;
@@ -962,6 +968,14 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
   __syncthreads();
   const int npairs = ne / 2;
   const int iters = (npairs + 4 * NW - 1) / (4 * NW);
+#ifdef SLRA_JAC_PROF
+  long long jp[6] = {0, 0, 0, 0, 0, 0};
+  long long jt0 = 0, jt1 = 0;
+  int jrounds = 0;
+#define JAC_MARK(i) do { jt1 = clock64(); jp[i] += jt1 - jt0; jt0 = jt1; } while (0)
+#else
+#define JAC_MARK(i) do { } while (0)
+#endif
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rot_any = 0;  // this thread rotated a pair during the sweep
     double thr2 = 0.0;
@@ -984,6 +998,10 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
     }
     int ab_next = pair_tab[(warp * 4 + grp) < npairs ? (warp * 4 + grp) : 0];
     for (int rd = 0; rd < ne - 1; ++rd) {
+#ifdef SLRA_JAC_PROF
+      jt0 = clock64();
+      ++jrounds;
+#endif
       for (int it = 0; it < iters; ++it) {
         const int pi = (warp + it * NW) * 4 + grp;
         const int ab = (iters == 1) ? ab_next : pair_tab[rd * npairs + (pi < npairs ? pi : 0)];
@@ -997,13 +1015,28 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
         // before the reduction and rotation chain starts
         double x[RPG], y[RPG], u[RPG], v[RPG];
         double aa = 0.0, bb = 0.0, gg = 0.0;
+        if constexpr (VEC2) {
 #pragma unroll
-        for (int r = 0; r < RPG; ++r) {
-          const int i = sub + 8 * r;
-          x[r] = (EXACT || i < p) ? wp[i] : 0.0;
-          y[r] = (EXACT || i < p) ? wq[i] : 0.0;
-          u[r] = (EXACT || i < n) ? vp[i] : 0.0;
-          v[r] = (EXACT || i < n) ? vq[i] : 0.0;
+          for (int rr = 0; rr < RPG / 2; ++rr) {
+            const int i = 2 * sub + 16 * rr;
+            const double2 tx = *reinterpret_cast<const double2*>(wp + i);
+            const double2 ty = *reinterpret_cast<const double2*>(wq + i);
+            const double2 tu = *reinterpret_cast<const double2*>(vp + i);
+            const double2 tv = *reinterpret_cast<const double2*>(vq + i);
+            x[2 * rr] = tx.x, x[2 * rr + 1] = tx.y;
+            y[2 * rr] = ty.x, y[2 * rr + 1] = ty.y;
+            u[2 * rr] = tu.x, u[2 * rr + 1] = tu.y;
+            v[2 * rr] = tv.x, v[2 * rr + 1] = tv.y;
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < RPG; ++r) {
+            const int i = sub + 8 * r;
+            x[r] = (EXACT || i < p) ? wp[i] : 0.0;
+            y[r] = (EXACT || i < p) ? wq[i] : 0.0;
+            u[r] = (EXACT || i < n) ? vp[i] : 0.0;
+            v[r] = (EXACT || i < n) ? vq[i] : 0.0;
+          }
         }
         {  // two accumulators per product: FP64 FMA latency is ~24 cycles on sm_100
           double a1 = 0.0, b1 = 0.0, g1 = 0.0;
@@ -1025,12 +1058,14 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
           bb += b1;
           gg += g1;
         }
+        JAC_MARK(0);  // loads + partial dots
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) {  // within the 8-lane group
           aa += __shfl_xor_sync(0xffffffffu, aa, o);
           bb += __shfl_xor_sync(0xffffffffu, bb, o);
           gg += __shfl_xor_sync(0xffffffffu, gg, o);
         }
+        JAC_MARK(1);  // shuffle reduction
         // the next round's pair, read before this round's barrier
         if (iters == 1 && rd + 1 < ne - 1) ab_next = pair_tab[(rd + 1) * npairs + (pi < npairs ? pi : 0)];
         // |g| <= tol sqrt(a b), squared (no sqrt on the chain)
@@ -1041,34 +1076,69 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
         // (common.cuh: jacobi_rotation). This chain is most of a round.
         double cs, sn;
         jacobi_rotation(aa, bb, gg, cs, sn);
+#ifdef SLRA_JAC_PROF
+        jp[5] += (long long)(cs != 2.0);  // keeps the rotation before the mark
+#endif
+        JAC_MARK(2);  // rotation
+        if constexpr (VEC2) {
 #pragma unroll
-        for (int r = 0; r < RPG; ++r) {
-          const int i = sub + 8 * r;
-          if (EXACT || i < p) {
-            wp[i] = cs * x[r] - sn * y[r];
-            wq[i] = sn * x[r] + cs * y[r];
+          for (int rr = 0; rr < RPG / 2; ++rr) {
+            const int i = 2 * sub + 16 * rr, r = 2 * rr;
+            *reinterpret_cast<double2*>(wp + i) = make_double2(cs * x[r] - sn * y[r], cs * x[r + 1] - sn * y[r + 1]);
+            *reinterpret_cast<double2*>(wq + i) = make_double2(sn * x[r] + cs * y[r], sn * x[r + 1] + cs * y[r + 1]);
+            *reinterpret_cast<double2*>(vp + i) = make_double2(cs * u[r] - sn * v[r], cs * u[r + 1] - sn * v[r + 1]);
+            *reinterpret_cast<double2*>(vq + i) = make_double2(sn * u[r] + cs * v[r], sn * u[r + 1] + cs * v[r + 1]);
           }
-          if (EXACT || i < n) {
-            vp[i] = cs * u[r] - sn * v[r];
-            vq[i] = sn * u[r] + cs * v[r];
+        } else {
+#pragma unroll
+          for (int r = 0; r < RPG; ++r) {
+            const int i = sub + 8 * r;
+            if (EXACT || i < p) {
+              wp[i] = cs * x[r] - sn * y[r];
+              wq[i] = sn * x[r] + cs * y[r];
+            }
+            if (EXACT || i < n) {
+              vp[i] = cs * u[r] - sn * v[r];
+              vq[i] = sn * u[r] + cs * v[r];
+            }
           }
         }
         rot_any = 1;
+        JAC_MARK(3);  // apply + stores
       }
+#ifdef SLRA_JAC_PROF
+      jt0 = clock64();
+#endif
       __syncthreads();
+      JAC_MARK(4);  // barrier
     }
     if (tid == 0) flag[2] = sweep + 1;  // sweeps used (diagnostics)
     if (!__syncthreads_or(rot_any)) break;
   }
+#ifdef SLRA_JAC_PROF
+  if (tid == 0 && blockIdx.x == 0)
+    printf("jacobi %dx%d sweeps %d rounds %d | per round: loads+dots %lld shuffles %lld rotation %lld apply %lld barrier %lld (rotated %lld)\n",
+           p, n, flag[2], jrounds, jp[0] / jrounds, jp[1] / jrounds, jp[2] / jrounds, jp[3] / jrounds, jp[4] / jrounds,
+           jp[5]);
+#endif
+#undef JAC_MARK
 }
 
 // PMAX < 256: only the rows-per-lane variants up to PMAX / 8 are instantiated
 // (callers with a register budget, p <= PMAX guaranteed).
-template <int NT, int PMAX = 256>
+template <int NT, int PMAX = 256, bool VEC = false>
 __device__ void cta_jacobi(double* W, int ldw, int p, int n, double* V, int ldv, int* flag, double deflate = 0.0) {
   if (p <= 64) {
     const int rpg = (p + 7) / 8;
     const bool exact = p == 8 * rpg && n == p;
+    if constexpr (VEC) {  // 16-byte row pairs (even leading dimensions, 16-byte aligned W and V)
+      if (exact && ((ldw | ldv) & 1) == 0) {
+        if (rpg == 2) return cta_jacobi_g8<NT, 2, true, true>(W, ldw, p, n, V, ldv, flag, deflate);
+        if (rpg == 4) return cta_jacobi_g8<NT, 4, true, true>(W, ldw, p, n, V, ldv, flag, deflate);
+        if (rpg == 6) return cta_jacobi_g8<NT, 6, true, true>(W, ldw, p, n, V, ldv, flag, deflate);
+        if (rpg == 8) return cta_jacobi_g8<NT, 8, true, true>(W, ldw, p, n, V, ldv, flag, deflate);
+      }
+    }
 #define SLRA_G8(R)                                                                   \
   if constexpr (R <= (PMAX + 7) / 8) {                                               \
     if (rpg == R) {                                                                  \
