@@ -1021,13 +1021,9 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
             const int i = 2 * sub + 16 * rr;
             const double2 tx = *reinterpret_cast<const double2*>(wp + i);
             const double2 ty = *reinterpret_cast<const double2*>(wq + i);
-            const double2 tu = *reinterpret_cast<const double2*>(vp + i);
-            const double2 tv = *reinterpret_cast<const double2*>(vq + i);
             x[2 * rr] = tx.x, x[2 * rr + 1] = tx.y;
             y[2 * rr] = ty.x, y[2 * rr + 1] = ty.y;
-            u[2 * rr] = tu.x, u[2 * rr + 1] = tu.y;
-            v[2 * rr] = tv.x, v[2 * rr + 1] = tv.y;
-          }
+          }  // (the V rows are loaded after the rotate / skip decision, behind the rotation's arithmetic)
         } else {
 #pragma unroll
           for (int r = 0; r < RPG; ++r) {
@@ -1074,6 +1070,16 @@ __device__ void cta_jacobi_g8(double* W, int ldw, int p, int n, double* V, int l
         // t = sign(z) / (|z| + sqrt(1 + z^2)), z = (b - a) / (2g), from the
         // hardware rsqrt / rcp seeds; c refined to full precision
         // (common.cuh: jacobi_rotation). This chain is most of a round.
+        if constexpr (VEC2) {
+#pragma unroll
+          for (int rr = 0; rr < RPG / 2; ++rr) {
+            const int i = 2 * sub + 16 * rr;
+            const double2 tu = *reinterpret_cast<const double2*>(vp + i);
+            const double2 tv = *reinterpret_cast<const double2*>(vq + i);
+            u[2 * rr] = tu.x, u[2 * rr + 1] = tu.y;
+            v[2 * rr] = tv.x, v[2 * rr + 1] = tv.y;
+          }
+        }
         double cs, sn;
         jacobi_rotation(aa, bb, gg, cs, sn);
 #ifdef SLRA_JAC_PROF
