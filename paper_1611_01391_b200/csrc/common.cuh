@@ -65,25 +65,29 @@ __device__ __forceinline__ double fast_sqrt(double x) {
 __device__ __forceinline__ void jacobi_rotation(double a, double b, double g, double& cs, double& sn) {
   const double d = b - a, g2 = 2.0 * g;
   const double h = fma(d, d, g2 * g2);
-  if (!(h < DBL_MAX) || h < DBL_MIN) {
-    // overflowing (column norms above ~1e154) or subnormal Gram entries: the
+  if (!(h < 0.125 * DBL_MAX) || h < DBL_MIN) {
+    // overflowing (column norms above ~1e154; 4 h is formed below) or subnormal Gram entries: the
     // IEEE sqrt / divide (the MUFU seeds would give inf * 0 or flush to zero)
     const double t = (g2 * g2 < 1e-17 * (d * d)) ? g2 / (2.0 * d) : copysign(1.0, d) * g2 / (fabs(d) + sqrt(h));
     cs = 1.0 / sqrt(fma(t, t, 1.0));
     sn = cs * t;
     return;
   }
-  const double rr = (g2 * g2 < 1e-17 * (d * d)) ? fabs(d) : h * mufu_rsqrt(h);
-  const double t = copysign(1.0, d) * g2 * mufu_rcp(fabs(d) + rr);
-  const double q = fma(t, t, 1.0);
-  double y = mufu_rsqrt(q);
-  const double hq = 0.5 * q;
-#pragma unroll
-  for (int it = 0; it < 2; ++it) y = y * fma(-hq * y, y, 1.5);  // y <- y (3 - q y^2) / 2
-  cs = y;
-  sn = y * t;
+  // c = w / sqrt(2 s w), s = sign(d) g2 / sqrt(2 s w) with s = sqrt(h), w = |d| + s
+  // (t = g2 / w, 1 + t^2 = 2 s / w): both square roots from the MUFU seed (the
+  // angle is then off by ~2^-22, as before), and the pair (c, s) renormalised to
+  // c^2 + s^2 = 1 by the second-order series of rsqrt(1 + e), e = c^2 + s^2 - 1
+  // ~ 2^-21 (e^3 is below the rounding): 13 dependent operations instead of 17
+  // (FP64 dependent latency is what a Jacobi round is made of).
+  const double s = h * mufu_rsqrt(h);
+  const double w = fabs(d) + s;
+  const double rz = mufu_rsqrt(2.0 * s * w);
+  const double c0 = w * rz, s0 = copysign(g2, d * g2) * rz;
+  const double e = fma(c0, c0, fma(s0, s0, -1.0));
+  const double f = fma(e, fma(0.375, e, -0.5), 1.0);
+  cs = c0 * f;
+  sn = s0 * f;
 }
-
 
 // ------------------------------------------------------------------ context
 constexpr int kArenaSlots = 14;
