@@ -43,16 +43,37 @@ __device__ __forceinline__ void house_make(double* x, int j, int m, double s, do
       if (i > j && i < m) x[i] = 0.0;
     }
   } else {
-    // FAST: MUFU-seeded sqrt / reciprocals (common.cuh), ~1 ulp
-    beta = FAST ? fast_sqrt(c0 * c0 + s) : sqrt(c0 * c0 + s);
-    if (c0 >= 0.0) beta = -beta;
-    const double rden = FAST ? fast_rcp(c0 - beta) : 1.0 / (c0 - beta);  // essential = tail / (c0 - beta)
+    double rden;
+    if constexpr (FAST) {
+      // MUFU-seeded, ~1 ulp, and arranged for the shortest dependent chain
+      // (FP64 dependent latency is ~35-40 cycles and this runs once per
+      // column on the critical path): y = rsqrt(v) by one cubically
+      // convergent step from the seed; c0 - beta = sgn (|c0| + v y) needs no
+      // corrected sqrt; tau = (beta - c0) / beta = 1 + |c0| y needs no
+      // division; beta = -sgn sqrt(v) (corrected) is off the chain.
+      const double v = fma(c0, c0, s), ac = fabs(c0);
+      const double y0 = mufu_rsqrt(v);
+      const double e = fma(-(v * y0), y0, 1.0);
+      const double y = fma(y0, e * fma(0.375, e, 0.5), y0);
+      const double den = fma(v, y, ac);
+      const double r0 = mufu_rcp(den);
+      const double er = fma(-den, r0, 1.0);
+      rden = copysign(fma(r0, fma(er, er, er), r0), c0 >= 0.0 ? 1.0 : -1.0);
+      const double sq = v * y;
+      const double sqc = fma(0.5 * y, fma(-sq, sq, v), sq);
+      beta = c0 >= 0.0 ? -sqc : sqc;
+      t = fma(ac, y, 1.0);
+    } else {
+      beta = sqrt(c0 * c0 + s);
+      if (c0 >= 0.0) beta = -beta;
+      rden = 1.0 / (c0 - beta);  // essential = tail / (c0 - beta)
+      t = (beta - c0) / beta;
+    }
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const int i = lane + 32 * r;
       if (i > j && i < m) x[i] *= rden;
     }
-    t = FAST ? (beta - c0) * fast_rcp(beta) : (beta - c0) / beta;
   }
   __syncwarp();
   if (lane == 0) {
