@@ -62,6 +62,27 @@ __device__ __forceinline__ double fast_sqrt(double x) {
   const double r = fma(0.5 * y, fma(-s, s, x), s);
   return x > 0.0 ? r : x;  // sqrt(0) = 0 (rsqrt(0) = inf)
 }
+// Householder reflector scalars of makeHouseholder (c0 the pivot entry, tail the
+// squared norm of the entries below it, tail > DBL_MIN): beta = -sgn sqrt(v),
+// rden = 1 / (c0 - beta) = sgn / (|c0| + sqrt(v)), tau = (beta - c0) / beta =
+// 1 + |c0| / sqrt(v), v = c0^2 + tail — arranged for the shortest dependent
+// chain (one cubic step from each MUFU seed, no corrected sqrt and no division
+// on the way to rden; FP64 dependent latency is ~35-40 cycles and a reflector
+// sits on the critical path of every pivot). ~1 ulp, not correctly rounded.
+__device__ __forceinline__ void fast_reflector(double c0, double tail, double& beta, double& rden, double& tau) {
+  const double v = fma(c0, c0, tail), ac = fabs(c0);
+  const double y0 = mufu_rsqrt(v);
+  const double e = fma(-(v * y0), y0, 1.0);
+  const double y = fma(y0, e * fma(0.375, e, 0.5), y0);
+  const double den = fma(v, y, ac);
+  const double r0 = mufu_rcp(den);
+  const double er = fma(-den, r0, 1.0);
+  rden = copysign(fma(r0, fma(er, er, er), r0), c0 >= 0.0 ? 1.0 : -1.0);
+  const double sq = v * y;
+  const double sqc = fma(0.5 * y, fma(-sq, sq, v), sq);
+  beta = c0 >= 0.0 ? -sqc : sqc;
+  tau = fma(ac, y, 1.0);
+}
 __device__ __forceinline__ void jacobi_rotation(double a, double b, double g, double& cs, double& sn) {
   const double d = b - a, g2 = 2.0 * g;
   const double h = fma(d, d, g2 * g2);

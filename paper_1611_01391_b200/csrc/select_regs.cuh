@@ -165,10 +165,10 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
       const double tail = warp_sum(lane > k && lane < r ? xl * xl : 0.0);
       // tail == 0: Eigen's tau = 0, beta = c0
       const bool zero = tail <= DBL_MIN;
-      double beta = fast_sqrt(fma(c0, c0, tail));
-      beta = c0 >= 0.0 ? -beta : beta;
+      double beta, rden, tauk;
+      fast_reflector(c0, zero ? 1.0 : tail, beta, rden, tauk);
       beta = zero ? c0 : beta;
-      const double rden = zero ? 0.0 : fast_rcp(c0 - beta);
+      rden = zero ? 0.0 : rden;
       if (lane < RMAX) {
         s.v[lane] = lane < k ? 0.0 : (lane == k ? 1.0 : (lane < r ? xl * rden : 0.0));
         // column k of R: entries above the diagonal (this pivot column after
@@ -176,7 +176,7 @@ __device__ int cta_select_regs(const double* Q, int ldq, int m, int r, double h,
         s.R[lane + k * s.ldr] = lane < k ? xl : (lane == k ? beta : 0.0);
       }
       if (lane == 0) {
-        s.tau[0] = zero ? 0.0 : (beta - c0) * fast_rcp(beta);
+        s.tau[0] = zero ? 0.0 : tauk;
         s.pv[k] = best.v;
         I_out[k] = (tid & ~31) + wl;
       }
@@ -362,11 +362,11 @@ __device__ inline void warp_colpiv_regs(const double* G, int ldg, int n, double*
     const double c0 = vb[k];
     const double tail = warp_sum(lane > k && lane < n ? xl * xl : 0.0);
     const bool zero = tail <= DBL_MIN;
-    double beta = fast_sqrt(fma(c0, c0, tail));
-    beta = c0 >= 0.0 ? -beta : beta;
+    double beta, rden, t;
+    fast_reflector(c0, zero ? 1.0 : tail, beta, rden, t);
     beta = zero ? c0 : beta;
-    const double rden = zero ? 0.0 : fast_rcp(c0 - beta);
-    const double t = zero ? 0.0 : (beta - c0) * fast_rcp(beta);
+    rden = zero ? 0.0 : rden;
+    t = zero ? 0.0 : t;
     const double vl = lane < k ? 0.0 : (lane == k ? 1.0 : (lane < n ? xl * rden : 0.0));
     if (own) {
       V[lane + k * ldv] = vl;
@@ -446,11 +446,11 @@ __device__ inline void warp_house_regs(double* X, int ldx, int n, int nc, double
     const double c0 = vb[k];
     const double tail = warp_sum(lane > k && lane < n ? xl * xl : 0.0);
     const bool zero = tail <= DBL_MIN;
-    double beta = fast_sqrt(fma(c0, c0, tail));
-    beta = c0 >= 0.0 ? -beta : beta;
+    double beta, rden, t;
+    fast_reflector(c0, zero ? 1.0 : tail, beta, rden, t);
     beta = zero ? c0 : beta;
-    const double rden = zero ? 0.0 : fast_rcp(c0 - beta);
-    const double t = zero ? 0.0 : (beta - c0) * fast_rcp(beta);
+    rden = zero ? 0.0 : rden;
+    t = zero ? 0.0 : t;
     const double vl = lane < k ? 0.0 : (lane == k ? 1.0 : (lane < n ? xl * rden : 0.0));
     if (lane < n) X[lane + k * ldx] = vl;
     if (lane <= k) W[k + lane * ldw] = lane < k ? xl : beta;  // R1(lane, k) = W(k, lane)
